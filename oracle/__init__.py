@@ -1,0 +1,259 @@
+"""fp64 CPU oracle for the MAPI / MAVP hot path (arXiv 2110.12065) — TEST INFRASTRUCTURE.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` /
+``--impl reference`` leg may import this package.  It shares no code with the CUDA library
+(``paper_2110_12065_b200``) and never imports it; the CUDA library never imports this.
+
+``oracle.c`` holds the arithmetic (plain loops, fp64, rows summed in index order,
+``-O2 -fno-fast-math -ffp-contract=off``); this module is ctypes marshalling only.
+``brute.py`` is the literal-definition brute force used to pin ``oracle.c``.
+
+Citation keys: ``P:n`` = PAPER.md line n; ``S:n`` = SPEC.md line n.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lock = threading.Lock()
+_lib = None
+
+MIN1, MIN2, DIAMOND, DOT = 0, 1, 2, 3
+NORM_L1, NORM_L2 = 1, 2
+OK, ERR_BAD_PARAM, ERR_DEGENERATE, ERR_NEGATIVE, ERR_NONFINITE = 0, 3, 4, 5, 6
+
+_OPS = {"min1": MIN1, "min2": MIN2, "diamond": DIAMOND, "dot": DOT}
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle.c -> liboracle.so with gcc (OpenMP over rows only)."""
+    if (not force and os.path.exists(_LIB)
+            and os.path.getmtime(_LIB) >= os.path.getmtime(_SRC)):
+        return _LIB
+    tmp = _LIB + f".tmp{os.getpid()}"
+    cmd = ["gcc", "-O2", "-fno-fast-math", "-ffp-contract=off", "-fopenmp", "-fPIC",
+           "-shared", "-std=c11", "-o", tmp, _SRC, "-lm"]
+    subprocess.run(cmd, check=True)
+    os.replace(tmp, _LIB)
+    return _LIB
+
+
+def _load():
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        build()
+        lib = ctypes.CDLL(_LIB)
+        P = ctypes.c_void_p
+        i64, i32, dbl, cint = ctypes.c_int64, ctypes.c_int32, ctypes.c_double, ctypes.c_int
+        lib.orc_mavp_dot.argtypes = [cint, P, P, i64]
+        lib.orc_mavp_dot.restype = dbl
+        lib.orc_matvec_f32.argtypes = [cint, P, i64, i64, i64, P, P, P]
+        lib.orc_matvec_f32.restype = None
+        lib.orc_matvec_f64.argtypes = [cint, P, i64, i64, i64, P, P, P]
+        lib.orc_matvec_f64.restype = None
+        lib.orc_power_iterate.argtypes = [cint, cint, P, cint, i64, i64, P, i32, dbl, P, P, P, P,
+                                          ctypes.POINTER(i32)]
+        lib.orc_power_iterate.restype = cint
+        lib.orc_deflate.argtypes = [P, i64, i64, P, i32, P]
+        lib.orc_deflate.restype = None
+        lib.orc_pca_topk.argtypes = [cint, P, i64, i64, i32, i32, P, P, P, P, P]
+        lib.orc_pca_topk.restype = cint
+        lib.orc_rank_csr.argtypes = [i64, i64, P, P, dbl, P, i32, dbl, P, P, P,
+                                     ctypes.POINTER(i32)]
+        lib.orc_rank_csr.restype = cint
+        lib.orc_num_threads.argtypes = []
+        lib.orc_num_threads.restype = cint
+        lib.orc_set_num_threads.argtypes = [cint]
+        lib.orc_set_num_threads.restype = None
+        _lib = lib
+        return lib
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+
+
+def _op(op) -> int:
+    return _OPS[op] if isinstance(op, str) else int(op)
+
+
+def num_threads() -> int:
+    return int(_load().orc_num_threads())
+
+
+def set_num_threads(n: int) -> None:
+    _load().orc_set_num_threads(int(n))
+
+
+def mavp_dot(w, x, op="min1") -> float:
+    """w^T (op) x — Eq.(3) min1, Eq.(4) min2, Eq.(9) diamond, dot."""
+    w, x = _f64(w), _f64(x)
+    if w.shape != x.shape or w.ndim != 1:
+        raise ValueError(f"dimension mismatch: {w.shape} vs {x.shape}")
+    return float(_load().orc_mavp_dot(_op(op), _ptr(w), _ptr(x), w.size))
+
+
+def _as_f32_matrix(A):
+    A = np.asarray(A)
+    if A.dtype != np.float32:
+        raise TypeError("oracle matrices are the fp32 input bytes (dtype float32)")
+    if A.ndim != 2 or A.strides[1] != 4:
+        raise ValueError("A must be a 2-D row-major float32 array")
+    lda = A.strides[0] // 4
+    return A, lda
+
+
+def matvec(A, x, op="min1", return_mag=False):
+    """y_j = row_j(A)^T (op) x  (matrix extension, reading Q6/Q7).
+
+    A is fp32 (the same bytes the GPU sees) or fp64; x is promoted to fp64.
+    Returns y (fp64) and, if requested, mag_j = sum_k |term_jk| (tolerance scale T1).
+    """
+    A = np.asarray(A)
+    x = _f64(x)
+    n_rows, n_cols = A.shape
+    if x.shape != (n_cols,):
+        raise ValueError(f"dimension mismatch: A has {n_cols} columns, x has {x.shape}")
+    y = np.empty(n_rows, np.float64)
+    mag = np.empty(n_rows, np.float64)
+    lib = _load()
+    if A.dtype == np.float64:
+        if A.strides[1] != 8:
+            A = np.ascontiguousarray(A)
+        lib.orc_matvec_f64(_op(op), _ptr(A), n_rows, n_cols, A.strides[0] // 8, _ptr(x),
+                           _ptr(y), _ptr(mag))
+    else:
+        A, lda = _as_f32_matrix(A)
+        lib.orc_matvec_f32(_op(op), _ptr(A), n_rows, n_cols, lda, _ptr(x), _ptr(y), _ptr(mag))
+    return (y, mag) if return_mag else y
+
+
+class IterResult:
+    """Result of a power iteration: w (l1- or l2-unit iterate), w_l2, norms, deltas, status."""
+
+    def __init__(self, status, w, w_l2, norms, deltas, iters_done):
+        self.status, self.w, self.w_l2 = status, w, w_l2
+        self.norms, self.deltas, self.iters_done = norms, deltas, iters_done
+
+    def __repr__(self):
+        return f"IterResult(status={self.status}, iters_done={self.iters_done})"
+
+
+def power_iterate(A, b0, iters, tol=0.0, op="min1", norm=None) -> IterResult:
+    """Algorithm 1 (MAPI) for min-type ops, Eq.(1) RPI for op='dot'.
+
+    norm defaults to l1 for MAVP ops (Eq. 8) and l2 for 'dot' (Eq. 1).
+    """
+    opc = _op(op)
+    if norm is None:
+        norm = NORM_L2 if opc == DOT else NORM_L1
+    A = np.asarray(A)
+    n = A.shape[0]
+    if A.ndim != 2 or A.shape[1] != n:
+        raise ValueError(f"A must be square, got {A.shape}")
+    if A.dtype == np.float64:
+        A = np.ascontiguousarray(A)
+        lda, is64 = n, 1
+    else:
+        A, lda = _as_f32_matrix(A)
+        is64 = 0
+    b0 = _f64(b0)
+    if b0.shape != (n,):
+        raise ValueError(f"dimension mismatch: A is {n}x{n}, b0 has {b0.shape}")
+    w = np.zeros(n)
+    wl2 = np.zeros(n)
+    norms = np.zeros(iters)
+    deltas = np.zeros(iters)
+    done = ctypes.c_int32(0)
+    st = _load().orc_power_iterate(opc, norm, _ptr(A), is64, n, lda, _ptr(b0), int(iters),
+                                   float(tol), _ptr(w), _ptr(wl2), _ptr(norms), _ptr(deltas),
+                                   ctypes.byref(done))
+    k = done.value
+    return IterResult(st, w, wl2, norms[:k], deltas[:k], k)
+
+
+def mapi(A, b0, iters, tol=0.0, op="min1") -> IterResult:
+    """MAPI, Eq.(8) / Algorithm 1: w <- (A (op) w) / ||A (op) w||_1."""
+    if _op(op) == DOT:
+        raise ValueError("mapi() takes a multiplication-avoiding operator; use rpi() for 'dot'")
+    return power_iterate(A, b0, iters, tol, op, NORM_L1)
+
+
+def rpi(A, b0, iters, tol=0.0) -> IterResult:
+    """Regular power iteration, Eq.(1): b <- Ab / ||Ab||_2."""
+    return power_iterate(A, b0, iters, tol, "dot", NORM_L2)
+
+
+def deflate(C, P, i) -> np.ndarray:
+    """D_i = (I - sum_{m<i} p_m p_m^T) C, fp64 result, C fp32."""
+    C, ldc = _as_f32_matrix(C)
+    n = C.shape[0]
+    P = _f64(P).reshape(-1, n)
+    D = np.empty((n, n), np.float64)
+    _load().orc_deflate(_ptr(C), n, ldc, _ptr(P), int(i), _ptr(D))
+    return D
+
+
+class PcaResult:
+    def __init__(self, status, P, norms, deltas, iters_done):
+        self.status, self.P, self.norms, self.deltas, self.iters_done = (
+            status, P, norms, deltas, iters_done)
+
+
+def pca_topk(C, k, iters, b0, op="min1") -> PcaResult:
+    """Top-k principal vectors by MAPI with L2 deflation (BJ configs[1])."""
+    C, ldc = _as_f32_matrix(C)
+    n = C.shape[0]
+    b0 = _f64(b0)
+    P = np.zeros((k, n))
+    norms = np.zeros((k, iters))
+    deltas = np.zeros((k, iters))
+    done = np.zeros(k, np.int32)
+    st = _load().orc_pca_topk(_op(op), _ptr(C), n, ldc, int(k), int(iters), _ptr(b0), _ptr(P),
+                              _ptr(norms), _ptr(deltas), _ptr(done))
+    return PcaResult(st, P, norms, deltas, done)
+
+
+def rank_csr(n, row_ptr, col_idx, alpha=0.85, b0=None, max_iters=200, tol=1e-7) -> IterResult:
+    """MAPI ranking on G = alpha M + (1-alpha)/n 1 (Eq. 13), CSR by destination."""
+    row_ptr = np.ascontiguousarray(np.asarray(row_ptr, dtype=np.int64))
+    col_idx = np.ascontiguousarray(np.asarray(col_idx, dtype=np.int32))
+    if row_ptr.shape != (n + 1,):
+        raise ValueError("row_ptr must have n+1 entries")
+    nnz = int(row_ptr[-1])
+    if b0 is None:
+        b0 = np.full(n, 1.0 / n)
+    b0 = _f64(b0)
+    w = np.zeros(n)
+    wl2 = np.zeros(n)
+    deltas = np.zeros(max_iters)
+    done = ctypes.c_int32(0)
+    st = _load().orc_rank_csr(n, nnz, _ptr(row_ptr), _ptr(col_idx), float(alpha), _ptr(b0),
+                              int(max_iters), float(tol), _ptr(w), _ptr(wl2), _ptr(deltas),
+                              ctypes.byref(done))
+    k = done.value
+    return IterResult(st, w, wl2, None, deltas[:k], k)
+
+
+def rank_order(scores) -> np.ndarray:
+    """Indices sorted by descending score, ties by ascending index."""
+    scores = np.asarray(scores)
+    return np.lexsort((np.arange(scores.size), -scores))
+
+
+def topk_overlap(a, b, k) -> int:
+    """|first k of a  ∩  first k of b| ("7 common top-10 ranks")."""
+    return len(set(list(a)[:k]) & set(list(b)[:k]))
