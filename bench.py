@@ -1,0 +1,406 @@
+#!/usr/bin/env python3
+"""bench.py — MAPI iterations/s and HBM GB/s on B200 (BASELINE.json metric), one JSON line.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl mapi|reference] [--workload cfg3]
+
+A step is one whole `mapi_iterate` call (100 MAPI iterations, Algorithm 1 / Eq. 8) on
+BASELINE configs[2] (dense symmetric 32768^2 fp32, 4 GiB).  `value` = MAPI iterations/s over all
+ranks with the matrix resident in HBM; `e2e` = the same through `mapi_iterate_host` with pinned
+HOST buffers (4 GiB H2D + 100 iterations + result D2H per step).  Under torchrun each rank runs
+an independent replica (weak scaling, no data-path collective).
+
+--impl reference times the fp64 CPU oracle (oracle/, test infrastructure) on the same workload,
+a bounded sample per step, on rank 0 only.
+Other workloads (cfg1, cfg2, cfg4, cfg5) are selectable with --workload for investigation.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    "cfg1": "dense MAPI single vector, C = XX^T/1024 of 256x1024 N(0,1) (seed 0), 50 iterations",
+    "cfg2": "PCA-image shaped: 4096^2 covariance of U[0,1]+5% +-10 outliers (seed 1), top-8 by MAPI "
+            "with L2 deflation, 100 iterations each",
+    "cfg3": "large dense HBM-bound: A = GG^T/32768 + diag(10|z|), G 32768x512 (seed 2), 4 GiB fp32, "
+            "100 MAPI iterations from b0 = 1/sqrt(n)",
+    "cfg4": "batched: 16384^2 A (G 16384x256, seed 3), k=64 N(0,1) starts, 100 iterations",
+    "cfg5": "graph ranking: R-MAT 2^22 nodes / 2^26 edges (seed 4), MAPI on G = 0.85 M + 0.15/n, "
+            "200 fixed iterations (tol 0) for steady state",
+}
+METRIC = "MAPI iterations/s and achieved HBM GB/s (% of B200 peak) at n=32768 fp32"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="mapi", choices=["mapi", "reference"])
+    p.add_argument("--workload", default="cfg3", choices=sorted(WORKLOADS))
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=15.0, help="budget of the oracle sample")
+    return p.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for name, val in zip(names, f[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------- workloads
+
+
+def setup_dense(workload, device):
+    import torch
+    import synth
+
+    cfg = synth.cfg3(device=device) if workload == "cfg3" else synth.cfg1()
+    A = cfg["A"] if isinstance(cfg["A"], torch.Tensor) else torch.from_numpy(cfg["A"]).to(device)
+    b0 = torch.from_numpy(cfg["b0"]).to(device)
+    return cfg, A, b0
+
+
+def dense_bytes_per_iter(n, lda):
+    # algorithmic: A once (4 n^2), w_t read once, y written once
+    return 4.0 * n * lda + 8.0 * n
+
+
+def run_mapi(args, rank, world, local_rank):
+    import torch
+
+    import paper_2110_12065_b200 as m
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    m.load()
+    dist = world > 1
+    if dist:
+        import torch.distributed as tdist
+    stream = torch.cuda.current_stream()
+    peak, peak_kind = peaks()
+
+    out = {"metric": METRIC, "unit": "iterations/s", "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "dtype": "f32", "data": "synthetic (seeded recipes, DESIGN.md §Inputs)", "impl": "mapi-b200"}
+
+    if args.workload in ("cfg1", "cfg3"):
+        cfg, A, b0 = setup_dense(args.workload, dev)
+        n, lda = A.shape[0], A.stride(0)
+        iters = cfg["iters"]
+        ws, need = m._workspace(m.WS_ITERATE, n, device=dev)
+        w = torch.empty(n, device=dev)
+        wl2 = torch.empty(n, device=dev)
+        norms = torch.empty(iters, device=dev)
+        deltas = torch.empty(iters, device=dev)
+        lib = m.load()
+        import ctypes
+
+        done = ctypes.c_int32(0)
+
+        def step():
+            st = lib.mapi_iterate(0, A.data_ptr(), n, lda, b0.data_ptr(), iters, 0.0, w.data_ptr(),
+                                  wl2.data_ptr(), norms.data_ptr(), deltas.data_ptr(), ctypes.byref(done),
+                                  ws.data_ptr(), need, stream.cuda_stream)
+            if st != 0:
+                raise RuntimeError(lib.mapi_last_error_message().decode())
+            return iters
+
+        bytes_per_launch = dense_bytes_per_iter(n, lda) * iters
+        units_per_step = iters
+        kernel_name = "k_iterate_persistent (K2, 1 cooperative launch = 100 iterations)"
+        cfg_out = {"workload": f"{args.workload}: {WORKLOADS[args.workload]}", "n": n, "lda": lda,
+                   "iters_per_step": iters, "op": "min1",
+                   "l2_flush": ("inputs larger than L2 (4 GiB matrix vs 126 MB L2)" if args.workload == "cfg3"
+                                else "none: latency-bound 256 KiB matrix is meant to stay on chip"),
+                   "parallelism": f"replicas x{world} (independent problems)" if dist else "single GPU"}
+    else:
+        raise SystemExit(f"--workload {args.workload}: use bench_extra.py for non-headline workloads")
+
+    # warm-up
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # timed region
+    sampler = ClockSampler(local_rank)
+    m.set_profiling(True)
+    kernel_ms = []
+    if dist:
+        tdist.barrier()
+    torch.cuda.synchronize()
+    launches0 = m.launch_count()
+    sampler.start()
+    time.sleep(0.3)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    t_wall = time.perf_counter()
+    units = 0
+    for _ in range(args.steps):
+        units += step()
+        kernel_ms.append(m.last_kernel_ms())
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    t_wall = time.perf_counter() - t_wall
+    launches = m.launch_count() - launches0
+    clocks = sampler.stop()
+    m.set_profiling(False)
+    elapsed_ms = ev0.elapsed_time(ev1)
+    if dist:
+        t = torch.tensor([elapsed_ms], device=dev, dtype=torch.float64)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        elapsed_ms = float(t.item())
+        tdist.barrier()
+    total_units = units * world
+    value = total_units / (elapsed_ms / 1e3)
+    kavg = float(np.mean(kernel_ms))
+    achieved = bytes_per_launch / (kavg / 1e3) / 1e9
+    out.update({"value": value, "ms_per_step": elapsed_ms / args.steps, "config": cfg_out,
+                "gpu_launches": int(launches), "wall_s_timed": t_wall})
+    out["hbm_gbs"] = dense_bytes_per_iter(n, lda) * units / (elapsed_ms / 1e3) / 1e9
+    out["hbm_frac_of_measured"] = out["hbm_gbs"] / peak
+    out["hbm_frac_of_nominal_8000"] = out["hbm_gbs"] / 8000.0
+    traffic = traffic_from_profiles(args.workload)
+    out["roofline"] = {"bound": "hbm", "kernel": kernel_name, "achieved": achieved, "peak": peak,
+                       "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs, copy read+write)",
+                       "unit": "GB/s", "frac": achieved / peak,
+                       "algorithmic_bytes_per_launch": bytes_per_launch,
+                       "kernel_ms_avg": kavg, "kernel_share_of_step": kavg / (elapsed_ms / args.steps),
+                       "traffic": traffic}
+    out["clocks"] = clocks
+
+    # e2e through host buffers
+    if not args.no_e2e and args.workload in ("cfg1", "cfg3"):
+        out["e2e"] = e2e_dense(args, m, A, b0, iters, dev, stream, world, dist)
+    # cpu baseline: oracle on a bounded sample (rank 0, N = 1 only)
+    if not args.no_cpu_baseline and world == 1 and rank == 0:
+        out["cpu_baseline"] = cpu_baseline_dense(args, A, b0, iters)
+    return out
+
+
+def e2e_dense(args, m, A, b0, iters, dev, stream, world, dist):
+    import ctypes
+
+    import torch
+
+    n, lda = A.shape[0], A.stride(0)
+    A_h = torch.empty((n, lda), dtype=torch.float32, pin_memory=True)
+    A_h.copy_(A.as_strided((n, lda), (lda, 1)) if lda == n else A)
+    b0_h = b0.cpu().pin_memory()
+    w_h = torch.empty(n, dtype=torch.float32, pin_memory=True)
+    nrm_h = torch.empty(iters, dtype=torch.float32, pin_memory=True)
+    dlt_h = torch.empty(iters, dtype=torch.float32, pin_memory=True)
+    ws, need = m._workspace(m.WS_ITERATE_HOST, n, lda, iters, device=dev)
+    lib = m.load()
+    done = ctypes.c_int32(0)
+
+    def step():
+        st = lib.mapi_iterate_host(0, A_h.data_ptr(), n, lda, b0_h.data_ptr(), iters, 0.0, w_h.data_ptr(), None,
+                                   nrm_h.data_ptr(), dlt_h.data_ptr(), ctypes.byref(done), ws.data_ptr(), need,
+                                   stream.cuda_stream)
+        if st != 0:
+            raise RuntimeError(lib.mapi_last_error_message().decode())
+
+    for _ in range(max(1, min(args.warmup, 2))):
+        step()
+    steps = max(2, min(args.steps, 5))
+    torch.cuda.synchronize()
+    if dist:
+        import torch.distributed as tdist
+
+        tdist.barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(steps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    if dist:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        ms = float(t.item())
+    del ws, A_h
+    return {"value": world * iters * steps / (ms / 1e3), "unit": "iterations/s",
+            "h2d_bytes_per_step": 4 * n * lda + 4 * n, "d2h_bytes_per_step": 4 * n + 8 * iters + 8,
+            "steps": steps, "ms_per_step": ms / steps,
+            "path": "mapi_iterate_host: pinned host A,b0 -> device, 100 iterations, w + trace -> host"}
+
+
+def cpu_baseline_dense(args, A, b0, iters):
+    import oracle
+
+    A_h = A.cpu().numpy()
+    b0_h = b0.cpu().numpy().astype(np.float64)
+    oracle.build()
+    t0 = time.perf_counter()
+    oracle.mapi(A_h, b0_h, 1)
+    one = time.perf_counter() - t0
+    k = int(max(1, min(iters, args.cpu_seconds // max(one, 1e-3))))
+    t0 = time.perf_counter()
+    r = oracle.mapi(A_h, b0_h, k)
+    dt = time.perf_counter() - t0
+    return {"value": r.iters_done / dt, "unit": "iterations/s", "cores": oracle.num_threads(),
+            "kind": "oracle",
+            "sample": f"{r.iters_done} of the {iters} MAPI iterations of the full {A_h.shape[0]}^2 matrix "
+                      f"(fp64 oracle, OpenMP over rows, {dt:.1f} s)"}
+
+
+def traffic_from_profiles(workload):
+    """dram bytes per launch of the dominant kernel, from the committed ncu --set full summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(path):
+        return None
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        e = d.get(workload)
+        return None if e is None else e.get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------------------------- reference arm
+
+
+def run_reference(args, rank, world):
+    import oracle
+    import synth
+
+    if rank != 0:
+        return None
+    oracle.build()
+    if args.workload == "cfg3":
+        dev = None
+        try:
+            import torch
+
+            if torch.cuda.is_available():
+                dev = "cuda"  # setup product only (cuBLAS DGEMM), never the product library
+        except Exception:
+            dev = None
+        cfg = synth.cfg3(device=dev)
+        A = cfg["A"].cpu().numpy() if dev else cfg["A"]
+    else:
+        cfg = synth.cfg1()
+        A = cfg["A"]
+    b0 = cfg["b0"].astype(np.float64)
+    iters_per_step = 1 if args.workload == "cfg3" else cfg["iters"]
+    for _ in range(args.warmup):
+        oracle.mapi(A, b0, iters_per_step)
+    t0 = time.perf_counter()
+    units = 0
+    for _ in range(args.steps):
+        units += oracle.mapi(A, b0, iters_per_step).iters_done
+    dt = time.perf_counter() - t0
+    v = units / dt
+    return {"metric": METRIC, "value": v, "unit": "iterations/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": f"{args.workload}: {WORKLOADS[args.workload]}",
+                       "n": int(A.shape[0]), "iters_per_step": iters_per_step},
+            "cpu_baseline": {"value": v, "unit": "iterations/s", "cores": oracle.num_threads(), "kind": "oracle",
+                             "sample": f"{iters_per_step} iteration(s) of the full workload per step"},
+            "e2e": {"value": v, "unit": "iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        out = run_reference(args, rank, world)
+        if out is not None:
+            print(json.dumps(out), flush=True)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as tdist
+
+        torch.cuda.set_device(local_rank)
+        tdist.init_process_group("nccl")
+    out = run_mapi(args, rank, world, local_rank)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as tdist
+
+        tdist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,160 @@
+/*
+ * mapi.h — C ABI of libmapi.so, the B200 (sm_100a) hot path of multiplication-avoiding power
+ * iteration (MAPI, arXiv 2110.12065).
+ *
+ * Citation keys: P:n = PAPER.md line n (the paper's LaTeX source), S:n = SPEC.md line n,
+ * Qn = reading n of the paper listed in DESIGN.md §Readings.
+ *
+ * CONVENTIONS (all entry points)
+ *  - Pointers are DEVICE pointers owned by the caller unless the parameter is marked (host).
+ *    The library never allocates, frees or retains caller memory; scratch comes from a
+ *    caller-provided device workspace `ws` of at least mapi_workspace_size(...) bytes
+ *    (any alignment >= 256 B; torch/cudaMalloc allocations qualify).  mapi_iterate_host is
+ *    the one exception that takes host buffers (it copies through the workspace).
+ *  - Matrices are fp32 row-major with leading dimension (row stride, in elements) >= #cols.
+ *    Vectors are fp32, contiguous.  Sizes are int64_t; graph indices are int32_t.
+ *  - `stream` is a cudaStream_t (CUstream) passed as void*; NULL = the legacy default stream.
+ *    Work is stream-ordered.  mapi_mavp_matvec and mapi_csr_prepare are asynchronous; every
+ *    call that returns an iteration count or a device-detected status (iterate, batched,
+ *    pca, rank) synchronises `stream` before returning.
+ *  - Errors: a non-MAPI_OK status; mapi_last_error_message() (thread-local) explains it,
+ *    e.g. "lda (100) < n_cols (128)".  Argument validation happens before any launch, so a
+ *    validation error leaves all outputs untouched.  MAPI_ERR_CUDA wraps a CUDA runtime
+ *    error (message = cudaGetErrorString).
+ *  - Operator `op`: MAPI_OP_MIN1 = Eq.(3), MAPI_OP_MIN2 = Eq.(4).
+ *  - Arithmetic: fp32, IEEE round-to-nearest adds, div.rn for the l1 normalisation (P:146
+ *    "N divisions"), no FTZ, no fast-math; the MAVP loops contain no multiplication (P:5).
+ *  - Determinism: every reduction has a fixed order for a given device and shape, so repeated
+ *    calls are bitwise identical.
+ */
+#ifndef MAPI_H
+#define MAPI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void *mapi_stream_t;
+
+typedef enum {
+    MAPI_OK = 0,
+    MAPI_ERR_NULL = 1,       /* a required pointer is NULL */
+    MAPI_ERR_SHAPE = 2,      /* inconsistent sizes; the message carries both values */
+    MAPI_ERR_BAD_PARAM = 3,  /* iters < 1, tol < 0, alpha not in (0,1), k < 1 or k > n, bad op */
+    MAPI_ERR_DEGENERATE = 4, /* ||A (+) w_t||_1 == 0 at iteration *iters_done */
+    MAPI_ERR_NEGATIVE = 5,   /* ranking: b0 has a negative entry */
+    MAPI_ERR_NONFINITE = 6,  /* the l1 norm became Inf/NaN (non-finite input) */
+    MAPI_ERR_WORKSPACE = 7,  /* ws is NULL or ws_bytes < mapi_workspace_size(...) */
+    MAPI_ERR_CUDA = 8        /* CUDA runtime error, or no sm_100 device */
+} mapi_status;
+
+typedef enum { MAPI_OP_MIN1 = 0, MAPI_OP_MIN2 = 1 } mapi_op;
+
+/* Workspace query ids (first argument of mapi_workspace_size). */
+typedef enum {
+    MAPI_WS_MATVEC = 0,
+    MAPI_WS_ITERATE = 1,
+    MAPI_WS_ITERATE_BATCHED = 2,
+    MAPI_WS_PCA_TOPK = 3,
+    MAPI_WS_CSR_PREPARE = 4,
+    MAPI_WS_RANK_CSR = 5,
+    MAPI_WS_ITERATE_HOST = 6
+} mapi_ws_op;
+
+/* y = A (op) x — the matrix extension of the MAVP (reading Q6: y_j uses ROW j):
+ *     y_j = sum_k sign(A[j*lda+k] * x_k) * min(|A[j*lda+k]|, |x_k|)      (op = MIN1, Eq. 3)
+ * A: n_rows x n_cols (lda >= n_cols), x: n_cols, y: n_rows (must not alias A or x).
+ * n_rows == 0 or n_cols == 0 is allowed (y = 0 for n_cols == 0).  Asynchronous. */
+mapi_status mapi_mavp_matvec(int32_t op, const float *A, int64_t n_rows, int64_t n_cols,
+                             int64_t lda, const float *x, float *y, mapi_stream_t stream);
+
+/* MAPI, Eq.(8) / Algorithm 1:
+ *     w_0 = b0 (used as given; Q2)
+ *     for t = 0..iters-1:  y = A (op) w_t;  s_t = ||y||_1;  w_{t+1} = y / s_t;
+ *                          delta_t = ||w_{t+1} - w_t||_1;  stop early iff tol > 0 && delta_t < tol (Q9)
+ *     optional final l2 copy w / ||w||_2 (Alg.1 line 6).
+ * A: n x n (lda >= n). b0: n. Outputs: w_out (n, l1-unit final iterate), w_l2_out (n, or NULL),
+ * norms[t] = s_t and deltas[t] = delta_t for t < *iters_done (arrays of `iters`, or NULL),
+ * *iters_done (host, may be NULL).  On MAPI_ERR_DEGENERATE / NONFINITE, w_out = the last good
+ * iterate and *iters_done = the iteration that failed.  Synchronises `stream`. */
+mapi_status mapi_iterate(int32_t op, const float *A, int64_t n, int64_t lda, const float *b0,
+                         int32_t iters, float tol, float *w_out, float *w_l2_out, float *norms,
+                         float *deltas, int32_t *iters_done, void *ws, size_t ws_bytes,
+                         mapi_stream_t stream);
+
+/* mapi_iterate with HOST buffers (end-to-end path): A_host (n x lda), b0_host, w_out_host,
+ * w_l2_out_host / norms_host / deltas_host (nullable), iters_done (host).  The call copies A and
+ * b0 host->device into the device workspace `ws` (mapi_workspace_size(MAPI_WS_ITERATE_HOST,
+ * n, lda, 0) bytes), runs mapi_iterate on the copies, and copies the results device->host, all
+ * on `stream`.  Pinned host memory gives full PCIe bandwidth.  Synchronises `stream`. */
+mapi_status mapi_iterate_host(int32_t op, const float *A_host, int64_t n, int64_t lda,
+                              const float *b0_host, int32_t iters, float tol, float *w_out_host,
+                              float *w_l2_out_host, float *norms_host, float *deltas_host,
+                              int32_t *iters_done, void *ws, size_t ws_bytes, mapi_stream_t stream);
+
+/* Batched MAPI: k independent runs of mapi_iterate on the same A ("multiple independent
+ * runs"; matrix extension P:69-70 with p = k columns), Y = A (op) W each iteration.
+ * B0, W_out: k x n, vector-major (vector v at B0 + v*n).  norms, deltas: iters x k
+ * (entry [t*k + v]), nullable.  iters_done (host, k entries, nullable): per-vector count; a
+ * vector stops individually when its own delta < tol (tol > 0).  The call returns the worst
+ * status over vectors.  Synchronises `stream`. */
+mapi_status mapi_iterate_batched(int32_t op, const float *A, int64_t n, int64_t lda,
+                                 const float *B0, int32_t k, int32_t iters, float tol, float *W_out,
+                                 float *norms, float *deltas, int32_t *iters_done, void *ws,
+                                 size_t ws_bytes, mapi_stream_t stream);
+
+/* Top-k principal vectors by MAPI with L2 deflation (BASELINE configs[1]):
+ *     for i = 0..k-1:  D_i = (I - sum_{m<i} p_m p_m^T) C ;  w = MAPI(D_i, b0, iters, tol = 0) ;
+ *                      p_i = w / ||w||_2
+ * D_i is formed as C - sum_m p_m r_m^T with r_m = p_m^T C, accumulated in fp64 and rounded
+ * once to fp32 (K5).  C: n x n (ldc >= n).  b0: n.  P_out: k x n (l2-unit rows).
+ * norms, deltas: k x iters (row i = vector i), nullable.  Synchronises `stream`. */
+mapi_status mapi_pca_topk(int32_t op, const float *C, int64_t n, int64_t ldc, int32_t k,
+                          int32_t iters, const float *b0, float *P_out, float *norms, float *deltas,
+                          void *ws, size_t ws_bytes, mapi_stream_t stream);
+
+/* Google-matrix preparation for MAPI ranking (Eq. 13; reading Q10):
+ * the graph is CSR by DESTINATION (row i lists the sources j of the distinct edges j -> i);
+ * row_ptr: n+1 int32 (nnz < 2^31), col_idx: nnz int32 in [0, n).
+ * Outputs per column j:  cap_out[j] = alpha / outdeg(j) (0 if dangling),
+ *                        bg_out[j]  = (1 - alpha)/n, or 1/n if j is dangling (outdeg 0).
+ * outdeg is counted from col_idx on the device.  Asynchronous. */
+mapi_status mapi_csr_prepare(int64_t n, int64_t nnz, const int32_t *row_ptr, const int32_t *col_idx,
+                             float alpha, float *cap_out, float *bg_out, void *ws, size_t ws_bytes,
+                             mapi_stream_t stream);
+
+/* MAPI ranking: w <- (G (min1) w) / ||G (min1) w||_1 with G = alpha M + (1-alpha)/n 1 never
+ * materialised.  For w >= 0 the min1 row product equals exactly (K3)
+ *     y_i = S + sum_{e in row i} min(max(w_j - bg_j, 0), cap_j),  j = col_idx[e],
+ *     S   = sum_j min(bg_j, w_j).
+ * cap, bg: from mapi_csr_prepare.  b0: n, >= 0 (else MAPI_ERR_NEGATIVE).  Stops when
+ * tol > 0 && delta_t < tol or after max_iters.  w_out: n (l1-unit), w_l2_out (n or NULL,
+ * final l2 copy P:322), deltas (max_iters, nullable), *iters_done (host).  Synchronises. */
+mapi_status mapi_rank_csr(int64_t n, int64_t nnz, const int32_t *row_ptr, const int32_t *col_idx,
+                          const float *cap, const float *bg, const float *b0, int32_t max_iters,
+                          float tol, float *w_out, float *w_l2_out, float *deltas,
+                          int32_t *iters_done, void *ws, size_t ws_bytes, mapi_stream_t stream);
+
+/* Bytes of device workspace the call `op` needs for the given sizes (0 if none).
+ *   MAPI_WS_MATVEC: 0.  MAPI_WS_ITERATE: n.  MAPI_WS_ITERATE_BATCHED: n, k.
+ *   MAPI_WS_PCA_TOPK: n, k.  MAPI_WS_CSR_PREPARE / MAPI_WS_RANK_CSR: n, nnz.
+ *   MAPI_WS_ITERATE_HOST: n, and nnz = lda (the device copy of A is n*lda floats). */
+size_t mapi_workspace_size(int32_t op, int64_t n, int64_t nnz, int32_t k);
+
+const char *mapi_status_string(mapi_status status);
+const char *mapi_last_error_message(void);
+
+/* Instrumentation (bench.py): number of kernels this library has launched in the process, and
+ * the device time (CUDA events on the launching stream) of the most recent launch of the
+ * dominant kernel of the last iterate / batched / pca / rank call when profiling is on. */
+uint64_t mapi_launch_count(void);
+void mapi_set_profiling(int32_t enable);
+float mapi_last_kernel_ms(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MAPI_H */

@@ -1,0 +1,313 @@
+"""paper_2110_12065_b200 — B200 (sm_100a) MAPI / MAVP hot path, Python binding of libmapi.so.
+
+Thin ctypes marshalling over the C ABI declared in ``include/mapi.h`` (same names):
+torch tensors supply device pointers and streams; workspaces are torch allocations.
+Every step of the hot path runs in the library's CUDA kernels.  There is no CPU fallback:
+if ``libmapi.so`` is missing or no sm_100 GPU is present, calls raise.
+
+Citation keys: ``P:n`` = PAPER.md line n (arXiv 2110.12065 LaTeX source).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from dataclasses import dataclass
+from typing import Optional
+
+from ._build import LIB as _LIB_PATH
+from ._build import build  # noqa: F401  (re-exported: compile in-tree)
+
+__all__ = ["load", "build", "MapiError", "mavp_matvec", "iterate", "iterate_host", "iterate_batched",
+           "pca_topk", "csr_prepare", "rank_csr", "workspace_size", "launch_count", "set_profiling",
+           "last_kernel_ms", "MIN1", "MIN2"]
+
+MIN1, MIN2 = 0, 1
+WS_MATVEC, WS_ITERATE, WS_ITERATE_BATCHED, WS_PCA_TOPK, WS_CSR_PREPARE, WS_RANK_CSR, WS_ITERATE_HOST = range(7)
+STATUS = {0: "MAPI_OK", 1: "MAPI_ERR_NULL", 2: "MAPI_ERR_SHAPE", 3: "MAPI_ERR_BAD_PARAM",
+          4: "MAPI_ERR_DEGENERATE", 5: "MAPI_ERR_NEGATIVE", 6: "MAPI_ERR_NONFINITE",
+          7: "MAPI_ERR_WORKSPACE", 8: "MAPI_ERR_CUDA"}
+
+_lock = threading.Lock()
+_lib = None
+
+
+class MapiError(RuntimeError):
+    def __init__(self, status: int, message: str, iters_done: Optional[int] = None):
+        self.status = status
+        self.name = STATUS.get(status, str(status))
+        self.iters_done = iters_done
+        super().__init__(f"{self.name}: {message}")
+
+
+def load():
+    """Load libmapi.so (built in-tree by build()); raises if it is missing."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(_LIB_PATH):
+            raise ImportError(f"{_LIB_PATH} not found: run paper_2110_12065_b200.build() "
+                              "(nvcc, sm_100a) first — there is no CPU fallback")
+        lib = ctypes.CDLL(_LIB_PATH)
+        P, i64, i32, f32, sz = (ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_float,
+                                ctypes.c_size_t)
+        st = ctypes.c_int
+        sig = {
+            "mapi_mavp_matvec": (st, [i32, P, i64, i64, i64, P, P, P]),
+            "mapi_iterate": (st, [i32, P, i64, i64, P, i32, f32, P, P, P, P, P, P, sz, P]),
+            "mapi_iterate_host": (st, [i32, P, i64, i64, P, i32, f32, P, P, P, P, P, P, sz, P]),
+            "mapi_iterate_batched": (st, [i32, P, i64, i64, P, i32, i32, f32, P, P, P, P, P, sz, P]),
+            "mapi_pca_topk": (st, [i32, P, i64, i64, i32, i32, P, P, P, P, P, sz, P]),
+            "mapi_csr_prepare": (st, [i64, i64, P, P, f32, P, P, P, sz, P]),
+            "mapi_rank_csr": (st, [i64, i64, P, P, P, P, P, i32, f32, P, P, P, P, P, sz, P]),
+            "mapi_workspace_size": (sz, [i32, i64, i64, i32]),
+            "mapi_status_string": (ctypes.c_char_p, [st]),
+            "mapi_last_error_message": (ctypes.c_char_p, []),
+            "mapi_launch_count": (ctypes.c_uint64, []),
+            "mapi_set_profiling": (None, [i32]),
+            "mapi_last_kernel_ms": (f32, []),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
+
+
+# ---------------------------------------------------------------------------------------- helpers
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def _ptr(t) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+def _stream(stream=None) -> Optional[int]:
+    torch = _torch()
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream
+
+
+def _check(st: int, iters_done: Optional[int] = None):
+    if st != 0:
+        msg = load().mapi_last_error_message().decode(errors="replace")
+        raise MapiError(st, msg, iters_done)
+
+
+def _need(t, name, dtype, shape=None, device=True):
+    torch = _torch()
+    if t is None:
+        raise ValueError(f"{name} is required")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if device and not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} has shape {tuple(t.shape)}, expected {tuple(shape)}")
+    del torch
+
+
+def _matrix(A, name="A"):
+    torch = _torch()
+    _need(A, name, torch.float32)
+    if A.dim() != 2 or A.stride(1) != 1:
+        raise ValueError(f"{name} must be a 2-D row-major (stride(1) == 1) fp32 CUDA tensor")
+    return A.shape[0], A.shape[1], A.stride(0)
+
+
+def workspace_size(op: int, n: int, nnz: int = 0, k: int = 0) -> int:
+    return int(load().mapi_workspace_size(op, n, nnz, k))
+
+
+def _workspace(op, n, nnz=0, k=0, device=None, ws=None):
+    torch = _torch()
+    need = workspace_size(op, n, nnz, k)
+    if ws is not None:
+        if ws.numel() * ws.element_size() < need:
+            raise ValueError(f"workspace too small: {ws.numel() * ws.element_size()} < {need}")
+        return ws, need
+    return torch.empty(max(need, 256), dtype=torch.uint8, device=device), need
+
+
+def launch_count() -> int:
+    return int(load().mapi_launch_count())
+
+
+def set_profiling(on: bool) -> None:
+    load().mapi_set_profiling(1 if on else 0)
+
+
+def last_kernel_ms() -> float:
+    return float(load().mapi_last_kernel_ms())
+
+
+# ---------------------------------------------------------------------------------------- API
+
+
+def mavp_matvec(A, x, y=None, op: int = MIN1, stream=None):
+    """y = A (op) x  (matrix extension of Eq. 3/4); asynchronous on `stream`."""
+    torch = _torch()
+    n_rows, n_cols, lda = _matrix(A)
+    _need(x, "x", torch.float32, (n_cols,))
+    if y is None:
+        y = torch.empty(n_rows, dtype=torch.float32, device=A.device)
+    _need(y, "y", torch.float32, (n_rows,))
+    _check(load().mapi_mavp_matvec(op, _ptr(A), n_rows, n_cols, lda, _ptr(x), _ptr(y), _stream(stream)))
+    return y
+
+
+@dataclass
+class IterResult:
+    w: object            # l1-unit final iterate (torch / numpy)
+    w_l2: object         # l2 copy or None
+    norms: object        # s_t = ||A (+) w_t||_1, t < iters_done
+    deltas: object       # ||w_{t+1} - w_t||_1
+    iters_done: int
+
+
+def iterate(A, b0, iters: int, tol: float = 0.0, op: int = MIN1, want_l2: bool = True,
+            want_trace: bool = True, ws=None, out=None, stream=None) -> IterResult:
+    """MAPI, Eq.(8) / Algorithm 1 on device tensors; synchronises the stream."""
+    torch = _torch()
+    n, n2, lda = _matrix(A)
+    if n != n2:
+        raise ValueError(f"A must be square, got {tuple(A.shape)}")
+    _need(b0, "b0", torch.float32, (n,))
+    dev = A.device
+    w = out if out is not None else torch.empty(n, dtype=torch.float32, device=dev)
+    wl2 = torch.empty(n, dtype=torch.float32, device=dev) if want_l2 else None
+    norms = torch.zeros(iters, dtype=torch.float32, device=dev) if want_trace else None
+    deltas = torch.zeros(iters, dtype=torch.float32, device=dev) if want_trace else None
+    ws, need = _workspace(WS_ITERATE, n, device=dev, ws=ws)
+    done = ctypes.c_int32(0)
+    st = load().mapi_iterate(op, _ptr(A), n, lda, _ptr(b0), int(iters), float(tol), _ptr(w), _ptr(wl2),
+                             _ptr(norms), _ptr(deltas), ctypes.byref(done), _ptr(ws), need,
+                             _stream(stream))
+    _check(st, done.value)
+    k = done.value
+    return IterResult(w, wl2, None if norms is None else norms[:k], None if deltas is None else deltas[:k], k)
+
+
+def iterate_host(A_host, b0_host, iters: int, tol: float = 0.0, op: int = MIN1, ws=None,
+                 out=None, norms=None, deltas=None, stream=None) -> IterResult:
+    """MAPI end-to-end from HOST buffers (torch CPU tensors, ideally pinned): the call copies A, b0
+    to the device workspace, iterates, and copies w / trace back.  Synchronises the stream."""
+    torch = _torch()
+    if A_host.is_cuda or b0_host.is_cuda:
+        raise ValueError("iterate_host takes host (CPU) tensors")
+    if A_host.dtype != torch.float32 or A_host.dim() != 2 or A_host.stride(1) != 1:
+        raise ValueError("A_host must be a 2-D row-major fp32 CPU tensor")
+    n, lda = A_host.shape[0], A_host.stride(0)
+    w = out if out is not None else torch.empty(n, dtype=torch.float32)
+    norms = norms if norms is not None else torch.zeros(iters, dtype=torch.float32)
+    deltas = deltas if deltas is not None else torch.zeros(iters, dtype=torch.float32)
+    ws, need = _workspace(WS_ITERATE_HOST, n, lda, iters, device=torch.device("cuda"), ws=ws)
+    done = ctypes.c_int32(0)
+    st = load().mapi_iterate_host(op, _ptr(A_host), n, lda, _ptr(b0_host), int(iters), float(tol), _ptr(w),
+                                  None, _ptr(norms), _ptr(deltas), ctypes.byref(done), _ptr(ws), need,
+                                  _stream(stream))
+    _check(st, done.value)
+    k = done.value
+    return IterResult(w, None, norms[:k], deltas[:k], k)
+
+
+@dataclass
+class BatchedResult:
+    W: object            # k x n, l1-unit rows
+    norms: object        # iters x k
+    deltas: object       # iters x k
+    iters_done: list
+
+
+def iterate_batched(A, B0, iters: int, tol: float = 0.0, op: int = MIN1, ws=None,
+                    stream=None) -> BatchedResult:
+    """k independent MAPI runs on one A (matrix extension P:69-70); synchronises the stream."""
+    torch = _torch()
+    n, n2, lda = _matrix(A)
+    if n != n2:
+        raise ValueError(f"A must be square, got {tuple(A.shape)}")
+    _need(B0, "B0", torch.float32)
+    if B0.dim() != 2 or B0.shape[1] != n or not B0.is_contiguous():
+        raise ValueError(f"B0 must be a contiguous (k, {n}) tensor")
+    k = B0.shape[0]
+    dev = A.device
+    W = torch.empty_like(B0)
+    norms = torch.zeros(iters, k, dtype=torch.float32, device=dev)
+    deltas = torch.zeros(iters, k, dtype=torch.float32, device=dev)
+    ws, need = _workspace(WS_ITERATE_BATCHED, n, 0, k, device=dev, ws=ws)
+    done = (ctypes.c_int32 * k)()
+    st = load().mapi_iterate_batched(op, _ptr(A), n, lda, _ptr(B0), k, int(iters), float(tol), _ptr(W),
+                                     _ptr(norms), _ptr(deltas), done, _ptr(ws), need, _stream(stream))
+    _check(st)
+    return BatchedResult(W, norms, deltas, list(done))
+
+
+@dataclass
+class PcaResult:
+    P: object            # k x n, l2-unit rows
+    norms: object        # k x iters
+    deltas: object       # k x iters
+
+
+def pca_topk(C, k: int, iters: int, b0, op: int = MIN1, ws=None, stream=None) -> PcaResult:
+    """Top-k principal vectors by MAPI with L2 deflation; synchronises the stream."""
+    torch = _torch()
+    n, n2, ldc = _matrix(C, "C")
+    if n != n2:
+        raise ValueError(f"C must be square, got {tuple(C.shape)}")
+    _need(b0, "b0", torch.float32, (n,))
+    dev = C.device
+    P = torch.empty(k, n, dtype=torch.float32, device=dev)
+    norms = torch.zeros(k, iters, dtype=torch.float32, device=dev)
+    deltas = torch.zeros(k, iters, dtype=torch.float32, device=dev)
+    ws, need = _workspace(WS_PCA_TOPK, n, 0, k, device=dev, ws=ws)
+    st = load().mapi_pca_topk(op, _ptr(C), n, ldc, int(k), int(iters), _ptr(b0), _ptr(P), _ptr(norms),
+                              _ptr(deltas), _ptr(ws), need, _stream(stream))
+    _check(st)
+    return PcaResult(P, norms, deltas)
+
+
+def csr_prepare(n: int, row_ptr, col_idx, alpha: float = 0.85, ws=None, stream=None):
+    """Per-column cap_j = alpha/outdeg(j) and bg_j of the Google matrix (Eq. 13)."""
+    torch = _torch()
+    _need(row_ptr, "row_ptr", torch.int32, (n + 1,))
+    _need(col_idx, "col_idx", torch.int32)
+    nnz = col_idx.numel()
+    dev = row_ptr.device
+    cap = torch.empty(n, dtype=torch.float32, device=dev)
+    bg = torch.empty(n, dtype=torch.float32, device=dev)
+    ws, need = _workspace(WS_CSR_PREPARE, n, nnz, device=dev, ws=ws)
+    _check(load().mapi_csr_prepare(n, nnz, _ptr(row_ptr), _ptr(col_idx) if nnz else None, float(alpha),
+                                   _ptr(cap), _ptr(bg), _ptr(ws), need, _stream(stream)))
+    return cap, bg
+
+
+def rank_csr(n: int, row_ptr, col_idx, cap, bg, b0, max_iters: int = 200, tol: float = 1e-7,
+             want_l2: bool = True, ws=None, stream=None) -> IterResult:
+    """MAPI ranking on G = alpha M + (1-alpha)/n 1 (Eq. 13); synchronises the stream."""
+    torch = _torch()
+    _need(row_ptr, "row_ptr", torch.int32, (n + 1,))
+    _need(col_idx, "col_idx", torch.int32)
+    for name, t in (("cap", cap), ("bg", bg), ("b0", b0)):
+        _need(t, name, torch.float32, (n,))
+    nnz = col_idx.numel()
+    dev = row_ptr.device
+    w = torch.empty(n, dtype=torch.float32, device=dev)
+    wl2 = torch.empty(n, dtype=torch.float32, device=dev) if want_l2 else None
+    deltas = torch.zeros(max_iters, dtype=torch.float32, device=dev)
+    ws, need = _workspace(WS_RANK_CSR, n, nnz, device=dev, ws=ws)
+    done = ctypes.c_int32(0)
+    st = load().mapi_rank_csr(n, nnz, _ptr(row_ptr), _ptr(col_idx) if nnz else None, _ptr(cap), _ptr(bg),
+                              _ptr(b0), int(max_iters), float(tol), _ptr(w), _ptr(wl2), _ptr(deltas),
+                              ctypes.byref(done), _ptr(ws), need, _stream(stream))
+    _check(st, done.value)
+    k = done.value
+    return IterResult(w, wl2, None, deltas[:k], k)

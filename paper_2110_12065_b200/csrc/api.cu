@@ -1,0 +1,617 @@
+// api.cu — the C ABI of libmapi.so (declared and documented in include/mapi.h).
+//
+// Host side only: argument validation, workspace carving, launch-shape selection, kernel
+// launches, status read-back.  Every step of the hot path runs in the kernels of
+// dense.cuh / deflate.cuh / csr.cuh / batched.cuh; there is no CPU fallback.
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <type_traits>
+
+#include "../../include/mapi.h"
+#include "batched.cuh"
+#include "csr.cuh"
+#include "deflate.cuh"
+#include "dense.cuh"
+
+using namespace mapi;
+
+// ---------------------------------------------------------------------------------------------
+// errors, instrumentation
+
+static thread_local char g_err[512] = "";
+static std::atomic<uint64_t> g_launches{0};
+static std::atomic<int> g_profiling{0};
+static thread_local float g_last_kernel_ms = 0.0f;
+
+static mapi_status fail(mapi_status st, const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return st;
+}
+
+#define MAPI_CUDA(call)                                                                          \
+    do {                                                                                         \
+        cudaError_t e_ = (call);                                                                 \
+        if (e_ != cudaSuccess)                                                                   \
+            return fail(MAPI_ERR_CUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, \
+                        __LINE__);                                                               \
+    } while (0)
+
+#define MAPI_LAUNCHED()                                                                         \
+    do {                                                                                        \
+        g_launches.fetch_add(1, std::memory_order_relaxed);                                     \
+        cudaError_t e_ = cudaGetLastError();                                                    \
+        if (e_ != cudaSuccess)                                                                  \
+            return fail(MAPI_ERR_CUDA, "launch failed: %s (%s:%d)", cudaGetErrorString(e_),    \
+                        __FILE__, __LINE__);                                                    \
+    } while (0)
+
+namespace {
+
+struct Device {
+    int id = -1;
+    int sms = 0;
+    int smem_optin = 0;
+    int cc_major = 0;
+    size_t l2_bytes = 0;
+};
+
+mapi_status device_info(Device& d) {
+    int id = 0;
+    MAPI_CUDA(cudaGetDevice(&id));
+    static thread_local Device cache;
+    if (cache.id != id) {
+        Device x;
+        x.id = id;
+        MAPI_CUDA(cudaDeviceGetAttribute(&x.sms, cudaDevAttrMultiProcessorCount, id));
+        MAPI_CUDA(cudaDeviceGetAttribute(&x.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, id));
+        MAPI_CUDA(cudaDeviceGetAttribute(&x.cc_major, cudaDevAttrComputeCapabilityMajor, id));
+        int l2 = 0;
+        MAPI_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, id));
+        x.l2_bytes = (size_t)l2;
+        if (x.cc_major != 10)
+            return fail(MAPI_ERR_CUDA, "libmapi is built for sm_100a; device %d has compute capability %d.x",
+                        id, x.cc_major);
+        cache = x;
+    }
+    d = cache;
+    return MAPI_OK;
+}
+
+inline size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
+
+template <int V>
+using IC = std::integral_constant<int, V>;
+
+template <typename F>
+auto with_op(int op, F&& f) {
+    return op == 1 ? f(IC<1>{}) : f(IC<0>{});
+}
+template <typename F>
+auto with_vec(int vec, F&& f) {
+    return vec == 8 ? f(IC<8>{}) : (vec == 4 ? f(IC<4>{}) : f(IC<1>{}));
+}
+template <typename F>
+auto with_pol(int pol, F&& f) {
+    return pol == 1 ? f(IC<1>{}) : f(IC<0>{});
+}
+
+constexpr int unroll_for(int vec) { return vec == 8 ? 4 : (vec == 4 ? 8 : 16); }
+
+// widest vector the row starts support: 32 B (v8) needs a 32 B-aligned base and lda % 8 == 0
+int vec_width(const void* base, int64_t lda) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(base);
+    if (a % 32 == 0 && lda % 8 == 0) return 8;
+    if (a % 16 == 0 && lda % 4 == 0) return 4;
+    return 1;
+}
+
+// cache policy: stream with L2 evict-first when the matrix cannot stay L2-resident
+int load_policy(const Device& d, int64_t rows, int64_t lda) {
+    const double bytes = (double)rows * (double)lda * 4.0;
+    return bytes > 0.5 * (double)d.l2_bytes ? 0 : 1;
+}
+
+mapi_status check_op(int32_t op) {
+    if (op != MAPI_OP_MIN1 && op != MAPI_OP_MIN2)
+        return fail(MAPI_ERR_BAD_PARAM, "op (%d) must be MAPI_OP_MIN1 (0) or MAPI_OP_MIN2 (1)", op);
+    return MAPI_OK;
+}
+
+struct Timer {
+    cudaEvent_t a = nullptr, b = nullptr;
+    cudaStream_t s = nullptr;
+    bool on = false;
+    explicit Timer(cudaStream_t st) : s(st) {
+        on = g_profiling.load() != 0;
+        if (on) {
+            cudaEventCreate(&a);
+            cudaEventCreate(&b);
+        }
+    }
+    void start() {
+        if (on) cudaEventRecord(a, s);
+    }
+    void stop() {
+        if (on) cudaEventRecord(b, s);
+    }
+    void harvest() {  // after a stream sync
+        if (on) {
+            float ms = 0.0f;
+            if (cudaEventElapsedTime(&ms, a, b) == cudaSuccess) g_last_kernel_ms = ms;
+        }
+    }
+    ~Timer() {
+        if (a) cudaEventDestroy(a);
+        if (b) cudaEventDestroy(b);
+    }
+};
+
+// ---------------------------------------------------------------------------------------------
+// dense iterate workspace: [header 256 B: bar @0, status[2] @64, stop @72]
+//                          [slots 2 x 1024 floats][y 2n floats][w n floats]
+constexpr int kMaxGrid = 1024;
+constexpr int kIterThreads = 512;
+
+size_t iterate_ws_bytes(int64_t n) {
+    return 256 + align256(sizeof(float) * 2 * kMaxGrid) + align256(sizeof(float) * 2 * (size_t)n) +
+           align256(sizeof(float) * (size_t)n);
+}
+
+struct IterWs {
+    unsigned int* bar;
+    int32_t* status;
+    int32_t* stop;
+    float* slots;
+    float* y;
+    float* w;
+};
+
+IterWs carve_iterate(void* ws, int64_t n) {
+    char* p = static_cast<char*>(ws);
+    IterWs w;
+    w.bar = reinterpret_cast<unsigned int*>(p);
+    w.status = reinterpret_cast<int32_t*>(p + 64);
+    w.stop = reinterpret_cast<int32_t*>(p + 72);
+    p += 256;
+    w.slots = reinterpret_cast<float*>(p);
+    p += align256(sizeof(float) * 2 * kMaxGrid);
+    w.y = reinterpret_cast<float*>(p);
+    p += align256(sizeof(float) * 2 * (size_t)n);
+    w.w = reinterpret_cast<float*>(p);
+    return w;
+}
+
+size_t persistent_smem_bytes(int64_t n) { return sizeof(float) * (size_t)(((n + 3) & ~int64_t(3)) + 33); }
+
+bool use_persistent(const Device& d, int64_t n) {
+    const char* e = getenv("MAPI_DENSE_PATH");
+    if (e && strcmp(e, "multi") == 0) return false;
+    return persistent_smem_bytes(n) <= (size_t)d.smem_optin;
+}
+
+// Runs MAPI on device buffers; no stream sync, no status read-back (caller does both).
+mapi_status iterate_launch(const Device& d, int32_t op, const float* A, int64_t n, int64_t lda,
+                           const float* b0, int32_t iters, float tol, float* w_out, float* norms,
+                           float* deltas, const IterWs& W, cudaStream_t s, Timer* timer) {
+    const int vec = vec_width(A, lda);
+    const int pol = load_policy(d, n, lda);
+    MAPI_CUDA(cudaMemsetAsync(W.bar, 0, 256, s));
+    if (use_persistent(d, n)) {
+        mapi_status st = MAPI_OK;
+        with_op(op, [&](auto OPc) {
+            return with_vec(vec, [&](auto VECc) {
+                return with_pol(pol, [&](auto POLc) {
+                    constexpr int OP = decltype(OPc)::value, VEC = decltype(VECc)::value,
+                                  POL = decltype(POLc)::value;
+                    auto kern = k_iterate_persistent<OP, VEC, POL, unroll_for(VEC)>;
+                    const size_t smem = persistent_smem_bytes(n);
+                    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                         (int)smem);
+                    int occ = 0;
+                    if (e == cudaSuccess)
+                        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kIterThreads, smem);
+                    if (e != cudaSuccess || occ < 1) {
+                        st = fail(MAPI_ERR_CUDA, "persistent kernel occupancy query failed: %s",
+                                  cudaGetErrorString(e));
+                        return 0;
+                    }
+                    int64_t want = (n + (kIterThreads / 32) - 1) / (kIterThreads / 32);
+                    int grid = (int)std::min<int64_t>({(int64_t)occ * d.sms, want, (int64_t)kMaxGrid});
+                    grid = std::max(grid, 1);
+                    IterArgs a;
+                    a.A = A; a.n = n; a.lda = lda; a.b0 = b0; a.iters = iters; a.tol = tol;
+                    a.w_out = w_out; a.norms = norms; a.deltas = deltas; a.y = W.y; a.slots = W.slots;
+                    a.bar = W.bar; a.status = W.status;
+                    void* args[] = {&a};
+                    if (timer) timer->start();
+                    e = cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kIterThreads), args,
+                                                    smem, s);
+                    if (timer) timer->stop();
+                    g_launches.fetch_add(1, std::memory_order_relaxed);
+                    if (e != cudaSuccess)
+                        st = fail(MAPI_ERR_CUDA, "cooperative launch (grid %d, smem %zu): %s", grid, smem,
+                                  cudaGetErrorString(e));
+                    return 0;
+                });
+            });
+        });
+        return st;
+    }
+    // multi-launch path
+    MAPI_CUDA(cudaMemcpyAsync(W.w, b0, sizeof(float) * (size_t)n, cudaMemcpyDeviceToDevice, s));
+    mapi_status st = MAPI_OK;
+    if (timer) timer->start();
+    with_op(op, [&](auto OPc) {
+        return with_vec(vec_width(A, lda) == 8 ? 8 : (vec_width(A, lda) == 4 ? 4 : 1), [&](auto VECc) {
+            return with_pol(pol, [&](auto POLc) {
+                constexpr int OP = decltype(OPc)::value, VEC = decltype(VECc)::value,
+                              POL = decltype(POLc)::value;
+                auto kern = k_rows_partial<OP, VEC, POL, unroll_for(VEC)>;
+                int occ = 0;
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kIterThreads, 0);
+                int64_t want = (n + 15) / 16;
+                int grid = (int)std::min<int64_t>({(int64_t)std::max(occ, 1) * d.sms, want, (int64_t)kMaxGrid});
+                grid = std::max(grid, 1);
+                for (int32_t t = 0; t < iters && st == MAPI_OK; ++t) {
+                    kern<<<grid, kIterThreads, 0, s>>>(A, n, lda, W.w, W.y, W.slots, W.stop);
+                    g_launches.fetch_add(1, std::memory_order_relaxed);
+                    k_normalize<<<1, 1024, 0, s>>>(n, W.y, W.slots, grid, W.w, t, tol, norms, deltas,
+                                                   W.status, W.stop);
+                    g_launches.fetch_add(1, std::memory_order_relaxed);
+                    cudaError_t e = cudaGetLastError();
+                    if (e != cudaSuccess) st = fail(MAPI_ERR_CUDA, "launch: %s", cudaGetErrorString(e));
+                }
+                return 0;
+            });
+        });
+    });
+    if (timer) timer->stop();
+    if (st != MAPI_OK) return st;
+    MAPI_CUDA(cudaMemcpyAsync(w_out, W.w, sizeof(float) * (size_t)n, cudaMemcpyDeviceToDevice, s));
+    return MAPI_OK;
+}
+
+mapi_status read_status(const IterWs& W, cudaStream_t s, int32_t* iters_done) {
+    int32_t h[2] = {0, 0};
+    MAPI_CUDA(cudaMemcpyAsync(h, W.status, sizeof(h), cudaMemcpyDeviceToHost, s));
+    MAPI_CUDA(cudaStreamSynchronize(s));
+    if (iters_done) *iters_done = h[1];
+    if (h[0] == MAPI_ERR_DEGENERATE)
+        return fail(MAPI_ERR_DEGENERATE, "||A (+) w_t||_1 == 0 at iteration %d", h[1]);
+    if (h[0] == MAPI_ERR_NONFINITE)
+        return fail(MAPI_ERR_NONFINITE, "||A (+) w_t||_1 is not finite at iteration %d", h[1]);
+    return MAPI_OK;
+}
+
+mapi_status validate_dense(int32_t op, const float* A, int64_t n, int64_t lda, const float* b0,
+                           int32_t iters, float tol, const float* w_out, void* ws) {
+    mapi_status st = check_op(op);
+    if (st != MAPI_OK) return st;
+    if (!A) return fail(MAPI_ERR_NULL, "A is NULL");
+    if (!b0) return fail(MAPI_ERR_NULL, "b0 is NULL");
+    if (!w_out) return fail(MAPI_ERR_NULL, "w_out is NULL");
+    if (!ws) return fail(MAPI_ERR_WORKSPACE, "workspace is NULL");
+    if (n < 1) return fail(MAPI_ERR_SHAPE, "n (%lld) must be >= 1", (long long)n);
+    if (lda < n) return fail(MAPI_ERR_SHAPE, "lda (%lld) < n (%lld)", (long long)lda, (long long)n);
+    if (iters < 1) return fail(MAPI_ERR_BAD_PARAM, "iters (%d) must be >= 1", iters);
+    if (!(tol >= 0.0f)) return fail(MAPI_ERR_BAD_PARAM, "tol (%g) must be >= 0", (double)tol);
+    return MAPI_OK;
+}
+
+}  // namespace
+
+// =============================================================================================
+extern "C" {
+
+const char* mapi_status_string(mapi_status s) {
+    switch (s) {
+    case MAPI_OK: return "MAPI_OK";
+    case MAPI_ERR_NULL: return "MAPI_ERR_NULL";
+    case MAPI_ERR_SHAPE: return "MAPI_ERR_SHAPE";
+    case MAPI_ERR_BAD_PARAM: return "MAPI_ERR_BAD_PARAM";
+    case MAPI_ERR_DEGENERATE: return "MAPI_ERR_DEGENERATE";
+    case MAPI_ERR_NEGATIVE: return "MAPI_ERR_NEGATIVE";
+    case MAPI_ERR_NONFINITE: return "MAPI_ERR_NONFINITE";
+    case MAPI_ERR_WORKSPACE: return "MAPI_ERR_WORKSPACE";
+    case MAPI_ERR_CUDA: return "MAPI_ERR_CUDA";
+    }
+    return "MAPI_ERR_UNKNOWN";
+}
+
+const char* mapi_last_error_message(void) { return g_err; }
+uint64_t mapi_launch_count(void) { return g_launches.load(); }
+void mapi_set_profiling(int32_t enable) { g_profiling.store(enable ? 1 : 0); }
+float mapi_last_kernel_ms(void) { return g_last_kernel_ms; }
+
+size_t mapi_workspace_size(int32_t op, int64_t n, int64_t nnz, int32_t k) {
+    if (n < 0) n = 0;
+    if (nnz < 0) nnz = 0;
+    if (k < 0) k = 0;
+    switch (op) {
+    case MAPI_WS_MATVEC: return 0;
+    case MAPI_WS_ITERATE: return iterate_ws_bytes(n);
+    case MAPI_WS_ITERATE_HOST:  // nnz = lda, k = iters
+        return iterate_ws_bytes(n) + align256(sizeof(float) * (size_t)n * (size_t)nnz) +
+               4 * align256(sizeof(float) * (size_t)n) + 2 * align256(sizeof(float) * (size_t)k);
+    case MAPI_WS_PCA_TOPK:
+        return iterate_ws_bytes(n) + align256(sizeof(float) * (size_t)n * (size_t)n) +
+               2 * align256(sizeof(double) * (size_t)k * (size_t)n) +
+               align256(sizeof(double) * 64 * (size_t)n) + align256(sizeof(float) * (size_t)n);
+    case MAPI_WS_ITERATE_BATCHED: return batched_ws_bytes(n, k);
+    case MAPI_WS_CSR_PREPARE: return csr_prepare_ws_bytes(n, nnz);
+    case MAPI_WS_RANK_CSR: return csr_rank_ws_bytes(n, nnz);
+    }
+    return 0;
+}
+
+mapi_status mapi_mavp_matvec(int32_t op, const float* A, int64_t n_rows, int64_t n_cols, int64_t lda,
+                             const float* x, float* y, mapi_stream_t stream) {
+    mapi_status st = check_op(op);
+    if (st != MAPI_OK) return st;
+    if (n_rows < 0 || n_cols < 0)
+        return fail(MAPI_ERR_SHAPE, "negative size: n_rows %lld, n_cols %lld", (long long)n_rows,
+                    (long long)n_cols);
+    if (lda < n_cols) return fail(MAPI_ERR_SHAPE, "lda (%lld) < n_cols (%lld)", (long long)lda, (long long)n_cols);
+    if (n_rows == 0) return MAPI_OK;
+    if (!y) return fail(MAPI_ERR_NULL, "y is NULL");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (n_cols == 0) {
+        MAPI_CUDA(cudaMemsetAsync(y, 0, sizeof(float) * (size_t)n_rows, s));
+        return MAPI_OK;
+    }
+    if (!A) return fail(MAPI_ERR_NULL, "A is NULL");
+    if (!x) return fail(MAPI_ERR_NULL, "x is NULL");
+    Device d;
+    if ((st = device_info(d)) != MAPI_OK) return st;
+    const size_t smem_x = sizeof(float) * (size_t)n_cols;
+    const bool x_in_smem = smem_x <= 200 * 1024;
+    int vec = vec_width(A, lda);
+    if (!x_in_smem) vec = std::min(vec, vec_width(x, 0));
+    const int pol = load_policy(d, n_rows, lda);
+    with_op(op, [&](auto OPc) {
+        return with_vec(vec, [&](auto VECc) {
+            return with_pol(pol, [&](auto POLc) {
+                constexpr int OP = decltype(OPc)::value, VEC = decltype(VECc)::value,
+                              POL = decltype(POLc)::value;
+                auto run = [&](auto kern, size_t smem) {
+                    cudaError_t e = cudaSuccess;
+                    if (smem > 48 * 1024)
+                        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                    int occ = 1;
+                    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 512, smem);
+                    if (e != cudaSuccess) {
+                        st = fail(MAPI_ERR_CUDA, "matvec setup: %s", cudaGetErrorString(e));
+                        return 0;
+                    }
+                    int64_t want = (n_rows + 15) / 16;
+                    int grid = (int)std::min<int64_t>((int64_t)std::max(occ, 1) * d.sms, want);
+                    kern<<<std::max(grid, 1), 512, smem, s>>>(A, n_rows, n_cols, lda, x, y);
+                    g_launches.fetch_add(1, std::memory_order_relaxed);
+                    e = cudaGetLastError();
+                    if (e != cudaSuccess) st = fail(MAPI_ERR_CUDA, "matvec launch: %s", cudaGetErrorString(e));
+                    return 0;
+                };
+                if (x_in_smem)
+                    return run(k_matvec<OP, VEC, POL, false, unroll_for(VEC)>, smem_x);
+                return run(k_matvec<OP, VEC, POL, true, unroll_for(VEC)>, (size_t)0);
+            });
+        });
+    });
+    return st;
+}
+
+mapi_status mapi_iterate(int32_t op, const float* A, int64_t n, int64_t lda, const float* b0, int32_t iters,
+                         float tol, float* w_out, float* w_l2_out, float* norms, float* deltas,
+                         int32_t* iters_done, void* ws, size_t ws_bytes, mapi_stream_t stream) {
+    mapi_status st = validate_dense(op, A, n, lda, b0, iters, tol, w_out, ws);
+    if (st != MAPI_OK) return st;
+    if (ws_bytes < iterate_ws_bytes(n))
+        return fail(MAPI_ERR_WORKSPACE, "ws_bytes (%zu) < required (%zu)", ws_bytes, iterate_ws_bytes(n));
+    Device d;
+    if ((st = device_info(d)) != MAPI_OK) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    IterWs W = carve_iterate(ws, n);
+    Timer timer(s);
+    st = iterate_launch(d, op, A, n, lda, b0, iters, tol, w_out, norms, deltas, W, s, &timer);
+    if (st != MAPI_OK) return st;
+    if (w_l2_out) {
+        k_l2_copy<<<1, 1024, 0, s>>>(n, w_out, w_l2_out);
+        MAPI_LAUNCHED();
+    }
+    st = read_status(W, s, iters_done);
+    timer.harvest();
+    return st;
+}
+
+mapi_status mapi_iterate_host(int32_t op, const float* A_host, int64_t n, int64_t lda, const float* b0_host,
+                              int32_t iters, float tol, float* w_out_host, float* w_l2_out_host,
+                              float* norms_host, float* deltas_host, int32_t* iters_done, void* ws,
+                              size_t ws_bytes, mapi_stream_t stream) {
+    mapi_status st = validate_dense(op, A_host, n, lda, b0_host, iters, tol, w_out_host, ws);
+    if (st != MAPI_OK) return st;
+    const size_t need = mapi_workspace_size(MAPI_WS_ITERATE_HOST, n, lda, iters);
+    if (ws_bytes < need) return fail(MAPI_ERR_WORKSPACE, "ws_bytes (%zu) < required (%zu)", ws_bytes, need);
+    Device d;
+    if ((st = device_info(d)) != MAPI_OK) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    char* p = static_cast<char*>(ws);
+    IterWs W = carve_iterate(p, n);
+    p += iterate_ws_bytes(n);
+    float* A = reinterpret_cast<float*>(p);
+    p += align256(sizeof(float) * (size_t)n * (size_t)lda);
+    float* b0 = reinterpret_cast<float*>(p);
+    p += align256(sizeof(float) * (size_t)n);
+    float* w = reinterpret_cast<float*>(p);
+    p += align256(sizeof(float) * (size_t)n);
+    float* wl2 = reinterpret_cast<float*>(p);
+    p += 2 * align256(sizeof(float) * (size_t)n);
+    float* nrm = reinterpret_cast<float*>(p);
+    p += align256(sizeof(float) * (size_t)iters);
+    float* dlt = reinterpret_cast<float*>(p);
+    MAPI_CUDA(cudaMemcpyAsync(A, A_host, sizeof(float) * (size_t)n * (size_t)lda, cudaMemcpyHostToDevice, s));
+    MAPI_CUDA(cudaMemcpyAsync(b0, b0_host, sizeof(float) * (size_t)n, cudaMemcpyHostToDevice, s));
+    Timer timer(s);
+    st = iterate_launch(d, op, A, n, lda, b0, iters, tol, w, nrm, dlt, W, s, &timer);
+    if (st != MAPI_OK) return st;
+    if (w_l2_out_host) {
+        k_l2_copy<<<1, 1024, 0, s>>>(n, w, wl2);
+        MAPI_LAUNCHED();
+        MAPI_CUDA(cudaMemcpyAsync(w_l2_out_host, wl2, sizeof(float) * (size_t)n, cudaMemcpyDeviceToHost, s));
+    }
+    MAPI_CUDA(cudaMemcpyAsync(w_out_host, w, sizeof(float) * (size_t)n, cudaMemcpyDeviceToHost, s));
+    if (norms_host)
+        MAPI_CUDA(cudaMemcpyAsync(norms_host, nrm, sizeof(float) * (size_t)iters, cudaMemcpyDeviceToHost, s));
+    if (deltas_host)
+        MAPI_CUDA(cudaMemcpyAsync(deltas_host, dlt, sizeof(float) * (size_t)iters, cudaMemcpyDeviceToHost, s));
+    st = read_status(W, s, iters_done);
+    timer.harvest();
+    return st;
+}
+
+mapi_status mapi_pca_topk(int32_t op, const float* C, int64_t n, int64_t ldc, int32_t k, int32_t iters,
+                          const float* b0, float* P_out, float* norms, float* deltas, void* ws,
+                          size_t ws_bytes, mapi_stream_t stream) {
+    mapi_status st = validate_dense(op, C, n, ldc, b0, iters, 0.0f, P_out, ws);
+    if (st != MAPI_OK) return st;
+    if (k < 1 || k > n) return fail(MAPI_ERR_BAD_PARAM, "k (%d) must be in [1, n = %lld]", k, (long long)n);
+    const size_t need = mapi_workspace_size(MAPI_WS_PCA_TOPK, n, 0, k);
+    if (ws_bytes < need) return fail(MAPI_ERR_WORKSPACE, "ws_bytes (%zu) < required (%zu)", ws_bytes, need);
+    Device d;
+    if ((st = device_info(d)) != MAPI_OK) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    char* p = static_cast<char*>(ws);
+    IterWs W = carve_iterate(p, n);
+    p += iterate_ws_bytes(n);
+    float* D = reinterpret_cast<float*>(p);
+    p += align256(sizeof(float) * (size_t)n * (size_t)n);
+    double* P64 = reinterpret_cast<double*>(p);
+    p += align256(sizeof(double) * (size_t)k * (size_t)n);
+    double* R = reinterpret_cast<double*>(p);
+    p += align256(sizeof(double) * (size_t)k * (size_t)n);
+    double* part = reinterpret_cast<double*>(p);
+    p += align256(sizeof(double) * 64 * (size_t)n);
+    float* wtmp = reinterpret_cast<float*>(p);
+    const int S = (int)std::min<int64_t>(64, n);
+    const int64_t rows_per = (n + S - 1) / S;
+    float total_ms = 0.0f;
+    for (int32_t i = 0; i < k; ++i) {
+        const float* Ai = C;
+        int64_t ld = ldc;
+        if (i > 0) {
+            const int gx = (int)std::min<int64_t>((n + 255) / 256, 65535);
+            const int gy = (int)std::min<int64_t>(n, 65535);
+            k_build_deflated<<<dim3(gx, gy), 256, 0, s>>>(C, n, ldc, P64, R, i, D);
+            MAPI_LAUNCHED();
+            Ai = D;
+            ld = n;
+        }
+        Timer timer(s);
+        st = iterate_launch(d, op, Ai, n, ld, b0, iters, 0.0f, wtmp, norms ? norms + (int64_t)i * iters : nullptr,
+                            deltas ? deltas + (int64_t)i * iters : nullptr, W, s, &timer);
+        if (st != MAPI_OK) return st;
+        int32_t done = 0;
+        st = read_status(W, s, &done);
+        timer.harvest();
+        total_ms += g_last_kernel_ms;
+        if (st != MAPI_OK) return fail(st, "vector %d: %s", i, g_err);
+        k_l2_to_p<<<1, 1024, 0, s>>>(n, wtmp, P64 + (int64_t)i * n, P_out + (int64_t)i * n);
+        MAPI_LAUNCHED();
+        if (i + 1 < k) {
+            k_colsum_partial<<<dim3((unsigned)((n + 255) / 256), S), 256, 0, s>>>(C, n, ldc, P64 + (int64_t)i * n,
+                                                                               part, rows_per);
+            MAPI_LAUNCHED();
+            k_colsum_final<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, S, part, R + (int64_t)i * n);
+            MAPI_LAUNCHED();
+        }
+    }
+    MAPI_CUDA(cudaStreamSynchronize(s));
+    if (g_profiling.load()) g_last_kernel_ms = total_ms;
+    return MAPI_OK;
+}
+
+mapi_status mapi_iterate_batched(int32_t op, const float* A, int64_t n, int64_t lda, const float* B0, int32_t k,
+                                 int32_t iters, float tol, float* W_out, float* norms, float* deltas,
+                                 int32_t* iters_done, void* ws, size_t ws_bytes, mapi_stream_t stream) {
+    mapi_status st = validate_dense(op, A, n, lda, B0, iters, tol, W_out, ws);
+    if (st != MAPI_OK) return st;
+    if (k < 1) return fail(MAPI_ERR_BAD_PARAM, "k (%d) must be >= 1", k);
+    const size_t need = batched_ws_bytes(n, k);
+    if (ws_bytes < need) return fail(MAPI_ERR_WORKSPACE, "ws_bytes (%zu) < required (%zu)", ws_bytes, need);
+    Device d;
+    if ((st = device_info(d)) != MAPI_OK) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    Timer timer(s);
+    st = batched_run(op, A, n, lda, B0, k, iters, tol, W_out, norms, deltas, ws, d.sms, s, &timer.a, &timer.b,
+                     timer.on, g_launches);
+    if (st != MAPI_OK) return fail(st, "%s", batched_last_error());
+    st = batched_finish(ws, n, k, s, iters_done);
+    timer.harvest();
+    if (st == MAPI_ERR_CUDA) return fail(st, "%s", batched_last_error());
+    if (st != MAPI_OK) return fail(st, "one or more vectors stopped with %s", mapi_status_string(st));
+    return MAPI_OK;
+}
+
+mapi_status mapi_csr_prepare(int64_t n, int64_t nnz, const int32_t* row_ptr, const int32_t* col_idx, float alpha,
+                             float* cap_out, float* bg_out, void* ws, size_t ws_bytes, mapi_stream_t stream) {
+    if (n < 1) return fail(MAPI_ERR_SHAPE, "n (%lld) must be >= 1", (long long)n);
+    if (nnz < 0 || nnz >= (int64_t)INT32_MAX)
+        return fail(MAPI_ERR_SHAPE, "nnz (%lld) must be in [0, 2^31)", (long long)nnz);
+    if (n >= (int64_t)INT32_MAX) return fail(MAPI_ERR_SHAPE, "n (%lld) must be < 2^31", (long long)n);
+    if (!row_ptr || (nnz > 0 && !col_idx)) return fail(MAPI_ERR_NULL, "row_ptr/col_idx is NULL");
+    if (!cap_out || !bg_out) return fail(MAPI_ERR_NULL, "cap_out/bg_out is NULL");
+    if (!(alpha > 0.0f && alpha < 1.0f)) return fail(MAPI_ERR_BAD_PARAM, "alpha (%g) must be in (0, 1)", (double)alpha);
+    if (!ws) return fail(MAPI_ERR_WORKSPACE, "workspace is NULL");
+    if (ws_bytes < csr_prepare_ws_bytes(n, nnz))
+        return fail(MAPI_ERR_WORKSPACE, "ws_bytes (%zu) < required (%zu)", ws_bytes, csr_prepare_ws_bytes(n, nnz));
+    Device d;
+    mapi_status st;
+    if ((st = device_info(d)) != MAPI_OK) return st;
+    st = csr_prepare_run(n, nnz, row_ptr, col_idx, alpha, cap_out, bg_out, ws, d.sms,
+                         static_cast<cudaStream_t>(stream), g_launches);
+    if (st != MAPI_OK) return fail(st, "%s", csr_last_error());
+    return MAPI_OK;
+}
+
+mapi_status mapi_rank_csr(int64_t n, int64_t nnz, const int32_t* row_ptr, const int32_t* col_idx, const float* cap,
+                          const float* bg, const float* b0, int32_t max_iters, float tol, float* w_out,
+                          float* w_l2_out, float* deltas, int32_t* iters_done, void* ws, size_t ws_bytes,
+                          mapi_stream_t stream) {
+    if (n < 1) return fail(MAPI_ERR_SHAPE, "n (%lld) must be >= 1", (long long)n);
+    if (nnz < 0 || nnz >= (int64_t)INT32_MAX)
+        return fail(MAPI_ERR_SHAPE, "nnz (%lld) must be in [0, 2^31)", (long long)nnz);
+    if (n >= (int64_t)INT32_MAX) return fail(MAPI_ERR_SHAPE, "n (%lld) must be < 2^31", (long long)n);
+    if (!row_ptr || (nnz > 0 && !col_idx) || !cap || !bg || !b0 || !w_out)
+        return fail(MAPI_ERR_NULL, "a required pointer (row_ptr/col_idx/cap/bg/b0/w_out) is NULL");
+    if (max_iters < 1) return fail(MAPI_ERR_BAD_PARAM, "max_iters (%d) must be >= 1", max_iters);
+    if (!(tol >= 0.0f)) return fail(MAPI_ERR_BAD_PARAM, "tol (%g) must be >= 0", (double)tol);
+    if (!ws) return fail(MAPI_ERR_WORKSPACE, "workspace is NULL");
+    if (ws_bytes < csr_rank_ws_bytes(n, nnz))
+        return fail(MAPI_ERR_WORKSPACE, "ws_bytes (%zu) < required (%zu)", ws_bytes, csr_rank_ws_bytes(n, nnz));
+    Device d;
+    mapi_status st;
+    if ((st = device_info(d)) != MAPI_OK) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    Timer timer(s);
+    st = csr_rank_run(n, nnz, row_ptr, col_idx, cap, bg, b0, max_iters, tol, w_out, deltas, ws, d.sms, s,
+                      timer.on ? &timer.a : nullptr, timer.on ? &timer.b : nullptr, g_launches);
+    if (st != MAPI_OK) return fail(st, "%s", csr_last_error());
+    if (w_l2_out) {
+        k_l2_copy<<<1, 1024, 0, s>>>(n, w_out, w_l2_out);
+        MAPI_LAUNCHED();
+    }
+    st = csr_rank_finish(ws, n, nnz, s, iters_done);
+    timer.harvest();
+    if (st == MAPI_ERR_CUDA) return fail(st, "%s", csr_last_error());
+    if (st == MAPI_ERR_NEGATIVE) return fail(st, "b0 has a negative entry");
+    if (st == MAPI_ERR_DEGENERATE) return fail(st, "||G (+) w_t||_1 == 0");
+    if (st == MAPI_ERR_NONFINITE) return fail(st, "||G (+) w_t||_1 is not finite");
+    return st;
+}
+
+}  // extern "C"

@@ -1,0 +1,139 @@
+"""Host-side checks of the C ABI (no GPU, no compute): the library builds/loads, exports every
+symbol include/mapi.h declares, validates arguments before touching the device, and its MAVP
+inner loops contain no multiplication (SASS inspection, the analogue of the paper's op-count
+claim P:5 / P:146)."""
+import ctypes
+import os
+import re
+import shutil
+import subprocess
+
+import pytest
+
+import paper_2110_12065_b200 as m
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "mapi.h")
+
+
+@pytest.fixture(scope="module")
+def lib():
+    m.build()
+    return m.load()
+
+
+def declared_functions():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(mapi_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_header_symbols_exported(lib):
+    names = declared_functions()
+    assert len(names) >= 13
+    for name in names:
+        assert hasattr(lib, name), f"{name} declared in mapi.h but not exported"
+    out = subprocess.run(["nm", "-D", "--defined-only", m._build.LIB], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (mapi_\w+)", out))
+    assert set(names) <= exported
+
+
+def test_status_strings(lib):
+    for code, name in m.STATUS.items():
+        assert lib.mapi_status_string(code).decode() == name
+
+
+def test_workspace_sizes_monotone(lib):
+    a = m.workspace_size(m.WS_ITERATE, 1000)
+    b = m.workspace_size(m.WS_ITERATE, 2000)
+    assert 0 < a < b
+    assert m.workspace_size(m.WS_MATVEC, 1000) == 0
+    assert m.workspace_size(m.WS_ITERATE_HOST, 100, 104, 50) >= 100 * 104 * 4
+    assert m.workspace_size(m.WS_PCA_TOPK, 64, 0, 8) >= 64 * 64 * 4
+    assert m.workspace_size(m.WS_RANK_CSR, 1000, 5000) > 0
+    assert m.workspace_size(m.WS_ITERATE_BATCHED, 1000, 0, 64) >= 2 * 64 * 1000 * 4
+
+
+def _err(lib):
+    return lib.mapi_last_error_message().decode()
+
+
+def test_validation_before_device(lib):
+    # every one of these fails argument validation on the host, before any CUDA call
+    fake = ctypes.c_void_p(4096)  # never dereferenced
+    st = lib.mapi_iterate(0, None, 4, 4, fake, 5, 0.0, fake, None, None, None, None, fake, 1 << 20, None)
+    assert st == 1 and "A is NULL" in _err(lib)
+    st = lib.mapi_iterate(0, fake, 4, 3, fake, 5, 0.0, fake, None, None, None, None, fake, 1 << 20, None)
+    assert st == 2 and "lda (3) < n (4)" in _err(lib)
+    st = lib.mapi_iterate(0, fake, 4, 4, fake, 0, 0.0, fake, None, None, None, None, fake, 1 << 20, None)
+    assert st == 3 and "iters" in _err(lib)
+    st = lib.mapi_iterate(0, fake, 4, 4, fake, 5, -1.0, fake, None, None, None, None, fake, 1 << 20, None)
+    assert st == 3 and "tol" in _err(lib)
+    st = lib.mapi_iterate(7, fake, 4, 4, fake, 5, 0.0, fake, None, None, None, None, fake, 1 << 20, None)
+    assert st == 3 and "op" in _err(lib)
+    st = lib.mapi_iterate(0, fake, 4, 4, fake, 5, 0.0, fake, None, None, None, None, fake, 16, None)
+    assert st == 7
+    st = lib.mapi_mavp_matvec(0, fake, 3, 10, 9, fake, fake, None)
+    assert st == 2 and "lda (9) < n_cols (10)" in _err(lib)
+    st = lib.mapi_pca_topk(0, fake, 8, 8, 9, 5, fake, fake, None, None, fake, 1 << 30, None)
+    assert st == 3 and "k (9)" in _err(lib)
+    st = lib.mapi_csr_prepare(10, 5, fake, fake, 1.5, fake, fake, fake, 1 << 20, None)
+    assert st == 3 and "alpha" in _err(lib)
+    st = lib.mapi_rank_csr(10, 5, fake, fake, fake, fake, fake, 0, 0.0, fake, None, None, None, fake,
+                           1 << 20, None)
+    assert st == 3 and "max_iters" in _err(lib)
+    st = lib.mapi_iterate_batched(0, fake, 8, 8, fake, 0, 5, 0.0, fake, None, None, None, fake, 1 << 30, None)
+    assert st == 3 and "k (0)" in _err(lib)
+
+
+def _sass_functions():
+    cuobjdump = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    out = subprocess.run([cuobjdump, "-sass", m._build.LIB], capture_output=True, text=True, check=True).stdout
+    funcs = {}
+    cur = None
+    for line in out.splitlines():
+        mm = re.match(r"\s+Function : (\S+)", line)
+        if mm:
+            cur = mm.group(1)
+            funcs[cur] = []
+        elif cur:
+            funcs[cur].append(line)
+    return funcs
+
+
+MUL = re.compile(r"\b(FMUL|FFMA|DMUL|DFMA|HMUL2?|HFMA2?|IMUL|FMUL2|FFMA2)\b")
+
+
+def test_mavp_loops_have_no_multiply(lib):
+    """AC3 analogue: the MAVP mat-vec kernels contain no floating multiply at all, and the
+    persistent iteration's only multiplies are the reciprocal refinement of the P:146 divisions."""
+    funcs = _sass_functions()
+    streaming = [f for f in funcs if re.search(r"k_matvec|k_rows_partial|k_batched_partial|k_rank_rows", f)]
+    assert len(streaming) >= 8
+    for f in streaming:
+        body = "\n".join(funcs[f])
+        assert "FMNMX" in body or "k_rank_rows" in f, f
+        # `HFMA2 Rd, -RZ, RZ, imm` is ptxas' constant-materialisation idiom (0 * 0 + imm), not a multiply
+        muls = [ln for ln in funcs[f] if MUL.search(ln) and not re.search(r"\bIMAD\b", ln)
+                and "-RZ, RZ," not in ln]
+        fmul = [ln for ln in muls if re.search(r"\b(FMUL|FFMA|DMUL|DFMA|HMUL2?|HFMA2?|FMUL2|FFMA2)\b", ln)]
+        assert not fmul, f"{f} has floating multiplies:\n" + "\n".join(fmul[:5])
+    for f in funcs:
+        if "k_iterate_persistent" in f:
+            body = funcs[f]
+            n_fmnmx = sum("FMNMX" in ln for ln in body)
+            n_ffma = sum(bool(re.search(r"\bFFMA\b|\bFMUL\b", ln)) for ln in body)
+            n_rcp = sum("MUFU.RCP" in ln for ln in body)
+            assert n_fmnmx >= 8
+            # IEEE division y/s: each MUFU.RCP is followed by 5 FFMA refinement steps, plus
+            # the out-of-range slow path; nothing else may multiply
+            assert n_ffma <= 5 * n_rcp + 24, f"{f}: {n_ffma} FFMA/FMUL vs {n_rcp} MUFU.RCP"
+
+
+def test_streaming_loads_are_256bit(lib):
+    funcs = _sass_functions()
+    hits = [f for f in funcs if "k_iterate_persistentILi0ELi8ELi0" in f]
+    assert hits
+    body = "\n".join(funcs[hits[0]])
+    assert re.search(r"LDG\.E\.NA\.EFL2\.256", body) or re.search(r"LDG\.E\.EF.*\.256", body), \
+        "expected 256-bit evict-first streaming loads"

@@ -1,0 +1,248 @@
+"""GPU parity of the dense MAVP mat-vec (K1) and the MAPI iteration (K2) against the fp64 oracle.
+
+Tolerances (from the BASELINE north star):
+  T1 single mat-vec:  |y_gpu_j - y_orc_j| <= 1e-5 * mag_j,  mag_j = sum_k |term_jk|
+  T2 after T iterations, on the l2-normalised vectors: |cos| >= 1 - 1e-6 and max|diff| <= 1e-4;
+     per-iteration norms s_t relative <= 1e-5.
+All calls go through the C ABI (paper_2110_12065_b200 -> libmapi.so).
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+T1 = 1e-5
+
+
+def _t1(y_gpu, y_orc, mag):
+    y_gpu = np.asarray(y_gpu, np.float64)
+    err = np.abs(y_gpu - y_orc)
+    bound = T1 * mag
+    bad = np.nonzero(err > bound)[0]
+    assert bad.size == 0, (f"T1 violated at {bad[:5]}: err {err[bad[:5]]}, bound {bound[bad[:5]]}, "
+                           f"y_gpu {y_gpu[bad[:5]]}, y_orc {y_orc[bad[:5]]}")
+
+
+def _t2(w_gpu_l2, w_orc, norms_gpu=None, norms_orc=None):
+    a = np.asarray(w_gpu_l2, np.float64)
+    b = np.asarray(w_orc, np.float64)
+    b = b / np.linalg.norm(b)
+    cos = float(a @ b / np.linalg.norm(a))
+    assert abs(cos) >= 1 - 1e-6, f"|cos| = {abs(cos)!r}"
+    assert np.max(np.abs(a - b)) <= 1e-4, f"max abs diff {np.max(np.abs(a - b))}"
+    if norms_gpu is not None:
+        ng = np.asarray(norms_gpu, np.float64)
+        np.testing.assert_allclose(ng, norms_orc, rtol=1e-5)
+
+
+SHAPES = [(1, 1), (1, 7), (3, 5), (9, 9), (31, 33), (33, 31), (255, 256), (256, 257), (257, 255),
+          (100, 4109), (64, 32768), (7, 70001)]
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+@pytest.mark.parametrize("pad", [0, 1, 4, 8])
+def test_matvec_t1(mapi_lib, orc, shape, pad):
+    m = mapi_lib
+    n_rows, n_cols = shape
+    for op, opname in ((m.MIN1, "min1"), (m.MIN2, "min2")):
+        for kind in ("normal", "mixed"):
+            seed = hash((n_rows, n_cols, pad, op, kind)) % (2 ** 31)
+            M, lda = synth.random_matrix(n_rows, n_cols, seed=seed, lda=n_cols + pad, kind=kind)
+            x = synth.random_vector(n_cols, seed=seed + 1, kind="mixed" if kind == "mixed" else "normal")
+            Ad = torch.from_numpy(M).cuda()
+            y = m.mavp_matvec(Ad[:, :n_cols], torch.from_numpy(x).cuda(), op=op)
+            torch.cuda.synchronize()
+            y_orc, mag = orc.matvec(M[:, :n_cols], x, opname, return_mag=True)
+            _t1(y.cpu().numpy(), y_orc, mag)
+
+
+def test_matvec_spec_examples_exact(mapi_lib):
+    m = mapi_lib
+    A = torch.tensor([[1.0, 0.0], [0.0, 1.0]], device="cuda")
+    y = m.mavp_matvec(A, torch.tensor([5.0, -7.0], device="cuda"))
+    assert y.tolist() == [1.0, -1.0]
+    y = m.mavp_matvec(torch.tensor([[2.0, 2.0]], device="cuda"), torch.zeros(2, device="cuda"))
+    assert y.tolist() == [0.0]
+    x = torch.tensor([1.0, -2.0, 3.0], device="cuda")
+    assert m.mavp_matvec(x[None, :], x).tolist() == [6.0]  # l1 induction
+    y = m.mavp_matvec(torch.tensor([[1.0]], device="cuda"), torch.tensor([-1.0], device="cuda"), op=m.MIN2)
+    assert y.tolist() == [0.0]
+
+
+def test_matvec_degenerate_shapes(mapi_lib):
+    m = mapi_lib
+    A = torch.empty(5, 0, device="cuda")
+    y = torch.full((5,), 3.0, device="cuda")
+    m.mavp_matvec(A, torch.empty(0, device="cuda"), y)
+    torch.cuda.synchronize()
+    assert y.tolist() == [0.0] * 5
+    m.mavp_matvec(torch.empty(0, 4, device="cuda"), torch.ones(4, device="cuda"), torch.empty(0, device="cuda"))
+
+
+def test_matvec_bitwise_oddness_and_symmetry(mapi_lib):
+    m = mapi_lib
+    M, _ = synth.random_matrix(300, 1000, seed=5)
+    x = synth.random_vector(1000, seed=6)
+    A = torch.from_numpy(M).cuda()
+    xd = torch.from_numpy(x).cuda()
+    y1 = m.mavp_matvec(A, xd)
+    y2 = m.mavp_matvec(A, -xd)
+    assert torch.equal(y1, -y2)  # (-x) (+) a = -(x (+) a), bitwise
+    # symmetry x (+) a = a (+) x: row j against x vs x (as a 1-row matrix) against row j
+    j = 17
+    ya = m.mavp_matvec(xd[None, :].contiguous(), A[j].contiguous())
+    assert torch.equal(ya[0], y1[j])
+
+
+# ------------------------------------------------------------------------------ iteration
+
+
+def _iterate_case(m, orc, A32, b0, iters, tol=0.0, op="min1"):
+    res = m.iterate(torch.from_numpy(A32).cuda(), torch.from_numpy(b0).cuda(), iters, tol,
+                    op=m.MIN1 if op == "min1" else m.MIN2)
+    ref = orc.mapi(A32, b0.astype(np.float64), iters, tol, op=op)
+    return res, ref
+
+
+def test_iterate_cfg1_parity(mapi_lib, orc):
+    cfg = synth.cfg1()
+    res, ref = _iterate_case(mapi_lib, orc, cfg["A"], cfg["b0"], cfg["iters"])
+    assert res.iters_done == ref.iters_done == 50
+    _t2(res.w_l2.cpu().numpy(), ref.w, res.norms.cpu().numpy(), ref.norms)
+    np.testing.assert_allclose(res.deltas.cpu().numpy(), ref.deltas, rtol=1e-3, atol=1e-7)
+    np.testing.assert_allclose(res.w.cpu().numpy(), ref.w, atol=1e-6)
+    assert abs(float(res.w.abs().sum()) - 1.0) < 1e-5
+
+
+@pytest.mark.parametrize("n", [1, 2, 7, 33, 255, 1000, 4099])
+@pytest.mark.parametrize("op", ["min1", "min2"])
+def test_iterate_random_nonsymmetric(mapi_lib, orc, n, op):
+    r = np.random.default_rng(n)
+    A = r.standard_normal((n, n)).astype(np.float32)
+    if op == "min2":
+        A = np.abs(A) + np.eye(n, dtype=np.float32)
+    b0 = (np.abs(r.standard_normal(n)) + 0.1).astype(np.float32)
+    b0 /= np.linalg.norm(b0)
+    res, ref = _iterate_case(mapi_lib, orc, A, b0, 25, op=op)
+    assert res.iters_done == ref.iters_done
+    _t2(res.w_l2.cpu().numpy(), ref.w, res.norms.cpu().numpy(), ref.norms)
+
+
+def test_iterate_padded_lda_and_unaligned(mapi_lib, orc):
+    m = mapi_lib
+    for pad in (1, 3, 4, 8):
+        M, lda = synth.random_matrix(300, 300, seed=pad, lda=300 + pad)
+        M[:, :300] += np.eye(300, dtype=np.float32) * 5
+        b0 = np.full(300, 1 / np.sqrt(300), np.float32)
+        Ad = torch.from_numpy(M).cuda()[:, :300]
+        res = m.iterate(Ad, torch.from_numpy(b0).cuda(), 20)
+        ref = orc.mapi(np.ascontiguousarray(M[:, :300]), b0, 20)
+        _t2(res.w_l2.cpu().numpy(), ref.w, res.norms.cpu().numpy(), ref.norms)
+
+
+def test_iterate_tolerance_stop_and_identity(mapi_lib, orc):
+    m = mapi_lib
+    n = 64
+    A = np.eye(n, dtype=np.float32)
+    b0 = np.linspace(0.1, 1.0, n).astype(np.float32)
+    b0 /= np.linalg.norm(b0)
+    res = m.iterate(torch.from_numpy(A).cuda(), torch.from_numpy(b0).cuda(), 50, tol=1e-6)
+    ref = orc.mapi(A, b0, 50, tol=1e-6)
+    assert res.iters_done == ref.iters_done == 2  # A = I: fixed point after one step
+    np.testing.assert_allclose(res.w.cpu().numpy(), b0 / np.abs(b0).sum(), rtol=2e-7)
+
+
+def test_iterate_degenerate(mapi_lib):
+    m = mapi_lib
+    A = torch.zeros(40, 40, device="cuda")
+    b0 = torch.full((40,), 0.1, device="cuda")
+    with pytest.raises(m.MapiError) as ei:
+        m.iterate(A, b0, 10)
+    assert ei.value.name == "MAPI_ERR_DEGENERATE" and ei.value.iters_done == 0
+
+
+def test_iterate_determinism_equivariance_resume(mapi_lib):
+    m = mapi_lib
+    cfg = synth.cfg1()
+    A = torch.from_numpy(cfg["A"]).cuda()
+    b0 = torch.from_numpy(cfg["b0"]).cuda()
+    r1 = m.iterate(A, b0, 30)
+    r2 = m.iterate(A, b0, 30)
+    assert torch.equal(r1.w, r2.w) and torch.equal(r1.norms, r2.norms) and torch.equal(r1.deltas, r2.deltas)
+    rn = m.iterate(A, -b0, 30)
+    assert torch.equal(rn.w, -r1.w)  # sign equivariance, bitwise
+    a = m.iterate(A, b0, 12)
+    b = m.iterate(A, a.w.clone(), 18)
+    assert torch.equal(b.w, r1.w)  # resume == uninterrupted run (checkpoint state is (w_t, t))
+    assert torch.equal(b.norms, r1.norms[12:])
+
+
+def test_iterate_multilaunch_path_matches(mapi_lib, orc, monkeypatch):
+    m = mapi_lib
+    cfg = synth.cfg1()
+    monkeypatch.setenv("MAPI_DENSE_PATH", "multi")
+    res = m.iterate(torch.from_numpy(cfg["A"]).cuda(), torch.from_numpy(cfg["b0"]).cuda(), 50)
+    ref = orc.mapi(cfg["A"], cfg["b0"], 50)
+    _t2(res.w_l2.cpu().numpy(), ref.w, res.norms.cpu().numpy(), ref.norms)
+
+
+def test_iterate_host_buffers(mapi_lib, orc):
+    m = mapi_lib
+    cfg = synth.cfg1()
+    A = torch.from_numpy(cfg["A"]).pin_memory()
+    b0 = torch.from_numpy(cfg["b0"]).pin_memory()
+    res = m.iterate_host(A, b0, 50)
+    dev = m.iterate(A.cuda(), b0.cuda(), 50)
+    assert torch.equal(res.w, dev.w.cpu()) and torch.equal(res.norms, dev.norms.cpu())
+
+
+# ------------------------------------------------------------------------------ full size (cfg3)
+
+
+@pytest.fixture(scope="module")
+def cfg3_device():
+    cfg = synth.cfg3(device="cuda")
+    return cfg
+
+
+def test_cfg3_matvec_sampled_rows(mapi_lib, orc, cfg3_device):
+    """Full BASELINE size (32768^2, 4 GiB) in the bench launch configuration: T1 on 512 sampled
+    rows of one mat-vec from the b0 start and from a rough iterate."""
+    m = mapi_lib
+    A = cfg3_device["A"]
+    n = A.shape[0]
+    r = np.random.default_rng(0)
+    rows = np.sort(r.choice(n, 512, replace=False))
+    A_rows = A[torch.from_numpy(rows).cuda()].cpu().numpy()
+    for x in (cfg3_device["b0"], (r.standard_normal(n) / n).astype(np.float32)):
+        y = m.mavp_matvec(A, torch.from_numpy(x).cuda()).cpu().numpy()
+        y_orc, mag = orc.matvec(A_rows, x, return_mag=True)
+        _t1(y[rows], y_orc, mag)
+
+
+def test_cfg3_last_step_and_invariants(mapi_lib, orc, cfg3_device):
+    """cfg3 as bench.py runs it (100 iterations, persistent kernel): the GPU's 100th iterate must
+    equal the oracle's fp64 step applied to the GPU's own 99th iterate (per-element T1-scaled bound),
+    s_99 must match, ||w||_1 = 1, and the run is bitwise reproducible."""
+    m = mapi_lib
+    A = cfg3_device["A"]
+    b0 = torch.from_numpy(cfg3_device["b0"]).cuda()
+    r100 = m.iterate(A, b0, 100)
+    r99 = m.iterate(A, b0, 99)
+    assert torch.equal(r100.norms[:99], r99.norms)
+    w99 = r99.w.cpu().numpy()
+    A_host = A.cpu().numpy()
+    y, mag = orc.matvec(A_host, w99, return_mag=True)
+    s = np.abs(y).sum()
+    assert abs(float(r100.norms[99]) - s) <= 1e-5 * s
+    w100 = r100.w.cpu().numpy().astype(np.float64)
+    err = np.abs(w100 - y / s)
+    assert np.all(err <= 1e-5 * mag / s + 2e-5 * np.abs(y / s)), float(np.max(err))
+    assert abs(np.abs(w100).sum() - 1.0) < 1e-5
+    r100b = m.iterate(A, b0, 100)
+    assert torch.equal(r100.w, r100b.w)
