@@ -180,7 +180,7 @@ def run_mapi(args, rank, world, local_rank):
 
         bytes_per_launch = dense_bytes_per_iter(n, lda) * iters
         units_per_step = iters
-        kernel_name = "k_iterate_persistent (K2, 1 cooperative launch = 100 iterations)"
+        kernel_name = "k_iterate_coop (K2c, 1 cooperative launch = all iterations of the step)"
         cfg_out = {"workload": f"{args.workload}: {WORKLOADS[args.workload]}", "n": n, "lda": lda,
                    "iters_per_step": iters, "op": "min1",
                    "l2_flush": ("inputs larger than L2 (4 GiB matrix vs 126 MB L2)" if args.workload == "cfg3"

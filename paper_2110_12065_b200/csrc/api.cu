@@ -159,7 +159,7 @@ constexpr int kMaxGrid = 1024;
 constexpr int kIterThreads = 512;
 
 size_t iterate_ws_bytes(int64_t n) {
-    return 256 + align256(sizeof(float) * 2 * kMaxGrid) + align256(sizeof(float) * 2 * (size_t)n) +
+    return 256 + align256(sizeof(double) * 2 * kMaxGrid) + align256(sizeof(float) * 2 * (size_t)n) +
            align256(sizeof(float) * (size_t)n);
 }
 
@@ -179,20 +179,39 @@ IterWs carve_iterate(void* ws, int64_t n) {
     w.status = reinterpret_cast<int32_t*>(p + 64);
     w.stop = reinterpret_cast<int32_t*>(p + 72);
     p += 256;
-    w.slots = reinterpret_cast<float*>(p);
-    p += align256(sizeof(float) * 2 * kMaxGrid);
+    w.slots = reinterpret_cast<float*>(p);  // holds 2 x kMaxGrid doubles
+    p += align256(sizeof(double) * 2 * kMaxGrid);
     w.y = reinterpret_cast<float*>(p);
     p += align256(sizeof(float) * 2 * (size_t)n);
     w.w = reinterpret_cast<float*>(p);
     return w;
 }
 
-size_t persistent_smem_bytes(int64_t n) { return sizeof(float) * (size_t)(((n + 3) & ~int64_t(3)) + 33); }
+size_t persistent_smem_bytes(int64_t n) { return sizeof(float) * (size_t)((n + 3) & ~int64_t(3)) + sizeof(double) * 33; }
+
+// Dense path selection (K2): "coop" (CTA-cooperative rows, default when A rows are
+// 32 B-aligned and n >= 16 chunks of 256), "rows" (one warp per row; any alignment, small n),
+// "multi" (two launches per iteration, any n).  MAPI_DENSE_PATH=coop|rows|multi forces one
+// (investigation / tests); a forced path that cannot run falls back in the order above.
+const char* dense_path_env() {
+    const char* e = getenv("MAPI_DENSE_PATH");
+    return e ? e : "";
+}
 
 bool use_persistent(const Device& d, int64_t n) {
-    const char* e = getenv("MAPI_DENSE_PATH");
-    if (e && strcmp(e, "multi") == 0) return false;
+    if (strcmp(dense_path_env(), "multi") == 0) return false;
     return persistent_smem_bytes(n) <= (size_t)d.smem_optin;
+}
+
+int coop_warps(int64_t n) { return (n / 256) >= 64 ? 32 : 16; }
+
+bool use_coop(const Device& d, const float* A, int64_t n, int64_t lda) {
+    const char* e = dense_path_env();
+    if (strcmp(e, "rows") == 0 || strcmp(e, "multi") == 0) return false;
+    if (vec_width(A, lda) != 8) return false;
+    if (strcmp(e, "coop") != 0 && n / 256 < 16) return false;
+    const int64_t grid = std::min<int64_t>(d.sms, n);
+    return coop_smem_bytes(n, (int)grid, coop_warps(n)) <= (size_t)d.smem_optin;
 }
 
 // Runs MAPI on device buffers; no stream sync, no status read-back (caller does both).
@@ -202,6 +221,43 @@ mapi_status iterate_launch(const Device& d, int32_t op, const float* A, int64_t 
     const int vec = vec_width(A, lda);
     const int pol = load_policy(d, n, lda);
     MAPI_CUDA(cudaMemsetAsync(W.bar, 0, 256, s));
+    if (use_coop(d, A, n, lda)) {
+        mapi_status st = MAPI_OK;
+        auto launch = [&](auto kern, int nw) {
+            const int threads = nw * 32;
+            // 1 CTA per SM (shared memory holds w); grid <= n so every CTA owns >= 1 row
+            const int grid = (int)std::min<int64_t>({(int64_t)d.sms, n, (int64_t)kMaxGrid});
+            const size_t smem = coop_smem_bytes(n, grid, nw);
+            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            int occ = 0;
+            if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
+            if (e != cudaSuccess || occ < 1) {
+                st = fail(MAPI_ERR_CUDA, "coop kernel occupancy query failed: %s", cudaGetErrorString(e));
+                return 0;
+            }
+            IterArgs a;
+            a.A = A; a.n = n; a.lda = lda; a.b0 = b0; a.iters = iters; a.tol = tol;
+            a.w_out = w_out; a.norms = norms; a.deltas = deltas; a.y = W.y; a.slots = W.slots;
+            a.bar = W.bar; a.status = W.status;
+            void* args[] = {&a};
+            if (timer) timer->start();
+            e = cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(threads), args, smem, s);
+            if (timer) timer->stop();
+            g_launches.fetch_add(1, std::memory_order_relaxed);
+            if (e != cudaSuccess)
+                st = fail(MAPI_ERR_CUDA, "cooperative launch (grid %d, smem %zu): %s", grid, smem,
+                          cudaGetErrorString(e));
+            return 0;
+        };
+        const int nw = coop_warps(n);
+        with_op(op, [&](auto OPc) {
+            return with_pol(pol, [&](auto POLc) {
+                constexpr int OP = decltype(OPc)::value, POL = decltype(POLc)::value;
+                return nw == 32 ? launch(k_iterate_coop<OP, POL, 32>, 32) : launch(k_iterate_coop<OP, POL, 16>, 16);
+            });
+        });
+        return st;
+    }
     if (use_persistent(d, n)) {
         mapi_status st = MAPI_OK;
         with_op(op, [&](auto OPc) {
@@ -598,13 +654,9 @@ mapi_status mapi_rank_csr(int64_t n, int64_t nnz, const int32_t* row_ptr, const 
     if ((st = device_info(d)) != MAPI_OK) return st;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     Timer timer(s);
-    st = csr_rank_run(n, nnz, row_ptr, col_idx, cap, bg, b0, max_iters, tol, w_out, deltas, ws, d.sms, s,
+    st = csr_rank_run(n, nnz, row_ptr, col_idx, cap, bg, b0, max_iters, tol, w_out, w_l2_out, deltas, ws, d.sms, s,
                       timer.on ? &timer.a : nullptr, timer.on ? &timer.b : nullptr, g_launches);
     if (st != MAPI_OK) return fail(st, "%s", csr_last_error());
-    if (w_l2_out) {
-        k_l2_copy<<<1, 1024, 0, s>>>(n, w_out, w_l2_out);
-        MAPI_LAUNCHED();
-    }
     st = csr_rank_finish(ws, n, nnz, s, iters_done);
     timer.harvest();
     if (st == MAPI_ERR_CUDA) return fail(st, "%s", csr_last_error());

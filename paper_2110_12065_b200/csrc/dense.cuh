@@ -17,16 +17,22 @@ namespace mapi {
 
 constexpr int kFold = 128;  // max fp32 terms per accumulator chain before folding
 
+// L2 bulk prefetch of `bytes` (multiple of 16) starting at 16 B-aligned `p` (no register cost).
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 // Row MAVP: sum_k a[k] (+) w[k] for k < n, by one warp. Returns the same value in all lanes.
-// a must be VEC*4-byte aligned; w (smem or global) likewise.
-template <int OP, int VEC, int POL, bool WG, int U>
+// a must be VEC*4-byte aligned; w (smem or global) likewise.  U = warp-wide loads in flight per
+// lane; PF > 0: lane 0 also bulk-prefetches into L2 the U-step group PF groups ahead (same row).
+// Summation order: per lane VEC chains of <= kFold terms, pairwise tree over the VEC slots, the
+// blocks of kFold steps added in order, the scalar tail, then the warp butterfly.
+template <int OP, int VEC, int POL, bool WG, int U, int PF = 0>
 __device__ __forceinline__ float row_mavp(const float* __restrict__ a, const float* __restrict__ w,
                                           int64_t n, int lane) {
     constexpr int STEP = kWarp * VEC;
     const int64_t n_main = (n / STEP) * STEP;
-    float tot[VEC];
-#pragma unroll
-    for (int i = 0; i < VEC; ++i) tot[i] = 0.0f;
+    float tot = 0.0f;
 
     for (int64_t blk = 0; blk < n_main; blk += (int64_t)kFold * STEP) {
         const int64_t blk_end = min(n_main, blk + (int64_t)kFold * STEP);
@@ -36,6 +42,11 @@ __device__ __forceinline__ float row_mavp(const float* __restrict__ a, const flo
         int64_t c = blk + lane * VEC;
         const int64_t base_end = blk_end - (int64_t)(U - 1) * STEP;  // warp-uniform bound
         for (; c - lane * VEC < base_end; c += (int64_t)U * STEP) {
+            if constexpr (PF > 0) {
+                const int64_t pf = c - lane * VEC + (int64_t)PF * U * STEP;
+                if (lane == 0 && pf + (int64_t)U * STEP <= n_main)
+                    prefetch_l2(a + pf, (uint32_t)(U * STEP * sizeof(float)));
+            }
             float v[U][VEC];
 #pragma unroll
             for (int u = 0; u < U; ++u) ld_stream<VEC, POL>(a + c + u * STEP, v[u]);
@@ -54,8 +65,7 @@ __device__ __forceinline__ float row_mavp(const float* __restrict__ a, const flo
 #pragma unroll
             for (int i = 0; i < VEC; ++i) acc[i] += mavp_term<OP>(v[i], x[i]);
         }
-#pragma unroll
-        for (int i = 0; i < VEC; ++i) tot[i] += acc[i];
+        tot += tree_sum(acc);
     }
     // ragged tail (< STEP elements): scalar loads, at most VEC terms per lane
     float tail = 0.0f;
@@ -64,7 +74,7 @@ __device__ __forceinline__ float row_mavp(const float* __restrict__ a, const flo
         ld_stream<1, POL>(a + k, v);
         tail += mavp_term<OP>(v[0], WG ? __ldg(w + k) : w[k]);
     }
-    return warp_sum(tree_sum(tot) + tail);
+    return warp_sum(tot + tail);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -110,11 +120,11 @@ struct IterArgs {
 // status codes (mirror mapi_status)
 constexpr int kStOk = 0, kStDegenerate = 4, kStNonfinite = 6;
 
-template <int OP, int VEC, int POL, int U>
+template <int OP, int VEC, int POL, int U, int PF = 0, int PH = 0>
 __global__ void __launch_bounds__(512, 1) k_iterate_persistent(IterArgs p) {
     extern __shared__ __align__(16) float ws_[];
-    float* w_s = ws_;                                // n floats (the current iterate w_t)
-    float* red = ws_ + ((p.n + 3) & ~int64_t(3));    // 33 floats of reduction scratch
+    float* w_s = ws_;                                                    // n floats (w_t)
+    double* red = reinterpret_cast<double*>(ws_ + ((p.n + 3) & ~int64_t(3)));  // 33 doubles
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
     const int64_t n = p.n;
 
@@ -128,24 +138,28 @@ __global__ void __launch_bounds__(512, 1) k_iterate_persistent(IterArgs p) {
     for (int32_t t = 0; t < p.iters; ++t) {
         float* y = p.y + (t & 1) * n;
         // ---- rows -> y, |y| partial (a1, a2)
-        float abs_part = 0.0f;
+        double abs_part = 0.0;
         for (int64_t row = gwarp; row < n; row += total_warps) {
-            const float v = row_mavp<OP, VEC, POL, false, U>(p.A + row * p.lda, w_s, n, lane);
+            if constexpr (PH > 0) {  // warm L2 with the head of this warp's next row
+                const int64_t nxt = row + total_warps;
+                if (lane == 0 && nxt < n)
+                    prefetch_l2(p.A + nxt * p.lda, (uint32_t)min((int64_t)PH * 1024, (n * 4) & ~int64_t(15)));
+            }
+            const float v = row_mavp<OP, VEC, POL, false, U, PF>(p.A + row * p.lda, w_s, n, lane);
             if (lane == 0) y[row] = v;
-            abs_part += fabsf(v);
+            abs_part += (double)fabsf(v);
         }
-        const float cta_abs = block_sum(lane == 0 ? abs_part : 0.0f, red);
-        if (tid == 0) p.slots[(t & 1) * gridDim.x + blockIdx.x] = cta_abs;
+        const double cta_abs = block_sum(lane == 0 ? abs_part : 0.0, red);
+        double* slots = reinterpret_cast<double*>(p.slots);
+        if (tid == 0) slots[(t & 1) * gridDim.x + blockIdx.x] = cta_abs;
         grid_barrier(p.bar, (unsigned int)(t + 1) * gridDim.x);
 
-        // ---- s_t = ||y||_1 from the per-CTA partials, same fixed order in every CTA (a3)
-        float s;
+        // ---- s_t = ||y||_1 from the per-CTA partials, same fixed fp64 order in every CTA (a3)
+        double s;
         {
-            float part = 0.0f;
-            if (warp == 0)
-                for (int c = lane; c < (int)gridDim.x; c += 32)
-                    part += ld_cg(p.slots + (t & 1) * gridDim.x + c);
             if (warp == 0) {
+                double part = 0.0;
+                for (int c = lane; c < (int)gridDim.x; c += 32) part += __ldcg(slots + (t & 1) * gridDim.x + c);
                 part = warp_sum(part);
                 if (lane == 0) red[32] = part;
             }
@@ -153,24 +167,24 @@ __global__ void __launch_bounds__(512, 1) k_iterate_persistent(IterArgs p) {
             s = red[32];
             __syncthreads();
         }
-        if (!(s > 0.0f) || isinf(s)) {  // uniform across the grid (same s everywhere)
-            status = (s == 0.0f) ? kStDegenerate : kStNonfinite;
+        if (!(s > 0.0) || isinf(s)) {  // uniform across the grid (same s everywhere)
+            status = (s == 0.0) ? kStDegenerate : kStNonfinite;
             break;
         }
-        // ---- w_{t+1} = y / s_t (IEEE division, a4), delta_t (a5)
-        float dpart = 0.0f;
+        // ---- w_{t+1} = fp32(y / s_t) (division in fp64, a4), delta_t in fp64 (a5)
+        double dpart = 0.0;
         for (int64_t k = tid; k < n; k += blockDim.x) {
-            const float wn = ld_cg(y + k) / s;
-            dpart += fabsf(wn - w_s[k]);
+            const float wn = (float)((double)ld_cg(y + k) / s);
+            dpart += (double)fabsf(wn - w_s[k]);
             w_s[k] = wn;
         }
-        const float delta = block_sum(dpart, red);  // also orders the w_s writes before reuse
+        const double delta = block_sum(dpart, red);  // also orders the w_s writes before reuse
         if (blockIdx.x == 0 && tid == 0) {
-            if (p.norms) p.norms[t] = s;
-            if (p.deltas) p.deltas[t] = delta;
+            if (p.norms) p.norms[t] = (float)s;
+            if (p.deltas) p.deltas[t] = (float)delta;
         }
         done = t + 1;
-        if (p.tol > 0.0f && delta < p.tol) break;
+        if (p.tol > 0.0f && delta < (double)p.tol) break;
     }
     // ---- final iterate out: CTA c writes its slice of its (identical) copy
     const int64_t per = (n + gridDim.x - 1) / gridDim.x;
@@ -183,6 +197,159 @@ __global__ void __launch_bounds__(512, 1) k_iterate_persistent(IterArgs p) {
 }
 
 // ---------------------------------------------------------------------------------------------
+// K2c: CTA-cooperative persistent MAPI iteration (the default dense path; K2).
+//
+// Rows are dealt to CTAs round-robin (row = cta + k*grid) and the NW warps of a CTA split every row
+// into NW contiguous runs of 1 KB chunks, so at any moment the grid streams a compact window of
+// ~grid consecutive rows (measured: 7.22 TB/s read ceiling for this pattern vs 7.00 TB/s for one
+// row per warp scattered over the matrix).  Each warp's chunk loads (one LDG.256 per lane) are
+// software-pipelined over its (row, chunk) sequence with a register double buffer, so row ends
+// never drain the load queue, and the first load of iteration t+1 is issued before the grid
+// barrier of iteration t (A does not depend on w).  Per row the NW warp partials go to shared
+// memory and are summed in warp order after the rows loop.  The n % 256 ragged tail of each row is
+// handled by the last warp with scalar loads.  Requires a 32 B-aligned A and lda % 8 == 0.
+//
+// Numerics: fp32 MAVP terms and row sums (per lane 8 chains of <= ceil(C/NW) terms, tree, butterfly,
+// NW warp partials in order); s_t and delta_t are accumulated in fp64 (fixed order), and
+// w_{t+1} = fp32(y / s_t) with the division in fp64, so w carries no common-mode rounding of s_t.
+template <int OP, int POL, int NW>
+__global__ void __launch_bounds__(NW * 32, 1) k_iterate_coop(IterArgs p) {
+    constexpr int STEP = 256;  // floats per warp-wide LDG.256 (one 1 KB chunk)
+    extern __shared__ __align__(16) float ws_[];
+    const int64_t n = p.n;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t rows_cta = (n - blockIdx.x + gridDim.x - 1) / gridDim.x;  // rows c, c+G, ...
+    float* w_s = ws_;                                                        // n (+pad) floats
+    float* part = ws_ + ((n + 7) & ~int64_t(7));                             // rows_cta * NW
+    double* red = reinterpret_cast<double*>(part + ((rows_cta * NW + 1) & ~int64_t(1)));  // 33 doubles
+    const int64_t cfull = n / STEP;                     // full chunks per row
+    const int c0 = (int)(warp * cfull / NW), c1 = (int)((warp + 1) * cfull / NW);
+    const int spr = c1 - c0;                            // this warp's chunks per row
+    const int nsteps = (int)rows_cta * spr;
+    const int64_t tail0 = cfull * STEP;                 // ragged tail [tail0, n), last warp
+    const bool has_tail = tail0 < n && warp == NW - 1;
+    const int64_t rstride = (int64_t)gridDim.x * p.lda;
+    const float* abase = p.A + (int64_t)blockIdx.x * p.lda + (int64_t)c0 * STEP + lane * 8;
+
+    for (int64_t k = tid; k < n; k += blockDim.x) w_s[k] = p.b0[k];
+
+    float bufA[8], bufB[8], acc[8];
+    int lr = 0, lq = 0;  // (row, chunk) of the next load
+    auto load = [&](float (&b)[8]) {
+        ld_stream<8, POL>(abase + lr * rstride + (int64_t)lq * STEP, b);
+        if (++lq == spr) { lq = 0; ++lr; }
+    };
+    if (nsteps > 0) load(bufA);  // first load of iteration 0 (overlaps the w staging)
+    __syncthreads();
+    int32_t done = 0, status = kStOk;
+
+    for (int32_t t = 0; t < p.iters; ++t) {
+        float* y = p.y + (t & 1) * n;
+        int cr = 0, cq = 0;  // (row, chunk) of the next consume
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
+        auto finish_row = [&]() {
+            float v = tree_sum(acc);
+            if (has_tail) {  // n % 256 elements of row (blockIdx.x + cr*G), scalar
+                const float* a = p.A + ((int64_t)blockIdx.x + (int64_t)cr * gridDim.x) * p.lda;
+                for (int64_t k = tail0 + lane; k < n; k += 32) {
+                    float x[1];
+                    ld_stream<1, POL>(a + k, x);
+                    v += mavp_term<OP>(x[0], w_s[k]);
+                }
+            }
+            v = warp_sum(v);
+            if (lane == 0) part[cr * NW + warp] = v;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
+        };
+        auto consume = [&](const float (&b)[8]) {
+            float x[8];
+            ld_vec<8, false>(w_s + (int64_t)(c0 + cq) * STEP + lane * 8, x);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) acc[i] += mavp_term<OP>(b[i], x[i]);
+            if (++cq == spr) {
+                finish_row();
+                cq = 0;
+                ++cr;
+            }
+        };
+        // ---- rows (a1, a2): bufA already holds step 0
+        int s = 0;
+        for (; s + 1 < nsteps; s += 2) {
+            load(bufB);
+            consume(bufA);
+            if (s + 2 < nsteps) load(bufA);
+            consume(bufB);
+        }
+        if (s < nsteps) consume(bufA);
+        if (spr == 0)  // no full chunk for this warp: zero partials (+ the tail if it owns it)
+            for (cr = 0; cr < (int)rows_cta; ++cr) finish_row();
+        lr = 0;
+        lq = 0;
+        if (nsteps > 0 && t + 1 < p.iters) load(bufA);  // next iteration's first chunk, in flight
+        __syncthreads();
+        // ---- y rows of this CTA (NW partials in warp order), fp64 |y| partial (a3)
+        double abs_part = 0.0;
+        for (int64_t r = tid; r < rows_cta; r += blockDim.x) {
+            float v = 0.0f;
+#pragma unroll 8
+            for (int q = 0; q < NW; ++q) v += part[r * NW + q];
+            y[blockIdx.x + r * gridDim.x] = v;
+            abs_part += (double)fabsf(v);
+        }
+        const double cta_abs = block_sum(abs_part, red);
+        double* slots = reinterpret_cast<double*>(p.slots);
+        if (tid == 0) slots[(t & 1) * gridDim.x + blockIdx.x] = cta_abs;
+        grid_barrier(p.bar, (unsigned int)(t + 1) * gridDim.x);
+        // ---- s_t: the same fixed-order fp64 sum in every CTA
+        double sd;
+        {
+            if (warp == 0) {
+                double pp = 0.0;
+                for (int c = lane; c < (int)gridDim.x; c += 32) pp += __ldcg(slots + (t & 1) * gridDim.x + c);
+                pp = warp_sum(pp);
+                if (lane == 0) red[32] = pp;
+            }
+            __syncthreads();
+            sd = red[32];
+            __syncthreads();
+        }
+        if (!(sd > 0.0) || isinf(sd)) {  // uniform across the grid
+            status = (sd == 0.0) ? kStDegenerate : kStNonfinite;
+            break;
+        }
+        // ---- w_{t+1} = y / s_t (a4), delta_t (a5), staged into this CTA's shared memory
+        double dpart = 0.0;
+        for (int64_t k = tid; k < n; k += blockDim.x) {
+            const float wn = (float)((double)ld_cg(y + k) / sd);
+            dpart += (double)fabsf(wn - w_s[k]);
+            w_s[k] = wn;
+        }
+        const double delta = block_sum(dpart, red);  // its barriers also publish w_s
+        if (blockIdx.x == 0 && tid == 0) {
+            if (p.norms) p.norms[t] = (float)sd;
+            if (p.deltas) p.deltas[t] = (float)delta;
+        }
+        done = t + 1;
+        if (p.tol > 0.0f && delta < (double)p.tol) break;
+    }
+    const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+    const int64_t k0 = (int64_t)blockIdx.x * per, k1 = min(n, k0 + per);
+    for (int64_t k = k0 + tid; k < k1; k += blockDim.x) p.w_out[k] = w_s[k];
+    if (blockIdx.x == 0 && tid == 0) {
+        p.status[0] = status;
+        p.status[1] = done;
+    }
+}
+
+inline size_t coop_smem_bytes(int64_t n, int grid, int nw) {
+    const int64_t rows_cta = (n + grid - 1) / grid;
+    return sizeof(float) * (size_t)(((n + 7) & ~int64_t(7)) + ((rows_cta * nw + 1) & ~int64_t(1))) +
+           sizeof(double) * 33;
+}
+
+// ---------------------------------------------------------------------------------------------
 // Multi-launch path (any n; also the CUDA-graph-style comparator): per iteration
 //   k_rows_partial: y = A (+) w (w in global, L1-cached), per-CTA sum|y| -> slots
 //   k_normalize   : 1 CTA; s = sum slots; w = y/s; delta; trace; stop flag
@@ -192,18 +359,18 @@ __global__ void __launch_bounds__(512, 1) k_rows_partial(const float* __restrict
                                                       int64_t lda, const float* __restrict__ w,
                                                       float* __restrict__ y, float* __restrict__ slots,
                                                       const int32_t* __restrict__ stop) {
-    __shared__ float red[33];
+    __shared__ double red[33];
     if (*(volatile const int32_t*)stop) return;
     const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     const int64_t total_warps = (int64_t)gridDim.x * nw;
-    float abs_part = 0.0f;
+    double abs_part = 0.0;
     for (int64_t row = (int64_t)blockIdx.x * nw + (threadIdx.x >> 5); row < n; row += total_warps) {
         const float v = row_mavp<OP, VEC, POL, true, U>(A + row * lda, w, n, lane);
         if (lane == 0) y[row] = v;
-        abs_part += fabsf(v);
+        abs_part += (double)fabsf(v);
     }
-    const float cta_abs = block_sum(lane == 0 ? abs_part : 0.0f, red);
-    if (threadIdx.x == 0) slots[blockIdx.x] = cta_abs;
+    const double cta_abs = block_sum(lane == 0 ? abs_part : 0.0, red);
+    if (threadIdx.x == 0) reinterpret_cast<double*>(slots)[blockIdx.x] = cta_abs;
 }
 
 __global__ void __launch_bounds__(1024) k_normalize(int64_t n, const float* __restrict__ y,
@@ -211,38 +378,38 @@ __global__ void __launch_bounds__(1024) k_normalize(int64_t n, const float* __re
                                                     float* __restrict__ w, int32_t t, float tol,
                                                     float* norms, float* deltas, int32_t* status,
                                                     int32_t* stop) {
-    __shared__ float red[33];
+    __shared__ double red[33];
     if (*(volatile int32_t*)stop) return;
-    float part = 0.0f;
-    if (threadIdx.x < 32)
-        for (int c = threadIdx.x; c < n_slots; c += 32) part += slots[c];
+    const double* dslots = reinterpret_cast<const double*>(slots);
     if (threadIdx.x < 32) {
+        double part = 0.0;
+        for (int c = threadIdx.x; c < n_slots; c += 32) part += dslots[c];
         part = warp_sum(part);
         if (threadIdx.x == 0) red[32] = part;
     }
     __syncthreads();
-    const float s = red[32];
+    const double s = red[32];
     __syncthreads();
-    if (!(s > 0.0f) || isinf(s)) {
+    if (!(s > 0.0) || isinf(s)) {
         if (threadIdx.x == 0) {
-            status[0] = (s == 0.0f) ? kStDegenerate : kStNonfinite;
+            status[0] = (s == 0.0) ? kStDegenerate : kStNonfinite;
             status[1] = t;
             *stop = 1;
         }
         return;
     }
-    float dpart = 0.0f;
+    double dpart = 0.0;
     for (int64_t k = threadIdx.x; k < n; k += blockDim.x) {
-        const float wn = y[k] / s;
-        dpart += fabsf(wn - w[k]);
+        const float wn = (float)((double)y[k] / s);
+        dpart += (double)fabsf(wn - w[k]);
         w[k] = wn;
     }
-    const float delta = block_sum(dpart, red);
+    const double delta = block_sum(dpart, red);
     if (threadIdx.x == 0) {
-        if (norms) norms[t] = s;
-        if (deltas) deltas[t] = delta;
+        if (norms) norms[t] = (float)s;
+        if (deltas) deltas[t] = (float)delta;
         status[1] = t + 1;
-        if (tol > 0.0f && delta < tol) *stop = 1;
+        if (tol > 0.0f && delta < (double)tol) *stop = 1;
     }
 }
 

@@ -1,0 +1,143 @@
+"""GPU parity of mapi_csr_prepare + mapi_rank_csr (MAPI ranking on the Google matrix, Eq. 13,
+P:305-312) against the oracle's rank_csr (itself pinned to the dense G brute force).
+
+T2 on the l2 copy (|cos| >= 1 - 1e-6, max|diff| <= 1e-4) after a fixed iteration count, and
+T3 on rankings: with O / G the oracle / GPU top-100 (ties by index), every id in O symmetric-
+difference G must be within 1e-6 (relative) of the oracle's 100th score (reading Q16).
+"""
+import numpy as np
+import pytest
+import torch
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+def _dev(a, dtype=None):
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    if dtype is not None:
+        t = t.to(dtype)
+    return t.cuda()
+
+
+def _t2(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    a, b = a / np.linalg.norm(a), b / np.linalg.norm(b)
+    assert abs(float(a @ b)) >= 1 - 1e-6
+    assert np.max(np.abs(a - b)) <= 1e-4
+
+
+def _t3(orc, w_gpu, w_orc, k=100):
+    k = min(k, w_orc.size)
+    O = orc.rank_order(w_orc)[:k]
+    G = orc.rank_order(np.asarray(w_gpu, np.float64))[:k]
+    kth = w_orc[O[-1]]
+    for i in set(O.tolist()) ^ set(G.tolist()):
+        assert abs(w_orc[i] - kth) <= 1e-6 * kth, f"id {i}: {w_orc[i]} vs 100th {kth}"
+
+
+def _run(m, n, row_ptr, col_idx, b0, iters, tol, alpha=0.85):
+    rp = _dev(row_ptr, torch.int32)
+    ci = _dev(col_idx.astype(np.int32)) if col_idx.size else torch.empty(0, dtype=torch.int32, device="cuda")
+    cap, bg = m.csr_prepare(n, rp, ci, alpha)
+    return m.rank_csr(n, rp, ci, cap, bg, _dev(b0.astype(np.float32)), iters, tol), cap, bg
+
+
+def test_prepare_exact(mapi_lib):
+    m = mapi_lib
+    edges, row_ptr, col_idx = synth.random_graph(150, 0.05, seed=3, n_dangling=20)
+    _, cap, bg = _run(m, 150, row_ptr, col_idx, np.full(150, 1 / 150), 1, 0.0)
+    outdeg = np.bincount(edges[:, 0], minlength=150)
+    a = np.float32(0.85)
+    with np.errstate(divide="ignore"):
+        cap_ref = np.where(outdeg > 0, a / outdeg.astype(np.float32), np.float32(0)).astype(np.float32)
+    bg_ref = np.where(outdeg > 0, (np.float32(1) - a) / np.float32(150), np.float32(1) / np.float32(150))
+    assert np.array_equal(cap.cpu().numpy(), cap_ref)
+    assert np.array_equal(bg.cpu().numpy(), bg_ref.astype(np.float32))
+
+
+@pytest.mark.parametrize("trial", range(12))
+def test_rank_random_graphs(mapi_lib, orc, trial):
+    m = mapi_lib
+    r = np.random.default_rng(trial)
+    n = int(r.integers(2, 400))
+    edges, row_ptr, col_idx = synth.random_graph(n, float(r.uniform(0.005, 0.1)), seed=trial,
+                                                 n_dangling=int(r.integers(0, n // 3 + 1)))
+    b0 = np.full(n, 1.0 / n)
+    res, _, _ = _run(m, n, row_ptr, col_idx, b0, 15, 0.0)
+    ref = orc.rank_csr(n, row_ptr, col_idx, b0=b0.astype(np.float32), max_iters=15, tol=0.0)
+    assert res.iters_done == ref.iters_done == 15
+    _t2(res.w_l2.cpu().numpy(), ref.w)
+    np.testing.assert_allclose(res.w.cpu().numpy(), ref.w, rtol=2e-5, atol=1e-9)
+    np.testing.assert_allclose(res.deltas.cpu().numpy(), ref.deltas, rtol=1e-2, atol=2e-7)
+    _t3(orc, res.w.cpu().numpy(), ref.w, k=min(20, n))
+
+
+def test_rank_gnutella_like_converged(mapi_lib, orc):
+    m = mapi_lib
+    g = synth.gnutella_like()
+    n = g["n"]
+    res, _, _ = _run(m, n, g["row_ptr"], g["col_idx"], g["b0"], 200, 1e-7)
+    ref = orc.rank_csr(n, g["row_ptr"], g["col_idx"], b0=g["b0"], max_iters=200, tol=1e-7)
+    assert abs(res.iters_done - ref.iters_done) <= 1  # fp32 vs fp64 may stop one step apart (F6)
+    _t2(res.w_l2.cpu().numpy(), ref.w)
+    _t3(orc, res.w.cpu().numpy(), ref.w)
+
+
+def test_rank_no_edges_uniform(mapi_lib):
+    m = mapi_lib
+    n = 100
+    row_ptr = np.zeros(n + 1, np.int64)
+    r = np.random.default_rng(1)
+    b0 = r.random(n)
+    b0 /= b0.sum()
+    res, cap, bg = _run(m, n, row_ptr, np.zeros(0, np.int32), b0, 3, 0.0)
+    assert np.all(cap.cpu().numpy() == 0)
+    np.testing.assert_allclose(res.w.cpu().numpy(), np.full(n, 1.0 / n), rtol=1e-6)
+
+
+def test_rank_star_hub_first(mapi_lib, orc):
+    m = mapi_lib
+    n = 50
+    row_ptr, col_idx = synth.csr_by_destination(n, np.arange(1, n), np.zeros(n - 1, np.int64))
+    res, _, _ = _run(m, n, row_ptr, col_idx, np.full(n, 1.0 / n), 20, 0.0)
+    assert int(np.argmax(res.w.cpu().numpy())) == 0
+
+
+def test_rank_negative_start(mapi_lib):
+    m = mapi_lib
+    row_ptr, col_idx = synth.csr_by_destination(3, np.array([0, 1]), np.array([1, 2]))
+    with pytest.raises(m.MapiError) as ei:
+        _run(m, 3, row_ptr, col_idx, np.array([0.5, -0.1, 0.6]), 5, 0.0)
+    assert ei.value.name == "MAPI_ERR_NEGATIVE"
+
+
+def test_rank_deterministic(mapi_lib):
+    m = mapi_lib
+    g = synth.gnutella_like()
+    a, _, _ = _run(m, g["n"], g["row_ptr"], g["col_idx"], g["b0"], 30, 0.0)
+    b, _, _ = _run(m, g["n"], g["row_ptr"], g["col_idx"], g["b0"], 30, 0.0)
+    assert torch.equal(a.w, b.w) and torch.equal(a.deltas, b.deltas)
+
+
+@pytest.fixture(scope="module")
+def cfg5():
+    return synth.cfg5()
+
+
+def test_cfg5_full_size(mapi_lib, orc, cfg5):
+    """BASELINE configs[4] at full size: tol 1e-7 / 200 as specified (T3 top-100), and a fixed
+    10-iteration run (T2 + T3) in the launch configuration bench uses."""
+    m = mapi_lib
+    n = cfg5["n"]
+    b0 = cfg5["b0"]
+    res, _, _ = _run(m, n, cfg5["row_ptr"], cfg5["col_idx"], b0, 200, 1e-7)
+    ref = orc.rank_csr(n, cfg5["row_ptr"], cfg5["col_idx"], b0=b0, max_iters=200, tol=1e-7)
+    assert abs(res.iters_done - ref.iters_done) <= 1
+    _t3(orc, res.w.cpu().numpy(), ref.w)
+    res10, _, _ = _run(m, n, cfg5["row_ptr"], cfg5["col_idx"], b0, 10, 0.0)
+    ref10 = orc.rank_csr(n, cfg5["row_ptr"], cfg5["col_idx"], b0=b0, max_iters=10, tol=0.0)
+    _t2(res10.w_l2.cpu().numpy(), ref10.w)
+    _t3(orc, res10.w.cpu().numpy(), ref10.w)
