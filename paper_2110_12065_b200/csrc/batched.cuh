@@ -11,6 +11,8 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
 #include "../../include/mapi.h"
 #include "mapi_common.cuh"
 
@@ -35,10 +37,11 @@ inline int batched_ksplit(int64_t n, int32_t k, int sms) {
 }
 
 // workspace: [hdr 256: unused][status 2k i32][stop k i32][W k*n][Y k*n][part KS*k*n][colpart k*RB]
+inline size_t batched_part_bytes(int64_t n, int32_t k);
 inline size_t batched_ws_bytes(int64_t n, int32_t k) {
     const int64_t rb = (n + 255) / 256;
     return 256 + bal256(8 * (size_t)k) + bal256(4 * (size_t)k) + 2 * bal256(4 * (size_t)k * n) +
-           bal256(4 * (size_t)64 * k * n) + bal256(4 * (size_t)k * rb);
+           bal256(batched_part_bytes(n, k)) + bal256(4 * (size_t)k * rb);
 }
 
 struct BatchedWs {
@@ -60,7 +63,7 @@ inline BatchedWs carve_batched(void* ws, int64_t n, int32_t k) {
     b.Y = reinterpret_cast<float*>(p);
     p += bal256(4 * (size_t)k * n);
     b.part = reinterpret_cast<float*>(p);
-    p += bal256(4 * (size_t)64 * k * n);
+    p += bal256(batched_part_bytes(n, k));
     b.colpart = reinterpret_cast<float*>(p);
     b.rb = (n + 255) / 256;
     return b;
@@ -198,8 +201,238 @@ __global__ void __launch_bounds__(1024) k_batched_normalize(int64_t n, int32_t k
     }
 }
 
+// ---------------------------------------------------------------------------------------------
+// K4 v2 (default when rows are 16 B aligned): stream-K persistent tiles.
+//
+// Work = (row tile of 256 rows) x (vector tile of 64) x (k stage of 32): U units, split into equal
+// contiguous ranges over G = #SMs CTAs (one CTA per SM), so every SM gets the same number of k-stages
+// (no wave quantisation).  A CTA accumulates consecutive stages of one tile in registers and writes
+// a partial tile when the tile (or its range) ends; k_batched_reduce2 adds the <= kMaxParts partials
+// of each tile in CTA order (deterministic).  Stages are staged global -> shared with cp.async
+// (16 B, zero-filled out of range) in a 3-deep ring.  Thread (tr, tv) = (lane, warp) owns rows
+// tr + 32 i and vectors tv + 8 j (i, j < 8): A reads are conflict-free LDS.128 across the warp, W
+// reads are warp-wide broadcasts.  Inner loop per term: FMNMX.XORSIGN + half an FADD2 (pairs of
+// vectors); accumulators are folded every kFoldStages stages into a second set (chains <= 128 terms).
+constexpr int kB2M = 256, kB2V = 64, kB2K = 32, kB2Threads = 256, kB2Stages = 3, kB2Ld = kB2K + 4;
+constexpr int kFoldStages = 4;  // 4 x 32 = 128 terms per fp32 chain before folding
+constexpr int kMaxParts = 8;
+
+struct StreamK {
+    int64_t row_tiles, vec_tiles, kstages, units;
+    int grid;
+};
+
+inline StreamK streamk_plan(int64_t n, int32_t k, int sms) {
+    StreamK p;
+    p.row_tiles = (n + kB2M - 1) / kB2M;
+    p.vec_tiles = (k + kB2V - 1) / kB2V;
+    p.kstages = (n + kB2K - 1) / kB2K;
+    p.units = p.row_tiles * p.vec_tiles * p.kstages;
+    p.grid = (int)std::min<int64_t>(sms, std::max<int64_t>(1, p.units));
+    return p;
+}
+
+// first CTA whose range [c*U/G, (c+1)*U/G) contains unit u
+__host__ __device__ inline int64_t streamk_cta_of(int64_t u, int64_t U, int64_t G) {
+    int64_t c = (u * G) / U;
+    while (c + 1 < G && ((c + 1) * U) / G <= u) ++c;
+    while (c > 0 && (c * U) / G > u) --c;
+    return c;
+}
+
+inline bool streamk_ok(int64_t n, int32_t k, int sms) {
+    const StreamK p = streamk_plan(n, k, sms);
+    const int64_t max_parts = (p.kstages * p.grid + p.units - 1) / p.units + 1;  // ranges spanning a tile
+    return max_parts <= kMaxParts;
+}
+
+__device__ __forceinline__ unsigned long long fadd2(unsigned long long a, unsigned long long b) {
+    unsigned long long d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ unsigned long long pack2(float lo, float hi) {
+    return ((unsigned long long)__float_as_uint(hi) << 32) | (unsigned long long)__float_as_uint(lo);
+}
+__device__ __forceinline__ float lo_of(unsigned long long x) { return __uint_as_float((unsigned)(x & 0xffffffffu)); }
+__device__ __forceinline__ float hi_of(unsigned long long x) { return __uint_as_float((unsigned)(x >> 32)); }
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <int OP>
+__global__ void __launch_bounds__(kB2Threads, 1) k_batched_streamk(const float* __restrict__ A, int64_t n, int64_t lda,
+                                                                   const float* __restrict__ W, int32_t kv,
+                                                                   StreamK plan, float* __restrict__ part) {
+    extern __shared__ __align__(16) float smem[];
+    float* As = smem;                                   // [stage][256][kB2Ld]
+    float* Ws = smem + kB2Stages * kB2M * kB2Ld;        // [stage][64][kB2Ld]
+    const int tid = threadIdx.x, tr = tid & 31, tv = tid >> 5;
+    const int64_t U = plan.units, G = gridDim.x;
+    const int64_t u0 = ((int64_t)blockIdx.x * U) / G, u1 = (((int64_t)blockIdx.x + 1) * U) / G;
+    if (u0 >= u1) return;
+
+    // load cursor: the (tile, k-stage) of the next stage to stage into shared memory
+    int64_t l_tile = u0 / plan.kstages, l_ks = u0 % plan.kstages;
+    const float* pA[8];  // this thread's 8 A chunk rows (tr8 + 32 i) of the current load tile
+    const float* pW[2];  // this thread's 2 W chunk rows (tr8 + 32 i)
+    uint32_t a_ok = 0, w_ok = 0;  // row-in-range masks
+    const int tr8 = tid >> 3, kq4 = (tid & 7) * 4;
+    auto set_tile = [&](int64_t tile) {
+        const int64_t rt = tile / plan.vec_tiles, vt = tile - rt * plan.vec_tiles;
+        const int64_t row0 = rt * kB2M, v0 = vt * kB2V;
+        a_ok = w_ok = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int64_t row = row0 + tr8 + 32 * i;
+            pA[i] = A + (row < n ? row : 0) * lda + kq4;
+            a_ok |= (row < n ? 1u : 0u) << i;
+        }
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const int64_t v = v0 + tr8 + 32 * i;
+            pW[i] = W + (v < kv ? v : 0) * n + kq4;
+            w_ok |= (v < kv ? 1u : 0u) << i;
+        }
+    };
+    set_tile(l_tile);
+    auto load_next = [&](int slot) {
+        const int64_t k0 = l_ks * kB2K;
+        const bool k_in = k0 + kq4 < n;
+        float* as = As + slot * kB2M * kB2Ld + tr8 * kB2Ld + kq4;
+        float* ws = Ws + slot * kB2V * kB2Ld + tr8 * kB2Ld + kq4;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const bool in = k_in && ((a_ok >> i) & 1u);
+            cp_async16(as + 32 * i * kB2Ld, in ? (const void*)(pA[i] + k0) : (const void*)A, in ? 16 : 0);
+        }
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const bool in = k_in && ((w_ok >> i) & 1u);
+            cp_async16(ws + 32 * i * kB2Ld, in ? (const void*)(pW[i] + k0) : (const void*)W, in ? 16 : 0);
+        }
+        if (++l_ks == plan.kstages) {
+            l_ks = 0;
+            set_tile(++l_tile);
+        }
+    };
+
+    unsigned long long acc[8][4], tot[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = tot[i][j] = 0ull;
+
+    const int64_t nst = u1 - u0;
+    load_next(0);
+    cp_async_commit();
+    if (nst > 1) load_next(1);
+    cp_async_commit();
+    int nfold = 0, slot = 0, lslot = 2;
+    int64_t c_tile = u0 / plan.kstages, c_ks = u0 % plan.kstages;  // compute cursor
+    for (int64_t st = 0; st < nst; ++st) {
+        cp_async_wait<1>();
+        __syncthreads();
+        if (st + 2 < nst) load_next(lslot);
+        cp_async_commit();
+        lslot = lslot == kB2Stages - 1 ? 0 : lslot + 1;
+        const float* as = As + slot * kB2M * kB2Ld + tr * kB2Ld;
+        const float* ws = Ws + slot * kB2V * kB2Ld + tv * kB2Ld;
+        slot = slot == kB2Stages - 1 ? 0 : slot + 1;
+#pragma unroll 2
+        for (int kq = 0; kq < kB2K; kq += 4) {
+            float4 a4[8], w4[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) a4[i] = *reinterpret_cast<const float4*>(as + i * 32 * kB2Ld + kq);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) w4[j] = *reinterpret_cast<const float4*>(ws + j * 8 * kB2Ld + kq);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const float a = c == 0 ? a4[i].x : c == 1 ? a4[i].y : c == 2 ? a4[i].z : a4[i].w;
+#pragma unroll
+                    for (int jp = 0; jp < 4; ++jp) {
+                        const float4& x0 = w4[2 * jp];
+                        const float4& x1 = w4[2 * jp + 1];
+                        const float w0 = c == 0 ? x0.x : c == 1 ? x0.y : c == 2 ? x0.z : x0.w;
+                        const float w1 = c == 0 ? x1.x : c == 1 ? x1.y : c == 2 ? x1.z : x1.w;
+                        acc[i][jp] = fadd2(acc[i][jp], pack2(mavp_term<OP>(a, w0), mavp_term<OP>(a, w1)));
+                    }
+                }
+            }
+        }
+        const bool tile_end = (st + 1 == nst) || (c_ks + 1 == plan.kstages);
+        if (++nfold == kFoldStages || tile_end) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    tot[i][j] = fadd2(tot[i][j], acc[i][j]);
+                    acc[i][j] = 0ull;
+                }
+            nfold = 0;
+        }
+        if (tile_end) {
+            // partial slot of this CTA within the tile: CTA index minus the tile's first CTA
+            const int64_t p = (int64_t)blockIdx.x - streamk_cta_of(c_tile * plan.kstages, U, G);
+            float* out = part + ((c_tile * kMaxParts + p) * kB2V) * kB2M;
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int jp = 0; jp < 4; ++jp) {
+                    const int r = tr + 32 * i, v = tv + 8 * (2 * jp);
+                    out[(int64_t)v * kB2M + r] = lo_of(tot[i][jp]);
+                    out[(int64_t)(v + 8) * kB2M + r] = hi_of(tot[i][jp]);
+                    tot[i][jp] = 0ull;
+                }
+        }
+        if (++c_ks == plan.kstages) {
+            c_ks = 0;
+            ++c_tile;
+        }
+    }
+    cp_async_wait<0>();
+}
+
+// Y[v][j] = sum of the tile's partials in CTA order; colpart[v][blk] = sum |Y[v][j]| over 256 rows.
+__global__ void __launch_bounds__(256) k_batched_reduce2(int64_t n, int32_t kv, StreamK plan, int G,
+                                                         const float* __restrict__ part, float* __restrict__ Y,
+                                                         float* __restrict__ colpart, int64_t rb) {
+    __shared__ float red[33];
+    const int v = blockIdx.y;
+    const int64_t j = (int64_t)blockIdx.x * 256 + threadIdx.x;
+    float y = 0.0f;
+    if (j < n) {
+        const int64_t rt = j / kB2M, vt = v / kB2V;
+        const int64_t tile = rt * plan.vec_tiles + vt;
+        const int64_t c0 = streamk_cta_of(tile * plan.kstages, plan.units, G);
+        const int64_t c1 = streamk_cta_of(tile * plan.kstages + plan.kstages - 1, plan.units, G);
+        for (int64_t p = 0; p <= c1 - c0; ++p)
+            y += part[((tile * kMaxParts + p) * kB2V + (v - vt * kB2V)) * kB2M + (j - rt * kB2M)];
+        Y[(int64_t)v * n + j] = y;
+    }
+    const float a = block_sum(fabsf(y), red);
+    if (threadIdx.x == 0) colpart[(int64_t)v * rb + blockIdx.x] = a;
+}
+
+inline size_t streamk_part_bytes(int64_t n, int32_t k) {
+    const int64_t tiles = ((n + kB2M - 1) / kB2M) * ((k + kB2V - 1) / kB2V);
+    return sizeof(float) * (size_t)tiles * kMaxParts * kB2V * kB2M;
+}
+inline size_t streamk_smem_bytes() { return sizeof(float) * kB2Stages * (kB2M + kB2V) * kB2Ld; }
+
 static thread_local char g_batched_err[256] = "";
 inline const char* batched_last_error() { return g_batched_err; }
+
+inline size_t batched_part_bytes(int64_t n, int32_t k) {
+    return std::max(sizeof(float) * (size_t)64 * k * n, streamk_part_bytes(n, k));
+}
 
 inline mapi_status batched_cuda_fail(cudaError_t e, const char* what) {
     snprintf(g_batched_err, sizeof(g_batched_err), "%s: %s", what, cudaGetErrorString(e));
@@ -223,13 +456,32 @@ inline mapi_status batched_run(int32_t op, const float* A, int64_t n, int64_t ld
     const int ks = (int)((n + kslice - 1) / kslice);
     const dim3 gp((unsigned)((n + kBM - 1) / kBM), (unsigned)((k + kBV - 1) / kBV), (unsigned)ks);
     const dim3 gr((unsigned)B.rb, (unsigned)k);
+    // v2 (stream-K) needs 16 B-aligned rows of A and of W (n % 4 == 0); MAPI_BATCHED_PATH=v1 forces v1
+    const char* env = getenv("MAPI_BATCHED_PATH");
+    const bool v2 = !(env && strcmp(env, "v1") == 0) && reinterpret_cast<uintptr_t>(A) % 16 == 0 && lda % 4 == 0 &&
+                    n % 4 == 0 && streamk_ok(n, k, sms);
+    const StreamK plan = streamk_plan(n, k, sms);
+    if (v2) {
+        auto kern = op == 1 ? k_batched_streamk<1> : k_batched_streamk<0>;
+        if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)streamk_smem_bytes())) !=
+            cudaSuccess)
+            return batched_cuda_fail(e, "smem attribute");
+    }
     if (timing) cudaEventRecord(*ev_a, s);
     for (int32_t t = 0; t < iters; ++t) {
-        if (op == 1)
-            k_batched_partial<1><<<gp, kBThreads, 0, s>>>(A, n, lda, B.W, k, kslice, B.part);
-        else
-            k_batched_partial<0><<<gp, kBThreads, 0, s>>>(A, n, lda, B.W, k, kslice, B.part);
-        k_batched_reduce<<<gr, 256, 0, s>>>(n, k, ks, B.part, B.Y, B.colpart, B.rb);
+        if (v2) {
+            if (op == 1)
+                k_batched_streamk<1><<<plan.grid, kB2Threads, streamk_smem_bytes(), s>>>(A, n, lda, B.W, k, plan, B.part);
+            else
+                k_batched_streamk<0><<<plan.grid, kB2Threads, streamk_smem_bytes(), s>>>(A, n, lda, B.W, k, plan, B.part);
+            k_batched_reduce2<<<gr, 256, 0, s>>>(n, k, plan, plan.grid, B.part, B.Y, B.colpart, B.rb);
+        } else {
+            if (op == 1)
+                k_batched_partial<1><<<gp, kBThreads, 0, s>>>(A, n, lda, B.W, k, kslice, B.part);
+            else
+                k_batched_partial<0><<<gp, kBThreads, 0, s>>>(A, n, lda, B.W, k, kslice, B.part);
+            k_batched_reduce<<<gr, 256, 0, s>>>(n, k, ks, B.part, B.Y, B.colpart, B.rb);
+        }
         k_batched_normalize<<<k, 1024, 0, s>>>(n, k, t, tol, B.Y, B.colpart, B.rb, B.W, norms, deltas, B.status,
                                                B.stop);
         launches.fetch_add(3, std::memory_order_relaxed);

@@ -74,25 +74,42 @@ inline mapi_status csr_prepare_run(int64_t n, int64_t nnz, const int32_t* /*row_
 // state has a delta noise floor of ~1e-7 (the BASELINE tol) and would decide the stopping iteration
 // by rounding noise; the paper computes in double (MATLAB).  Cost: +~70 MB/iteration of node traffic.
 //
-// workspace: [hdr 256: status[2] @0, stop @8][w n f64][e n f32][v n f32]
+// workspace: [hdr 256: status[2] @0, stop @8, s f64 @16][w n f64][e n f32][v n f32]
 //            [slotS 2*G f64][slotY G f64][slotD G f64]
+//            [merge-path partition: (i,k) x (T+1) i32][carry_row T i32][carry_val T f32][gsum T f64]
+// T = number of merge-path tiles = ceil((n + nnz) / kMpTile).
+constexpr int kMpThreads = 256;
+constexpr int kMpIpt = 8;                           // merge items (rows + nonzeros) per thread
+constexpr int kMpTile = kMpThreads * kMpIpt;        // 2048 items per CTA
+
 struct CsrWs {
     int32_t* status;
     int32_t* stop;
+    double* s;
     double* w;
     float *e, *v;
     double *slotS, *slotY, *slotD;
+    int32_t *part_i, *part_k, *carry_row;
+    float* carry_val;
+    double* gsum;
+    int64_t tiles;
 };
 
-inline size_t csr_rank_ws_bytes(int64_t n, int64_t /*nnz*/) {
-    return 256 + cal256(8 * (size_t)n) + 2 * cal256(4 * (size_t)n) + 4 * cal256(8 * (size_t)kCsrMaxGrid);
+inline int64_t mp_tiles(int64_t n, int64_t nnz) { return (n + nnz + kMpTile - 1) / kMpTile; }
+
+inline size_t csr_rank_ws_bytes(int64_t n, int64_t nnz) {
+    const int64_t T = mp_tiles(n, nnz);
+    return 256 + cal256(8 * (size_t)n) + 2 * cal256(4 * (size_t)n) + 4 * cal256(8 * (size_t)kCsrMaxGrid) +
+           2 * cal256(4 * (size_t)(T + 1)) + 2 * cal256(4 * (size_t)T) + cal256(8 * (size_t)T);
 }
 
-inline CsrWs carve_csr(void* ws, int64_t n) {
+inline CsrWs carve_csr(void* ws, int64_t n, int64_t nnz) {
     char* p = static_cast<char*>(ws);
     CsrWs c;
+    c.tiles = mp_tiles(n, nnz);
     c.status = reinterpret_cast<int32_t*>(p);
     c.stop = reinterpret_cast<int32_t*>(p + 8);
+    c.s = reinterpret_cast<double*>(p + 16);
     p += 256;
     c.w = reinterpret_cast<double*>(p);
     p += cal256(8 * (size_t)n);
@@ -105,6 +122,16 @@ inline CsrWs carve_csr(void* ws, int64_t n) {
     c.slotY = reinterpret_cast<double*>(p);
     p += cal256(8 * (size_t)kCsrMaxGrid);
     c.slotD = reinterpret_cast<double*>(p);
+    p += cal256(8 * (size_t)kCsrMaxGrid);
+    c.part_i = reinterpret_cast<int32_t*>(p);
+    p += cal256(4 * (size_t)(c.tiles + 1));
+    c.part_k = reinterpret_cast<int32_t*>(p);
+    p += cal256(4 * (size_t)(c.tiles + 1));
+    c.carry_row = reinterpret_cast<int32_t*>(p);
+    p += cal256(4 * (size_t)c.tiles);
+    c.carry_val = reinterpret_cast<float*>(p);
+    p += cal256(4 * (size_t)c.tiles);
+    c.gsum = reinterpret_cast<double*>(p);
     return c;
 }
 
@@ -151,34 +178,153 @@ __global__ void __launch_bounds__(kCsrThreads) k_rank_init(int64_t n, const floa
     if (threadIdx.x == 0) slotS[blockIdx.x] = S;
 }
 
-// K3b: e_i = sum_{e in row i} v[col_idx[e]] (fp32 gather, one warp per row); fp64 partials of
-// sum_i y_i = sum_i (S + e_i) (= ||y||_1, all terms >= 0).
-__global__ void __launch_bounds__(kCsrThreads) k_rank_rows(int64_t n, const int32_t* __restrict__ row_ptr,
-                                                           const int32_t* __restrict__ col_idx,
-                                                           const float* __restrict__ v, const double* __restrict__ slotS,
-                                                           int nslots, float* __restrict__ e, double* __restrict__ slotY,
-                                                           const int32_t* stop) {
-    __shared__ double red[33];
-    if (*(volatile const int32_t*)stop) return;
-    const double S = slots_sum(slotS, nslots, red);
-    const int lane = threadIdx.x & 31;
-    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-    double ypart = 0.0;
-    for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += warps) {
-        const int32_t e0 = row_ptr[i], e1 = row_ptr[i + 1];
-        float acc = 0.0f;
-        for (int32_t k = e0 + lane; k < e1; k += 32) acc += __ldg(v + col_idx[k]);
-        acc = warp_sum(acc);
-        if (lane == 0) {
-            e[i] = acc;
-            ypart += S + (double)acc;
-        }
+// ---- K3b: merge-path gather-sum  e_i = sum_{e in row i} v[col_idx[e]]  (fp32)
+// The (n row ends) + (nnz nonzeros) merge list is cut into equal tiles of kMpTile items, so hub
+// rows (97k edges) and empty rows (52% at cfg5) cost the same per item (Merrill & Garland's
+// merge-based SpMV decomposition, re-derived for a value-free gather-sum).  Every row end is
+// emitted exactly once; a row that spans threads collects the preceding threads' carries in thread
+// order, and a row that spans CTAs gets the CTA carry-outs added by k_rank_fixup in CTA order, so
+// the summation order is fixed for a given graph.
+
+// merge-path search on diagonal d: the number of row ends consumed before d
+__device__ __forceinline__ int64_t mp_search(int64_t d, const int32_t* __restrict__ row_end, int64_t n,
+                                             int64_t nnz) {
+    int64_t lo = max((int64_t)0, d - nnz), hi = min(d, n);
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if ((int64_t)row_end[mid] <= d - 1 - mid) lo = mid + 1;
+        else hi = mid;
     }
-    const double Y = block_sum(ypart, red);
-    if (threadIdx.x == 0) slotY[blockIdx.x] = Y;
+    return lo;
 }
 
-// K3c: s = ||y||_1, w_new = (S + e_j) / s (fp64), delta partials; next v_j and S partials.
+// once per call: tile start coordinates (i, k) for every tile boundary
+__global__ void k_mp_partition(int64_t n, int64_t nnz, const int32_t* __restrict__ row_ptr, int64_t tiles,
+                               int32_t* __restrict__ part_i, int32_t* __restrict__ part_k) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c > tiles) return;
+    const int64_t d = min(c * kMpTile, n + nnz);
+    const int64_t i = mp_search(d, row_ptr + 1, n, nnz);
+    part_i[c] = (int32_t)i;
+    part_k[c] = (int32_t)(d - i);
+}
+
+__global__ void __launch_bounds__(kMpThreads) k_rank_rows_mp(int64_t n, int64_t nnz, const int32_t* __restrict__ row_ptr,
+                                                             const int32_t* __restrict__ col_idx,
+                                                             const float* __restrict__ v,
+                                                             const int32_t* __restrict__ part_i,
+                                                             const int32_t* __restrict__ part_k, float* __restrict__ e,
+                                                             int32_t* __restrict__ carry_row,
+                                                             float* __restrict__ carry_val, double* __restrict__ gsum,
+                                                             const int32_t* stop) {
+    __shared__ int32_t s_end[kMpTile + 1];  // row_ptr[i0+1 .. i1+1]
+    __shared__ float s_val[kMpTile];        // v[col_idx[k0 .. k1)]
+    __shared__ int32_t c_row[kMpThreads];
+    __shared__ float c_val[kMpThreads];
+    __shared__ double red[33];
+    if (*(volatile const int32_t*)stop) return;
+    const int tid = threadIdx.x;
+    const int32_t i0 = part_i[blockIdx.x], i1 = part_i[blockIdx.x + 1];
+    const int32_t k0 = part_k[blockIdx.x], k1 = part_k[blockIdx.x + 1];
+    const int nrows = i1 - i0, nk = k1 - k0;  // nrows + nk == items of this tile
+    // stage row ends (rows i0 .. i1, the last possibly partial) and gathered values
+    for (int r = tid; r <= nrows; r += kMpThreads)
+        s_end[r] = (i0 + r < n) ? row_ptr[i0 + r + 1] : (int32_t)nnz;
+    // nk <= kMpTile = kMpIpt * kMpThreads: all kMpIpt column ids first, then all gathers in flight
+    int32_t cj[kMpIpt];
+#pragma unroll
+    for (int u = 0; u < kMpIpt; ++u) {
+        const int j = tid + u * kMpThreads;
+        cj[u] = j < nk ? __ldg(col_idx + k0 + j) : -1;
+    }
+    float xv[kMpIpt];
+#pragma unroll
+    for (int u = 0; u < kMpIpt; ++u) xv[u] = cj[u] >= 0 ? __ldg(v + cj[u]) : 0.0f;
+    double gpart = 0.0;
+#pragma unroll
+    for (int u = 0; u < kMpIpt; ++u) {
+        const int j = tid + u * kMpThreads;
+        if (j < nk) s_val[j] = xv[u];
+        gpart += (double)xv[u];
+    }
+    __syncthreads();
+    // this thread's diagonal within the tile
+    const int items = nrows + nk;
+    const int dt = min(tid * kMpIpt, items);
+    int lo = max(0, dt - nk), hi = min(dt, nrows);
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (s_end[mid] - k0 <= dt - 1 - mid) lo = mid + 1;
+        else hi = mid;
+    }
+    int ri = lo, kj = dt - lo;
+    float acc = 0.0f, own_first = 0.0f;
+    int first_row = -1;  // first row this thread emits (local index); earlier threads may feed it
+    const int dend = min(dt + kMpIpt, items);
+    for (int d = dt; d < dend; ++d) {
+        if (ri < nrows && k0 + kj >= s_end[ri]) {  // the end of row ri
+            if (first_row < 0) {
+                first_row = ri;
+                own_first = acc;
+            } else {
+                e[i0 + ri] = acc;  // started inside this thread: complete
+            }
+            acc = 0.0f;
+            ++ri;
+        } else {
+            acc += s_val[kj];
+            ++kj;
+        }
+    }
+    c_row[tid] = ri;  // carry: row still open at this thread's end, and its partial
+    c_val[tid] = acc;
+    __syncthreads();
+    if (first_row >= 0) {  // add the carries of the run of preceding threads open on this row
+        int t0 = tid;
+        while (t0 > 0 && c_row[t0 - 1] == first_row) --t0;
+        float sum = 0.0f;
+        for (int t = t0; t < tid; ++t) sum += c_val[t];
+        e[i0 + first_row] = sum + own_first;
+    }
+    // CTA carry-out: the trailing run of threads still open on the tile's last row
+    if (tid == kMpThreads - 1) {
+        const int last = c_row[kMpThreads - 1];
+        float sum = 0.0f;
+        int t0 = kMpThreads;
+        while (t0 > 0 && c_row[t0 - 1] == last) --t0;
+        for (int t = t0; t < kMpThreads; ++t) sum += c_val[t];
+        carry_row[blockIdx.x] = (last < nrows || (last == nrows && i1 < n)) ? i0 + last : -1;
+        carry_val[blockIdx.x] = sum;
+    }
+    const double g = block_sum(gpart, red);
+    if (tid == 0) gsum[blockIdx.x] = g;
+}
+
+// CTA carry-outs into the rows they belong to (tile order), and the fp64 partials of sum_i e_i.
+__global__ void __launch_bounds__(256) k_rank_fixup(int64_t tiles, const int32_t* __restrict__ carry_row,
+                                                    const float* __restrict__ carry_val,
+                                                    const double* __restrict__ gsum, float* __restrict__ e,
+                                                    double* __restrict__ slotY, const int32_t* stop) {
+    __shared__ double red[33];
+    if (*(volatile const int32_t*)stop) return;
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    double g = 0.0;
+    if (c < tiles) {
+        g = gsum[c];
+        const int32_t r = carry_row[c];
+        if (r >= 0 && (c == 0 || carry_row[c - 1] != r)) {
+            float sum = 0.0f;
+            for (int64_t q = c; q < tiles && carry_row[q] == r; ++q) sum += carry_val[q];
+            e[r] += sum;  // the emitting tile (after this run) already wrote its part
+        }
+    }
+    const double G = block_sum(g, red);
+    if (threadIdx.x == 0) slotY[blockIdx.x] = G;
+}
+
+// K3c: s = ||y||_1 = n S + sum_i e_i (fp64), w_new = (S + e_j) / s (fp64), delta partials; next v_j
+// and S partials.  (One fp64 product n*S per iteration: the l1 norm of the common background.)
+template <bool V4>
 __global__ void __launch_bounds__(kCsrThreads) k_rank_normalize(int64_t n, const float* __restrict__ e,
                                                                 const double* __restrict__ slotS_cur,
                                                                 double* __restrict__ slotS_next, int nS,
@@ -186,13 +332,58 @@ __global__ void __launch_bounds__(kCsrThreads) k_rank_normalize(int64_t n, const
                                                                 const float* __restrict__ bg,
                                                                 const float* __restrict__ cap, double* __restrict__ w,
                                                                 float* __restrict__ v, double* __restrict__ slotD,
-                                                                const int32_t* stop) {
+                                                                double* s_out, const int32_t* stop) {
     __shared__ double red[33];
     if (*(volatile const int32_t*)stop) return;
     const double S = slots_sum(slotS_cur, nS, red);
-    const double s = slots_sum(slotY, nY, red);
+    const double s = (double)n * S + slots_sum(slotY, nY, red);
+    if (blockIdx.x == 0 && threadIdx.x == 0) *s_out = s;
+    if (!(s > 0.0) || isinf(s)) return;  // uniform: flagged by k_rank_step_end
     double dp = 0.0, sp = 0.0;
-    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t j0 = 0;
+    if constexpr (V4) {
+        // groups of 4 consecutive nodes, two groups per trip: 16 B vector loads, 8 nodes in flight
+        const int64_t groups = n / 4;
+        for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < groups; g += 2 * stride) {
+            float4 ev[2], bv[2], cv[2];
+            double2 wv[2][2];
+            const bool two = g + stride < groups;
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                if (q == 1 && !two) break;
+                const int64_t gg = g + q * stride;
+                ev[q] = reinterpret_cast<const float4*>(e)[gg];
+                bv[q] = __ldg(reinterpret_cast<const float4*>(bg) + gg);
+                cv[q] = __ldg(reinterpret_cast<const float4*>(cap) + gg);
+                wv[q][0] = reinterpret_cast<const double2*>(w)[2 * gg];
+                wv[q][1] = reinterpret_cast<const double2*>(w)[2 * gg + 1];
+            }
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                if (q == 1 && !two) break;
+                const int64_t gg = g + q * stride;
+                const float ee[4] = {ev[q].x, ev[q].y, ev[q].z, ev[q].w};
+                const float bb[4] = {bv[q].x, bv[q].y, bv[q].z, bv[q].w};
+                const float cc[4] = {cv[q].x, cv[q].y, cv[q].z, cv[q].w};
+                const double wo[4] = {wv[q][0].x, wv[q][0].y, wv[q][1].x, wv[q][1].y};
+                double wn[4];
+                float vn[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    wn[i] = (S + (double)ee[i]) / s;
+                    dp += fabs(wn[i] - wo[i]);
+                    vn[i] = csr_v(wn[i], bb[i], cc[i]);
+                    sp += fmin((double)bb[i], wn[i]);
+                }
+                reinterpret_cast<double2*>(w)[2 * gg] = make_double2(wn[0], wn[1]);
+                reinterpret_cast<double2*>(w)[2 * gg + 1] = make_double2(wn[2], wn[3]);
+                reinterpret_cast<float4*>(v)[gg] = make_float4(vn[0], vn[1], vn[2], vn[3]);
+            }
+        }
+        j0 = groups * 4;
+    }
+    for (int64_t j = j0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride) {
         const double wn = (S + (double)e[j]) / s;
         dp += fabs(wn - w[j]);
         w[j] = wn;
@@ -209,11 +400,11 @@ __global__ void __launch_bounds__(kCsrThreads) k_rank_normalize(int64_t n, const
 }
 
 // K3d: delta_t, trace, status, stop.
-__global__ void k_rank_step_end(const double* __restrict__ slotY, int ny, const double* __restrict__ slotD, int nd,
-                                int32_t t, float tol, float* deltas, int32_t* status, int32_t* stop) {
+__global__ void k_rank_step_end(const double* __restrict__ s_in, const double* __restrict__ slotD, int nd, int32_t t,
+                                float tol, float* deltas, int32_t* status, int32_t* stop) {
     __shared__ double red[33];
     if (*(volatile int32_t*)stop) return;
-    const double s = slots_sum(slotY, ny, red);
+    const double s = *s_in;
     const double d = slots_sum(slotD, nd, red);
     if (threadIdx.x == 0) {
         if (!(s > 0.0) || isinf(s)) {
@@ -246,23 +437,37 @@ inline mapi_status csr_rank_run(int64_t n, int64_t nnz, const int32_t* row_ptr, 
                                 const float* cap, const float* bg, const float* b0, int32_t max_iters, float tol,
                                 float* w_out, float* w_l2_out, float* deltas, void* ws, int sms, cudaStream_t s,
                                 cudaEvent_t* ev_a, cudaEvent_t* ev_b, std::atomic<uint64_t>& launches) {
-    (void)nnz;
-    CsrWs W = carve_csr(ws, n);
+    CsrWs W = carve_csr(ws, n, nnz);
     cudaError_t err = cudaMemsetAsync(ws, 0, 256, s);
     if (err != cudaSuccess) return csr_cuda_fail(err, "memset");
     const int gcol = (int)std::min<int64_t>({(n + kCsrThreads - 1) / kCsrThreads, (int64_t)4 * sms, (int64_t)kCsrMaxGrid});
-    const int grow = (int)std::min<int64_t>({(n + 7) / 8, (int64_t)8 * sms, (int64_t)kCsrMaxGrid});
+    const int64_t T = W.tiles;
+    // 16 B vector path for the node arrays when the caller's bg / cap are 16 B aligned
+    const bool v4 = (reinterpret_cast<uintptr_t>(bg) % 16 == 0) && (reinterpret_cast<uintptr_t>(cap) % 16 == 0);
+    const int gfix = (int)((T + 255) / 256);
+    if (gfix > kCsrMaxGrid) {
+        snprintf(g_csr_err, sizeof(g_csr_err), "graph too large: %lld merge tiles", (long long)T);
+        return MAPI_ERR_SHAPE;
+    }
+    k_mp_partition<<<(unsigned)((T + 1 + 255) / 256), 256, 0, s>>>(n, nnz, row_ptr, T, W.part_i, W.part_k);
+    launches.fetch_add(1, std::memory_order_relaxed);
     if (ev_a) cudaEventRecord(*ev_a, s);
     k_rank_init<<<gcol, kCsrThreads, 0, s>>>(n, b0, bg, cap, W.w, W.v, W.slotS, W.status, W.stop);
     launches.fetch_add(1, std::memory_order_relaxed);
     for (int32_t t = 0; t < max_iters; ++t) {
         double* S_cur = W.slotS + (t & 1) * kCsrMaxGrid;
         double* S_next = W.slotS + ((t + 1) & 1) * kCsrMaxGrid;
-        k_rank_rows<<<grow, kCsrThreads, 0, s>>>(n, row_ptr, col_idx, W.v, S_cur, gcol, W.e, W.slotY, W.stop);
-        k_rank_normalize<<<gcol, kCsrThreads, 0, s>>>(n, W.e, S_cur, S_next, gcol, W.slotY, grow, bg, cap, W.w, W.v,
-                                                       W.slotD, W.stop);
-        k_rank_step_end<<<1, 32, 0, s>>>(W.slotY, grow, W.slotD, gcol, t, tol, deltas, W.status, W.stop);
-        launches.fetch_add(3, std::memory_order_relaxed);
+        k_rank_rows_mp<<<(unsigned)T, kMpThreads, 0, s>>>(n, nnz, row_ptr, col_idx, W.v, W.part_i, W.part_k, W.e,
+                                                          W.carry_row, W.carry_val, W.gsum, W.stop);
+        k_rank_fixup<<<gfix, 256, 0, s>>>(T, W.carry_row, W.carry_val, W.gsum, W.e, W.slotY, W.stop);
+        if (v4)
+            k_rank_normalize<true><<<gcol, kCsrThreads, 0, s>>>(n, W.e, S_cur, S_next, gcol, W.slotY, gfix, bg, cap, W.w,
+                                                                W.v, W.slotD, W.s, W.stop);
+        else
+            k_rank_normalize<false><<<gcol, kCsrThreads, 0, s>>>(n, W.e, S_cur, S_next, gcol, W.slotY, gfix, bg, cap,
+                                                                 W.w, W.v, W.slotD, W.s, W.stop);
+        k_rank_step_end<<<1, 32, 0, s>>>(W.s, W.slotD, gcol, t, tol, deltas, W.status, W.stop);
+        launches.fetch_add(4, std::memory_order_relaxed);
         if ((err = cudaGetLastError()) != cudaSuccess) return csr_cuda_fail(err, "rank launch");
     }
     if (ev_b) cudaEventRecord(*ev_b, s);
