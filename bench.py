@@ -55,6 +55,20 @@ def parse():
     return p.parse_args()
 
 
+def max_over_ranks(x: float, device=None) -> float:
+    """Max of a per-rank scalar over all ranks (the contract's max-over-ranks timing).  Works with
+    NCCL (device tensor) and gloo (CPU tensor); identity when torch.distributed is not initialised."""
+    import torch
+    import torch.distributed as tdist
+
+    if not (tdist.is_available() and tdist.is_initialized()) or tdist.get_world_size() == 1:
+        return float(x)
+    dev = device if (device is not None and tdist.get_backend() == "nccl") else torch.device("cpu")
+    t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
+    tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
@@ -333,11 +347,8 @@ def run_mapi(args, rank, world, local_rank):
     launches = m.launch_count() - launches0
     clocks = sampler.stop()
     m.set_profiling(False)
-    elapsed_ms = ev0.elapsed_time(ev1)
+    elapsed_ms = max_over_ranks(ev0.elapsed_time(ev1), dev)
     if dist:
-        t = torch.tensor([elapsed_ms], device=dev, dtype=torch.float64)
-        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
-        elapsed_ms = float(t.item())
         tdist.barrier()
     value = units * world / (elapsed_ms / 1e3)
     kavg = float(np.mean(kernel_ms))
@@ -412,11 +423,7 @@ def e2e_dense(args, m, A, b0, iters, dev, stream, world, dist):
         step()
     ev1.record(stream)
     torch.cuda.synchronize()
-    ms = ev0.elapsed_time(ev1)
-    if dist:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(ev0.elapsed_time(ev1), dev)
     del ws, A_h
     return {"value": world * iters * steps / (ms / 1e3), "unit": "iterations/s",
             "h2d_bytes_per_step": 4 * n * lda + 4 * n, "d2h_bytes_per_step": 4 * n + 8 * iters + 8,

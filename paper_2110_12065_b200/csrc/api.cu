@@ -205,11 +205,19 @@ bool use_persistent(const Device& d, int64_t n) {
 
 int coop_warps(int64_t n) { return (n / 256) >= 64 ? 32 : 16; }
 
+// K6 (one 8-CTA cluster, A in distributed shared memory) for small n; MAPI_DENSE_PATH=cluster forces
+bool use_cluster(const Device& d, int64_t n) {
+    const char* e = dense_path_env();
+    if (strcmp(e, "rows") == 0 || strcmp(e, "multi") == 0 || strcmp(e, "coop") == 0) return false;
+    if (cluster_smem_bytes(n) > (size_t)d.smem_optin) return false;
+    return strcmp(e, "cluster") == 0 || n <= 512;
+}
+
 bool use_coop(const Device& d, const float* A, int64_t n, int64_t lda) {
     const char* e = dense_path_env();
     if (strcmp(e, "rows") == 0 || strcmp(e, "multi") == 0) return false;
     if (vec_width(A, lda) != 8) return false;
-    if (strcmp(e, "coop") != 0 && n / 256 < 16) return false;
+    if (strcmp(e, "coop") != 0 && n / 256 < 32) return false;  // n < 8192: the per-row kernel is faster
     const int64_t grid = std::min<int64_t>(d.sms, n);
     return coop_smem_bytes(n, (int)grid, coop_warps(n)) <= (size_t)d.smem_optin;
 }
@@ -221,6 +229,33 @@ mapi_status iterate_launch(const Device& d, int32_t op, const float* A, int64_t 
     const int vec = vec_width(A, lda);
     const int pol = load_policy(d, n, lda);
     MAPI_CUDA(cudaMemsetAsync(W.bar, 0, 256, s));
+    if (use_cluster(d, n)) {
+        auto kern = op == 1 ? k_iterate_cluster<1> : k_iterate_cluster<0>;
+        const size_t smem = cluster_smem_bytes(n);
+        MAPI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        IterArgs a;
+        a.A = A; a.n = n; a.lda = lda; a.b0 = b0; a.iters = iters; a.tol = tol;
+        a.w_out = w_out; a.norms = norms; a.deltas = deltas; a.y = W.y; a.slots = W.slots;
+        a.bar = W.bar; a.status = W.status;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(kClusterCtas);
+        cfg.blockDim = dim3(kClusterThreads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = kClusterCtas;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        if (timer) timer->start();
+        cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a);
+        if (timer) timer->stop();
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        if (e != cudaSuccess) return fail(MAPI_ERR_CUDA, "cluster launch (smem %zu): %s", smem, cudaGetErrorString(e));
+        return MAPI_OK;
+    }
     if (use_coop(d, A, n, lda)) {
         mapi_status st = MAPI_OK;
         auto launch = [&](auto kern, int nw) {
@@ -265,7 +300,11 @@ mapi_status iterate_launch(const Device& d, int32_t op, const float* A, int64_t 
                 return with_pol(pol, [&](auto POLc) {
                     constexpr int OP = decltype(OPc)::value, VEC = decltype(VECc)::value,
                                   POL = decltype(POLc)::value;
-                    auto kern = k_iterate_persistent<OP, VEC, POL, unroll_for(VEC)>;
+                    // mid-size n (< 8192, w fits twice per SM): 16 B loads, 2 CTAs/SM (measured 12.0 vs
+                    // 13.0 us/iteration at n = 4096; profiles/r01_probe_dense.log)
+                    const bool two = VEC >= 4 && n < 8192;
+                    auto kern = two ? k_iterate_persistent<OP, (VEC >= 4 ? 4 : VEC), POL, 4, 0, 0, 2>
+                                    : k_iterate_persistent<OP, VEC, POL, unroll_for(VEC)>;
                     const size_t smem = persistent_smem_bytes(n);
                     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                          (int)smem);

@@ -120,8 +120,8 @@ struct IterArgs {
 // status codes (mirror mapi_status)
 constexpr int kStOk = 0, kStDegenerate = 4, kStNonfinite = 6;
 
-template <int OP, int VEC, int POL, int U, int PF = 0, int PH = 0>
-__global__ void __launch_bounds__(512, 1) k_iterate_persistent(IterArgs p) {
+template <int OP, int VEC, int POL, int U, int PF = 0, int PH = 0, int MINB = 1>
+__global__ void __launch_bounds__(512, MINB) k_iterate_persistent(IterArgs p) {
     extern __shared__ __align__(16) float ws_[];
     float* w_s = ws_;                                                    // n floats (w_t)
     double* red = reinterpret_cast<double*>(ws_ + ((p.n + 3) & ~int64_t(3)));  // 33 doubles
@@ -212,7 +212,7 @@ __global__ void __launch_bounds__(512, 1) k_iterate_persistent(IterArgs p) {
 // Numerics: fp32 MAVP terms and row sums (per lane 8 chains of <= ceil(C/NW) terms, tree, butterfly,
 // NW warp partials in order); s_t and delta_t are accumulated in fp64 (fixed order), and
 // w_{t+1} = fp32(y / s_t) with the division in fp64, so w carries no common-mode rounding of s_t.
-template <int OP, int POL, int NW>
+template <int OP, int POL, int NW, int D = 2>
 __global__ void __launch_bounds__(NW * 32, 1) k_iterate_coop(IterArgs p) {
     constexpr int STEP = 256;  // floats per warp-wide LDG.256 (one 1 KB chunk)
     extern __shared__ __align__(16) float ws_[];
@@ -233,13 +233,16 @@ __global__ void __launch_bounds__(NW * 32, 1) k_iterate_coop(IterArgs p) {
 
     for (int64_t k = tid; k < n; k += blockDim.x) w_s[k] = p.b0[k];
 
-    float bufA[8], bufB[8], acc[8];
-    int lr = 0, lq = 0;  // (row, chunk) of the next load
+    float buf[D][8], acc[8];  // register ring: D chunk loads in flight per warp
+    int lr = 0, lq = 0;        // (row, chunk) of the next load
     auto load = [&](float (&b)[8]) {
         ld_stream<8, POL>(abase + lr * rstride + (int64_t)lq * STEP, b);
         if (++lq == spr) { lq = 0; ++lr; }
     };
-    if (nsteps > 0) load(bufA);  // first load of iteration 0 (overlaps the w staging)
+    constexpr int D0 = D == 2 ? 1 : D;  // chunks pre-loaded ahead of the rows loop
+#pragma unroll
+    for (int j = 0; j < D0; ++j)
+        if (j < nsteps) load(buf[j]);  // first loads of iteration 0 (overlap the w staging)
     __syncthreads();
     int32_t done = 0, status = kStOk;
 
@@ -274,20 +277,36 @@ __global__ void __launch_bounds__(NW * 32, 1) k_iterate_coop(IterArgs p) {
                 ++cr;
             }
         };
-        // ---- rows (a1, a2): bufA already holds step 0
-        int s = 0;
-        for (; s + 1 < nsteps; s += 2) {
-            load(bufB);
-            consume(bufA);
-            if (s + 2 < nsteps) load(bufA);
-            consume(bufB);
+        // ---- rows (a1, a2): buf[0..D) already hold steps 0..D-1; step s lives in buf[s % D]
+        if constexpr (D == 2) {  // explicit double buffer (measured faster than the generic ring)
+            // here only buf[0] holds step 0; buf[1] is loaded just ahead of each consume
+            int s = 0;
+            for (; s + 1 < nsteps; s += 2) {
+                load(buf[1]);
+                consume(buf[0]);
+                if (s + 2 < nsteps) load(buf[0]);
+                consume(buf[1]);
+            }
+            if (s < nsteps) consume(buf[0]);
+        } else {
+            for (int s = 0; s < nsteps; s += D) {
+#pragma unroll
+                for (int j = 0; j < D; ++j) {
+                    if (s + j < nsteps) {
+                        consume(buf[j]);
+                        if (s + j + D < nsteps) load(buf[j]);
+                    }
+                }
+            }
         }
-        if (s < nsteps) consume(bufA);
         if (spr == 0)  // no full chunk for this warp: zero partials (+ the tail if it owns it)
             for (cr = 0; cr < (int)rows_cta; ++cr) finish_row();
         lr = 0;
         lq = 0;
-        if (nsteps > 0 && t + 1 < p.iters) load(bufA);  // next iteration's first chunk, in flight
+        if (t + 1 < p.iters)  // next iteration's first chunks, in flight across the barrier
+#pragma unroll
+            for (int j = 0; j < D0; ++j)
+                if (j < nsteps) load(buf[j]);
         __syncthreads();
         // ---- y rows of this CTA (NW partials in warp order), fp64 |y| partial (a3)
         double abs_part = 0.0;
@@ -347,6 +366,122 @@ inline size_t coop_smem_bytes(int64_t n, int grid, int nw) {
     const int64_t rows_cta = (n + grid - 1) / grid;
     return sizeof(float) * (size_t)(((n + 7) & ~int64_t(7)) + ((rows_cta * nw + 1) & ~int64_t(1))) +
            sizeof(double) * 33;
+}
+
+// ---------------------------------------------------------------------------------------------
+// K6: small-n MAPI in ONE thread-block cluster of kClusterCtas CTAs (latency-bound case, cfg1).
+// CTA r of the cluster stages rows [r*R, (r+1)*R) of A into its shared memory once; every iteration
+// each CTA computes its y rows (warp per row, lane-strided columns, butterfly), pushes each y_j into
+// the y buffer of every CTA of the cluster with DSMEM stores (st.shared::cluster), and one cluster
+// barrier (release/acquire) publishes them.  Each CTA then forms s_t, w_{t+1} = fp32(y/s_t) and
+// delta_t in the same fixed fp64 order (identical in all CTAs).  y is double-buffered by parity.
+constexpr int kClusterCtas = 8;
+constexpr int kClusterThreads = 1024;
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// store v to the same shared-memory offset as `local` in CTA `rank` of this cluster
+__device__ __forceinline__ void st_cluster(float* local, uint32_t rank, float v) {
+    const uint32_t a = (uint32_t)__cvta_generic_to_shared(local);
+    uint32_t ra;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+    asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(ra), "f"(v) : "memory");
+}
+
+__host__ __device__ inline int64_t cluster_rows_per_cta(int64_t n) { return (n + kClusterCtas - 1) / kClusterCtas; }
+__host__ __device__ inline int64_t cluster_ld(int64_t n) { return (n + 255) & ~int64_t(255); }  // zero-padded rows
+inline size_t cluster_smem_bytes(int64_t n) {
+    const int64_t R = cluster_rows_per_cta(n), np = cluster_ld(n);
+    return sizeof(float) * (size_t)(R * np + 3 * np);
+}
+
+// Row r of this CTA against w: lane-contiguous 8-column chunks (LDS.128 x 2 each), tree, butterfly.
+template <int OP>
+__device__ __forceinline__ float cluster_row(const float* __restrict__ a, const float* __restrict__ w, int64_t np,
+                                             int lane) {
+    float acc[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
+    for (int64_t c = lane * 8; c < np; c += 256) {
+        float x[8], v[8];
+        ld_vec<8, false>(a + c, v);
+        ld_vec<8, false>(w + c, x);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] += mavp_term<OP>(v[i], x[i]);
+    }
+    return warp_sum(tree_sum(acc));
+}
+
+template <int OP>
+__global__ void __launch_bounds__(kClusterThreads, 1) k_iterate_cluster(IterArgs p) {
+    extern __shared__ __align__(16) float sm[];
+    const int64_t n = p.n, np = cluster_ld(n);
+    const int64_t R = cluster_rows_per_cta(n);
+    float* As = sm;              // R x np, zero padded (padding terms are exactly 0)
+    float* w_s = sm + R * np;    // np, zero padded
+    float* ybuf = w_s + np;      // 2 x np
+    const uint32_t rank = cluster_ctarank();
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = kClusterThreads / 32;
+    const int64_t r0 = (int64_t)rank * R, r1 = min(n, r0 + R);
+    for (int64_t q = tid; q < R * np; q += kClusterThreads) {
+        const int64_t r = q / np, c = q - r * np;
+        As[q] = (r0 + r < n && c < n) ? p.A[(r0 + r) * p.lda + c] : 0.0f;
+    }
+    for (int64_t k = tid; k < np; k += kClusterThreads) w_s[k] = k < n ? p.b0[k] : 0.0f;
+    cluster_sync_all();  // every CTA resident and staged before any DSMEM store
+    int32_t done = 0, status = kStOk;
+    __shared__ int32_t s_flag[2];
+    for (int32_t t = 0; t < p.iters; ++t) {
+        float* yb = ybuf + (t & 1) * np;
+        for (int64_t r = r0 + warp; r < r1; r += nw) {
+            const float v = cluster_row<OP>(As + (r - r0) * np, w_s, np, lane);
+            if (lane < kClusterCtas) st_cluster(yb + r, (uint32_t)lane, v);
+        }
+        cluster_sync_all();
+        // epilogue by warp 0 (fixed order, identical in every CTA): s_t, w_{t+1}, delta_t
+        if (warp == 0) {
+            double ap = 0.0;
+            for (int64_t k = lane; k < n; k += 32) ap += (double)fabsf(yb[k]);
+            const double sd = warp_sum(ap);
+            int st = kStOk;
+            if (!(sd > 0.0) || isinf(sd)) st = (sd == 0.0) ? kStDegenerate : kStNonfinite;
+            double dp = 0.0;
+            if (st == kStOk)
+                for (int64_t k = lane; k < n; k += 32) {
+                    const float wn = (float)((double)yb[k] / sd);
+                    dp += (double)fabsf(wn - w_s[k]);
+                    w_s[k] = wn;
+                }
+            const double delta = warp_sum(dp);
+            if (lane == 0) {
+                s_flag[0] = st;
+                s_flag[1] = (st == kStOk && p.tol > 0.0f && delta < (double)p.tol) ? 1 : 0;
+                if (rank == 0 && st == kStOk) {
+                    if (p.norms) p.norms[t] = (float)sd;
+                    if (p.deltas) p.deltas[t] = (float)delta;
+                }
+            }
+        }
+        __syncthreads();
+        if (s_flag[0] != kStOk) {
+            status = s_flag[0];
+            break;
+        }
+        done = t + 1;
+        if (s_flag[1]) break;
+    }
+    for (int64_t k = r0 + tid; k < r1; k += kClusterThreads) p.w_out[k] = w_s[k];
+    if (rank == 0 && tid == 0) {
+        p.status[0] = status;
+        p.status[1] = done;
+    }
+    cluster_sync_all();  // keep every CTA's shared memory alive until all DSMEM stores landed
 }
 
 // ---------------------------------------------------------------------------------------------

@@ -160,19 +160,31 @@ int main() {
     const int iters = 20;
     std::vector<float> ref;
     {
-        std::vector<float> ref2;
-        run_iter(k_iterate_persistent<0, 8, 0, 4, 0, 0>, "rows U4 (per-row kernel)", 512, A, n, b0, w, ws, iters, ref2);
-        run_iter(k_iterate_coop<0, 0, 32>, "coop NW32 (production)", 1024, A, n, b0, w, ws, iters, ref2, 3, coop_smem_bytes(n, 148, 32));
-        run_iter(k_iterate_coop<0, 0, 16>, "coop NW16", 512, A, n, b0, w, ws, iters, ref2, 3, coop_smem_bytes(n, 148, 16));
-        run_iter(k_iterate_coop<0, 1, 32>, "coop NW32 L2-normal", 1024, A, n, b0, w, ws, iters, ref2, 3, coop_smem_bytes(n, 148, 32));
+        std::vector<float> ref2, ref2b;
+        run_iter(k_iterate_coop<0, 0, 32, 2>, "coop NW32 D2 (production)", 1024, A, n, b0, w, ws, iters, ref2, 3, coop_smem_bytes(n, 148, 32));
+        run_iter(k_iterate_coop<0, 0, 32, 3>, "coop NW32 D3", 1024, A, n, b0, w, ws, iters, ref2, 3, coop_smem_bytes(n, 148, 32));
+        run_iter(k_iterate_coop<0, 0, 16, 4>, "coop NW16 D4", 512, A, n, b0, w, ws, iters, ref2b, 3, coop_smem_bytes(n, 148, 16));
+        run_iter(k_iterate_coop<0, 0, 16, 6>, "coop NW16 D6", 512, A, n, b0, w, ws, iters, ref2b, 3, coop_smem_bytes(n, 148, 16));
         // cfg2-size (n = 4096, 64 MiB: may stay L2-resident)
         const int64_t n2 = 4096;
-        std::vector<float> ref3;
+        std::vector<float> ref3, ref4, ref5;
         run_iter(k_iterate_persistent<0, 8, 1, 4, 0, 0>, "n4096 rows U4 L2-normal", 512, A, n2, b0, w, ws, 100, ref3);
-        run_iter(k_iterate_persistent<0, 8, 0, 4, 0, 0>, "n4096 rows U4 evict-first", 512, A, n2, b0, w, ws, 100, ref3);
-        run_iter(k_iterate_coop<0, 1, 16>, "n4096 coop NW16 L2-normal", 512, A, n2, b0, w, ws, 100, ref3, 3, coop_smem_bytes(n2, 148, 16));
-        run_iter(k_iterate_coop<0, 0, 16>, "n4096 coop NW16 evict-first", 512, A, n2, b0, w, ws, 100, ref3, 3, coop_smem_bytes(n2, 148, 16));
-        run_iter(k_iterate_coop<0, 1, 32>, "n4096 coop NW32 L2-normal", 1024, A, n2, b0, w, ws, 100, ref3, 3, coop_smem_bytes(n2, 148, 32));
+        run_iter(k_iterate_persistent<0, 8, 1, 2, 0, 0, 2>, "n4096 rows U2 2CTA/SM", 512, A, n2, b0, w, ws, 100, ref3);
+        run_iter(k_iterate_persistent<0, 8, 1, 4, 0, 0, 2>, "n4096 rows U4 2CTA/SM", 512, A, n2, b0, w, ws, 100, ref3);
+        run_iter(k_iterate_persistent<0, 8, 1, 1, 0, 0, 2>, "n4096 rows U1 2CTA/SM", 512, A, n2, b0, w, ws, 100, ref3);
+        run_iter(k_iterate_persistent<0, 4, 1, 4, 0, 0, 2>, "n4096 rows V4 U4 2CTA/SM", 512, A, n2, b0, w, ws, 100, ref3);
+        const int64_t n3 = 8192;
+        std::vector<float> ref6;
+        run_iter(k_iterate_persistent<0, 8, 1, 4, 0, 0>, "n8192 rows U4", 512, A, n3, b0, w, ws, 100, ref6);
+        run_iter(k_iterate_coop<0, 1, 16, 2>, "n8192 coop NW16", 512, A, n3, b0, w, ws, 100, ref6, 3, coop_smem_bytes(n3, 148, 16));
+        run_iter(k_iterate_coop<0, 1, 32, 2>, "n8192 coop NW32", 1024, A, n3, b0, w, ws, 100, ref6, 3, coop_smem_bytes(n3, 148, 32));
+        run_iter(k_iterate_coop<0, 1, 16, 2>, "n4096 coop NW16 D2", 512, A, n2, b0, w, ws, 100, ref4, 3, coop_smem_bytes(n2, 148, 16));
+        run_iter(k_iterate_coop<0, 1, 16, 4>, "n4096 coop NW16 D4", 512, A, n2, b0, w, ws, 100, ref4, 3, coop_smem_bytes(n2, 148, 16));
+        run_iter(k_iterate_coop<0, 1, 16, 8>, "n4096 coop NW16 D8", 512, A, n2, b0, w, ws, 100, ref4, 3, coop_smem_bytes(n2, 148, 16));
+        run_iter(k_iterate_coop<0, 1, 16, 12>, "n4096 coop NW16 D12", 512, A, n2, b0, w, ws, 100, ref4, 3, coop_smem_bytes(n2, 148, 16));
+        run_iter(k_iterate_coop<0, 0, 16, 8>, "n4096 coop NW16 D8 evict-first", 512, A, n2, b0, w, ws, 100, ref4, 3, coop_smem_bytes(n2, 148, 16));
+        run_iter(k_iterate_coop<0, 1, 32, 2>, "n4096 coop NW32 D2", 1024, A, n2, b0, w, ws, 100, ref5, 3, coop_smem_bytes(n2, 148, 32));
+        run_iter(k_iterate_coop<0, 1, 32, 3>, "n4096 coop NW32 D3", 1024, A, n2, b0, w, ws, 100, ref5, 3, coop_smem_bytes(n2, 148, 32));
     }
     return 0;
 }

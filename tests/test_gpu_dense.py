@@ -246,3 +246,20 @@ def test_cfg3_last_step_and_invariants(mapi_lib, orc, cfg3_device):
     assert abs(np.abs(w100).sum() - 1.0) < 1e-5
     r100b = m.iterate(A, b0, 100)
     assert torch.equal(r100.w, r100b.w)
+
+
+@pytest.mark.parametrize("path", ["cluster", "rows", "coop", "multi"])
+@pytest.mark.parametrize("n", [256, 511, 4096, 8200])
+def test_every_dense_path_matches_oracle(mapi_lib, orc, monkeypatch, path, n):
+    """Each dense iteration kernel (K6 cluster, K2 per-row, K2c cooperative rows, multi-launch),
+    forced through MAPI_DENSE_PATH, against the oracle (T2).  Paths a shape cannot use fall back."""
+    m = mapi_lib
+    r = np.random.default_rng(n)
+    A = r.standard_normal((n, n)).astype(np.float32)
+    A += np.diag(np.abs(r.standard_normal(n)) * 4).astype(np.float32)
+    b0 = np.full(n, 1.0 / np.sqrt(n), np.float32)
+    monkeypatch.setenv("MAPI_DENSE_PATH", path)
+    res = m.iterate(torch.from_numpy(A).cuda(), torch.from_numpy(b0).cuda(), 20)
+    ref = orc.mapi(A, b0, 20)
+    assert res.iters_done == 20
+    _t2(res.w_l2.cpu().numpy(), ref.w, res.norms.cpu().numpy(), ref.norms)
