@@ -219,11 +219,12 @@ __global__ void __launch_bounds__(kMpThreads) k_rank_rows_mp(int64_t n, int64_t 
                                                              const int32_t* stop) {
     __shared__ int32_t s_end[kMpTile + 1];  // row_ptr[i0+1 .. i1+1]
     __shared__ float s_val[kMpTile];        // v[col_idx[k0 .. k1)]
-    __shared__ int32_t c_row[kMpThreads];
-    __shared__ float c_val[kMpThreads];
+    __shared__ float s_fp[kMpThreads];      // segmented prefix of the threads' carries
+    __shared__ int32_t wl_row[kMpThreads / 32], wf_row[kMpThreads / 32];
+    __shared__ float wl_val[kMpThreads / 32];
     __shared__ double red[33];
     if (*(volatile const int32_t*)stop) return;
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int32_t i0 = part_i[blockIdx.x], i1 = part_i[blockIdx.x + 1];
     const int32_t k0 = part_k[blockIdx.x], k1 = part_k[blockIdx.x + 1];
     const int nrows = i1 - i0, nk = k1 - k0;  // nrows + nk == items of this tile
@@ -248,7 +249,7 @@ __global__ void __launch_bounds__(kMpThreads) k_rank_rows_mp(int64_t n, int64_t 
         gpart += (double)xv[u];
     }
     __syncthreads();
-    // this thread's diagonal within the tile
+    // this thread's diagonal within the tile (merge-path search in shared memory)
     const int items = nrows + nk;
     const int dt = min(tid * kMpIpt, items);
     int lo = max(0, dt - nk), hi = min(dt, nrows);
@@ -276,25 +277,40 @@ __global__ void __launch_bounds__(kMpThreads) k_rank_rows_mp(int64_t n, int64_t 
             ++kj;
         }
     }
-    c_row[tid] = ri;  // carry: row still open at this thread's end, and its partial
-    c_val[tid] = acc;
-    __syncthreads();
-    if (first_row >= 0) {  // add the carries of the run of preceding threads open on this row
-        int t0 = tid;
-        while (t0 > 0 && c_row[t0 - 1] == first_row) --t0;
-        float sum = 0.0f;
-        for (int t = t0; t < tid; ++t) sum += c_val[t];
-        e[i0 + first_row] = sum + own_first;
+    // Carries: thread t leaves row ri open with partial acc.  Rows are non-decreasing in t, so the
+    // threads open on one row form a contiguous run; a segmented inclusive scan (keyed by row) gives
+    // each thread the sum of its run so far.  Warp level: Hillis-Steele shuffles; block level: the
+    // trailing runs of the preceding warps, nearest first.  Fixed order -> deterministic.
+    float pv = acc;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const float ov = __shfl_up_sync(0xffffffffu, pv, off);
+        const int orow = __shfl_up_sync(0xffffffffu, ri, off);
+        if (lane >= off && orow == ri) pv += ov;
     }
-    // CTA carry-out: the trailing run of threads still open on the tile's last row
-    if (tid == kMpThreads - 1) {
-        const int last = c_row[kMpThreads - 1];
-        float sum = 0.0f;
-        int t0 = kMpThreads;
-        while (t0 > 0 && c_row[t0 - 1] == last) --t0;
-        for (int t = t0; t < kMpThreads; ++t) sum += c_val[t];
-        carry_row[blockIdx.x] = (last < nrows || (last == nrows && i1 < n)) ? i0 + last : -1;
-        carry_val[blockIdx.x] = sum;
+    if (lane == 31) {
+        wl_row[warp] = ri;
+        wl_val[warp] = pv;
+    }
+    if (lane == 0) wf_row[warp] = ri;
+    __syncthreads();
+    if (ri == wf_row[warp]) {  // my run reaches the start of my warp: add preceding warps' tails
+        float extra = 0.0f;
+        for (int q = warp - 1; q >= 0; --q) {
+            if (wl_row[q] != ri) break;
+            extra += wl_val[q];
+            if (wf_row[q] != ri) break;
+        }
+        pv += extra;
+    }
+    s_fp[tid] = pv;
+    __syncthreads();
+    // the first row this thread emits was left open by thread tid-1 (its carry row is this thread's
+    // start row), so its preceding partials are exactly s_fp[tid-1]
+    if (first_row >= 0) e[i0 + first_row] = (tid > 0 ? s_fp[tid - 1] : 0.0f) + own_first;
+    if (tid == kMpThreads - 1) {  // CTA carry-out: the run still open on the tile's last row
+        carry_row[blockIdx.x] = (ri < nrows || (ri == nrows && i1 < n)) ? i0 + ri : -1;
+        carry_val[blockIdx.x] = pv;
     }
     const double g = block_sum(gpart, red);
     if (tid == 0) gsum[blockIdx.x] = g;
