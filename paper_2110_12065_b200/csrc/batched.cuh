@@ -265,13 +265,25 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-template <int OP>
-__global__ void __launch_bounds__(kB2Threads, 1) k_batched_streamk(const float* __restrict__ A, int64_t n, int64_t lda,
-                                                                   const float* __restrict__ W, int32_t kv,
-                                                                   StreamK plan, float* __restrict__ part) {
+// TV = vectors per thread (8: 256 threads, fold accumulators in registers; 4: 512 threads = 4 warps per
+// scheduler for latency hiding, fold accumulators in shared memory).
+template <int TV>
+struct SkCfg {
+    static constexpr int threads = 32 * (kB2V / TV);
+    static constexpr int vstride = kB2V / TV;      // vectors of a thread: warp + vstride * j
+    static constexpr bool smem_fold = TV == 4;
+};
+
+template <int OP, int TV>
+__global__ void __launch_bounds__(SkCfg<TV>::threads, 1) k_batched_streamk(const float* __restrict__ A, int64_t n,
+                                                                           int64_t lda, const float* __restrict__ W,
+                                                                           int32_t kv, StreamK plan,
+                                                                           float* __restrict__ part) {
+    constexpr int NT = SkCfg<TV>::threads, VS = SkCfg<TV>::vstride, TP = TV / 2;  // TP: vector pairs
     extern __shared__ __align__(16) float smem[];
     float* As = smem;                                   // [stage][256][kB2Ld]
     float* Ws = smem + kB2Stages * kB2M * kB2Ld;        // [stage][64][kB2Ld]
+    unsigned long long* fold = reinterpret_cast<unsigned long long*>(Ws + kB2Stages * kB2V * kB2Ld);  // [8*TP][NT]
     const int tid = threadIdx.x, tr = tid & 31, tv = tid >> 5;
     const int64_t U = plan.units, G = gridDim.x;
     const int64_t u0 = ((int64_t)blockIdx.x * U) / G, u1 = (((int64_t)blockIdx.x + 1) * U) / G;
@@ -279,23 +291,26 @@ __global__ void __launch_bounds__(kB2Threads, 1) k_batched_streamk(const float* 
 
     // load cursor: the (tile, k-stage) of the next stage to stage into shared memory
     int64_t l_tile = u0 / plan.kstages, l_ks = u0 % plan.kstages;
-    const float* pA[8];  // this thread's 8 A chunk rows (tr8 + 32 i) of the current load tile
-    const float* pW[2];  // this thread's 2 W chunk rows (tr8 + 32 i)
-    uint32_t a_ok = 0, w_ok = 0;  // row-in-range masks
+    constexpr int AQ = kB2M * (kB2K / 4) / NT;   // A chunks per thread per stage (8 or 4)
+    constexpr int WQ = kB2V * (kB2K / 4) / NT;   // W chunks per thread per stage (2 or 1)
+    constexpr int RS = NT / 8;                   // row stride between a thread's chunks
+    const float* pA[AQ];
+    const float* pW[WQ];
+    uint32_t a_ok = 0, w_ok = 0;
     const int tr8 = tid >> 3, kq4 = (tid & 7) * 4;
     auto set_tile = [&](int64_t tile) {
         const int64_t rt = tile / plan.vec_tiles, vt = tile - rt * plan.vec_tiles;
         const int64_t row0 = rt * kB2M, v0 = vt * kB2V;
         a_ok = w_ok = 0;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int64_t row = row0 + tr8 + 32 * i;
+        for (int i = 0; i < AQ; ++i) {
+            const int64_t row = row0 + tr8 + RS * i;
             pA[i] = A + (row < n ? row : 0) * lda + kq4;
             a_ok |= (row < n ? 1u : 0u) << i;
         }
 #pragma unroll
-        for (int i = 0; i < 2; ++i) {
-            const int64_t v = v0 + tr8 + 32 * i;
+        for (int i = 0; i < WQ; ++i) {
+            const int64_t v = v0 + tr8 + RS * i;
             pW[i] = W + (v < kv ? v : 0) * n + kq4;
             w_ok |= (v < kv ? 1u : 0u) << i;
         }
@@ -307,14 +322,14 @@ __global__ void __launch_bounds__(kB2Threads, 1) k_batched_streamk(const float* 
         float* as = As + slot * kB2M * kB2Ld + tr8 * kB2Ld + kq4;
         float* ws = Ws + slot * kB2V * kB2Ld + tr8 * kB2Ld + kq4;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
+        for (int i = 0; i < AQ; ++i) {
             const bool in = k_in && ((a_ok >> i) & 1u);
-            cp_async16(as + 32 * i * kB2Ld, in ? (const void*)(pA[i] + k0) : (const void*)A, in ? 16 : 0);
+            cp_async16(as + RS * i * kB2Ld, in ? (const void*)(pA[i] + k0) : (const void*)A, in ? 16 : 0);
         }
 #pragma unroll
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < WQ; ++i) {
             const bool in = k_in && ((w_ok >> i) & 1u);
-            cp_async16(ws + 32 * i * kB2Ld, in ? (const void*)(pW[i] + k0) : (const void*)W, in ? 16 : 0);
+            cp_async16(ws + RS * i * kB2Ld, in ? (const void*)(pW[i] + k0) : (const void*)W, in ? 16 : 0);
         }
         if (++l_ks == plan.kstages) {
             l_ks = 0;
@@ -322,11 +337,21 @@ __global__ void __launch_bounds__(kB2Threads, 1) k_batched_streamk(const float* 
         }
     };
 
-    unsigned long long acc[8][4], tot[8][4];
+    unsigned long long acc[8][TP];
+    unsigned long long tot[SkCfg<TV>::smem_fold ? 1 : 8][SkCfg<TV>::smem_fold ? 1 : TP];
 #pragma unroll
     for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = tot[i][j] = 0ull;
+        for (int j = 0; j < TP; ++j) acc[i][j] = 0ull;
+    if constexpr (SkCfg<TV>::smem_fold) {
+#pragma unroll
+        for (int q = 0; q < 8 * TP; ++q) fold[q * NT + tid] = 0ull;
+    } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int j = 0; j < TP; ++j) tot[i][j] = 0ull;
+    }
 
     const int64_t nst = u1 - u0;
     load_next(0);
@@ -346,18 +371,18 @@ __global__ void __launch_bounds__(kB2Threads, 1) k_batched_streamk(const float* 
         slot = slot == kB2Stages - 1 ? 0 : slot + 1;
 #pragma unroll 2
         for (int kq = 0; kq < kB2K; kq += 4) {
-            float4 a4[8], w4[8];
+            float4 a4[8], w4[TV];
 #pragma unroll
             for (int i = 0; i < 8; ++i) a4[i] = *reinterpret_cast<const float4*>(as + i * 32 * kB2Ld + kq);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) w4[j] = *reinterpret_cast<const float4*>(ws + j * 8 * kB2Ld + kq);
+            for (int j = 0; j < TV; ++j) w4[j] = *reinterpret_cast<const float4*>(ws + j * VS * kB2Ld + kq);
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
                     const float a = c == 0 ? a4[i].x : c == 1 ? a4[i].y : c == 2 ? a4[i].z : a4[i].w;
 #pragma unroll
-                    for (int jp = 0; jp < 4; ++jp) {
+                    for (int jp = 0; jp < TP; ++jp) {
                         const float4& x0 = w4[2 * jp];
                         const float4& x1 = w4[2 * jp + 1];
                         const float w0 = c == 0 ? x0.x : c == 1 ? x0.y : c == 2 ? x0.z : x0.w;
@@ -372,8 +397,13 @@ __global__ void __launch_bounds__(kB2Threads, 1) k_batched_streamk(const float* 
 #pragma unroll
             for (int i = 0; i < 8; ++i)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    tot[i][j] = fadd2(tot[i][j], acc[i][j]);
+                for (int j = 0; j < TP; ++j) {
+                    if constexpr (SkCfg<TV>::smem_fold) {
+                        unsigned long long& f = fold[(i * TP + j) * NT + tid];
+                        f = fadd2(f, acc[i][j]);
+                    } else {
+                        tot[i][j] = fadd2(tot[i][j], acc[i][j]);
+                    }
                     acc[i][j] = 0ull;
                 }
             nfold = 0;
@@ -385,11 +415,18 @@ __global__ void __launch_bounds__(kB2Threads, 1) k_batched_streamk(const float* 
 #pragma unroll
             for (int i = 0; i < 8; ++i)
 #pragma unroll
-                for (int jp = 0; jp < 4; ++jp) {
-                    const int r = tr + 32 * i, v = tv + 8 * (2 * jp);
-                    out[(int64_t)v * kB2M + r] = lo_of(tot[i][jp]);
-                    out[(int64_t)(v + 8) * kB2M + r] = hi_of(tot[i][jp]);
-                    tot[i][jp] = 0ull;
+                for (int jp = 0; jp < TP; ++jp) {
+                    const int r = tr + 32 * i, v = tv + VS * (2 * jp);
+                    unsigned long long x;
+                    if constexpr (SkCfg<TV>::smem_fold) {
+                        x = fold[(i * TP + jp) * NT + tid];
+                        fold[(i * TP + jp) * NT + tid] = 0ull;
+                    } else {
+                        x = tot[i][jp];
+                        tot[i][jp] = 0ull;
+                    }
+                    out[(int64_t)v * kB2M + r] = lo_of(x);
+                    out[(int64_t)(v + VS) * kB2M + r] = hi_of(x);
                 }
         }
         if (++c_ks == plan.kstages) {
@@ -425,7 +462,11 @@ inline size_t streamk_part_bytes(int64_t n, int32_t k) {
     const int64_t tiles = ((n + kB2M - 1) / kB2M) * ((k + kB2V - 1) / kB2V);
     return sizeof(float) * (size_t)tiles * kMaxParts * kB2V * kB2M;
 }
-inline size_t streamk_smem_bytes() { return sizeof(float) * kB2Stages * (kB2M + kB2V) * kB2Ld; }
+template <int TV>
+inline size_t streamk_smem_bytes() {
+    return sizeof(float) * kB2Stages * (kB2M + kB2V) * kB2Ld +
+           (SkCfg<TV>::smem_fold ? sizeof(unsigned long long) * 8 * (TV / 2) * SkCfg<TV>::threads : 0);
+}
 
 static thread_local char g_batched_err[256] = "";
 inline const char* batched_last_error() { return g_batched_err; }
@@ -461,19 +502,24 @@ inline mapi_status batched_run(int32_t op, const float* A, int64_t n, int64_t ld
     const bool v2 = !(env && strcmp(env, "v1") == 0) && reinterpret_cast<uintptr_t>(A) % 16 == 0 && lda % 4 == 0 &&
                     n % 4 == 0 && streamk_ok(n, k, sms);
     const StreamK plan = streamk_plan(n, k, sms);
+    // v2 (256 threads, 8x8 register tiles) is the default; MAPI_BATCHED_PATH=v3 selects the 512-thread
+    // 8x4 variant with the fold in shared memory (measured 63.5% vs 64.5% of the FMNMX peak at cfg4)
+    const bool v3 = env && strcmp(env, "v3") == 0;
+    auto k2 = op == 1 ? k_batched_streamk<1, 8> : k_batched_streamk<0, 8>;
+    auto k3 = op == 1 ? k_batched_streamk<1, 4> : k_batched_streamk<0, 4>;
+    const size_t sm2 = streamk_smem_bytes<8>(), sm3 = streamk_smem_bytes<4>();
     if (v2) {
-        auto kern = op == 1 ? k_batched_streamk<1> : k_batched_streamk<0>;
-        if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)streamk_smem_bytes())) !=
+        if ((e = cudaFuncSetAttribute(v3 ? k3 : k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(v3 ? sm3 : sm2))) !=
             cudaSuccess)
             return batched_cuda_fail(e, "smem attribute");
     }
     if (timing) cudaEventRecord(*ev_a, s);
     for (int32_t t = 0; t < iters; ++t) {
         if (v2) {
-            if (op == 1)
-                k_batched_streamk<1><<<plan.grid, kB2Threads, streamk_smem_bytes(), s>>>(A, n, lda, B.W, k, plan, B.part);
+            if (v3)
+                k3<<<plan.grid, SkCfg<4>::threads, sm3, s>>>(A, n, lda, B.W, k, plan, B.part);
             else
-                k_batched_streamk<0><<<plan.grid, kB2Threads, streamk_smem_bytes(), s>>>(A, n, lda, B.W, k, plan, B.part);
+                k2<<<plan.grid, SkCfg<8>::threads, sm2, s>>>(A, n, lda, B.W, k, plan, B.part);
             k_batched_reduce2<<<gr, 256, 0, s>>>(n, k, plan, plan.grid, B.part, B.Y, B.colpart, B.rb);
         } else {
             if (op == 1)

@@ -98,3 +98,21 @@ def test_cfg4_full_size(mapi_lib, orc, cfg4):
         ref = orc.mapi(A_host, cfg4["B0"][v], T)
         _t2(W[v], ref.w)
         np.testing.assert_allclose(norms[:, v], ref.norms, rtol=1e-5)
+
+
+@pytest.mark.parametrize("path", ["v1", "v2", "v3"])
+@pytest.mark.parametrize("n,k", [(300, 64), (1028, 70), (2048, 5)])
+def test_batched_every_kernel(mapi_lib, orc, monkeypatch, path, n, k):
+    """Each batched kernel (v1 split-K, v2 stream-K 8x8, v3 stream-K 8x4 + smem fold) vs the oracle."""
+    m = mapi_lib
+    r = np.random.default_rng(n + k)
+    A = (r.standard_normal((n, n)) + np.eye(n) * 3).astype(np.float32)
+    B0 = r.standard_normal((k, n))
+    B0 = (B0 / np.linalg.norm(B0, axis=1, keepdims=True)).astype(np.float32)
+    monkeypatch.setenv("MAPI_BATCHED_PATH", path)
+    res = m.iterate_batched(torch.from_numpy(A).cuda(), torch.from_numpy(B0).cuda(), 15)
+    W = res.W.cpu().numpy()
+    for v in sorted({0, k - 1}):
+        ref = orc.mapi(A, B0[v], 15)
+        _t2(W[v], ref.w)
+        np.testing.assert_allclose(res.norms.cpu().numpy()[:, v], ref.norms, rtol=1e-5)
