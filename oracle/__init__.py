@@ -63,6 +63,8 @@ def _load():
         lib.orc_power_iterate.argtypes = [cint, cint, P, cint, i64, i64, P, i32, dbl, P, P, P, P,
                                           ctypes.POINTER(i32)]
         lib.orc_power_iterate.restype = cint
+        lib.orc_matmat_f32.argtypes = [cint, P, i64, i64, i64, P, i64, i64, dbl, P]
+        lib.orc_matmat_f32.restype = None
         lib.orc_deflate.argtypes = [P, i64, i64, P, i32, P]
         lib.orc_deflate.restype = None
         lib.orc_pca_topk.argtypes = [cint, P, i64, i64, i32, i32, P, P, P, P, P]
@@ -110,6 +112,8 @@ def _as_f32_matrix(A):
     A = np.asarray(A)
     if A.dtype != np.float32:
         raise TypeError("oracle matrices are the fp32 input bytes (dtype float32)")
+    if A.ndim == 2 and A.size == 0:
+        return np.ascontiguousarray(A), max(1, A.shape[1])
     if A.ndim != 2 or A.strides[1] != 4:
         raise ValueError("A must be a 2-D row-major float32 array")
     lda = A.strides[0] // 4
@@ -195,6 +199,27 @@ def mapi(A, b0, iters, tol=0.0, op="min1") -> IterResult:
 def rpi(A, b0, iters, tol=0.0) -> IterResult:
     """Regular power iteration, Eq.(1): b <- Ab / ||Ab||_2."""
     return power_iterate(A, b0, iters, tol, "dot", NORM_L2)
+
+
+def matmat(A, B, op="min1", d=1.0) -> np.ndarray:
+    """C[i][j] = (row_i(A) (op) row_j(B)) / d — matrix extension; A, B fp32 row-major."""
+    A, lda = _as_f32_matrix(A)
+    B, ldb = _as_f32_matrix(B)
+    m, K = A.shape
+    p, K2 = B.shape
+    if K != K2:
+        raise ValueError(f"dimension mismatch: A is {m}x{K}, B is {p}x{K2}")
+    C = np.empty((m, p), np.float64)
+    _load().orc_matmat_f32(_op(op), _ptr(A), m, K, lda, _ptr(B), p, ldb, float(d), _ptr(C))
+    return C
+
+
+def min_covariance(V, divisor=None, op="min1") -> np.ndarray:
+    """Min-covariance (1/d) V (+) V^T of mean-removed samples V (pixels x N): d = N - 1 as in Alg. 2
+    step 4 by default; d = N reproduces Eq. (5)."""
+    V = np.asarray(V)
+    d = (V.shape[1] - 1) if divisor is None else divisor
+    return matmat(V, V, op, d)
 
 
 def deflate(C, P, i) -> np.ndarray:

@@ -166,6 +166,22 @@ int orc_power_iterate(int op, int norm, const void *A, int a_is_f64, int64_t n, 
     return status;
 }
 
+/* MAVP matrix product, the matrix extension (reading Q7: entry (i,j) = w_i^T (op) x_j) with the
+ * vectors stored as ROWS:  C[i][j] = ( a_i (op) b_j ) / d,  a_i = row i of A (m x K, lda),
+ * b_j = row j of B (p x K, ldb).  With A = B = V (pixels x samples) and d = N-1 this is the
+ * min-covariance of Alg. 2 step 4; d = N gives Eq. (5).  fp64, k in index order. */
+void orc_matmat_f32(int op, const float *A, int64_t m, int64_t K, int64_t lda, const float *B, int64_t p,
+                    int64_t ldb, double d, double *C) {
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < m; ++i) {
+        for (int64_t j = 0; j < p; ++j) {
+            double acc = 0.0;
+            for (int64_t k = 0; k < K; ++k) acc += orc_term(op, (double)A[i * lda + k], (double)B[j * ldb + k]);
+            C[i * p + j] = acc / d;
+        }
+    }
+}
+
 /* L2 deflation: the i-th principal vector is extracted by power iteration on
  *     D_i = (I - sum_{m<i} p_m p_m^T) C,
  * with p_m the l2-normalised MAPI outputs.  Expanded entry-wise:

@@ -420,3 +420,42 @@ def test_paper_printed_rank_orders(orc):
 
 def test_rank_order_ties_by_index(orc):
     assert list(orc.rank_order([0.5, 0.7, 0.5, 0.7])) == [1, 3, 0, 2]
+
+
+# ---------------------------------------------------------------- matrix extension / min-covariance (NEXT-1)
+
+
+@pytest.mark.parametrize("op", ["min1", "min2", "dot"])
+def test_matmat_vs_brute(orc, op):
+    r = np.random.default_rng(71)
+    for trial in range(25):
+        m, p, K = (int(x) for x in r.integers(1, 8, size=3))
+        A = r.standard_normal((m, K)).astype(np.float32)
+        B = r.standard_normal((p, K)).astype(np.float32)
+        A[r.random(A.shape) < 0.1] = 0.0
+        C = orc.matmat(A, B, op, d=3.0)
+        f = brute.OPS[op]
+        for i in range(m):
+            for j in range(p):
+                assert C[i, j] == pytest.approx(f(A[i], B[j]) / 3.0, rel=1e-14, abs=1e-300)
+
+
+def test_matmat_spec_examples(orc):
+    # W = X = [[1],[-2]] (one column; vectors as rows here: one vector [1,-2]) -> [[3]]
+    v = np.array([[1.0, -2.0]], np.float32)
+    assert orc.matmat(v, v).tolist() == [[3.0]]
+    # empty p -> m x 0
+    assert orc.matmat(v, np.zeros((0, 2), np.float32)).shape == (1, 0)
+
+
+def test_min_covariance_properties(orc):
+    r = np.random.default_rng(72)
+    V = r.standard_normal((40, 10))
+    V -= V.mean(axis=1, keepdims=True)
+    V = V.astype(np.float32)
+    C = orc.min_covariance(V)
+    np.testing.assert_array_equal(C, C.T)  # min1 is symmetric (exact)
+    np.testing.assert_allclose(np.diag(C), np.abs(V.astype(np.float64)).sum(axis=1) / 9, rtol=1e-14)
+    assert np.all(np.abs(C) <= np.diag(C)[:, None] + 1e-15)  # |a (+) b| <= min(||a||_1, ||b||_1)
+    C5 = orc.min_covariance(V, divisor=10)  # Eq. (5) divisor N
+    np.testing.assert_allclose(C5 * 10, C * 9, rtol=1e-14)
