@@ -38,6 +38,10 @@ WORKLOADS = {
     "cfg4": "batched: 16384^2 A (G 16384x256, seed 3), k=64 N(0,1) starts, 100 iterations",
     "cfg5": "graph ranking: R-MAT 2^22 nodes / 2^26 edges (seed 4), MAPI on G = 0.85 M + 0.15/n, "
             "200 fixed iterations (tol 0) for steady state",
+    "mincov": "NEXT-1 min-covariance (Alg. 2 step 4): V = 128x128 synthetic image, N = 10 occluded copies "
+              "(seed 6), C = V (+) V^T / (N-1), 16384^2 fp32 output",
+    "mincov_k4096": "NEXT-1 MAVP matrix product, ALU-bound regime: 4096 x 8192 N(0,1) rows (seed 7), "
+                    "C = V (+) V^T / 8192, 4096^2 output",
 }
 METRIC = "MAPI iterations/s and achieved HBM GB/s (% of B200 peak) at n=32768 fp32"
 
@@ -288,8 +292,40 @@ def build_rank(args, m, dev, stream):
                 oracle=("rank", cfg))
 
 
+def build_mincov(args, m, dev, stream):
+    import torch
+
+    import synth
+
+    if args.workload == "mincov":
+        V, _ = synth.occluded_images()
+        d = V.shape[1] - 1
+    else:
+        V = np.random.default_rng(7).standard_normal((4096, 8192)).astype(np.float32)
+        d = 8192
+    Vd = torch.from_numpy(V).to(dev)
+    n, K = V.shape
+    C = torch.empty(n, n, device=dev)
+    lib = m.load()
+
+    def step():
+        _abi_check(lib, lib.mapi_mavp_matmat(0, Vd.data_ptr(), n, K, Vd.stride(0), Vd.data_ptr(), n, Vd.stride(0),
+                                             float(d), C.data_ptr(), n, stream.cuda_stream))
+        return 1
+
+    out_bytes = 4.0 * n * n + 8.0 * n * K
+    small = args.workload == "mincov"
+    return Work(step=step, unit="matrices/s", per_launch=out_bytes if small else float(n) * n * K,
+                bytes_per_unit=out_bytes, bound="hbm" if small else "alu",
+                kernel="k_mavp_matmat (K8, one launch per matrix)",
+                config={"workload": f"{args.workload}: {WORKLOADS[args.workload]}", "m": n, "p": n, "K": K,
+                        "divisor": d, "op": "min1",
+                        "l2_flush": "output (1 GiB) larger than L2" if small else "none: ALU-bound"},
+                oracle=None)
+
+
 BUILDERS = {"cfg1": build_dense, "cfg3": build_dense, "cfg2": build_pca, "cfg4": build_batched,
-            "cfg5": build_rank}
+            "cfg5": build_rank, "mincov": build_mincov, "mincov_k4096": build_mincov}
 
 
 def alu_peak_terms_per_s(sm_mhz):
@@ -378,7 +414,7 @@ def run_mapi(args, rank, world, local_rank):
     out["clocks"] = clocks
     if args.workload == "cfg3" and not args.no_e2e:
         out["e2e"] = e2e_dense(args, m, work.A, work.b0, work.iters, dev, stream, world, dist)
-    if not args.no_cpu_baseline and world == 1 and rank == 0:
+    if not args.no_cpu_baseline and world == 1 and rank == 0 and work.oracle is not None:
         if work.oracle[0] == "dense":
             out["cpu_baseline"] = cpu_baseline_dense(args, *work.oracle[1:])
         else:

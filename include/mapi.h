@@ -71,6 +71,17 @@ typedef enum {
 mapi_status mapi_mavp_matvec(int32_t op, const float *A, int64_t n_rows, int64_t n_cols,
                              int64_t lda, const float *x, float *y, mapi_stream_t stream);
 
+/* MAVP matrix product — the matrix extension of P:69-70 with the vectors as rows (reading Q7):
+ *     C[i*ldc + j] = (1/divisor) * ( sum_k A[i*lda + k] (op) B[j*ldb + k] )
+ * (the scalar factor of Eq. 5 is applied as one fp32 multiply by fp32(1/divisor) per element)
+ * A: m x K (lda >= K), B: p x K (ldb >= K), C: m x p (ldc >= p), divisor > 0 (1 for the plain product).
+ * With B = A = V (pixels x N mean-removed samples) this is the min-covariance: divisor N-1 as in
+ * Alg. 2 step 4, N as in Eq. (5).  C must not alias A or B.  K == 0 gives C = 0;
+ * m == 0 or p == 0 is a no-op.  Asynchronous. */
+mapi_status mapi_mavp_matmat(int32_t op, const float *A, int64_t m, int64_t K, int64_t lda, const float *B,
+                             int64_t p, int64_t ldb, float divisor, float *C, int64_t ldc,
+                             mapi_stream_t stream);
+
 /* MAPI, Eq.(8) / Algorithm 1:
  *     w_0 = b0 (used as given; Q2)
  *     for t = 0..iters-1:  y = A (op) w_t;  s_t = ||y||_1;  w_{t+1} = y / s_t;

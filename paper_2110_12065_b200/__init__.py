@@ -18,7 +18,7 @@ from typing import Optional
 from ._build import LIB as _LIB_PATH
 from ._build import build  # noqa: F401  (re-exported: compile in-tree)
 
-__all__ = ["load", "build", "MapiError", "mavp_matvec", "iterate", "iterate_host", "iterate_batched",
+__all__ = ["load", "build", "MapiError", "mavp_matvec", "mavp_matmat", "min_covariance", "iterate", "iterate_host", "iterate_batched",
            "pca_topk", "csr_prepare", "rank_csr", "workspace_size", "launch_count", "set_profiling",
            "last_kernel_ms", "MIN1", "MIN2"]
 
@@ -55,6 +55,7 @@ def load():
         st = ctypes.c_int
         sig = {
             "mapi_mavp_matvec": (st, [i32, P, i64, i64, i64, P, P, P]),
+            "mapi_mavp_matmat": (st, [i32, P, i64, i64, i64, P, i64, i64, f32, P, i64, P]),
             "mapi_iterate": (st, [i32, P, i64, i64, P, i32, f32, P, P, P, P, P, P, sz, P]),
             "mapi_iterate_host": (st, [i32, P, i64, i64, P, i32, f32, P, P, P, P, P, P, sz, P]),
             "mapi_iterate_batched": (st, [i32, P, i64, i64, P, i32, i32, f32, P, P, P, P, P, sz, P]),
@@ -162,6 +163,30 @@ def mavp_matvec(A, x, y=None, op: int = MIN1, stream=None):
     _need(y, "y", torch.float32, (n_rows,))
     _check(load().mapi_mavp_matvec(op, _ptr(A), n_rows, n_cols, lda, _ptr(x), _ptr(y), _stream(stream)))
     return y
+
+
+def mavp_matmat(A, B, divisor: float = 1.0, C=None, op: int = MIN1, stream=None):
+    """C[i][j] = (row_i(A) (op) row_j(B)) / divisor — matrix extension; asynchronous."""
+    torch = _torch()
+    m, K, lda = _matrix(A, "A")
+    p, K2, ldb = _matrix(B, "B")
+    if K != K2:
+        raise ValueError(f"dimension mismatch: A is {m}x{K}, B is {p}x{K2}")
+    if C is None:
+        C = torch.empty(m, p, dtype=torch.float32, device=A.device)
+    _need(C, "C", torch.float32)
+    if C.dim() != 2 or tuple(C.shape) != (m, p) or (C.numel() and C.stride(1) != 1):
+        raise ValueError(f"C must be a row-major ({m}, {p}) fp32 tensor")
+    _check(load().mapi_mavp_matmat(op, _ptr(A), m, K, lda, _ptr(B), p, ldb, float(divisor), _ptr(C),
+                                   C.stride(0) if C.numel() else p, _stream(stream)))
+    return C
+
+
+def min_covariance(V, divisor=None, op: int = MIN1, stream=None):
+    """Min-covariance (1/d) V (+) V^T of mean-removed samples V (pixels x N) (Eq. 5):
+    d = N - 1 by default as in Alg. 2 step 4."""
+    d = (V.shape[1] - 1) if divisor is None else divisor
+    return mavp_matmat(V, V, float(d), op=op, stream=stream)
 
 
 @dataclass

@@ -15,6 +15,7 @@
 #include "csr.cuh"
 #include "deflate.cuh"
 #include "dense.cuh"
+#include "matmat.cuh"
 
 using namespace mapi;
 
@@ -499,6 +500,49 @@ mapi_status mapi_mavp_matvec(int32_t op, const float* A, int64_t n_rows, int64_t
         });
     });
     return st;
+}
+
+mapi_status mapi_mavp_matmat(int32_t op, const float* A, int64_t m, int64_t K, int64_t lda, const float* B,
+                             int64_t p, int64_t ldb, float divisor, float* C, int64_t ldc, mapi_stream_t stream) {
+    mapi_status st = check_op(op);
+    if (st != MAPI_OK) return st;
+    if (m < 0 || K < 0 || p < 0)
+        return fail(MAPI_ERR_SHAPE, "negative size: m %lld, K %lld, p %lld", (long long)m, (long long)K, (long long)p);
+    if (lda < K) return fail(MAPI_ERR_SHAPE, "lda (%lld) < K (%lld)", (long long)lda, (long long)K);
+    if (ldb < K) return fail(MAPI_ERR_SHAPE, "ldb (%lld) < K (%lld)", (long long)ldb, (long long)K);
+    if (ldc < p) return fail(MAPI_ERR_SHAPE, "ldc (%lld) < p (%lld)", (long long)ldc, (long long)p);
+    if (!(divisor > 0.0f) || isinf(divisor))
+        return fail(MAPI_ERR_BAD_PARAM, "divisor (%g) must be finite and > 0", (double)divisor);
+    if (m == 0 || p == 0) return MAPI_OK;
+    if (!C) return fail(MAPI_ERR_NULL, "C is NULL");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (K == 0) {
+        MAPI_CUDA(cudaMemset2DAsync(C, sizeof(float) * (size_t)ldc, 0, sizeof(float) * (size_t)p, (size_t)m, s));
+        return MAPI_OK;
+    }
+    if (!A || !B) return fail(MAPI_ERR_NULL, "A or B is NULL");
+    Device d;
+    if ((st = device_info(d)) != MAPI_OK) return st;
+    const bool async = reinterpret_cast<uintptr_t>(A) % 16 == 0 && reinterpret_cast<uintptr_t>(B) % 16 == 0 &&
+                       lda % 4 == 0 && ldb % 4 == 0 && K % 4 == 0;  // 16 B chunks never cross K
+    const int64_t ntiles = ((p + kMmJ - 1) / kMmJ) * ((m + kMmI - 1) / kMmI);
+    const size_t smem = matmat_smem_bytes();
+    auto kern = op == 1 ? (async ? k_mavp_matmat<1, true> : k_mavp_matmat<1, false>)
+                        : (async ? k_mavp_matmat<0, true> : k_mavp_matmat<0, false>);
+    MAPI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int occ = 1;
+    MAPI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kMmThreads, smem));
+    const unsigned grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)std::max(occ, 1) * d.sms);
+    Timer timer(s);
+    timer.start();
+    kern<<<grid, kMmThreads, smem, s>>>(A, m, K, lda, B, p, ldb, divisor, C, ldc);
+    timer.stop();
+    MAPI_LAUNCHED();
+    if (timer.on) {
+        MAPI_CUDA(cudaStreamSynchronize(s));
+        timer.harvest();
+    }
+    return MAPI_OK;
 }
 
 mapi_status mapi_iterate(int32_t op, const float* A, int64_t n, int64_t lda, const float* b0, int32_t iters,
