@@ -56,6 +56,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=15.0, help="budget of the oracle sample")
+    p.add_argument("--op", default="min1", choices=["min1", "min2", "dot"],
+                   help="MAVP operator (Eq. 3 / Eq. 4) or 'dot' = the RPI comparator of Eq. (1) (dense workloads)")
     return p.parse_args()
 
 
@@ -80,6 +82,30 @@ def peaks():
             d = json.load(f)
         return float(d["hbm_gbs"]), "measured"
     return 6650.0, "fallback"
+
+
+class EnergyMeter:
+    """Board energy over the timed region from NVML's total-energy counter (mJ), if available."""
+
+    def __init__(self, index):
+        self.h = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.nv.nvmlDeviceGetTotalEnergyConsumption(self.h)
+        except Exception:
+            self.h = None
+
+    def read(self):
+        if self.h is None:
+            return None
+        try:
+            return float(self.nv.nvmlDeviceGetTotalEnergyConsumption(self.h)) / 1e3  # J
+        except Exception:
+            return None
 
 
 class ClockSampler:
@@ -178,8 +204,10 @@ def build_dense(args, m, dev, stream):
     lib = m.load()
     done = ctypes.c_int32(0)
 
+    opc = {"min1": 0, "min2": 1, "dot": 2}[args.op]
+
     def step():
-        _abi_check(lib, lib.mapi_iterate(0, A.data_ptr(), n, lda, b0.data_ptr(), iters, 0.0, w.data_ptr(),
+        _abi_check(lib, lib.mapi_iterate(opc, A.data_ptr(), n, lda, b0.data_ptr(), iters, 0.0, w.data_ptr(),
                                          wl2.data_ptr(), norms.data_ptr(), deltas.data_ptr(), ctypes.byref(done),
                                          ws.data_ptr(), need, stream.cuda_stream))
         return iters
@@ -190,7 +218,8 @@ def build_dense(args, m, dev, stream):
                 kernel="k_iterate_coop (K2c: one cooperative launch runs all iterations of a step)"
                 if big else "k_iterate_persistent (K2, one cooperative launch per step)",
                 config={"workload": f"{args.workload}: {WORKLOADS[args.workload]}", "n": n, "lda": lda,
-                        "iters_per_step": iters, "op": "min1",
+                        "iters_per_step": iters,
+                        "op": args.op if args.op != "dot" else "dot (RPI comparator, Eq. 1, l2 normalisation)",
                         "l2_flush": "inputs larger than L2 (4 GiB matrix vs 126 MB L2)" if big else
                         "none: the 256 KiB matrix is meant to stay on chip (latency-bound case)"},
                 A=A, b0=b0, iters=iters, oracle=("dense", A, b0, iters))
@@ -351,6 +380,8 @@ def run_mapi(args, rank, world, local_rank):
     torch.cuda.synchronize()
 
     metric = METRIC if args.workload == "cfg3" else f"MAPI {work.unit} ({args.workload})"
+    if args.op == "dot":
+        metric = f"RPI (Eq. 1 comparator) {work.unit} ({args.workload})"
     out = {"metric": metric, "unit": work.unit, "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
            "dtype": "f32", "data": "synthetic (seeded recipes, DESIGN.md §5)", "impl": "mapi-b200"}
@@ -362,6 +393,7 @@ def run_mapi(args, rank, world, local_rank):
     torch.cuda.synchronize()
 
     sampler = ClockSampler(local_rank)
+    meter = EnergyMeter(local_rank)
     m.set_profiling(True)
     kernel_ms = []
     if dist:
@@ -372,6 +404,7 @@ def run_mapi(args, rank, world, local_rank):
     time.sleep(0.3)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
+    e0 = meter.read()
     t_wall = time.perf_counter()
     units = 0
     for _ in range(args.steps):
@@ -380,6 +413,7 @@ def run_mapi(args, rank, world, local_rank):
     ev1.record(stream)
     torch.cuda.synchronize()
     t_wall = time.perf_counter() - t_wall
+    e1 = meter.read()
     launches = m.launch_count() - launches0
     clocks = sampler.stop()
     m.set_profiling(False)
@@ -412,6 +446,9 @@ def run_mapi(args, rank, world, local_rank):
                            "kernel_ms_avg": kavg, "kernel_share_of_step": kavg / (elapsed_ms / args.steps),
                            "traffic": traffic}
     out["clocks"] = clocks
+    if e0 is not None and e1 is not None and e1 > e0:
+        out["energy"] = {"joules": e1 - e0, "joules_per_unit": (e1 - e0) / units, "unit": work.unit.split("/")[0],
+                         "avg_power_w": (e1 - e0) / t_wall, "source": "NVML total energy counter, timed region"}
     if args.workload == "cfg3" and not args.no_e2e:
         out["e2e"] = e2e_dense(args, m, work.A, work.b0, work.iters, dev, stream, world, dist)
     if not args.no_cpu_baseline and world == 1 and rank == 0 and work.oracle is not None:

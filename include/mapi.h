@@ -21,7 +21,8 @@
  *    e.g. "lda (100) < n_cols (128)".  Argument validation happens before any launch, so a
  *    validation error leaves all outputs untouched.  MAPI_ERR_CUDA wraps a CUDA runtime
  *    error (message = cudaGetErrorString).
- *  - Operator `op`: MAPI_OP_MIN1 = Eq.(3), MAPI_OP_MIN2 = Eq.(4).
+ *  - Operator `op`: MAPI_OP_MIN1 = Eq.(3), MAPI_OP_MIN2 = Eq.(4);
+ *    MAPI_OP_DOT = Eq.(1) (RPI comparator, see mapi_op).
  *  - Arithmetic: fp32, IEEE round-to-nearest adds, div.rn for the l1 normalisation (P:146
  *    "N divisions"), no FTZ, no fast-math; the MAVP loops contain no multiplication (P:5).
  *  - Determinism: every reduction has a fixed order for a given device and shape, so repeated
@@ -51,7 +52,11 @@ typedef enum {
     MAPI_ERR_CUDA = 8        /* CUDA runtime error, or no sm_100 device */
 } mapi_status;
 
-typedef enum { MAPI_OP_MIN1 = 0, MAPI_OP_MIN2 = 1 } mapi_op;
+/* MAPI_OP_MIN1: Eq.(3); MAPI_OP_MIN2: Eq.(4); MAPI_OP_DOT: the regular product of
+ * Eq.(1), the RPI comparator: accepted by mapi_mavp_matvec, mapi_iterate(_host)
+ * and mapi_pca_topk, where it also switches the normalisation to l2 (b <- Ab/||Ab||_2, norms[t] =
+ * ||A w_t||_2); the batched, matmat and ranking entry points take MIN1/MIN2 only. */
+typedef enum { MAPI_OP_MIN1 = 0, MAPI_OP_MIN2 = 1, MAPI_OP_DOT = 2 } mapi_op;
 
 /* Workspace query ids (first argument of mapi_workspace_size). */
 typedef enum {

@@ -224,7 +224,9 @@ int orc_pca_topk(int op, const float *C, int64_t n, int64_t ldc, int32_t k, int3
     for (int32_t i = 0; i < k; ++i) {
         orc_deflate(C, n, ldc, P, i, D);
         int32_t done = 0;
-        status = orc_power_iterate(op, ORC_NORM_L1, D, 1, n, n, b0, T, 0.0, NULL,
+        /* MAVP operators use the l1 normalisation of Eq. (8); the regular product (RPI comparator)
+         * the l2 normalisation of Eq. (1) */
+        status = orc_power_iterate(op, op == ORC_DOT ? ORC_NORM_L2 : ORC_NORM_L1, D, 1, n, n, b0, T, 0.0, NULL,
                                    P + (int64_t)i * n, norms ? norms + (int64_t)i * T : NULL,
                                    deltas ? deltas + (int64_t)i * T : NULL, &done);
         if (iters_done) iters_done[i] = done;

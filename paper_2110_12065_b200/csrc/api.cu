@@ -91,7 +91,7 @@ using IC = std::integral_constant<int, V>;
 
 template <typename F>
 auto with_op(int op, F&& f) {
-    return op == 1 ? f(IC<1>{}) : f(IC<0>{});
+    return op == 2 ? f(IC<2>{}) : (op == 1 ? f(IC<1>{}) : f(IC<0>{}));
 }
 template <typename F>
 auto with_vec(int vec, F&& f) {
@@ -118,9 +118,12 @@ int load_policy(const Device& d, int64_t rows, int64_t lda) {
     return bytes > 0.5 * (double)d.l2_bytes ? 0 : 1;
 }
 
-mapi_status check_op(int32_t op) {
+mapi_status check_op(int32_t op, bool dot_ok = false) {
+    if (op == MAPI_OP_DOT && dot_ok) return MAPI_OK;
     if (op != MAPI_OP_MIN1 && op != MAPI_OP_MIN2)
-        return fail(MAPI_ERR_BAD_PARAM, "op (%d) must be MAPI_OP_MIN1 (0) or MAPI_OP_MIN2 (1)", op);
+        return fail(MAPI_ERR_BAD_PARAM, dot_ok ? "op (%d) must be MAPI_OP_MIN1 (0), MAPI_OP_MIN2 (1) or MAPI_OP_DOT (2)"
+                                               : "op (%d) must be MAPI_OP_MIN1 (0) or MAPI_OP_MIN2 (1)",
+                    op);
     return MAPI_OK;
 }
 
@@ -231,7 +234,7 @@ mapi_status iterate_launch(const Device& d, int32_t op, const float* A, int64_t 
     const int pol = load_policy(d, n, lda);
     MAPI_CUDA(cudaMemsetAsync(W.bar, 0, 256, s));
     if (use_cluster(d, n)) {
-        auto kern = op == 1 ? k_iterate_cluster<1> : k_iterate_cluster<0>;
+        auto kern = op == 2 ? k_iterate_cluster<2> : (op == 1 ? k_iterate_cluster<1> : k_iterate_cluster<0>);
         const size_t smem = cluster_smem_bytes(n);
         MAPI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         IterArgs a;
@@ -358,7 +361,7 @@ mapi_status iterate_launch(const Device& d, int32_t op, const float* A, int64_t 
                     kern<<<grid, kIterThreads, 0, s>>>(A, n, lda, W.w, W.y, W.slots, W.stop);
                     g_launches.fetch_add(1, std::memory_order_relaxed);
                     k_normalize<<<1, 1024, 0, s>>>(n, W.y, W.slots, grid, W.w, t, tol, norms, deltas,
-                                                   W.status, W.stop);
+                                                   W.status, W.stop, OP == 2 ? 1 : 0);
                     g_launches.fetch_add(1, std::memory_order_relaxed);
                     cudaError_t e = cudaGetLastError();
                     if (e != cudaSuccess) st = fail(MAPI_ERR_CUDA, "launch: %s", cudaGetErrorString(e));
@@ -386,8 +389,8 @@ mapi_status read_status(const IterWs& W, cudaStream_t s, int32_t* iters_done) {
 }
 
 mapi_status validate_dense(int32_t op, const float* A, int64_t n, int64_t lda, const float* b0,
-                           int32_t iters, float tol, const float* w_out, void* ws) {
-    mapi_status st = check_op(op);
+                           int32_t iters, float tol, const float* w_out, void* ws, bool dot_ok = true) {
+    mapi_status st = check_op(op, dot_ok);
     if (st != MAPI_OK) return st;
     if (!A) return fail(MAPI_ERR_NULL, "A is NULL");
     if (!b0) return fail(MAPI_ERR_NULL, "b0 is NULL");
@@ -448,7 +451,7 @@ size_t mapi_workspace_size(int32_t op, int64_t n, int64_t nnz, int32_t k) {
 
 mapi_status mapi_mavp_matvec(int32_t op, const float* A, int64_t n_rows, int64_t n_cols, int64_t lda,
                              const float* x, float* y, mapi_stream_t stream) {
-    mapi_status st = check_op(op);
+    mapi_status st = check_op(op, true);
     if (st != MAPI_OK) return st;
     if (n_rows < 0 || n_cols < 0)
         return fail(MAPI_ERR_SHAPE, "negative size: n_rows %lld, n_cols %lld", (long long)n_rows,
@@ -677,7 +680,7 @@ mapi_status mapi_pca_topk(int32_t op, const float* C, int64_t n, int64_t ldc, in
 mapi_status mapi_iterate_batched(int32_t op, const float* A, int64_t n, int64_t lda, const float* B0, int32_t k,
                                  int32_t iters, float tol, float* W_out, float* norms, float* deltas,
                                  int32_t* iters_done, void* ws, size_t ws_bytes, mapi_stream_t stream) {
-    mapi_status st = validate_dense(op, A, n, lda, B0, iters, tol, W_out, ws);
+    mapi_status st = validate_dense(op, A, n, lda, B0, iters, tol, W_out, ws, false);
     if (st != MAPI_OK) return st;
     if (k < 1) return fail(MAPI_ERR_BAD_PARAM, "k (%d) must be >= 1", k);
     const size_t need = batched_ws_bytes(n, k);

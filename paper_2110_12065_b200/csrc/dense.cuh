@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(512, MINB) k_iterate_persistent(IterArgs p) {
             }
             const float v = row_mavp<OP, VEC, POL, false, U, PF>(p.A + row * p.lda, w_s, n, lane);
             if (lane == 0) y[row] = v;
-            abs_part += (double)fabsf(v);
+            abs_part += norm_part<OP>(v);
         }
         const double cta_abs = block_sum(lane == 0 ? abs_part : 0.0, red);
         double* slots = reinterpret_cast<double*>(p.slots);
@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(512, MINB) k_iterate_persistent(IterArgs p) {
                 if (lane == 0) red[32] = part;
             }
             __syncthreads();
-            s = red[32];
+            s = norm_final<OP>(red[32]);
             __syncthreads();
         }
         if (!(s > 0.0) || isinf(s)) {  // uniform across the grid (same s everywhere)
@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_iterate_coop(IterArgs p) {
 #pragma unroll 8
             for (int q = 0; q < NW; ++q) v += part[r * NW + q];
             y[blockIdx.x + r * gridDim.x] = v;
-            abs_part += (double)fabsf(v);
+            abs_part += norm_part<OP>(v);
         }
         const double cta_abs = block_sum(abs_part, red);
         double* slots = reinterpret_cast<double*>(p.slots);
@@ -331,7 +331,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_iterate_coop(IterArgs p) {
                 if (lane == 0) red[32] = pp;
             }
             __syncthreads();
-            sd = red[32];
+            sd = norm_final<OP>(red[32]);
             __syncthreads();
         }
         if (!(sd > 0.0) || isinf(sd)) {  // uniform across the grid
@@ -447,8 +447,8 @@ __global__ void __launch_bounds__(kClusterThreads, 1) k_iterate_cluster(IterArgs
         // epilogue by warp 0 (fixed order, identical in every CTA): s_t, w_{t+1}, delta_t
         if (warp == 0) {
             double ap = 0.0;
-            for (int64_t k = lane; k < n; k += 32) ap += (double)fabsf(yb[k]);
-            const double sd = warp_sum(ap);
+            for (int64_t k = lane; k < n; k += 32) ap += norm_part<OP>(yb[k]);
+            const double sd = norm_final<OP>(warp_sum(ap));
             int st = kStOk;
             if (!(sd > 0.0) || isinf(sd)) st = (sd == 0.0) ? kStDegenerate : kStNonfinite;
             double dp = 0.0;
@@ -502,7 +502,7 @@ __global__ void __launch_bounds__(512, 1) k_rows_partial(const float* __restrict
     for (int64_t row = (int64_t)blockIdx.x * nw + (threadIdx.x >> 5); row < n; row += total_warps) {
         const float v = row_mavp<OP, VEC, POL, true, U>(A + row * lda, w, n, lane);
         if (lane == 0) y[row] = v;
-        abs_part += (double)fabsf(v);
+        abs_part += norm_part<OP>(v);
     }
     const double cta_abs = block_sum(lane == 0 ? abs_part : 0.0, red);
     if (threadIdx.x == 0) reinterpret_cast<double*>(slots)[blockIdx.x] = cta_abs;
@@ -512,7 +512,7 @@ __global__ void __launch_bounds__(1024) k_normalize(int64_t n, const float* __re
                                                     const float* __restrict__ slots, int n_slots,
                                                     float* __restrict__ w, int32_t t, float tol,
                                                     float* norms, float* deltas, int32_t* status,
-                                                    int32_t* stop) {
+                                                    int32_t* stop, int l2) {
     __shared__ double red[33];
     if (*(volatile int32_t*)stop) return;
     const double* dslots = reinterpret_cast<const double*>(slots);
@@ -523,7 +523,7 @@ __global__ void __launch_bounds__(1024) k_normalize(int64_t n, const float* __re
         if (threadIdx.x == 0) red[32] = part;
     }
     __syncthreads();
-    const double s = red[32];
+    const double s = l2 ? sqrt(red[32]) : red[32];
     __syncthreads();
     if (!(s > 0.0) || isinf(s)) {
         if (threadIdx.x == 0) {

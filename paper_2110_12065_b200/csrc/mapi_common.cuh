@@ -14,12 +14,31 @@ constexpr int kWarp = 32;
 
 // ---------------------------------------------------------------------------------------------
 // MAVP term. OP 0 = min1 (Eq. 3), OP 1 = min2 (Eq. 4: 1(sign a = sign w) min(|a|,|w|)).
+// OP 2 = the regular product a*w of Eq. (1): the RPI comparator, the only
+// operator with a multiply; it is never used by the MAVP entry points' default path.
 template <int OP>
 __device__ __forceinline__ float mavp_term(float a, float w) {
-    float d;
-    asm("min.xorsign.abs.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(w));
-    if constexpr (OP == 1) d = fmaxf(d, 0.0f);  // opposite signs -> 0 (indicator false)
-    return d;
+    if constexpr (OP == 2) {
+        return a * w;
+    } else {
+        float d;
+        asm("min.xorsign.abs.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(w));
+        if constexpr (OP == 1) d = fmaxf(d, 0.0f);  // opposite signs -> 0 (indicator false)
+        return d;
+    }
+}
+
+// Per-element contribution to the normalisation and its finish: l1 for MAVP (Eq. 8),
+// l2 for the regular product (Eq. 1).  Accumulated in fp64.
+template <int OP>
+__device__ __forceinline__ double norm_part(float v) {
+    if constexpr (OP == 2) return (double)v * (double)v;
+    else return (double)fabsf(v);
+}
+template <int OP>
+__device__ __forceinline__ double norm_final(double s) {
+    if constexpr (OP == 2) return sqrt(s);
+    else return s;
 }
 
 // ---------------------------------------------------------------------------------------------

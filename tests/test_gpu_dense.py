@@ -263,3 +263,31 @@ def test_every_dense_path_matches_oracle(mapi_lib, orc, monkeypatch, path, n):
     ref = orc.mapi(A, b0, 20)
     assert res.iters_done == 20
     _t2(res.w_l2.cpu().numpy(), ref.w, res.norms.cpu().numpy(), ref.norms)
+
+
+# ------------------------------------------------------------------------------ RPI comparator (NEXT-3)
+
+
+@pytest.mark.parametrize("path", ["cluster", "rows", "coop", "multi"])
+def test_rpi_comparator_matches_oracle(mapi_lib, orc, monkeypatch, path):
+    """op = MAPI_OP_DOT: b <- Ab/||Ab||_2 (Eq. 1) through every dense path, vs the oracle's rpi."""
+    m = mapi_lib
+    n = 256 if path == "cluster" else 8192
+    r = np.random.default_rng(n)
+    A = (r.standard_normal((n, n)) / np.sqrt(n)).astype(np.float32)
+    A = (A + A.T) / 2 + np.diag(np.linspace(2.0, 0.0, n)).astype(np.float32)
+    b0 = np.full(n, 1.0 / np.sqrt(n), np.float32)
+    monkeypatch.setenv("MAPI_DENSE_PATH", path)
+    res = m.iterate(torch.from_numpy(A).cuda(), torch.from_numpy(b0).cuda(), 30, op=m.DOT)
+    ref = orc.rpi(A, b0, 30)
+    _t2(res.w.cpu().numpy(), ref.w, res.norms.cpu().numpy(), ref.norms)
+    assert abs(float(res.w.norm()) - 1.0) < 1e-5
+
+
+def test_matvec_dot(mapi_lib, orc):
+    m = mapi_lib
+    M, _ = synth.random_matrix(300, 700, seed=9)
+    x = synth.random_vector(700, seed=10)
+    y = m.mavp_matvec(torch.from_numpy(M).cuda(), torch.from_numpy(x).cuda(), op=m.DOT).cpu().numpy()
+    ref, mag = orc.matvec(M, x, "dot", return_mag=True)
+    assert np.all(np.abs(y - ref) <= 1e-5 * mag)

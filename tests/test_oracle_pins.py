@@ -459,3 +459,18 @@ def test_min_covariance_properties(orc):
     assert np.all(np.abs(C) <= np.diag(C)[:, None] + 1e-15)  # |a (+) b| <= min(||a||_1, ||b||_1)
     C5 = orc.min_covariance(V, divisor=10)  # Eq. (5) divisor N
     np.testing.assert_allclose(C5 * 10, C * 9, rtol=1e-14)
+
+
+def test_pca_topk_dot_recovers_lapack_eigenvectors(orc):
+    # with the regular product (Eq. 1) and L2 deflation, power iteration + deflation returns the
+    # leading eigenvectors of a symmetric matrix with a spectral gap (LAPACK eigh)
+    r = np.random.default_rng(53)
+    n = 24
+    Q, _ = np.linalg.qr(r.standard_normal((n, n)))
+    lam = np.array([10.0, 6.0, 3.5] + list(np.linspace(1.0, 0.1, n - 3)))
+    C = ((Q * lam) @ Q.T).astype(np.float32)
+    res = orc.pca_topk(C, 3, 300, np.ones(n) / np.sqrt(n), op="dot")
+    evals, evecs = np.linalg.eigh(C.astype(np.float64))
+    for i in range(3):
+        u = evecs[:, -1 - i]
+        np.testing.assert_allclose(res.P[i] * np.sign(res.P[i] @ u), u, atol=1e-6)
