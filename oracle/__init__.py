@@ -65,6 +65,8 @@ def _load():
         lib.orc_power_iterate.restype = cint
         lib.orc_matmat_f32.argtypes = [cint, P, i64, i64, i64, P, i64, i64, dbl, P]
         lib.orc_matmat_f32.restype = None
+        lib.orc_outer_apply.argtypes = [cint, P, i64, i64, i64, P, i64, i64, cint, P, i64]
+        lib.orc_outer_apply.restype = None
         lib.orc_deflate.argtypes = [P, i64, i64, P, i32, P]
         lib.orc_deflate.restype = None
         lib.orc_pca_topk.argtypes = [cint, P, i64, i64, i32, i32, P, P, P, P, P]
@@ -114,6 +116,8 @@ def _as_f32_matrix(A):
         raise TypeError("oracle matrices are the fp32 input bytes (dtype float32)")
     if A.ndim == 2 and A.size == 0:
         return np.ascontiguousarray(A), max(1, A.shape[1])
+    if A.ndim == 2 and A.flags.c_contiguous:
+        return A, A.shape[1]
     if A.ndim != 2 or A.strides[1] != 4:
         raise ValueError("A must be a 2-D row-major float32 array")
     lda = A.strides[0] // 4
@@ -220,6 +224,46 @@ def min_covariance(V, divisor=None, op="min1") -> np.ndarray:
     V = np.asarray(V)
     d = (V.shape[1] - 1) if divisor is None else divisor
     return matmat(V, V, op, d)
+
+
+def outer_apply(W, X, op="min1", subtract=False) -> np.ndarray:
+    """Y = (W (op) W^T) X, or X - (W (op) W^T) X: Alg. 2 steps 8 / 6, regular product."""
+    W = np.asarray(W, np.float32)
+    if W.ndim == 1:
+        W = W[:, None]
+    W, ldw = _as_f32_matrix(np.ascontiguousarray(W))
+    X = np.asarray(X, np.float32)
+    vec = X.ndim == 1
+    if vec:
+        X = X[:, None]
+    X, ldx = _as_f32_matrix(np.ascontiguousarray(X))
+    M, r = W.shape
+    if X.shape[0] != M:
+        raise ValueError(f"dimension mismatch: W has {M} rows, X has {X.shape[0]}")
+    q = X.shape[1]
+    Y = np.empty((M, q), np.float64)
+    _load().orc_outer_apply(_op(op), _ptr(W), M, r, ldw, _ptr(X), q, ldx, 1 if subtract else 0, _ptr(Y), q)
+    return Y[:, 0] if vec else Y
+
+
+def mavp_deflate(C, w, op="min1") -> np.ndarray:
+    """Alg. 2 step 6: C - (w (op) w^T) C, the scalar-MAVP outer product times C."""
+    return outer_apply(w, C, op, subtract=True)
+
+
+def reconstruct(W, V, op="min1"):
+    """Alg. 2 steps 3 and 8: m = mean(V, 2); v_hat_i = (W (op) W^T)(v_i - m) + m for every
+    column i of V (pixels x N).  Returns (V_hat fp64, m)."""
+    V64 = np.asarray(V, np.float64)
+    m = V64.mean(axis=1)
+    Xc = (V64 - m[:, None]).astype(np.float32)
+    return outer_apply(W, Xc, op) + m[:, None], m
+
+
+def psnr(ref, test) -> float:
+    """10 log10(1 / MSE), pixels in [0, 1] (peak 1)."""
+    mse = float(np.mean((np.asarray(ref, np.float64) - np.asarray(test, np.float64)) ** 2))
+    return float("inf") if mse == 0.0 else 10.0 * np.log10(1.0 / mse)
 
 
 def deflate(C, P, i) -> np.ndarray:

@@ -182,6 +182,34 @@ void orc_matmat_f32(int op, const float *A, int64_t m, int64_t K, int64_t lda, c
     }
 }
 
+/* MAVP outer-product operator of Alg. 2: for W (M x r, ldw; columns w_1..w_r) the M x M
+ * matrix Q = W (op) W^T has Q[i][j] = sum_c term(W[i][c], W[j][c])  (row i of W against row j, i.e. the
+ * matrix extension P:69-70 with the r-component rows as vectors; r = 1 gives the scalar-MAVP outer
+ * product of step 6, r = 2 the W = [w1 w2] of step 8).  Y = X - Q X  (subtract = 1, step 6) or
+ * Y = Q X (subtract = 0, step 8), with Q X a REGULAR matrix product.  X: M x q (ldx),
+ * Y: M x q (ldy).  Literal: Q is materialised row by row, the product summed over j in index order. */
+void orc_outer_apply(int op, const float *W, int64_t M, int64_t r, int64_t ldw, const float *X, int64_t q,
+                     int64_t ldx, int subtract, double *Y, int64_t ldy) {
+#pragma omp parallel
+    {
+        double *Qi = (double *)malloc(sizeof(double) * (size_t)M);
+#pragma omp for schedule(static)
+        for (int64_t i = 0; i < M; ++i) {
+            for (int64_t j = 0; j < M; ++j) {
+                double t = 0.0;
+                for (int64_t c = 0; c < r; ++c) t += orc_term(op, (double)W[i * ldw + c], (double)W[j * ldw + c]);
+                Qi[j] = t;
+            }
+            for (int64_t k = 0; k < q; ++k) {
+                double acc = 0.0;
+                for (int64_t j = 0; j < M; ++j) acc += Qi[j] * (double)X[j * ldx + k];
+                Y[i * ldy + k] = subtract ? (double)X[i * ldx + k] - acc : acc;
+            }
+        }
+        free(Qi);
+    }
+}
+
 /* L2 deflation: the i-th principal vector is extracted by power iteration on
  *     D_i = (I - sum_{m<i} p_m p_m^T) C,
  * with p_m the l2-normalised MAPI outputs.  Expanded entry-wise:

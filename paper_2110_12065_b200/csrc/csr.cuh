@@ -217,8 +217,10 @@ __global__ void __launch_bounds__(kMpThreads) k_rank_rows_mp(int64_t n, int64_t 
                                                              int32_t* __restrict__ carry_row,
                                                              float* __restrict__ carry_val, double* __restrict__ gsum,
                                                              const int32_t* stop) {
-    __shared__ int32_t s_end[kMpTile + 1];  // row_ptr[i0+1 .. i1+1]
-    __shared__ float s_val[kMpTile];        // v[col_idx[k0 .. k1)]
+    // shared arrays indexed through pad(): one spare word per 8 so that the lane-strided reads of the
+    // consume loop (thread t walks ~8 consecutive items) hit 32 distinct banks instead of 4
+    __shared__ int32_t s_end[kMpTile + 1 + (kMpTile + 1) / 8 + 1];  // row_ptr[i0+1 .. i1+1]
+    __shared__ float s_val[kMpTile + kMpTile / 8];                  // v[col_idx[k0 .. k1)]
     __shared__ float s_fp[kMpThreads];      // segmented prefix of the threads' carries
     __shared__ int32_t wl_row[kMpThreads / 32], wf_row[kMpThreads / 32];
     __shared__ float wl_val[kMpThreads / 32];
@@ -229,8 +231,9 @@ __global__ void __launch_bounds__(kMpThreads) k_rank_rows_mp(int64_t n, int64_t 
     const int32_t k0 = part_k[blockIdx.x], k1 = part_k[blockIdx.x + 1];
     const int nrows = i1 - i0, nk = k1 - k0;  // nrows + nk == items of this tile
     // stage row ends (rows i0 .. i1, the last possibly partial) and gathered values
+    auto pad = [](int x) { return x + (x >> 3); };
     for (int r = tid; r <= nrows; r += kMpThreads)
-        s_end[r] = (i0 + r < n) ? row_ptr[i0 + r + 1] : (int32_t)nnz;
+        s_end[pad(r)] = (i0 + r < n) ? row_ptr[i0 + r + 1] : (int32_t)nnz;
     // nk <= kMpTile = kMpIpt * kMpThreads: all kMpIpt column ids first, then all gathers in flight
     int32_t cj[kMpIpt];
 #pragma unroll
@@ -245,7 +248,7 @@ __global__ void __launch_bounds__(kMpThreads) k_rank_rows_mp(int64_t n, int64_t 
 #pragma unroll
     for (int u = 0; u < kMpIpt; ++u) {
         const int j = tid + u * kMpThreads;
-        if (j < nk) s_val[j] = xv[u];
+        if (j < nk) s_val[pad(j)] = xv[u];
         gpart += (double)xv[u];
     }
     __syncthreads();
@@ -255,7 +258,7 @@ __global__ void __launch_bounds__(kMpThreads) k_rank_rows_mp(int64_t n, int64_t 
     int lo = max(0, dt - nk), hi = min(dt, nrows);
     while (lo < hi) {
         const int mid = (lo + hi) >> 1;
-        if (s_end[mid] - k0 <= dt - 1 - mid) lo = mid + 1;
+        if (s_end[pad(mid)] - k0 <= dt - 1 - mid) lo = mid + 1;
         else hi = mid;
     }
     int ri = lo, kj = dt - lo;
@@ -263,7 +266,7 @@ __global__ void __launch_bounds__(kMpThreads) k_rank_rows_mp(int64_t n, int64_t 
     int first_row = -1;  // first row this thread emits (local index); earlier threads may feed it
     const int dend = min(dt + kMpIpt, items);
     for (int d = dt; d < dend; ++d) {
-        if (ri < nrows && k0 + kj >= s_end[ri]) {  // the end of row ri
+        if (ri < nrows && k0 + kj >= s_end[pad(ri)]) {  // the end of row ri
             if (first_row < 0) {
                 first_row = ri;
                 own_first = acc;
@@ -273,7 +276,7 @@ __global__ void __launch_bounds__(kMpThreads) k_rank_rows_mp(int64_t n, int64_t 
             acc = 0.0f;
             ++ri;
         } else {
-            acc += s_val[kj];
+            acc += s_val[pad(kj)];
             ++kj;
         }
     }

@@ -474,3 +474,55 @@ def test_pca_topk_dot_recovers_lapack_eigenvectors(orc):
     for i in range(3):
         u = evecs[:, -1 - i]
         np.testing.assert_allclose(res.P[i] * np.sign(res.P[i] @ u), u, atol=1e-6)
+
+
+# ---------------------------------------------------------------- Alg. 2 MAVP deflation / reconstruction (NEXT-2)
+
+
+def test_mavp_deflate_spec_e1(orc):
+    # w1 = e1 -> P(1,1) = 1, zeros elsewhere -> the deflation zeroes row 1 of C
+    r = np.random.default_rng(81)
+    C = r.standard_normal((6, 6)).astype(np.float32)
+    w = np.zeros(6, np.float32)
+    w[0] = 1.0
+    D = orc.mavp_deflate(C, w)
+    np.testing.assert_array_equal(D[0], 0.0)
+    np.testing.assert_array_equal(D[1:], C[1:].astype(np.float64))
+
+
+def test_mavp_deflate_dot_is_l2_deflation(orc):
+    # with the regular product P = w w^T, matching (I - w w^T) C — vs the numpy product
+    r = np.random.default_rng(82)
+    C = r.standard_normal((9, 9)).astype(np.float32)
+    w = r.standard_normal(9)
+    w = (w / np.linalg.norm(w)).astype(np.float32)
+    D = orc.mavp_deflate(C, w, op="dot")
+    w64 = w.astype(np.float64)
+    np.testing.assert_allclose(D, (np.eye(9) - np.outer(w64, w64)) @ C.astype(np.float64), rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("op", ["min1", "min2"])
+def test_outer_apply_vs_brute(orc, op):
+    r = np.random.default_rng(83)
+    for trial in range(10):
+        M, rr, q = int(r.integers(1, 8)), int(r.integers(1, 3)), int(r.integers(1, 4))
+        W = r.standard_normal((M, rr)).astype(np.float32)
+        X = r.standard_normal((M, q)).astype(np.float32)
+        f = brute.OPS[op]
+        Q = np.array([[f(W[i], W[j]) for j in range(M)] for i in range(M)])
+        np.testing.assert_allclose(orc.outer_apply(W, X, op), Q @ X.astype(np.float64), rtol=1e-12, atol=1e-13)
+
+
+def test_reconstruct_identical_copies_returns_image(orc):
+    # N identical copies -> zero-centred V = 0 -> v_hat = m = the image
+    img = np.random.default_rng(84).random(64)
+    V = np.repeat(img[:, None], 5, axis=1).astype(np.float32)
+    W = np.random.default_rng(85).standard_normal((64, 2)).astype(np.float32)
+    Vh, m = orc.reconstruct(W, V)
+    np.testing.assert_allclose(Vh, np.repeat(img[:, None], 5, axis=1), atol=1e-7)
+
+
+def test_psnr_closed_forms(orc):
+    a = np.zeros(100)
+    assert orc.psnr(a, np.full(100, 0.1)) == pytest.approx(20.0)  # MSE 0.01 -> 20 dB
+    assert orc.psnr(a, np.ones(100)) == pytest.approx(0.0)  # MSE 1 -> 0 dB
