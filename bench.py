@@ -42,6 +42,8 @@ WORKLOADS = {
               "(seed 6), C = V (+) V^T / (N-1), 16384^2 fp32 output",
     "mincov_k4096": "NEXT-1 MAVP matrix product, ALU-bound regime: 4096 x 8192 N(0,1) rows (seed 7), "
                     "C = V (+) V^T / 8192, 4096^2 output",
+    "alg2": "NEXT-2 Alg. 2 image reconstruction end to end (steps 3-8): 10 occluded 128x128 synthetic copies "
+            "(seed 6), min-covariance, 2 x 100 MAPI iterations, MAVP deflation, reconstruction",
 }
 METRIC = "MAPI iterations/s and achieved HBM GB/s (% of B200 peak) at n=32768 fp32"
 
@@ -353,7 +355,39 @@ def build_mincov(args, m, dev, stream):
                 oracle=None)
 
 
-BUILDERS = {"cfg1": build_dense, "cfg3": build_dense, "cfg2": build_pca, "cfg4": build_batched,
+def build_alg2(args, m, dev, stream):
+    import torch
+
+    import synth
+
+    V_raw, img = synth.occluded_copies()
+    Vd = torch.from_numpy(V_raw).to(dev)
+    M, N = V_raw.shape
+    op = {"min1": 0, "min2": 1, "dot": 0}[args.op]
+    b0 = torch.full((M,), 1.0 / np.sqrt(M), device=dev)
+    Vc = torch.empty_like(Vd)
+    C = torch.empty(M, M, device=dev)
+    D = torch.empty(M, M, device=dev)
+
+    def step():
+        m.center_rows(Vd, Vc)  # step 3
+        m.mavp_matmat(Vc, Vc, float(N - 1), C=C, op=op)  # step 4
+        w1 = m.iterate(C, b0, 100, op=op, want_l2=False, want_trace=False).w  # step 5 (l1-unit, R11)
+        m.mavp_deflate(C, w1, op=op, D=D)  # step 6
+        w2 = m.iterate(D, b0, 100, op=op, want_l2=False, want_trace=False).w
+        m.mavp_reconstruct(torch.stack([w1, w2], 1).contiguous(), Vd, op=op)  # steps 7-8
+        return 1
+
+    # HBM bytes of the dominant phases: C written once, read by 200 iterations, read twice + D written
+    per = 4.0 * M * M * (1 + 200 + 3)
+    return Work(step=step, unit="reconstructions/s", per_launch=per, bytes_per_unit=per, bound="hbm",
+                kernel="whole Alg. 2 pipeline (events per phase not separated)",
+                config={"workload": f"alg2: {WORKLOADS['alg2']}", "M": M, "N": N, "op": args.op,
+                        "l2_flush": "none (1 GiB matrices exceed L2)"},
+                oracle=None)
+
+
+BUILDERS = {"cfg1": build_dense, "alg2": build_alg2, "cfg3": build_dense, "cfg2": build_pca, "cfg4": build_batched,
             "cfg5": build_rank, "mincov": build_mincov, "mincov_k4096": build_mincov}
 
 

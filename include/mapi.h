@@ -66,7 +66,9 @@ typedef enum {
     MAPI_WS_PCA_TOPK = 3,
     MAPI_WS_CSR_PREPARE = 4,
     MAPI_WS_RANK_CSR = 5,
-    MAPI_WS_ITERATE_HOST = 6
+    MAPI_WS_ITERATE_HOST = 6,
+    MAPI_WS_MAVP_DEFLATE = 7, /* n = M */
+    MAPI_WS_RECONSTRUCT = 8   /* n = M, nnz = N (images), k = r (components) */
 } mapi_ws_op;
 
 /* y = A (op) x — the matrix extension of the MAVP (reading Q6: y_j uses ROW j):
@@ -132,6 +134,30 @@ mapi_status mapi_pca_topk(int32_t op, const float *C, int64_t n, int64_t ldc, in
                           int32_t iters, const float *b0, float *P_out, float *norms, float *deltas,
                           void *ws, size_t ws_bytes, mapi_stream_t stream);
 
+/* Alg. 2 step 3: mean over the N columns of each row of V (M x N, ldv; the images as columns),
+ * mean_out[i] = m_i (fp64 sum, rounded once), Vc = V - m (M x N, ldvc; may alias V).  Asynchronous. */
+mapi_status mapi_center_rows(const float *V, int64_t M, int64_t N, int64_t ldv, float *Vc, int64_t ldvc,
+                             float *mean_out, mapi_stream_t stream);
+
+/* Alg. 2 step 6: D = C - (w (op) w^T) C, where (w (op) w^T)[i][j] = term(w_i, w_j) is
+ * the scalar-MAVP outer product and the product with C is a REGULAR matrix product.  Evaluated exactly
+ * in O(M^2) through the sorted prefix-sum regrouping of DESIGN.md R10 (fp64 scans, one fp32 rounding).
+ * C: M x M (ldc >= M), w: M (normally the l2-unit MAPI output, Alg. 1 line 6), D: M x M (ldd >= M, must
+ * not alias C).  op: MIN1, MIN2 or DOT (DOT gives the L2 deflation (I - w w^T) C of P:26).
+ * M <= 16384.  Workspace: mapi_workspace_size(MAPI_WS_MAVP_DEFLATE, M, 0, 0).  Asynchronous. */
+mapi_status mapi_mavp_deflate(int32_t op, const float *C, int64_t M, int64_t ldc, const float *w, float *D,
+                              int64_t ldd, void *ws, size_t ws_bytes, mapi_stream_t stream);
+
+/* Alg. 2 steps 3 and 8: for the N images stored as the columns of V (M x N, ldv),
+ * m = mean over the columns, and every column j of Vhat (M x N, ldvh) is
+ *     v_hat_j = (W (op) W^T)(v_j - m) + m,   (W (op) W^T)[i][i'] = sum_c term(W[i][c], W[i'][c]),
+ * W: M x r (ldw >= r; normally [w1 w2], r = 2).  mean_out (M, required).  Same exact O(M r N) regrouping
+ * as mapi_mavp_deflate; M <= 16384.  Workspace: mapi_workspace_size(MAPI_WS_RECONSTRUCT, M, N, r).
+ * No clamping (the paper is silent; callers clamp to [0, 1] for display / PSNR).  Asynchronous. */
+mapi_status mapi_mavp_reconstruct(int32_t op, const float *W, int64_t M, int32_t r, int64_t ldw, const float *V,
+                                  int64_t N, int64_t ldv, float *Vhat, int64_t ldvh, float *mean_out, void *ws,
+                                  size_t ws_bytes, mapi_stream_t stream);
+
 /* Google-matrix preparation for MAPI ranking (Eq. 13; reading Q10):
  * the graph is CSR by DESTINATION (row i lists the sources j of the distinct edges j -> i);
  * row_ptr: n+1 int32 (nnz < 2^31), col_idx: nnz int32 in [0, n).
@@ -157,7 +183,8 @@ mapi_status mapi_rank_csr(int64_t n, int64_t nnz, const int32_t *row_ptr, const 
 /* Bytes of device workspace the call `op` needs for the given sizes (0 if none).
  *   MAPI_WS_MATVEC: 0.  MAPI_WS_ITERATE: n.  MAPI_WS_ITERATE_BATCHED: n, k.
  *   MAPI_WS_PCA_TOPK: n, k.  MAPI_WS_CSR_PREPARE / MAPI_WS_RANK_CSR: n, nnz.
- *   MAPI_WS_ITERATE_HOST: n, and nnz = lda (the device copy of A is n*lda floats). */
+ *   MAPI_WS_ITERATE_HOST: n, and nnz = lda (the device copy of A is n*lda floats), k = iters.
+ *   MAPI_WS_MAVP_DEFLATE: n = M.  MAPI_WS_RECONSTRUCT: n = M, nnz = N, k = r. */
 size_t mapi_workspace_size(int32_t op, int64_t n, int64_t nnz, int32_t k);
 
 const char *mapi_status_string(mapi_status status);

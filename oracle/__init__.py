@@ -67,6 +67,8 @@ def _load():
         lib.orc_matmat_f32.restype = None
         lib.orc_outer_apply.argtypes = [cint, P, i64, i64, i64, P, i64, i64, cint, P, i64]
         lib.orc_outer_apply.restype = None
+        lib.orc_outer_apply_rows.argtypes = [cint, P, i64, i64, i64, P, i64, i64, cint, P, i64, P, i64]
+        lib.orc_outer_apply_rows.restype = None
         lib.orc_deflate.argtypes = [P, i64, i64, P, i32, P]
         lib.orc_deflate.restype = None
         lib.orc_pca_topk.argtypes = [cint, P, i64, i64, i32, i32, P, P, P, P, P]
@@ -244,6 +246,22 @@ def outer_apply(W, X, op="min1", subtract=False) -> np.ndarray:
     Y = np.empty((M, q), np.float64)
     _load().orc_outer_apply(_op(op), _ptr(W), M, r, ldw, _ptr(X), q, ldx, 1 if subtract else 0, _ptr(Y), q)
     return Y[:, 0] if vec else Y
+
+
+def outer_apply_rows(W, X, rows, op="min1", subtract=False) -> np.ndarray:
+    """Rows `rows` of outer_apply(W, X, op, subtract) (full-size checks on sampled rows)."""
+    W = np.asarray(W, np.float32)
+    if W.ndim == 1:
+        W = W[:, None]
+    W, ldw = _as_f32_matrix(np.ascontiguousarray(W))
+    X, ldx = _as_f32_matrix(np.ascontiguousarray(np.asarray(X, np.float32)))
+    rows = np.ascontiguousarray(np.asarray(rows, np.int64))
+    M, r = W.shape
+    q = X.shape[1]
+    Y = np.empty((rows.size, q), np.float64)
+    _load().orc_outer_apply_rows(_op(op), _ptr(W), M, r, ldw, _ptr(X), q, ldx, 1 if subtract else 0, _ptr(rows),
+                                 rows.size, _ptr(Y), q)
+    return Y
 
 
 def mavp_deflate(C, w, op="min1") -> np.ndarray:

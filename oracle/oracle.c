@@ -210,6 +210,31 @@ void orc_outer_apply(int op, const float *W, int64_t M, int64_t r, int64_t ldw, 
     }
 }
 
+/* orc_outer_apply restricted to the rows listed in `rows` (nrows of them): Y is nrows x q (ldy).
+ * Same arithmetic, used to check full-size GPU results on sampled rows. */
+void orc_outer_apply_rows(int op, const float *W, int64_t M, int64_t r, int64_t ldw, const float *X, int64_t q,
+                          int64_t ldx, int subtract, const int64_t *rows, int64_t nrows, double *Y, int64_t ldy) {
+#pragma omp parallel
+    {
+        double *Qi = (double *)malloc(sizeof(double) * (size_t)M);
+#pragma omp for schedule(static)
+        for (int64_t ri = 0; ri < nrows; ++ri) {
+            const int64_t i = rows[ri];
+            for (int64_t j = 0; j < M; ++j) {
+                double t = 0.0;
+                for (int64_t c = 0; c < r; ++c) t += orc_term(op, (double)W[i * ldw + c], (double)W[j * ldw + c]);
+                Qi[j] = t;
+            }
+            for (int64_t k = 0; k < q; ++k) {
+                double acc = 0.0;
+                for (int64_t j = 0; j < M; ++j) acc += Qi[j] * (double)X[j * ldx + k];
+                Y[ri * ldy + k] = subtract ? (double)X[i * ldx + k] - acc : acc;
+            }
+        }
+        free(Qi);
+    }
+}
+
 /* L2 deflation: the i-th principal vector is extracted by power iteration on
  *     D_i = (I - sum_{m<i} p_m p_m^T) C,
  * with p_m the l2-normalised MAPI outputs.  Expanded entry-wise:

@@ -18,12 +18,14 @@ from typing import Optional
 from ._build import LIB as _LIB_PATH
 from ._build import build  # noqa: F401  (re-exported: compile in-tree)
 
-__all__ = ["load", "build", "MapiError", "mavp_matvec", "mavp_matmat", "min_covariance", "iterate", "iterate_host", "iterate_batched",
+__all__ = ["load", "build", "MapiError", "mavp_matvec", "mavp_matmat", "min_covariance", "center_rows", "mavp_deflate",
+           "mavp_reconstruct", "iterate", "iterate_host", "iterate_batched",
            "pca_topk", "csr_prepare", "rank_csr", "workspace_size", "launch_count", "set_profiling",
            "last_kernel_ms", "MIN1", "MIN2", "DOT"]
 
 MIN1, MIN2, DOT = 0, 1, 2  # DOT: regular product of Eq. (1), the RPI comparator
-WS_MATVEC, WS_ITERATE, WS_ITERATE_BATCHED, WS_PCA_TOPK, WS_CSR_PREPARE, WS_RANK_CSR, WS_ITERATE_HOST = range(7)
+(WS_MATVEC, WS_ITERATE, WS_ITERATE_BATCHED, WS_PCA_TOPK, WS_CSR_PREPARE, WS_RANK_CSR, WS_ITERATE_HOST,
+ WS_MAVP_DEFLATE, WS_RECONSTRUCT) = range(9)
 STATUS = {0: "MAPI_OK", 1: "MAPI_ERR_NULL", 2: "MAPI_ERR_SHAPE", 3: "MAPI_ERR_BAD_PARAM",
           4: "MAPI_ERR_DEGENERATE", 5: "MAPI_ERR_NEGATIVE", 6: "MAPI_ERR_NONFINITE",
           7: "MAPI_ERR_WORKSPACE", 8: "MAPI_ERR_CUDA"}
@@ -56,6 +58,9 @@ def load():
         sig = {
             "mapi_mavp_matvec": (st, [i32, P, i64, i64, i64, P, P, P]),
             "mapi_mavp_matmat": (st, [i32, P, i64, i64, i64, P, i64, i64, f32, P, i64, P]),
+            "mapi_center_rows": (st, [P, i64, i64, i64, P, i64, P, P]),
+            "mapi_mavp_deflate": (st, [i32, P, i64, i64, P, P, i64, P, sz, P]),
+            "mapi_mavp_reconstruct": (st, [i32, P, i64, i32, i64, P, i64, i64, P, i64, P, P, sz, P]),
             "mapi_iterate": (st, [i32, P, i64, i64, P, i32, f32, P, P, P, P, P, P, sz, P]),
             "mapi_iterate_host": (st, [i32, P, i64, i64, P, i32, f32, P, P, P, P, P, P, sz, P]),
             "mapi_iterate_batched": (st, [i32, P, i64, i64, P, i32, i32, f32, P, P, P, P, P, sz, P]),
@@ -187,6 +192,45 @@ def min_covariance(V, divisor=None, op: int = MIN1, stream=None):
     d = N - 1 by default as in Alg. 2 step 4."""
     d = (V.shape[1] - 1) if divisor is None else divisor
     return mavp_matmat(V, V, float(d), op=op, stream=stream)
+
+
+def center_rows(V, Vc=None, stream=None):
+    """Alg. 2 step 3: m = mean over the columns of V (pixels x N), Vc = V - m."""
+    torch = _torch()
+    M, N, ldv = _matrix(V, "V")
+    Vc = torch.empty_like(V) if Vc is None else Vc
+    mean = torch.empty(M, dtype=torch.float32, device=V.device)
+    _check(load().mapi_center_rows(_ptr(V), M, N, ldv, _ptr(Vc), Vc.stride(0), _ptr(mean), _stream(stream)))
+    return Vc, mean
+
+
+def mavp_deflate(C, w, op: int = MIN1, D=None, ws=None, stream=None):
+    """Alg. 2 step 6: D = C - (w (op) w^T) C (regular product; exact O(M^2) evaluation)."""
+    torch = _torch()
+    M, M2, ldc = _matrix(C, "C")
+    if M != M2:
+        raise ValueError(f"C must be square, got {tuple(C.shape)}")
+    _need(w, "w", torch.float32, (M,))
+    D = torch.empty_like(C) if D is None else D
+    ws, need = _workspace(WS_MAVP_DEFLATE, M, device=C.device, ws=ws)
+    _check(load().mapi_mavp_deflate(op, _ptr(C), M, ldc, _ptr(w), _ptr(D), D.stride(0), _ptr(ws), need,
+                                    _stream(stream)))
+    return D
+
+
+def mavp_reconstruct(W, V, op: int = MIN1, Vhat=None, ws=None, stream=None):
+    """Alg. 2 steps 3 + 8: v_hat_j = (W (op) W^T)(v_j - m) + m for the columns of V."""
+    torch = _torch()
+    M, r, ldw = _matrix(W, "W")
+    M2, N, ldv = _matrix(V, "V")
+    if M != M2:
+        raise ValueError(f"dimension mismatch: W has {M} rows, V has {M2}")
+    Vhat = torch.empty_like(V) if Vhat is None else Vhat
+    mean = torch.empty(M, dtype=torch.float32, device=V.device)
+    ws, need = _workspace(WS_RECONSTRUCT, M, N, r, device=V.device, ws=ws)
+    _check(load().mapi_mavp_reconstruct(op, _ptr(W), M, r, ldw, _ptr(V), N, ldv, _ptr(Vhat), Vhat.stride(0),
+                                        _ptr(mean), _ptr(ws), need, _stream(stream)))
+    return Vhat, mean
 
 
 @dataclass

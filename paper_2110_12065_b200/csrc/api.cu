@@ -16,6 +16,7 @@
 #include "deflate.cuh"
 #include "dense.cuh"
 #include "matmat.cuh"
+#include "outer.cuh"
 
 using namespace mapi;
 
@@ -403,6 +404,50 @@ mapi_status validate_dense(int32_t op, const float* A, int64_t n, int64_t lda, c
     return MAPI_OK;
 }
 
+// ---------------------------------------------------------------------------------------------
+// K9 outer-product operator: workspace [idx r*M i32][a r*M f32][s r*M f32][part r*NB*q*4 f64][Xc M*N f32]
+size_t outer_ws_bytes(int64_t M, int64_t q, int64_t r, int64_t N) {
+    return 3 * align256(sizeof(int32_t) * (size_t)(r * M)) +
+           align256(sizeof(double) * 4 * (size_t)r * (size_t)outer_blocks(M) * (size_t)q) +
+           align256(sizeof(float) * (size_t)M * (size_t)N);
+}
+
+// Y = [X -] (W (op) W^T) X [+ bias], r components in sequence (each pass in its own sorted row order)
+mapi_status outer_run(int32_t op, const float* W, int64_t M, int64_t r, int64_t ldw, const float* X, int64_t q,
+                      int64_t ldx, bool subtract, const float* bias, float* Y, int64_t ldy, char* ws, cudaStream_t s) {
+    int32_t* idx = reinterpret_cast<int32_t*>(ws);
+    ws += align256(sizeof(int32_t) * (size_t)(r * M));
+    float* as = reinterpret_cast<float*>(ws);
+    ws += align256(sizeof(float) * (size_t)(r * M));
+    float* ss = reinterpret_cast<float*>(ws);
+    ws += align256(sizeof(float) * (size_t)(r * M));
+    double* part = reinterpret_cast<double*>(ws);
+    int P = 1;
+    while (P < M) P <<= 1;
+    const size_t sort_smem = sizeof(unsigned long long) * (size_t)P;
+    MAPI_CUDA(cudaFuncSetAttribute(k_outer_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sort_smem));
+    k_outer_sort<<<(unsigned)r, 1024, sort_smem, s>>>(W, M, ldw, idx, as, ss);
+    MAPI_LAUNCHED();
+    const dim3 grid((unsigned)((q + kOuterThreads - 1) / kOuterThreads), (unsigned)outer_blocks(M));
+    for (int c = 0; c < (int)r; ++c) {
+        const int acc = c > 0, sub = (c == 0 && subtract) ? 1 : 0;
+        const float* bb = (c == (int)r - 1) ? bias : nullptr;
+        if (op == 1) {
+            k_outer_blocksum<1><<<grid, kOuterThreads, 0, s>>>(X, M, q, ldx, idx, as, ss, c, part);
+            k_outer_apply<1><<<grid, kOuterThreads, 0, s>>>(X, M, q, ldx, idx, as, ss, c, part, Y, ldy, acc, sub, bb);
+        } else if (op == 2) {
+            k_outer_blocksum<2><<<grid, kOuterThreads, 0, s>>>(X, M, q, ldx, idx, as, ss, c, part);
+            k_outer_apply<2><<<grid, kOuterThreads, 0, s>>>(X, M, q, ldx, idx, as, ss, c, part, Y, ldy, acc, sub, bb);
+        } else {
+            k_outer_blocksum<0><<<grid, kOuterThreads, 0, s>>>(X, M, q, ldx, idx, as, ss, c, part);
+            k_outer_apply<0><<<grid, kOuterThreads, 0, s>>>(X, M, q, ldx, idx, as, ss, c, part, Y, ldy, acc, sub, bb);
+        }
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        MAPI_LAUNCHED();
+    }
+    return MAPI_OK;
+}
+
 }  // namespace
 
 // =============================================================================================
@@ -443,6 +488,8 @@ size_t mapi_workspace_size(int32_t op, int64_t n, int64_t nnz, int32_t k) {
                2 * align256(sizeof(double) * (size_t)k * (size_t)n) +
                align256(sizeof(double) * 64 * (size_t)n) + align256(sizeof(float) * (size_t)n);
     case MAPI_WS_ITERATE_BATCHED: return batched_ws_bytes(n, k);
+    case MAPI_WS_MAVP_DEFLATE: return outer_ws_bytes(n, n, 1, 0);
+    case MAPI_WS_RECONSTRUCT: return outer_ws_bytes(n, nnz, k, nnz);
     case MAPI_WS_CSR_PREPARE: return csr_prepare_ws_bytes(n, nnz);
     case MAPI_WS_RANK_CSR: return csr_rank_ws_bytes(n, nnz);
     }
@@ -750,6 +797,72 @@ mapi_status mapi_rank_csr(int64_t n, int64_t nnz, const int32_t* row_ptr, const 
     if (st == MAPI_ERR_DEGENERATE) return fail(st, "||G (+) w_t||_1 == 0");
     if (st == MAPI_ERR_NONFINITE) return fail(st, "||G (+) w_t||_1 is not finite");
     return st;
+}
+
+mapi_status mapi_center_rows(const float* V, int64_t M, int64_t N, int64_t ldv, float* Vc, int64_t ldvc,
+                             float* mean_out, mapi_stream_t stream) {
+    if (M < 0 || N < 1) return fail(MAPI_ERR_SHAPE, "M (%lld) must be >= 0 and N (%lld) >= 1", (long long)M, (long long)N);
+    if (ldv < N || ldvc < N) return fail(MAPI_ERR_SHAPE, "ldv (%lld) / ldvc (%lld) < N (%lld)", (long long)ldv,
+                                         (long long)ldvc, (long long)N);
+    if (M == 0) return MAPI_OK;
+    if (!V || !Vc || !mean_out) return fail(MAPI_ERR_NULL, "V, Vc or mean_out is NULL");
+    Device d;
+    mapi_status st;
+    if ((st = device_info(d)) != MAPI_OK) return st;
+    k_center_rows<<<(unsigned)((M + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(V, M, N, ldv, Vc, ldvc,
+                                                                                            mean_out);
+    MAPI_LAUNCHED();
+    return MAPI_OK;
+}
+
+mapi_status mapi_mavp_deflate(int32_t op, const float* C, int64_t M, int64_t ldc, const float* w, float* D,
+                              int64_t ldd, void* ws, size_t ws_bytes, mapi_stream_t stream) {
+    mapi_status st = check_op(op, true);
+    if (st != MAPI_OK) return st;
+    if (M < 1 || M > kOuterMaxM) return fail(MAPI_ERR_SHAPE, "M (%lld) must be in [1, %d]", (long long)M, kOuterMaxM);
+    if (ldc < M || ldd < M) return fail(MAPI_ERR_SHAPE, "ldc (%lld) / ldd (%lld) < M (%lld)", (long long)ldc,
+                                        (long long)ldd, (long long)M);
+    if (!C || !w || !D) return fail(MAPI_ERR_NULL, "C, w or D is NULL");
+    if (!ws) return fail(MAPI_ERR_WORKSPACE, "workspace is NULL");
+    const size_t need = outer_ws_bytes(M, M, 1, 0);
+    if (ws_bytes < need) return fail(MAPI_ERR_WORKSPACE, "ws_bytes (%zu) < required (%zu)", ws_bytes, need);
+    Device d;
+    if ((st = device_info(d)) != MAPI_OK) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    Timer timer(s);
+    timer.start();
+    st = outer_run(op, w, M, 1, 1, C, M, ldc, true, nullptr, D, ldd, static_cast<char*>(ws), s);
+    timer.stop();
+    if (st != MAPI_OK) return st;
+    if (timer.on) {
+        MAPI_CUDA(cudaStreamSynchronize(s));
+        timer.harvest();
+    }
+    return MAPI_OK;
+}
+
+mapi_status mapi_mavp_reconstruct(int32_t op, const float* W, int64_t M, int32_t r, int64_t ldw, const float* V,
+                                  int64_t N, int64_t ldv, float* Vhat, int64_t ldvh, float* mean_out, void* ws,
+                                  size_t ws_bytes, mapi_stream_t stream) {
+    mapi_status st = check_op(op, true);
+    if (st != MAPI_OK) return st;
+    if (M < 1 || M > kOuterMaxM) return fail(MAPI_ERR_SHAPE, "M (%lld) must be in [1, %d]", (long long)M, kOuterMaxM);
+    if (r < 1 || ldw < r) return fail(MAPI_ERR_SHAPE, "r (%d) must be >= 1 and ldw (%lld) >= r", r, (long long)ldw);
+    if (N < 1 || ldv < N || ldvh < N)
+        return fail(MAPI_ERR_SHAPE, "N (%lld) must be >= 1 with ldv, ldvh >= N", (long long)N);
+    if (!W || !V || !Vhat) return fail(MAPI_ERR_NULL, "W, V or Vhat is NULL");
+    if (!ws) return fail(MAPI_ERR_WORKSPACE, "workspace is NULL");
+    const size_t need = outer_ws_bytes(M, N, r, N);
+    if (ws_bytes < need) return fail(MAPI_ERR_WORKSPACE, "ws_bytes (%zu) < required (%zu)", ws_bytes, need);
+    Device d;
+    if ((st = device_info(d)) != MAPI_OK) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    char* p = static_cast<char*>(ws);
+    float* Xc = reinterpret_cast<float*>(p + outer_ws_bytes(M, N, r, N) - align256(sizeof(float) * (size_t)M * N));
+    if (!mean_out) return fail(MAPI_ERR_NULL, "mean_out is NULL (it is added back in step 8)");
+    k_center_rows<<<(unsigned)((M + 255) / 256), 256, 0, s>>>(V, M, N, ldv, Xc, N, mean_out);
+    MAPI_LAUNCHED();
+    return outer_run(op, W, M, r, ldw, Xc, N, N, false, mean_out, Vhat, ldvh, p, s);
 }
 
 }  // extern "C"

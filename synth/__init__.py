@@ -21,7 +21,7 @@ import hashlib
 
 import numpy as np
 
-__all__ = ["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "gnutella_like", "occluded_images", "rmat_edges",
+__all__ = ["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "gnutella_like", "occluded_images", "occluded_copies", "rmat_edges",
            "csr_by_destination", "random_matrix", "random_graph", "digest", "covariance_like"]
 
 
@@ -232,11 +232,11 @@ def random_graph(n, p_edge, seed, n_dangling=0):
     return np.stack([src, dst], 1).astype(np.int64), row_ptr, col_idx
 
 
-def occluded_images(D=128, N=10, seed=6, tiles=3, tile=32):
-    """Stand-in for the paper's image-reconstruction input (Alg. 2 steps 1-3): a smooth
+def occluded_copies(D=128, N=10, seed=6, tiles=3, tile=32):
+    """Stand-in for the paper's image-reconstruction input (Alg. 2 steps 1-2): a smooth
     synthetic D x D "image" with pixels in [0, 1] (sum of random low-frequency cosines, min-max
-    scaled), N copies each with `tiles` of the (D/tile)^2 tiles replaced by i.i.d. U[0,1] noise.
-    Returns V (D^2 x N) fp32 after the mean removal of Alg. 2 step 3, and the clean image.
+    scaled) and N copies, each with `tiles` of the (D/tile)^2 tiles replaced by i.i.d. U[0,1] noise.
+    Returns (V raw, D^2 x N fp32, the images as columns; the clean image, D x D fp64).
     Not the paper's images (unpublished): same shape, value range and corruption model."""
     r = np.random.default_rng(seed)
     yy, xx = np.meshgrid(np.arange(D) / D, np.arange(D) / D, indexing="ij")
@@ -253,8 +253,14 @@ def occluded_images(D=128, N=10, seed=6, tiles=3, tile=32):
             ty, tx = divmod(int(t), per)
             x[ty * tile:(ty + 1) * tile, tx * tile:(tx + 1) * tile] = r.random((tile, tile))
         V[:, i] = x.reshape(-1)
-    V = V - V.mean(axis=1, keepdims=True)
     return V.astype(np.float32), img
+
+
+def occluded_images(D=128, N=10, seed=6, tiles=3, tile=32):
+    """occluded_copies after the mean removal of Alg. 2 step 3: (V centred fp32, clean image)."""
+    V, img = occluded_copies(D, N, seed, tiles, tile)
+    V64 = V.astype(np.float64)
+    return (V64 - V64.mean(axis=1, keepdims=True)).astype(np.float32), img
 
 
 # ----------------------------------------------------------------------------------------

@@ -526,3 +526,12 @@ def test_psnr_closed_forms(orc):
     a = np.zeros(100)
     assert orc.psnr(a, np.full(100, 0.1)) == pytest.approx(20.0)  # MSE 0.01 -> 20 dB
     assert orc.psnr(a, np.ones(100)) == pytest.approx(0.0)  # MSE 1 -> 0 dB
+
+
+def test_outer_apply_rows_matches_full(orc):
+    r = np.random.default_rng(86)
+    W = r.standard_normal((40, 2)).astype(np.float32)
+    X = r.standard_normal((40, 5)).astype(np.float32)
+    full = orc.outer_apply(W, X, "min1", subtract=True)
+    rows = np.array([0, 7, 39, 7])
+    np.testing.assert_array_equal(orc.outer_apply_rows(W, X, rows, "min1", subtract=True), full[rows])
