@@ -58,6 +58,9 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=15.0, help="budget of the oracle sample")
+    p.add_argument("--mode", default="auto", choices=["auto", "single", "sharded", "replicas"],
+                   help="multi-GPU layout for cfg3: sharded = row-sharded MAPI with an NCCL all-gather of y per "
+                        "iteration (strong scaling, the default for N > 1); replicas = independent copies")
     p.add_argument("--op", default="min1", choices=["min1", "min2", "dot"],
                    help="MAVP operator (Eq. 3 / Eq. 4) or 'dot' = the RPI comparator of Eq. (1) (dense workloads)")
     return p.parse_args()
@@ -387,6 +390,35 @@ def build_alg2(args, m, dev, stream):
                 oracle=None)
 
 
+def build_sharded(args, m, dev, stream):
+    """cfg3 row-sharded over the ranks (paper_2110_12065_b200.sharded)."""
+    import torch
+
+    import synth
+    from paper_2110_12065_b200.sharded import iterate_sharded, row_partition
+
+    n, world, rank = 32768, args.world, args.rank
+    r0, r1 = row_partition(n, world, rank)
+    cfg = synth.cfg3_rows(r0, r1, device=dev)
+    A_local = cfg["A"]
+    b0 = torch.from_numpy(cfg["b0"]).to(dev)
+    iters = cfg["iters"]
+    opc = {"min1": 0, "min2": 1, "dot": 2}[args.op]
+
+    def step():
+        iterate_sharded(A_local, n, b0, iters, 0.0, op=opc)
+        return iters
+
+    job_bytes = dense_bytes_per_iter(n, n)
+    return Work(step=step, unit="iterations/s", per_launch=job_bytes * iters, bytes_per_unit=job_bytes, bound="hbm",
+                kernel=f"row-sharded step: K1 k_matvec on {r1 - r0} rows + NCCL all-gather of y + k_normalize_full, "
+                       "x100 (step time)", whole_step=True, shared_units=True,
+                config={"workload": f"cfg3: {WORKLOADS['cfg3']}", "n": n, "rows_per_rank": r1 - r0,
+                        "iters_per_step": iters, "op": args.op,
+                        "l2_flush": "inputs larger than L2 (4 GiB / N per rank)"},
+                A=A_local, b0=b0, iters=iters, oracle=None, sharded=True)
+
+
 BUILDERS = {"cfg1": build_dense, "alg2": build_alg2, "cfg3": build_dense, "cfg2": build_pca, "cfg4": build_batched,
             "cfg5": build_rank, "mincov": build_mincov, "mincov_k4096": build_mincov}
 
@@ -405,12 +437,18 @@ def run_mapi(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     m.load()
-    dist = world > 1
-    if dist:
-        import torch.distributed as tdist
+    import torch.distributed as tdist
+
+    dist = tdist.is_initialized() and world > 1
     stream = torch.cuda.current_stream()
     peak, peak_kind = peaks()
-    work = BUILDERS[args.workload](args, m, dev, stream)
+    args.rank, args.world = rank, world
+    mode = args.mode
+    if mode == "auto":
+        mode = "sharded" if (world > 1 and args.workload == "cfg3") else "single"
+    if mode == "sharded" and args.workload != "cfg3":
+        raise SystemExit("--mode sharded is implemented for the cfg3 workload")
+    work = build_sharded(args, m, dev, stream) if mode == "sharded" else BUILDERS[args.workload](args, m, dev, stream)
     torch.cuda.synchronize()
 
     metric = METRIC if args.workload == "cfg3" else f"MAPI {work.unit} ({args.workload})"
@@ -420,7 +458,11 @@ def run_mapi(args, rank, world, local_rank):
            "warmup": args.warmup, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
            "dtype": "f32", "data": "synthetic (seeded recipes, DESIGN.md §5)", "impl": "mapi-b200"}
     cfg_out = dict(work.config)
-    cfg_out["parallelism"] = f"replicas x{world} (independent problems, no collective)" if dist else "single GPU"
+    if getattr(work, "sharded", False):
+        cfg_out["parallelism"] = f"row-sharded x{world}: NCCL all-gather of y ({4 * 32768} B) per iteration"
+        out["scaling"] = "strong"
+    else:
+        cfg_out["parallelism"] = f"replicas x{world} (independent problems, no collective)" if dist else "single GPU"
 
     for _ in range(args.warmup):
         work.step()
@@ -454,7 +496,8 @@ def run_mapi(args, rank, world, local_rank):
     elapsed_ms = max_over_ranks(ev0.elapsed_time(ev1), dev)
     if dist:
         tdist.barrier()
-    value = units * world / (elapsed_ms / 1e3)
+    job_units = units if getattr(work, "shared_units", False) else units * world
+    value = job_units / (elapsed_ms / 1e3)
     kavg = float(np.mean(kernel_ms))
     if getattr(work, "whole_step", False):
         kavg = elapsed_ms / args.steps
@@ -462,13 +505,15 @@ def run_mapi(args, rank, world, local_rank):
                 "gpu_launches": int(launches), "wall_s_timed": t_wall})
     traffic = traffic_from_profiles(args.workload)
     if work.bound == "hbm":
-        out["hbm_gbs"] = work.bytes_per_unit * units / (elapsed_ms / 1e3) / 1e9
-        out["hbm_frac_of_measured"] = out["hbm_gbs"] / peak
-        out["hbm_frac_of_nominal_8000"] = out["hbm_gbs"] / 8000.0
+        gpus_in_roof = world if getattr(work, "sharded", False) else 1
+        out["hbm_gbs"] = work.bytes_per_unit * job_units / (elapsed_ms / 1e3) / 1e9
+        out["hbm_frac_of_measured"] = out["hbm_gbs"] / (peak * world)
+        out["hbm_frac_of_nominal_8000"] = out["hbm_gbs"] / (8000.0 * world)
         achieved = work.per_launch / (kavg / 1e3) / 1e9
-        out["roofline"] = {"bound": "hbm", "kernel": work.kernel, "achieved": achieved, "peak": peak,
+        peak_r = peak * gpus_in_roof
+        out["roofline"] = {"bound": "hbm", "kernel": work.kernel, "achieved": achieved, "peak": peak_r,
                            "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs, copy read+write)",
-                           "unit": "GB/s", "frac": achieved / peak, "algorithmic_bytes_per_launch": work.per_launch,
+                           "unit": "GB/s", "frac": achieved / peak_r, "algorithmic_bytes_per_launch": work.per_launch,
                            "kernel_ms_avg": kavg, "kernel_share_of_step": kavg / (elapsed_ms / args.steps),
                            "traffic": traffic}
     else:
@@ -486,7 +531,10 @@ def run_mapi(args, rank, world, local_rank):
         out["energy"] = {"joules": e1 - e0, "joules_per_unit": (e1 - e0) / units, "unit": work.unit.split("/")[0],
                          "avg_power_w": (e1 - e0) / t_wall, "source": "NVML total energy counter, timed region"}
     if args.workload == "cfg3" and not args.no_e2e:
-        out["e2e"] = e2e_dense(args, m, work.A, work.b0, work.iters, dev, stream, world, dist)
+        if getattr(work, "sharded", False):
+            out["e2e"] = e2e_sharded(args, m, work.A, work.b0, work.iters, dev, stream, world)
+        else:
+            out["e2e"] = e2e_dense(args, m, work.A, work.b0, work.iters, dev, stream, world, dist)
     if not args.no_cpu_baseline and world == 1 and rank == 0 and work.oracle is not None:
         if work.oracle[0] == "dense":
             out["cpu_baseline"] = cpu_baseline_dense(args, *work.oracle[1:])
@@ -538,6 +586,45 @@ def e2e_dense(args, m, A, b0, iters, dev, stream, world, dist):
             "h2d_bytes_per_step": 4 * n * lda + 4 * n, "d2h_bytes_per_step": 4 * n + 8 * iters + 8,
             "steps": steps, "ms_per_step": ms / steps,
             "path": "mapi_iterate_host: pinned host A,b0 -> device, 100 iterations, w + trace -> host"}
+
+
+def e2e_sharded(args, m, A_local, b0, iters, dev, stream, world):
+    """Row-sharded end to end: each rank copies its pinned host rows + b0 to the device, iterates with the
+    per-iteration all-gather, and copies w back, all inside the timed region."""
+    import torch
+    import torch.distributed as tdist
+
+    from paper_2110_12065_b200.sharded import iterate_sharded
+
+    n = b0.numel()
+    A_h = A_local.cpu().pin_memory()
+    b0_h = b0.cpu().pin_memory()
+    A_d = torch.empty_like(A_local)
+    b0_d = torch.empty_like(b0)
+    w_h = torch.empty(n, dtype=torch.float32, pin_memory=True)
+
+    def step():
+        A_d.copy_(A_h, non_blocking=True)
+        b0_d.copy_(b0_h, non_blocking=True)
+        res = iterate_sharded(A_d, n, b0_d, iters, 0.0)
+        w_h.copy_(res.w, non_blocking=True)
+
+    step()
+    steps = max(2, min(args.steps, 5))
+    torch.cuda.synchronize()
+    if tdist.is_initialized():
+        tdist.barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(steps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    ms = max_over_ranks(ev0.elapsed_time(ev1), dev)
+    return {"value": iters * steps / (ms / 1e3), "unit": "iterations/s",
+            "h2d_bytes_per_step": world * (4 * A_local.numel() + 4 * n), "d2h_bytes_per_step": world * 4 * n,
+            "steps": steps, "ms_per_step": ms / steps,
+            "path": "row-sharded: pinned host row blocks -> each GPU, 100 iterations with all-gathers, w -> host"}
 
 
 def cpu_baseline_dense(args, A, b0, iters):
@@ -644,7 +731,8 @@ def main():
         if out is not None:
             print(json.dumps(out), flush=True)
         return
-    if world > 1:
+    launched = "WORLD_SIZE" in os.environ  # torchrun (any size, incl. 1) -> NCCL process group
+    if launched:
         import torch
         import torch.distributed as tdist
 
@@ -653,7 +741,7 @@ def main():
     out = run_mapi(args, rank, world, local_rank)
     if rank == 0:
         print(json.dumps(out), flush=True)
-    if world > 1:
+    if launched:
         import torch.distributed as tdist
 
         tdist.destroy_process_group()

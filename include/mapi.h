@@ -103,6 +103,14 @@ mapi_status mapi_iterate(int32_t op, const float *A, int64_t n, int64_t lda, con
                          float *deltas, int32_t *iters_done, void *ws, size_t ws_bytes,
                          mapi_stream_t stream);
 
+/* One normalisation step of Algorithm 1 on a full y (used by the row-sharded multi-GPU path after
+ * the all-gather of y):  s = ||y|| (l1 for MIN1/MIN2, l2 for DOT; fp64, fixed order),
+ * w_new = fp32(y / s), delta = ||w_new - w||_1;  w (n, in/out), *s_out and *delta_out (device, float,
+ * nullable), status_out (device int32[1], nullable): 0, MAPI_ERR_DEGENERATE or MAPI_ERR_NONFINITE (w is
+ * left unchanged then).  One CTA, deterministic; every rank computes the same bits.  Asynchronous. */
+mapi_status mapi_normalize(int32_t op, const float *y, int64_t n, float *w, float *s_out, float *delta_out,
+                           int32_t *status_out, mapi_stream_t stream);
+
 /* mapi_iterate with HOST buffers (end-to-end path): A_host (n x lda), b0_host, w_out_host,
  * w_l2_out_host / norms_host / deltas_host (nullable), iters_done (host).  The call copies A and
  * b0 host->device into the device workspace `ws` (mapi_workspace_size(MAPI_WS_ITERATE_HOST,

@@ -59,6 +59,7 @@ def load():
             "mapi_mavp_matvec": (st, [i32, P, i64, i64, i64, P, P, P]),
             "mapi_mavp_matmat": (st, [i32, P, i64, i64, i64, P, i64, i64, f32, P, i64, P]),
             "mapi_center_rows": (st, [P, i64, i64, i64, P, i64, P, P]),
+            "mapi_normalize": (st, [i32, P, i64, P, P, P, P, P]),
             "mapi_mavp_deflate": (st, [i32, P, i64, i64, P, P, i64, P, sz, P]),
             "mapi_mavp_reconstruct": (st, [i32, P, i64, i32, i64, P, i64, i64, P, i64, P, P, sz, P]),
             "mapi_iterate": (st, [i32, P, i64, i64, P, i32, f32, P, P, P, P, P, P, sz, P]),
@@ -192,6 +193,15 @@ def min_covariance(V, divisor=None, op: int = MIN1, stream=None):
     d = N - 1 by default as in Alg. 2 step 4."""
     d = (V.shape[1] - 1) if divisor is None else divisor
     return mavp_matmat(V, V, float(d), op=op, stream=stream)
+
+
+def normalize(y, w, s_out=None, delta_out=None, status_out=None, op: int = MIN1, stream=None):
+    """One Algorithm 1 normalisation on a full y: w <- y / ||y|| (l1; l2 for DOT), delta."""
+    torch = _torch()
+    _need(y, "y", torch.float32)
+    _need(w, "w", torch.float32, tuple(y.shape))
+    _check(load().mapi_normalize(op, _ptr(y), y.numel(), _ptr(w), _ptr(s_out), _ptr(delta_out), _ptr(status_out),
+                                 _stream(stream)))
 
 
 def center_rows(V, Vc=None, stream=None):

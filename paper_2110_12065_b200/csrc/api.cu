@@ -865,4 +865,18 @@ mapi_status mapi_mavp_reconstruct(int32_t op, const float* W, int64_t M, int32_t
     return outer_run(op, W, M, r, ldw, Xc, N, N, false, mean_out, Vhat, ldvh, p, s);
 }
 
+mapi_status mapi_normalize(int32_t op, const float* y, int64_t n, float* w, float* s_out, float* delta_out,
+                           int32_t* status_out, mapi_stream_t stream) {
+    mapi_status st = check_op(op, true);
+    if (st != MAPI_OK) return st;
+    if (n < 1) return fail(MAPI_ERR_SHAPE, "n (%lld) must be >= 1", (long long)n);
+    if (!y || !w) return fail(MAPI_ERR_NULL, "y or w is NULL");
+    Device d;
+    if ((st = device_info(d)) != MAPI_OK) return st;
+    k_normalize_full<<<1, 1024, 0, static_cast<cudaStream_t>(stream)>>>(n, y, w, op == MAPI_OP_DOT ? 1 : 0, s_out,
+                                                                        delta_out, status_out);
+    MAPI_LAUNCHED();
+    return MAPI_OK;
+}
+
 }  // extern "C"

@@ -549,6 +549,39 @@ __global__ void __launch_bounds__(1024) k_normalize(int64_t n, const float* __re
 }
 
 // ---------------------------------------------------------------------------------------------
+// Stand-alone normalisation step (row-sharded path): one CTA, fixed order, fp64 reductions.
+__global__ void __launch_bounds__(1024) k_normalize_full(int64_t n, const float* __restrict__ y, float* __restrict__ w,
+                                                         int l2, float* s_out, float* delta_out, int32_t* status) {
+    __shared__ double red[33];
+    double part = 0.0;
+    for (int64_t k = threadIdx.x; k < n; k += blockDim.x) {
+        const double v = (double)y[k];
+        part += l2 ? v * v : fabs(v);
+    }
+    double s = block_sum(part, red);
+    if (l2) s = sqrt(s);
+    if (!(s > 0.0) || isinf(s)) {
+        if (threadIdx.x == 0) {
+            if (status) *status = (s == 0.0) ? kStDegenerate : kStNonfinite;
+            if (s_out) *s_out = (float)s;
+        }
+        return;
+    }
+    double dp = 0.0;
+    for (int64_t k = threadIdx.x; k < n; k += blockDim.x) {
+        const float wn = (float)((double)y[k] / s);
+        dp += (double)fabsf(wn - w[k]);
+        w[k] = wn;
+    }
+    const double d = block_sum(dp, red);
+    if (threadIdx.x == 0) {
+        if (status) *status = kStOk;
+        if (s_out) *s_out = (float)s;
+        if (delta_out) *delta_out = (float)d;
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
 // Optional final l2 copy (Alg. 1 line 6): the n multiplies of the whole run, once.
 // One CTA, fixed order.  Works on `rows` independent vectors of length n (vector-major).
 __global__ void __launch_bounds__(1024) k_l2_copy(int64_t n, const float* __restrict__ w,

@@ -21,7 +21,7 @@ import hashlib
 
 import numpy as np
 
-__all__ = ["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "gnutella_like", "occluded_images", "occluded_copies", "rmat_edges",
+__all__ = ["cfg1", "cfg2", "cfg3", "cfg3_rows", "covariance_like_rows", "cfg4", "cfg5", "gnutella_like", "occluded_images", "occluded_copies", "rmat_edges",
            "csr_by_destination", "random_matrix", "random_graph", "digest", "covariance_like"]
 
 
@@ -94,6 +94,60 @@ def covariance_like(F, scale, diag=None, device=None, block=4096):
         out = torch.empty((n, n), dtype=torch.float32, device=device)
     return _sym_product_blocks(np.ascontiguousarray(F, dtype=np.float64), scale,
                                np.asarray(diag, np.float64), out, block, device)
+
+
+def covariance_like_rows(F, scale, diag, row0, row1, device=None, block=4096):
+    """Rows [row0, row1) of covariance_like(F, scale, diag, device, block), computed with the same block
+    convention (upper-triangle blocks as F_bi F_bj^T, lower ones as their transposes), so every rank of a
+    row-sharded run generates exactly its slice of the same matrix.  row0 must be a multiple of block."""
+    n = F.shape[0]
+    if row0 % block != 0:
+        raise ValueError("row0 must be a multiple of the block size")
+    F = np.ascontiguousarray(F, dtype=np.float64)
+    diag = np.asarray(diag, np.float64)
+    if device is None:
+        out = np.empty((row1 - row0, n), np.float32)
+        mm = lambda a, b: a @ b.T  # noqa: E731
+        Fd = F
+    else:
+        import torch
+
+        out = torch.empty((row1 - row0, n), dtype=torch.float32, device=device)
+        Fd = torch.from_numpy(F).to(device)
+        mm = lambda a, b: a @ b.T  # noqa: E731
+    for r0 in range(row0, row1, block):
+        r1 = min(row1, r0 + block)
+        for c0 in range(0, n, block):
+            c1 = min(n, c0 + block)
+            if c0 >= r0:
+                M = mm(Fd[r0:r1], Fd[c0:c1]) * scale
+                if c0 == r0:
+                    idx = np.arange(r1 - r0)
+                    if device is None:
+                        M[idx, idx] += diag[r0:r1]
+                        M = np.triu(M) + np.triu(M, 1).T
+                    else:
+                        import torch
+
+                        ti = torch.arange(r1 - r0, device=device)
+                        M[ti, ti] += torch.from_numpy(diag[r0:r1]).to(device)
+                        M = torch.triu(M) + torch.triu(M, 1).T
+                blk = M.astype(np.float32) if device is None else M.to(torch.float32)
+            else:  # lower block: transpose of the (c, r) upper block, as covariance_like mirrors it
+                M = mm(Fd[c0:c1], Fd[r0:r1]) * scale
+                blk = (M.astype(np.float32) if device is None else M.to(torch.float32)).T
+            out[r0 - row0:r1 - row0, c0:c1] = blk
+    return out
+
+
+def cfg3_rows(row0, row1, device=None, n=32768, rank=512):
+    """Rows [row0, row1) of cfg3's A (row-sharded multi-GPU runs)."""
+    r = np.random.default_rng(2)
+    G = r.standard_normal((n, rank))
+    z = r.standard_normal(n)
+    A = covariance_like_rows(G, 1.0 / n, 10.0 * np.abs(z), row0, row1, device=device)
+    b0 = np.full(n, 1.0 / np.sqrt(n), dtype=np.float32)
+    return {"name": "cfg3", "A": A, "b0": b0, "iters": 100, "tol": 0.0, "row0": row0, "row1": row1}
 
 
 def cfg1():

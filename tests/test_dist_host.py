@@ -57,3 +57,84 @@ def test_max_over_ranks_single_process():
     import bench
 
     assert bench.max_over_ranks(3.5) == 3.5
+
+
+# ---------------------------------------------------------------- row-sharded MAPI orchestration (NEXT-4)
+
+
+def _sharded_worker(rank, world, port, q):
+    import sys
+
+    import numpy as np
+    import torch
+    import torch.distributed as tdist
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle
+    from paper_2110_12065_b200.sharded import iterate_sharded, row_partition
+
+    n = 48
+    r = np.random.default_rng(3)
+    A = (r.standard_normal((n, n)) + np.eye(n) * 2).astype(np.float32)
+    b0 = np.full(n, 1 / np.sqrt(n), np.float32)
+    r0, r1 = row_partition(n, world, rank)
+
+    # CPU stand-ins for the CUDA steps (test only): oracle mat-vec of the local rows, and the
+    # Algorithm 1 normalisation written out in numpy (fp64, fixed order)
+    def local_matvec(A_loc, w, y_loc):
+        y_loc.copy_(torch.from_numpy(oracle.matvec(A_loc.numpy(), w.numpy().astype(np.float64)).astype(np.float32)))
+
+    def normalize(y, w, s_out, d_out, st_out):
+        yv = y.numpy().astype(np.float64)
+        s = np.sum(np.abs(yv))
+        wn = (yv / s).astype(np.float32)
+        d_out[0] = float(np.sum(np.abs(wn.astype(np.float64) - w.numpy().astype(np.float64))))
+        s_out[0] = s
+        st_out[0] = 0
+        w.copy_(torch.from_numpy(wn))
+
+    res = iterate_sharded(torch.from_numpy(A[r0:r1].copy()), n, torch.from_numpy(b0), 12,
+                          local_matvec=local_matvec, normalize=normalize,
+                          all_gather=lambda full, part: tdist.all_gather_into_tensor(full, part))
+    q.put((rank, res.w.numpy().copy(), res.norms.numpy().copy(), res.iters_done))
+    tdist.barrier()
+    tdist.destroy_process_group()
+
+
+def test_row_sharded_mapi_gloo_world2():
+    """Two ranks, each holding half of A's rows: every rank ends with the same w, equal to the
+    single-process MAPI of the oracle (the shard/gather/normalise orchestration of DESIGN.md §8)."""
+    import numpy as np
+
+    import oracle
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sharded_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = {r: (w, nr, k) for r, w, nr, k in [q.get(timeout=180) for _ in range(2)]}
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    np.testing.assert_array_equal(out[0][0], out[1][0])  # identical on every rank
+    n = 48
+    r = np.random.default_rng(3)
+    A = (r.standard_normal((n, n)) + np.eye(n) * 2).astype(np.float32)
+    ref = oracle.mapi(A, np.full(n, 1 / np.sqrt(n), np.float32), 12)
+    np.testing.assert_allclose(out[0][0], ref.w, rtol=2e-6, atol=1e-7)
+    np.testing.assert_allclose(out[0][1], ref.norms, rtol=1e-6)
+    assert out[0][2] == 12
+
+
+def test_row_partition():
+    from paper_2110_12065_b200.sharded import row_partition
+
+    assert [row_partition(32768, 8, r) for r in (0, 7)] == [(0, 4096), (28672, 32768)]
+    import pytest
+
+    with pytest.raises(ValueError):
+        row_partition(10, 3, 0)

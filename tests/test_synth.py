@@ -52,3 +52,12 @@ def test_random_matrix_padding_is_nan():
     M, lda = synth.random_matrix(5, 7, seed=1, lda=9, kind="mixed")
     assert lda == 9 and M.shape == (5, 9)
     assert np.all(np.isnan(M[:, 7:])) and np.all(np.isfinite(M[:, :7]))
+
+
+def test_covariance_like_rows_is_a_slice_of_the_full_matrix():
+    r = np.random.default_rng(5)
+    F = r.standard_normal((96, 7))
+    d = np.abs(r.standard_normal(96))
+    full = synth.covariance_like(F, 0.25, d, block=32)
+    for row0, row1 in ((0, 32), (32, 64), (64, 96), (32, 96)):
+        np.testing.assert_array_equal(synth.covariance_like_rows(F, 0.25, d, row0, row1, block=32), full[row0:row1])
