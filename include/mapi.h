@@ -111,6 +111,16 @@ mapi_status mapi_iterate(int32_t op, const float *A, int64_t n, int64_t lda, con
 mapi_status mapi_normalize(int32_t op, const float *y, int64_t n, float *w, float *s_out, float *delta_out,
                            int32_t *status_out, mapi_stream_t stream);
 
+/* One fused Algorithm 1 step for a block of rows given the previous FULL y (row-sharded path,
+ * DESIGN.md §8): x = y_prev / ||y_prev|| (l1; l2 for DOT), y_out = A (op) x for the n_rows rows of A
+ * (n_cols = length of y_prev), and w_next = x, *s_out = ||y_prev||, *delta_out = ||x - w_prev||_1,
+ * *status_out as in mapi_normalize (device pointers, nullable).  Every CTA derives x itself in the same
+ * fixed order, so no separate normalisation launch is needed.  n_cols * 4 bytes must fit in shared
+ * memory (n_cols <= 51200).  Asynchronous. */
+mapi_status mapi_matvec_normalized(int32_t op, const float *A, int64_t n_rows, int64_t n_cols, int64_t lda,
+                                   const float *y_prev, const float *w_prev, float *w_next, float *y_out,
+                                   float *s_out, float *delta_out, int32_t *status_out, mapi_stream_t stream);
+
 /* mapi_iterate with HOST buffers (end-to-end path): A_host (n x lda), b0_host, w_out_host,
  * w_l2_out_host / norms_host / deltas_host (nullable), iters_done (host).  The call copies A and
  * b0 host->device into the device workspace `ws` (mapi_workspace_size(MAPI_WS_ITERATE_HOST,

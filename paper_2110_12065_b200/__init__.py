@@ -60,6 +60,7 @@ def load():
             "mapi_mavp_matmat": (st, [i32, P, i64, i64, i64, P, i64, i64, f32, P, i64, P]),
             "mapi_center_rows": (st, [P, i64, i64, i64, P, i64, P, P]),
             "mapi_normalize": (st, [i32, P, i64, P, P, P, P, P]),
+            "mapi_matvec_normalized": (st, [i32, P, i64, i64, i64, P, P, P, P, P, P, P, P]),
             "mapi_mavp_deflate": (st, [i32, P, i64, i64, P, P, i64, P, sz, P]),
             "mapi_mavp_reconstruct": (st, [i32, P, i64, i32, i64, P, i64, i64, P, i64, P, P, sz, P]),
             "mapi_iterate": (st, [i32, P, i64, i64, P, i32, f32, P, P, P, P, P, P, sz, P]),

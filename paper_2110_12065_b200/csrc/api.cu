@@ -879,4 +879,47 @@ mapi_status mapi_normalize(int32_t op, const float* y, int64_t n, float* w, floa
     return MAPI_OK;
 }
 
+mapi_status mapi_matvec_normalized(int32_t op, const float* A, int64_t n_rows, int64_t n_cols, int64_t lda,
+                                   const float* y_prev, const float* w_prev, float* w_next, float* y_out,
+                                   float* s_out, float* delta_out, int32_t* status_out, mapi_stream_t stream) {
+    mapi_status st = check_op(op, true);
+    if (st != MAPI_OK) return st;
+    if (n_rows < 0 || n_cols < 1) return fail(MAPI_ERR_SHAPE, "n_rows (%lld) >= 0 and n_cols (%lld) >= 1 required",
+                                              (long long)n_rows, (long long)n_cols);
+    if (lda < n_cols) return fail(MAPI_ERR_SHAPE, "lda (%lld) < n_cols (%lld)", (long long)lda, (long long)n_cols);
+    if (!y_prev || !w_prev || !w_next || (n_rows > 0 && (!A || !y_out)))
+        return fail(MAPI_ERR_NULL, "a required pointer (A/y_prev/w_prev/w_next/y_out) is NULL");
+    const size_t smem = sizeof(float) * (size_t)n_cols;
+    if (smem > 200 * 1024) return fail(MAPI_ERR_SHAPE, "n_cols (%lld) too large for the staged x", (long long)n_cols);
+    Device d;
+    if ((st = device_info(d)) != MAPI_OK) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int vec = vec_width(A ? A : y_prev, lda);
+    const int pol = load_policy(d, n_rows, lda);
+    with_op(op, [&](auto OPc) {
+        return with_vec(vec, [&](auto VECc) {
+            return with_pol(pol, [&](auto POLc) {
+                constexpr int OP = decltype(OPc)::value, VEC = decltype(VECc)::value, POL = decltype(POLc)::value;
+                auto kern = k_matvec_norm<OP, VEC, POL, unroll_for(VEC)>;
+                cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                int occ = 1;
+                if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 512, smem);
+                if (e != cudaSuccess) {
+                    st = fail(MAPI_ERR_CUDA, "matvec_normalized setup: %s", cudaGetErrorString(e));
+                    return 0;
+                }
+                const int64_t want = std::max<int64_t>(1, (n_rows + 15) / 16);
+                const int grid = (int)std::min<int64_t>((int64_t)std::max(occ, 1) * d.sms, want);
+                kern<<<grid, 512, smem, s>>>(A, n_rows, n_cols, lda, y_prev, w_prev, w_next, y_out, s_out, delta_out,
+                                            status_out);
+                g_launches.fetch_add(1, std::memory_order_relaxed);
+                e = cudaGetLastError();
+                if (e != cudaSuccess) st = fail(MAPI_ERR_CUDA, "matvec_normalized launch: %s", cudaGetErrorString(e));
+                return 0;
+            });
+        });
+    });
+    return st;
+}
+
 }  // extern "C"

@@ -17,6 +17,9 @@ namespace mapi {
 
 constexpr int kFold = 128;  // max fp32 terms per accumulator chain before folding
 
+// status codes (mirror mapi_status)
+constexpr int kStOk = 0, kStDegenerate = 4, kStNonfinite = 6;
+
 // L2 bulk prefetch of `bytes` (multiple of 16) starting at 16 B-aligned `p` (no register cost).
 __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
@@ -101,6 +104,52 @@ __global__ void __launch_bounds__(512, 1) k_matvec(const float* __restrict__ A, 
 }
 
 // ---------------------------------------------------------------------------------------------
+// K1n: one fused Algorithm 1 step for a row block, given the previous FULL y (row-sharded path):
+//   s = ||y_prev|| (l1; l2 for DOT; fp64, the same fixed order in every CTA and on every rank),
+//   x = fp32(y_prev / s) staged into shared memory,  y_out = A_rows (op) x  (as K1),
+//   CTA 0 also writes w_next = x, s_out, delta_out = ||x - w_prev||_1 and the status word.
+template <int OP, int VEC, int POL, int U>
+__global__ void __launch_bounds__(512, 1) k_matvec_norm(const float* __restrict__ A, int64_t n_rows, int64_t n_cols,
+                                                        int64_t lda, const float* __restrict__ y_prev,
+                                                        const float* __restrict__ w_prev, float* __restrict__ w_next,
+                                                        float* __restrict__ y, float* s_out, float* delta_out,
+                                                        int32_t* status) {
+    extern __shared__ __align__(16) float xs[];
+    __shared__ double red[33];
+    double part = 0.0;
+    for (int64_t k = threadIdx.x; k < n_cols; k += blockDim.x) part += norm_part<OP>(y_prev[k]);
+    const double sd = norm_final<OP>(block_sum(part, red));
+    if (!(sd > 0.0) || isinf(sd)) {  // uniform in every CTA
+        if (blockIdx.x == 0 && threadIdx.x == 0 && status) *status = (sd == 0.0) ? kStDegenerate : kStNonfinite;
+        return;
+    }
+    double dp = 0.0;
+    for (int64_t k = threadIdx.x; k < n_cols; k += blockDim.x) {
+        const float x = (float)((double)y_prev[k] / sd);
+        xs[k] = x;
+        if (blockIdx.x == 0) {
+            dp += (double)fabsf(x - w_prev[k]);
+            w_next[k] = x;
+        }
+    }
+    if (blockIdx.x == 0) {
+        const double d = block_sum(dp, red);
+        if (threadIdx.x == 0) {
+            if (s_out) *s_out = (float)sd;
+            if (delta_out) *delta_out = (float)d;
+            if (status) *status = kStOk;
+        }
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < n_rows; row += warps) {
+        const float v = row_mavp<OP, VEC, POL, false, U>(A + row * lda, xs, n_cols, lane);
+        if (lane == 0) y[row] = v;
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
 // K2 persistent MAPI iteration.
 struct IterArgs {
     const float* A;
@@ -117,8 +166,6 @@ struct IterArgs {
     int32_t* status;   // [0] status, [1] iters_done
 };
 
-// status codes (mirror mapi_status)
-constexpr int kStOk = 0, kStDegenerate = 4, kStNonfinite = 6;
 
 template <int OP, int VEC, int POL, int U, int PF = 0, int PH = 0, int MINB = 1>
 __global__ void __launch_bounds__(512, MINB) k_iterate_persistent(IterArgs p) {

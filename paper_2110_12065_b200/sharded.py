@@ -60,26 +60,37 @@ def iterate_sharded(A_local, n: int, b0, iters: int, tol: float = 0.0, op: int =
     norms = torch.zeros(iters, dtype=torch.float32, device=dev)
     deltas = torch.zeros(iters, dtype=torch.float32, device=dev)
     status = torch.zeros(iters, dtype=torch.int32, device=dev)
-    if local_matvec is None and normalize is None:
-        # product path: raw C-ABI calls with precomputed pointers (host overhead per iteration ~ a few us)
+    fused = local_matvec is None and normalize is None
+    if fused:
+        # product path, one kernel + one all-gather per iteration: iteration t's launch normalises the
+        # gathered y_{t-1} inside every CTA (mapi_matvec_normalized) and then computes its local rows
         from . import load
 
         lib = load()
         if A_local.dim() != 2 or A_local.stride(1) != 1:
             raise ValueError("A_local must be a row-major fp32 CUDA tensor")
         sp = torch.cuda.current_stream(dev).cuda_stream
-        pa, lda, pw, pyl, py = A_local.data_ptr(), A_local.stride(0), w.data_ptr(), y_local.data_ptr(), y.data_ptr()
+        wbuf = torch.empty(2, n, dtype=torch.float32, device=dev)
+        wbuf[0].copy_(w)
+        pa, lda, pyl, py = A_local.data_ptr(), A_local.stride(0), y_local.data_ptr(), y.data_ptr()
+        pw = [wbuf[0].data_ptr(), wbuf[1].data_ptr()]
         pn, pd, ps = norms.data_ptr(), deltas.data_ptr(), status.data_ptr()
 
-        def local_matvec(A, w_, yl):  # noqa: ARG001
-            st = lib.mapi_mavp_matvec(op, pa, rows, n, lda, pw, pyl, sp)
+        def fused_step(t):
+            if t == 0:  # w_0 = b0 as given: plain mat-vec
+                st = lib.mapi_mavp_matvec(op, pa, rows, n, lda, pw[0], pyl, sp)
+            else:  # w_t = y_{t-1}/s_{t-1} (recorded as iteration t-1), then y_local = A_local (op) w_t
+                st = lib.mapi_matvec_normalized(op, pa, rows, n, lda, py, pw[(t - 1) & 1], pw[t & 1], pyl,
+                                                pn + 4 * (t - 1), pd + 4 * (t - 1), ps + 4 * (t - 1), sp)
             if st:
                 raise MapiError(st, lib.mapi_last_error_message().decode())
 
-        def step_normalize(t):
-            st = lib.mapi_normalize(op, py, n, pw, pn + 4 * t, pd + 4 * t, ps + 4 * t, sp)
+        def final_normalize(t):  # the normalisation of the last gathered y (iteration t)
+            tmp = wbuf[t & 1].clone()
+            st = lib.mapi_normalize(op, py, n, tmp.data_ptr(), pn + 4 * t, pd + 4 * t, ps + 4 * t, sp)
             if st:
                 raise MapiError(st, lib.mapi_last_error_message().decode())
+            return tmp
     else:
         local_matvec = local_matvec or (lambda A, w_, yl: _matvec(A, w_, yl, op=op))
         normalize = normalize or (lambda y_, w_, s_, d_, st_: _normalize(y_, w_, s_, d_, st_, op=op))
@@ -91,17 +102,34 @@ def iterate_sharded(A_local, n: int, b0, iters: int, tol: float = 0.0, op: int =
             else (lambda full, part: full.copy_(part))
     check_every = check_every or 1
     done = 0
-    for t in range(iters):
-        local_matvec(A_local, w, y_local)
-        all_gather(y, y_local)
-        step_normalize(t)
-        done = t + 1
-        if tol > 0.0 and (done % check_every == 0):
-            st = int(status[t].item())
-            if st != 0:
-                raise MapiError(st, f"{STATUS.get(st, st)} at iteration {t}", t)
-            if float(deltas[t].item()) < tol:
-                break
+    if fused:
+        # the stop test of iteration t is known after launch t+1; a stop at t discards that extra launch's y
+        for t in range(iters):
+            fused_step(t)
+            all_gather(y, y_local)
+            if t > 0 and tol > 0.0 and (t % check_every == 0):
+                st = int(status[t - 1].item())
+                if st != 0:
+                    raise MapiError(st, f"{STATUS.get(st, st)} at iteration {t - 1}", t - 1)
+                if float(deltas[t - 1].item()) < tol:
+                    done = t
+                    w = wbuf[t & 1].clone()
+                    break
+        else:
+            w = final_normalize(iters - 1)
+            done = iters
+    else:
+        for t in range(iters):
+            local_matvec(A_local, w, y_local)
+            all_gather(y, y_local)
+            step_normalize(t)
+            done = t + 1
+            if tol > 0.0 and (done % check_every == 0):
+                st = int(status[t].item())
+                if st != 0:
+                    raise MapiError(st, f"{STATUS.get(st, st)} at iteration {t}", t)
+                if float(deltas[t].item()) < tol:
+                    break
     st = status[:done].cpu()
     bad = (st != 0).nonzero()
     if bad.numel():
