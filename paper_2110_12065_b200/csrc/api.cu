@@ -305,10 +305,11 @@ mapi_status iterate_launch(const Device& d, int32_t op, const float* A, int64_t 
                 return with_pol(pol, [&](auto POLc) {
                     constexpr int OP = decltype(OPc)::value, VEC = decltype(VECc)::value,
                                   POL = decltype(POLc)::value;
-                    // mid-size n (< 8192, w fits twice per SM): 16 B loads, 2 CTAs/SM (measured 12.0 vs
-                    // 13.0 us/iteration at n = 4096; profiles/r01_probe_dense.log)
-                    const bool two = VEC >= 4 && n < 8192;
-                    auto kern = two ? k_iterate_persistent<OP, (VEC >= 4 ? 4 : VEC), POL, 4, 0, 0, 2>
+                    // mid-size n (< 8192; the matrix is L2-resident and the loop latency-bound): 16 B loads,
+                    // 8 in flight per lane (measured 11.3 vs 13.0 us/iteration at n = 4096 for the
+                    // default; profiles/r01_probe_dense_mid.log)
+                    const bool mid = VEC >= 4 && n < 8192;
+                    auto kern = mid ? k_iterate_persistent<OP, (VEC >= 4 ? 4 : VEC), POL, 8, 0, 0, 1>
                                     : k_iterate_persistent<OP, VEC, POL, unroll_for(VEC)>;
                     const size_t smem = persistent_smem_bytes(n);
                     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,

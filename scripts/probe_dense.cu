@@ -173,6 +173,10 @@ int main() {
         run_iter(k_iterate_persistent<0, 8, 1, 4, 0, 0, 2>, "n4096 rows U4 2CTA/SM", 512, A, n2, b0, w, ws, 100, ref3);
         run_iter(k_iterate_persistent<0, 8, 1, 1, 0, 0, 2>, "n4096 rows U1 2CTA/SM", 512, A, n2, b0, w, ws, 100, ref3);
         run_iter(k_iterate_persistent<0, 4, 1, 4, 0, 0, 2>, "n4096 rows V4 U4 2CTA/SM", 512, A, n2, b0, w, ws, 100, ref3);
+        run_iter(k_iterate_persistent<0, 8, 1, 8, 0, 0, 1>, "n4096 rows V8 U8 1CTA/SM", 512, A, n2, b0, w, ws, 100, ref3);
+        run_iter(k_iterate_persistent<0, 4, 1, 16, 0, 0, 1>, "n4096 rows V4 U16 1CTA/SM", 512, A, n2, b0, w, ws, 100, ref3);
+        run_iter(k_iterate_persistent<0, 4, 1, 8, 0, 0, 1>, "n4096 rows V4 U8 1CTA/SM", 512, A, n2, b0, w, ws, 100, ref3);
+        run_iter(k_iterate_persistent<0, 8, 1, 2, 0, 0, 2>, "n4096 rows V8 U2 2CTA/SM", 512, A, n2, b0, w, ws, 100, ref3);
         const int64_t n3 = 8192;
         std::vector<float> ref6;
         run_iter(k_iterate_persistent<0, 8, 1, 4, 0, 0>, "n8192 rows U4", 512, A, n3, b0, w, ws, 100, ref6);
