@@ -479,17 +479,17 @@ def run_mapi(args, rank, world, local_rank):
     sampler.start()
     time.sleep(0.3)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record(stream)
-    e0 = meter.read()
+    e0 = meter.read()  # (an NVML read takes ~tens of ms: never inside the event bracket)
     t_wall = time.perf_counter()
+    ev0.record(stream)
     units = 0
     for _ in range(args.steps):
         units += work.step()
         kernel_ms.append(m.last_kernel_ms())
     ev1.record(stream)
     torch.cuda.synchronize()
-    t_wall = time.perf_counter() - t_wall
     e1 = meter.read()
+    t_wall = time.perf_counter() - t_wall
     launches = m.launch_count() - launches0
     clocks = sampler.stop()
     m.set_profiling(False)

@@ -1,19 +1,19 @@
 # full GPU suite + every workload's bench line (round-end style)
 mkdir -p gpurun_out
-timeout 1800 python -m pytest tests -m gpu -q --timeout 900 > gpurun_out/pytest_all.log 2>&1; tail -3 gpurun_out/pytest_all.log
+timeout 2400 python -m pytest tests -m gpu -q --timeout 900 > gpurun_out/pytest_all.log 2>&1; tail -3 gpurun_out/pytest_all.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; tail -1 gpurun_out/smoke.log
 timeout 600 python bench.py > gpurun_out/bench_default.log 2>&1; echo "default rc=$?"
-for w in cfg1 cfg2 cfg4 cfg5; do
+for w in cfg1 cfg2 cfg4 cfg5 mincov mincov_k4096 alg2; do
   timeout 900 python bench.py --workload $w --steps 5 --warmup 3 --cpu-seconds 8 > gpurun_out/bench_$w.log 2>&1; echo "$w rc=$?"
 done
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_reference.log 2>&1; echo "ref rc=$?"
 python - <<'PY'
 import json
-for w in ["default","cfg1","cfg2","cfg4","cfg5","reference"]:
+for w in ["default","cfg1","cfg2","cfg4","cfg5","mincov","mincov_k4096","alg2","reference"]:
     try:
         d=json.loads(open(f"gpurun_out/bench_{w}.log").read().strip().splitlines()[-1])
         r=d.get("roofline",{})
-        print(w, round(d["value"],1), d["unit"], "frac", round(r.get("frac",0),3), r.get("unit"), "e2e", (d.get("e2e") or {}).get("value"), "cpu", (d.get("cpu_baseline") or {}).get("value"))
+        print(w, round(d["value"],2), d["unit"], "frac", round(r.get("frac",0),3), r.get("unit"), "e2e", (d.get("e2e") or {}).get("value"), "cpu", (d.get("cpu_baseline") or {}).get("value"), "clk", (d.get("clocks") or {}).get("sm_mhz"))
     except Exception as e:
         print(w, "ERR", e)
 PY
