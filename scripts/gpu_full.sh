@@ -6,14 +6,16 @@ timeout 600 python bench.py > gpurun_out/bench_default.log 2>&1; echo "default r
 for w in cfg1 cfg2 cfg4 cfg5 mincov mincov_k4096 alg2; do
   timeout 900 python bench.py --workload $w --steps 5 --warmup 3 --cpu-seconds 8 > gpurun_out/bench_$w.log 2>&1; echo "$w rc=$?"
 done
+timeout 600 python bench.py --mode sharded --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_sharded.log 2>&1; echo "sharded rc=$?"
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_reference.log 2>&1; echo "ref rc=$?"
 python - <<'PY'
 import json
-for w in ["default","cfg1","cfg2","cfg4","cfg5","mincov","mincov_k4096","alg2","reference"]:
+for w in ["default","cfg1","cfg2","cfg4","cfg5","mincov","mincov_k4096","alg2","sharded","reference"]:
     try:
         d=json.loads(open(f"gpurun_out/bench_{w}.log").read().strip().splitlines()[-1])
         r=d.get("roofline",{})
         print(w, round(d["value"],2), d["unit"], "frac", round(r.get("frac",0),3), r.get("unit"), "e2e", (d.get("e2e") or {}).get("value"), "cpu", (d.get("cpu_baseline") or {}).get("value"), "clk", (d.get("clocks") or {}).get("sm_mhz"))
+        open(f"gpurun_out/r01_bench_{w}.json","w").write(json.dumps(d)+"\n")
     except Exception as e:
         print(w, "ERR", e)
 PY
