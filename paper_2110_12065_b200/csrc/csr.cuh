@@ -186,6 +186,44 @@ __global__ void __launch_bounds__(kCsrThreads) k_rank_init(int64_t n, const floa
 // order, and a row that spans CTAs gets the CTA carry-outs added by k_rank_fixup in CTA order, so
 // the summation order is fixed for a given graph.
 
+// L2 policy knobs for the gather (K3b): the col_idx / row_ptr streams are read once per
+// iteration (evict-first, no L1 allocation) so that they do not push the 16 MB gathered vector v out
+// of L2 / L1; the gathers themselves ask L2 to keep v (evict-last).
+#ifndef MAPI_CSR_HINT
+#define MAPI_CSR_HINT 1
+#endif
+#ifndef MAPI_CSR_SHARE
+#define MAPI_CSR_SHARE 1
+#endif
+__device__ __forceinline__ uint64_t l2_policy_stream() {
+    uint64_t p;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_keep() {
+    uint64_t p;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ int32_t ld_stream_i32(const int32_t* p, uint64_t pol) {
+#if MAPI_CSR_HINT
+    int32_t r;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
+    return r;
+#else
+    return __ldg(p);
+#endif
+}
+__device__ __forceinline__ float ld_keep_f32(const float* p, uint64_t pol) {
+#if MAPI_CSR_HINT
+    float r;
+    asm("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(r) : "l"(p), "l"(pol));
+    return r;
+#else
+    return __ldg(p);
+#endif
+}
+
 // merge-path search on diagonal d: the number of row ends consumed before d
 __device__ __forceinline__ int64_t mp_search(int64_t d, const int32_t* __restrict__ row_end, int64_t n,
                                              int64_t nnz) {
@@ -219,31 +257,40 @@ __global__ void __launch_bounds__(kMpThreads) k_rank_rows_mp(int64_t n, int64_t 
                                                              const int32_t* stop) {
     // shared arrays indexed through pad(): one spare word per 8 so that the lane-strided reads of the
     // consume loop (thread t walks ~8 consecutive items) hit 32 distinct banks instead of 4
-    __shared__ int32_t s_end[kMpTile + 1 + (kMpTile + 1) / 8 + 1];  // row_ptr[i0+1 .. i1+1]
-    __shared__ float s_val[kMpTile + kMpTile / 8];                  // v[col_idx[k0 .. k1)]
-    __shared__ float s_fp[kMpThreads];      // segmented prefix of the threads' carries
-    __shared__ int32_t wl_row[kMpThreads / 32], wf_row[kMpThreads / 32];
-    __shared__ float wl_val[kMpThreads / 32];
     __shared__ double red[33];
     if (*(volatile const int32_t*)stop) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int32_t i0 = part_i[blockIdx.x], i1 = part_i[blockIdx.x + 1];
     const int32_t k0 = part_k[blockIdx.x], k1 = part_k[blockIdx.x + 1];
     const int nrows = i1 - i0, nk = k1 - k0;  // nrows + nk == items of this tile
-    // stage row ends (rows i0 .. i1, the last possibly partial) and gathered values
     auto pad = [](int x) { return x + (x >> 3); };
+#if MAPI_CSR_SHARE
+    // one buffer: nrows + 1 row ends, then nk values (nrows + nk <= kMpTile); half the shared memory
+    // of two full-size arrays, which leaves more of the unified L1 to cache the gathered v
+    __shared__ int32_t s_buf[kMpTile + 2 + (kMpTile + 2) / 8 + 1];
+    int32_t* s_end = s_buf;
+    float* s_val = reinterpret_cast<float*>(s_buf) + pad(nrows + 1) + 1;
+#else
+    __shared__ int32_t s_end[kMpTile + 1 + (kMpTile + 1) / 8 + 1];  // row_ptr[i0+1 .. i1+1]
+    __shared__ float s_val[kMpTile + kMpTile / 8];                  // v[col_idx[k0 .. k1)]
+#endif
+    __shared__ float s_fp[kMpThreads];      // segmented prefix of the threads' carries
+    __shared__ int32_t wl_row[kMpThreads / 32], wf_row[kMpThreads / 32];
+    __shared__ float wl_val[kMpThreads / 32];
+    const uint64_t pol_s = l2_policy_stream(), pol_k = l2_policy_keep();
+    // stage row ends (rows i0 .. i1, the last possibly partial) and gathered values
     for (int r = tid; r <= nrows; r += kMpThreads)
-        s_end[pad(r)] = (i0 + r < n) ? row_ptr[i0 + r + 1] : (int32_t)nnz;
+        s_end[pad(r)] = (i0 + r < n) ? ld_stream_i32(row_ptr + i0 + r + 1, pol_s) : (int32_t)nnz;
     // nk <= kMpTile = kMpIpt * kMpThreads: all kMpIpt column ids first, then all gathers in flight
     int32_t cj[kMpIpt];
 #pragma unroll
     for (int u = 0; u < kMpIpt; ++u) {
         const int j = tid + u * kMpThreads;
-        cj[u] = j < nk ? __ldg(col_idx + k0 + j) : -1;
+        cj[u] = j < nk ? ld_stream_i32(col_idx + k0 + j, pol_s) : -1;
     }
     float xv[kMpIpt];
 #pragma unroll
-    for (int u = 0; u < kMpIpt; ++u) xv[u] = cj[u] >= 0 ? __ldg(v + cj[u]) : 0.0f;
+    for (int u = 0; u < kMpIpt; ++u) xv[u] = cj[u] >= 0 ? ld_keep_f32(v + cj[u], pol_k) : 0.0f;
     double gpart = 0.0;
 #pragma unroll
     for (int u = 0; u < kMpIpt; ++u) {
