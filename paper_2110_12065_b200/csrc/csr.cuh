@@ -76,11 +76,12 @@ inline mapi_status csr_prepare_run(int64_t n, int64_t nnz, const int32_t* /*row_
 //
 // workspace: [hdr 256: status[2] @0, stop @8, s f64 @16][w n f64][e n f32][v n f32]
 //            [slotS 2*G f64][slotY G f64][slotD G f64]
-//            [merge-path partition: (i,k) x (T+1) i32][carry_row T i32][carry_val T f32][gsum T f64]
+//            [merge-path partition: (i,k) x (T+1) i32][carry_row T i32][carry_val T f32][gsum T x 8 f64]
 // T = number of merge-path tiles = ceil((n + nnz) / kMpTile).
 constexpr int kMpThreads = 256;
 constexpr int kMpIpt = 8;                           // merge items (rows + nonzeros) per thread
 constexpr int kMpTile = kMpThreads * kMpIpt;        // 2048 items per CTA
+constexpr int kMpWarps = kMpThreads / 32;           // per-warp fp64 partials of sum e
 
 struct CsrWs {
     int32_t* status;
@@ -100,7 +101,7 @@ inline int64_t mp_tiles(int64_t n, int64_t nnz) { return (n + nnz + kMpTile - 1)
 inline size_t csr_rank_ws_bytes(int64_t n, int64_t nnz) {
     const int64_t T = mp_tiles(n, nnz);
     return 256 + cal256(8 * (size_t)n) + 2 * cal256(4 * (size_t)n) + 4 * cal256(8 * (size_t)kCsrMaxGrid) +
-           2 * cal256(4 * (size_t)(T + 1)) + 2 * cal256(4 * (size_t)T) + cal256(8 * (size_t)T);
+           2 * cal256(4 * (size_t)(T + 1)) + 2 * cal256(4 * (size_t)T) + cal256(8 * (size_t)T * kMpWarps);
 }
 
 inline CsrWs carve_csr(void* ws, int64_t n, int64_t nnz) {
@@ -257,22 +258,26 @@ __global__ void __launch_bounds__(kMpThreads) k_rank_rows_mp(int64_t n, int64_t 
                                                              const int32_t* stop) {
     // shared arrays indexed through pad(): one spare word per 8 so that the lane-strided reads of the
     // consume loop (thread t walks ~8 consecutive items) hit 32 distinct banks instead of 4
-    __shared__ double red[33];
-    if (*(volatile const int32_t*)stop) return;
+    // the stop flag (written by the previous launch) is read together with the partition, not
+    // ahead of it: one global round trip before the streams start instead of two
+    const int32_t halt = *stop;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int32_t i0 = part_i[blockIdx.x], i1 = part_i[blockIdx.x + 1];
     const int32_t k0 = part_k[blockIdx.x], k1 = part_k[blockIdx.x + 1];
+    if (halt) return;
     const int nrows = i1 - i0, nk = k1 - k0;  // nrows + nk == items of this tile
-    auto pad = [](int x) { return x + (x >> 3); };
+    // one spare word per 32: the staging writes (32 consecutive items per warp) are conflict-free and
+    // the consume loop's ~8-apart lane reads land on distinct banks
+    auto pad = [](int x) { return x + (x >> 5); };
 #if MAPI_CSR_SHARE
     // one buffer: nrows + 1 row ends, then nk values (nrows + nk <= kMpTile); half the shared memory
     // of two full-size arrays, which leaves more of the unified L1 to cache the gathered v
-    __shared__ int32_t s_buf[kMpTile + 2 + (kMpTile + 2) / 8 + 1];
+    __shared__ int32_t s_buf[kMpTile + 2 + (kMpTile + 2) / 32 + 1];
     int32_t* s_end = s_buf;
     float* s_val = reinterpret_cast<float*>(s_buf) + pad(nrows + 1) + 1;
 #else
-    __shared__ int32_t s_end[kMpTile + 1 + (kMpTile + 1) / 8 + 1];  // row_ptr[i0+1 .. i1+1]
-    __shared__ float s_val[kMpTile + kMpTile / 8];                  // v[col_idx[k0 .. k1)]
+    __shared__ int32_t s_end[kMpTile + 1 + (kMpTile + 1) / 32 + 1];  // row_ptr[i0+1 .. i1+1]
+    __shared__ float s_val[kMpTile + kMpTile / 32];                  // v[col_idx[k0 .. k1)]
 #endif
     __shared__ float s_fp[kMpThreads];      // segmented prefix of the threads' carries
     __shared__ int32_t wl_row[kMpThreads / 32], wf_row[kMpThreads / 32];
@@ -312,8 +317,9 @@ __global__ void __launch_bounds__(kMpThreads) k_rank_rows_mp(int64_t n, int64_t 
     float acc = 0.0f, own_first = 0.0f;
     int first_row = -1;  // first row this thread emits (local index); earlier threads may feed it
     const int dend = min(dt + kMpIpt, items);
+    int32_t cur_end = ri < nrows ? s_end[pad(ri)] - k0 : 0x7fffffff;  // end of row ri, tile-relative
     for (int d = dt; d < dend; ++d) {
-        if (ri < nrows && k0 + kj >= s_end[pad(ri)]) {  // the end of row ri
+        if (kj >= cur_end) {  // the end of row ri (ri < nrows)
             if (first_row < 0) {
                 first_row = ri;
                 own_first = acc;
@@ -322,6 +328,7 @@ __global__ void __launch_bounds__(kMpThreads) k_rank_rows_mp(int64_t n, int64_t 
             }
             acc = 0.0f;
             ++ri;
+            cur_end = ri < nrows ? s_end[pad(ri)] - k0 : 0x7fffffff;
         } else {
             acc += s_val[pad(kj)];
             ++kj;
@@ -362,8 +369,9 @@ __global__ void __launch_bounds__(kMpThreads) k_rank_rows_mp(int64_t n, int64_t 
         carry_row[blockIdx.x] = (ri < nrows || (ri == nrows && i1 < n)) ? i0 + ri : -1;
         carry_val[blockIdx.x] = pv;
     }
-    const double g = block_sum(gpart, red);
-    if (tid == 0) gsum[blockIdx.x] = g;
+    // fp64 sum of this tile's gathered values, per warp (k_rank_fixup adds the warps in order)
+    gpart = warp_sum(gpart);
+    if (lane == 0) gsum[(int64_t)blockIdx.x * kMpWarps + warp] = gpart;
 }
 
 // CTA carry-outs into the rows they belong to (tile order), and the fp64 partials of sum_i e_i.
@@ -376,7 +384,8 @@ __global__ void __launch_bounds__(256) k_rank_fixup(int64_t tiles, const int32_t
     const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     double g = 0.0;
     if (c < tiles) {
-        g = gsum[c];
+#pragma unroll
+        for (int q = 0; q < kMpWarps; ++q) g += gsum[c * kMpWarps + q];
         const int32_t r = carry_row[c];
         if (r >= 0 && (c == 0 || carry_row[c - 1] != r)) {
             float sum = 0.0f;
