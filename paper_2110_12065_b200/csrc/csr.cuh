@@ -78,9 +78,15 @@ inline mapi_status csr_prepare_run(int64_t n, int64_t nnz, const int32_t* /*row_
 //            [slotS 2*G f64][slotY G f64][slotD G f64]
 //            [merge-path partition: (i,k) x (T+1) i32][carry_row T i32][carry_val T f32][gsum T x 8 f64]
 // T = number of merge-path tiles = ceil((n + nnz) / kMpTile).
-constexpr int kMpThreads = 256;
-constexpr int kMpIpt = 8;                           // merge items (rows + nonzeros) per thread
-constexpr int kMpTile = kMpThreads * kMpIpt;        // 2048 items per CTA
+#ifndef MAPI_MP_THREADS
+#define MAPI_MP_THREADS 128
+#endif
+constexpr int kMpThreads = MAPI_MP_THREADS;
+#ifndef MAPI_MP_IPT
+#define MAPI_MP_IPT 12
+#endif
+constexpr int kMpIpt = MAPI_MP_IPT;                          // merge items (rows + nonzeros) per thread
+constexpr int kMpTile = kMpThreads * kMpIpt;        // 1536 items per CTA (sweep: r01_summary.md)
 constexpr int kMpWarps = kMpThreads / 32;           // per-warp fp64 partials of sum e
 
 struct CsrWs {

@@ -31,6 +31,50 @@ __global__ void stream_only(const int* __restrict__ col, long long nnz, float* o
     if (acc == 12345) out[0] = (float)acc;
 }
 
+// hot-prefix replication: v[0..H) is stored R times; SM s gathers from copy s % R (spreads the
+// hottest lines of a power-law graph over R different L2 slices)
+template <int U>
+__global__ void gather_sum_rep(const int* __restrict__ col, long long nnz, const float* __restrict__ v,
+                               const float* __restrict__ rep, int H, int R, float* out) {
+    unsigned smid;
+    asm("mov.u32 %0, %%smid;" : "=r"(smid));
+    const float* my = rep + (size_t)(smid % R) * H;
+    float acc = 0.f;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += stride * U) {
+        int c[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) c[u] = (k + u * stride < nnz) ? __ldg(col + k + u * stride) : -1;
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc += c[u] >= 0 ? __ldg((c[u] < H ? my : v) + c[u]) : 0.f;
+    }
+    if (acc == 1234.5f) out[0] = acc;
+}
+template <int U>
+__global__ void stream_v4(const int4* __restrict__ col, long long n4, float* out) {
+    int acc = 0;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n4; k += stride * U) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) if (k + u * stride < n4) { int4 q = __ldg(col + k + u * stride); acc += q.x ^ q.y ^ q.z ^ q.w; }
+    }
+    if (acc == 12345) out[0] = (float)acc;
+}
+
+// col_idx read as int4 (4 consecutive columns per thread), 2 int4 = 8 gathers in flight per trip
+__global__ void gather_sum_v4(const int4* __restrict__ col, long long n4, const float* __restrict__ v, float* out) {
+    float acc = 0.f;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n4; k += 2 * stride) {
+        int4 a = __ldg(col + k);
+        int4 b = (k + stride < n4) ? __ldg(col + k + stride) : make_int4(-1, -1, -1, -1);
+        const int c[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc += c[u] >= 0 ? __ldg(v + c[u]) : 0.f;
+    }
+    if (acc == 1234.5f) out[0] = acc;
+}
+
 template <typename F>
 float timeit(F f) {
     cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
@@ -64,5 +108,25 @@ int main(int argc, char** argv) {
     }
     float t2 = timeit([&] { stream_only<8><<<sms * 8, 256>>>(col, nnz, out); });
     printf("col_idx stream only:          %8.1f us  %6.0f GB/s\n", t2 * 1e3, 4.0 * nnz / (t2 / 1e3) / 1e9);
+    float t3 = timeit([&] { stream_v4<4><<<sms * 8, 256>>>((const int4*)col, nnz / 4, out); });
+    printf("col_idx stream int4:          %8.1f us  %6.0f GB/s\n", t3 * 1e3, 4.0 * nnz / (t3 / 1e3) / 1e9);
+    // edge share of the hottest prefixes
+    for (int H : {1024, 8192, 65536}) {
+        long long c = 0;
+        for (long long k = 0; k < nnz; ++k) c += h[k] < H;
+        printf("edges with col < %6d: %5.1f%%\n", H, 100.0 * c / nnz);
+    }
+    for (int g : {8, 16}) {
+        float t5 = timeit([&] { gather_sum_v4<<<sms * g, 256>>>((const int4*)col, nnz / 4, v, out); });
+        printf("gather_sum_v4 grid %dx256:    %8.1f us  %6.2f Ggather/s\n", sms * g, t5 * 1e3, nnz / (t5 / 1e3) / 1e9);
+    }
+    float* rep;
+    CK(cudaMalloc(&rep, 4ll * 65536 * 32));
+    CK(cudaMemset(rep, 0, 4ll * 65536 * 32));
+    for (int H : {1024, 8192, 65536})
+        for (int R : {4, 16, 32}) {
+            float t4 = timeit([&] { gather_sum_rep<8><<<sms * 16, 256>>>(col, nnz, v, rep, H, R, out); });
+            printf("gather_sum_rep H %6d R %2d:   %8.1f us  %6.2f Ggather/s\n", H, R, t4 * 1e3, nnz / (t4 / 1e3) / 1e9);
+        }
     return 0;
 }
