@@ -72,9 +72,13 @@ inline mapi_status csr_prepare_run(int64_t n, int64_t nnz, const int32_t* /*row_
 // (w, S, y_i = S + e_i, s = ||y||_1, w = y / s, delta) is fp64.  Reason: at n = 2^22 the iterate
 // entries are ~2.4e-7 and y_i = S + e_i is dominated by the common background S ~ 0.6, so an fp32
 // state has a delta noise floor of ~1e-7 (the BASELINE tol) and would decide the stopping iteration
-// by rounding noise; the paper computes in double (MATLAB).  Cost: +~70 MB/iteration of node traffic.
+// by rounding noise; the paper computes in double (MATLAB).  The fp64 iterate is never stored: w_t is
+// a pure function of (S_{t-1}, s_{t-1}, e_{t-1}), so the next launch recomputes it bit-exactly from
+// the previous gather output (e is double-buffered) and two fp64 scalars — 20 B/node of traffic
+// per normalise instead of 32 B/node with an fp64 w array.
 //
-// workspace: [hdr 256: status[2] @0, stop @8, s f64 @16][w n f64][e n f32][v n f32]
+// workspace: [hdr 256: status[2] @0, stop @8, counter u32 @12, s f64 @16, hist (S, s) x 2 f64 @32]
+//            [e0 n f32][e1 n f32][v n f32]
 //            [slotS 2*G f64][slotY G f64][slotD G f64]
 //            [merge-path partition: (i,k) x (T+1) i32][carry_row T i32][carry_val T f32][gsum T x 8 f64]
 // T = number of merge-path tiles = ceil((n + nnz) / kMpTile).
@@ -92,9 +96,10 @@ constexpr int kMpWarps = kMpThreads / 32;           // per-warp fp64 partials of
 struct CsrWs {
     int32_t* status;
     int32_t* stop;
+    uint32_t* counter;
     double* s;
-    double* w;
-    float *e, *v;
+    double* hist;  // [2][2]: (S_t, s_t) of the last normalised iteration t, slot (t + 1) & 1
+    float *e[2], *v;
     double *slotS, *slotY, *slotD;
     int32_t *part_i, *part_k, *carry_row;
     float* carry_val;
@@ -106,7 +111,7 @@ inline int64_t mp_tiles(int64_t n, int64_t nnz) { return (n + nnz + kMpTile - 1)
 
 inline size_t csr_rank_ws_bytes(int64_t n, int64_t nnz) {
     const int64_t T = mp_tiles(n, nnz);
-    return 256 + cal256(8 * (size_t)n) + 2 * cal256(4 * (size_t)n) + 4 * cal256(8 * (size_t)kCsrMaxGrid) +
+    return 256 + 3 * cal256(4 * (size_t)n) + 4 * cal256(8 * (size_t)kCsrMaxGrid) +
            2 * cal256(4 * (size_t)(T + 1)) + 2 * cal256(4 * (size_t)T) + cal256(8 * (size_t)T * kMpWarps);
 }
 
@@ -116,12 +121,14 @@ inline CsrWs carve_csr(void* ws, int64_t n, int64_t nnz) {
     c.tiles = mp_tiles(n, nnz);
     c.status = reinterpret_cast<int32_t*>(p);
     c.stop = reinterpret_cast<int32_t*>(p + 8);
+    c.counter = reinterpret_cast<uint32_t*>(p + 12);
     c.s = reinterpret_cast<double*>(p + 16);
+    c.hist = reinterpret_cast<double*>(p + 32);
     p += 256;
-    c.w = reinterpret_cast<double*>(p);
-    p += cal256(8 * (size_t)n);
-    c.e = reinterpret_cast<float*>(p);
-    p += cal256(4 * (size_t)n);
+    for (int b = 0; b < 2; ++b) {
+        c.e[b] = reinterpret_cast<float*>(p);
+        p += cal256(4 * (size_t)n);
+    }
     c.v = reinterpret_cast<float*>(p);
     p += cal256(4 * (size_t)n);
     c.slotS = reinterpret_cast<double*>(p);
@@ -161,18 +168,31 @@ __device__ __forceinline__ double slots_sum(const double* slots, int count, doub
     return r;
 }
 
-// K3a at t = 0: w = b0 (checked >= 0), v_j, S partials (slot parity 0).
+// same, reading the slots through L2 (written by other CTAs of the running launch)
+__device__ __forceinline__ double slots_sum_cg(const double* slots, int count, double* red) {
+    if (threadIdx.x < 32) {
+        double part = 0.0;
+        for (int c = threadIdx.x; c < count; c += 32) part += __ldcg(slots + c);
+        part = warp_sum(part);
+        if (threadIdx.x == 0) red[32] = part;
+    }
+    __syncthreads();
+    const double r = red[32];
+    __syncthreads();
+    return r;
+}
+
+// K3a at t = 0: w_0 = b0 (checked >= 0), v_j, S partials (slot parity 0).
 __global__ void __launch_bounds__(kCsrThreads) k_rank_init(int64_t n, const float* __restrict__ b0,
                                                            const float* __restrict__ bg, const float* __restrict__ cap,
-                                                           double* __restrict__ w, float* __restrict__ v,
-                                                           double* __restrict__ slotS, int32_t* status, int32_t* stop) {
+                                                           float* __restrict__ v, double* __restrict__ slotS,
+                                                           int32_t* status, int32_t* stop) {
     __shared__ double red[33];
     double sp = 0.0;
     bool neg = false;
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
         const double wj = (double)b0[j];
         neg |= wj < 0.0;
-        w[j] = wj;
         const float b = bg[j];
         v[j] = csr_v(wj, b, cap[j]);
         sp += fmin((double)b, wj);
@@ -403,62 +423,69 @@ __global__ void __launch_bounds__(256) k_rank_fixup(int64_t tiles, const int32_t
     if (threadIdx.x == 0) slotY[blockIdx.x] = G;
 }
 
-// K3c: s = ||y||_1 = n S + sum_i e_i (fp64), w_new = (S + e_j) / s (fp64), delta partials; next v_j
-// and S partials.  (One fp64 product n*S per iteration: the l1 norm of the common background.)
+// K3c+d: s = ||y||_1 = n S + sum_i e_i (fp64), w_new = (S + e_j) / s (fp64), w_old recomputed from the
+// previous gather (bit-identical to last launch's w_new), delta partials, next v_j and S partials; the
+// last CTA to finish (counter) sums the delta partials in slot order and writes delta_t, the trace,
+// iters_done and the stop flag.  (One fp64 product n*S per iteration: the l1 norm of the background.)
 template <bool V4>
-__global__ void __launch_bounds__(kCsrThreads) k_rank_normalize(int64_t n, const float* __restrict__ e,
-                                                                const double* __restrict__ slotS_cur,
-                                                                double* __restrict__ slotS_next, int nS,
-                                                                const double* __restrict__ slotY, int nY,
-                                                                const float* __restrict__ bg,
-                                                                const float* __restrict__ cap, double* __restrict__ w,
-                                                                float* __restrict__ v, double* __restrict__ slotD,
-                                                                double* s_out, const int32_t* stop) {
+__global__ void __launch_bounds__(kCsrThreads) k_rank_normalize(
+    int64_t n, const float* __restrict__ e, const float* __restrict__ e_prev, const float* __restrict__ b0,
+    double* __restrict__ hist, const double* __restrict__ slotS_cur, double* __restrict__ slotS_next, int nS,
+    const double* __restrict__ slotY, int nY, const float* __restrict__ bg, const float* __restrict__ cap,
+    float* __restrict__ v, double* __restrict__ slotD, double* s_out, uint32_t* counter, int32_t t, float tol,
+    float* deltas, int32_t* status, int32_t* stop) {
     __shared__ double red[33];
+    __shared__ int s_last;
     if (*(volatile const int32_t*)stop) return;
     const double S = slots_sum(slotS_cur, nS, red);
     const double s = (double)n * S + slots_sum(slotY, nY, red);
-    if (blockIdx.x == 0 && threadIdx.x == 0) *s_out = s;
-    if (!(s > 0.0) || isinf(s)) return;  // uniform: flagged by k_rank_step_end
-    double dp = 0.0, sp = 0.0;
+    if (!(s > 0.0) || isinf(s)) {  // uniform across CTAs: CTA 0 reports, nothing is updated
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            *s_out = s;
+            status[0] = (s == 0.0) ? 4 : 6;
+            *stop = 1;
+        }
+        return;
+    }
+    // w_old = w_t: b0 at t = 0, else (S_{t-1} + e_{t-1}) / s_{t-1} exactly as the last launch formed it
+    const bool first = e_prev == nullptr;
+    const double Sp = first ? 0.0 : hist[(t & 1) * 2], sp_ = first ? 1.0 : hist[(t & 1) * 2 + 1];
+    auto w_old = [&](int64_t j, float ep) -> double { return first ? (double)b0[j] : (Sp + (double)ep) / sp_; };
+    double dp = 0.0, sn = 0.0;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     int64_t j0 = 0;
     if constexpr (V4) {
         // groups of 4 consecutive nodes, two groups per trip: 16 B vector loads, 8 nodes in flight
         const int64_t groups = n / 4;
         for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < groups; g += 2 * stride) {
-            float4 ev[2], bv[2], cv[2];
-            double2 wv[2][2];
+            float4 ev[2], pv[2], bv[2], cv[2];
             const bool two = g + stride < groups;
 #pragma unroll
             for (int q = 0; q < 2; ++q) {
                 if (q == 1 && !two) break;
                 const int64_t gg = g + q * stride;
                 ev[q] = reinterpret_cast<const float4*>(e)[gg];
+                pv[q] = reinterpret_cast<const float4*>(first ? b0 : e_prev)[gg];
                 bv[q] = __ldg(reinterpret_cast<const float4*>(bg) + gg);
                 cv[q] = __ldg(reinterpret_cast<const float4*>(cap) + gg);
-                wv[q][0] = reinterpret_cast<const double2*>(w)[2 * gg];
-                wv[q][1] = reinterpret_cast<const double2*>(w)[2 * gg + 1];
             }
 #pragma unroll
             for (int q = 0; q < 2; ++q) {
                 if (q == 1 && !two) break;
                 const int64_t gg = g + q * stride;
                 const float ee[4] = {ev[q].x, ev[q].y, ev[q].z, ev[q].w};
+                const float pp[4] = {pv[q].x, pv[q].y, pv[q].z, pv[q].w};
                 const float bb[4] = {bv[q].x, bv[q].y, bv[q].z, bv[q].w};
                 const float cc[4] = {cv[q].x, cv[q].y, cv[q].z, cv[q].w};
-                const double wo[4] = {wv[q][0].x, wv[q][0].y, wv[q][1].x, wv[q][1].y};
-                double wn[4];
                 float vn[4];
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
-                    wn[i] = (S + (double)ee[i]) / s;
-                    dp += fabs(wn[i] - wo[i]);
-                    vn[i] = csr_v(wn[i], bb[i], cc[i]);
-                    sp += fmin((double)bb[i], wn[i]);
+                    const double wn = (S + (double)ee[i]) / s;
+                    const double wo = first ? (double)pp[i] : (Sp + (double)pp[i]) / sp_;
+                    dp += fabs(wn - wo);
+                    vn[i] = csr_v(wn, bb[i], cc[i]);
+                    sn += fmin((double)bb[i], wn);
                 }
-                reinterpret_cast<double2*>(w)[2 * gg] = make_double2(wn[0], wn[1]);
-                reinterpret_cast<double2*>(w)[2 * gg + 1] = make_double2(wn[2], wn[3]);
                 reinterpret_cast<float4*>(v)[gg] = make_float4(vn[0], vn[1], vn[2], vn[3]);
             }
         }
@@ -466,52 +493,81 @@ __global__ void __launch_bounds__(kCsrThreads) k_rank_normalize(int64_t n, const
     }
     for (int64_t j = j0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride) {
         const double wn = (S + (double)e[j]) / s;
-        dp += fabs(wn - w[j]);
-        w[j] = wn;
+        dp += fabs(wn - w_old(j, first ? 0.0f : e_prev[j]));
         const float b = bg[j];
         v[j] = csr_v(wn, b, cap[j]);
-        sp += fmin((double)b, wn);
+        sn += fmin((double)b, wn);
     }
     const double D = block_sum(dp, red);
-    const double Sn = block_sum(sp, red);
+    const double Sn = block_sum(sn, red);
     if (threadIdx.x == 0) {
         slotD[blockIdx.x] = D;
         slotS_next[blockIdx.x] = Sn;
+        __threadfence();
+        s_last = atomicAdd(counter, 1u) == gridDim.x - 1;
     }
-}
-
-// K3d: delta_t, trace, status, stop.
-__global__ void k_rank_step_end(const double* __restrict__ s_in, const double* __restrict__ slotD, int nd, int32_t t,
-                                float tol, float* deltas, int32_t* status, int32_t* stop) {
-    __shared__ double red[33];
-    if (*(volatile int32_t*)stop) return;
-    const double s = *s_in;
-    const double d = slots_sum(slotD, nd, red);
+    __syncthreads();
+    if (!s_last) return;
+    // K3d (last CTA): delta_t in slot order, trace, iters_done, (S_t, s_t) for the next launch, stop
+    __threadfence();
+    const double d = slots_sum_cg(slotD, gridDim.x, red);
     if (threadIdx.x == 0) {
-        if (!(s > 0.0) || isinf(s)) {
-            status[0] = (s == 0.0) ? 4 : 6;
-            *stop = 1;
-            return;
-        }
+        *counter = 0u;
+        *s_out = s;
+        hist[((t + 1) & 1) * 2] = S;
+        hist[((t + 1) & 1) * 2 + 1] = s;
         if (deltas) deltas[t] = (float)d;
         status[1] = t + 1;
         if (tol > 0.0f && d < (double)tol) *stop = 1;
     }
 }
 
-// Final outputs from the fp64 state: w_out = fp32(w), optional l2 copy, one CTA.
-__global__ void __launch_bounds__(1024) k_rank_output(int64_t n, const double* __restrict__ w, float* __restrict__ w_out,
-                                                      float* __restrict__ w_l2) {
+// Final outputs: w = (S + e) / s of the last normalised iteration (b0 if none), recomputed in fp64
+// exactly as the loop formed it; w_out = fp32(w) and the per-CTA sums of w^2 (pass 1), then the
+// optional l2 copy (pass 2).
+struct RankLast {
+    const float* e;
+    double S, s;
+    bool none;
+};
+__device__ __forceinline__ RankLast rank_last(const float* e0, const float* e1, const double* hist,
+                                              const int32_t* status) {
+    const int32_t done = status[1];
+    RankLast r;
+    r.none = done == 0;
+    const int32_t last = done - 1;
+    r.e = (last & 1) ? e1 : e0;
+    r.S = r.none ? 0.0 : hist[((last + 1) & 1) * 2];
+    r.s = r.none ? 1.0 : hist[((last + 1) & 1) * 2 + 1];
+    return r;
+}
+__global__ void __launch_bounds__(kCsrThreads) k_rank_output(int64_t n, const float* __restrict__ e0,
+                                                            const float* __restrict__ e1, const double* hist,
+                                                            const int32_t* status, const float* __restrict__ b0,
+                                                            float* __restrict__ w_out, double* __restrict__ slotQ) {
     __shared__ double red[33];
+    const RankLast L = rank_last(e0, e1, hist, status);
     double part = 0.0;
-    for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
-        const double x = w[j];
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+        const double x = L.none ? (double)b0[j] : (L.S + (double)L.e[j]) / L.s;
         w_out[j] = (float)x;
         part = fma(x, x, part);
     }
-    if (!w_l2) return;
-    const double l2 = sqrt(block_sum(part, red));
-    for (int64_t j = threadIdx.x; j < n; j += blockDim.x) w_l2[j] = l2 > 0.0 ? (float)(w[j] / l2) : 0.0f;
+    const double q = block_sum(part, red);
+    if (threadIdx.x == 0) slotQ[blockIdx.x] = q;
+}
+__global__ void __launch_bounds__(kCsrThreads) k_rank_output_l2(int64_t n, const float* __restrict__ e0,
+                                                               const float* __restrict__ e1, const double* hist,
+                                                               const int32_t* status, const float* __restrict__ b0,
+                                                               const double* __restrict__ slotQ, int nq,
+                                                               float* __restrict__ w_l2) {
+    __shared__ double red[33];
+    const RankLast L = rank_last(e0, e1, hist, status);
+    const double l2 = sqrt(slots_sum(slotQ, nq, red));
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+        const double x = L.none ? (double)b0[j] : (L.S + (double)L.e[j]) / L.s;
+        w_l2[j] = l2 > 0.0 ? (float)(x / l2) : 0.0f;
+    }
 }
 
 inline mapi_status csr_rank_run(int64_t n, int64_t nnz, const int32_t* row_ptr, const int32_t* col_idx,
@@ -523,8 +579,9 @@ inline mapi_status csr_rank_run(int64_t n, int64_t nnz, const int32_t* row_ptr, 
     if (err != cudaSuccess) return csr_cuda_fail(err, "memset");
     const int gcol = (int)std::min<int64_t>({(n + kCsrThreads - 1) / kCsrThreads, (int64_t)4 * sms, (int64_t)kCsrMaxGrid});
     const int64_t T = W.tiles;
-    // 16 B vector path for the node arrays when the caller's bg / cap are 16 B aligned
-    const bool v4 = (reinterpret_cast<uintptr_t>(bg) % 16 == 0) && (reinterpret_cast<uintptr_t>(cap) % 16 == 0);
+    // 16 B vector path for the node arrays when the caller's b0 / bg / cap are 16 B aligned
+    const bool v4 = (reinterpret_cast<uintptr_t>(bg) % 16 == 0) && (reinterpret_cast<uintptr_t>(cap) % 16 == 0) &&
+                    (reinterpret_cast<uintptr_t>(b0) % 16 == 0);
     const int gfix = (int)((T + 255) / 256);
     if (gfix > kCsrMaxGrid) {
         snprintf(g_csr_err, sizeof(g_csr_err), "graph too large: %lld merge tiles", (long long)T);
@@ -533,27 +590,35 @@ inline mapi_status csr_rank_run(int64_t n, int64_t nnz, const int32_t* row_ptr, 
     k_mp_partition<<<(unsigned)((T + 1 + 255) / 256), 256, 0, s>>>(n, nnz, row_ptr, T, W.part_i, W.part_k);
     launches.fetch_add(1, std::memory_order_relaxed);
     if (ev_a) cudaEventRecord(*ev_a, s);
-    k_rank_init<<<gcol, kCsrThreads, 0, s>>>(n, b0, bg, cap, W.w, W.v, W.slotS, W.status, W.stop);
+    k_rank_init<<<gcol, kCsrThreads, 0, s>>>(n, b0, bg, cap, W.v, W.slotS, W.status, W.stop);
     launches.fetch_add(1, std::memory_order_relaxed);
     for (int32_t t = 0; t < max_iters; ++t) {
         double* S_cur = W.slotS + (t & 1) * kCsrMaxGrid;
         double* S_next = W.slotS + ((t + 1) & 1) * kCsrMaxGrid;
-        k_rank_rows_mp<<<(unsigned)T, kMpThreads, 0, s>>>(n, nnz, row_ptr, col_idx, W.v, W.part_i, W.part_k, W.e,
+        float* e_cur = W.e[t & 1];
+        const float* e_prev = t == 0 ? nullptr : W.e[(t + 1) & 1];
+        k_rank_rows_mp<<<(unsigned)T, kMpThreads, 0, s>>>(n, nnz, row_ptr, col_idx, W.v, W.part_i, W.part_k, e_cur,
                                                           W.carry_row, W.carry_val, W.gsum, W.stop);
-        k_rank_fixup<<<gfix, 256, 0, s>>>(T, W.carry_row, W.carry_val, W.gsum, W.e, W.slotY, W.stop);
+        k_rank_fixup<<<gfix, 256, 0, s>>>(T, W.carry_row, W.carry_val, W.gsum, e_cur, W.slotY, W.stop);
         if (v4)
-            k_rank_normalize<true><<<gcol, kCsrThreads, 0, s>>>(n, W.e, S_cur, S_next, gcol, W.slotY, gfix, bg, cap, W.w,
-                                                                W.v, W.slotD, W.s, W.stop);
+            k_rank_normalize<true><<<gcol, kCsrThreads, 0, s>>>(n, e_cur, e_prev, b0, W.hist, S_cur, S_next, gcol,
+                                                                W.slotY, gfix, bg, cap, W.v, W.slotD, W.s, W.counter,
+                                                                t, tol, deltas, W.status, W.stop);
         else
-            k_rank_normalize<false><<<gcol, kCsrThreads, 0, s>>>(n, W.e, S_cur, S_next, gcol, W.slotY, gfix, bg, cap,
-                                                                 W.w, W.v, W.slotD, W.s, W.stop);
-        k_rank_step_end<<<1, 32, 0, s>>>(W.s, W.slotD, gcol, t, tol, deltas, W.status, W.stop);
-        launches.fetch_add(4, std::memory_order_relaxed);
+            k_rank_normalize<false><<<gcol, kCsrThreads, 0, s>>>(n, e_cur, e_prev, b0, W.hist, S_cur, S_next, gcol,
+                                                                 W.slotY, gfix, bg, cap, W.v, W.slotD, W.s, W.counter,
+                                                                 t, tol, deltas, W.status, W.stop);
+        launches.fetch_add(3, std::memory_order_relaxed);
         if ((err = cudaGetLastError()) != cudaSuccess) return csr_cuda_fail(err, "rank launch");
     }
     if (ev_b) cudaEventRecord(*ev_b, s);
-    k_rank_output<<<1, 1024, 0, s>>>(n, W.w, w_out, w_l2_out);
+    k_rank_output<<<gcol, kCsrThreads, 0, s>>>(n, W.e[0], W.e[1], W.hist, W.status, b0, w_out, W.slotD);
     launches.fetch_add(1, std::memory_order_relaxed);
+    if (w_l2_out) {
+        k_rank_output_l2<<<gcol, kCsrThreads, 0, s>>>(n, W.e[0], W.e[1], W.hist, W.status, b0, W.slotD, gcol,
+                                                      w_l2_out);
+        launches.fetch_add(1, std::memory_order_relaxed);
+    }
     if ((err = cudaGetLastError()) != cudaSuccess) return csr_cuda_fail(err, "rank output");
     return MAPI_OK;
 }
