@@ -317,12 +317,13 @@ def build_rank(args, m, dev, stream):
                                           ctypes.byref(done), ws.data_ptr(), need, stream.cuda_stream))
         return T
 
-    # algorithmic HBM bytes per iteration (DESIGN.md §6 K3): row_ptr + col_idx once, node arrays
-    per_iter = 4.0 * (n + 1) + 4.0 * nnz + 36.0 * n
+    # algorithmic HBM bytes per iteration (DESIGN.md §6 K3): row_ptr + col_idx once; node arrays: e written
+    # by the gather, then e, e_prev, bg, cap read and v written by the normalise (24 B/node)
+    per_iter = 4.0 * (n + 1) + 4.0 * nnz + 24.0 * n
     return Work(step=step, unit="iterations/s", per_launch=per_iter * T, bytes_per_unit=per_iter, bound="hbm",
                 kernel="k_rank_rows + k_rank_normalize + k_rank_step_end loop (events around the loop)",
                 config={"workload": f"cfg5: {WORKLOADS['cfg5']}", "n": n, "nnz": nnz, "iters_per_step": T,
-                        "tol": 0.0, "l2_flush": "inputs larger than L2 (0.43 GB per iteration)"},
+                        "tol": 0.0, "l2_flush": "inputs larger than L2 (0.38 GB per iteration)"},
                 oracle=("rank", cfg))
 
 
