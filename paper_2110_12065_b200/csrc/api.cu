@@ -12,6 +12,7 @@
 
 #include "../../include/mapi.h"
 #include "batched.cuh"
+#include "bulk.cuh"
 #include "csr.cuh"
 #include "deflate.cuh"
 #include "dense.cuh"
@@ -218,9 +219,31 @@ bool use_cluster(const Device& d, int64_t n) {
     return strcmp(e, "cluster") == 0 || n <= 512;
 }
 
+// K2t (TMA bulk-copy ring, bulk.cuh) for mid-size n where A stays L2-resident and the per-row kernel
+// is latency-bound; needs 16 B-aligned rows.  MAPI_DENSE_PATH=bulk forces it (any n it can hold).
+int bulk_slots(const Device& d, int64_t n) {
+    const int64_t grid = std::min<int64_t>(d.sms, n);
+    const size_t fixed = bulk_fixed_smem(n, (n + grid - 1) / grid);
+    if (fixed >= (size_t)d.smem_optin) return 0;
+    const int64_t sl = std::min<int64_t>(kBulkMaxSlots, ((size_t)d.smem_optin - fixed) / (sizeof(float) * kBulkChunk));
+    return (int)(sl / kBulkNC * kBulkNC);  // whole slots per warp
+}
+
+bool use_bulk(const Device& d, const float* A, int64_t n, int64_t lda) {
+    const char* e = dense_path_env();
+    if (strcmp(e, "rows") == 0 || strcmp(e, "multi") == 0 || strcmp(e, "coop") == 0) return false;
+    if (n % 4 != 0 || lda % 4 != 0 || (reinterpret_cast<uintptr_t>(A) & 15) != 0) return false;
+    if (bulk_slots(d, n) < 2 * kBulkNC) return false;
+    if (strcmp(e, "bulk") == 0) return true;
+    // default: L2-resident A at n >= 3072 (measured vs K2 per-row, profiles/r01_probe_bulk.log:
+    // n = 4096 13.4 vs 14.7 us/iteration; at n <= 2048 and for HBM-resident A the others win or tie)
+    return n >= 3072 && n < 8192 && (double)n * (double)lda * 4.0 <= 0.6 * (double)d.l2_bytes;
+}
+
 bool use_coop(const Device& d, const float* A, int64_t n, int64_t lda) {
     const char* e = dense_path_env();
     if (strcmp(e, "rows") == 0 || strcmp(e, "multi") == 0) return false;
+    if (strcmp(e, "bulk") == 0 && use_bulk(d, A, n, lda)) return false;
     if (vec_width(A, lda) != 8) return false;
     if (strcmp(e, "coop") != 0 && n / 256 < 32) return false;  // n < 8192: the per-row kernel is faster
     const int64_t grid = std::min<int64_t>(d.sms, n);
@@ -297,6 +320,28 @@ mapi_status iterate_launch(const Device& d, int32_t op, const float* A, int64_t 
             });
         });
         return st;
+    }
+    if (use_bulk(d, A, n, lda)) {
+        const int slots = bulk_slots(d, n);
+        const int grid = (int)std::min<int64_t>(d.sms, n);
+        const size_t smem = bulk_fixed_smem(n, (n + grid - 1) / grid) + sizeof(float) * kBulkChunk * (size_t)slots;
+        auto kern = op == 2 ? k_iterate_bulk<2> : (op == 1 ? k_iterate_bulk<1> : k_iterate_bulk<0>);
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return fail(MAPI_ERR_CUDA, "bulk kernel smem (%zu): %s", smem, cudaGetErrorString(e));
+        IterArgs a;
+        a.A = A; a.n = n; a.lda = lda; a.b0 = b0; a.iters = iters; a.tol = tol;
+        a.w_out = w_out; a.norms = norms; a.deltas = deltas; a.y = W.y; a.slots = W.slots;
+        a.bar = W.bar; a.status = W.status;
+        int sl = slots;
+        void* args[] = {&a, &sl};
+        if (timer) timer->start();
+        e = cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kBulkThreads), args, smem, s);
+        if (timer) timer->stop();
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        if (e != cudaSuccess)
+            return fail(MAPI_ERR_CUDA, "bulk cooperative launch (grid %d, smem %zu): %s", grid, smem,
+                        cudaGetErrorString(e));
+        return MAPI_OK;
     }
     if (use_persistent(d, n)) {
         mapi_status st = MAPI_OK;

@@ -248,7 +248,7 @@ def test_cfg3_last_step_and_invariants(mapi_lib, orc, cfg3_device):
     assert torch.equal(r100.w, r100b.w)
 
 
-@pytest.mark.parametrize("path", ["cluster", "rows", "coop", "multi"])
+@pytest.mark.parametrize("path", ["cluster", "rows", "coop", "bulk", "multi"])
 @pytest.mark.parametrize("n", [256, 511, 4096, 8200])
 def test_every_dense_path_matches_oracle(mapi_lib, orc, monkeypatch, path, n):
     """Each dense iteration kernel (K6 cluster, K2 per-row, K2c cooperative rows, multi-launch),
@@ -265,10 +265,58 @@ def test_every_dense_path_matches_oracle(mapi_lib, orc, monkeypatch, path, n):
     _t2(res.w_l2.cpu().numpy(), ref.w, res.norms.cpu().numpy(), ref.norms)
 
 
+@pytest.mark.parametrize("n,pad", [(1024, 0), (1500, 4), (2052, 8), (4096, 0), (5000, 12)])
+@pytest.mark.parametrize("op", ["min1", "min2"])
+def test_bulk_ring_path(mapi_lib, orc, monkeypatch, n, pad, op):
+    """K2t (TMA bulk-copy ring): ragged last chunk (n % 1024 != 0), padded lda, both MAVP operators,
+    vs the oracle (T2), bitwise reproducible, and NaN row padding never read."""
+    m = mapi_lib
+    r = np.random.default_rng(n + pad)
+    Af = np.full((n, n + pad), np.nan, np.float32)
+    A = r.standard_normal((n, n)).astype(np.float32) + np.diag(np.abs(r.standard_normal(n)) * 4).astype(np.float32)
+    Af[:, :n] = A
+    b0 = np.full(n, 1.0 / np.sqrt(n), np.float32)
+    monkeypatch.setenv("MAPI_DENSE_PATH", "bulk")
+    Ad = torch.from_numpy(Af).cuda()[:, :n]
+    opc = m.MIN1 if op == "min1" else m.MIN2
+    res = m.iterate(Ad, torch.from_numpy(b0).cuda(), 25, op=opc)
+    ref = orc.mapi(A, b0, 25, op=op)
+    assert res.iters_done == 25
+    _t2(res.w_l2.cpu().numpy(), ref.w, res.norms.cpu().numpy(), ref.norms)
+    again = m.iterate(Ad, torch.from_numpy(b0).cuda(), 25, op=opc)
+    assert torch.equal(res.w, again.w) and torch.equal(res.deltas, again.deltas)
+
+
+def test_bulk_ring_early_stop_and_degenerate(mapi_lib, orc, monkeypatch):
+    """Early stop by tol (the producer has copies in flight past the last iteration and must drain
+    them) and the degenerate status, on the bulk path; then a normal run on the same stream."""
+    m = mapi_lib
+    monkeypatch.setenv("MAPI_DENSE_PATH", "bulk")
+    n = 2048
+    r = np.random.default_rng(3)
+    A = (r.standard_normal((n, n)) / 8).astype(np.float32) + np.diag(np.linspace(4.0, 1.0, n)).astype(np.float32)
+    b0 = np.full(n, 1.0 / np.sqrt(n), np.float32)
+    Ad, bd = torch.from_numpy(A).cuda(), torch.from_numpy(b0).cuda()
+    full = m.iterate(Ad, bd, 200)
+    d = full.deltas.cpu().numpy()
+    tol = float(d[40]) * 1.0001  # first crossing near iteration 40
+    first = int(np.nonzero(d < tol)[0][0])
+    res = m.iterate(Ad, bd, 200, tol=tol)
+    assert res.iters_done == first + 1
+    assert torch.equal(res.deltas, full.deltas[: first + 1])
+    ref = orc.mapi(A, b0, first + 1)
+    _t2(res.w_l2.cpu().numpy(), ref.w)
+    with pytest.raises(m.MapiError) as ei:
+        m.iterate(torch.zeros(n, n, device="cuda"), bd, 10)
+    assert ei.value.name == "MAPI_ERR_DEGENERATE" and ei.value.iters_done == 0
+    again = m.iterate(Ad, bd, 200)
+    assert torch.equal(again.w, full.w)
+
+
 # ------------------------------------------------------------------------------ RPI comparator (NEXT-3)
 
 
-@pytest.mark.parametrize("path", ["cluster", "rows", "coop", "multi"])
+@pytest.mark.parametrize("path", ["cluster", "rows", "coop", "bulk", "multi"])
 def test_rpi_comparator_matches_oracle(mapi_lib, orc, monkeypatch, path):
     """op = MAPI_OP_DOT: b <- Ab/||Ab||_2 (Eq. 1) through every dense path, vs the oracle's rpi."""
     m = mapi_lib
