@@ -741,7 +741,22 @@ mapi_status mapi_pca_topk(int32_t op, const float* C, int64_t n, int64_t ldc, in
         if (i > 0) {
             const int gx = (int)std::min<int64_t>((n + 255) / 256, 65535);
             const int gy = (int)std::min<int64_t>(n, 65535);
-            k_build_deflated<<<dim3(gx, gy), 256, 0, s>>>(C, n, ldc, P64, R, i, D);
+            const bool v4 = i <= 8 && n % 4 == 0 && ldc % 4 == 0 && (reinterpret_cast<uintptr_t>(C) & 15) == 0;
+            if (v4) {
+                const dim3 g((unsigned)((n / 4 + 255) / 256), (unsigned)((n + kDeflRows - 1) / kDeflRows));
+                switch (i) {
+                    case 1: k_build_deflated_v4<1><<<g, 256, 0, s>>>(C, n, ldc, P64, R, D); break;
+                    case 2: k_build_deflated_v4<2><<<g, 256, 0, s>>>(C, n, ldc, P64, R, D); break;
+                    case 3: k_build_deflated_v4<3><<<g, 256, 0, s>>>(C, n, ldc, P64, R, D); break;
+                    case 4: k_build_deflated_v4<4><<<g, 256, 0, s>>>(C, n, ldc, P64, R, D); break;
+                    case 5: k_build_deflated_v4<5><<<g, 256, 0, s>>>(C, n, ldc, P64, R, D); break;
+                    case 6: k_build_deflated_v4<6><<<g, 256, 0, s>>>(C, n, ldc, P64, R, D); break;
+                    case 7: k_build_deflated_v4<7><<<g, 256, 0, s>>>(C, n, ldc, P64, R, D); break;
+                    default: k_build_deflated_v4<8><<<g, 256, 0, s>>>(C, n, ldc, P64, R, D); break;
+                }
+            } else {
+                k_build_deflated<<<dim3(gx, gy), 256, 0, s>>>(C, n, ldc, P64, R, i, D);
+            }
             MAPI_LAUNCHED();
             Ai = D;
             ld = n;

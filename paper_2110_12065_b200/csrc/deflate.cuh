@@ -65,4 +65,39 @@ __global__ void __launch_bounds__(256) k_build_deflated(const float* __restrict_
     }
 }
 
+// Vectorised form for i <= 8 components (the BASELINE k = 8): thread owns 4 consecutive columns of a
+// 1024-column strip and a run of rows; r_m for its columns stays in registers (i x 4 doubles), C is
+// read and D written as float4, p_m[row] comes from L1 (warp broadcast).  Same per-element fp64
+// sequence as k_build_deflated (v = C; v = fma(-p_m[row], r_m[c], v) for m = 0..i-1; one rounding),
+// so the two are bitwise identical.  Requires n % 4 == 0, ldc % 4 == 0, 16 B-aligned C and D.
+constexpr int kDeflRows = 16;  // rows per CTA
+template <int I>
+__global__ void __launch_bounds__(256) k_build_deflated_v4(const float* __restrict__ C, int64_t n, int64_t ldc,
+                                                           const double* __restrict__ P,
+                                                           const double* __restrict__ R,
+                                                           float* __restrict__ D) {
+    const int64_t c = ((int64_t)blockIdx.x * 256 + threadIdx.x) * 4;
+    if (c >= n) return;
+    double r[I][4];
+#pragma unroll
+    for (int m = 0; m < I; ++m) {
+        const double2 a = __ldg(reinterpret_cast<const double2*>(R + (int64_t)m * n + c));
+        const double2 b = __ldg(reinterpret_cast<const double2*>(R + (int64_t)m * n + c) + 1);
+        r[m][0] = a.x; r[m][1] = a.y; r[m][2] = b.x; r[m][3] = b.y;
+    }
+    const int64_t row0 = (int64_t)blockIdx.y * kDeflRows, row1 = min(n, row0 + kDeflRows);
+#pragma unroll 4
+    for (int64_t row = row0; row < row1; ++row) {
+        const float4 x = __ldg(reinterpret_cast<const float4*>(C + row * ldc + c));
+        double v[4] = {(double)x.x, (double)x.y, (double)x.z, (double)x.w};
+#pragma unroll
+        for (int m = 0; m < I; ++m) {
+            const double pm = -__ldg(P + (int64_t)m * n + row);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) v[j] = fma(pm, r[m][j], v[j]);
+        }
+        reinterpret_cast<float4*>(D + row * n)[c >> 2] = make_float4((float)v[0], (float)v[1], (float)v[2], (float)v[3]);
+    }
+}
+
 }  // namespace mapi
