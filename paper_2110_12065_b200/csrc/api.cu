@@ -214,9 +214,11 @@ int coop_warps(int64_t n) { return (n / 256) >= 64 ? 32 : 16; }
 // K6 (one 8-CTA cluster, A in distributed shared memory) for small n; MAPI_DENSE_PATH=cluster forces
 bool use_cluster(const Device& d, int64_t n) {
     const char* e = dense_path_env();
-    if (strcmp(e, "rows") == 0 || strcmp(e, "multi") == 0 || strcmp(e, "coop") == 0) return false;
+    if (strcmp(e, "rows") == 0 || strcmp(e, "multi") == 0 || strcmp(e, "coop") == 0 || strcmp(e, "bulk") == 0)
+        return false;
+    if (n <= 512) return true;  // K6r (registers) fits any n <= 512
     if (cluster_smem_bytes(n) > (size_t)d.smem_optin) return false;
-    return strcmp(e, "cluster") == 0 || n <= 512;
+    return strcmp(e, "cluster") == 0 || strcmp(e, "cluster_smem") == 0;
 }
 
 // K2t (TMA bulk-copy ring, bulk.cuh) for mid-size n where A stays L2-resident and the per-row kernel
@@ -258,9 +260,18 @@ mapi_status iterate_launch(const Device& d, int32_t op, const float* A, int64_t 
     const int pol = load_policy(d, n, lda);
     MAPI_CUDA(cudaMemsetAsync(W.bar, 0, 256, s));
     if (use_cluster(d, n)) {
-        auto kern = op == 2 ? k_iterate_cluster<2> : (op == 1 ? k_iterate_cluster<1> : k_iterate_cluster<0>);
-        const size_t smem = cluster_smem_bytes(n);
-        MAPI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        // K6r (A in registers) for n <= 512 unless MAPI_DENSE_PATH=cluster_smem; K6 (A in shared memory) above
+        const bool reg = n <= 512 && strcmp(dense_path_env(), "cluster_smem") != 0;
+        using KernT = void (*)(IterArgs);
+        KernT kern;
+        if (reg) {
+            kern = n <= 256 ? (op == 2 ? k_iterate_cluster_reg<2, 1> : (op == 1 ? k_iterate_cluster_reg<1, 1> : k_iterate_cluster_reg<0, 1>))
+                            : (op == 2 ? k_iterate_cluster_reg<2, 2> : (op == 1 ? k_iterate_cluster_reg<1, 2> : k_iterate_cluster_reg<0, 2>));
+        } else {
+            kern = op == 2 ? k_iterate_cluster<2> : (op == 1 ? k_iterate_cluster<1> : k_iterate_cluster<0>);
+        }
+        const size_t smem = reg ? 0 : cluster_smem_bytes(n);
+        if (!reg) MAPI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         IterArgs a;
         a.A = A; a.n = n; a.lda = lda; a.b0 = b0; a.iters = iters; a.tol = tol;
         a.w_out = w_out; a.norms = norms; a.deltas = deltas; a.y = W.y; a.slots = W.slots;

@@ -531,6 +531,140 @@ __global__ void __launch_bounds__(kClusterThreads, 1) k_iterate_cluster(IterArgs
     cluster_sync_all();  // keep every CTA's shared memory alive until all DSMEM stores landed
 }
 
+// K6r: the same cluster iteration with the CTA's rows held in REGISTERS (n <= 512: a warp owns
+// RW = NPT rows, a lane 8 * NPT columns of each — 8 or 32 registers), so an iteration reads only w
+// from shared memory (the smem version spent ~1700 of its ~5500 cycles per iteration queueing the
+// 64 KB of A + w reads on the shared-memory pipe; scripts/probe_k6.cu).  The epilogue is spread
+// over the CTA instead of warp 0 (which spent ~2300 cycles on 8 dependent fp64 divisions per lane):
+// every warp forms s_t itself from the broadcast y (same fixed order everywhere), thread k forms
+// w_k = fp32(y_k / s_t) and its |delta| term, the warps' delta partials meet in shared memory, and
+// after the one __syncthreads every warp sums them in warp order -> the stop decision is uniform
+// without a second barrier.  Same per-row summation order as K6 (bitwise-identical w; the fp64
+// delta is summed in a different order).
+// Alternative y hand-off, off by default (measured slower: 2.42 vs 2.03 us/iteration at n = 256,
+// 4.19 vs 3.68 at n = 500): instead of a full cluster barrier (MAPI_K6_MBAR=1), each warp, after its DSMEM stores of
+// y, arrives (release.cluster, lane L -> CTA L) on the destination CTA's mbarrier for this iteration
+// parity; a CTA waits (acquire.cluster) for the 8 x 32 warp arrivals.  Two barriers alternate by
+// iteration, so arrivals of iteration t+1 never mix with t (a CTA can only be one iteration ahead
+// of the slowest one: it needs that CTA's arrivals to leave the current iteration).
+#ifndef MAPI_K6_MBAR
+#define MAPI_K6_MBAR 0
+#endif
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t* local_bar, uint32_t rank) {
+    const uint32_t a = (uint32_t)__cvta_generic_to_shared(local_bar);
+    uint32_t ra;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(ra) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+    const uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
+    uint32_t ok = 0;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+            " selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(ok)
+            : "r"(a), "r"(parity)
+            : "memory");
+    } while (!ok);
+}
+
+template <int OP, int NPT>
+__global__ void __launch_bounds__(kClusterThreads, 1) k_iterate_cluster_reg(IterArgs p) {
+    constexpr int NP = 256 * NPT, RW = NPT, CPL = 8 * NPT;
+    __shared__ __align__(16) float w_s[NP];
+    __shared__ __align__(16) float ybuf[2][NP];
+    __shared__ double dpart[kClusterThreads / 32];
+    __shared__ __align__(8) uint64_t ybar[2];
+    const int64_t n = p.n;
+    const int64_t R = cluster_rows_per_cta(n);
+    const uint32_t rank = cluster_ctarank();
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t r0 = (int64_t)rank * R, r1 = min(n, r0 + R);
+    const int nwd = (int)((n + 31) / 32);  // warps holding a delta partial
+    float a[RW][CPL];
+#pragma unroll
+    for (int j = 0; j < RW; ++j) {
+        const int64_t r = r0 + warp + 32 * j;
+#pragma unroll
+        for (int k = 0; k < NPT; ++k)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int64_t c = (int64_t)lane * 8 + 256 * k + i;
+                a[j][8 * k + i] = (r < r1 && c < n) ? p.A[r * p.lda + c] : 0.0f;
+            }
+    }
+    for (int k = tid; k < NP; k += kClusterThreads) w_s[k] = k < n ? p.b0[k] : 0.0f;
+    for (int k = tid; k < 2 * NP; k += kClusterThreads) (&ybuf[0][0])[k] = 0.0f;
+    if (MAPI_K6_MBAR && tid == 0) {
+        const uint32_t b0a = (uint32_t)__cvta_generic_to_shared(&ybar[0]);
+        const uint32_t b1a = (uint32_t)__cvta_generic_to_shared(&ybar[1]);
+        const uint32_t cnt = kClusterCtas * (kClusterThreads / 32);
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(b0a), "r"(cnt) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(b1a), "r"(cnt) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    cluster_sync_all();  // every CTA resident and staged before any DSMEM store
+    int32_t done = 0, status = kStOk;
+    for (int32_t t = 0; t < p.iters; ++t) {
+        float* yb = ybuf[t & 1];
+#pragma unroll
+        for (int j = 0; j < RW; ++j) {
+            const int64_t r = r0 + warp + 32 * j;
+            float acc[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
+#pragma unroll
+            for (int k = 0; k < NPT; ++k) {
+                float x[8];
+                ld_vec<8, false>(w_s + lane * 8 + 256 * k, x);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) acc[i] += mavp_term<OP>(a[j][8 * k + i], x[i]);
+            }
+            const float v = warp_sum(tree_sum(acc));
+            if (r < r1 && lane < kClusterCtas) st_cluster(yb + r, (uint32_t)lane, v);
+        }
+#if MAPI_K6_MBAR
+        if (lane < kClusterCtas) mbar_arrive_remote(&ybar[t & 1], (uint32_t)lane);
+        mbar_wait_cluster(&ybar[t & 1], (uint32_t)((t >> 1) & 1));
+#else
+        cluster_sync_all();
+#endif
+        // s_t: every warp, same fixed order (lane-strided fp64 partials, butterfly)
+        double ap = 0.0;
+        for (int64_t k = lane; k < n; k += 32) ap += norm_part<OP>(yb[k]);
+        const double sd = norm_final<OP>(warp_sum(ap));
+        if (!(sd > 0.0) || isinf(sd)) {  // uniform across the cluster
+            status = (sd == 0.0) ? kStDegenerate : kStNonfinite;
+            break;
+        }
+        // w_{t+1} = fp32(y / s_t) (fp64 division), one element per thread; delta partial per warp
+        double dp = 0.0;
+        if (tid < n) {
+            const float wn = (float)((double)yb[tid] / sd);
+            dp = (double)fabsf(wn - w_s[tid]);
+            w_s[tid] = wn;
+        }
+        dp = warp_sum(dp);
+        if (lane == 0 && warp < nwd) dpart[warp] = dp;
+        __syncthreads();
+        double delta = 0.0;
+        for (int q = 0; q < nwd; ++q) delta += dpart[q];
+        if (rank == 0 && tid == 0) {
+            if (p.norms) p.norms[t] = (float)sd;
+            if (p.deltas) p.deltas[t] = (float)delta;
+        }
+        done = t + 1;
+        if (p.tol > 0.0f && delta < (double)p.tol) break;
+    }
+    for (int64_t k = r0 + tid; k < r1; k += kClusterThreads) p.w_out[k] = w_s[k];
+    if (rank == 0 && tid == 0) {
+        p.status[0] = status;
+        p.status[1] = done;
+    }
+    cluster_sync_all();  // keep every CTA's shared memory alive until all DSMEM stores landed
+}
+
 // ---------------------------------------------------------------------------------------------
 // Multi-launch path (any n; also the CUDA-graph-style comparator): per iteration
 //   k_rows_partial: y = A (+) w (w in global, L1-cached), per-CTA sum|y| -> slots

@@ -12,10 +12,13 @@ import synth
 
 m.load()
 m.set_profiling(True)
-cfg = synth.cfg2(device="cuda")
-mats = {4096: cfg["A"]}
-b0s = {}
-for n in (1024, 2048, 6144, 8192, 16384):
+sizes = [int(x) for x in os.environ.get("PROBE_SIZES", "1024,2048,4096,6144,8192,16384").split(",")]
+mats = {}
+if 4096 in sizes:
+    mats[4096] = synth.cfg2(device="cuda")["A"]
+if 256 in sizes:
+    mats[256] = torch.from_numpy(synth.cfg1()["A"]).cuda()
+for n in [x for x in sizes if x not in (256, 4096)]:
     r = np.random.default_rng(n)
     mats[n] = torch.from_numpy((r.standard_normal((n, n)) + np.eye(n) * 5).astype(np.float32)).cuda()
 for n, A in sorted(mats.items()):

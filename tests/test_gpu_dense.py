@@ -248,7 +248,7 @@ def test_cfg3_last_step_and_invariants(mapi_lib, orc, cfg3_device):
     assert torch.equal(r100.w, r100b.w)
 
 
-@pytest.mark.parametrize("path", ["cluster", "rows", "coop", "bulk", "multi"])
+@pytest.mark.parametrize("path", ["cluster", "cluster_smem", "rows", "coop", "bulk", "multi"])
 @pytest.mark.parametrize("n", [256, 511, 4096, 8200])
 def test_every_dense_path_matches_oracle(mapi_lib, orc, monkeypatch, path, n):
     """Each dense iteration kernel (K6 cluster, K2 per-row, K2c cooperative rows, multi-launch),
@@ -311,6 +311,28 @@ def test_bulk_ring_early_stop_and_degenerate(mapi_lib, orc, monkeypatch):
     assert ei.value.name == "MAPI_ERR_DEGENERATE" and ei.value.iters_done == 0
     again = m.iterate(Ad, bd, 200)
     assert torch.equal(again.w, full.w)
+
+
+@pytest.mark.parametrize("n", [1, 7, 100, 256, 257, 500, 512])
+@pytest.mark.parametrize("op", ["min1", "min2"])
+def test_cluster_register_kernel_bitwise_vs_smem_kernel(mapi_lib, orc, monkeypatch, n, op):
+    """K6r (rows in registers, spread epilogue) keeps K6's per-row summation order: the iterates and
+    norms are bitwise identical to K6 (rows in shared memory); both match the oracle (T2)."""
+    m = mapi_lib
+    r = np.random.default_rng(n)
+    A = r.standard_normal((n, n)).astype(np.float32) + np.diag(np.abs(r.standard_normal(n)) * 3).astype(np.float32)
+    b0 = np.full(n, 1.0 / np.sqrt(n), np.float32)
+    opc = m.MIN1 if op == "min1" else m.MIN2
+    Ad, bd = torch.from_numpy(A).cuda(), torch.from_numpy(b0).cuda()
+    monkeypatch.setenv("MAPI_DENSE_PATH", "cluster")
+    reg = m.iterate(Ad, bd, 30, op=opc)
+    monkeypatch.setenv("MAPI_DENSE_PATH", "cluster_smem")
+    smem = m.iterate(Ad, bd, 30, op=opc)
+    assert torch.equal(reg.w, smem.w) and torch.equal(reg.norms, smem.norms)
+    np.testing.assert_allclose(reg.deltas.cpu().numpy(), smem.deltas.cpu().numpy(), rtol=1e-6)
+    if n > 1:
+        ref = orc.mapi(A, b0, 30, op=op)
+        _t2(reg.w_l2.cpu().numpy(), ref.w, reg.norms.cpu().numpy(), ref.norms)
 
 
 # ------------------------------------------------------------------------------ RPI comparator (NEXT-3)
