@@ -58,9 +58,10 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=15.0, help="budget of the oracle sample")
-    p.add_argument("--mode", default="auto", choices=["auto", "single", "sharded", "replicas"],
-                   help="multi-GPU layout for cfg3: sharded = row-sharded MAPI with an NCCL all-gather of y per "
-                        "iteration (strong scaling, the default for N > 1); replicas = independent copies")
+    p.add_argument("--mode", default="auto", choices=["auto", "single", "p2p", "sharded", "replicas"],
+                   help="multi-GPU layout for cfg3: p2p = row-sharded MAPI with the y exchange fused into one "
+                        "persistent kernel per rank (NVLink P2P; the default for N > 1); sharded = the same "
+                        "with an NCCL all-gather per iteration; replicas = independent copies")
     p.add_argument("--op", default="min1", choices=["min1", "min2", "dot"],
                    help="MAVP operator (Eq. 3 / Eq. 4) or 'dot' = the RPI comparator of Eq. (1) (dense workloads)")
     return p.parse_args()
@@ -391,12 +392,14 @@ def build_alg2(args, m, dev, stream):
                 oracle=None)
 
 
-def build_sharded(args, m, dev, stream):
-    """cfg3 row-sharded over the ranks (paper_2110_12065_b200.sharded)."""
+def build_sharded(args, m, dev, stream, fused=False):
+    """cfg3 row-sharded over the ranks (paper_2110_12065_b200.sharded).  fused: K2p, one
+    persistent kernel per rank with the y exchange done in-kernel over NVLink P2P (CUDA IPC mappings);
+    else K1n + an NCCL all-gather of y per iteration."""
     import torch
 
     import synth
-    from paper_2110_12065_b200.sharded import iterate_sharded, row_partition
+    from paper_2110_12065_b200.sharded import P2PExchange, iterate_sharded, iterate_sharded_p2p, row_partition
 
     n, world, rank = 32768, args.world, args.rank
     r0, r1 = row_partition(n, world, rank)
@@ -405,19 +408,33 @@ def build_sharded(args, m, dev, stream):
     b0 = torch.from_numpy(cfg["b0"]).to(dev)
     iters = cfg["iters"]
     opc = {"min1": 0, "min2": 1, "dot": 2}[args.op]
+    if fused:
+        ex = P2PExchange(n, rank, world, device=dev)
+
+        def run(A, b):
+            return iterate_sharded_p2p(A, n, r0, b, iters, ex, 0.0, op=opc, want_trace=False)
+
+        kernel = (f"K2p k_iterate_p2p: one cooperative launch per rank, {r1 - r0} rows, y exchanged in-kernel "
+                  "(P2P stores + sys-scope flags), 100 iterations (step time)")
+    else:
+        def run(A, b):
+            return iterate_sharded(A, n, b, iters, 0.0, op=opc)
+
+        kernel = (f"row-sharded step: K1n k_matvec_norm on {r1 - r0} rows + NCCL all-gather of y, x100 "
+                  "(step time)")
 
     def step():
-        iterate_sharded(A_local, n, b0, iters, 0.0, op=opc)
+        run(A_local, b0)
         return iters
 
     job_bytes = dense_bytes_per_iter(n, n)
     return Work(step=step, unit="iterations/s", per_launch=job_bytes * iters, bytes_per_unit=job_bytes, bound="hbm",
-                kernel=f"row-sharded step: K1 k_matvec on {r1 - r0} rows + NCCL all-gather of y + k_normalize_full, "
-                       "x100 (step time)", whole_step=True, shared_units=True,
+                kernel=kernel, whole_step=True, shared_units=True,
                 config={"workload": f"cfg3: {WORKLOADS['cfg3']}", "n": n, "rows_per_rank": r1 - r0,
                         "iters_per_step": iters, "op": args.op,
+                        "exchange": "in-kernel P2P (K2p)" if fused else "NCCL all-gather",
                         "l2_flush": "inputs larger than L2 (4 GiB / N per rank)"},
-                A=A_local, b0=b0, iters=iters, oracle=None, sharded=True)
+                A=A_local, b0=b0, iters=iters, oracle=None, sharded=True, run=run)
 
 
 BUILDERS = {"cfg1": build_dense, "alg2": build_alg2, "cfg3": build_dense, "cfg2": build_pca, "cfg4": build_batched,
@@ -446,10 +463,13 @@ def run_mapi(args, rank, world, local_rank):
     args.rank, args.world = rank, world
     mode = args.mode
     if mode == "auto":
-        mode = "sharded" if (world > 1 and args.workload == "cfg3") else "single"
-    if mode == "sharded" and args.workload != "cfg3":
-        raise SystemExit("--mode sharded is implemented for the cfg3 workload")
-    work = build_sharded(args, m, dev, stream) if mode == "sharded" else BUILDERS[args.workload](args, m, dev, stream)
+        mode = "p2p" if (world > 1 and args.workload == "cfg3") else "single"
+    if mode in ("sharded", "p2p") and args.workload != "cfg3":
+        raise SystemExit(f"--mode {mode} is implemented for the cfg3 workload")
+    if mode in ("sharded", "p2p"):
+        work = build_sharded(args, m, dev, stream, fused=mode == "p2p")
+    else:
+        work = BUILDERS[args.workload](args, m, dev, stream)
     torch.cuda.synchronize()
 
     metric = METRIC if args.workload == "cfg3" else f"MAPI {work.unit} ({args.workload})"
@@ -533,7 +553,8 @@ def run_mapi(args, rank, world, local_rank):
                          "avg_power_w": (e1 - e0) / t_wall, "source": "NVML total energy counter, timed region"}
     if args.workload == "cfg3" and not args.no_e2e:
         if getattr(work, "sharded", False):
-            out["e2e"] = e2e_sharded(args, m, work.A, work.b0, work.iters, dev, stream, world)
+            out["e2e"] = e2e_sharded(args, m, work.A, work.b0, work.iters, dev, stream, world,
+                                     getattr(work, "run", None))
         else:
             out["e2e"] = e2e_dense(args, m, work.A, work.b0, work.iters, dev, stream, world, dist)
     if not args.no_cpu_baseline and world == 1 and rank == 0 and work.oracle is not None:
@@ -589,7 +610,7 @@ def e2e_dense(args, m, A, b0, iters, dev, stream, world, dist):
             "path": "mapi_iterate_host: pinned host A,b0 -> device, 100 iterations, w + trace -> host"}
 
 
-def e2e_sharded(args, m, A_local, b0, iters, dev, stream, world):
+def e2e_sharded(args, m, A_local, b0, iters, dev, stream, world, run=None):
     """Row-sharded end to end: each rank copies its pinned host rows + b0 to the device, iterates with the
     per-iteration all-gather, and copies w back, all inside the timed region."""
     import torch
@@ -607,7 +628,7 @@ def e2e_sharded(args, m, A_local, b0, iters, dev, stream, world):
     def step():
         A_d.copy_(A_h, non_blocking=True)
         b0_d.copy_(b0_h, non_blocking=True)
-        res = iterate_sharded(A_d, n, b0_d, iters, 0.0)
+        res = run(A_d, b0_d) if run is not None else iterate_sharded(A_d, n, b0_d, iters, 0.0)
         w_h.copy_(res.w, non_blocking=True)
 
     step()

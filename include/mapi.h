@@ -68,7 +68,8 @@ typedef enum {
     MAPI_WS_RANK_CSR = 5,
     MAPI_WS_ITERATE_HOST = 6,
     MAPI_WS_MAVP_DEFLATE = 7, /* n = M */
-    MAPI_WS_RECONSTRUCT = 8   /* n = M, nnz = N (images), k = r (components) */
+    MAPI_WS_RECONSTRUCT = 8,  /* n = M, nnz = N (images), k = r (components) */
+    MAPI_WS_ITERATE_SHARDED = 9
 } mapi_ws_op;
 
 /* y = A (op) x — the matrix extension of the MAVP (reading Q6: y_j uses ROW j):
@@ -120,6 +121,38 @@ mapi_status mapi_normalize(int32_t op, const float *y, int64_t n, float *w, floa
 mapi_status mapi_matvec_normalized(int32_t op, const float *A, int64_t n_rows, int64_t n_cols, int64_t lda,
                                    const float *y_prev, const float *w_prev, float *w_next, float *y_out,
                                    float *s_out, float *delta_out, int32_t *status_out, mapi_stream_t stream);
+
+/* ---- Row-sharded MAPI with the y exchange fused into the kernel.
+ * Every rank allocates one EXCHANGE buffer with mapi_p2p_alloc (device memory, zeroed; layout in
+ * p2p.cuh: a u64 arrival flag, y for two iteration parities, per-CTA norm partials), publishes its
+ * 64-byte CUDA IPC handle (mapi_ipc_get_handle), opens every peer's (mapi_ipc_open_handle; the own
+ * buffer is used directly), and passes the device array `peers` (world x u64 base addresses, peers[rank]
+ * = own) to mapi_iterate_sharded.  Ownership: the caller frees with mapi_p2p_free / closes with
+ * mapi_ipc_close_handle. */
+size_t mapi_p2p_exchange_bytes(int64_t n, int32_t world);
+mapi_status mapi_p2p_alloc(size_t bytes, void **ptr_out);
+mapi_status mapi_p2p_free(void *ptr);
+mapi_status mapi_ipc_get_handle(const void *ptr, void *handle_out /* 64 bytes, host */);
+mapi_status mapi_ipc_open_handle(const void *handle /* 64 bytes, host */, void **ptr_out);
+mapi_status mapi_ipc_close_handle(void *ptr);
+
+/* Algorithm 1 on a row-sharded A in ONE cooperative launch per rank: rank `rank` of `world`
+ * holds rows [row0, row0 + m) of the n x n matrix (A_local: m x n, lda; 32 B-aligned rows, lda % 8 == 0,
+ * n >= 256); b0 is the full start vector (n).  Per iteration every CTA computes its rows, stores them
+ * (and its fp64 norm partial) into every rank's exchange buffer through NVLink P2P, release-adds the
+ * peers' flags (system scope) and waits for all world x G arrivals on its own; then s_t, w_{t+1} and
+ * delta_t are formed in the same fixed order on every rank (identical bits, identical stop decision).
+ * epoch0 / flag_base: the global iteration index and own flag value at the start of this call (0 / 0
+ * for a fresh exchange buffer; afterwards advance both by *published_out and *published_out * world *
+ * (*grid_out)); identical on every rank.  Outputs: w_out (full n, l1-unit; l2-unit for DOT), norms /
+ * deltas (iters, nullable), host *iters_done, *published_out (iterations that reached the exchange),
+ * *grid_out (CTAs per rank).  ws: mapi_workspace_size(MAPI_WS_ITERATE_SHARDED, ...) = 256 bytes of
+ * status.  Synchronises `stream`. */
+mapi_status mapi_iterate_sharded(int32_t op, const float *A_local, int64_t m, int64_t n, int64_t lda, int64_t row0,
+                                 const float *b0, int32_t iters, float tol, int32_t rank, int32_t world,
+                                 const uint64_t *peers, uint64_t epoch0, uint64_t flag_base, float *w_out,
+                                 float *norms, float *deltas, int32_t *iters_done, int32_t *published_out,
+                                 int32_t *grid_out, void *ws, size_t ws_bytes, mapi_stream_t stream);
 
 /* mapi_iterate with HOST buffers (end-to-end path): A_host (n x lda), b0_host, w_out_host,
  * w_l2_out_host / norms_host / deltas_host (nullable), iters_done (host).  The call copies A and
@@ -202,7 +235,8 @@ mapi_status mapi_rank_csr(int64_t n, int64_t nnz, const int32_t *row_ptr, const 
  *   MAPI_WS_MATVEC: 0.  MAPI_WS_ITERATE: n.  MAPI_WS_ITERATE_BATCHED: n, k.
  *   MAPI_WS_PCA_TOPK: n, k.  MAPI_WS_CSR_PREPARE / MAPI_WS_RANK_CSR: n, nnz.
  *   MAPI_WS_ITERATE_HOST: n, and nnz = lda (the device copy of A is n*lda floats), k = iters.
- *   MAPI_WS_MAVP_DEFLATE: n = M.  MAPI_WS_RECONSTRUCT: n = M, nnz = N, k = r. */
+ *   MAPI_WS_MAVP_DEFLATE: n = M.  MAPI_WS_RECONSTRUCT: n = M, nnz = N, k = r.
+ *   MAPI_WS_ITERATE_SHARDED: 256 (status words). */
 size_t mapi_workspace_size(int32_t op, int64_t n, int64_t nnz, int32_t k);
 
 const char *mapi_status_string(mapi_status status);

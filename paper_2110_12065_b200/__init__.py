@@ -25,7 +25,7 @@ __all__ = ["load", "build", "MapiError", "mavp_matvec", "mavp_matmat", "min_cova
 
 MIN1, MIN2, DOT = 0, 1, 2  # DOT: regular product of Eq. (1), the RPI comparator
 (WS_MATVEC, WS_ITERATE, WS_ITERATE_BATCHED, WS_PCA_TOPK, WS_CSR_PREPARE, WS_RANK_CSR, WS_ITERATE_HOST,
- WS_MAVP_DEFLATE, WS_RECONSTRUCT) = range(9)
+ WS_MAVP_DEFLATE, WS_RECONSTRUCT, WS_ITERATE_SHARDED) = range(10)
 STATUS = {0: "MAPI_OK", 1: "MAPI_ERR_NULL", 2: "MAPI_ERR_SHAPE", 3: "MAPI_ERR_BAD_PARAM",
           4: "MAPI_ERR_DEGENERATE", 5: "MAPI_ERR_NEGATIVE", 6: "MAPI_ERR_NONFINITE",
           7: "MAPI_ERR_WORKSPACE", 8: "MAPI_ERR_CUDA"}
@@ -70,6 +70,14 @@ def load():
             "mapi_csr_prepare": (st, [i64, i64, P, P, f32, P, P, P, sz, P]),
             "mapi_rank_csr": (st, [i64, i64, P, P, P, P, P, i32, f32, P, P, P, P, P, sz, P]),
             "mapi_workspace_size": (sz, [i32, i64, i64, i32]),
+            "mapi_p2p_exchange_bytes": (sz, [i64, i32]),
+            "mapi_p2p_alloc": (st, [sz, ctypes.POINTER(ctypes.c_void_p)]),
+            "mapi_p2p_free": (st, [P]),
+            "mapi_ipc_get_handle": (st, [P, P]),
+            "mapi_ipc_open_handle": (st, [P, ctypes.POINTER(ctypes.c_void_p)]),
+            "mapi_ipc_close_handle": (st, [P]),
+            "mapi_iterate_sharded": (st, [i32, P, i64, i64, i64, i64, P, i32, f32, i32, i32, P, ctypes.c_uint64,
+                                          ctypes.c_uint64, P, P, P, P, P, P, P, sz, P]),
             "mapi_status_string": (ctypes.c_char_p, [st]),
             "mapi_last_error_message": (ctypes.c_char_p, []),
             "mapi_launch_count": (ctypes.c_uint64, []),

@@ -18,6 +18,7 @@
 #include "dense.cuh"
 #include "matmat.cuh"
 #include "outer.cuh"
+#include "p2p.cuh"
 
 using namespace mapi;
 
@@ -549,6 +550,7 @@ size_t mapi_workspace_size(int32_t op, int64_t n, int64_t nnz, int32_t k) {
     case MAPI_WS_RECONSTRUCT: return outer_ws_bytes(n, nnz, k, nnz);
     case MAPI_WS_CSR_PREPARE: return csr_prepare_ws_bytes(n, nnz);
     case MAPI_WS_RANK_CSR: return csr_rank_ws_bytes(n, nnz);
+    case MAPI_WS_ITERATE_SHARDED: return 256;
     }
     return 0;
 }
@@ -948,6 +950,114 @@ mapi_status mapi_normalize(int32_t op, const float* y, int64_t n, float* w, floa
     k_normalize_full<<<1, 1024, 0, static_cast<cudaStream_t>(stream)>>>(n, y, w, op == MAPI_OP_DOT ? 1 : 0, s_out,
                                                                         delta_out, status_out);
     MAPI_LAUNCHED();
+    return MAPI_OK;
+}
+
+// ---------------------------------------------------------------------------- fused P2P sharding
+size_t mapi_p2p_exchange_bytes(int64_t n, int32_t world) {
+    if (n < 0 || world < 1) return 0;
+    return p2p_exchange_bytes(n, world);
+}
+
+mapi_status mapi_p2p_alloc(size_t bytes, void** ptr_out) {
+    if (!ptr_out) return fail(MAPI_ERR_NULL, "ptr_out is NULL");
+    *ptr_out = nullptr;
+    if (bytes == 0) return fail(MAPI_ERR_BAD_PARAM, "bytes must be > 0");
+    MAPI_CUDA(cudaMalloc(ptr_out, bytes));
+    MAPI_CUDA(cudaMemset(*ptr_out, 0, bytes));
+    return MAPI_OK;
+}
+
+mapi_status mapi_p2p_free(void* ptr) {
+    if (ptr) MAPI_CUDA(cudaFree(ptr));
+    return MAPI_OK;
+}
+
+mapi_status mapi_ipc_get_handle(const void* ptr, void* handle_out) {
+    if (!ptr || !handle_out) return fail(MAPI_ERR_NULL, "ptr / handle_out is NULL");
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    cudaIpcMemHandle_t h;
+    MAPI_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(ptr)));
+    memcpy(handle_out, &h, sizeof(h));
+    return MAPI_OK;
+}
+
+mapi_status mapi_ipc_open_handle(const void* handle, void** ptr_out) {
+    if (!handle || !ptr_out) return fail(MAPI_ERR_NULL, "handle / ptr_out is NULL");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    MAPI_CUDA(cudaIpcOpenMemHandle(ptr_out, h, cudaIpcMemLazyEnablePeerAccess));
+    return MAPI_OK;
+}
+
+mapi_status mapi_ipc_close_handle(void* ptr) {
+    if (ptr) MAPI_CUDA(cudaIpcCloseMemHandle(ptr));
+    return MAPI_OK;
+}
+
+mapi_status mapi_iterate_sharded(int32_t op, const float* A_local, int64_t m, int64_t n, int64_t lda, int64_t row0,
+                                 const float* b0, int32_t iters, float tol, int32_t rank, int32_t world,
+                                 const uint64_t* peers, uint64_t epoch0, uint64_t flag_base, float* w_out,
+                                 float* norms, float* deltas, int32_t* iters_done, int32_t* published_out,
+                                 int32_t* grid_out, void* ws, size_t ws_bytes, mapi_stream_t stream) {
+    mapi_status st = check_op(op, true);
+    if (st != MAPI_OK) return st;
+    if (!A_local || !b0 || !peers || !w_out || !ws) return fail(MAPI_ERR_NULL, "a required pointer is NULL");
+    if (world < 1 || world > kP2pMaxWorld || rank < 0 || rank >= world)
+        return fail(MAPI_ERR_BAD_PARAM, "rank %d / world %d (world in [1, %d])", rank, world, kP2pMaxWorld);
+    if (n < 256 || m < 1 || m > n || row0 < 0 || row0 + m > n)
+        return fail(MAPI_ERR_SHAPE, "rows [%lld, %lld) of n = %lld (n >= 256 required)", (long long)row0,
+                    (long long)(row0 + m), (long long)n);
+    if (lda < n) return fail(MAPI_ERR_SHAPE, "lda (%lld) < n (%lld)", (long long)lda, (long long)n);
+    if (vec_width(A_local, lda) != 8) return fail(MAPI_ERR_SHAPE, "A_local rows must be 32 B-aligned (lda %% 8 == 0)");
+    if (iters < 1) return fail(MAPI_ERR_BAD_PARAM, "iters (%d) must be >= 1", iters);
+    if (!(tol >= 0.0f)) return fail(MAPI_ERR_BAD_PARAM, "tol must be >= 0");
+    if (ws_bytes < 256) return fail(MAPI_ERR_WORKSPACE, "ws_bytes (%zu) < 256", ws_bytes);
+    Device d;
+    if ((st = device_info(d)) != MAPI_OK) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int nw = coop_warps(n);
+    const int grid = (int)std::min<int64_t>({(int64_t)d.sms, m, (int64_t)kP2pMaxGrid});
+    const size_t smem = p2p_smem_bytes(m, n, grid, nw);
+    if (smem > (size_t)d.smem_optin) return fail(MAPI_ERR_SHAPE, "n (%lld) too large for the staged w", (long long)n);
+    int32_t* status = static_cast<int32_t*>(ws);
+    MAPI_CUDA(cudaMemsetAsync(status, 0, 8, s));
+    P2PArgs a;
+    a.A = A_local; a.m = m; a.n = n; a.lda = lda; a.row0 = row0; a.b0 = b0; a.iters = iters; a.tol = tol;
+    a.rank = rank; a.world = world; a.peers = reinterpret_cast<const unsigned long long*>(peers);
+    a.epoch0 = epoch0; a.flag_base = flag_base; a.w_out = w_out; a.norms = norms; a.deltas = deltas;
+    a.status = status;
+    const int pol = load_policy(d, m, lda);
+    Timer timer(s);
+    with_op(op, [&](auto OPc) {
+        return with_pol(pol, [&](auto POLc) {
+            constexpr int OP = decltype(OPc)::value, POL = decltype(POLc)::value;
+            auto kern = nw == 32 ? k_iterate_p2p<OP, POL, 32> : k_iterate_p2p<OP, POL, 16>;
+            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e == cudaSuccess) {
+                void* args[] = {&a};
+                timer.start();
+                e = cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(nw * 32), args, smem, s);
+                timer.stop();
+                g_launches.fetch_add(1, std::memory_order_relaxed);
+            }
+            if (e != cudaSuccess) st = fail(MAPI_ERR_CUDA, "sharded launch (grid %d): %s", grid, cudaGetErrorString(e));
+            return 0;
+        });
+    });
+    if (st != MAPI_OK) return st;
+    int32_t h[2] = {0, 0};
+    MAPI_CUDA(cudaMemcpyAsync(h, status, sizeof(h), cudaMemcpyDeviceToHost, s));
+    MAPI_CUDA(cudaStreamSynchronize(s));
+    timer.harvest();
+    if (iters_done) *iters_done = h[1];
+    // iterations that reached the exchange: the completed ones, plus the one a degenerate s stopped
+    // (a timed-out exchange leaves the buffers inconsistent: the caller must discard the exchange)
+    if (published_out) *published_out = h[1] + ((h[0] == kStDegenerate || h[0] == kStNonfinite) ? 1 : 0);
+    if (grid_out) *grid_out = grid;
+    if (h[0] == kStP2pTimeout)
+        return fail(MAPI_ERR_CUDA, "peer exchange timed out at iteration %d (a rank did not arrive)", h[1]);
+    if (h[0] != 0) return fail((mapi_status)h[0], "degenerate / non-finite norm at iteration %d", h[1]);
     return MAPI_OK;
 }
 

@@ -12,6 +12,13 @@ of Algorithm 1:
 The local mat-vec, the all-gather and the normalisation are injectable so that the orchestration (the
 partition, the gather order, the per-rank agreement) is tested with gloo on CPU (tests/test_dist_host.py).
 The product path passes the CUDA entry points and torch.distributed over NCCL.
+
+`P2PExchange` + `iterate_sharded_p2p` are the fused alternative (K2p, csrc/p2p.cuh): ONE cooperative
+launch per rank runs every iteration and the y exchange happens inside it — each CTA stores its rows of
+y straight into every rank's exchange buffer over NVLink (CUDA IPC mappings), release-adds the peers'
+arrival flags at system scope and waits for all of them; no NCCL call on the data path.  The host side
+here only sets up the mappings once (IPC handles all-gathered over torch.distributed) and carries the
+global iteration epoch / flag base from call to call.
 """
 from __future__ import annotations
 
@@ -136,3 +143,122 @@ def iterate_sharded(A_local, n: int, b0, iters: int, tol: float = 0.0, op: int =
         t = int(bad[0, 0])
         raise MapiError(int(st[t]), f"{STATUS.get(int(st[t]), int(st[t]))} at iteration {t}", t)
     return ShardedResult(w, norms[:done], deltas[:done], done)
+
+
+# ------------------------------------------------------------------------------ fused P2P exchange (K2p)
+
+
+class P2PExchange:
+    """The per-rank exchange buffer of K2p and its peers' IPC mappings.
+
+    lib: the loaded libmapi (or a stand-in with the same six entry points, for host-logic tests);
+    allgather(bytes) -> list of every rank's bytes, in rank order (torch.distributed by default).
+    `epoch` / `flag_base` carry the global iteration index and the own flag value across calls; they
+    advance by `published` and `published * world * grid` after each call, identically on every rank.
+    """
+
+    def __init__(self, n: int, rank: int, world: int, lib=None, allgather=None, group=None, device=None):
+        import ctypes
+
+        if lib is None:
+            from . import load
+
+            lib = load()
+        self.lib, self.n, self.rank, self.world = lib, n, rank, world
+        self.bytes = int(lib.mapi_p2p_exchange_bytes(n, world))
+        ptr = ctypes.c_void_p()
+        self._check(lib.mapi_p2p_alloc(self.bytes, ctypes.byref(ptr)))
+        self.own = int(ptr.value)
+        handle = ctypes.create_string_buffer(64)
+        self._check(lib.mapi_ipc_get_handle(self.own, handle))
+        if allgather is None:
+            allgather = _dist_allgather_bytes(group, device)
+        handles = allgather(bytes(handle.raw))
+        if len(handles) != world:
+            raise ValueError(f"expected {world} handles, got {len(handles)}")
+        self.opened = []
+        peers = []
+        for q, h in enumerate(handles):
+            if q == rank:
+                peers.append(self.own)
+                continue
+            out = ctypes.c_void_p()
+            self._check(lib.mapi_ipc_open_handle(ctypes.create_string_buffer(h, 64), ctypes.byref(out)))
+            self.opened.append(int(out.value))
+            peers.append(int(out.value))
+        self.peer_addrs = peers
+        self.epoch = 0
+        self.flag_base = 0
+        self.peers_dev = None
+        if device is not None:
+            import torch
+
+            self.peers_dev = torch.tensor(peers, dtype=torch.int64, device=device)
+
+    def _check(self, st):
+        if st:
+            from . import MapiError
+
+            raise MapiError(st, self.lib.mapi_last_error_message().decode(errors="replace"))
+
+    def advance(self, published: int, grid: int):
+        self.epoch += published
+        self.flag_base += published * self.world * grid
+
+    def close(self):
+        for a in self.opened:
+            self.lib.mapi_ipc_close_handle(a)
+        self.opened = []
+        if self.own:
+            self.lib.mapi_p2p_free(self.own)
+            self.own = 0
+
+
+def _dist_allgather_bytes(group, device):
+    import torch
+    import torch.distributed as dist
+
+    def gather(b: bytes):
+        if not dist.is_initialized() or dist.get_world_size(group) == 1:
+            return [b]
+        t = torch.frombuffer(bytearray(b), dtype=torch.uint8).to(device if device is not None else "cpu")
+        out = torch.empty(dist.get_world_size(group) * t.numel(), dtype=torch.uint8, device=t.device)
+        dist.all_gather_into_tensor(out, t, group=group)
+        return [bytes(c.cpu().numpy().tobytes()) for c in out.view(-1, t.numel())]
+
+    return gather
+
+
+def iterate_sharded_p2p(A_local, n: int, row0: int, b0, iters: int, exchange: P2PExchange, tol: float = 0.0,
+                        op: int = 0, want_trace: bool = True) -> ShardedResult:
+    """MAPI on a row-sharded A with the exchange fused into one persistent kernel per rank (K2p)."""
+    import ctypes
+
+    import torch
+
+    from . import MapiError, STATUS, WS_ITERATE_SHARDED
+
+    lib = exchange.lib
+    dev = A_local.device
+    m = A_local.shape[0]
+    if A_local.dim() != 2 or A_local.stride(1) != 1 or A_local.dtype != torch.float32:
+        raise ValueError("A_local must be a row-major fp32 CUDA tensor")
+    if exchange.peers_dev is None:
+        exchange.peers_dev = torch.tensor(exchange.peer_addrs, dtype=torch.int64, device=dev)
+    w = torch.empty(n, dtype=torch.float32, device=dev)
+    norms = torch.zeros(iters, dtype=torch.float32, device=dev) if want_trace else None
+    deltas = torch.zeros(iters, dtype=torch.float32, device=dev) if want_trace else None
+    ws = torch.empty(int(lib.mapi_workspace_size(WS_ITERATE_SHARDED, 0, 0, 0)), dtype=torch.uint8, device=dev)
+    done, published, grid = ctypes.c_int32(0), ctypes.c_int32(0), ctypes.c_int32(0)
+    sp = torch.cuda.current_stream(dev).cuda_stream
+    st = lib.mapi_iterate_sharded(op, A_local.data_ptr(), m, n, A_local.stride(0), row0, b0.data_ptr(), iters,
+                                  float(tol), exchange.rank, exchange.world, exchange.peers_dev.data_ptr(),
+                                  exchange.epoch, exchange.flag_base, w.data_ptr(),
+                                  None if norms is None else norms.data_ptr(),
+                                  None if deltas is None else deltas.data_ptr(), ctypes.byref(done),
+                                  ctypes.byref(published), ctypes.byref(grid), ws.data_ptr(), ws.numel(), sp)
+    exchange.advance(published.value, grid.value)
+    if st:
+        raise MapiError(st, lib.mapi_last_error_message().decode(errors="replace"), done.value)
+    k = done.value
+    return ShardedResult(w, norms[:k] if norms is not None else None, deltas[:k] if deltas is not None else None, k)

@@ -138,3 +138,91 @@ def test_row_partition():
 
     with pytest.raises(ValueError):
         row_partition(10, 3, 0)
+
+
+# ---------------------------------------------------------------- fused P2P exchange set-up (K2p)
+
+
+class _FakeP2PLib:
+    """Stand-in for libmapi's six exchange entry points (host logic only): addresses encode ranks."""
+
+    def __init__(self, rank):
+        self.rank = rank
+        self.closed, self.freed = [], []
+
+    def mapi_p2p_exchange_bytes(self, n, world):
+        return 256 + 8 * n + 16 * world
+
+    def mapi_p2p_alloc(self, nbytes, ptr_ref):
+        ptr_ref._obj.value = 0x100000 * (self.rank + 1)
+        return 0
+
+    def mapi_ipc_get_handle(self, ptr, handle):
+        handle.raw = bytes([self.rank + 1]) * 64
+        return 0
+
+    def mapi_ipc_open_handle(self, handle, ptr_ref):
+        ptr_ref._obj.value = 0xA0000000 + handle.raw[0]
+        return 0
+
+    def mapi_ipc_close_handle(self, ptr):
+        self.closed.append(ptr)
+        return 0
+
+    def mapi_p2p_free(self, ptr):
+        self.freed.append(ptr)
+        return 0
+
+    def mapi_last_error_message(self):
+        return b""
+
+
+def _p2p_setup_worker(rank, world, port, q):
+    import sys
+
+    import torch.distributed as tdist
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2110_12065_b200.sharded import P2PExchange
+
+    def allgather(b):
+        out = [None] * world
+        tdist.all_gather_object(out, b)
+        return out
+
+    lib = _FakeP2PLib(rank)
+    ex = P2PExchange(96, rank, world, lib=lib, allgather=allgather)
+    peers = list(ex.peer_addrs)
+    ex.advance(7, 148)
+    ex.advance(3, 148)
+    adv = (ex.epoch, ex.flag_base)
+    ex.close()
+    q.put((rank, peers, adv, sorted(lib.closed), lib.freed))
+    tdist.barrier()
+    tdist.destroy_process_group()
+
+
+def test_p2p_exchange_setup_gloo_world3():
+    """K2p host set-up with three ranks: IPC handles all-gathered in rank order, peers[rank] is the
+    own buffer and peers[q] the mapping of rank q's handle, the epoch / flag base advance by the
+    published iterations (x world x grid), and close() unmaps every peer and frees the own buffer."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    world = 3
+    procs = [ctx.Process(target=_p2p_setup_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = {r: rest for r, *rest in [q.get(timeout=180) for _ in range(world)]}
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in range(world):
+        peers, adv, closed, freed = out[r]
+        own = 0x100000 * (r + 1)
+        assert peers == [own if p == r else 0xA0000000 + p + 1 for p in range(world)]
+        assert adv == (10, 10 * world * 148)
+        assert closed == sorted(0xA0000000 + p + 1 for p in range(world) if p != r)
+        assert freed == [own]

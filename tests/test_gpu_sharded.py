@@ -59,3 +59,97 @@ def test_sharded_tol_and_rows_generator(mapi_lib, orc, nccl_world1):
     assert res.iters_done < 200 and d[-1] < 5e-3 and np.all(d[:-1] >= 5e-3)  # stops at the first delta < tol
     A_full = synth.cfg3(device="cuda", n=n, rank=64)["A"]
     assert torch.equal(A_full, cfg["A"])  # the row-block generator reproduces the full matrix
+
+
+# ------------------------------------------------------------------ fused P2P exchange (K2p)
+
+
+def _p2p_exchange(n):
+    from paper_2110_12065_b200.sharded import P2PExchange
+
+    return P2PExchange(n, 0, 1, device="cuda")
+
+
+def test_p2p_world1_bitwise_vs_coop(mapi_lib, monkeypatch):
+    """With one rank the fused kernel runs the exchange through its own buffer (local stores, own
+    flag as the grid barrier); its rows, partial order and s order are K2c's, so the iterates, norms
+    and deltas are bitwise identical to mapi_iterate on the cooperative path."""
+    from paper_2110_12065_b200.sharded import iterate_sharded_p2p
+
+    m = mapi_lib
+    n = 8192
+    r = np.random.default_rng(11)
+    A = torch.from_numpy((r.standard_normal((n, n)) + np.eye(n) * 4).astype(np.float32)).cuda()
+    b0 = torch.full((n,), 1 / np.sqrt(n), device="cuda")
+    ex = _p2p_exchange(n)
+    try:
+        res = iterate_sharded_p2p(A, n, 0, b0, 30, ex)
+        monkeypatch.setenv("MAPI_DENSE_PATH", "coop")
+        ref = m.iterate(A, b0, 30)
+        assert torch.equal(res.w, ref.w) and torch.equal(res.norms, ref.norms) and torch.equal(res.deltas, ref.deltas)
+        assert ex.epoch == 30
+    finally:
+        ex.close()
+
+
+def test_p2p_world1_calls_continue_epoch_and_parity(mapi_lib, orc):
+    """Consecutive calls on one exchange buffer (odd iteration counts flip the buffer parity between
+    calls; the flag keeps counting) give the same results as fresh buffers; ragged n (n % 256 != 0)
+    and min2 / dot operators against the oracle (T2)."""
+    from paper_2110_12065_b200.sharded import iterate_sharded_p2p
+
+    m = mapi_lib
+    n = 4104
+    r = np.random.default_rng(5)
+    A_h = (r.standard_normal((n, n)) + np.eye(n) * 3).astype(np.float32)
+    A = torch.from_numpy(A_h).cuda()
+    b0_h = np.full(n, 1 / np.sqrt(n), np.float32)
+    b0 = torch.from_numpy(b0_h).cuda()
+    ex = _p2p_exchange(n)
+    try:
+        outs = [iterate_sharded_p2p(A, n, 0, b0, k, ex) for k in (7, 8, 5)]
+        assert ex.epoch == 20
+        for k, o in zip((7, 8, 5), outs):
+            fresh_ex = _p2p_exchange(n)
+            try:
+                fresh = iterate_sharded_p2p(A, n, 0, b0, k, fresh_ex)
+            finally:
+                fresh_ex.close()
+            assert torch.equal(o.w, fresh.w) and torch.equal(o.deltas, fresh.deltas)
+        for op, name in ((m.MIN2, "min2"), (m.DOT, None)):
+            res = iterate_sharded_p2p(A, n, 0, b0, 20, ex, op=op)
+            ref = orc.mapi(A_h, b0_h, 20, op=name) if name else orc.rpi(A_h, b0_h, 20)
+            _t2(res.w.cpu().numpy(), ref.w)
+            np.testing.assert_allclose(res.norms.cpu().numpy(), ref.norms, rtol=1e-5)
+    finally:
+        ex.close()
+
+
+def test_p2p_world1_tol_stop_and_degenerate(mapi_lib):
+    """Early stop by tol and a degenerate run advance the exchange epoch by the iterations that
+    reached the exchange; a following normal call is unaffected."""
+    from paper_2110_12065_b200.sharded import iterate_sharded_p2p
+
+    m = mapi_lib
+    n = 2048
+    r = np.random.default_rng(2)
+    A = torch.from_numpy(((r.standard_normal((n, n)) / 8) + np.diag(np.linspace(4, 1, n))).astype(np.float32)).cuda()
+    b0 = torch.full((n,), 1 / np.sqrt(n), device="cuda")
+    ex = _p2p_exchange(n)
+    try:
+        full = iterate_sharded_p2p(A, n, 0, b0, 100, ex)
+        d = full.deltas.cpu().numpy()
+        tol = float(d[30]) * 1.0001
+        first = int(np.nonzero(d < tol)[0][0])
+        e0 = ex.epoch
+        res = iterate_sharded_p2p(A, n, 0, b0, 100, ex, tol=tol)
+        assert res.iters_done == first + 1 and ex.epoch == e0 + first + 1
+        assert torch.equal(res.deltas, full.deltas[: first + 1])
+        e1 = ex.epoch
+        with pytest.raises(m.MapiError) as ei:
+            iterate_sharded_p2p(torch.zeros(n, n, device="cuda"), n, 0, b0, 10, ex)
+        assert ei.value.name == "MAPI_ERR_DEGENERATE" and ex.epoch == e1 + 1
+        again = iterate_sharded_p2p(A, n, 0, b0, 100, ex)
+        assert torch.equal(again.w, full.w)
+    finally:
+        ex.close()
