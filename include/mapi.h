@@ -69,7 +69,8 @@ typedef enum {
     MAPI_WS_ITERATE_HOST = 6,
     MAPI_WS_MAVP_DEFLATE = 7, /* n = M */
     MAPI_WS_RECONSTRUCT = 8,  /* n = M, nnz = N (images), k = r (components) */
-    MAPI_WS_ITERATE_SHARDED = 9
+    MAPI_WS_ITERATE_SHARDED = 9,
+    MAPI_WS_ITERATE_HOST_MANY = 10  /* n, nnz = lda, k = iters; add 8 bytes per problem beyond 2 */
 } mapi_ws_op;
 
 /* y = A (op) x — the matrix extension of the MAVP (reading Q6: y_j uses ROW j):
@@ -164,6 +165,19 @@ mapi_status mapi_iterate_host(int32_t op, const float *A_host, int64_t n, int64_
                               float *w_l2_out_host, float *norms_host, float *deltas_host,
                               int32_t *iters_done, void *ws, size_t ws_bytes, mapi_stream_t stream);
 
+/* `count` independent mapi_iterate problems with HOST buffers, pipelined (end-to-end serving path):
+ * problem i+1's A_hosts[i+1] / b0_hosts[i+1] host->device copies run on an internal copy stream while
+ * problem i iterates on `stream` (two device slots alternate), and each result is copied back to
+ * w_out_hosts[i] (norms_hosts / deltas_hosts: nullable arrays of nullable pointers).  Host buffers must
+ * be PINNED for the copies to overlap.  iters_done: host int32[count] (nullable).  ws:
+ * mapi_workspace_size(MAPI_WS_ITERATE_HOST_MANY, n, lda, iters) + 8 * max(0, count - 2) bytes.  Returns the
+ * first problem's error, if any.  Synchronises `stream`. */
+mapi_status mapi_iterate_host_many(int32_t op, int32_t count, const float *const *A_hosts, int64_t n, int64_t lda,
+                                   const float *const *b0_hosts, int32_t iters, float tol,
+                                   float *const *w_out_hosts, float *const *norms_hosts,
+                                   float *const *deltas_hosts, int32_t *iters_done, void *ws, size_t ws_bytes,
+                                   mapi_stream_t stream);
+
 /* Batched MAPI: k independent runs of mapi_iterate on the same A ("multiple independent
  * runs"; matrix extension P:69-70 with p = k columns), Y = A (op) W each iteration.
  * B0, W_out: k x n, vector-major (vector v at B0 + v*n).  norms, deltas: iters x k
@@ -236,7 +250,8 @@ mapi_status mapi_rank_csr(int64_t n, int64_t nnz, const int32_t *row_ptr, const 
  *   MAPI_WS_PCA_TOPK: n, k.  MAPI_WS_CSR_PREPARE / MAPI_WS_RANK_CSR: n, nnz.
  *   MAPI_WS_ITERATE_HOST: n, and nnz = lda (the device copy of A is n*lda floats), k = iters.
  *   MAPI_WS_MAVP_DEFLATE: n = M.  MAPI_WS_RECONSTRUCT: n = M, nnz = N, k = r.
- *   MAPI_WS_ITERATE_SHARDED: 256 (status words). */
+ *   MAPI_WS_ITERATE_SHARDED: 256 (status words).
+ *   MAPI_WS_ITERATE_HOST_MANY: n, nnz = lda, k = iters (two slots; + 8 bytes per problem beyond 2). */
 size_t mapi_workspace_size(int32_t op, int64_t n, int64_t nnz, int32_t k);
 
 const char *mapi_status_string(mapi_status status);

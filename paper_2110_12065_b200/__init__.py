@@ -21,11 +21,11 @@ from ._build import build  # noqa: F401  (re-exported: compile in-tree)
 __all__ = ["load", "build", "MapiError", "mavp_matvec", "mavp_matmat", "min_covariance", "center_rows", "mavp_deflate",
            "mavp_reconstruct", "iterate", "iterate_host", "iterate_batched",
            "pca_topk", "csr_prepare", "rank_csr", "workspace_size", "launch_count", "set_profiling",
-           "last_kernel_ms", "MIN1", "MIN2", "DOT"]
+           "last_kernel_ms", "MIN1", "MIN2", "DOT", "iterate_host_many"]
 
 MIN1, MIN2, DOT = 0, 1, 2  # DOT: regular product of Eq. (1), the RPI comparator
 (WS_MATVEC, WS_ITERATE, WS_ITERATE_BATCHED, WS_PCA_TOPK, WS_CSR_PREPARE, WS_RANK_CSR, WS_ITERATE_HOST,
- WS_MAVP_DEFLATE, WS_RECONSTRUCT, WS_ITERATE_SHARDED) = range(10)
+ WS_MAVP_DEFLATE, WS_RECONSTRUCT, WS_ITERATE_SHARDED, WS_ITERATE_HOST_MANY) = range(11)
 STATUS = {0: "MAPI_OK", 1: "MAPI_ERR_NULL", 2: "MAPI_ERR_SHAPE", 3: "MAPI_ERR_BAD_PARAM",
           4: "MAPI_ERR_DEGENERATE", 5: "MAPI_ERR_NEGATIVE", 6: "MAPI_ERR_NONFINITE",
           7: "MAPI_ERR_WORKSPACE", 8: "MAPI_ERR_CUDA"}
@@ -65,6 +65,7 @@ def load():
             "mapi_mavp_reconstruct": (st, [i32, P, i64, i32, i64, P, i64, i64, P, i64, P, P, sz, P]),
             "mapi_iterate": (st, [i32, P, i64, i64, P, i32, f32, P, P, P, P, P, P, sz, P]),
             "mapi_iterate_host": (st, [i32, P, i64, i64, P, i32, f32, P, P, P, P, P, P, sz, P]),
+            "mapi_iterate_host_many": (st, [i32, i32, P, i64, i64, P, i32, f32, P, P, P, P, P, sz, P]),
             "mapi_iterate_batched": (st, [i32, P, i64, i64, P, i32, i32, f32, P, P, P, P, P, sz, P]),
             "mapi_pca_topk": (st, [i32, P, i64, i64, i32, i32, P, P, P, P, P, sz, P]),
             "mapi_csr_prepare": (st, [i64, i64, P, P, f32, P, P, P, sz, P]),
@@ -305,6 +306,42 @@ def iterate_host(A_host, b0_host, iters: int, tol: float = 0.0, op: int = MIN1, 
     _check(st, done.value)
     k = done.value
     return IterResult(w, None, norms[:k], deltas[:k], k)
+
+
+def iterate_host_many(As, b0s, iters: int, tol: float = 0.0, op: int = MIN1, ws=None, outs=None,
+                      want_trace: bool = True, stream=None) -> list:
+    """`len(As)` independent MAPI problems from HOST buffers (pinned CPU tensors), pipelined: the next
+    problem's host->device copy overlaps the current one's iterations (mapi_iterate_host_many).  All
+    problems share n / lda.  Returns one IterResult per problem; synchronises the stream."""
+    torch = _torch()
+    count = len(As)
+    if count < 1 or len(b0s) != count:
+        raise ValueError("need >= 1 problem and one b0 per problem")
+    n, lda = As[0].shape[0], As[0].stride(0)
+    for A, b in zip(As, b0s):
+        if A.is_cuda or b.is_cuda or A.dtype != torch.float32 or A.dim() != 2 or A.stride(1) != 1:
+            raise ValueError("As must be 2-D row-major fp32 CPU tensors (pinned for overlap)")
+        if A.shape[0] != n or A.stride(0) != lda or b.numel() != n:
+            raise ValueError("every problem must have the same n and lda")
+    outs = outs if outs is not None else [torch.empty(n, dtype=torch.float32) for _ in range(count)]
+    pin = torch.cuda.is_available()
+    norms = [torch.zeros(iters, dtype=torch.float32, pin_memory=pin) for _ in range(count)] if want_trace else None
+    deltas = [torch.zeros(iters, dtype=torch.float32, pin_memory=pin) for _ in range(count)] if want_trace else None
+    lib = load()
+    need = int(lib.mapi_workspace_size(WS_ITERATE_HOST_MANY, n, lda, iters)) + 8 * max(0, count - 2)
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(need, dtype=torch.uint8, device="cuda")
+    arr = lambda ts: (ctypes.c_void_p * count)(*[t.data_ptr() for t in ts])  # noqa: E731
+    done = (ctypes.c_int32 * count)()
+    st = lib.mapi_iterate_host_many(op, count, arr(As), n, lda, arr(b0s), int(iters), float(tol), arr(outs),
+                                    arr(norms) if norms else None, arr(deltas) if deltas else None, done,
+                                    _ptr(ws), ws.numel(), _stream(stream))
+    _check(st)
+    res = []
+    for i in range(count):
+        k = done[i]
+        res.append(IterResult(outs[i], None, norms[i][:k] if norms else None, deltas[i][:k] if deltas else None, k))
+    return res
 
 
 @dataclass

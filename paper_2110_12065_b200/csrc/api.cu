@@ -9,6 +9,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <type_traits>
+#include <vector>
 
 #include "../../include/mapi.h"
 #include "batched.cuh"
@@ -531,6 +532,14 @@ uint64_t mapi_launch_count(void) { return g_launches.load(); }
 void mapi_set_profiling(int32_t enable) { g_profiling.store(enable ? 1 : 0); }
 float mapi_last_kernel_ms(void) { return g_last_kernel_ms; }
 
+// count independent host problems, pipelined: problem i+1's A / b0 host->device copies (a second, copy
+// stream) overlap problem i's iterations (the compute stream); two device slots alternate.
+size_t iterate_host_many_ws_bytes(int64_t n, int64_t lda, int32_t iters, int32_t count) {
+    const size_t slot = align256(sizeof(float) * (size_t)n * (size_t)lda) + 2 * align256(sizeof(float) * (size_t)n) +
+                        2 * align256(sizeof(float) * (size_t)std::max(iters, 1));
+    return iterate_ws_bytes(n) + 2 * slot + sizeof(int32_t) * 2 * (size_t)std::max(count, 2);
+}
+
 size_t mapi_workspace_size(int32_t op, int64_t n, int64_t nnz, int32_t k) {
     if (n < 0) n = 0;
     if (nnz < 0) nnz = 0;
@@ -551,6 +560,7 @@ size_t mapi_workspace_size(int32_t op, int64_t n, int64_t nnz, int32_t k) {
     case MAPI_WS_CSR_PREPARE: return csr_prepare_ws_bytes(n, nnz);
     case MAPI_WS_RANK_CSR: return csr_rank_ws_bytes(n, nnz);
     case MAPI_WS_ITERATE_SHARDED: return 256;
+    case MAPI_WS_ITERATE_HOST_MANY: return iterate_host_many_ws_bytes(n, nnz, k, 2);
     }
     return 0;
 }
@@ -720,6 +730,111 @@ mapi_status mapi_iterate_host(int32_t op, const float* A_host, int64_t n, int64_
     st = read_status(W, s, iters_done);
     timer.harvest();
     return st;
+}
+
+mapi_status mapi_iterate_host_many(int32_t op, int32_t count, const float* const* A_hosts, int64_t n, int64_t lda,
+                                   const float* const* b0_hosts, int32_t iters, float tol, float* const* w_out_hosts,
+                                   float* const* norms_hosts, float* const* deltas_hosts, int32_t* iters_done,
+                                   void* ws, size_t ws_bytes, mapi_stream_t stream) {
+    if (count < 1) return fail(MAPI_ERR_BAD_PARAM, "count (%d) must be >= 1", count);
+    if (!A_hosts || !b0_hosts || !w_out_hosts) return fail(MAPI_ERR_NULL, "A_hosts / b0_hosts / w_out_hosts is NULL");
+    for (int32_t i = 0; i < count; ++i) {
+        mapi_status st = validate_dense(op, A_hosts[i], n, lda, b0_hosts[i], iters, tol, w_out_hosts[i], ws);
+        if (st != MAPI_OK) return fail(st, "problem %d: %s", i, g_err);
+    }
+    const size_t need = iterate_host_many_ws_bytes(n, lda, iters, count);
+    if (ws_bytes < need) return fail(MAPI_ERR_WORKSPACE, "ws_bytes (%zu) < required (%zu)", ws_bytes, need);
+    Device d;
+    mapi_status st = device_info(d);
+    if (st != MAPI_OK) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    char* p = static_cast<char*>(ws);
+    IterWs W = carve_iterate(p, n);
+    p += iterate_ws_bytes(n);
+    struct Slot {
+        float *A, *b0, *w, *nrm, *dlt;
+    } sl[2];
+    for (auto& x : sl) {
+        x.A = reinterpret_cast<float*>(p);
+        p += align256(sizeof(float) * (size_t)n * (size_t)lda);
+        x.b0 = reinterpret_cast<float*>(p);
+        p += align256(sizeof(float) * (size_t)n);
+        x.w = reinterpret_cast<float*>(p);
+        p += align256(sizeof(float) * (size_t)n);
+        x.nrm = reinterpret_cast<float*>(p);
+        p += align256(sizeof(float) * (size_t)std::max(iters, 1));
+        x.dlt = reinterpret_cast<float*>(p);
+        p += align256(sizeof(float) * (size_t)std::max(iters, 1));
+    }
+    int32_t* st_all = reinterpret_cast<int32_t*>(p);
+    cudaStream_t cs = nullptr;
+    cudaEvent_t loaded[2] = {nullptr, nullptr}, freed[2] = {nullptr, nullptr};
+    auto cleanup = [&]() {
+        for (int j = 0; j < 2; ++j) {
+            if (loaded[j]) cudaEventDestroy(loaded[j]);
+            if (freed[j]) cudaEventDestroy(freed[j]);
+        }
+        if (cs) cudaStreamDestroy(cs);
+    };
+    cudaError_t e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+    for (int j = 0; j < 2 && e == cudaSuccess; ++j) {
+        e = cudaEventCreateWithFlags(&loaded[j], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&freed[j], cudaEventDisableTiming);
+    }
+    // the copy stream starts after everything already queued on the caller's stream
+    if (e == cudaSuccess) e = cudaEventRecord(freed[1], s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, freed[1], 0);
+    if (e != cudaSuccess) {
+        cleanup();
+        return fail(MAPI_ERR_CUDA, "stream / event setup: %s", cudaGetErrorString(e));
+    }
+    Timer timer(s);
+    timer.start();
+    // copy of problem i into slot i & 1 on the copy stream, after problem i-2 released that slot
+    auto issue_copy = [&](int32_t i) {
+        Slot& x = sl[i & 1];
+        cudaError_t r = cudaSuccess;
+        if (i >= 2) r = cudaStreamWaitEvent(cs, freed[i & 1], 0);
+        if (r == cudaSuccess)
+            r = cudaMemcpyAsync(x.A, A_hosts[i], sizeof(float) * (size_t)n * (size_t)lda, cudaMemcpyHostToDevice, cs);
+        if (r == cudaSuccess) r = cudaMemcpyAsync(x.b0, b0_hosts[i], sizeof(float) * (size_t)n, cudaMemcpyHostToDevice, cs);
+        if (r == cudaSuccess) r = cudaEventRecord(loaded[i & 1], cs);
+        return r;
+    };
+    e = issue_copy(0);
+    for (int32_t i = 0; i < count && st == MAPI_OK && e == cudaSuccess; ++i) {
+        Slot& x = sl[i & 1];
+        e = cudaStreamWaitEvent(s, loaded[i & 1], 0);
+        if (e != cudaSuccess) break;
+        st = iterate_launch(d, op, x.A, n, lda, x.b0, iters, tol, x.w, x.nrm, x.dlt, W, s, nullptr);
+        if (st != MAPI_OK) break;
+        // queue the next problem's copy before this one's read-back (a pageable read-back may block the host)
+        if (i + 1 < count && (e = issue_copy(i + 1)) != cudaSuccess) break;
+        e = cudaMemcpyAsync(st_all + 2 * i, W.status, 2 * sizeof(int32_t), cudaMemcpyDeviceToDevice, s);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(w_out_hosts[i], x.w, sizeof(float) * (size_t)n, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess && norms_hosts && norms_hosts[i])
+            e = cudaMemcpyAsync(norms_hosts[i], x.nrm, sizeof(float) * (size_t)iters, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess && deltas_hosts && deltas_hosts[i])
+            e = cudaMemcpyAsync(deltas_hosts[i], x.dlt, sizeof(float) * (size_t)iters, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaEventRecord(freed[i & 1], s);
+    }
+    timer.stop();
+    if (e != cudaSuccess && st == MAPI_OK) st = fail(MAPI_ERR_CUDA, "pipelined host iterate: %s", cudaGetErrorString(e));
+    std::vector<int32_t> h(2 * (size_t)count, 0);
+    cudaError_t e2 = cudaMemcpyAsync(h.data(), st_all, sizeof(int32_t) * 2 * (size_t)count, cudaMemcpyDeviceToHost, s);
+    if (e2 == cudaSuccess) e2 = cudaStreamSynchronize(s);
+    cleanup();
+    if (st != MAPI_OK) return st;
+    if (e2 != cudaSuccess) return fail(MAPI_ERR_CUDA, "status read-back: %s", cudaGetErrorString(e2));
+    timer.harvest();
+    for (int32_t i = 0; i < count; ++i) {
+        if (iters_done) iters_done[i] = h[2 * i + 1];
+        if (h[2 * i] != 0)
+            return fail((mapi_status)h[2 * i], "problem %d: %s at iteration %d", i,
+                        h[2 * i] == MAPI_ERR_DEGENERATE ? "||A (op) w||_1 == 0" : "non-finite norm", h[2 * i + 1]);
+    }
+    return MAPI_OK;
 }
 
 mapi_status mapi_pca_topk(int32_t op, const float* C, int64_t n, int64_t ldc, int32_t k, int32_t iters,

@@ -361,3 +361,25 @@ def test_matvec_dot(mapi_lib, orc):
     y = m.mavp_matvec(torch.from_numpy(M).cuda(), torch.from_numpy(x).cuda(), op=m.DOT).cpu().numpy()
     ref, mag = orc.matvec(M, x, "dot", return_mag=True)
     assert np.all(np.abs(y - ref) <= 1e-5 * mag)
+
+
+def test_iterate_host_many_pipelined(mapi_lib):
+    """Pipelined host problems (copy stream overlapping the previous problem's iterations): every
+    result equals the one-problem host path bitwise, distinct inputs stay distinct, iters_done per
+    problem, and a degenerate problem reports its index."""
+    m = mapi_lib
+    n = 2048
+    r = np.random.default_rng(8)
+    As = [torch.from_numpy((r.standard_normal((n, n)) + np.eye(n) * (2 + i)).astype(np.float32)).pin_memory()
+          for i in range(5)]
+    b0s = [torch.full((n,), 1 / np.sqrt(n)).pin_memory() for _ in range(5)]
+    res = m.iterate_host_many(As, b0s, 20)
+    for A, b0, got in zip(As, b0s, res):
+        one = m.iterate_host(A, b0, 20)
+        assert got.iters_done == 20
+        assert torch.equal(got.w, one.w) and torch.equal(got.norms, one.norms) and torch.equal(got.deltas, one.deltas)
+    assert not torch.equal(res[0].w, res[1].w)
+    bad = [As[0], torch.zeros(n, n).pin_memory(), As[2]]
+    with pytest.raises(m.MapiError) as ei:
+        m.iterate_host_many(bad, b0s[:3], 5)
+    assert ei.value.name == "MAPI_ERR_DEGENERATE" and "problem 1" in str(ei.value)
