@@ -165,6 +165,15 @@ __global__ void __launch_bounds__(kBulkThreads, 1) k_iterate_bulk(IterArgs p, in
         double* slots_g = reinterpret_cast<double*>(p.slots);
         if (tid == 0) slots_g[(t & 1) * gridDim.x + blockIdx.x] = cta_abs;
         grid_barrier(p.bar, (unsigned int)(t + 1) * gridDim.x);  // the issued copies keep flowing
+        // the y loads of the normalisation do not depend on s_t: issue them together with the slot
+        // loads (one L2 round trip after the barrier instead of two)
+        constexpr int YR = 16;  // y values held per thread (n <= 8192 with 512 threads); the rest streams
+        float yr[YR];
+#pragma unroll
+        for (int q = 0; q < YR; ++q) {
+            const int64_t k = tid + (int64_t)q * kBulkThreads;
+            yr[q] = k < n ? __ldcg(y + k) : 0.0f;
+        }
         // s_t in the same fixed fp64 order in every CTA
         double s;
         {
@@ -184,7 +193,16 @@ __global__ void __launch_bounds__(kBulkThreads, 1) k_iterate_bulk(IterArgs p, in
         }
         // w_{t+1} = fp32(y / s_t) (fp64 division), delta_t in fp64
         double dpart = 0.0;
-        for (int64_t k = tid; k < n; k += blockDim.x) {
+#pragma unroll
+        for (int q = 0; q < YR; ++q) {
+            const int64_t k = tid + (int64_t)q * kBulkThreads;
+            if (k < n) {
+                const float wn = (float)((double)yr[q] / s);
+                dpart += (double)fabsf(wn - w_s[k]);
+                w_s[k] = wn;
+            }
+        }
+        for (int64_t k = tid + (int64_t)YR * kBulkThreads; k < n; k += blockDim.x) {
             const float wn = (float)((double)__ldcg(y + k) / s);
             dpart += (double)fabsf(wn - w_s[k]);
             w_s[k] = wn;
