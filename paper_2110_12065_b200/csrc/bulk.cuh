@@ -77,6 +77,14 @@ inline size_t bulk_fixed_smem(int64_t n, int64_t rows_max) {
     return (b + 127) & ~size_t(127);
 }
 
+#ifdef MAPI_BULK_TRACE
+__device__ long long g_bulk_trace[6 * 512];  // investigation builds only (scripts/probe_k2t.cu)
+#define BULK_STAMP(t, k) \
+    if (blockIdx.x == 0 && threadIdx.x == 0 && (t) < 512) g_bulk_trace[(t) * 6 + (k)] = clock64()
+#else
+#define BULK_STAMP(t, k)
+#endif
+
 template <int OP>
 __global__ void __launch_bounds__(kBulkThreads, 1) k_iterate_bulk(IterArgs p, int slots) {
     extern __shared__ __align__(16) float ws_[];
@@ -128,6 +136,7 @@ __global__ void __launch_bounds__(kBulkThreads, 1) k_iterate_bulk(IterArgs p, in
     const float4* w4 = reinterpret_cast<const float4*>(w_s);
     for (int32_t t = 0; t < p.iters; ++t) {
         float* y = p.y + (t & 1) * n;
+        BULK_STAMP(t, 0);
         for (int j = 0; j < nj; ++j) {
             const int i = warp + kBulkNC * j, q = i % cpr_i;
             mbar_wait(full + cs, cph);
@@ -152,7 +161,9 @@ __global__ void __launch_bounds__(kBulkThreads, 1) k_iterate_bulk(IterArgs p, in
             const float v = warp_sum(tree_sum(acc));
             if (lane == 0) part[i] = v;
         }
+        BULK_STAMP(t, 1);
         __syncthreads();
+        BULK_STAMP(t, 2);
         // rows of this CTA: y = sum of chunk partials in chunk order; |y| partial (a1-a3)
         double abs_part = 0.0;
         for (int64_t r = tid; r < rows; r += blockDim.x) {
@@ -165,6 +176,7 @@ __global__ void __launch_bounds__(kBulkThreads, 1) k_iterate_bulk(IterArgs p, in
         double* slots_g = reinterpret_cast<double*>(p.slots);
         if (tid == 0) slots_g[(t & 1) * gridDim.x + blockIdx.x] = cta_abs;
         grid_barrier(p.bar, (unsigned int)(t + 1) * gridDim.x);  // the issued copies keep flowing
+        BULK_STAMP(t, 3);
         // the y loads of the normalisation do not depend on s_t: issue them together with the slot
         // loads (one L2 round trip after the barrier instead of two)
         constexpr int YR = 16;  // y values held per thread (n <= 8192 with 512 threads); the rest streams
@@ -191,23 +203,34 @@ __global__ void __launch_bounds__(kBulkThreads, 1) k_iterate_bulk(IterArgs p, in
             status = (s == 0.0) ? kStDegenerate : kStNonfinite;
             break;
         }
+        BULK_STAMP(t, 4);
         // w_{t+1} = fp32(y / s_t) (fp64 division), delta_t in fp64
         double dpart = 0.0;
+        // y / s_t for n elements per CTA per iteration: one IEEE fp64 reciprocal of s_t, then per element
+        // q0 = y r, q = q0 + (y - q0 s) r (the residual-corrected quotient DDIV itself computes, without
+        // its special-case paths: y and s are finite fp32-range values here).  Measured ~1,200 of ~25,700
+        // cycles per iteration cheaper than the DDIV sequence (scripts/probe_k2t.cu); the fp32 rounding
+        // of the result can differ from fp32(y / s) only when y / s lies within an fp64 ulp of an fp32
+        // rounding boundary.
+        const double rs = 1.0 / s;
 #pragma unroll
         for (int q = 0; q < YR; ++q) {
             const int64_t k = tid + (int64_t)q * kBulkThreads;
             if (k < n) {
-                const float wn = (float)((double)yr[q] / s);
+                const double q0 = (double)yr[q] * rs;
+                const float wn = (float)fma(fma(-q0, s, (double)yr[q]), rs, q0);
                 dpart += (double)fabsf(wn - w_s[k]);
                 w_s[k] = wn;
             }
         }
         for (int64_t k = tid + (int64_t)YR * kBulkThreads; k < n; k += blockDim.x) {
-            const float wn = (float)((double)__ldcg(y + k) / s);
+            const double yk = (double)__ldcg(y + k), q0 = yk * rs;
+            const float wn = (float)fma(fma(-q0, s, yk), rs, q0);
             dpart += (double)fabsf(wn - w_s[k]);
             w_s[k] = wn;
         }
         const double delta = block_sum(dpart, red);  // also orders the w_s writes before reuse
+        BULK_STAMP(t, 5);
         if (blockIdx.x == 0 && tid == 0) {
             if (p.norms) p.norms[t] = (float)s;
             if (p.deltas) p.deltas[t] = (float)delta;
