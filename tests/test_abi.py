@@ -84,6 +84,40 @@ def test_validation_before_device(lib):
     assert st == 3 and "max_iters" in _err(lib)
     st = lib.mapi_iterate_batched(0, fake, 8, 8, fake, 0, 5, 0.0, fake, None, None, None, fake, 1 << 30, None)
     assert st == 3 and "k (0)" in _err(lib)
+    # fused P2P sharding (K2p): argument checks before any CUDA call
+    sh = lambda **kw: lib.mapi_iterate_sharded(  # noqa: E731
+        kw.get("op", 0), kw.get("A", fake), kw.get("m", 256), kw.get("n", 512), kw.get("lda", 512),
+        kw.get("row0", 0), fake, kw.get("iters", 5), kw.get("tol", 0.0), kw.get("rank", 0), kw.get("world", 2),
+        kw.get("peers", fake), 0, 0, fake, None, None, None, None, None, fake, kw.get("ws_bytes", 256), None)
+    assert sh(peers=None) == 1 and "NULL" in _err(lib)
+    assert sh(world=0) == 3 and "world" in _err(lib)
+    assert sh(rank=2) == 3 and "rank 2" in _err(lib)
+    assert sh(n=128, m=64, lda=128) == 2 and "n >= 256" in _err(lib)
+    assert sh(row0=300) == 2
+    assert sh(lda=516) == 2 and "32 B-aligned" in _err(lib)
+    assert sh(iters=0) == 3 and "iters" in _err(lib)
+    assert sh(ws_bytes=16) == 7
+    assert sh(op=5) == 3
+    # pipelined host problems
+    arr = (ctypes.c_void_p * 1)(fake.value)
+    st = lib.mapi_iterate_host_many(0, 0, arr, 4, 4, arr, 5, 0.0, arr, None, None, None, fake, 1 << 20, None)
+    assert st == 3 and "count" in _err(lib)
+    st = lib.mapi_iterate_host_many(0, 1, None, 4, 4, arr, 5, 0.0, arr, None, None, None, fake, 1 << 20, None)
+    assert st == 1
+    st = lib.mapi_iterate_host_many(0, 1, arr, 4, 4, arr, 5, 0.0, arr, None, None, None, fake, 16, None)
+    assert st == 7
+
+
+def test_p2p_exchange_layout_and_new_workspaces(lib):
+    """Exchange buffer = 256 B flag header + y for two parities + fp64 partial slots (2 x world x 1024)."""
+    al = lambda b: (b + 255) // 256 * 256  # noqa: E731
+    for n, world in ((4096, 2), (32768, 8), (1000, 1)):
+        assert lib.mapi_p2p_exchange_bytes(n, world) == 256 + al(8 * n) + al(16 * world * 1024)
+    assert lib.mapi_p2p_exchange_bytes(100, 0) == 0
+    assert lib.mapi_workspace_size(m.WS_ITERATE_SHARDED, 0, 0, 0) == 256
+    one = lib.mapi_workspace_size(m.WS_ITERATE_HOST, 1024, 1024, 50)
+    many = lib.mapi_workspace_size(m.WS_ITERATE_HOST_MANY, 1024, 1024, 50)
+    assert many > one and many >= 2 * 4 * 1024 * 1024  # two A slots
 
 
 def _sass_functions():
