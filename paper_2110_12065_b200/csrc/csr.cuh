@@ -407,9 +407,8 @@ __global__ void __launch_bounds__(256) k_rank_fixup(int64_t tiles, const int32_t
                                                     double* __restrict__ slotY, const int32_t* stop) {
     __shared__ double red[33];
     if (*(volatile const int32_t*)stop) return;
-    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    double g = 0.0;
-    if (c < tiles) {
+    double g = 0.0;  // grid-stride over tiles: any graph size with a bounded grid
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < tiles; c += (int64_t)gridDim.x * blockDim.x) {
 #pragma unroll
         for (int q = 0; q < kMpWarps; ++q) g += gsum[c * kMpWarps + q];
         const int32_t r = carry_row[c];
@@ -582,11 +581,7 @@ inline mapi_status csr_rank_run(int64_t n, int64_t nnz, const int32_t* row_ptr, 
     // 16 B vector path for the node arrays when the caller's b0 / bg / cap are 16 B aligned
     const bool v4 = (reinterpret_cast<uintptr_t>(bg) % 16 == 0) && (reinterpret_cast<uintptr_t>(cap) % 16 == 0) &&
                     (reinterpret_cast<uintptr_t>(b0) % 16 == 0);
-    const int gfix = (int)((T + 255) / 256);
-    if (gfix > kCsrMaxGrid) {
-        snprintf(g_csr_err, sizeof(g_csr_err), "graph too large: %lld merge tiles", (long long)T);
-        return MAPI_ERR_SHAPE;
-    }
+    const int gfix = (int)std::min<int64_t>((T + 255) / 256, kCsrMaxGrid);
     k_mp_partition<<<(unsigned)((T + 1 + 255) / 256), 256, 0, s>>>(n, nnz, row_ptr, T, W.part_i, W.part_k);
     launches.fetch_add(1, std::memory_order_relaxed);
     if (ev_a) cudaEventRecord(*ev_a, s);
