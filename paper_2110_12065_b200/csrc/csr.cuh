@@ -149,6 +149,15 @@ inline CsrWs carve_csr(void* ws, int64_t n, int64_t nnz) {
     return c;
 }
 
+// x / d for the n node quotients of an iteration, given rd = 1/d (one IEEE fp64 division per CTA):
+// q0 = x rd, q = q0 + (x - q0 d) rd — the residual-corrected quotient DDIV itself computes, without its
+// special-case paths (x, d are finite and normal here); used by every kernel that forms w so that a
+// recomputed w_t is bit-identical to the one formed the iteration before.
+__device__ __forceinline__ double qdiv(double x, double d, double rd) {
+    const double q0 = x * rd;
+    return fma(fma(-q0, d, x), rd, q0);
+}
+
 // v_j = min(max(w_j - bg_j, 0), cap_j) = min(bg+cap, w) - min(bg, w)   (exact identity, F7)
 __device__ __forceinline__ float csr_v(double w, float bg, float cap) {
     return (float)fmin(fmax(w - (double)bg, 0.0), (double)cap);
@@ -427,7 +436,7 @@ __global__ void __launch_bounds__(256) k_rank_fixup(int64_t tiles, const int32_t
 // last CTA to finish (counter) sums the delta partials in slot order and writes delta_t, the trace,
 // iters_done and the stop flag.  (One fp64 product n*S per iteration: the l1 norm of the background.)
 template <bool V4>
-__global__ void __launch_bounds__(kCsrThreads) k_rank_normalize(
+__global__ void __launch_bounds__(kCsrThreads, 4) k_rank_normalize(
     int64_t n, const float* __restrict__ e, const float* __restrict__ e_prev, const float* __restrict__ b0,
     double* __restrict__ hist, const double* __restrict__ slotS_cur, double* __restrict__ slotS_next, int nS,
     const double* __restrict__ slotY, int nY, const float* __restrict__ bg, const float* __restrict__ cap,
@@ -449,7 +458,8 @@ __global__ void __launch_bounds__(kCsrThreads) k_rank_normalize(
     // w_old = w_t: b0 at t = 0, else (S_{t-1} + e_{t-1}) / s_{t-1} exactly as the last launch formed it
     const bool first = e_prev == nullptr;
     const double Sp = first ? 0.0 : hist[(t & 1) * 2], sp_ = first ? 1.0 : hist[(t & 1) * 2 + 1];
-    auto w_old = [&](int64_t j, float ep) -> double { return first ? (double)b0[j] : (Sp + (double)ep) / sp_; };
+    const double rs = 1.0 / s, rsp = 1.0 / sp_;
+    auto w_old = [&](int64_t j, float ep) -> double { return first ? (double)b0[j] : qdiv(Sp + (double)ep, sp_, rsp); };
     double dp = 0.0, sn = 0.0;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     int64_t j0 = 0;
@@ -479,8 +489,8 @@ __global__ void __launch_bounds__(kCsrThreads) k_rank_normalize(
                 float vn[4];
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
-                    const double wn = (S + (double)ee[i]) / s;
-                    const double wo = first ? (double)pp[i] : (Sp + (double)pp[i]) / sp_;
+                    const double wn = qdiv(S + (double)ee[i], s, rs);
+                    const double wo = first ? (double)pp[i] : qdiv(Sp + (double)pp[i], sp_, rsp);
                     dp += fabs(wn - wo);
                     vn[i] = csr_v(wn, bb[i], cc[i]);
                     sn += fmin((double)bb[i], wn);
@@ -491,7 +501,7 @@ __global__ void __launch_bounds__(kCsrThreads) k_rank_normalize(
         j0 = groups * 4;
     }
     for (int64_t j = j0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride) {
-        const double wn = (S + (double)e[j]) / s;
+        const double wn = qdiv(S + (double)e[j], s, rs);
         dp += fabs(wn - w_old(j, first ? 0.0f : e_prev[j]));
         const float b = bg[j];
         v[j] = csr_v(wn, b, cap[j]);
@@ -546,9 +556,10 @@ __global__ void __launch_bounds__(kCsrThreads) k_rank_output(int64_t n, const fl
                                                             float* __restrict__ w_out, double* __restrict__ slotQ) {
     __shared__ double red[33];
     const RankLast L = rank_last(e0, e1, hist, status);
+    const double rls = 1.0 / L.s;
     double part = 0.0;
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
-        const double x = L.none ? (double)b0[j] : (L.S + (double)L.e[j]) / L.s;
+        const double x = L.none ? (double)b0[j] : qdiv(L.S + (double)L.e[j], L.s, rls);
         w_out[j] = (float)x;
         part = fma(x, x, part);
     }
@@ -562,9 +573,10 @@ __global__ void __launch_bounds__(kCsrThreads) k_rank_output_l2(int64_t n, const
                                                                float* __restrict__ w_l2) {
     __shared__ double red[33];
     const RankLast L = rank_last(e0, e1, hist, status);
+    const double rls = 1.0 / L.s;
     const double l2 = sqrt(slots_sum(slotQ, nq, red));
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
-        const double x = L.none ? (double)b0[j] : (L.S + (double)L.e[j]) / L.s;
+        const double x = L.none ? (double)b0[j] : qdiv(L.S + (double)L.e[j], L.s, rls);
         w_l2[j] = l2 > 0.0 ? (float)(x / l2) : 0.0f;
     }
 }
