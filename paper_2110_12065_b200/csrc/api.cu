@@ -642,6 +642,28 @@ mapi_status mapi_mavp_matmat(int32_t op, const float* A, int64_t m, int64_t K, i
     if (!A || !B) return fail(MAPI_ERR_NULL, "A or B is NULL");
     Device d;
     if ((st = device_info(d)) != MAPI_OK) return st;
+    const char* mp = getenv("MAPI_MATMAT_PATH");  // "tiled" forces K8 for small K (tests / comparison)
+    if (K <= 12 && !(mp && strcmp(mp, "tiled") == 0)) {
+        using KernT = void (*)(const float*, int64_t, int, int64_t, const float*, int64_t, int64_t, float, float*,
+                               int64_t);
+        KernT kern = K <= 4 ? (op == 1 ? k_mavp_matmat_smallk<1, 4> : k_mavp_matmat_smallk<0, 4>)
+                   : K <= 8 ? (op == 1 ? k_mavp_matmat_smallk<1, 8> : k_mavp_matmat_smallk<0, 8>)
+                            : (op == 1 ? k_mavp_matmat_smallk<1, 12> : k_mavp_matmat_smallk<0, 12>);
+        int occ = 1;
+        MAPI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kMsThreads, 0));
+        const int64_t units = ((m + kMsI - 1) / kMsI) * ((p + kMsJ - 1) / kMsJ);
+        const unsigned grid = (unsigned)std::min<int64_t>(units, (int64_t)std::max(occ, 1) * d.sms);
+        Timer timer(s);
+        timer.start();
+        kern<<<grid, kMsThreads, 0, s>>>(A, m, (int)K, lda, B, p, ldb, divisor, C, ldc);
+        timer.stop();
+        MAPI_LAUNCHED();
+        if (timer.on) {
+            MAPI_CUDA(cudaStreamSynchronize(s));
+            timer.harvest();
+        }
+        return MAPI_OK;
+    }
     const bool async = reinterpret_cast<uintptr_t>(A) % 16 == 0 && reinterpret_cast<uintptr_t>(B) % 16 == 0 &&
                        lda % 4 == 0 && ldb % 4 == 0 && K % 4 == 0;  // 16 B chunks never cross K
     const int64_t ntiles = ((p + kMmJ - 1) / kMmJ) * ((m + kMmI - 1) / kMmI);

@@ -172,4 +172,106 @@ __global__ void __launch_bounds__(kMmThreads, 1) k_mavp_matmat(const float* __re
     cp_async_wait<0>();
 }
 
+// ---------------------------------------------------------------------------------------------
+// K8s: small K (K <= 12 — the paper's N = 10 samples; Alg. 2 step 4 on 128^2-pixel images gives a
+// 16384^2 C from only 10 terms per element).  There the tiled kernel is bound by its per-element
+// staging (4 B cp.async per value) and by 1 CTA/SM of 234-register threads (ncu: issue 49%, warps
+// active 12.5%, "wait" stalls), not by the 10 FMNMX per output.  K8s keeps a 256-column j-tile of B in
+// REGISTERS (lane owns columns j0 + lane + 32 jj, jj < 8: 8 x KP values) and sweeps 32-row i-tiles of
+// A through a double-buffered shared-memory stage (32 x K floats, warp-broadcast reads): per output
+// K terms (FMNMX.XORSIGN, FADD2 over column pairs), the 1/d scale and one coalesced store.  Units =
+// (j-tile, i-tile) in j-major order split evenly over a persistent grid, so a CTA reloads B only when
+// its range crosses a j-tile.  Per element the k order is ascending from 0, as in K8 for K <= 32: the
+// two kernels give bitwise-identical C (tested).
+constexpr int kMsI = 32, kMsJ = 256, kMsThreads = 256;
+
+template <int OP, int KP>
+__global__ void __launch_bounds__(kMsThreads, 1) k_mavp_matmat_smallk(const float* __restrict__ A, int64_t m, int K,
+                                                                    int64_t lda, const float* __restrict__ B,
+                                                                    int64_t p, int64_t ldb, float d,
+                                                                    float* __restrict__ C, int64_t ldc) {
+    __shared__ float As[2][kMsI][KP];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t ni = (m + kMsI - 1) / kMsI, nj = (p + kMsJ - 1) / kMsJ, units = ni * nj;
+    const int64_t u0 = units * blockIdx.x / gridDim.x, u1 = units * (blockIdx.x + 1) / gridDim.x;
+    if (u0 >= u1) return;
+    const float inv_d = 1.0f / d;
+    float breg[8][KP];
+    int64_t cur_jt = -1;
+    // A stage of unit u into registers (<= 2 values per thread: 32 x K <= 384 floats)
+    float ar[2];
+    auto load_a = [&](int64_t u) {
+        const int64_t i0 = (u % ni) * kMsI;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int idx = tid + h * kMsThreads;
+            const int r = idx / K, k = idx - r * K;
+            ar[h] = (idx < kMsI * K && i0 + r < m) ? __ldg(A + (i0 + r) * lda + k) : 0.0f;
+        }
+    };
+    auto store_a = [&](int buf) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int idx = tid + h * kMsThreads;
+            if (idx < kMsI * K) {
+                const int r = idx / K, k = idx - r * K;
+                As[buf][r][k] = ar[h];
+            }
+        }
+    };
+    load_a(u0);
+    store_a(0);
+    __syncthreads();
+    int buf = 0;
+    for (int64_t u = u0; u < u1; ++u) {
+        const int64_t jt = u / ni, i0 = (u % ni) * kMsI, j0 = jt * kMsJ;
+        if (jt != cur_jt) {  // (re)load this j-tile's B columns into registers
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj) {
+                const int64_t j = j0 + lane + 32 * jj;
+#pragma unroll
+                for (int k = 0; k < KP; ++k) breg[jj][k] = (j < p && k < K) ? __ldg(B + j * ldb + k) : 0.0f;
+            }
+            cur_jt = jt;
+        }
+        if (u + 1 < u1) load_a(u + 1);  // next stage in flight during this unit's compute
+        unsigned long long acc[4][4];
+#pragma unroll
+        for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+            for (int jp = 0; jp < 4; ++jp) acc[ii][jp] = 0ull;
+#pragma unroll
+        for (int k = 0; k < KP; ++k) {
+            if (k < K) {
+#pragma unroll
+                for (int ii = 0; ii < 4; ++ii) {
+                    const float a = As[buf][warp + 8 * ii][k];
+#pragma unroll
+                    for (int jp = 0; jp < 4; ++jp)
+                        acc[ii][jp] = fadd2(acc[ii][jp], pack2(mavp_term<OP>(a, breg[2 * jp][k]),
+                                                               mavp_term<OP>(a, breg[2 * jp + 1][k])));
+                }
+            }
+        }
+#pragma unroll
+        for (int ii = 0; ii < 4; ++ii) {
+            const int64_t i = i0 + warp + 8 * ii;
+            if (i < m) {
+                float* crow = C + i * ldc;
+#pragma unroll
+                for (int jp = 0; jp < 4; ++jp) {
+                    const int64_t ja = j0 + lane + 64 * jp, jb = ja + 32;
+                    if (ja < p) crow[ja] = d == 1.0f ? lo_of(acc[ii][jp]) : inv_d * lo_of(acc[ii][jp]);
+                    if (jb < p) crow[jb] = d == 1.0f ? hi_of(acc[ii][jp]) : inv_d * hi_of(acc[ii][jp]);
+                }
+            }
+        }
+        if (u + 1 < u1) {
+            store_a(buf ^ 1);
+            __syncthreads();
+            buf ^= 1;
+        }
+    }
+}
+
 }  // namespace mapi

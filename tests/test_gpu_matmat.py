@@ -83,3 +83,22 @@ def test_min_covariance_large_K_symmetric(mapi_lib, orc):
     ref = orc.matmat(np.ascontiguousarray(V[rows]), V, "min1", 4096.0)
     mag = orc.matmat(np.ascontiguousarray(np.abs(V[rows])), np.abs(V), "min1", 4096.0)
     assert np.all(np.abs(Crow - ref) <= 1e-5 * mag + 1e-30)
+
+
+@pytest.mark.parametrize("m,p,K", [(1, 1, 1), (33, 257, 3), (64, 256, 4), (100, 300, 10), (97, 513, 12), (300, 70, 8)])
+@pytest.mark.parametrize("op", ["min1", "min2"])
+def test_small_k_kernel_bitwise_vs_tiled(mapi_lib, orc, monkeypatch, m, p, K, op):
+    """K8s (B columns in registers, K <= 12) accumulates every element in ascending k from 0, as K8
+    does for K <= 32: bitwise-identical C; both within T1 of the oracle; divisor applied."""
+    mm = mapi_lib
+    r = np.random.default_rng(m * 1000 + p + K)
+    A = r.standard_normal((m, K)).astype(np.float32)
+    B = r.standard_normal((p, K)).astype(np.float32)
+    opc = mm.MIN1 if op == "min1" else mm.MIN2
+    Ad, Bd = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    small = mm.mavp_matmat(Ad, Bd, 9.0, op=opc)
+    monkeypatch.setenv("MAPI_MATMAT_PATH", "tiled")
+    tiled = mm.mavp_matmat(Ad, Bd, 9.0, op=opc)
+    torch.cuda.synchronize()
+    assert torch.equal(small, tiled)
+    _check(small.cpu().numpy(), A, B, 9.0, orc, op)
