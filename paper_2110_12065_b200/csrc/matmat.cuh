@@ -183,27 +183,34 @@ __global__ void __launch_bounds__(kMmThreads, 1) k_mavp_matmat(const float* __re
 // (j-tile, i-tile) in j-major order split evenly over a persistent grid, so a CTA reloads B only when
 // its range crosses a j-tile.  Per element the k order is ascending from 0, as in K8 for K <= 32: the
 // two kernels give bitwise-identical C (tested).
-constexpr int kMsI = 32, kMsJ = 256, kMsThreads = 256;
+constexpr int kMsThreads = 256;
+#ifndef MAPI_MS_JJ
+#define MAPI_MS_JJ 4
+#endif
+constexpr int kMsJJ = MAPI_MS_JJ;          // B columns per lane (registers: kMsJJ x KP)
+constexpr int kMsII = 32 / kMsJJ;          // A rows per warp  (accumulators: kMsII x kMsJJ)
+constexpr int kMsI = 8 * kMsII, kMsJ = 32 * kMsJJ;
 
 template <int OP, int KP>
-__global__ void __launch_bounds__(kMsThreads, 1) k_mavp_matmat_smallk(const float* __restrict__ A, int64_t m, int K,
-                                                                    int64_t lda, const float* __restrict__ B,
-                                                                    int64_t p, int64_t ldb, float d,
-                                                                    float* __restrict__ C, int64_t ldc) {
+__global__ void __launch_bounds__(kMsThreads) k_mavp_matmat_smallk(const float* __restrict__ A, int64_t m, int K,
+                                                                 int64_t lda, const float* __restrict__ B,
+                                                                 int64_t p, int64_t ldb, float d,
+                                                                 float* __restrict__ C, int64_t ldc) {
+    constexpr int JP = kMsJJ / 2, AR = (kMsI * KP + kMsThreads - 1) / kMsThreads;
     __shared__ float As[2][kMsI][KP];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t ni = (m + kMsI - 1) / kMsI, nj = (p + kMsJ - 1) / kMsJ, units = ni * nj;
     const int64_t u0 = units * blockIdx.x / gridDim.x, u1 = units * (blockIdx.x + 1) / gridDim.x;
     if (u0 >= u1) return;
     const float inv_d = 1.0f / d;
-    float breg[8][KP];
+    float breg[kMsJJ][KP];
     int64_t cur_jt = -1;
-    // A stage of unit u into registers (<= 2 values per thread: 32 x K <= 384 floats)
-    float ar[2];
+    // A stage of unit u into registers (AR values per thread: kMsI x K floats)
+    float ar[AR];
     auto load_a = [&](int64_t u) {
         const int64_t i0 = (u % ni) * kMsI;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < AR; ++h) {
             const int idx = tid + h * kMsThreads;
             const int r = idx / K, k = idx - r * K;
             ar[h] = (idx < kMsI * K && i0 + r < m) ? __ldg(A + (i0 + r) * lda + k) : 0.0f;
@@ -211,7 +218,7 @@ __global__ void __launch_bounds__(kMsThreads, 1) k_mavp_matmat_smallk(const floa
     };
     auto store_a = [&](int buf) {
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < AR; ++h) {
             const int idx = tid + h * kMsThreads;
             if (idx < kMsI * K) {
                 const int r = idx / K, k = idx - r * K;
@@ -227,7 +234,7 @@ __global__ void __launch_bounds__(kMsThreads, 1) k_mavp_matmat_smallk(const floa
         const int64_t jt = u / ni, i0 = (u % ni) * kMsI, j0 = jt * kMsJ;
         if (jt != cur_jt) {  // (re)load this j-tile's B columns into registers
 #pragma unroll
-            for (int jj = 0; jj < 8; ++jj) {
+            for (int jj = 0; jj < kMsJJ; ++jj) {
                 const int64_t j = j0 + lane + 32 * jj;
 #pragma unroll
                 for (int k = 0; k < KP; ++k) breg[jj][k] = (j < p && k < K) ? __ldg(B + j * ldb + k) : 0.0f;
@@ -235,31 +242,31 @@ __global__ void __launch_bounds__(kMsThreads, 1) k_mavp_matmat_smallk(const floa
             cur_jt = jt;
         }
         if (u + 1 < u1) load_a(u + 1);  // next stage in flight during this unit's compute
-        unsigned long long acc[4][4];
+        unsigned long long acc[kMsII][JP];
 #pragma unroll
-        for (int ii = 0; ii < 4; ++ii)
+        for (int ii = 0; ii < kMsII; ++ii)
 #pragma unroll
-            for (int jp = 0; jp < 4; ++jp) acc[ii][jp] = 0ull;
+            for (int jp = 0; jp < JP; ++jp) acc[ii][jp] = 0ull;
 #pragma unroll
         for (int k = 0; k < KP; ++k) {
             if (k < K) {
 #pragma unroll
-                for (int ii = 0; ii < 4; ++ii) {
+                for (int ii = 0; ii < kMsII; ++ii) {
                     const float a = As[buf][warp + 8 * ii][k];
 #pragma unroll
-                    for (int jp = 0; jp < 4; ++jp)
+                    for (int jp = 0; jp < JP; ++jp)
                         acc[ii][jp] = fadd2(acc[ii][jp], pack2(mavp_term<OP>(a, breg[2 * jp][k]),
                                                                mavp_term<OP>(a, breg[2 * jp + 1][k])));
                 }
             }
         }
 #pragma unroll
-        for (int ii = 0; ii < 4; ++ii) {
+        for (int ii = 0; ii < kMsII; ++ii) {
             const int64_t i = i0 + warp + 8 * ii;
             if (i < m) {
                 float* crow = C + i * ldc;
 #pragma unroll
-                for (int jp = 0; jp < 4; ++jp) {
+                for (int jp = 0; jp < JP; ++jp) {
                     const int64_t ja = j0 + lane + 64 * jp, jb = ja + 32;
                     if (ja < p) crow[ja] = d == 1.0f ? lo_of(acc[ii][jp]) : inv_d * lo_of(acc[ii][jp]);
                     if (jb < p) crow[jb] = d == 1.0f ? hi_of(acc[ii][jp]) : inv_d * hi_of(acc[ii][jp]);
