@@ -7,10 +7,11 @@ for w in cfg1 cfg2 cfg4 cfg5 mincov mincov_k4096 alg2; do
   timeout 900 python bench.py --workload $w --steps 5 --warmup 3 --cpu-seconds 8 > gpurun_out/bench_$w.log 2>&1; echo "$w rc=$?"
 done
 timeout 600 python bench.py --mode sharded --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_sharded.log 2>&1; echo "sharded rc=$?"
+timeout 600 python bench.py --mode p2p --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_p2p.log 2>&1; echo "p2p rc=$?"
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_reference.log 2>&1; echo "ref rc=$?"
 python - <<'PY'
 import json
-for w in ["default","cfg1","cfg2","cfg4","cfg5","mincov","mincov_k4096","alg2","sharded","reference"]:
+for w in ["default","cfg1","cfg2","cfg4","cfg5","mincov","mincov_k4096","alg2","sharded","p2p","reference"]:
     try:
         d=json.loads(open(f"gpurun_out/bench_{w}.log").read().strip().splitlines()[-1])
         r=d.get("roofline",{})
