@@ -252,11 +252,14 @@ def build_pca(args, m, dev, stream):
                                           deltas.data_ptr(), ws.data_ptr(), need, stream.cuda_stream))
         return k * T
 
-    return Work(step=step, unit="iterations/s", per_launch=dense_bytes_per_iter(n, n) * T * k,
-                bytes_per_unit=dense_bytes_per_iter(n, n), bound="hbm",
-                kernel="k_iterate_coop x 8 (one per principal vector; events summed per step)",
+    # K2r holds each D_i on chip (TMEM + shared memory) for its 100 iterations: no matrix traffic inside the
+    # loop, so the roofline is the FMNMX issue rate (terms), not HBM (DESIGN.md §6 K2r)
+    return Work(step=step, unit="iterations/s", per_launch=float(n) * n * T * k,
+                bytes_per_unit=dense_bytes_per_iter(n, n), bound="alu",
+                kernel="k_iterate_resident x 8 (K2r, D_i in TMEM + shared memory; one launch per principal "
+                       "vector, events summed per step)",
                 config={"workload": f"cfg2: {WORKLOADS['cfg2']}", "n": n, "k": k, "iters_per_vector": T,
-                        "op": "min1", "l2_flush": "none: D_i (64 MiB) fits L2 by design; rates are vs HBM peak"},
+                        "op": "min1", "l2_flush": "none: each D_i is staged on chip once per vector (TMEM + smem)"},
                 oracle=("dense", C, b0, T))
 
 

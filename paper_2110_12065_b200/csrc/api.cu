@@ -14,6 +14,7 @@
 #include "../../include/mapi.h"
 #include "batched.cuh"
 #include "bulk.cuh"
+#include "resident.cuh"
 #include "csr.cuh"
 #include "deflate.cuh"
 #include "dense.cuh"
@@ -167,7 +168,7 @@ constexpr int kMaxGrid = 1024;
 constexpr int kIterThreads = 512;
 
 size_t iterate_ws_bytes(int64_t n) {
-    return 256 + align256(sizeof(double) * 2 * kMaxGrid) + align256(sizeof(float) * 2 * (size_t)n) +
+    return 256 + align256(sizeof(double) * 2 * kMaxGrid) + align256(sizeof(double) * 2 * (size_t)n) +
            align256(sizeof(float) * (size_t)n);
 }
 
@@ -189,8 +190,8 @@ IterWs carve_iterate(void* ws, int64_t n) {
     p += 256;
     w.slots = reinterpret_cast<float*>(p);  // holds 2 x kMaxGrid doubles
     p += align256(sizeof(double) * 2 * kMaxGrid);
-    w.y = reinterpret_cast<float*>(p);
-    p += align256(sizeof(float) * 2 * (size_t)n);
+    w.y = reinterpret_cast<float*>(p);  // 2n floats, or 2n tagged 8-byte words (K2r)
+    p += align256(sizeof(double) * 2 * (size_t)n);
     w.w = reinterpret_cast<float*>(p);
     return w;
 }
@@ -216,7 +217,8 @@ int coop_warps(int64_t n) { return (n / 256) >= 64 ? 32 : 16; }
 // K6 (one 8-CTA cluster, A in distributed shared memory) for small n; MAPI_DENSE_PATH=cluster forces
 bool use_cluster(const Device& d, int64_t n) {
     const char* e = dense_path_env();
-    if (strcmp(e, "rows") == 0 || strcmp(e, "multi") == 0 || strcmp(e, "coop") == 0 || strcmp(e, "bulk") == 0)
+    if (strcmp(e, "rows") == 0 || strcmp(e, "multi") == 0 || strcmp(e, "coop") == 0 || strcmp(e, "bulk") == 0 ||
+        strcmp(e, "resident") == 0)
         return false;
     if (n <= 512) return true;  // K6r (registers) fits any n <= 512
     if (cluster_smem_bytes(n) > (size_t)d.smem_optin) return false;
@@ -252,6 +254,24 @@ bool use_coop(const Device& d, const float* A, int64_t n, int64_t lda) {
     if (strcmp(e, "coop") != 0 && n / 256 < 32) return false;  // n < 8192: the per-row kernel is faster
     const int64_t grid = std::min<int64_t>(d.sms, n);
     return coop_smem_bytes(n, (int)grid, coop_warps(n)) <= (size_t)d.smem_optin;
+}
+
+// K2r (resident.cuh): the whole matrix on chip (TMEM + shared memory) for n <= 4096 when every CTA's
+// rows fit (ceil(n / grid) <= 28).  MAPI_DENSE_PATH=resident forces it; default range set by measurement.
+bool use_resident(const Device& d, int64_t n) {
+    const char* e = dense_path_env();
+    if (strcmp(e, "rows") == 0 || strcmp(e, "multi") == 0 || strcmp(e, "coop") == 0 || strcmp(e, "bulk") == 0)
+        return false;
+    const int64_t grid = std::min<int64_t>(d.sms, n);
+    if (n > kResNPad || (n + grid - 1) / grid > kResMaxRows) return false;
+    if (resident_smem_bytes() > (size_t)d.smem_optin) return false;
+    if (strcmp(e, "resident") == 0) return true;
+    return n >= 2048;
+}
+
+int resident_warps() {
+    const char* e = getenv("MAPI_RES_NW");
+    return (e && atoi(e) == 16) ? 16 : 8;  // 8 measured faster at n = 4096 (scripts/probe_k2r.cu)
 }
 
 // Runs MAPI on device buffers; no stream sync, no status read-back (caller does both).
@@ -333,6 +353,31 @@ mapi_status iterate_launch(const Device& d, int32_t op, const float* A, int64_t 
             });
         });
         return st;
+    }
+    if (use_resident(d, n)) {
+        const int grid = (int)std::min<int64_t>(d.sms, n);
+        // tagged y words: a tag never matches zeroed memory (tags are t + 1), so each call starts clean
+        MAPI_CUDA(cudaMemsetAsync(W.y, 0, sizeof(uint64_t) * 2 * (size_t)n, s));
+        const size_t smem = resident_smem_bytes();
+        const int nw = resident_warps();
+        using KernT = void (*)(IterArgs);
+        KernT kern = nw == 8 ? (op == 2 ? k_iterate_resident<2, 8> : (op == 1 ? k_iterate_resident<1, 8> : k_iterate_resident<0, 8>))
+                             : (op == 2 ? k_iterate_resident<2, 16> : (op == 1 ? k_iterate_resident<1, 16> : k_iterate_resident<0, 16>));
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return fail(MAPI_ERR_CUDA, "resident kernel smem (%zu): %s", smem, cudaGetErrorString(e));
+        IterArgs a;
+        a.A = A; a.n = n; a.lda = lda; a.b0 = b0; a.iters = iters; a.tol = tol;
+        a.w_out = w_out; a.norms = norms; a.deltas = deltas; a.y = W.y; a.slots = W.slots;
+        a.bar = W.bar; a.status = W.status;
+        void* args[] = {&a};
+        if (timer) timer->start();
+        e = cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(nw * 32), args, smem, s);
+        if (timer) timer->stop();
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        if (e != cudaSuccess)
+            return fail(MAPI_ERR_CUDA, "resident cooperative launch (grid %d, smem %zu): %s", grid, smem,
+                        cudaGetErrorString(e));
+        return MAPI_OK;
     }
     if (use_bulk(d, A, n, lda)) {
         const int slots = bulk_slots(d, n);

@@ -1,0 +1,398 @@
+// resident.cuh — K2r: persistent MAPI iteration with the whole matrix held ON CHIP (TMEM + shared memory).
+//
+// Alg. 1 for mid-size n (cfg2's 4096 x 4096 D_i = 64 MiB).  Every iteration of K2t
+// re-reads A from L2 (~453 KB per SM per iteration, L2-bandwidth/latency bound at ~13 us/iteration).
+// But 148 SMs hold 148 x (256 KB TMEM + 227 KB shared memory) = 70 MB on chip, more than D_i.  K2r
+// loads its CTA's rows ONCE per call, into tensor memory (`tcgen05.st`, 16 rows of 4096) and shared
+// memory (kResSmemRows rows), and every iteration reads them back with `tcgen05.ld` / `LDS.128`: no
+// L2 or HBM traffic for A inside the loop.  TMEM is used purely as storage (no MMA: MAVP is not a
+// contraction, the tensor cores cannot compute sign(a w) min(|a|,|w|)).
+//
+// Thread mapping (NW warps, 1 CTA per SM, cooperative launch): quarter q = warp % 4 (the TMEM lane
+// quarter a warp may access), group g = warp / 4.  Thread (q, lane) is "column lane" L = 32q + lane
+// and owns the 32 columns [32L, 32L + 32) of EVERY row of the CTA (n <= 4096 = 128 x 32), so it keeps
+// those 32 entries of w_t in registers for the whole pass.  Local rows 0..15 live in TMEM (row i =
+// TMEM columns [32i, 32i + 32) of the 128 lanes), local rows 16.. in shared memory (row-major, 4096
+// floats per row); group g computes TMEM rows [g TR, (g+1) TR) and shared rows [g SR, (g+1) SR).
+// Within a row slice, the 8 float4 chunks are visited in the lane-rotated order c = (m + lane) % 8
+// (conflict-free LDS.128: the 8 lanes of a quarter-warp phase hit 8 distinct 4-bank groups); the
+// TMEM copy and the w registers are stored in the same rotated order so the pairing is static.
+//
+// Per iteration: every thread forms its 32-term partial of each of its rows (4 chains: FMNMX.XORSIGN
+// + FADD2, pairwise), the warp reduces its P partials across the 32 lanes with a reduce-scatter
+// butterfly (P + log2 steps shuffles instead of 5P), the 4 quarters meet in shared memory
+// (y_i = (q0 + q1) + (q2 + q3)), warp 0 writes y and the CTA's fp64 |y| partial, ONE grid barrier,
+// then every CTA forms s_t (fixed order), w_{t+1} = fp32(y/s_t) for all n and the fp64 delta_t
+// exactly as K2t does (identical bits and stop decision in every CTA).  Deterministic for a given
+// (n, grid).  Requirements: n <= 4096, ceil(n / grid) <= 16 + kResSmemRows, 1 CTA per SM.
+#pragma once
+#include "dense.cuh"
+#include "mapi_common.cuh"
+
+namespace mapi {
+
+constexpr int kResLanes = 128;                   // TMEM lanes = column lanes
+constexpr int kResCPL = 32;                      // columns per lane
+constexpr int kResNPad = kResLanes * kResCPL;    // 4096: padded row length (max n)
+constexpr int kResTmemRows = 512 / kResCPL;      // 16 rows in the 512 TMEM columns
+constexpr int kResSmemRows = 12;                 // rows in shared memory (192 KB)
+constexpr int kResMaxRows = kResTmemRows + kResSmemRows;
+
+inline size_t resident_smem_bytes() {
+    return sizeof(float) * ((size_t)kResSmemRows * kResNPad + kResNPad + 4 * 32) + sizeof(double) * 40 + 16;
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t ta, float (&v)[32]) {
+    uint32_t* r = reinterpret_cast<uint32_t*>(v);
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(ta));
+}
+// wait for this thread's outstanding tcgen05.ld; the loaded registers are "+r" operands, so no use of
+// them can be scheduled above the wait (the load writes them asynchronously)
+__device__ __forceinline__ void tmem_wait_ld(float (&v)[32]) {
+    uint32_t* r = reinterpret_cast<uint32_t*>(v);
+    asm volatile(
+        "tcgen05.wait::ld.sync.aligned;"
+        : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+          "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15]),
+          "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]), "+r"(r[22]), "+r"(r[23]),
+          "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]), "+r"(r[29]), "+r"(r[30]), "+r"(r[31])
+        :
+        : "memory");
+}
+__device__ __forceinline__ void st_tagged(uint64_t* p, uint64_t v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_tagged(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p));
+    return v;
+}
+// fixed-shape pairwise tree over NW per-warp partials in shared memory (same order in every CTA)
+template <int NW>
+__device__ __forceinline__ double res_tree(const double* v) {
+    double a[NW];
+#pragma unroll
+    for (int i = 0; i < NW; ++i) a[i] = v[i];
+#pragma unroll
+    for (int h = NW / 2; h > 0; h >>= 1)
+#pragma unroll
+        for (int i = 0; i < h; ++i) a[i] = a[2 * i] + a[2 * i + 1];
+    return a[0];
+}
+__device__ __forceinline__ void tmem_st32(uint32_t ta, const float (&v)[32]) {
+    const uint32_t* r = reinterpret_cast<const uint32_t*>(v);
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(ta),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+        "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]),
+        "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]),
+        "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+        : "memory");
+}
+
+__device__ __forceinline__ unsigned long long res_fadd2(unsigned long long a, unsigned long long b) {
+    unsigned long long d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ unsigned long long res_pack2(float x, float y) {
+    return (unsigned long long)__float_as_uint(x) | ((unsigned long long)__float_as_uint(y) << 32);
+}
+
+// 32 terms (one row slice) against the thread's 32 w registers: 4 chains of 8 (two FADD2 pairs),
+// pairwise final tree.  Same pairing in every row, TMEM or shared.
+template <int OP>
+__device__ __forceinline__ float res_row32(const float (&a)[32], const float (&w)[32]) {
+    unsigned long long p0 = 0, p1 = 0;
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+        p0 = res_fadd2(p0, res_pack2(mavp_term<OP>(a[4 * m], w[4 * m]), mavp_term<OP>(a[4 * m + 1], w[4 * m + 1])));
+        p1 = res_fadd2(p1, res_pack2(mavp_term<OP>(a[4 * m + 2], w[4 * m + 2]), mavp_term<OP>(a[4 * m + 3], w[4 * m + 3])));
+    }
+    return (__uint_as_float((uint32_t)p0) + __uint_as_float((uint32_t)(p0 >> 32))) +
+           (__uint_as_float((uint32_t)p1) + __uint_as_float((uint32_t)(p1 >> 32)));
+}
+
+// Reduce PP per-lane partials across the 32 lanes: reduce-scatter butterfly (at offset o the lanes with
+// bit o set keep the upper half of the live values, the others the lower half; each adds its partner's
+// copy), then plain butterfly steps.  Returns the full 32-lane sum of value index res_row_of<PP>(lane).
+template <int PP>
+__device__ __forceinline__ float res_lane_reduce(float (&v)[PP], int lane) {
+#pragma unroll
+    for (int j = 0; (PP >> j) > 1; ++j) {
+        const int o = 16 >> j, half = PP >> (j + 1);
+        const bool up = (lane & o) != 0;
+#pragma unroll
+        for (int i = 0; i < half; ++i) {
+            const float send = up ? v[i] : v[i + half];
+            const float keep = up ? v[i + half] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+    }
+    float x = v[0];
+    constexpr int LOGPP = PP >= 16 ? 4 : (PP >= 8 ? 3 : (PP >= 4 ? 2 : (PP >= 2 ? 1 : 0)));
+#pragma unroll
+    for (int o = 16 >> LOGPP; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    return x;
+}
+template <int PP>
+__device__ __forceinline__ int res_row_of(int lane) {
+    int r = 0;
+#pragma unroll
+    for (int j = 0; (PP >> j) > 1; ++j) r = 2 * r + ((lane >> (4 - j)) & 1);
+    return r;
+}
+
+// one-time load of a 32-column row slice in rotated chunk order (zero beyond n / for absent rows)
+__device__ __forceinline__ void res_load_slice(const float* A, int64_t lda, int64_t n, int64_t row, bool valid,
+                                               int L, int lane, bool vec4, float (&v)[32]) {
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+        const int c = (m + lane) & 7;
+        const int64_t k0 = (int64_t)kResCPL * L + 4 * c;
+        const float* src = A + row * lda + k0;
+        if (valid && vec4 && k0 + 3 < n) {
+            const float4 x = __ldg(reinterpret_cast<const float4*>(src));
+            v[4 * m] = x.x; v[4 * m + 1] = x.y; v[4 * m + 2] = x.z; v[4 * m + 3] = x.w;
+        } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) v[4 * m + e] = (valid && k0 + e < n) ? __ldg(src + e) : 0.0f;
+        }
+    }
+}
+
+#ifdef MAPI_RES_TRACE
+__device__ long long g_res_trace[8 * 512];  // investigation builds only (scripts/probe_k2r.cu)
+#define RES_STAMP(t, k) \
+    if (blockIdx.x == 0 && threadIdx.x == 0 && (t) < 512) g_res_trace[(t) * 8 + (k)] = clock64()
+#else
+#define RES_STAMP(t, k)
+#endif
+
+// XM: y exchange.  0 = every thread polls its tagged y words until they carry the iteration's tag (no
+// barrier, no fence); 1 = arrival counter (release add by warp 0 after its tagged stores, one acquiring
+// spinner per CTA, __syncthreads), then one round of tagged loads.
+template <int OP, int NW, int XM = 0>
+__global__ void __launch_bounds__(NW * 32, 1) k_iterate_resident(IterArgs p) {
+    constexpr int NT = NW * 32, G = NW / 4;                    // threads, warp groups
+    constexpr int TR = kResTmemRows / G, SR = kResSmemRows / G, P = TR + SR;
+    constexpr int PP = P <= 2 ? 2 : (P <= 4 ? 4 : (P <= 8 ? 8 : 16));
+    static_assert(kResTmemRows % G == 0 && kResSmemRows % G == 0 && P <= 16, "row split");
+    extern __shared__ __align__(16) float ws_[];
+    float* a_s = ws_;                                           // kResSmemRows x 4096
+    float* w_s = a_s + (size_t)kResSmemRows * kResNPad;         // 4096 (w_t, zero-padded)
+    float* yq = w_s + kResNPad;                                 // [4][32] quarter partials of y
+    double* red = reinterpret_cast<double*>(yq + 4 * 32);       // 40: per-warp partials
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(red + 40);
+    const int64_t n = p.n;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, q = warp & 3, g = warp >> 2;
+    const int L = 32 * q + lane;
+    const int64_t r0 = (int64_t)blockIdx.x * n / gridDim.x, r1 = (int64_t)(blockIdx.x + 1) * n / gridDim.x;
+    const int R = (int)(r1 - r0);
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+            (uint32_t)__cvta_generic_to_shared(tslot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tbase = *tslot;
+    const uint32_t ta = tbase + ((uint32_t)(32 * q) << 16) + (uint32_t)(kResCPL * TR * g);
+
+    // ---- one-time staging of this CTA's rows (A does not change across iterations)
+    const bool vec4 = (n % 4 == 0) && (p.lda % 4 == 0) && ((reinterpret_cast<uintptr_t>(p.A) & 15) == 0);
+#pragma unroll 1
+    for (int r = 0; r < TR; ++r) {
+        const int i = g * TR + r;
+        float v[32];
+        res_load_slice(p.A, p.lda, n, r0 + i, i < R, L, lane, vec4, v);
+        tmem_st32(ta + (uint32_t)(kResCPL * r), v);
+    }
+#pragma unroll 1
+    for (int r = 0; r < SR; ++r) {
+        const int i = kResTmemRows + g * SR + r;
+        float v[32];
+        res_load_slice(p.A, p.lda, n, r0 + i, i < R, L, lane, vec4, v);
+        float4* dst = reinterpret_cast<float4*>(a_s + (size_t)(g * SR + r) * kResNPad) + 8 * L;
+#pragma unroll
+        for (int m = 0; m < 8; ++m) dst[(m + lane) & 7] = make_float4(v[4 * m], v[4 * m + 1], v[4 * m + 2], v[4 * m + 3]);
+    }
+    for (int k = tid; k < kResNPad; k += NT) w_s[k] = k < n ? p.b0[k] : 0.0f;
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    __syncthreads();
+
+    float wr[32];  // w_t at this thread's columns, rotated order
+    auto load_w = [&]() {
+        const float4* src = reinterpret_cast<const float4*>(w_s) + 8 * L;
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+            const float4 x = src[(m + lane) & 7];
+            wr[4 * m] = x.x; wr[4 * m + 1] = x.y; wr[4 * m + 2] = x.z; wr[4 * m + 3] = x.w;
+        }
+    };
+    load_w();
+
+    int32_t done = 0, status = kStOk;
+    uint64_t* yt = reinterpret_cast<uint64_t*>(p.y);  // [2][n] tagged words: (t + 1) << 32 | bits(y)
+    double* wsum = red;                               // [NW] per-warp |y| partials
+    double* dsum = red + 16;                          // [NW] per-warp delta partials
+    constexpr int YR = kResNPad / NT;  // y values per thread in the normalisation (n <= 4096)
+    for (int32_t t = 0; t < p.iters; ++t) {
+        uint64_t* yb = yt + (t & 1) * n;
+        const uint32_t tag = (uint32_t)t + 1u;
+        RES_STAMP(t, 0);
+        float part[PP];
+#pragma unroll
+        for (int r = 0; r < PP; ++r) part[r] = 0.0f;
+        // TMEM row i is in flight while shared-memory row i is computed (the two read paths overlap).
+        // Row guards are warp-uniform (tcgen05.ld / wait are .sync.aligned).
+        float at[32];
+        if (g * TR < R) tmem_ld32(ta, at);
+#pragma unroll
+        for (int i = 0; i < (TR > SR ? TR : SR); ++i) {
+            if (i < SR && kResTmemRows + g * SR + i < R) {
+                const float4* src = reinterpret_cast<const float4*>(a_s + (size_t)(g * SR + i) * kResNPad) + 8 * L;
+                float as[32];
+#pragma unroll
+                for (int m = 0; m < 8; ++m) {
+                    const float4 x = src[(m + lane) & 7];
+                    as[4 * m] = x.x; as[4 * m + 1] = x.y; as[4 * m + 2] = x.z; as[4 * m + 3] = x.w;
+                }
+                part[TR + i] = res_row32<OP>(as, wr);
+            }
+            if (i < TR && g * TR + i < R) {
+                tmem_wait_ld(at);
+                part[i] = res_row32<OP>(at, wr);
+                if (i + 1 < TR && g * TR + i + 1 < R) tmem_ld32(ta + (uint32_t)(kResCPL * (i + 1)), at);
+            }
+        }
+        RES_STAMP(t, 1);
+        const float rv = res_lane_reduce<PP>(part, lane);
+        {
+            const int ri = res_row_of<PP>(lane);
+            if ((lane & (32 / PP - 1)) == 0 && ri < P) {
+                const int i = ri < TR ? g * TR + ri : kResTmemRows + g * SR + (ri - TR);
+                yq[q * 32 + i] = rv;
+            }
+        }
+        __syncthreads();
+        // publish this CTA's rows: one 8-byte word per row carries the value AND its iteration tag, so
+        // the exchange needs no grid barrier, fence or counter (a reader that sees the tag sees the value)
+        RES_STAMP(t, 2);
+        if (warp == 0) {
+            if (lane < R) {
+                const float v = (yq[lane] + yq[32 + lane]) + (yq[64 + lane] + yq[96 + lane]);
+                st_tagged(yb + r0 + lane, ((uint64_t)tag << 32) | __float_as_uint(v));
+            }
+            if constexpr (XM == 1) {
+                __syncwarp();
+                if (lane == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.bar) : "memory");
+            }
+        }
+        if constexpr (XM == 1) {
+            if (tid == 0) {
+                const unsigned int target = (unsigned int)(t + 1) * gridDim.x;
+                unsigned int v;
+                do {
+                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.bar) : "memory");
+                } while (v < target);
+            }
+            __syncthreads();
+        }
+        RES_STAMP(t, 3);
+        // gather all of y_t: every thread polls its YR words until they carry this iteration's tag
+        float yr[YR];
+        {
+            uint32_t pending = 0;
+#pragma unroll
+            for (int j = 0; j < YR; ++j) {
+                yr[j] = 0.0f;
+                if (tid + (int64_t)j * NT < n) pending |= 1u << j;
+            }
+            while (pending) {
+                uint64_t xv[YR];  // all loads of a round in flight together, then the tag checks
+#pragma unroll
+                for (int j = 0; j < YR; ++j) xv[j] = (pending & (1u << j)) ? ld_tagged(yb + tid + (int64_t)j * NT) : 0;
+#pragma unroll
+                for (int j = 0; j < YR; ++j) {
+                    if ((pending & (1u << j)) && (uint32_t)(xv[j] >> 32) == tag) {
+                        yr[j] = __uint_as_float((uint32_t)xv[j]);
+                        pending &= ~(1u << j);
+                    }
+                }
+            }
+        }
+        RES_STAMP(t, 4);
+        // s_t: per-thread fp64 partials in a fixed order, warp butterflies, warps summed in warp order
+        // (the same thread -> element mapping in every CTA: identical s_t everywhere)
+        double yd[YR];  // converted once: the |y| partial and the quotient both use it
+#pragma unroll
+        for (int j = 0; j < YR; ++j) yd[j] = (double)yr[j];
+        {
+            double ap = 0.0;
+#pragma unroll
+            for (int j = 0; j < YR; ++j) ap += (OP == 2) ? yd[j] * yd[j] : fabs(yd[j]);
+            ap = warp_sum(ap);
+            if (lane == 0) wsum[warp] = ap;
+        }
+        __syncthreads();
+        RES_STAMP(t, 5);
+        const double s = norm_final<OP>(res_tree<NW>(wsum));
+        if (!(s > 0.0) || isinf(s)) {  // uniform across the grid
+            status = (s == 0.0) ? kStDegenerate : kStNonfinite;
+            break;
+        }
+        // w_{t+1} = fp32(y / s_t) with s_t in fp64, evaluated in fp32 pairs: 1/s_t = rh + rl (fp64
+        // reciprocal split into two floats), q = p + (e + y rl) with p = y rh and e = fma(y, rh, -p) its
+        // exact error: |q - y/s_t| ~ 2^-47 |q|, so the fp32 result equals fp32(y / s_t) except when y/s_t
+        // lies within ~2^-47 (relative) of an fp32 rounding boundary.  No fp64 conversion per element
+        // (F2F is the bottleneck of a per-element fp64 quotient: 4096 per CTA per iteration).  delta_t:
+        // fp32 |w_{t+1} - w_t| per element, fp32 within a thread (YR terms), fp64 across threads.
+        // Branch-free over the padded 4096: beyond n, y = 0 and w_s = 0, so w stays 0 and adds 0 to delta.
+        const double rs = 1.0 / s;
+        const float rh = (float)rs, rl = (float)(rs - (double)rh);
+        float dv = 0.0f;
+#pragma unroll
+        for (int j = 0; j < YR; ++j) {
+            const int k = tid + j * NT;
+            const float pj = yr[j] * rh;
+            const float wn = pj + fmaf(yr[j], rl, fmaf(yr[j], rh, -pj));
+            dv += fabsf(wn - w_s[k]);
+            w_s[k] = wn;
+        }
+        double dpart = (double)dv;
+        RES_STAMP(t, 7);
+        dpart = warp_sum(dpart);
+        if (lane == 0) dsum[warp] = dpart;
+        __syncthreads();  // also orders the w_s writes before load_w
+        RES_STAMP(t, 6);
+        const double delta = res_tree<NW>(dsum);
+        if (blockIdx.x == 0 && tid == 0) {
+            if (p.norms) p.norms[t] = (float)s;
+            if (p.deltas) p.deltas[t] = (float)delta;
+        }
+        done = t + 1;
+        if (p.tol > 0.0f && delta < (double)p.tol) break;
+        load_w();
+    }
+    for (int64_t k = r0 + tid; k < r1; k += NT) p.w_out[k] = w_s[k];
+    if (blockIdx.x == 0 && tid == 0) {
+        p.status[0] = status;
+        p.status[1] = done;
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tbase));
+}
+
+}  // namespace mapi

@@ -248,7 +248,7 @@ def test_cfg3_last_step_and_invariants(mapi_lib, orc, cfg3_device):
     assert torch.equal(r100.w, r100b.w)
 
 
-@pytest.mark.parametrize("path", ["cluster", "cluster_smem", "rows", "coop", "bulk", "multi"])
+@pytest.mark.parametrize("path", ["cluster", "cluster_smem", "rows", "coop", "bulk", "resident", "multi"])
 @pytest.mark.parametrize("n", [256, 511, 4096, 8200])
 def test_every_dense_path_matches_oracle(mapi_lib, orc, monkeypatch, path, n):
     """Each dense iteration kernel (K6 cluster, K2 per-row, K2c cooperative rows, multi-launch),
@@ -300,6 +300,83 @@ def test_bulk_ring_early_stop_and_degenerate(mapi_lib, orc, monkeypatch):
     full = m.iterate(Ad, bd, 200)
     d = full.deltas.cpu().numpy()
     tol = float(d[40]) * 1.0001  # first crossing near iteration 40
+    first = int(np.nonzero(d < tol)[0][0])
+    res = m.iterate(Ad, bd, 200, tol=tol)
+    assert res.iters_done == first + 1
+    assert torch.equal(res.deltas, full.deltas[: first + 1])
+    ref = orc.mapi(A, b0, first + 1)
+    _t2(res.w_l2.cpu().numpy(), ref.w)
+    with pytest.raises(m.MapiError) as ei:
+        m.iterate(torch.zeros(n, n, device="cuda"), bd, 10)
+    assert ei.value.name == "MAPI_ERR_DEGENERATE" and ei.value.iters_done == 0
+    again = m.iterate(Ad, bd, 200)
+    assert torch.equal(again.w, full.w)
+
+
+@pytest.mark.parametrize("n,pad", [(1, 0), (33, 3), (700, 0), (1500, 4), (2049, 8), (3001, 1), (4096, 0), (4096, 12)])
+@pytest.mark.parametrize("op", ["min1", "min2", "dot"])
+@pytest.mark.parametrize("nw", ["8", "16"])
+def test_resident_path(mapi_lib, orc, monkeypatch, n, pad, op, nw):
+    """K2r (matrix held in TMEM + shared memory for the whole call): ragged n (partial column lanes,
+    scalar staging when rows are not 16 B-aligned), padded lda with NaN padding, every operator, both
+    warp counts, vs the oracle (T2; the RPI limit for dot), bitwise reproducible."""
+    m = mapi_lib
+    r = np.random.default_rng(n + pad)
+    Af = np.full((n, n + pad), np.nan, np.float32)
+    A = r.standard_normal((n, n)).astype(np.float32) + np.diag(np.abs(r.standard_normal(n)) * 4).astype(np.float32)
+    if op == "dot":
+        A = ((A + A.T) / (2 * np.sqrt(n))).astype(np.float32)
+    Af[:, :n] = A
+    b0 = np.full(n, 1.0 / np.sqrt(n), np.float32)
+    monkeypatch.setenv("MAPI_DENSE_PATH", "resident")
+    monkeypatch.setenv("MAPI_RES_NW", nw)
+    Ad = torch.from_numpy(Af).cuda()[:, :n]
+    opc = {"min1": m.MIN1, "min2": m.MIN2, "dot": m.DOT}[op]
+    res = m.iterate(Ad, torch.from_numpy(b0).cuda(), 25, op=opc)
+    ref = orc.rpi(A, b0, 25) if op == "dot" else orc.mapi(A, b0, 25, op=op)
+    assert res.iters_done == 25
+    got = res.w.cpu().numpy() if op == "dot" else res.w_l2.cpu().numpy()
+    _t2(got, ref.w, res.norms.cpu().numpy(), ref.norms)
+    again = m.iterate(Ad, torch.from_numpy(b0).cuda(), 25, op=opc)
+    assert torch.equal(res.w, again.w) and torch.equal(res.deltas, again.deltas)
+
+
+def test_resident_matvec_t1_each_iteration(mapi_lib, orc, monkeypatch):
+    """K2r per-iteration T1: the GPU's t-th norm and iterate against one fp64 oracle step from the GPU's
+    own (t-1)-th iterate, at cfg2's size (4096, 28 rows per CTA: 16 in TMEM, 12 in shared memory)."""
+    m = mapi_lib
+    n = 4096
+    r = np.random.default_rng(11)
+    A = r.standard_normal((n, n)).astype(np.float32) + np.diag(np.abs(r.standard_normal(n)) * 4).astype(np.float32)
+    b0 = np.full(n, 1.0 / np.sqrt(n), np.float32)
+    monkeypatch.setenv("MAPI_DENSE_PATH", "resident")
+    Ad, bd = torch.from_numpy(A).cuda(), torch.from_numpy(b0).cuda()
+    r4 = m.iterate(Ad, bd, 4)
+    r5 = m.iterate(Ad, bd, 5)
+    w4 = r4.w.cpu().numpy()
+    y, mag = orc.matvec(A, w4, return_mag=True)
+    s = np.abs(y).sum()
+    assert abs(float(r5.norms[4]) - s) <= 1e-5 * s
+    w5 = r5.w.cpu().numpy().astype(np.float64)
+    err = np.abs(w5 - y / s)
+    assert np.all(err <= 1e-5 * mag / s + 2e-5 * np.abs(y / s)), float(np.max(err))
+    resumed = m.iterate(Ad, r4.w, 1)
+    assert torch.equal(resumed.w, r5.w)
+
+
+def test_resident_early_stop_and_degenerate(mapi_lib, orc, monkeypatch):
+    """tol stop and the degenerate status on K2r (TMEM is released on every exit path: the next call
+    allocates it again), then a normal run on the same stream."""
+    m = mapi_lib
+    monkeypatch.setenv("MAPI_DENSE_PATH", "resident")
+    n = 3000
+    r = np.random.default_rng(3)
+    A = (r.standard_normal((n, n)) / 8).astype(np.float32) + np.diag(np.linspace(4.0, 1.0, n)).astype(np.float32)
+    b0 = np.full(n, 1.0 / np.sqrt(n), np.float32)
+    Ad, bd = torch.from_numpy(A).cuda(), torch.from_numpy(b0).cuda()
+    full = m.iterate(Ad, bd, 200)
+    d = full.deltas.cpu().numpy()
+    tol = float(d[40]) * 1.0001
     first = int(np.nonzero(d < tol)[0][0])
     res = m.iterate(Ad, bd, 200, tol=tol)
     assert res.iters_done == first + 1
