@@ -266,7 +266,9 @@ bool use_resident(const Device& d, int64_t n) {
     if (n > kResNPad || (n + grid - 1) / grid > kResMaxRows) return false;
     if (resident_smem_bytes() > (size_t)d.smem_optin) return false;
     if (strcmp(e, "resident") == 0) return true;
-    return n >= 2048;
+    // measured (profiles/r01_probe_resident_range.log, us / iteration incl. launch): n = 1536 5.5 vs 6.2
+    // (per-row K2), n = 4096 4.7 vs 12.8 (K2t); at n <= 1024 all grid-wide kernels tie at ~5 us (exchange-bound)
+    return n > 1024;
 }
 
 int resident_warps() {
@@ -358,11 +360,15 @@ mapi_status iterate_launch(const Device& d, int32_t op, const float* A, int64_t 
         const int grid = (int)std::min<int64_t>(d.sms, n);
         // tagged y words: a tag never matches zeroed memory (tags are t + 1), so each call starts clean
         MAPI_CUDA(cudaMemsetAsync(W.y, 0, sizeof(uint64_t) * 2 * (size_t)n, s));
-        const size_t smem = resident_smem_bytes();
+        // 8 warps with 2 register-resident rows per warp group (4 of the CTA's <= 28 rows in registers, 16 in
+        // TMEM, 8 in shared memory); 16 warps (MAPI_RES_NW=16) have no register room for rows
         const int nw = resident_warps();
+        const size_t smem = resident_smem_bytes(nw == 8 ? kResSmemRows - 2 * 2 : kResSmemRows);
         using KernT = void (*)(IterArgs);
-        KernT kern = nw == 8 ? (op == 2 ? k_iterate_resident<2, 8> : (op == 1 ? k_iterate_resident<1, 8> : k_iterate_resident<0, 8>))
-                             : (op == 2 ? k_iterate_resident<2, 16> : (op == 1 ? k_iterate_resident<1, 16> : k_iterate_resident<0, 16>));
+        KernT kern = nw == 8 ? (op == 2 ? k_iterate_resident<2, 8, 1, 2>
+                                        : (op == 1 ? k_iterate_resident<1, 8, 1, 2> : k_iterate_resident<0, 8, 1, 2>))
+                             : (op == 2 ? k_iterate_resident<2, 16, 1, 0>
+                                        : (op == 1 ? k_iterate_resident<1, 16, 1, 0> : k_iterate_resident<0, 16, 1, 0>));
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return fail(MAPI_ERR_CUDA, "resident kernel smem (%zu): %s", smem, cudaGetErrorString(e));
         IterArgs a;

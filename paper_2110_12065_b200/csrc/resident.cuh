@@ -38,8 +38,9 @@ constexpr int kResTmemRows = 512 / kResCPL;      // 16 rows in the 512 TMEM colu
 constexpr int kResSmemRows = 12;                 // rows in shared memory (192 KB)
 constexpr int kResMaxRows = kResTmemRows + kResSmemRows;
 
-inline size_t resident_smem_bytes() {
-    return sizeof(float) * ((size_t)kResSmemRows * kResNPad + kResNPad + 4 * 32) + sizeof(double) * 40 + 16;
+// smem_rows = rows kept in shared memory (kResSmemRows minus the register-resident rows)
+inline size_t resident_smem_bytes(int smem_rows = kResSmemRows) {
+    return sizeof(float) * ((size_t)smem_rows * kResNPad + kResNPad + 4 * 32) + sizeof(double) * 64 + 16;
 }
 
 __device__ __forceinline__ void tmem_ld32(uint32_t ta, float (&v)[32]) {
@@ -73,6 +74,12 @@ __device__ __forceinline__ uint64_t ld_tagged(const uint64_t* p) {
     uint64_t v;
     asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p));
     return v;
+}
+__device__ __forceinline__ void st_cluster_f64(double* local, uint32_t rank, double v) {
+    const uint32_t a = (uint32_t)__cvta_generic_to_shared(local);
+    uint32_t ra;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+    asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(ra), "d"(v) : "memory");
 }
 // fixed-shape pairwise tree over NW per-warp partials in shared memory (same order in every CTA)
 template <int NW>
@@ -171,27 +178,34 @@ __device__ __forceinline__ void res_load_slice(const float* A, int64_t lda, int6
 
 #ifdef MAPI_RES_TRACE
 __device__ long long g_res_trace[8 * 512];  // investigation builds only (scripts/probe_k2r.cu)
+__device__ int g_res_polls[148 * 512];  // poll rounds of thread 0 per (CTA, iteration)
 #define RES_STAMP(t, k) \
     if (blockIdx.x == 0 && threadIdx.x == 0 && (t) < 512) g_res_trace[(t) * 8 + (k)] = clock64()
+#define RES_POLLS(t, c) \
+    if (threadIdx.x == 0 && (t) < 512 && blockIdx.x < 148) g_res_polls[blockIdx.x * 512 + (t)] = (c)
 #else
+#define RES_POLLS(t, c)
 #define RES_STAMP(t, k)
 #endif
 
-// XM: y exchange.  0 = every thread polls its tagged y words until they carry the iteration's tag (no
-// barrier, no fence); 1 = arrival counter (release add by warp 0 after its tagged stores, one acquiring
-// spinner per CTA, __syncthreads), then one round of tagged loads.
-template <int OP, int NW, int XM = 0>
+// CL: 1 = every CTA gathers all of y_t and forms all n quotients itself; 2 = CTA pairs (a 2-CTA
+// cluster: 148 SMs hold 74 pairs) split the epilogue: each CTA polls HALF of y_t (halving the L2 read
+// volume of the exchange, the bound of a poll round) and forms half of w_{t+1}, written into both CTAs'
+// shared memory with DSMEM stores; the |y| and delta partials cross the pair the same way, each behind
+// one barrier.cluster (release / acquire).
+template <int OP, int NW, int CL = 1, int RR = 0>
 __global__ void __launch_bounds__(NW * 32, 1) k_iterate_resident(IterArgs p) {
     constexpr int NT = NW * 32, G = NW / 4;                    // threads, warp groups
-    constexpr int TR = kResTmemRows / G, SR = kResSmemRows / G, P = TR + SR;
+    constexpr int SMR = kResSmemRows - G * RR;                 // rows in shared memory
+    constexpr int TR = kResTmemRows / G, SR = SMR / G, P = TR + RR + SR;
     constexpr int PP = P <= 2 ? 2 : (P <= 4 ? 4 : (P <= 8 ? 8 : 16));
-    static_assert(kResTmemRows % G == 0 && kResSmemRows % G == 0 && P <= 16, "row split");
+    static_assert(kResTmemRows % G == 0 && SMR % G == 0 && SMR >= 0 && P <= 16, "row split");
     extern __shared__ __align__(16) float ws_[];
-    float* a_s = ws_;                                           // kResSmemRows x 4096
-    float* w_s = a_s + (size_t)kResSmemRows * kResNPad;         // 4096 (w_t, zero-padded)
+    float* a_s = ws_;                                           // SMR x 4096
+    float* w_s = a_s + (size_t)SMR * kResNPad;                  // 4096 (w_t, zero-padded)
     float* yq = w_s + kResNPad;                                 // [4][32] quarter partials of y
-    double* red = reinterpret_cast<double*>(yq + 4 * 32);       // 40: per-warp partials
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(red + 40);
+    double* red = reinterpret_cast<double*>(yq + 4 * 32);       // 64: per-warp partials
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(red + 64);
     const int64_t n = p.n;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, q = warp & 3, g = warp >> 2;
     const int L = 32 * q + lane;
@@ -218,9 +232,15 @@ __global__ void __launch_bounds__(NW * 32, 1) k_iterate_resident(IterArgs p) {
         res_load_slice(p.A, p.lda, n, r0 + i, i < R, L, lane, vec4, v);
         tmem_st32(ta + (uint32_t)(kResCPL * r), v);
     }
+    float areg[RR > 0 ? RR : 1][32];
+#pragma unroll
+    for (int r = 0; r < RR; ++r) {
+        const int i = kResTmemRows + g * RR + r;
+        res_load_slice(p.A, p.lda, n, r0 + i, i < R, L, lane, vec4, areg[r]);
+    }
 #pragma unroll 1
     for (int r = 0; r < SR; ++r) {
-        const int i = kResTmemRows + g * SR + r;
+        const int i = kResTmemRows + G * RR + g * SR + r;
         float v[32];
         res_load_slice(p.A, p.lda, n, r0 + i, i < R, L, lane, vec4, v);
         float4* dst = reinterpret_cast<float4*>(a_s + (size_t)(g * SR + r) * kResNPad) + 8 * L;
@@ -244,9 +264,11 @@ __global__ void __launch_bounds__(NW * 32, 1) k_iterate_resident(IterArgs p) {
 
     int32_t done = 0, status = kStOk;
     uint64_t* yt = reinterpret_cast<uint64_t*>(p.y);  // [2][n] tagged words: (t + 1) << 32 | bits(y)
-    double* wsum = red;                               // [NW] per-warp |y| partials
-    double* dsum = red + 16;                          // [NW] per-warp delta partials
-    constexpr int YR = kResNPad / NT;  // y values per thread in the normalisation (n <= 4096)
+    double* wsum = red;                               // [CL * NW] per-warp |y| partials
+    double* dsum = red + 32;                          // [CL * NW] per-warp delta partials
+    constexpr int YH = kResNPad / NT / CL;            // y values per thread in the normalisation
+    const uint32_t half = CL == 2 ? cluster_ctarank() : 0u;
+    const int64_t kb = (int64_t)half * (kResNPad / CL);  // first element of this CTA's share
     for (int32_t t = 0; t < p.iters; ++t) {
         uint64_t* yb = yt + (t & 1) * n;
         const uint32_t tag = (uint32_t)t + 1u;
@@ -259,16 +281,19 @@ __global__ void __launch_bounds__(NW * 32, 1) k_iterate_resident(IterArgs p) {
         float at[32];
         if (g * TR < R) tmem_ld32(ta, at);
 #pragma unroll
-        for (int i = 0; i < (TR > SR ? TR : SR); ++i) {
-            if (i < SR && kResTmemRows + g * SR + i < R) {
-                const float4* src = reinterpret_cast<const float4*>(a_s + (size_t)(g * SR + i) * kResNPad) + 8 * L;
+        for (int i = 0; i < (TR > SR + RR ? TR : SR + RR); ++i) {
+            if (i < RR) {  // register row (rows beyond R were staged as zeros: no guard needed)
+                part[TR + i] = res_row32<OP>(areg[i], wr);
+            } else if (i < RR + SR && kResTmemRows + G * RR + g * SR + (i - RR) < R) {
+                const int sr = i - RR;
+                const float4* src = reinterpret_cast<const float4*>(a_s + (size_t)(g * SR + sr) * kResNPad) + 8 * L;
                 float as[32];
 #pragma unroll
                 for (int m = 0; m < 8; ++m) {
                     const float4 x = src[(m + lane) & 7];
                     as[4 * m] = x.x; as[4 * m + 1] = x.y; as[4 * m + 2] = x.z; as[4 * m + 3] = x.w;
                 }
-                part[TR + i] = res_row32<OP>(as, wr);
+                part[TR + RR + sr] = res_row32<OP>(as, wr);
             }
             if (i < TR && g * TR + i < R) {
                 tmem_wait_ld(at);
@@ -281,7 +306,9 @@ __global__ void __launch_bounds__(NW * 32, 1) k_iterate_resident(IterArgs p) {
         {
             const int ri = res_row_of<PP>(lane);
             if ((lane & (32 / PP - 1)) == 0 && ri < P) {
-                const int i = ri < TR ? g * TR + ri : kResTmemRows + g * SR + (ri - TR);
+                const int i = ri < TR ? g * TR + ri
+                            : (ri < TR + RR ? kResTmemRows + g * RR + (ri - TR)
+                                            : kResTmemRows + G * RR + g * SR + (ri - TR - RR));
                 yq[q * 32 + i] = rv;
             }
         }
@@ -289,42 +316,30 @@ __global__ void __launch_bounds__(NW * 32, 1) k_iterate_resident(IterArgs p) {
         // publish this CTA's rows: one 8-byte word per row carries the value AND its iteration tag, so
         // the exchange needs no grid barrier, fence or counter (a reader that sees the tag sees the value)
         RES_STAMP(t, 2);
-        if (warp == 0) {
-            if (lane < R) {
-                const float v = (yq[lane] + yq[32 + lane]) + (yq[64 + lane] + yq[96 + lane]);
-                st_tagged(yb + r0 + lane, ((uint64_t)tag << 32) | __float_as_uint(v));
-            }
-            if constexpr (XM == 1) {
-                __syncwarp();
-                if (lane == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.bar) : "memory");
-            }
-        }
-        if constexpr (XM == 1) {
-            if (tid == 0) {
-                const unsigned int target = (unsigned int)(t + 1) * gridDim.x;
-                unsigned int v;
-                do {
-                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.bar) : "memory");
-                } while (v < target);
-            }
-            __syncthreads();
+        if (warp == 0 && lane < R) {
+            const float v = (yq[lane] + yq[32 + lane]) + (yq[64 + lane] + yq[96 + lane]);
+            st_tagged(yb + r0 + lane, ((uint64_t)tag << 32) | __float_as_uint(v));
         }
         RES_STAMP(t, 3);
-        // gather all of y_t: every thread polls its YR words until they carry this iteration's tag
-        float yr[YR];
+        // gather y_t (this CTA's share: all of it for CL = 1, half for CL = 2): every thread polls its YH
+        // words until they carry this iteration's tag
+        float yr[YH];
+        int rounds = 0;
         {
             uint32_t pending = 0;
 #pragma unroll
-            for (int j = 0; j < YR; ++j) {
+            for (int j = 0; j < YH; ++j) {
                 yr[j] = 0.0f;
-                if (tid + (int64_t)j * NT < n) pending |= 1u << j;
+                if (kb + tid + (int64_t)j * NT < n) pending |= 1u << j;
             }
             while (pending) {
-                uint64_t xv[YR];  // all loads of a round in flight together, then the tag checks
+                ++rounds;
+                uint64_t xv[YH];  // all loads of a round in flight together, then the tag checks
 #pragma unroll
-                for (int j = 0; j < YR; ++j) xv[j] = (pending & (1u << j)) ? ld_tagged(yb + tid + (int64_t)j * NT) : 0;
+                for (int j = 0; j < YH; ++j)
+                    xv[j] = (pending & (1u << j)) ? ld_tagged(yb + kb + tid + (int64_t)j * NT) : 0;
 #pragma unroll
-                for (int j = 0; j < YR; ++j) {
+                for (int j = 0; j < YH; ++j) {
                     if ((pending & (1u << j)) && (uint32_t)(xv[j] >> 32) == tag) {
                         yr[j] = __uint_as_float((uint32_t)xv[j]);
                         pending &= ~(1u << j);
@@ -332,22 +347,27 @@ __global__ void __launch_bounds__(NW * 32, 1) k_iterate_resident(IterArgs p) {
                 }
             }
         }
+        RES_POLLS(t, rounds);
         RES_STAMP(t, 4);
-        // s_t: per-thread fp64 partials in a fixed order, warp butterflies, warps summed in warp order
-        // (the same thread -> element mapping in every CTA: identical s_t everywhere)
-        double yd[YR];  // converted once: the |y| partial and the quotient both use it
-#pragma unroll
-        for (int j = 0; j < YR; ++j) yd[j] = (double)yr[j];
+        // s_t: per-thread fp64 partials in a fixed order, warp butterflies, then the CL x NW warp partials
+        // (half 0's warps, then half 1's) in a fixed tree: the same element -> thread mapping in every CTA
+        // and cluster gives identical s_t everywhere
         {
             double ap = 0.0;
 #pragma unroll
-            for (int j = 0; j < YR; ++j) ap += (OP == 2) ? yd[j] * yd[j] : fabs(yd[j]);
+            for (int j = 0; j < YH; ++j) {
+                const double yd = (double)yr[j];
+                ap += (OP == 2) ? yd * yd : fabs(yd);
+            }
             ap = warp_sum(ap);
-            if (lane == 0) wsum[warp] = ap;
+            if (lane == 0) {
+                wsum[half * NW + warp] = ap;
+                if constexpr (CL == 2) st_cluster_f64(&wsum[half * NW + warp], half ^ 1u, ap);
+            }
         }
-        __syncthreads();
+        if constexpr (CL == 2) cluster_sync_all(); else __syncthreads();
         RES_STAMP(t, 5);
-        const double s = norm_final<OP>(res_tree<NW>(wsum));
+        const double s = norm_final<OP>(res_tree<CL * NW>(wsum));
         if (!(s > 0.0) || isinf(s)) {  // uniform across the grid
             status = (s == 0.0) ? kStDegenerate : kStNonfinite;
             break;
@@ -357,26 +377,31 @@ __global__ void __launch_bounds__(NW * 32, 1) k_iterate_resident(IterArgs p) {
         // exact error: |q - y/s_t| ~ 2^-47 |q|, so the fp32 result equals fp32(y / s_t) except when y/s_t
         // lies within ~2^-47 (relative) of an fp32 rounding boundary.  No fp64 conversion per element
         // (F2F is the bottleneck of a per-element fp64 quotient: 4096 per CTA per iteration).  delta_t:
-        // fp32 |w_{t+1} - w_t| per element, fp32 within a thread (YR terms), fp64 across threads.
+        // fp32 |w_{t+1} - w_t| per element, fp32 within a thread (YH terms), fp64 across threads.
         // Branch-free over the padded 4096: beyond n, y = 0 and w_s = 0, so w stays 0 and adds 0 to delta.
         const double rs = 1.0 / s;
         const float rh = (float)rs, rl = (float)(rs - (double)rh);
         float dv = 0.0f;
 #pragma unroll
-        for (int j = 0; j < YR; ++j) {
-            const int k = tid + j * NT;
+        for (int j = 0; j < YH; ++j) {
+            const int k = (int)kb + tid + j * NT;
             const float pj = yr[j] * rh;
             const float wn = pj + fmaf(yr[j], rl, fmaf(yr[j], rh, -pj));
             dv += fabsf(wn - w_s[k]);
             w_s[k] = wn;
+            if constexpr (CL == 2) st_cluster(&w_s[k], half ^ 1u, wn);
         }
         double dpart = (double)dv;
         RES_STAMP(t, 7);
         dpart = warp_sum(dpart);
-        if (lane == 0) dsum[warp] = dpart;
-        __syncthreads();  // also orders the w_s writes before load_w
+        if (lane == 0) {
+            dsum[half * NW + warp] = dpart;
+            if constexpr (CL == 2) st_cluster_f64(&dsum[half * NW + warp], half ^ 1u, dpart);
+        }
+        // orders the w_s writes (both halves) before load_w
+        if constexpr (CL == 2) cluster_sync_all(); else __syncthreads();
         RES_STAMP(t, 6);
-        const double delta = res_tree<NW>(dsum);
+        const double delta = res_tree<CL * NW>(dsum);
         if (blockIdx.x == 0 && tid == 0) {
             if (p.norms) p.norms[t] = (float)s;
             if (p.deltas) p.deltas[t] = (float)delta;
@@ -385,6 +410,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_iterate_resident(IterArgs p) {
         if (p.tol > 0.0f && delta < (double)p.tol) break;
         load_w();
     }
+    if constexpr (CL == 2) cluster_sync_all();  // no DSMEM access may target an exited CTA
     for (int64_t k = r0 + tid; k < r1; k += NT) p.w_out[k] = w_s[k];
     if (blockIdx.x == 0 && tid == 0) {
         p.status[0] = status;

@@ -1,17 +1,17 @@
 // probe_k2r.cu — per-phase cycle breakdown of the K2r on-chip-resident iteration (investigation only):
 // compiled with -DMAPI_RES_TRACE so CTA 0 / thread 0 stamps clock64 at: iteration start, pass done,
-// after the first __syncthreads, y published (+ barrier for XM=1), y gathered, s_t known, delta_t known.
-// n = 4096 (cfg2 size), random data, 200 iterations; both exchange modes and warp counts.
+// after the first __syncthreads, y published, y gathered, s_t known, quotients done, delta_t known.
+// n = 4096 (cfg2 size), random data, 200 iterations; warp counts, register rows (RR), cluster-pair epilogue (CL).
 #include <cstdio>
 #include <vector>
 #include "../paper_2110_12065_b200/csrc/resident.cuh"
 using namespace mapi;
 
-template <int NW, int XM>
+template <int NW, int CL, int RR = 0>
 void run(float* A, float* b0, float* w, float* y, float* norms, float* deltas, double* slots, unsigned* bar, int* st,
          int n, int T, int grid) {
-    auto kern = k_iterate_resident<0, NW, XM>;
-    const size_t smem = resident_smem_bytes();
+    auto kern = k_iterate_resident<0, NW, CL, RR>;
+    const size_t smem = resident_smem_bytes(kResSmemRows - (NW / 4) * RR);
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     IterArgs a{};
     a.A = A; a.n = n; a.lda = n; a.b0 = b0; a.iters = T; a.tol = 0; a.w_out = w; a.norms = norms; a.deltas = deltas;
@@ -22,9 +22,15 @@ void run(float* A, float* b0, float* w, float* y, float* norms, float* deltas, d
     for (int rep = 0; rep < 3; ++rep) {
         cudaMemset(bar, 0, 256);
         cudaMemset(y, 0, 16 * n);
-        void* args[] = {&a};
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(grid); cfg.blockDim = dim3(NW * 32); cfg.dynamicSmemBytes = smem;
+        cudaLaunchAttribute at[2];
+        at[0].id = cudaLaunchAttributeCooperative; at[0].val.cooperative = 1;
+        at[1].id = cudaLaunchAttributeClusterDimension;
+        at[1].val.clusterDim.x = CL; at[1].val.clusterDim.y = 1; at[1].val.clusterDim.z = 1;
+        cfg.attrs = at; cfg.numAttrs = 2;
         cudaEventRecord(e0);
-        cudaError_t e = cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(NW * 32), args, smem, 0);
+        cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a);
         cudaEventRecord(e1);
         if (e != cudaSuccess) { printf("launch: %s\n", cudaGetErrorString(e)); return; }
         if ((e = cudaDeviceSynchronize()) != cudaSuccess) { printf("sync: %s\n", cudaGetErrorString(e)); return; }
@@ -39,10 +45,20 @@ void run(float* A, float* b0, float* w, float* y, float* norms, float* deltas, d
         for (int k = 0; k < 7; ++k) ph[k] += h[t * 8 + ord[k + 1]] - h[t * 8 + ord[k]];
         tot += h[(t + 1) * 8] - h[t * 8];
     }
-    printf("K2r NW=%d XM=%d: %.2f us/iteration (events, incl. staging) | cycles: pass %.0f | reduce+sync %.0f | "
-           "publish%s %.0f | gather y %.0f | |y| partial + sync %.0f | s, 1/s, quotients, delta partial %.0f | "
+    {
+        std::vector<int> pr(148 * 512);
+        cudaMemcpyFromSymbol(pr.data(), g_res_polls, 4 * 148 * 512);
+        double m0 = 0, mall = 0; int mx = 0;
+        for (int t = 20; t < T - 1; ++t) {
+            m0 += pr[t];
+            for (int c = 0; c < grid; ++c) { mall += pr[c * 512 + t]; mx = pr[c * 512 + t] > mx ? pr[c * 512 + t] : mx; }
+        }
+        printf("  poll rounds: CTA0 mean %.2f, all-CTA mean %.2f, max %d\n", m0 / (T - 21), mall / (T - 21) / grid, mx);
+    }
+    printf("K2r NW=%d CL=%d RR=%d: %.2f us/iteration (events, incl. staging) | cycles: pass %.0f | reduce+sync %.0f | "
+           "publish %.0f | gather y %.0f | |y| partial + sync %.0f | s, 1/s, quotients, delta partial %.0f | "
            "delta reduce + sync %.0f | total %.0f\n",
-           NW, XM, 1e3 * ms / T, ph[0] / cnt, ph[1] / cnt, XM ? "+barrier" : "", ph[2] / cnt, ph[3] / cnt, ph[4] / cnt,
+           NW, CL, RR, 1e3 * ms / T, ph[0] / cnt, ph[1] / cnt, ph[2] / cnt, ph[3] / cnt, ph[4] / cnt,
            ph[5] / cnt, ph[6] / cnt, tot / cnt);
 }
 
@@ -85,9 +101,10 @@ int main() {
         cudaEventElapsedTime(&ms, e0, e1);
         printf("1.0/x (DDIV): %.2f lane-ops/clk/SM at 1965 MHz\n", 1.0 * 10000 * sms * 2 * 1024 / (ms * 1e-3) / sms / 1.965e9);
     }
-    run<16, 0>(A, b0, w, y, norms, deltas, slots, bar, st, n, T, sms);
-    run<16, 1>(A, b0, w, y, norms, deltas, slots, bar, st, n, T, sms);
-    run<8, 0>(A, b0, w, y, norms, deltas, slots, bar, st, n, T, sms);
-    run<8, 1>(A, b0, w, y, norms, deltas, slots, bar, st, n, T, sms);
+    run<8, 1, 0>(A, b0, w, y, norms, deltas, slots, bar, st, n, T, sms);
+    run<8, 1, 1>(A, b0, w, y, norms, deltas, slots, bar, st, n, T, sms);
+    run<8, 1, 2>(A, b0, w, y, norms, deltas, slots, bar, st, n, T, sms);
+    run<8, 2, 2>(A, b0, w, y, norms, deltas, slots, bar, st, n, T, sms);
+    run<16, 1, 0>(A, b0, w, y, norms, deltas, slots, bar, st, n, T, sms);
     return 0;
 }
