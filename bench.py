@@ -569,22 +569,40 @@ def run_mapi(args, rank, world, local_rank):
 
 
 def e2e_dense(args, m, A, b0, iters, dev, stream, world, dist):
-    """End to end through the public host API, pipelined the way a server runs a stream of problems:
-    mapi_iterate_host_many (one call for the timed steps) copies each step's A and b0 from pinned host
-    memory on a copy stream while the previous step iterates, and copies each w + trace back."""
+    """End to end through the public host API, pipelined the way a server runs a stream of problems: each
+    step's matrix and b0 go from pinned host memory to the device on a copy stream while the previous step
+    iterates, and each w + trace comes back.  A symmetric matrix (cfg3's covariance-like A, exactly
+    symmetric by construction) travels as its packed upper triangle (mapi_iterate_host_many_packed: half
+    the PCIe bytes, unpacked bitwise on the device); any other matrix as a whole (mapi_iterate_host_many)."""
     import torch
 
     n, lda = A.shape[0], A.stride(0)
-    A_h = torch.empty((n, lda), dtype=torch.float32, pin_memory=True)
-    A_h.copy_(A.as_strided((n, lda), (lda, 1)) if lda == n else A)
+    sym = lda == n and bool(torch.equal(A, A.t()))
     b0_h = b0.cpu().pin_memory()
     steps = max(2, min(args.steps, 10))
     outs = [torch.empty(n, dtype=torch.float32, pin_memory=True) for _ in range(steps)]
-    need = int(m.load().mapi_workspace_size(m.WS_ITERATE_HOST_MANY, n, lda, iters)) + 8 * steps
+    if sym:
+        A_h = m.pack_upper(A.cpu(), out=torch.empty(n * (n + 1) // 2, dtype=torch.float32, pin_memory=True))
+        need = int(m.load().mapi_workspace_size(m.WS_ITERATE_HOST_MANY_PACKED, n, 0, iters)) + 8 * steps
+        h2d = 4 * (n * (n + 1) // 2) + 4 * n
+        path = ("mapi_iterate_host_many_packed: per step, the pinned host matrix as its packed upper triangle "
+                "(n(n+1)/2 floats) + b0 -> device on a copy stream overlapping the previous step's iterations, "
+                "bitwise unpack on the device (k_unpack_sym), 100 iterations, w + trace -> host")
+    else:
+        A_h = torch.empty((n, lda), dtype=torch.float32, pin_memory=True)
+        A_h.copy_(A.as_strided((n, lda), (lda, 1)) if lda == n else A)
+        need = int(m.load().mapi_workspace_size(m.WS_ITERATE_HOST_MANY, n, lda, iters)) + 8 * steps
+        h2d = 4 * n * lda + 4 * n
+        path = ("mapi_iterate_host_many: per step, pinned host A,b0 -> device (copy stream, overlapping the "
+                "previous step's iterations), 100 iterations, w + trace -> host")
     ws = torch.empty(need, dtype=torch.uint8, device=dev)
 
     def run(count):
-        m.iterate_host_many([A_h] * count, [b0_h] * count, iters, outs=outs[:count], ws=ws, stream=stream)
+        if sym:
+            m.iterate_host_many_packed([A_h] * count, n, [b0_h] * count, iters, outs=outs[:count], ws=ws,
+                                       stream=stream)
+        else:
+            m.iterate_host_many([A_h] * count, [b0_h] * count, iters, outs=outs[:count], ws=ws, stream=stream)
 
     run(2)  # warm-up
     torch.cuda.synchronize()
@@ -600,10 +618,8 @@ def e2e_dense(args, m, A, b0, iters, dev, stream, world, dist):
     ms = max_over_ranks(ev0.elapsed_time(ev1), dev)
     del ws, A_h
     return {"value": world * iters * steps / (ms / 1e3), "unit": "iterations/s",
-            "h2d_bytes_per_step": 4 * n * lda + 4 * n, "d2h_bytes_per_step": 4 * n + 8 * iters + 8,
-            "steps": steps, "ms_per_step": ms / steps,
-            "path": "mapi_iterate_host_many: per step, pinned host A,b0 -> device (copy stream, overlapping the "
-                    "previous step's iterations), 100 iterations, w + trace -> host"}
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 4 * n + 8 * iters + 8,
+            "steps": steps, "ms_per_step": ms / steps, "path": path}
 
 
 def e2e_sharded(args, m, A_local, b0, iters, dev, stream, world, run=None):

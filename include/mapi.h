@@ -70,7 +70,8 @@ typedef enum {
     MAPI_WS_MAVP_DEFLATE = 7, /* n = M */
     MAPI_WS_RECONSTRUCT = 8,  /* n = M, nnz = N (images), k = r (components) */
     MAPI_WS_ITERATE_SHARDED = 9,
-    MAPI_WS_ITERATE_HOST_MANY = 10  /* n, nnz = lda, k = iters; add 8 bytes per problem beyond 2 */
+    MAPI_WS_ITERATE_HOST_MANY = 10, /* n, nnz = lda, k = iters; add 8 bytes per problem beyond 2 */
+    MAPI_WS_ITERATE_HOST_MANY_PACKED = 11 /* n, k = iters; add 8 bytes per problem beyond 2 */
 } mapi_ws_op;
 
 /* y = A (op) x — the matrix extension of the MAVP (reading Q6: y_j uses ROW j):
@@ -178,6 +179,19 @@ mapi_status mapi_iterate_host_many(int32_t op, int32_t count, const float *const
                                    float *const *deltas_hosts, int32_t *iters_done, void *ws, size_t ws_bytes,
                                    mapi_stream_t stream);
 
+/* mapi_iterate_host_many for SYMMETRIC matrices (the covariance inputs of Eq. 2 / Eq. 5) sent in
+ * packed upper-triangular form: Ap_hosts[i] holds n(n+1)/2 floats, row j = A[j][j..n-1] at offset
+ * j*n - j*(j-1)/2 (LAPACK "packed" storage, row-major).  Half the host->device bytes of the full matrix;
+ * the device rebuilds the full row-major matrix bitwise (A[k][j] = A[j][k]) before iterating, so results are
+ * bitwise those of mapi_iterate_host_many on the full matrix.  The library does not check symmetry: it is
+ * the caller's declaration by choosing this entry point.  ws: mapi_workspace_size(
+ * MAPI_WS_ITERATE_HOST_MANY_PACKED, n, 0, iters) + 8 * max(0, count - 2) bytes.  Synchronises `stream`. */
+mapi_status mapi_iterate_host_many_packed(int32_t op, int32_t count, const float *const *Ap_hosts, int64_t n,
+                                          const float *const *b0_hosts, int32_t iters, float tol,
+                                          float *const *w_out_hosts, float *const *norms_hosts,
+                                          float *const *deltas_hosts, int32_t *iters_done, void *ws,
+                                          size_t ws_bytes, mapi_stream_t stream);
+
 /* Batched MAPI: k independent runs of mapi_iterate on the same A ("multiple independent
  * runs"; matrix extension P:69-70 with p = k columns), Y = A (op) W each iteration.
  * B0, W_out: k x n, vector-major (vector v at B0 + v*n).  norms, deltas: iters x k
@@ -251,7 +265,8 @@ mapi_status mapi_rank_csr(int64_t n, int64_t nnz, const int32_t *row_ptr, const 
  *   MAPI_WS_ITERATE_HOST: n, and nnz = lda (the device copy of A is n*lda floats), k = iters.
  *   MAPI_WS_MAVP_DEFLATE: n = M.  MAPI_WS_RECONSTRUCT: n = M, nnz = N, k = r.
  *   MAPI_WS_ITERATE_SHARDED: 256 (status words).
- *   MAPI_WS_ITERATE_HOST_MANY: n, nnz = lda, k = iters (two slots; + 8 bytes per problem beyond 2). */
+ *   MAPI_WS_ITERATE_HOST_MANY: n, nnz = lda, k = iters (two slots; + 8 bytes per problem beyond 2).
+ *   MAPI_WS_ITERATE_HOST_MANY_PACKED: n, k = iters (same, plus a packed buffer per slot). */
 size_t mapi_workspace_size(int32_t op, int64_t n, int64_t nnz, int32_t k);
 
 const char *mapi_status_string(mapi_status status);

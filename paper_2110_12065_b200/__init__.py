@@ -21,11 +21,12 @@ from ._build import build  # noqa: F401  (re-exported: compile in-tree)
 __all__ = ["load", "build", "MapiError", "mavp_matvec", "mavp_matmat", "min_covariance", "center_rows", "mavp_deflate",
            "mavp_reconstruct", "iterate", "iterate_host", "iterate_batched",
            "pca_topk", "csr_prepare", "rank_csr", "workspace_size", "launch_count", "set_profiling",
-           "last_kernel_ms", "MIN1", "MIN2", "DOT", "iterate_host_many"]
+           "last_kernel_ms", "MIN1", "MIN2", "DOT", "iterate_host_many", "iterate_host_many_packed", "pack_upper"]
 
 MIN1, MIN2, DOT = 0, 1, 2  # DOT: regular product of Eq. (1), the RPI comparator
 (WS_MATVEC, WS_ITERATE, WS_ITERATE_BATCHED, WS_PCA_TOPK, WS_CSR_PREPARE, WS_RANK_CSR, WS_ITERATE_HOST,
- WS_MAVP_DEFLATE, WS_RECONSTRUCT, WS_ITERATE_SHARDED, WS_ITERATE_HOST_MANY) = range(11)
+ WS_MAVP_DEFLATE, WS_RECONSTRUCT, WS_ITERATE_SHARDED, WS_ITERATE_HOST_MANY,
+ WS_ITERATE_HOST_MANY_PACKED) = range(12)
 STATUS = {0: "MAPI_OK", 1: "MAPI_ERR_NULL", 2: "MAPI_ERR_SHAPE", 3: "MAPI_ERR_BAD_PARAM",
           4: "MAPI_ERR_DEGENERATE", 5: "MAPI_ERR_NEGATIVE", 6: "MAPI_ERR_NONFINITE",
           7: "MAPI_ERR_WORKSPACE", 8: "MAPI_ERR_CUDA"}
@@ -66,6 +67,7 @@ def load():
             "mapi_iterate": (st, [i32, P, i64, i64, P, i32, f32, P, P, P, P, P, P, sz, P]),
             "mapi_iterate_host": (st, [i32, P, i64, i64, P, i32, f32, P, P, P, P, P, P, sz, P]),
             "mapi_iterate_host_many": (st, [i32, i32, P, i64, i64, P, i32, f32, P, P, P, P, P, sz, P]),
+            "mapi_iterate_host_many_packed": (st, [i32, i32, P, i64, P, i32, f32, P, P, P, P, P, sz, P]),
             "mapi_iterate_batched": (st, [i32, P, i64, i64, P, i32, i32, f32, P, P, P, P, P, sz, P]),
             "mapi_pca_topk": (st, [i32, P, i64, i64, i32, i32, P, P, P, P, P, sz, P]),
             "mapi_csr_prepare": (st, [i64, i64, P, P, f32, P, P, P, sz, P]),
@@ -336,6 +338,60 @@ def iterate_host_many(As, b0s, iters: int, tol: float = 0.0, op: int = MIN1, ws=
     st = lib.mapi_iterate_host_many(op, count, arr(As), n, lda, arr(b0s), int(iters), float(tol), arr(outs),
                                     arr(norms) if norms else None, arr(deltas) if deltas else None, done,
                                     _ptr(ws), ws.numel(), _stream(stream))
+    _check(st)
+    res = []
+    for i in range(count):
+        k = done[i]
+        res.append(IterResult(outs[i], None, norms[i][:k] if norms else None, deltas[i][:k] if deltas else None, k))
+    return res
+
+
+def pack_upper(A, out=None):
+    """Host-side input preparation for iterate_host_many_packed: the upper triangle of a symmetric n x n
+    fp32 CPU matrix in packed row-major order (row j = A[j, j:], LAPACK "packed" layout), n(n+1)/2 floats.
+    Pure data movement (no arithmetic); `out` may be a pinned 1-D fp32 tensor to fill."""
+    torch = _torch()
+    A = torch.as_tensor(A)
+    if A.dim() != 2 or A.shape[0] != A.shape[1] or A.dtype != torch.float32 or A.is_cuda:
+        raise ValueError("A must be a square fp32 CPU matrix")
+    n = A.shape[0]
+    out = out if out is not None else torch.empty(n * (n + 1) // 2, dtype=torch.float32)
+    if out.numel() != n * (n + 1) // 2:
+        raise ValueError("out must hold n(n+1)/2 floats")
+    off = 0
+    for j in range(n):
+        out[off:off + n - j].copy_(A[j, j:])
+        off += n - j
+    return out
+
+
+def iterate_host_many_packed(Aps, n: int, b0s, iters: int, tol: float = 0.0, op: int = MIN1, ws=None, outs=None,
+                             want_trace: bool = True, stream=None) -> list:
+    """iterate_host_many for symmetric matrices sent as packed upper triangles (pack_upper): half the
+    host->device bytes; the device rebuilds each full matrix bitwise before iterating
+    (mapi_iterate_host_many_packed).  Returns one IterResult per problem; synchronises the stream."""
+    torch = _torch()
+    count = len(Aps)
+    if count < 1 or len(b0s) != count:
+        raise ValueError("need >= 1 problem and one b0 per problem")
+    for Ap, b in zip(Aps, b0s):
+        if Ap.is_cuda or b.is_cuda or Ap.dtype != torch.float32 or not Ap.is_contiguous():
+            raise ValueError("Aps must be contiguous fp32 CPU tensors (pinned for overlap)")
+        if Ap.numel() != n * (n + 1) // 2 or b.numel() != n:
+            raise ValueError(f"each packed matrix must hold n(n+1)/2 = {n * (n + 1) // 2} floats and b0 n floats")
+    outs = outs if outs is not None else [torch.empty(n, dtype=torch.float32) for _ in range(count)]
+    pin = torch.cuda.is_available()
+    norms = [torch.zeros(iters, dtype=torch.float32, pin_memory=pin) for _ in range(count)] if want_trace else None
+    deltas = [torch.zeros(iters, dtype=torch.float32, pin_memory=pin) for _ in range(count)] if want_trace else None
+    lib = load()
+    need = int(lib.mapi_workspace_size(WS_ITERATE_HOST_MANY_PACKED, n, 0, iters)) + 8 * max(0, count - 2)
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(need, dtype=torch.uint8, device="cuda")
+    arr = lambda ts: (ctypes.c_void_p * count)(*[t.data_ptr() for t in ts])  # noqa: E731
+    done = (ctypes.c_int32 * count)()
+    st = lib.mapi_iterate_host_many_packed(op, count, arr(Aps), n, arr(b0s), int(iters), float(tol), arr(outs),
+                                           arr(norms) if norms else None, arr(deltas) if deltas else None, done,
+                                           _ptr(ws), ws.numel(), _stream(stream))
     _check(st)
     res = []
     for i in range(count):

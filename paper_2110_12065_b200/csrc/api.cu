@@ -15,6 +15,7 @@
 #include "batched.cuh"
 #include "bulk.cuh"
 #include "resident.cuh"
+#include "packed.cuh"
 #include "csr.cuh"
 #include "deflate.cuh"
 #include "dense.cuh"
@@ -585,11 +586,15 @@ float mapi_last_kernel_ms(void) { return g_last_kernel_ms; }
 
 // count independent host problems, pipelined: problem i+1's A / b0 host->device copies (a second, copy
 // stream) overlap problem i's iterations (the compute stream); two device slots alternate.
-size_t iterate_host_many_ws_bytes(int64_t n, int64_t lda, int32_t iters, int32_t count) {
+// packed: each slot also holds the packed upper triangle (n(n+1)/2 floats) the host sends
+size_t iterate_host_many_ws_bytes(int64_t n, int64_t lda, int32_t iters, int32_t count, bool packed = false) {
     const size_t slot = align256(sizeof(float) * (size_t)n * (size_t)lda) + 2 * align256(sizeof(float) * (size_t)n) +
-                        2 * align256(sizeof(float) * (size_t)std::max(iters, 1));
+                        2 * align256(sizeof(float) * (size_t)std::max(iters, 1)) +
+                        (packed ? align256(sizeof(float) * (size_t)packed_floats(n)) : 0);
     return iterate_ws_bytes(n) + 2 * slot + sizeof(int32_t) * 2 * (size_t)std::max(count, 2);
 }
+// device leading dimension of the unpacked matrix: 32 B-aligned rows (the 256-bit load path)
+inline int64_t packed_lda(int64_t n) { return (n + 7) & ~int64_t(7); }
 
 size_t mapi_workspace_size(int32_t op, int64_t n, int64_t nnz, int32_t k) {
     if (n < 0) n = 0;
@@ -612,6 +617,7 @@ size_t mapi_workspace_size(int32_t op, int64_t n, int64_t nnz, int32_t k) {
     case MAPI_WS_RANK_CSR: return csr_rank_ws_bytes(n, nnz);
     case MAPI_WS_ITERATE_SHARDED: return 256;
     case MAPI_WS_ITERATE_HOST_MANY: return iterate_host_many_ws_bytes(n, nnz, k, 2);
+    case MAPI_WS_ITERATE_HOST_MANY_PACKED: return iterate_host_many_ws_bytes(n, packed_lda(n), k, 2, true);
     }
     return 0;
 }
@@ -805,17 +811,20 @@ mapi_status mapi_iterate_host(int32_t op, const float* A_host, int64_t n, int64_
     return st;
 }
 
-mapi_status mapi_iterate_host_many(int32_t op, int32_t count, const float* const* A_hosts, int64_t n, int64_t lda,
-                                   const float* const* b0_hosts, int32_t iters, float tol, float* const* w_out_hosts,
-                                   float* const* norms_hosts, float* const* deltas_hosts, int32_t* iters_done,
-                                   void* ws, size_t ws_bytes, mapi_stream_t stream) {
+// packed = true: A_hosts[i] are packed upper triangles (n(n+1)/2 floats), unpacked on the device into an
+// n x packed_lda(n) matrix before the iterations (lda is ignored)
+static mapi_status host_many_impl(int32_t op, int32_t count, const float* const* A_hosts, int64_t n, int64_t lda,
+                                  const float* const* b0_hosts, int32_t iters, float tol, float* const* w_out_hosts,
+                                  float* const* norms_hosts, float* const* deltas_hosts, int32_t* iters_done,
+                                  void* ws, size_t ws_bytes, mapi_stream_t stream, bool packed) {
     if (count < 1) return fail(MAPI_ERR_BAD_PARAM, "count (%d) must be >= 1", count);
     if (!A_hosts || !b0_hosts || !w_out_hosts) return fail(MAPI_ERR_NULL, "A_hosts / b0_hosts / w_out_hosts is NULL");
+    if (packed) lda = packed_lda(n);
     for (int32_t i = 0; i < count; ++i) {
         mapi_status st = validate_dense(op, A_hosts[i], n, lda, b0_hosts[i], iters, tol, w_out_hosts[i], ws);
         if (st != MAPI_OK) return fail(st, "problem %d: %s", i, g_err);
     }
-    const size_t need = iterate_host_many_ws_bytes(n, lda, iters, count);
+    const size_t need = iterate_host_many_ws_bytes(n, lda, iters, count, packed);
     if (ws_bytes < need) return fail(MAPI_ERR_WORKSPACE, "ws_bytes (%zu) < required (%zu)", ws_bytes, need);
     Device d;
     mapi_status st = device_info(d);
@@ -825,11 +834,16 @@ mapi_status mapi_iterate_host_many(int32_t op, int32_t count, const float* const
     IterWs W = carve_iterate(p, n);
     p += iterate_ws_bytes(n);
     struct Slot {
-        float *A, *b0, *w, *nrm, *dlt;
+        float *A, *b0, *w, *nrm, *dlt, *pk;
     } sl[2];
     for (auto& x : sl) {
         x.A = reinterpret_cast<float*>(p);
         p += align256(sizeof(float) * (size_t)n * (size_t)lda);
+        x.pk = nullptr;
+        if (packed) {
+            x.pk = reinterpret_cast<float*>(p);
+            p += align256(sizeof(float) * (size_t)packed_floats(n));
+        }
         x.b0 = reinterpret_cast<float*>(p);
         p += align256(sizeof(float) * (size_t)n);
         x.w = reinterpret_cast<float*>(p);
@@ -869,7 +883,10 @@ mapi_status mapi_iterate_host_many(int32_t op, int32_t count, const float* const
         cudaError_t r = cudaSuccess;
         if (i >= 2) r = cudaStreamWaitEvent(cs, freed[i & 1], 0);
         if (r == cudaSuccess)
-            r = cudaMemcpyAsync(x.A, A_hosts[i], sizeof(float) * (size_t)n * (size_t)lda, cudaMemcpyHostToDevice, cs);
+            r = packed ? cudaMemcpyAsync(x.pk, A_hosts[i], sizeof(float) * (size_t)packed_floats(n),
+                                         cudaMemcpyHostToDevice, cs)
+                       : cudaMemcpyAsync(x.A, A_hosts[i], sizeof(float) * (size_t)n * (size_t)lda,
+                                         cudaMemcpyHostToDevice, cs);
         if (r == cudaSuccess) r = cudaMemcpyAsync(x.b0, b0_hosts[i], sizeof(float) * (size_t)n, cudaMemcpyHostToDevice, cs);
         if (r == cudaSuccess) r = cudaEventRecord(loaded[i & 1], cs);
         return r;
@@ -879,6 +896,13 @@ mapi_status mapi_iterate_host_many(int32_t op, int32_t count, const float* const
         Slot& x = sl[i & 1];
         e = cudaStreamWaitEvent(s, loaded[i & 1], 0);
         if (e != cudaSuccess) break;
+        if (packed) {
+            const int64_t nb = (n + kPackTile - 1) / kPackTile;
+            const int64_t tiles = nb * (nb + 1) / 2;
+            k_unpack_sym<<<(unsigned)std::min<int64_t>(tiles, (int64_t)d.sms * 8), 256, 0, s>>>(x.pk, n, x.A, lda);
+            g_launches.fetch_add(1, std::memory_order_relaxed);
+            if ((e = cudaGetLastError()) != cudaSuccess) break;
+        }
         st = iterate_launch(d, op, x.A, n, lda, x.b0, iters, tol, x.w, x.nrm, x.dlt, W, s, nullptr);
         if (st != MAPI_OK) break;
         // queue the next problem's copy before this one's read-back (a pageable read-back may block the host)
@@ -908,6 +932,23 @@ mapi_status mapi_iterate_host_many(int32_t op, int32_t count, const float* const
                         h[2 * i] == MAPI_ERR_DEGENERATE ? "||A (op) w||_1 == 0" : "non-finite norm", h[2 * i + 1]);
     }
     return MAPI_OK;
+}
+
+mapi_status mapi_iterate_host_many(int32_t op, int32_t count, const float* const* A_hosts, int64_t n, int64_t lda,
+                                   const float* const* b0_hosts, int32_t iters, float tol, float* const* w_out_hosts,
+                                   float* const* norms_hosts, float* const* deltas_hosts, int32_t* iters_done,
+                                   void* ws, size_t ws_bytes, mapi_stream_t stream) {
+    return host_many_impl(op, count, A_hosts, n, lda, b0_hosts, iters, tol, w_out_hosts, norms_hosts, deltas_hosts,
+                          iters_done, ws, ws_bytes, stream, false);
+}
+
+mapi_status mapi_iterate_host_many_packed(int32_t op, int32_t count, const float* const* Ap_hosts, int64_t n,
+                                          const float* const* b0_hosts, int32_t iters, float tol,
+                                          float* const* w_out_hosts, float* const* norms_hosts,
+                                          float* const* deltas_hosts, int32_t* iters_done, void* ws, size_t ws_bytes,
+                                          mapi_stream_t stream) {
+    return host_many_impl(op, count, Ap_hosts, n, 0, b0_hosts, iters, tol, w_out_hosts, norms_hosts, deltas_hosts,
+                          iters_done, ws, ws_bytes, stream, true);
 }
 
 mapi_status mapi_pca_topk(int32_t op, const float* C, int64_t n, int64_t ldc, int32_t k, int32_t iters,

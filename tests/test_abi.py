@@ -8,6 +8,7 @@ import re
 import shutil
 import subprocess
 
+import numpy as np
 import pytest
 
 import paper_2110_12065_b200 as m
@@ -106,6 +107,28 @@ def test_validation_before_device(lib):
     assert st == 1
     st = lib.mapi_iterate_host_many(0, 1, arr, 4, 4, arr, 5, 0.0, arr, None, None, None, fake, 16, None)
     assert st == 7
+    # packed symmetric host problems: same validation (lda is derived from n)
+    st = lib.mapi_iterate_host_many_packed(0, 0, arr, 4, arr, 5, 0.0, arr, None, None, None, fake, 1 << 20, None)
+    assert st == 3 and "count" in _err(lib)
+    st = lib.mapi_iterate_host_many_packed(0, 1, arr, 0, arr, 5, 0.0, arr, None, None, None, fake, 1 << 20, None)
+    assert st == 2
+    st = lib.mapi_iterate_host_many_packed(0, 1, arr, 4, arr, 5, 0.0, arr, None, None, None, fake, 16, None)
+    assert st == 7
+    assert m.workspace_size(m.WS_ITERATE_HOST_MANY_PACKED, 1000, 0, 50) >= \
+        m.workspace_size(m.WS_ITERATE_HOST_MANY, 1000, 1000, 50) + 2 * 4 * 1000 * 1001 // 2
+
+
+def test_pack_upper_layout():
+    """pack_upper: row j of the packed buffer is A[j, j:], rows back to back (offset j n - j (j-1) / 2),
+    checked against numpy's triu index order on odd / even sizes."""
+    for n in (1, 2, 7, 64, 101):
+        A = np.arange(n * n, dtype=np.float32).reshape(n, n)
+        got = m.pack_upper(A).numpy()
+        iu = np.triu_indices(n)
+        assert np.array_equal(got, A[iu])
+        for j in (0, n // 2, n - 1):
+            off = j * n - j * (j - 1) // 2
+            assert np.array_equal(got[off:off + n - j], A[j, j:])
 
 
 def test_p2p_exchange_layout_and_new_workspaces(lib):

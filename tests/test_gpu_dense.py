@@ -460,3 +460,26 @@ def test_iterate_host_many_pipelined(mapi_lib):
     with pytest.raises(m.MapiError) as ei:
         m.iterate_host_many(bad, b0s[:3], 5)
     assert ei.value.name == "MAPI_ERR_DEGENERATE" and "problem 1" in str(ei.value)
+
+
+@pytest.mark.parametrize("n", [1, 7, 33, 256, 1000, 1031, 2600, 5000, 8200])
+def test_iterate_host_many_packed_bitwise(mapi_lib, n):
+    """Symmetric matrices sent as packed upper triangles (half the PCIe bytes): the device-side unpack
+    rebuilds the full matrix bitwise, so every result equals the full-matrix pipelined path bitwise (on
+    every dense kernel the sizes select: cluster, per-row, resident, bulk, cooperative)."""
+    m = mapi_lib
+    r = np.random.default_rng(n + 17)
+    As, Aps, b0s = [], [], []
+    for i in range(3):
+        G = r.standard_normal((n, n)).astype(np.float32)
+        S = np.triu(G) + np.triu(G, 1).T + np.eye(n, dtype=np.float32) * (3 + i)
+        assert np.array_equal(S, S.T)
+        A = torch.from_numpy(S)
+        As.append(A.pin_memory())
+        Aps.append(m.pack_upper(A).pin_memory())
+        b0s.append(torch.full((n,), 1 / np.sqrt(n)).pin_memory())
+    full = m.iterate_host_many(As, b0s, 15)
+    packed = m.iterate_host_many_packed(Aps, n, b0s, 15)
+    for a, b in zip(full, packed):
+        assert a.iters_done == b.iters_done == 15
+        assert torch.equal(a.w, b.w) and torch.equal(a.norms, b.norms) and torch.equal(a.deltas, b.deltas)
