@@ -16,6 +16,7 @@
 #include "bulk.cuh"
 #include "resident.cuh"
 #include "packed.cuh"
+#include "single.cuh"
 #include "csr.cuh"
 #include "deflate.cuh"
 #include "dense.cuh"
@@ -257,6 +258,14 @@ bool use_coop(const Device& d, const float* A, int64_t n, int64_t lda) {
     return coop_smem_bytes(n, (int)grid, coop_warps(n)) <= (size_t)d.smem_optin;
 }
 
+// K6t (single.cuh): one CTA, matrix in registers + TMEM, for n <= 256.  MAPI_DENSE_PATH=single forces it.
+bool use_single(const Device& d, int64_t n) {
+    (void)d;
+    const char* e = dense_path_env();
+    if (n > kSingleN) return false;
+    return strcmp(e, "single") == 0 || e[0] == 0;
+}
+
 // K2r (resident.cuh): the whole matrix on chip (TMEM + shared memory) for n <= 4096 when every CTA's
 // rows fit (ceil(n / grid) <= 28).  MAPI_DENSE_PATH=resident forces it; default range set by measurement.
 bool use_resident(const Device& d, int64_t n) {
@@ -284,6 +293,21 @@ mapi_status iterate_launch(const Device& d, int32_t op, const float* A, int64_t 
     const int vec = vec_width(A, lda);
     const int pol = load_policy(d, n, lda);
     MAPI_CUDA(cudaMemsetAsync(W.bar, 0, 256, s));
+    if (use_single(d, n)) {
+        using KernT = void (*)(IterArgs);
+        KernT kern = op == 2 ? k_iterate_single<2> : (op == 1 ? k_iterate_single<1> : k_iterate_single<0>);
+        IterArgs a;
+        a.A = A; a.n = n; a.lda = lda; a.b0 = b0; a.iters = iters; a.tol = tol;
+        a.w_out = w_out; a.norms = norms; a.deltas = deltas; a.y = W.y; a.slots = W.slots;
+        a.bar = W.bar; a.status = W.status;
+        if (timer) timer->start();
+        kern<<<1, kSingleThreads, 0, s>>>(a);
+        if (timer) timer->stop();
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return fail(MAPI_ERR_CUDA, "single-CTA launch: %s", cudaGetErrorString(e));
+        return MAPI_OK;
+    }
     if (use_cluster(d, n)) {
         // K6r (A in registers) for n <= 512 unless MAPI_DENSE_PATH=cluster_smem; K6 (A in shared memory) above
         const bool reg = n <= 512 && strcmp(dense_path_env(), "cluster_smem") != 0;

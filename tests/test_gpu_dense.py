@@ -248,7 +248,7 @@ def test_cfg3_last_step_and_invariants(mapi_lib, orc, cfg3_device):
     assert torch.equal(r100.w, r100b.w)
 
 
-@pytest.mark.parametrize("path", ["cluster", "cluster_smem", "rows", "coop", "bulk", "resident", "multi"])
+@pytest.mark.parametrize("path", ["single", "cluster", "cluster_smem", "rows", "coop", "bulk", "resident", "multi"])
 @pytest.mark.parametrize("n", [256, 511, 4096, 8200])
 def test_every_dense_path_matches_oracle(mapi_lib, orc, monkeypatch, path, n):
     """Each dense iteration kernel (K6 cluster, K2 per-row, K2c cooperative rows, multi-launch),
@@ -339,6 +339,59 @@ def test_resident_path(mapi_lib, orc, monkeypatch, n, pad, op, nw):
     _t2(got, ref.w, res.norms.cpu().numpy(), ref.norms)
     again = m.iterate(Ad, torch.from_numpy(b0).cuda(), 25, op=opc)
     assert torch.equal(res.w, again.w) and torch.equal(res.deltas, again.deltas)
+
+
+@pytest.mark.parametrize("n,pad", [(1, 0), (2, 1), (7, 0), (31, 3), (100, 4), (128, 0), (129, 8), (255, 1), (256, 0), (256, 5)])
+@pytest.mark.parametrize("op", ["min1", "min2", "dot"])
+def test_single_cta_path(mapi_lib, orc, monkeypatch, n, pad, op):
+    """K6t (one CTA, rows in registers + TMEM; BASELINE configs[0]'s path): ragged n (padded rows and
+    columns), padded lda with NaN padding, every operator, vs the oracle (T2; the RPI limit for dot), bitwise
+    reproducible, and resume: iterate(A, iterate(A, b0, 10).w, 15) == iterate(A, b0, 25)."""
+    m = mapi_lib
+    r = np.random.default_rng(n * 7 + pad)
+    Af = np.full((n, n + pad), np.nan, np.float32)
+    A = r.standard_normal((n, n)).astype(np.float32) + np.diag(np.abs(r.standard_normal(n)) * 4).astype(np.float32)
+    if op == "dot":
+        A = ((A + A.T) / (2 * np.sqrt(n))).astype(np.float32)
+    Af[:, :n] = A
+    b0 = np.full(n, 1.0 / np.sqrt(n), np.float32)
+    monkeypatch.setenv("MAPI_DENSE_PATH", "single")
+    Ad, bd = torch.from_numpy(Af).cuda()[:, :n], torch.from_numpy(b0).cuda()
+    opc = {"min1": m.MIN1, "min2": m.MIN2, "dot": m.DOT}[op]
+    res = m.iterate(Ad, bd, 25, op=opc)
+    ref = orc.rpi(A, b0, 25) if op == "dot" else orc.mapi(A, b0, 25, op=op)
+    assert res.iters_done == 25
+    got = res.w.cpu().numpy() if op == "dot" else res.w_l2.cpu().numpy()
+    if n > 1:
+        _t2(got, ref.w, res.norms.cpu().numpy(), ref.norms)
+    again = m.iterate(Ad, bd, 25, op=opc)
+    assert torch.equal(res.w, again.w) and torch.equal(res.deltas, again.deltas)
+    if op != "dot":
+        first = m.iterate(Ad, bd, 10, op=opc)
+        resumed = m.iterate(Ad, first.w, 15, op=opc)
+        assert torch.equal(resumed.w, res.w)
+
+
+def test_single_cta_early_stop_and_degenerate(mapi_lib, orc, monkeypatch):
+    """tol stop and the degenerate status on K6t (TMEM released on every exit path), then a normal run."""
+    m = mapi_lib
+    monkeypatch.setenv("MAPI_DENSE_PATH", "single")
+    cfg = synth.cfg1()
+    Ad, bd = torch.from_numpy(cfg["A"]).cuda(), torch.from_numpy(cfg["b0"]).cuda()
+    full = m.iterate(Ad, bd, 200)
+    d = full.deltas.cpu().numpy()
+    tol = float(d[40]) * 1.0001
+    first = int(np.nonzero(d < tol)[0][0])
+    res = m.iterate(Ad, bd, 200, tol=tol)
+    assert res.iters_done == first + 1
+    assert torch.equal(res.deltas, full.deltas[: first + 1])
+    ref = orc.mapi(cfg["A"], cfg["b0"], first + 1)
+    _t2(res.w_l2.cpu().numpy(), ref.w)
+    with pytest.raises(m.MapiError) as ei:
+        m.iterate(torch.zeros(256, 256, device="cuda"), bd, 10)
+    assert ei.value.name == "MAPI_ERR_DEGENERATE" and ei.value.iters_done == 0
+    again = m.iterate(Ad, bd, 200)
+    assert torch.equal(again.w, full.w)
 
 
 def test_resident_matvec_t1_each_iteration(mapi_lib, orc, monkeypatch):
