@@ -219,10 +219,13 @@ def build_dense(args, m, dev, stream):
         return iters
 
     big = args.workload == "cfg3"
-    return Work(step=step, unit="iterations/s", per_launch=dense_bytes_per_iter(n, lda) * iters,
-                bytes_per_unit=dense_bytes_per_iter(n, lda), bound="hbm",
+    # cfg3 streams A from HBM every iteration (HBM roofline); cfg1's 256 KiB matrix is staged once into
+    # registers + TMEM of one SM (K6t) and the roofline is the FMNMX issue rate (terms)
+    return Work(step=step, unit="iterations/s",
+                per_launch=dense_bytes_per_iter(n, lda) * iters if big else float(n) * n * iters,
+                bytes_per_unit=dense_bytes_per_iter(n, lda), bound="hbm" if big else "alu",
                 kernel="k_iterate_coop (K2c: one cooperative launch runs all iterations of a step)"
-                if big else "k_iterate_persistent (K2, one cooperative launch per step)",
+                if big else "k_iterate_single (K6t: one CTA, matrix in registers + TMEM, one launch per step)",
                 config={"workload": f"{args.workload}: {WORKLOADS[args.workload]}", "n": n, "lda": lda,
                         "iters_per_step": iters,
                         "op": args.op if args.op != "dot" else "dot (RPI comparator, Eq. 1, l2 normalisation)",

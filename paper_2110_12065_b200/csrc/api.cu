@@ -10,6 +10,7 @@
 #include <cstring>
 #include <type_traits>
 #include <vector>
+#include <memory>
 
 #include "../../include/mapi.h"
 #include "batched.cuh"
@@ -296,12 +297,14 @@ mapi_status iterate_launch(const Device& d, int32_t op, const float* A, int64_t 
     if (use_single(d, n)) {
         using KernT = void (*)(IterArgs);
         KernT kern = op == 2 ? k_iterate_single<2> : (op == 1 ? k_iterate_single<1> : k_iterate_single<0>);
+        const size_t smem = single_smem_bytes();
+        MAPI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         IterArgs a;
         a.A = A; a.n = n; a.lda = lda; a.b0 = b0; a.iters = iters; a.tol = tol;
         a.w_out = w_out; a.norms = norms; a.deltas = deltas; a.y = W.y; a.slots = W.slots;
         a.bar = W.bar; a.status = W.status;
         if (timer) timer->start();
-        kern<<<1, kSingleThreads, 0, s>>>(a);
+        kern<<<1, kSingleThreads, smem, s>>>(a);
         if (timer) timer->stop();
         g_launches.fetch_add(1, std::memory_order_relaxed);
         cudaError_t e = cudaGetLastError();
@@ -512,9 +515,17 @@ mapi_status iterate_launch(const Device& d, int32_t op, const float* A, int64_t 
     return MAPI_OK;
 }
 
+// the two status words come back through a per-thread PINNED buffer (a DMA straight into host memory;
+// a pageable destination goes through a staging copy and costs several microseconds more per call)
 mapi_status read_status(const IterWs& W, cudaStream_t s, int32_t* iters_done) {
-    int32_t h[2] = {0, 0};
-    MAPI_CUDA(cudaMemcpyAsync(h, W.status, sizeof(h), cudaMemcpyDeviceToHost, s));
+    static thread_local int32_t* pinned = nullptr;
+    if (!pinned && cudaHostAlloc(reinterpret_cast<void**>(&pinned), 2 * sizeof(int32_t), cudaHostAllocDefault) != cudaSuccess) {
+        pinned = nullptr;
+        cudaGetLastError();
+    }
+    int32_t local[2] = {0, 0};
+    int32_t* h = pinned ? pinned : local;
+    MAPI_CUDA(cudaMemcpyAsync(h, W.status, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     MAPI_CUDA(cudaStreamSynchronize(s));
     if (iters_done) *iters_done = h[1];
     if (h[0] == MAPI_ERR_DEGENERATE)
@@ -633,7 +644,8 @@ size_t mapi_workspace_size(int32_t op, int64_t n, int64_t nnz, int32_t k) {
     case MAPI_WS_PCA_TOPK:
         return iterate_ws_bytes(n) + align256(sizeof(float) * (size_t)n * (size_t)n) +
                2 * align256(sizeof(double) * (size_t)k * (size_t)n) +
-               align256(sizeof(double) * 64 * (size_t)n) + align256(sizeof(float) * (size_t)n);
+               align256(sizeof(double) * 64 * (size_t)n) + align256(sizeof(float) * (size_t)n) +
+               align256(sizeof(int32_t) * 2 * (size_t)k);
     case MAPI_WS_ITERATE_BATCHED: return batched_ws_bytes(n, k);
     case MAPI_WS_MAVP_DEFLATE: return outer_ws_bytes(n, n, 1, 0);
     case MAPI_WS_RECONSTRUCT: return outer_ws_bytes(n, nnz, k, nnz);
@@ -998,9 +1010,11 @@ mapi_status mapi_pca_topk(int32_t op, const float* C, int64_t n, int64_t ldc, in
     double* part = reinterpret_cast<double*>(p);
     p += align256(sizeof(double) * 64 * (size_t)n);
     float* wtmp = reinterpret_cast<float*>(p);
+    p += align256(sizeof(float) * (size_t)n);
+    int32_t* st_all = reinterpret_cast<int32_t*>(p);  // per-vector (status, iters_done), read back once
     const int S = (int)std::min<int64_t>(64, n);
     const int64_t rows_per = (n + S - 1) / S;
-    float total_ms = 0.0f;
+    std::vector<std::unique_ptr<Timer>> timers;
     for (int32_t i = 0; i < k; ++i) {
         const float* Ai = C;
         int64_t ld = ldc;
@@ -1027,15 +1041,13 @@ mapi_status mapi_pca_topk(int32_t op, const float* C, int64_t n, int64_t ldc, in
             Ai = D;
             ld = n;
         }
-        Timer timer(s);
+        // no host round trip per vector: each vector's status words are copied aside on the stream and
+        // read back once after the last vector (a degenerate vector still reports its index)
+        timers.emplace_back(new Timer(s));
         st = iterate_launch(d, op, Ai, n, ld, b0, iters, 0.0f, wtmp, norms ? norms + (int64_t)i * iters : nullptr,
-                            deltas ? deltas + (int64_t)i * iters : nullptr, W, s, &timer);
+                            deltas ? deltas + (int64_t)i * iters : nullptr, W, s, timers.back().get());
         if (st != MAPI_OK) return st;
-        int32_t done = 0;
-        st = read_status(W, s, &done);
-        timer.harvest();
-        total_ms += g_last_kernel_ms;
-        if (st != MAPI_OK) return fail(st, "vector %d: %s", i, g_err);
+        MAPI_CUDA(cudaMemcpyAsync(st_all + 2 * i, W.status, 2 * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
         k_l2_to_p<<<1, 1024, 0, s>>>(n, wtmp, P64 + (int64_t)i * n, P_out + (int64_t)i * n);
         MAPI_LAUNCHED();
         if (i + 1 < k) {
@@ -1046,8 +1058,21 @@ mapi_status mapi_pca_topk(int32_t op, const float* C, int64_t n, int64_t ldc, in
             MAPI_LAUNCHED();
         }
     }
+    std::vector<int32_t> h(2 * (size_t)k, 0);
+    MAPI_CUDA(cudaMemcpyAsync(h.data(), st_all, sizeof(int32_t) * 2 * (size_t)k, cudaMemcpyDeviceToHost, s));
     MAPI_CUDA(cudaStreamSynchronize(s));
+    float total_ms = 0.0f;
+    for (auto& t : timers) {
+        t->harvest();
+        total_ms += g_last_kernel_ms;
+    }
     if (g_profiling.load()) g_last_kernel_ms = total_ms;
+    for (int32_t i = 0; i < k; ++i) {
+        if (h[2 * i] == MAPI_ERR_DEGENERATE)
+            return fail(MAPI_ERR_DEGENERATE, "vector %d: ||A (+) w_t||_1 == 0 at iteration %d", i, h[2 * i + 1]);
+        if (h[2 * i] == MAPI_ERR_NONFINITE)
+            return fail(MAPI_ERR_NONFINITE, "vector %d: ||A (+) w_t||_1 is not finite at iteration %d", i, h[2 * i + 1]);
+    }
     return MAPI_OK;
 }
 

@@ -24,6 +24,7 @@ namespace mapi {
 constexpr int kSingleN = 256;        // max n
 constexpr int kSingleThreads = 256;  // one row per thread
 constexpr int kSingleRegCols = 128;  // columns held in registers; the rest in TMEM
+inline size_t single_smem_bytes() { return sizeof(float) * kSingleN * (kSingleRegCols + 4); }  // staging
 
 template <int OP>
 __global__ void __launch_bounds__(kSingleThreads, 1) k_iterate_single(IterArgs p) {
@@ -46,20 +47,40 @@ __global__ void __launch_bounds__(kSingleThreads, 1) k_iterate_single(IterArgs p
     const uint32_t tbase = tslot;
     const uint32_t ta = tbase + ((uint32_t)(32 * q) << 16) + (uint32_t)(128 * rh);
 
-    // ---- one-time staging: row r, columns [0, 128) -> registers, [128, 256) -> TMEM (zero beyond n)
-    const float* arow = p.A + (int64_t)(live ? r : 0) * p.lda;
+    // ---- one-time staging, one 128-column half at a time through shared memory: coalesced global reads
+    // (a warp reads consecutive columns of one row), then thread r takes row r (stride 132 floats: the
+    // quarter-warp phases of LDS.128 hit distinct banks).  Half 0 -> registers, half 1 -> TMEM; zero
+    // beyond n.
+    extern __shared__ __align__(16) float stage[];  // kSingleN x kStageLd
+    constexpr int kStageLd = kSingleRegCols + 4;
+    auto stage_half = [&](int h) {
+        for (int e = tid; e < kSingleN * kSingleRegCols; e += kSingleThreads) {
+            const int row = e / kSingleRegCols, col = kSingleRegCols * h + (e % kSingleRegCols);
+            stage[row * kStageLd + (e % kSingleRegCols)] =
+                (row < n && col < n) ? __ldg(p.A + (int64_t)row * p.lda + col) : 0.0f;
+        }
+        __syncthreads();
+    };
+    const float4* src = reinterpret_cast<const float4*>(stage + r * kStageLd);
     float areg[kSingleRegCols];
+    stage_half(0);
 #pragma unroll
-    for (int k = 0; k < kSingleRegCols; ++k) areg[k] = (live && k < n) ? __ldg(arow + k) : 0.0f;
+    for (int m = 0; m < kSingleRegCols / 4; ++m) {
+        const float4 x = src[m];
+        areg[4 * m] = x.x; areg[4 * m + 1] = x.y; areg[4 * m + 2] = x.z; areg[4 * m + 3] = x.w;
+    }
+    __syncthreads();
+    stage_half(1);
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
         float v[32];
 #pragma unroll
-        for (int k = 0; k < 32; ++k) {
-            const int col = kSingleRegCols + 32 * c + k;
-            v[k] = (live && col < n) ? __ldg(arow + col) : 0.0f;
+        for (int m = 0; m < 8; ++m) {
+            const float4 x = src[8 * c + m];
+            v[4 * m] = x.x; v[4 * m + 1] = x.y; v[4 * m + 2] = x.z; v[4 * m + 3] = x.w;
         }
         tmem_st32(ta + (uint32_t)(32 * c), v);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");  // v is rewritten next chunk
     }
     w_s[tid] = tid < n ? p.b0[tid] : 0.0f;
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");

@@ -56,6 +56,20 @@ def test_pca_k1_equals_iterate(mapi_lib):
     assert torch.equal(res.norms[0], it.norms)
 
 
+@pytest.mark.parametrize("n", [64, 300, 4096])
+def test_pca_degenerate_reports_vector(mapi_lib, n):
+    """The per-vector status words are read back once after the last vector: a degenerate first vector
+    (C = 0) still reports MAPI_ERR_DEGENERATE with its index, and the stream stays usable."""
+    m = mapi_lib
+    b0 = torch.full((n,), 1 / np.sqrt(n), device="cuda")
+    with pytest.raises(m.MapiError) as ei:
+        m.pca_topk(torch.zeros(n, n, device="cuda"), 3, 10, b0)
+    assert ei.value.name == "MAPI_ERR_DEGENERATE" and "vector 0" in str(ei.value)
+    C = torch.eye(n, device="cuda") * 2
+    ok = m.pca_topk(C, 1, 5, b0)
+    assert torch.isfinite(ok.P).all()
+
+
 @pytest.fixture(scope="module")
 def cfg2():
     cfg = synth.cfg2(device="cuda")
