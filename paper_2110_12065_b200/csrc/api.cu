@@ -288,12 +288,15 @@ int resident_warps() {
 }
 
 // Runs MAPI on device buffers; no stream sync, no status read-back (caller does both).
+// dP / dR / dk: fused L2 deflation of A (only when use_resident(d, n); the caller checks)
 mapi_status iterate_launch(const Device& d, int32_t op, const float* A, int64_t n, int64_t lda,
                            const float* b0, int32_t iters, float tol, float* w_out, float* norms,
-                           float* deltas, const IterWs& W, cudaStream_t s, Timer* timer) {
+                           float* deltas, const IterWs& W, cudaStream_t s, Timer* timer,
+                           const double* dP = nullptr, const double* dR = nullptr, int32_t dk = 0) {
     const int vec = vec_width(A, lda);
     const int pol = load_policy(d, n, lda);
     MAPI_CUDA(cudaMemsetAsync(W.bar, 0, 256, s));
+    if (dk > 0 && !use_resident(d, n)) return fail(MAPI_ERR_BAD_PARAM, "fused deflation needs the resident path");
     if (use_single(d, n)) {
         using KernT = void (*)(IterArgs);
         KernT kern = op == 2 ? k_iterate_single<2> : (op == 1 ? k_iterate_single<1> : k_iterate_single<0>);
@@ -403,6 +406,7 @@ mapi_status iterate_launch(const Device& d, int32_t op, const float* A, int64_t 
         a.A = A; a.n = n; a.lda = lda; a.b0 = b0; a.iters = iters; a.tol = tol;
         a.w_out = w_out; a.norms = norms; a.deltas = deltas; a.y = W.y; a.slots = W.slots;
         a.bar = W.bar; a.status = W.status;
+        a.dP = dP; a.dR = dR; a.dk = dk;
         void* args[] = {&a};
         if (timer) timer->start();
         e = cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(nw * 32), args, smem, s);
@@ -1018,7 +1022,14 @@ mapi_status mapi_pca_topk(int32_t op, const float* C, int64_t n, int64_t ldc, in
     for (int32_t i = 0; i < k; ++i) {
         const float* Ai = C;
         int64_t ld = ldc;
-        if (i > 0) {
+        // MAPI_PCA_FUSE=1: K2r stages D_i itself from C, P and R (bitwise the k_build_deflated result), no
+        // D_i round trip through memory.  Measured slower at cfg2 (190k vs 193k it/s: the staging runs at 8
+        // warps per SM inside the persistent kernel, the separate build at full occupancy), so the separate
+        // build stays the default; tests compare the two bitwise.
+        const char* fe = getenv("MAPI_PCA_FUSE");
+        const bool fuse = i > 0 && i <= kResDeflMax && use_resident(d, n) && resident_warps() == 8 && fe &&
+                          fe[0] == '1';
+        if (i > 0 && !fuse) {
             const int gx = (int)std::min<int64_t>((n + 255) / 256, 65535);
             const int gy = (int)std::min<int64_t>(n, 65535);
             const bool v4 = i <= 8 && n % 4 == 0 && ldc % 4 == 0 && (reinterpret_cast<uintptr_t>(C) & 15) == 0;
@@ -1045,7 +1056,8 @@ mapi_status mapi_pca_topk(int32_t op, const float* C, int64_t n, int64_t ldc, in
         // read back once after the last vector (a degenerate vector still reports its index)
         timers.emplace_back(new Timer(s));
         st = iterate_launch(d, op, Ai, n, ld, b0, iters, 0.0f, wtmp, norms ? norms + (int64_t)i * iters : nullptr,
-                            deltas ? deltas + (int64_t)i * iters : nullptr, W, s, timers.back().get());
+                            deltas ? deltas + (int64_t)i * iters : nullptr, W, s, timers.back().get(),
+                            fuse ? P64 : nullptr, fuse ? R : nullptr, fuse ? i : 0);
         if (st != MAPI_OK) return st;
         MAPI_CUDA(cudaMemcpyAsync(st_all + 2 * i, W.status, 2 * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
         k_l2_to_p<<<1, 1024, 0, s>>>(n, wtmp, P64 + (int64_t)i * n, P_out + (int64_t)i * n);

@@ -164,6 +164,10 @@ struct IterArgs {
     float* slots;      // 2*gridDim.x
     unsigned int* bar; // grid barrier counter (zeroed before launch)
     int32_t* status;   // [0] status, [1] iters_done
+    // fused L2 deflation (K2r staging only; dk = 0 elsewhere): A_eff = C - sum_{m<dk} dP[m] dR[m]^T
+    const double* dP = nullptr;  // dk x n
+    const double* dR = nullptr;  // dk x n
+    int32_t dk = 0;
 };
 
 

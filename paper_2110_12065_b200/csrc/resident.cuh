@@ -37,6 +37,7 @@ constexpr int kResNPad = kResLanes * kResCPL;    // 4096: padded row length (max
 constexpr int kResTmemRows = 512 / kResCPL;      // 16 rows in the 512 TMEM columns
 constexpr int kResSmemRows = 12;                 // rows in shared memory (192 KB)
 constexpr int kResMaxRows = kResTmemRows + kResSmemRows;
+constexpr int kResDeflMax = 8;                   // fused deflation: at most 8 previous components
 
 // smem_rows = rows kept in shared memory (kResSmemRows minus the register-resident rows)
 inline size_t resident_smem_bytes(int smem_rows = kResSmemRows) {
@@ -66,6 +67,11 @@ __device__ __forceinline__ void tmem_wait_ld(float (&v)[32]) {
           "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]), "+r"(r[29]), "+r"(r[30]), "+r"(r[31])
         :
         : "memory");
+}
+__device__ __forceinline__ void tmem_st4(uint32_t ta, const float (&v)[4]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(ta), "r"(__float_as_uint(v[0])),
+                 "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3]))
+                 : "memory");
 }
 __device__ __forceinline__ void st_tagged(uint64_t* p, uint64_t v) {
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
@@ -225,6 +231,101 @@ __global__ void __launch_bounds__(NW * 32, 1) k_iterate_resident(IterArgs p) {
 
     // ---- one-time staging of this CTA's rows (A does not change across iterations)
     const bool vec4 = (n % 4 == 0) && (p.lda % 4 == 0) && ((reinterpret_cast<uintptr_t>(p.A) & 15) == 0);
+    float areg[RR > 0 ? RR : 1][32];
+    if (NW == 8 && p.dk > 0) {  // (the 16-warp variant has no register room for it: never fused)
+        // fused L2 deflation (mapi_pca_topk): stage D_i = fp32(C - sum_{m<dk} p_m r_m^T) straight from C
+        // instead of a separate build kernel writing D_i to memory.  Per element the same fp64 sequence as
+        // k_build_deflated (v = C; v = fma(-p_m[row], r_m[col], v), m ascending; one rounding): bitwise the
+        // same D_i.  Position-major: at position m every lane handles its column chunk (m + lane) % 8 (the
+        // rotated layout) of all its rows, with r_m of those 4 columns in registers, the rows' p_m values
+        // in shared memory (staged once) and all the rows' C loads of a position in flight together.
+        constexpr int NR = TR + SR;  // TMEM + shared rows per thread (register rows: a row-major pass below)
+        double* p_s = reinterpret_cast<double*>(w_s);  // [kResMaxRows][kResDeflMax], w_s is free until later
+        for (int e = tid; e < kResMaxRows * kResDeflMax; e += NT) {
+            const int i = e / kResDeflMax, mm = e % kResDeflMax;
+            p_s[e] = (i < R && mm < p.dk) ? -__ldg(p.dP + (int64_t)mm * n + r0 + i) : 0.0;
+        }
+        __syncthreads();
+        auto row_of = [&](int j) {  // local row index of this thread's j-th row (TMEM, then shared)
+            return j < TR ? g * TR + j : kResTmemRows + G * RR + g * SR + (j - TR);
+        };
+        // rows per load batch (register budget: r_m of 4 columns = 64 registers)
+        constexpr int NB = NR % 4 == 0 ? 4 : (NR % 2 == 0 ? 2 : 1);
+#pragma unroll 1
+        for (int m = 0; m < 8; ++m) {
+            const int c = (m + lane) & 7;
+            const int64_t k0 = (int64_t)kResCPL * L + 4 * c;
+            double r4[kResDeflMax][4];
+#pragma unroll
+            for (int mm = 0; mm < kResDeflMax; ++mm)
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    r4[mm][e] = (mm < p.dk && k0 + e < n) ? __ldg(p.dR + (int64_t)mm * n + k0 + e) : 0.0;
+#pragma unroll 1
+            for (int jb = 0; jb < NR; jb += NB) {
+            float x[NB][4];
+#pragma unroll
+            for (int jj = 0; jj < NB; ++jj) {
+                const int j = jb + jj;
+                const int i = row_of(j);
+                const bool valid = i < R;
+                const float* src = p.A + (r0 + (valid ? i : 0)) * p.lda + k0;
+                if (valid && vec4 && k0 + 3 < n) {
+                    const float4 t = __ldg(reinterpret_cast<const float4*>(src));
+                    x[jj][0] = t.x; x[jj][1] = t.y; x[jj][2] = t.z; x[jj][3] = t.w;
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) x[jj][e] = (valid && k0 + e < n) ? __ldg(src + e) : 0.0f;
+                }
+            }
+#pragma unroll
+            for (int jj = 0; jj < NB; ++jj) {
+                const int j = jb + jj;
+                const int i = row_of(j);
+                double v[4] = {(double)x[jj][0], (double)x[jj][1], (double)x[jj][2], (double)x[jj][3]};
+#pragma unroll
+                for (int mm = 0; mm < kResDeflMax; ++mm) {
+                    if (mm < p.dk) {
+                        const double pm = p_s[i * kResDeflMax + mm];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) v[e] = fma(pm, r4[mm][e], v[e]);
+                    }
+                }
+                float o[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) o[e] = (i < R && k0 + e < n) ? (float)v[e] : 0.0f;
+                if (j < TR) {
+                    tmem_st4(ta + (uint32_t)(kResCPL * j + 4 * m), o);
+                } else {
+                    reinterpret_cast<float4*>(a_s + (size_t)(g * SR + (j - TR)) * kResNPad)[8 * L + c] =
+                        make_float4(o[0], o[1], o[2], o[3]);
+                }
+            }
+            }
+        }
+        // register rows, row-major (static register indices): chunk by chunk with r_m from L2
+#pragma unroll
+        for (int rr = 0; rr < RR; ++rr) {
+            const int i = kResTmemRows + g * RR + rr;
+            float x[32];
+            res_load_slice(p.A, p.lda, n, r0 + i, i < R, L, lane, vec4, x);
+#pragma unroll
+            for (int m = 0; m < 8; ++m) {
+                const int c = (m + lane) & 7;
+                const int64_t k0 = (int64_t)kResCPL * L + 4 * c;
+                double v[4] = {(double)x[4 * m], (double)x[4 * m + 1], (double)x[4 * m + 2], (double)x[4 * m + 3]};
+                for (int mm = 0; mm < p.dk; ++mm) {
+                    const double pm = p_s[i * kResDeflMax + mm];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                        v[e] = fma(pm, k0 + e < n ? __ldg(p.dR + (int64_t)mm * n + k0 + e) : 0.0, v[e]);
+                }
+#pragma unroll
+                for (int e = 0; e < 4; ++e) areg[rr][4 * m + e] = (i < R && k0 + e < n) ? (float)v[e] : 0.0f;
+            }
+        }
+        __syncthreads();  // p_s (in w_s) is overwritten below
+    } else {
 #pragma unroll 1
     for (int r = 0; r < TR; ++r) {
         const int i = g * TR + r;
@@ -232,7 +333,6 @@ __global__ void __launch_bounds__(NW * 32, 1) k_iterate_resident(IterArgs p) {
         res_load_slice(p.A, p.lda, n, r0 + i, i < R, L, lane, vec4, v);
         tmem_st32(ta + (uint32_t)(kResCPL * r), v);
     }
-    float areg[RR > 0 ? RR : 1][32];
 #pragma unroll
     for (int r = 0; r < RR; ++r) {
         const int i = kResTmemRows + g * RR + r;
@@ -246,6 +346,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_iterate_resident(IterArgs p) {
         float4* dst = reinterpret_cast<float4*>(a_s + (size_t)(g * SR + r) * kResNPad) + 8 * L;
 #pragma unroll
         for (int m = 0; m < 8; ++m) dst[(m + lane) & 7] = make_float4(v[4 * m], v[4 * m + 1], v[4 * m + 2], v[4 * m + 3]);
+    }
     }
     for (int k = tid; k < kResNPad; k += NT) w_s[k] = k < n ? p.b0[k] : 0.0f;
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");

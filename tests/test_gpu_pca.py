@@ -56,6 +56,24 @@ def test_pca_k1_equals_iterate(mapi_lib):
     assert torch.equal(res.norms[0], it.norms)
 
 
+@pytest.mark.parametrize("n,k,pad", [(1500, 3, 0), (3001, 4, 5), (4096, 8, 0)])
+def test_pca_fused_deflation_bitwise(mapi_lib, monkeypatch, n, k, pad):
+    """K2r stages D_i = fp32(C - sum p_m r_m^T) itself when MAPI_PCA_FUSE=1 (no D_i written to memory): P,
+    norms and deltas are bitwise those of the separate build kernel, ragged n and padded ldc included."""
+    m = mapi_lib
+    r = np.random.default_rng(n + k)
+    X = r.standard_normal((n, 2 * n // 3)).astype(np.float32)
+    Cf = np.full((n, n + pad), np.nan, np.float32)
+    Cf[:, :n] = (X @ X.T / X.shape[1]).astype(np.float32)
+    C = torch.from_numpy(Cf).cuda()[:, :n]
+    b0 = torch.full((n,), 1 / np.sqrt(n), device="cuda")
+    monkeypatch.setenv("MAPI_PCA_FUSE", "1")
+    fused = m.pca_topk(C, k, 30, b0)
+    monkeypatch.setenv("MAPI_PCA_FUSE", "0")
+    sep = m.pca_topk(C, k, 30, b0)
+    assert torch.equal(fused.P, sep.P) and torch.equal(fused.norms, sep.norms) and torch.equal(fused.deltas, sep.deltas)
+
+
 @pytest.mark.parametrize("n", [64, 300, 4096])
 def test_pca_degenerate_reports_vector(mapi_lib, n):
     """The per-vector status words are read back once after the last vector: a degenerate first vector
