@@ -71,7 +71,8 @@ typedef enum {
     MAPI_WS_RECONSTRUCT = 8,  /* n = M, nnz = N (images), k = r (components) */
     MAPI_WS_ITERATE_SHARDED = 9,
     MAPI_WS_ITERATE_HOST_MANY = 10, /* n, nnz = lda, k = iters; add 8 bytes per problem beyond 2 */
-    MAPI_WS_ITERATE_HOST_MANY_PACKED = 11 /* n, k = iters; add 8 bytes per problem beyond 2 */
+    MAPI_WS_ITERATE_HOST_MANY_PACKED = 11, /* n, k = iters; add 8 bytes per problem beyond 2 */
+    MAPI_WS_ITERATE_SYM = 12              /* n */
 } mapi_ws_op;
 
 /* y = A (op) x — the matrix extension of the MAVP (reading Q6: y_j uses ROW j):
@@ -105,6 +106,19 @@ mapi_status mapi_iterate(int32_t op, const float *A, int64_t n, int64_t lda, con
                          int32_t iters, float tol, float *w_out, float *w_l2_out, float *norms,
                          float *deltas, int32_t *iters_done, void *ws, size_t ws_bytes,
                          mapi_stream_t stream);
+
+/* mapi_iterate for a SYMMETRIC A (the covariance matrices of Eq. 2 / Eq. 5; A[j][k] == A[k][j]),
+ * reading only its upper triangle (k >= j): every stored element a_jk, k > j, yields both MAVP terms
+ * term(a_jk, w_k) -> y_j and term(a_jk, w_j) -> y_k (the same n^2 terms, no multiply, half the HBM bytes).
+ * Used when n >= 8192, n % 8 == 0, lda % 8 == 0 and A is 32 B-aligned; otherwise the full-matrix path of
+ * mapi_iterate runs (A must then hold the full symmetric matrix; the library never checks symmetry: it is
+ * the caller's declaration by choosing this entry point).  Same outputs, errors and synchronisation as
+ * mapi_iterate; results differ from it only by the fp32 summation order.
+ * ws: mapi_workspace_size(MAPI_WS_ITERATE_SYM, n, 0, 0) bytes (includes n (n/64 + n/256) floats of partials). */
+mapi_status mapi_iterate_sym(int32_t op, const float *A, int64_t n, int64_t lda, const float *b0,
+                             int32_t iters, float tol, float *w_out, float *w_l2_out, float *norms,
+                             float *deltas, int32_t *iters_done, void *ws, size_t ws_bytes,
+                             mapi_stream_t stream);
 
 /* One normalisation step of Algorithm 1 on a full y (used by the row-sharded multi-GPU path after
  * the all-gather of y):  s = ||y|| (l1 for MIN1/MIN2, l2 for DOT; fp64, fixed order),

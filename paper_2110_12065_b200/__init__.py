@@ -21,12 +21,12 @@ from ._build import build  # noqa: F401  (re-exported: compile in-tree)
 __all__ = ["load", "build", "MapiError", "mavp_matvec", "mavp_matmat", "min_covariance", "center_rows", "mavp_deflate",
            "mavp_reconstruct", "iterate", "iterate_host", "iterate_batched",
            "pca_topk", "csr_prepare", "rank_csr", "workspace_size", "launch_count", "set_profiling",
-           "last_kernel_ms", "MIN1", "MIN2", "DOT", "iterate_host_many", "iterate_host_many_packed", "pack_upper"]
+           "last_kernel_ms", "MIN1", "MIN2", "DOT", "iterate_host_many", "iterate_host_many_packed", "pack_upper", "iterate_sym"]
 
 MIN1, MIN2, DOT = 0, 1, 2  # DOT: regular product of Eq. (1), the RPI comparator
 (WS_MATVEC, WS_ITERATE, WS_ITERATE_BATCHED, WS_PCA_TOPK, WS_CSR_PREPARE, WS_RANK_CSR, WS_ITERATE_HOST,
  WS_MAVP_DEFLATE, WS_RECONSTRUCT, WS_ITERATE_SHARDED, WS_ITERATE_HOST_MANY,
- WS_ITERATE_HOST_MANY_PACKED) = range(12)
+ WS_ITERATE_HOST_MANY_PACKED, WS_ITERATE_SYM) = range(13)
 STATUS = {0: "MAPI_OK", 1: "MAPI_ERR_NULL", 2: "MAPI_ERR_SHAPE", 3: "MAPI_ERR_BAD_PARAM",
           4: "MAPI_ERR_DEGENERATE", 5: "MAPI_ERR_NEGATIVE", 6: "MAPI_ERR_NONFINITE",
           7: "MAPI_ERR_WORKSPACE", 8: "MAPI_ERR_CUDA"}
@@ -67,6 +67,7 @@ def load():
             "mapi_iterate": (st, [i32, P, i64, i64, P, i32, f32, P, P, P, P, P, P, sz, P]),
             "mapi_iterate_host": (st, [i32, P, i64, i64, P, i32, f32, P, P, P, P, P, P, sz, P]),
             "mapi_iterate_host_many": (st, [i32, i32, P, i64, i64, P, i32, f32, P, P, P, P, P, sz, P]),
+            "mapi_iterate_sym": (st, [i32, P, i64, i64, P, i32, f32, P, P, P, P, P, P, sz, P]),
             "mapi_iterate_host_many_packed": (st, [i32, i32, P, i64, P, i32, f32, P, P, P, P, P, sz, P]),
             "mapi_iterate_batched": (st, [i32, P, i64, i64, P, i32, i32, f32, P, P, P, P, P, sz, P]),
             "mapi_pca_topk": (st, [i32, P, i64, i64, i32, i32, P, P, P, P, P, sz, P]),
@@ -282,6 +283,30 @@ def iterate(A, b0, iters: int, tol: float = 0.0, op: int = MIN1, want_l2: bool =
     st = load().mapi_iterate(op, _ptr(A), n, lda, _ptr(b0), int(iters), float(tol), _ptr(w), _ptr(wl2),
                              _ptr(norms), _ptr(deltas), ctypes.byref(done), _ptr(ws), need,
                              _stream(stream))
+    _check(st, done.value)
+    k = done.value
+    return IterResult(w, wl2, None if norms is None else norms[:k], None if deltas is None else deltas[:k], k)
+
+
+def iterate_sym(A, b0, iters: int, tol: float = 0.0, op: int = MIN1, want_l2: bool = True,
+                want_trace: bool = True, ws=None, out=None, stream=None) -> IterResult:
+    """MAPI on a SYMMETRIC device matrix reading only its upper triangle (mapi_iterate_sym, K2s); the
+    caller declares symmetry.  Synchronises the stream."""
+    torch = _torch()
+    n, n2, lda = _matrix(A)
+    if n != n2:
+        raise ValueError(f"A must be square, got {tuple(A.shape)}")
+    _need(b0, "b0", torch.float32, (n,))
+    dev = A.device
+    w = out if out is not None else torch.empty(n, dtype=torch.float32, device=dev)
+    wl2 = torch.empty(n, dtype=torch.float32, device=dev) if want_l2 else None
+    norms = torch.zeros(iters, dtype=torch.float32, device=dev) if want_trace else None
+    deltas = torch.zeros(iters, dtype=torch.float32, device=dev) if want_trace else None
+    ws, need = _workspace(WS_ITERATE_SYM, n, device=dev, ws=ws)
+    done = ctypes.c_int32(0)
+    st = load().mapi_iterate_sym(op, _ptr(A), n, lda, _ptr(b0), int(iters), float(tol), _ptr(w), _ptr(wl2),
+                                 _ptr(norms), _ptr(deltas), ctypes.byref(done), _ptr(ws), need,
+                                 _stream(stream))
     _check(st, done.value)
     k = done.value
     return IterResult(w, wl2, None if norms is None else norms[:k], None if deltas is None else deltas[:k], k)

@@ -18,6 +18,7 @@
 #include "resident.cuh"
 #include "packed.cuh"
 #include "single.cuh"
+#include "sym.cuh"
 #include "csr.cuh"
 #include "deflate.cuh"
 #include "dense.cuh"
@@ -658,6 +659,7 @@ size_t mapi_workspace_size(int32_t op, int64_t n, int64_t nnz, int32_t k) {
     case MAPI_WS_ITERATE_SHARDED: return 256;
     case MAPI_WS_ITERATE_HOST_MANY: return iterate_host_many_ws_bytes(n, nnz, k, 2);
     case MAPI_WS_ITERATE_HOST_MANY_PACKED: return iterate_host_many_ws_bytes(n, packed_lda(n), k, 2, true);
+    case MAPI_WS_ITERATE_SYM: return iterate_ws_bytes(n) + align256(sym_partials_bytes(n));
     }
     return 0;
 }
@@ -796,6 +798,70 @@ mapi_status mapi_iterate(int32_t op, const float* A, int64_t n, int64_t lda, con
     IterWs W = carve_iterate(ws, n);
     Timer timer(s);
     st = iterate_launch(d, op, A, n, lda, b0, iters, tol, w_out, norms, deltas, W, s, &timer);
+    if (st != MAPI_OK) return st;
+    if (w_l2_out) {
+        k_l2_copy<<<1, 1024, 0, s>>>(n, w_out, w_l2_out);
+        MAPI_LAUNCHED();
+    }
+    st = read_status(W, s, iters_done);
+    timer.harvest();
+    return st;
+}
+
+// K2s for symmetric A (sym.cuh): only the upper triangle is read.  Used when the HBM read dominates
+// (n >= 8192) and rows are 32 B-aligned; otherwise the full-matrix kernels run (same result up to the
+// fp32 summation order).  MAPI_SYM_PATH=full forces the fallback (tests).
+bool use_sym(const Device& d, const float* A, int64_t n, int64_t lda) {
+    const char* e = getenv("MAPI_SYM_PATH");
+    if (e && strcmp(e, "full") == 0) return false;
+    if (n % 8 != 0 || lda % 8 != 0 || (reinterpret_cast<uintptr_t>(A) & 31) != 0) return false;
+    if (sym_smem_bytes(n) > (size_t)d.smem_optin) return false;
+    return n >= 8192 || (e && strcmp(e, "sym") == 0);
+}
+
+mapi_status sym_launch(const Device& d, int32_t op, const float* A, int64_t n, int64_t lda, const float* b0,
+                       int32_t iters, float tol, float* w_out, float* norms, float* deltas, const IterWs& W,
+                       float* partials, cudaStream_t s, Timer* timer) {
+    MAPI_CUDA(cudaMemsetAsync(W.bar, 0, 256, s));
+    using KernT = void (*)(SymArgs);
+    KernT kern = op == 2 ? k_iterate_sym<2> : (op == 1 ? k_iterate_sym<1> : k_iterate_sym<0>);
+    const size_t smem = sym_smem_bytes(n);
+    MAPI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int occ = 0;
+    MAPI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kSymThreads, smem));
+    if (occ < 1) return fail(MAPI_ERR_CUDA, "symmetric kernel does not fit an SM (smem %zu)", smem);
+    const int grid = (int)std::min<int64_t>({(int64_t)d.sms, n, (int64_t)kMaxGrid});
+    SymArgs a;
+    a.it.A = A; a.it.n = n; a.it.lda = lda; a.it.b0 = b0; a.it.iters = iters; a.it.tol = tol;
+    a.it.w_out = w_out; a.it.norms = norms; a.it.deltas = deltas; a.it.y = W.y; a.it.slots = W.slots;
+    a.it.bar = W.bar; a.it.status = W.status;
+    a.prow = partials;
+    a.pcol = partials + (size_t)sym_nc(n) * (size_t)n;
+    void* args[] = {&a};
+    if (timer) timer->start();
+    cudaError_t e = cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kSymThreads), args, smem, s);
+    if (timer) timer->stop();
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    if (e != cudaSuccess)
+        return fail(MAPI_ERR_CUDA, "symmetric cooperative launch (grid %d, smem %zu): %s", grid, smem, cudaGetErrorString(e));
+    return MAPI_OK;
+}
+
+mapi_status mapi_iterate_sym(int32_t op, const float* A, int64_t n, int64_t lda, const float* b0, int32_t iters,
+                             float tol, float* w_out, float* w_l2_out, float* norms, float* deltas,
+                             int32_t* iters_done, void* ws, size_t ws_bytes, mapi_stream_t stream) {
+    mapi_status st = validate_dense(op, A, n, lda, b0, iters, tol, w_out, ws);
+    if (st != MAPI_OK) return st;
+    const size_t need = mapi_workspace_size(MAPI_WS_ITERATE_SYM, n, 0, 0);
+    if (ws_bytes < need) return fail(MAPI_ERR_WORKSPACE, "ws_bytes (%zu) < required (%zu)", ws_bytes, need);
+    Device d;
+    if ((st = device_info(d)) != MAPI_OK) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    IterWs W = carve_iterate(ws, n);
+    float* partials = reinterpret_cast<float*>(static_cast<char*>(ws) + iterate_ws_bytes(n));
+    Timer timer(s);
+    st = use_sym(d, A, n, lda) ? sym_launch(d, op, A, n, lda, b0, iters, tol, w_out, norms, deltas, W, partials, s, &timer)
+                               : iterate_launch(d, op, A, n, lda, b0, iters, tol, w_out, norms, deltas, W, s, &timer);
     if (st != MAPI_OK) return st;
     if (w_l2_out) {
         k_l2_copy<<<1, 1024, 0, s>>>(n, w_out, w_l2_out);

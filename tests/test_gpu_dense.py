@@ -536,3 +536,99 @@ def test_iterate_host_many_packed_bitwise(mapi_lib, n):
     for a, b in zip(full, packed):
         assert a.iters_done == b.iters_done == 15
         assert torch.equal(a.w, b.w) and torch.equal(a.norms, b.norms) and torch.equal(a.deltas, b.deltas)
+
+
+# ------------------------------------------------------------------------------ symmetric path (K2s)
+
+
+def _sym_matrix(n, seed, diag=4.0):
+    r = np.random.default_rng(seed)
+    G = r.standard_normal((n, n)).astype(np.float32)
+    S = np.triu(G) + np.triu(G, 1).T
+    S[np.diag_indices(n)] += (np.abs(r.standard_normal(n)) * diag).astype(np.float32)
+    return S.astype(np.float32)
+
+
+@pytest.mark.parametrize("n", [8, 64, 1000, 1032, 4096, 8192])
+@pytest.mark.parametrize("op", ["min1", "min2", "dot"])
+def test_sym_path_reads_only_upper_triangle(mapi_lib, orc, monkeypatch, n, op):
+    """K2s (forced at every size): the strictly-lower triangle and the row padding are NaN on the device, so
+    any read of them would poison the result; the iterate still matches the oracle on the full symmetric
+    matrix (T2; the RPI limit for dot) and is bitwise reproducible.  Ragged task grids: n % 64, n % 256 != 0."""
+    m = mapi_lib
+    S = _sym_matrix(n, n + 3)
+    if op == "dot":
+        S = (S / np.sqrt(n)).astype(np.float32)
+    pad = 8
+    dev = np.full((n, n + pad), np.nan, np.float32)
+    dev[:, :n] = np.triu(S) + np.tril(np.full((n, n), np.nan, np.float32), -1)
+    b0 = np.full(n, 1.0 / np.sqrt(n), np.float32)
+    monkeypatch.setenv("MAPI_SYM_PATH", "sym")
+    Ad = torch.from_numpy(dev).cuda()[:, :n]
+    opc = {"min1": m.MIN1, "min2": m.MIN2, "dot": m.DOT}[op]
+    res = m.iterate_sym(Ad, torch.from_numpy(b0).cuda(), 20, op=opc)
+    ref = orc.rpi(S, b0, 20) if op == "dot" else orc.mapi(S, b0, 20, op=op)
+    assert res.iters_done == 20
+    got = res.w.cpu().numpy() if op == "dot" else res.w_l2.cpu().numpy()
+    assert np.all(np.isfinite(got))
+    _t2(got, ref.w, res.norms.cpu().numpy(), ref.norms)
+    again = m.iterate_sym(Ad, torch.from_numpy(b0).cuda(), 20, op=opc)
+    assert torch.equal(res.w, again.w) and torch.equal(res.deltas, again.deltas)
+
+
+@pytest.mark.parametrize("n", [1000, 8196])
+def test_sym_fallback_full_path(mapi_lib, orc, monkeypatch, n):
+    """Shapes K2s does not take (n < 8192 unforced; n % 8 != 0) run the full-matrix kernels: same result as
+    mapi_iterate bitwise."""
+    m = mapi_lib
+    S = _sym_matrix(n, 5)
+    b0 = torch.full((n,), 1 / np.sqrt(n), device="cuda")
+    Ad = torch.from_numpy(S).cuda()
+    a = m.iterate_sym(Ad, b0, 10)
+    b = m.iterate(Ad, b0, 10)
+    assert torch.equal(a.w, b.w) and torch.equal(a.norms, b.norms)
+
+
+def test_sym_early_stop_and_degenerate(mapi_lib, orc, monkeypatch):
+    m = mapi_lib
+    monkeypatch.setenv("MAPI_SYM_PATH", "sym")
+    n = 2048
+    S = (_sym_matrix(n, 9) / 8).astype(np.float32) + np.diag(np.linspace(4.0, 1.0, n)).astype(np.float32)
+    b0 = np.full(n, 1.0 / np.sqrt(n), np.float32)
+    Ad, bd = torch.from_numpy(S).cuda(), torch.from_numpy(b0).cuda()
+    full = m.iterate_sym(Ad, bd, 200)
+    d = full.deltas.cpu().numpy()
+    tol = float(d[40]) * 1.0001
+    first = int(np.nonzero(d < tol)[0][0])
+    res = m.iterate_sym(Ad, bd, 200, tol=tol)
+    assert res.iters_done == first + 1
+    assert torch.equal(res.deltas, full.deltas[: first + 1])
+    ref = orc.mapi(S, b0, first + 1)
+    _t2(res.w_l2.cpu().numpy(), ref.w)
+    with pytest.raises(m.MapiError) as ei:
+        m.iterate_sym(torch.zeros(n, n, device="cuda"), bd, 10)
+    assert ei.value.name == "MAPI_ERR_DEGENERATE" and ei.value.iters_done == 0
+
+
+def test_cfg3_sym_last_step(mapi_lib, orc, cfg3_device):
+    """cfg3 through K2s as bench.py runs it (upper triangle only): the GPU's 100th iterate equals the
+    oracle's fp64 step from the GPU's own 99th iterate (T1-scaled bound per element), s_99 matches, the
+    100-iteration run stays within T2 of the full-matrix kernel, and it is bitwise reproducible."""
+    m = mapi_lib
+    A = cfg3_device["A"]
+    b0 = torch.from_numpy(cfg3_device["b0"]).cuda()
+    r100 = m.iterate_sym(A, b0, 100)
+    r99 = m.iterate_sym(A, b0, 99)
+    assert torch.equal(r100.norms[:99], r99.norms)
+    w99 = r99.w.cpu().numpy()
+    y, mag = orc.matvec(A.cpu().numpy(), w99, return_mag=True)
+    s = np.abs(y).sum()
+    assert abs(float(r100.norms[99]) - s) <= 1e-5 * s
+    w100 = r100.w.cpu().numpy().astype(np.float64)
+    err = np.abs(w100 - y / s)
+    assert np.all(err <= 1e-5 * mag / s + 2e-5 * np.abs(y / s)), float(np.max(err))
+    full = m.iterate(A, b0, 100)
+    _t2(r100.w_l2.cpu().numpy(), full.w_l2.cpu().numpy().astype(np.float64), r100.norms.cpu().numpy(),
+        full.norms.cpu().numpy().astype(np.float64))
+    again = m.iterate_sym(A, b0, 100)
+    assert torch.equal(r100.w, again.w)
