@@ -56,6 +56,8 @@ def parse():
     p.add_argument("--impl", default="mapi", choices=["mapi", "reference"])
     p.add_argument("--workload", default="cfg3", choices=sorted(WORKLOADS))
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-sym", action="store_true",
+                   help="cfg3: time the full-matrix kernel (mapi_iterate) instead of the symmetric one")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=15.0, help="budget of the oracle sample")
     p.add_argument("--mode", default="auto", choices=["auto", "single", "p2p", "sharded", "replicas"],
@@ -187,6 +189,12 @@ def dense_bytes_per_iter(n, lda):
     return 4.0 * n * lda + 8.0 * n
 
 
+def sym_bytes_per_iter(n):
+    # K2s on a symmetric A: the upper triangle once (4 n (n+1) / 2), w_t read once, y written once
+    # (DESIGN.md §6 K2s; the fp32 row / column partials are L2 traffic of the implementation, not counted)
+    return 4.0 * n * (n + 1) / 2 + 8.0 * n
+
+
 def _abi_check(lib, st):
     if st != 0:
         raise RuntimeError(lib.mapi_last_error_message().decode())
@@ -211,14 +219,41 @@ def build_dense(args, m, dev, stream):
     done = ctypes.c_int32(0)
 
     opc = {"min1": 0, "min2": 1, "dot": 2}[args.op]
+    big = args.workload == "cfg3"
+    # cfg3's A is symmetric by construction (A = G G^T / n + diag): the default runs mapi_iterate_sym (K2s,
+    # upper triangle only); --no-sym (or a non-symmetric input) runs the full-matrix mapi_iterate (K2c)
+    sym = big and not args.no_sym and bool(torch.equal(A, A.t()))
+    if sym:
+        ws_s, need_s = m._workspace(m.WS_ITERATE_SYM, n, device=dev)
 
-    def step():
+    def step_full():
         _abi_check(lib, lib.mapi_iterate(opc, A.data_ptr(), n, lda, b0.data_ptr(), iters, 0.0, w.data_ptr(),
                                          wl2.data_ptr(), norms.data_ptr(), deltas.data_ptr(), ctypes.byref(done),
                                          ws.data_ptr(), need, stream.cuda_stream))
         return iters
 
-    big = args.workload == "cfg3"
+    def step_sym():
+        _abi_check(lib, lib.mapi_iterate_sym(opc, A.data_ptr(), n, lda, b0.data_ptr(), iters, 0.0, w.data_ptr(),
+                                             wl2.data_ptr(), norms.data_ptr(), deltas.data_ptr(),
+                                             ctypes.byref(done), ws_s.data_ptr(), need_s, stream.cuda_stream))
+        return iters
+
+    step = step_sym if sym else step_full
+    if sym:
+        return Work(step=step, unit="iterations/s", per_launch=sym_bytes_per_iter(n) * iters,
+                    bytes_per_unit=sym_bytes_per_iter(n), bound="hbm",
+                    kernel="k_iterate_sym (K2s: symmetric A, upper triangle read once, both MAVP terms per "
+                           "stored element; one cooperative launch runs all iterations of a step)",
+                    config={"workload": f"{args.workload}: {WORKLOADS[args.workload]}", "n": n, "lda": lda,
+                            "iters_per_step": iters, "op": args.op if args.op != "dot" else
+                            "dot (RPI comparator, Eq. 1, l2 normalisation)",
+                            "symmetric": "A is symmetric (covariance); mapi_iterate_sym reads the upper triangle "
+                                         "(n(n+1)/2 floats) once per iteration; all n^2 MAVP terms are formed",
+                            "l2_flush": "inputs larger than L2 (2.1 GB upper triangle vs 126 MB L2)",
+                            "parallelism": "single GPU"},
+                    A=A, b0=b0, iters=iters, oracle=("dense", A, b0, iters), step_full=step_full,
+                    full_bytes=dense_bytes_per_iter(n, lda), traffic_key="cfg3_sym")
+
     # cfg3 streams A from HBM every iteration (HBM roofline); cfg1's 256 KiB matrix is staged once into
     # registers + TMEM of one SM (K6t) and the roofline is the FMNMX issue rate (terms)
     return Work(step=step, unit="iterations/s",
@@ -530,7 +565,7 @@ def run_mapi(args, rank, world, local_rank):
         kavg = elapsed_ms / args.steps
     out.update({"value": value, "ms_per_step": elapsed_ms / args.steps, "config": cfg_out,
                 "gpu_launches": int(launches), "wall_s_timed": t_wall})
-    traffic = traffic_from_profiles(args.workload)
+    traffic = traffic_from_profiles(getattr(work, "traffic_key", args.workload))
     if work.bound == "hbm":
         gpus_in_roof = world if getattr(work, "sharded", False) else 1
         out["hbm_gbs"] = work.bytes_per_unit * job_units / (elapsed_ms / 1e3) / 1e9
@@ -554,6 +589,21 @@ def run_mapi(args, rank, world, local_rank):
                            "kernel_ms_avg": kavg, "kernel_share_of_step": kavg / (elapsed_ms / args.steps),
                            "traffic": traffic}
     out["clocks"] = clocks
+    if getattr(work, "step_full", None) is not None:
+        # the same workload through the full-matrix kernel (reads all n^2 entries), for comparison
+        work.step_full()
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        fsteps = max(2, min(args.steps, 5))
+        f0.record(stream)
+        fu = sum(work.step_full() for _ in range(fsteps))
+        f1.record(stream)
+        torch.cuda.synchronize()
+        fms = max_over_ranks(f0.elapsed_time(f1), dev)
+        out["full_matrix_path"] = {"kernel": "k_iterate_coop (K2c, mapi_iterate: all n^2 entries read)",
+                                   "value": fu * world / (fms / 1e3), "unit": work.unit, "steps": fsteps,
+                                   "ms_per_step": fms / fsteps,
+                                   "hbm_gbs": work.full_bytes * fu * world / (fms / 1e3) / 1e9}
     if e0 is not None and e1 is not None and e1 > e0:
         out["energy"] = {"joules": e1 - e0, "joules_per_unit": (e1 - e0) / units, "unit": work.unit.split("/")[0],
                          "avg_power_w": (e1 - e0) / t_wall, "source": "NVML total energy counter, timed region"}

@@ -631,7 +631,9 @@ size_t iterate_host_many_ws_bytes(int64_t n, int64_t lda, int32_t iters, int32_t
     const size_t slot = align256(sizeof(float) * (size_t)n * (size_t)lda) + 2 * align256(sizeof(float) * (size_t)n) +
                         2 * align256(sizeof(float) * (size_t)std::max(iters, 1)) +
                         (packed ? align256(sizeof(float) * (size_t)packed_floats(n)) : 0);
-    return iterate_ws_bytes(n) + 2 * slot + sizeof(int32_t) * 2 * (size_t)std::max(count, 2);
+    // packed (= symmetric) problems may run K2s, which needs its partial buffers
+    return iterate_ws_bytes(n) + 2 * slot + sizeof(int32_t) * 2 * (size_t)std::max(count, 2) +
+           (packed ? 256 + align256(sym_partials_bytes(n)) : 0);  // (+256: alignment of the partials)
 }
 // device leading dimension of the unpacked matrix: 32 B-aligned rows (the 256-bit load path)
 inline int64_t packed_lda(int64_t n) { return (n + 7) & ~int64_t(7); }
@@ -960,6 +962,9 @@ static mapi_status host_many_impl(int32_t op, int32_t count, const float* const*
         p += align256(sizeof(float) * (size_t)std::max(iters, 1));
     }
     int32_t* st_all = reinterpret_cast<int32_t*>(p);
+    p += sizeof(int32_t) * 2 * (size_t)std::max(count, 2);
+    // K2s partials (the packed input is symmetric), 256 B-aligned (float4 stores)
+    float* sym_part = packed ? reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(p) + 255) & ~uintptr_t(255)) : nullptr;
     cudaStream_t cs = nullptr;
     cudaEvent_t loaded[2] = {nullptr, nullptr}, freed[2] = {nullptr, nullptr};
     auto cleanup = [&]() {
@@ -1009,7 +1014,9 @@ static mapi_status host_many_impl(int32_t op, int32_t count, const float* const*
             g_launches.fetch_add(1, std::memory_order_relaxed);
             if ((e = cudaGetLastError()) != cudaSuccess) break;
         }
-        st = iterate_launch(d, op, x.A, n, lda, x.b0, iters, tol, x.w, x.nrm, x.dlt, W, s, nullptr);
+        st = (packed && use_sym(d, x.A, n, lda))
+                 ? sym_launch(d, op, x.A, n, lda, x.b0, iters, tol, x.w, x.nrm, x.dlt, W, sym_part, s, nullptr)
+                 : iterate_launch(d, op, x.A, n, lda, x.b0, iters, tol, x.w, x.nrm, x.dlt, W, s, nullptr);
         if (st != MAPI_OK) break;
         // queue the next problem's copy before this one's read-back (a pageable read-back may block the host)
         if (i + 1 < count && (e = issue_copy(i + 1)) != cudaSuccess) break;

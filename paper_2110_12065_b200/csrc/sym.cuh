@@ -8,31 +8,37 @@
 // and no multiply, n^2 terms per iteration, exactly the same sum as the full read:
 //     y_j = sum_{k >= j} term(a_jk, w_k)  [row terms]  +  sum_{k < j} term(a_kj, w_k)  [column terms].
 //
-// Tasks: (row block b of kSymRB = 64 rows, column chunk c of kSymCC = 256 columns = 1 KB per row) with
-// chunk end > block start, i.e. chunks c >= b / 4; tasks are dealt round-robin to the grid's warps (~14
-// per warp at n = 32768: balanced to 0.4%).  A warp streams its task row by row (lane l holds columns
+// Tasks: (row block b of kSymRB = 128 rows, column chunk c of kSymCC = 256 columns = 1 KB per row) with
+// chunk end > block start, i.e. chunks c >= b / 2; tasks are dealt round-robin to the grid's warps (~7
+// per warp at n = 32768).  A warp streams its task row by row (lane l holds columns
 // c0 + 8l .. +8 of the row: one 256-bit evict-first load; two 4-row batches in flight): the row term of the
-// lane's 8 elements against w_k (registers, loaded once per task) is summed in a tree and across the warp
-// by a butterfly -> P_row[c][j]; the column terms against w_j (a shared-memory broadcast) accumulate per
+// lane's 8 elements against w_k (registers, loaded once per task) is summed in a tree, and the 8 row
+// partials of an 8-row group cross the warp in one reduce-scatter butterfly (9 shuffles) -> P_row[c][j]; the column terms against w_j (a shared-memory broadcast) accumulate per
 // lane in 8 registers over the task's 64 rows (64-term chains) -> P_col[b][k].  On the diagonal tasks
-// the row term keeps k >= j and the column term k > j; everything below the diagonal is skipped.
+// the row term keeps k >= j and the column term k > j; everything below the diagonal is skipped (never
+// read into a result: the tests fill it with NaN).  w_t lives in global memory (L2): a task reads its
+// 256 w_k (one 256-bit load per lane) and its 128 w_j (staged per warp in shared memory).
 //
-// Per iteration: tasks -> grid barrier -> every CTA sums its rows' partials in fp64 (4 threads per row,
-// interleaved, fixed combine order): y_j = sum_{c >= c(j)} P_row[c][j] + sum_{b <= b(j)} P_col[b][j]
-// (fp32 chains <= 256 terms inside the partials, fp64 across them: within T1) -> fp64 |y|
-// partial per CTA -> grid barrier -> s_t, w_{t+1} = fp32(y / s_t), delta_t exactly as K2c.  Deterministic
-// for a given (n, grid).  Requirements: n % 8 == 0, lda % 8 == 0, 32 B-aligned A (the caller falls back to
-// the full-matrix kernels otherwise), w (n floats) in shared memory.
+// Per iteration, three grid barriers: tasks -> | -> each CTA sums the partials of the rows it OWNS (a range
+// balanced by partial count, 4 threads per row, fp64, fixed combine order): y_j = sum_{c >= c(j)} P_row[c][j]
+// + sum_{b <= b(j)} P_col[b][j] (fp32 chains <= 256 terms inside the partials, fp64 across them: within T1,
+// DESIGN.md), fp64 |y| partial per CTA -> | -> s_t (fixed order, every CTA), the owner forms w_{t+1,j} =
+// fp32(y_j / s_t) (fp64 division, as K2c) and its delta partial -> | -> delta_t (fixed order, every CTA),
+// stop test.  Nothing is replicated per CTA (K2c forms all n quotients in every CTA).  Deterministic for a
+// given (n, grid).  Requirements: n % 8 == 0, lda % 8 == 0, 32 B-aligned A (the caller falls back to the
+// full-matrix kernels otherwise); workspace y region >= 4n floats, slots >= 4 x grid doubles.
 #pragma once
 #include "dense.cuh"
 #include "mapi_common.cuh"
+#include "resident.cuh"  // res_lane_reduce (reduce-scatter butterfly)
 
 namespace mapi {
 
-constexpr int kSymRB = 64;         // rows per task (column-partial chain length)
+constexpr int kSymRB = 128;        // rows per task (column-partial chain length: T1's 128-term limit)
 constexpr int kSymCC = 256;        // columns per task (one 1 KB row chunk per warp row)
 constexpr int kSymNW = 16;         // warps per CTA
 constexpr int kSymThreads = kSymNW * 32;
+constexpr int kSymCR = kSymCC / kSymRB;  // chunks per row block (2): tasks of block b start at chunk b / 2
 
 struct SymArgs {
     IterArgs it;
@@ -42,15 +48,35 @@ struct SymArgs {
 
 __host__ __device__ inline int64_t sym_nb(int64_t n) { return (n + kSymRB - 1) / kSymRB; }
 __host__ __device__ inline int64_t sym_nc(int64_t n) { return (n + kSymCC - 1) / kSymCC; }
-// first task of row block b: sum_{b' < b} (nc - b' / 4)   (kSymCC / kSymRB = 4)
-__host__ __device__ inline int64_t sym_task_start(int64_t b, int64_t nc) {
-    const int64_t q = b / 4, r = b % 4;
-    return b * nc - (2 * q * (q - 1) + r * q);
+// sum_{x < j} floor(x / m)
+__host__ __device__ inline int64_t sym_floor_sum(int64_t j, int64_t m) {
+    const int64_t q = j / m, r = j % m;
+    return m * q * (q - 1) / 2 + r * q;
+}
+// first task of row block b: sum_{b' < b} (nc - b' / kSymCR)
+__host__ __device__ inline int64_t sym_task_start(int64_t b, int64_t nc) { return b * nc - sym_floor_sum(b, kSymCR); }
+// partials summed for row j: row partials of chunks [j / CC, nc) + column partials of blocks [0, j / RB]
+__host__ __device__ inline int64_t sym_partials_before(int64_t j, int64_t nc) {  // sum over rows < j
+    return j * (nc + 1) - sym_floor_sum(j, kSymCC) + sym_floor_sum(j, kSymRB);
+}
+// phase-2 row ownership: CTA c owns rows [own(c), own(c+1)), balanced by the number of partials to sum
+// (rows near n sum ~3x more partials than rows near 0)
+__host__ __device__ inline int64_t sym_own_start(int64_t c, int64_t grid, int64_t n) {
+    const int64_t nc = sym_nc(n), total = sym_partials_before(n, nc);
+    int64_t lo = 0, hi = n;  // smallest j with F(j) * grid >= c * total
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if ((double)sym_partials_before(mid, nc) * (double)grid >= (double)c * (double)total) hi = mid;
+        else lo = mid + 1;
+    }
+    return lo;
 }
 inline size_t sym_partials_bytes(int64_t n) {
     return sizeof(float) * (size_t)n * (size_t)(sym_nb(n) + sym_nc(n));
 }
-inline size_t sym_smem_bytes(int64_t n) { return sizeof(float) * (size_t)((n + 3) & ~int64_t(3)) + sizeof(double) * 40; }
+// per-warp w_j staging (phase 1) / 4 x 128 fp64 sub-sums (phase 2), then the reduction scratch
+constexpr int kSymSmemRegion = (kSymNW * kSymRB * 4 > 4 * 128 * 8) ? kSymNW * kSymRB * 4 : 4 * 128 * 8;  // bytes
+inline size_t sym_smem_bytes(int64_t /*n*/) { return kSymSmemRegion + sizeof(double) * 40; }
 
 template <int OP>
 __device__ __forceinline__ float sym_tree8(const float (&a)[8], const float (&w)[8]) {
@@ -60,24 +86,40 @@ __device__ __forceinline__ float sym_tree8(const float (&a)[8], const float (&w)
     return tree_sum(t);
 }
 
+#ifdef MAPI_SYM_TRACE
+__device__ long long g_sym_trace[6 * 512];  // investigation builds only (scripts/probe_k2s.cu)
+#define SYM_STAMP(t, k) \
+    if (blockIdx.x == 0 && threadIdx.x == 0 && (t) < 512) g_sym_trace[(t) * 6 + (k)] = clock64()
+#else
+#define SYM_STAMP(t, k)
+#endif
+
 template <int OP>
 __global__ void __launch_bounds__(kSymThreads, 1) k_iterate_sym(SymArgs sa) {
-    extern __shared__ __align__(16) float w_s[];
+    extern __shared__ __align__(16) float sm_[];
+    float* wj_s = sm_ + (threadIdx.x >> 5) * kSymRB;             // per warp: w_j of its task's rows
+    double* red = reinterpret_cast<double*>(reinterpret_cast<char*>(sm_) + kSymSmemRegion);
     const IterArgs& p = sa.it;
     const int64_t n = p.n;
-    double* red = reinterpret_cast<double*>(w_s + ((n + 3) & ~int64_t(3)));
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t nb = sym_nb(n), nc = sym_nc(n), ntasks = sym_task_start(nb, nc);
     const int64_t gw = (int64_t)blockIdx.x * kSymNW + warp, W = (int64_t)gridDim.x * kSymNW;
-    const int64_t r0 = (int64_t)blockIdx.x * n / gridDim.x, r1 = (int64_t)(blockIdx.x + 1) * n / gridDim.x;
-    for (int64_t k = tid; k < n; k += blockDim.x) w_s[k] = p.b0[k];
-    __syncthreads();
+    const int64_t o0 = sym_own_start(blockIdx.x, gridDim.x, n), o1 = sym_own_start(blockIdx.x + 1, gridDim.x, n);
+    // global state (workspace y region, 4n floats): w_t double-buffered by parity, y of the owned rows
+    float* wbuf = p.y;
+    float* yg = p.y + 2 * n;
+    double* slotA = reinterpret_cast<double*>(p.slots);  // [2][grid] |y| partials
+    double* slotD = slotA + 2 * gridDim.x;              // [2][grid] delta partials
+    unsigned int epoch = 0;
+    for (int64_t j = o0 + tid; j < o1; j += blockDim.x) wbuf[j] = p.b0[j];
+    grid_barrier(p.bar, ++epoch * gridDim.x);
 
     int32_t done = 0, status = kStOk;
-    double* slots = reinterpret_cast<double*>(p.slots);
     for (int32_t t = 0; t < p.iters; ++t) {
-        float* y = p.y + (t & 1) * n;
-        // ---- phase 1: upper-triangle tasks
+        const float* wcur = wbuf + (t & 1) * n;
+        float* wnext = wbuf + ((t + 1) & 1) * n;
+        SYM_STAMP(t, 0);
+        // ---- phase 1: upper-triangle tasks (w read from L2: written by the owners before the last barrier)
         for (int64_t task = gw; task < ntasks; task += W) {
             int64_t lo = 0, hi = nb - 1;  // row block: last b with start(b) <= task
             while (lo < hi) {
@@ -85,21 +127,32 @@ __global__ void __launch_bounds__(kSymThreads, 1) k_iterate_sym(SymArgs sa) {
                 if (sym_task_start(mid, nc) <= task) lo = mid;
                 else hi = mid - 1;
             }
-            const int64_t b = lo, c = b / 4 + (task - sym_task_start(b, nc));
+            const int64_t b = lo, c = b / kSymCR + (task - sym_task_start(b, nc));
             const int64_t j0 = b * kSymRB, j1 = min(n, j0 + kSymRB), c0 = c * kSymCC;
             const int64_t kl = c0 + 8 * lane;  // this lane's first column
             const bool live = kl < n;          // n % 8 == 0: a lane is all in or all out
             const bool diag = c0 < j1;         // some element with k <= j: masked path
-            float wk[8], col[8];
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                wk[e] = live ? w_s[kl + e] : 0.0f;
-                col[e] = 0.0f;
-            }
-            float keep0 = 0.0f, keep1 = 0.0f;  // row partials of rows j0 + lane, j0 + 32 + lane
-            const float* base = p.A + j0 * p.lda + kl;
             const int rows = (int)(j1 - j0);
+            float wk[8], col[8];
+            if (live) {
+                const float4 u = __ldcg(reinterpret_cast<const float4*>(wcur + kl));
+                const float4 v = __ldcg(reinterpret_cast<const float4*>(wcur + kl) + 1);
+                wk[0] = u.x; wk[1] = u.y; wk[2] = u.z; wk[3] = u.w; wk[4] = v.x; wk[5] = v.y; wk[6] = v.z; wk[7] = v.w;
+            } else {
+#pragma unroll
+                for (int e = 0; e < 8; ++e) wk[e] = 0.0f;
+            }
+#pragma unroll
+            for (int e = 0; e < 8; ++e) col[e] = 0.0f;
+            __syncwarp();  // the previous task's reads of wj_s are done
+#pragma unroll
+            for (int i = 0; i < kSymRB / 32; ++i)
+                wj_s[32 * i + lane] = (32 * i + lane < rows) ? __ldcg(wcur + j0 + 32 * i + lane) : 0.0f;
+            __syncwarp();
+            float* prow = sa.prow + c * n + j0;
+            const float* base = p.A + j0 * p.lda + kl;
             float a[2][4][8];
+            float pr[8];  // per-lane row partials of the current 8-row group
             auto load = [&](float (&buf)[4][8], int rb) {
 #pragma unroll
                 for (int r = 0; r < 4; ++r) {
@@ -109,16 +162,15 @@ __global__ void __launch_bounds__(kSymThreads, 1) k_iterate_sym(SymArgs sa) {
                         for (int e = 0; e < 8; ++e) buf[r][e] = 0.0f;
                 }
             };
-            auto consume = [&](const float (&buf)[4][8], int rb) {
+            // rows rb .. rb+3 of the group -> pr[h*4 .. h*4+3] (rows beyond the task add zeros and are
+            // never stored)
+            auto consume = [&](const float (&buf)[4][8], int rb, int h) {
 #pragma unroll
                 for (int r = 0; r < 4; ++r) {
-                    const int jr = rb + r;
-                    if (jr >= rows) break;  // warp-uniform
-                    const int64_t j = j0 + jr;
-                    const float wj = w_s[j];
-                    float rs;
+                    const int64_t j = j0 + rb + r;
+                    const float wj = wj_s[rb + r];
                     if (!diag) {
-                        rs = sym_tree8<OP>(buf[r], wk);
+                        pr[4 * h + r] = sym_tree8<OP>(buf[r], wk);
 #pragma unroll
                         for (int e = 0; e < 8; ++e) col[e] += mavp_term<OP>(buf[r][e], wj);
                     } else {
@@ -129,61 +181,83 @@ __global__ void __launch_bounds__(kSymThreads, 1) k_iterate_sym(SymArgs sa) {
                             tr[e] = k >= j ? mavp_term<OP>(buf[r][e], wk[e]) : 0.0f;
                             if (k > j) col[e] += mavp_term<OP>(buf[r][e], wj);
                         }
-                        rs = tree_sum(tr);
-                    }
-                    rs = warp_sum(rs);
-                    if (lane == (jr & 31)) {
-                        if (jr < 32) keep0 = rs;
-                        else keep1 = rs;
+                        pr[4 * h + r] = tree_sum(tr);
                     }
                 }
+            };
+            // the 8 row partials of a group across the warp: reduce-scatter butterfly (9 shuffles for 8
+            // rows); lanes with (lane & 3) == 0 hold row res_row_of<8>(lane) and store it
+            auto finish_group = [&](int rb) {
+                const float v = res_lane_reduce<8>(pr, lane);
+                const int ri = res_row_of<8>(lane);
+                if ((lane & 3) == 0 && rb + ri < rows) prow[rb + ri] = v;
             };
             load(a[0], 0);
             for (int rb = 0; rb < rows; rb += 8) {
                 load(a[1], rb + 4);
-                consume(a[0], rb);
+                consume(a[0], rb, 0);
                 if (rb + 8 < rows) load(a[0], rb + 8);
-                consume(a[1], rb + 4);
+                consume(a[1], rb + 4, 1);
+                finish_group(rb);
             }
-            float* prow = sa.prow + c * n;
-            if (j0 + lane < j1) prow[j0 + lane] = keep0;
-            if (j0 + 32 + lane < j1) prow[j0 + 32 + lane] = keep1;
             if (live) {
                 float4* pc = reinterpret_cast<float4*>(sa.pcol + b * n + kl);
                 pc[0] = make_float4(col[0], col[1], col[2], col[3]);
                 pc[1] = make_float4(col[4], col[5], col[6], col[7]);
             }
         }
-        grid_barrier(p.bar, (unsigned int)(2 * t + 1) * gridDim.x);
-        // ---- phase 2: y_j of this CTA's rows; 4 threads per row take every 4th partial, fp64
+        SYM_STAMP(t, 1);
+        grid_barrier(p.bar, ++epoch * gridDim.x);
+        SYM_STAMP(t, 2);
+        // ---- phase 2: y_j of the owned rows.  Warp w: lanes = 32 consecutive rows (row group w % 4 of a
+        // 128-row pass), partials q = sub, sub + 4, ... (sub = w / 4) in ascending order: every load is a
+        // coalesced 128 B row segment of one partial array; fp64 per lane; the 4 subs meet in shared memory
+        // and are added in sub order.
         double abs_part = 0.0;
-        for (int64_t rbase = r0; rbase < r1; rbase += kSymThreads / 4) {
-            const int64_t j = rbase + tid / 4;
-            const int sub = tid & 3;
-            double acc = 0.0;
-            if (j < r1) {
-                const int64_t cj = j / kSymCC, bj = j / kSymRB;
-                const int64_t nrow = nc - cj, ntot = nrow + bj + 1;
-                for (int64_t q = sub; q < ntot; q += 4)
-                    acc += (double)(q < nrow ? __ldcg(sa.prow + (cj + q) * n + j) : __ldcg(sa.pcol + (q - nrow) * n + j));
-            }
-            acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-            acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-            if (sub == 0 && j < r1) {
-                const float v = (float)acc;
-                y[j] = v;
-                abs_part += norm_part<OP>(v);
+        {
+            double* red4 = reinterpret_cast<double*>(sm_);  // [4][128] (aliases wj_s: phase 1 is over)
+            const int rg = warp & 3, sub = warp >> 2;
+            for (int64_t rbase = o0; rbase < o1; rbase += 128) {
+                const int64_t j = rbase + 32 * rg + lane;
+                double acc = 0.0;
+                if (j < o1) {
+                    const int64_t cj = j / kSymCC, bj = j / kSymRB;
+                    const int64_t nrow = nc - cj, ntot = nrow + bj + 1;
+                    for (int64_t q0 = sub; q0 < ntot; q0 += 32) {
+                        float v[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            const int64_t q = q0 + 4 * u;
+                            v[u] = q < ntot ? (q < nrow ? __ldcg(sa.prow + (cj + q) * n + j)
+                                                        : __ldcg(sa.pcol + (q - nrow) * n + j))
+                                            : 0.0f;
+                        }
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) acc += (double)v[u];
+                    }
+                }
+                red4[sub * 128 + 32 * rg + lane] = acc;
+                __syncthreads();
+                if (tid < 128 && rbase + tid < o1) {
+                    const double tot = ((red4[tid] + red4[128 + tid]) + red4[256 + tid]) + red4[384 + tid];
+                    const float v = (float)tot;
+                    yg[rbase + tid] = v;
+                    abs_part += norm_part<OP>(v);
+                }
+                __syncthreads();
             }
         }
-        const double cta_abs = block_sum(abs_part, red);
-        if (tid == 0) slots[(t & 1) * gridDim.x + blockIdx.x] = cta_abs;
-        grid_barrier(p.bar, (unsigned int)(2 * t + 2) * gridDim.x);
+        const double cta_abs = block_sum(abs_part, red);  // its barriers also publish yg to this CTA
+        if (tid == 0) slotA[(t & 1) * gridDim.x + blockIdx.x] = cta_abs;
+        SYM_STAMP(t, 3);
+        grid_barrier(p.bar, ++epoch * gridDim.x);
+        SYM_STAMP(t, 4);
         // ---- s_t: the same fixed-order fp64 sum in every CTA
         double sd;
         {
             if (warp == 0) {
                 double pp = 0.0;
-                for (int cc = lane; cc < (int)gridDim.x; cc += 32) pp += __ldcg(slots + (t & 1) * gridDim.x + cc);
+                for (int cc = lane; cc < (int)gridDim.x; cc += 32) pp += __ldcg(slotA + (t & 1) * gridDim.x + cc);
                 pp = warp_sum(pp);
                 if (lane == 0) red[32] = pp;
             }
@@ -195,14 +269,28 @@ __global__ void __launch_bounds__(kSymThreads, 1) k_iterate_sym(SymArgs sa) {
             status = (sd == 0.0) ? kStDegenerate : kStNonfinite;
             break;
         }
-        // ---- w_{t+1} = y / s_t, delta_t, into this CTA's shared memory (as K2c)
+        // ---- w_{t+1} = fp32(y / s_t) (fp64 division, as K2c) for the owned rows only, delta partial
         double dpart = 0.0;
-        for (int64_t k = tid; k < n; k += blockDim.x) {
-            const float wn = (float)((double)ld_cg(y + k) / sd);
-            dpart += (double)fabsf(wn - w_s[k]);
-            w_s[k] = wn;
+        for (int64_t j = o0 + tid; j < o1; j += blockDim.x) {
+            const float wn = (float)((double)yg[j] / sd);
+            dpart += (double)fabsf(wn - wcur[j]);
+            wnext[j] = wn;
         }
-        const double delta = block_sum(dpart, red);  // its barriers also publish w_s
+        const double cta_d = block_sum(dpart, red);
+        if (tid == 0) slotD[(t & 1) * gridDim.x + blockIdx.x] = cta_d;
+        grid_barrier(p.bar, ++epoch * gridDim.x);  // also publishes w_{t+1} for the next tasks
+        double delta;
+        {
+            if (warp == 0) {
+                double pp = 0.0;
+                for (int cc = lane; cc < (int)gridDim.x; cc += 32) pp += __ldcg(slotD + (t & 1) * gridDim.x + cc);
+                pp = warp_sum(pp);
+                if (lane == 0) red[33] = pp;
+            }
+            __syncthreads();
+            delta = red[33];
+            __syncthreads();
+        }
         if (blockIdx.x == 0 && tid == 0) {
             if (p.norms) p.norms[t] = (float)sd;
             if (p.deltas) p.deltas[t] = (float)delta;
@@ -210,7 +298,8 @@ __global__ void __launch_bounds__(kSymThreads, 1) k_iterate_sym(SymArgs sa) {
         done = t + 1;
         if (p.tol > 0.0f && delta < (double)p.tol) break;
     }
-    for (int64_t k = r0 + tid; k < r1; k += blockDim.x) p.w_out[k] = w_s[k];
+    const float* wfin = wbuf + (done & 1) * n;  // w_done (on a degenerate stop: the last good iterate)
+    for (int64_t j = o0 + tid; j < o1; j += blockDim.x) p.w_out[j] = wfin[j];
     if (blockIdx.x == 0 && tid == 0) {
         p.status[0] = status;
         p.status[1] = done;

@@ -1,5 +1,6 @@
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests/test_gpu_dense.py -q -x -k "sym" --timeout 600 > gpurun_out/pytest_sym.log 2>&1; tail -3 gpurun_out/pytest_sym.log
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -DMAPI_SYM_TRACE -o /tmp/p scripts/probe_k2s.cu && timeout 120 /tmp/p | tee gpurun_out/probe_k2s.log
 timeout 300 python - <<'PY'
 import sys, torch, numpy as np
 sys.path.insert(0, ".")

@@ -533,9 +533,17 @@ def test_iterate_host_many_packed_bitwise(mapi_lib, n):
         b0s.append(torch.full((n,), 1 / np.sqrt(n)).pin_memory())
     full = m.iterate_host_many(As, b0s, 15)
     packed = m.iterate_host_many_packed(Aps, n, b0s, 15)
-    for a, b in zip(full, packed):
+    for A, b0, a, b in zip(As, b0s, full, packed):
         assert a.iters_done == b.iters_done == 15
-        assert torch.equal(a.w, b.w) and torch.equal(a.norms, b.norms) and torch.equal(a.deltas, b.deltas)
+        # packed (= declared symmetric) problems take the same kernel as mapi_iterate_sym: K2s where it
+        # applies (n >= 8192, n % 8 == 0), else the full-matrix kernels (bitwise = mapi_iterate_host_many)
+        ref = m.iterate_sym(A.cuda(), b0.cuda(), 15)
+        assert torch.equal(ref.w.cpu(), b.w) and torch.equal(ref.norms.cpu(), b.norms)
+        if n < 8192:
+            assert torch.equal(a.w, b.w) and torch.equal(a.norms, b.norms) and torch.equal(a.deltas, b.deltas)
+        else:
+            _t2(b.w.numpy() / np.linalg.norm(b.w.numpy()), a.w.numpy().astype(np.float64), b.norms.numpy(),
+                a.norms.numpy().astype(np.float64))
 
 
 # ------------------------------------------------------------------------------ symmetric path (K2s)
