@@ -9,8 +9,8 @@
 //     y_j = sum_{k >= j} term(a_jk, w_k)  [row terms]  +  sum_{k < j} term(a_kj, w_k)  [column terms].
 //
 // Tasks: (row block b of kSymRB = 128 rows, column chunk c of kSymCC = 256 columns = 1 KB per row) with
-// chunk end > block start, i.e. chunks c >= b / 2; tasks are dealt round-robin to the grid's warps (~7
-// per warp at n = 32768).  A warp streams its task row by row (lane l holds columns
+// chunk end > block start, i.e. chunks c >= b / 2; warps take tasks from a per-iteration atomic counter
+// (~7 per warp at n = 32768; dynamic because SMs stream at different rates).  A warp streams its task row by row (lane l holds columns
 // c0 + 8l .. +8 of the row: one 256-bit evict-first load; two 4-row batches in flight): the row term of the
 // lane's 8 elements against w_k (registers, loaded once per task) is summed in a tree, and the 8 row
 // partials of an 8-row group cross the warp in one reduce-scatter butterfly (9 shuffles) -> P_row[c][j]; the column terms against w_j (a shared-memory broadcast) accumulate per
@@ -74,9 +74,25 @@ __host__ __device__ inline int64_t sym_own_start(int64_t c, int64_t grid, int64_
 inline size_t sym_partials_bytes(int64_t n) {
     return sizeof(float) * (size_t)n * (size_t)(sym_nb(n) + sym_nc(n));
 }
-// per-warp w_j staging (phase 1) / 4 x 128 fp64 sub-sums (phase 2), then the reduction scratch
-constexpr int kSymSmemRegion = (kSymNW * kSymRB * 4 > 4 * 128 * 8) ? kSymNW * kSymRB * 4 : 4 * 128 * 8;  // bytes
+// per-warp w_j staging (phase 1) / one fp64 sub-sum per thread (phase 2), then the reduction scratch
+constexpr int kSymSmemRegion = (kSymNW * kSymRB * 4 > kSymThreads * 8) ? kSymNW * kSymRB * 4 : kSymThreads * 8;  // bytes
 inline size_t sym_smem_bytes(int64_t /*n*/) { return kSymSmemRegion + sizeof(double) * 40; }
+
+// partial stores ask L2 to keep the lines (evict_last): the next phase re-reads them, while A streams
+// through L2 evict-first
+__device__ __forceinline__ uint64_t sym_keep_policy() {
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void sym_st_keep(float* p, float v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void sym_st4_keep(float* p, float a, float b, float c, float d, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "f"(a), "f"(b), "f"(c),
+                 "f"(d), "l"(pol)
+                 : "memory");
+}
 
 template <int OP>
 __device__ __forceinline__ float sym_tree8(const float (&a)[8], const float (&w)[8]) {
@@ -88,8 +104,11 @@ __device__ __forceinline__ float sym_tree8(const float (&a)[8], const float (&w)
 
 #ifdef MAPI_SYM_TRACE
 __device__ long long g_sym_trace[6 * 512];  // investigation builds only (scripts/probe_k2s.cu)
+__device__ long long g_sym_cta[2 * 256 * 32];  // per-CTA task-phase start / end (globaltimer), iteration < 32
 #define SYM_STAMP(t, k) \
-    if (blockIdx.x == 0 && threadIdx.x == 0 && (t) < 512) g_sym_trace[(t) * 6 + (k)] = clock64()
+    if (blockIdx.x == 0 && threadIdx.x == 0 && (t) < 512) g_sym_trace[(t) * 6 + (k)] = clock64(); \
+    if (threadIdx.x == 0 && (k) <= 1 && (t) < 32 && blockIdx.x < 256) { \
+        long long gt; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt)); g_sym_cta[((t) * 256 + blockIdx.x) * 2 + (k)] = gt; }
 #else
 #define SYM_STAMP(t, k)
 #endif
@@ -103,7 +122,6 @@ __global__ void __launch_bounds__(kSymThreads, 1) k_iterate_sym(SymArgs sa) {
     const int64_t n = p.n;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t nb = sym_nb(n), nc = sym_nc(n), ntasks = sym_task_start(nb, nc);
-    const int64_t gw = (int64_t)blockIdx.x * kSymNW + warp, W = (int64_t)gridDim.x * kSymNW;
     const int64_t o0 = sym_own_start(blockIdx.x, gridDim.x, n), o1 = sym_own_start(blockIdx.x + 1, gridDim.x, n);
     // global state (workspace y region, 4n floats): w_t double-buffered by parity, y of the owned rows
     float* wbuf = p.y;
@@ -111,6 +129,7 @@ __global__ void __launch_bounds__(kSymThreads, 1) k_iterate_sym(SymArgs sa) {
     double* slotA = reinterpret_cast<double*>(p.slots);  // [2][grid] |y| partials
     double* slotD = slotA + 2 * gridDim.x;              // [2][grid] delta partials
     unsigned int epoch = 0;
+    const uint64_t keep = sym_keep_policy();
     for (int64_t j = o0 + tid; j < o1; j += blockDim.x) wbuf[j] = p.b0[j];
     grid_barrier(p.bar, ++epoch * gridDim.x);
 
@@ -119,8 +138,20 @@ __global__ void __launch_bounds__(kSymThreads, 1) k_iterate_sym(SymArgs sa) {
         const float* wcur = wbuf + (t & 1) * n;
         float* wnext = wbuf + ((t + 1) & 1) * n;
         SYM_STAMP(t, 0);
-        // ---- phase 1: upper-triangle tasks (w read from L2: written by the owners before the last barrier)
-        for (int64_t task = gw; task < ntasks; task += W) {
+        // ---- phase 1: upper-triangle tasks (w read from L2: written by the owners before the last barrier).
+        // Tasks are taken dynamically from a per-iteration counter (SMs stream at different rates: a static
+        // deal left the fastest CTAs idle ~40 us per iteration); a task's partials do not depend on which
+        // warp computes them, so the results stay bitwise reproducible.  The next task index is fetched
+        // while the current task streams.
+        unsigned int* ctr = p.bar + 32 + (t & 1);  // two counters at byte 128 of the zeroed header
+        auto fetch = [&]() -> unsigned int {
+            unsigned int v = 0;
+            if (lane == 0) v = atomicAdd(ctr, 1u);
+            return v;
+        };
+        unsigned int nxt = fetch();
+        for (int64_t task = __shfl_sync(0xffffffffu, nxt, 0); task < ntasks;) {
+            nxt = fetch();
             int64_t lo = 0, hi = nb - 1;  // row block: last b with start(b) <= task
             while (lo < hi) {
                 const int64_t mid = (lo + hi + 1) >> 1;
@@ -190,7 +221,7 @@ __global__ void __launch_bounds__(kSymThreads, 1) k_iterate_sym(SymArgs sa) {
             auto finish_group = [&](int rb) {
                 const float v = res_lane_reduce<8>(pr, lane);
                 const int ri = res_row_of<8>(lane);
-                if ((lane & 3) == 0 && rb + ri < rows) prow[rb + ri] = v;
+                if ((lane & 3) == 0 && rb + ri < rows) sym_st_keep(prow + rb + ri, v, keep);
             };
             load(a[0], 0);
             for (int rb = 0; rb < rows; rb += 8) {
@@ -201,47 +232,54 @@ __global__ void __launch_bounds__(kSymThreads, 1) k_iterate_sym(SymArgs sa) {
                 finish_group(rb);
             }
             if (live) {
-                float4* pc = reinterpret_cast<float4*>(sa.pcol + b * n + kl);
-                pc[0] = make_float4(col[0], col[1], col[2], col[3]);
-                pc[1] = make_float4(col[4], col[5], col[6], col[7]);
+                float* pc = sa.pcol + b * n + kl;
+                sym_st4_keep(pc, col[0], col[1], col[2], col[3], keep);
+                sym_st4_keep(pc + 4, col[4], col[5], col[6], col[7], keep);
             }
+            task = __shfl_sync(0xffffffffu, nxt, 0);
         }
         SYM_STAMP(t, 1);
         grid_barrier(p.bar, ++epoch * gridDim.x);
         SYM_STAMP(t, 2);
-        // ---- phase 2: y_j of the owned rows.  Warp w: lanes = 32 consecutive rows (row group w % 4 of a
-        // 128-row pass), partials q = sub, sub + 4, ... (sub = w / 4) in ascending order: every load is a
-        // coalesced 128 B row segment of one partial array; fp64 per lane; the 4 subs meet in shared memory
+        // every warp is past its last fetch of iteration t - 1's counter: re-arm it for iteration t + 1
+        if (blockIdx.x == 0 && tid == 0) p.bar[32 + ((t + 1) & 1)] = 0u;
+        // ---- phase 2: y_j of the owned rows.  `subs` threads per row (the most that fit the owned rows in
+        // one pass), consecutive threads on consecutive rows (coalesced partial reads); sub k takes partials
+        // q = k, k + subs, ... in ascending order, 48 loads in flight, fp64; the subs meet in shared memory
         // and are added in sub order.
         double abs_part = 0.0;
         {
-            double* red4 = reinterpret_cast<double*>(sm_);  // [4][128] (aliases wj_s: phase 1 is over)
-            const int rg = warp & 3, sub = warp >> 2;
-            for (int64_t rbase = o0; rbase < o1; rbase += 128) {
-                const int64_t j = rbase + 32 * rg + lane;
+            double* redp = reinterpret_cast<double*>(sm_);  // [kSymThreads] (aliases wj_s: phase 1 is over)
+            const int64_t rown = o1 - o0;
+            const int subs = rown * 8 <= kSymThreads ? 8 : (rown * 4 <= kSymThreads ? 4 : (rown * 2 <= kSymThreads ? 2 : 1));
+            const int rpp = kSymThreads / subs;  // rows per pass
+            const int rl = tid % rpp, sub = tid / rpp;
+            for (int64_t pbase = o0; pbase < o1; pbase += rpp) {
+                const int64_t j = pbase + rl;
                 double acc = 0.0;
                 if (j < o1) {
                     const int64_t cj = j / kSymCC, bj = j / kSymRB;
                     const int64_t nrow = nc - cj, ntot = nrow + bj + 1;
-                    for (int64_t q0 = sub; q0 < ntot; q0 += 32) {
-                        float v[8];
+                    for (int64_t q0 = sub; q0 < ntot; q0 += 48 * subs) {
+                        float v[48];
 #pragma unroll
-                        for (int u = 0; u < 8; ++u) {
-                            const int64_t q = q0 + 4 * u;
+                        for (int u = 0; u < 48; ++u) {
+                            const int64_t q = q0 + (int64_t)u * subs;
                             v[u] = q < ntot ? (q < nrow ? __ldcg(sa.prow + (cj + q) * n + j)
                                                         : __ldcg(sa.pcol + (q - nrow) * n + j))
                                             : 0.0f;
                         }
 #pragma unroll
-                        for (int u = 0; u < 8; ++u) acc += (double)v[u];
+                        for (int u = 0; u < 48; ++u) acc += (double)v[u];
                     }
                 }
-                red4[sub * 128 + 32 * rg + lane] = acc;
+                redp[tid] = acc;
                 __syncthreads();
-                if (tid < 128 && rbase + tid < o1) {
-                    const double tot = ((red4[tid] + red4[128 + tid]) + red4[256 + tid]) + red4[384 + tid];
+                if (tid < rpp && pbase + tid < o1) {
+                    double tot = 0.0;
+                    for (int k = 0; k < subs; ++k) tot += redp[k * rpp + tid];
                     const float v = (float)tot;
-                    yg[rbase + tid] = v;
+                    yg[pbase + tid] = v;
                     abs_part += norm_part<OP>(v);
                 }
                 __syncthreads();

@@ -4,6 +4,7 @@
 // n = 32768 symmetric synthetic matrix generated on the device, 20 iterations.
 #include <cstdio>
 #include <vector>
+#include <algorithm>
 #include "../paper_2110_12065_b200/csrc/sym.cuh"
 using namespace mapi;
 
@@ -55,6 +56,37 @@ int main() {
         for (int k = 0; k < 4; ++k) ph[k] += h[t * 6 + k + 1] - h[t * 6 + k];
         ph[4] += h[(t + 1) * 6] - h[t * 6 + 4];
         tot += h[(t + 1) * 6] - h[t * 6];
+    }
+    {
+        std::vector<long long> g(2 * 256 * 32);
+        cudaMemcpyFromSymbol(g.data(), g_sym_cta, 8 * g.size());
+        // task-phase end per CTA relative to the earliest end, averaged over iterations 3..T-2
+        std::vector<double> endrel(sms, 0.0), dur(sms, 0.0);
+        for (int t = 3; t < T - 1 && t < 32; ++t) {
+            long long mn = 1LL << 62;
+            for (int c = 0; c < sms; ++c) mn = std::min(mn, g[((t * 256) + c) * 2 + 1]);
+            for (int c = 0; c < sms; ++c) {
+                endrel[c] += (g[((t * 256) + c) * 2 + 1] - mn) / 1e3;
+                dur[c] += (g[((t * 256) + c) * 2 + 1] - g[((t * 256) + c) * 2 + 0]) / 1e3;
+            }
+        }
+        const int it = std::min(T - 1, 32) - 3;
+        double mx = 0, avg = 0, dmx = 0, dmn = 1e30;
+        for (int c = 0; c < sms; ++c) {
+            endrel[c] /= it; dur[c] /= it;
+            mx = std::max(mx, endrel[c]); avg += endrel[c] / sms;
+            dmx = std::max(dmx, dur[c]); dmn = std::min(dmn, dur[c]);
+        }
+        printf("task phase: end spread over CTAs max %.1f us (mean %.1f us after the earliest); duration min %.1f max %.1f us\n",
+               mx, avg, dmn, dmx);
+        printf("  slowest CTAs:");
+        for (int k = 0; k < 6; ++k) {
+            int bi = 0;
+            for (int c = 0; c < sms; ++c) if (endrel[c] > endrel[bi]) bi = c;
+            printf(" %d(+%.1f)", bi, endrel[bi]);
+            endrel[bi] = -1;
+        }
+        printf("\n");
     }
     printf("K2s n=%lld: %.1f us/iteration (events) | cycles: own tasks %.0f | barrier 1 %.0f | partial reduction %.0f | "
            "barrier 2 %.0f | s, w, delta %.0f | total %.0f\n", (long long)n, 1e3 * ms / T, ph[0] / cnt, ph[1] / cnt,
