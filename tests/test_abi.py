@@ -74,6 +74,16 @@ def test_validation_before_device(lib):
     assert st == 3 and "op" in _err(lib)
     st = lib.mapi_iterate(0, fake, 4, 4, fake, 5, 0.0, fake, None, None, None, None, fake, 16, None)
     assert st == 7
+    # the symmetric entry point validates the same way; its workspace adds the K2s partial buffers
+    st = lib.mapi_iterate_sym(0, None, 4, 4, fake, 5, 0.0, fake, None, None, None, None, fake, 1 << 20, None)
+    assert st == 1 and "A is NULL" in _err(lib)
+    st = lib.mapi_iterate_sym(0, fake, 4, 3, fake, 5, 0.0, fake, None, None, None, None, fake, 1 << 20, None)
+    assert st == 2 and "lda (3) < n (4)" in _err(lib)
+    st = lib.mapi_iterate_sym(0, fake, 4, 4, fake, 5, 0.0, fake, None, None, None, None, fake, 16, None)
+    assert st == 7
+    n = 32768
+    assert m.workspace_size(m.WS_ITERATE_SYM, n) == m.workspace_size(m.WS_ITERATE, n) + \
+        4 * n * (n // 128 + n // 256)
     st = lib.mapi_mavp_matvec(0, fake, 3, 10, 9, fake, fake, None)
     assert st == 2 and "lda (9) < n_cols (10)" in _err(lib)
     st = lib.mapi_pca_topk(0, fake, 8, 8, 9, 5, fake, fake, None, None, fake, 1 << 30, None)
