@@ -838,7 +838,7 @@ mapi_status sym_launch(const Device& d, int32_t op, const float* A, int64_t n, i
     a.it.w_out = w_out; a.it.norms = norms; a.it.deltas = deltas; a.it.y = W.y; a.it.slots = W.slots;
     a.it.bar = W.bar; a.it.status = W.status;
     a.prow = partials;
-    a.pcol = partials + (size_t)sym_nc(n) * (size_t)n;
+    a.pcol = partials + (size_t)sym_nc(n) * (size_t)((n + 31) & ~int64_t(31));  // row-tiled, whole tiles
     void* args[] = {&a};
     if (timer) timer->start();
     cudaError_t e = cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kSymThreads), args, smem, s);

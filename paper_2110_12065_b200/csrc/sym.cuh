@@ -71,8 +71,11 @@ __host__ __device__ inline int64_t sym_own_start(int64_t c, int64_t grid, int64_
     }
     return lo;
 }
+// row-tiled partial layout: element (j, q) of an array with m entries per row at sym_tile(j, m) + 32 q
+__host__ __device__ inline int64_t sym_tile(int64_t j, int64_t m) { return (j >> 5) * 32 * m + (j & 31); }
 inline size_t sym_partials_bytes(int64_t n) {
-    return sizeof(float) * (size_t)n * (size_t)(sym_nb(n) + sym_nc(n));
+    const int64_t np = (n + 31) & ~int64_t(31);  // whole 32-row tiles
+    return sizeof(float) * (size_t)np * (size_t)(sym_nb(n) + sym_nc(n));
 }
 // per-warp w_j staging (phase 1) / one fp64 sub-sum per thread (phase 2), then the reduction scratch
 constexpr int kSymSmemRegion = (kSymNW * kSymRB * 4 > kSymThreads * 8) ? kSymNW * kSymRB * 4 : kSymThreads * 8;  // bytes
@@ -180,7 +183,9 @@ __global__ void __launch_bounds__(kSymThreads, 1) k_iterate_sym(SymArgs sa) {
             for (int i = 0; i < kSymRB / 32; ++i)
                 wj_s[32 * i + lane] = (32 * i + lane < rows) ? __ldcg(wcur + j0 + 32 * i + lane) : 0.0f;
             __syncwarp();
-            float* prow = sa.prow + c * n + j0;
+            // partial layouts are row-tiled ([j / 32][chunk or block][j % 32]): phase 2 reads all partials of
+            // 32 consecutive rows as one contiguous run
+            float* prow = sa.prow + c * 32;  // + sym_tile(j) for row j
             const float* base = p.A + j0 * p.lda + kl;
             float a[2][4][8];
             float pr[8];  // per-lane row partials of the current 8-row group
@@ -221,7 +226,7 @@ __global__ void __launch_bounds__(kSymThreads, 1) k_iterate_sym(SymArgs sa) {
             auto finish_group = [&](int rb) {
                 const float v = res_lane_reduce<8>(pr, lane);
                 const int ri = res_row_of<8>(lane);
-                if ((lane & 3) == 0 && rb + ri < rows) sym_st_keep(prow + rb + ri, v, keep);
+                if ((lane & 3) == 0 && rb + ri < rows) sym_st_keep(prow + sym_tile(j0 + rb + ri, nc), v, keep);
             };
             load(a[0], 0);
             for (int rb = 0; rb < rows; rb += 8) {
@@ -231,8 +236,8 @@ __global__ void __launch_bounds__(kSymThreads, 1) k_iterate_sym(SymArgs sa) {
                 consume(a[1], rb + 4, 1);
                 finish_group(rb);
             }
-            if (live) {
-                float* pc = sa.pcol + b * n + kl;
+            if (live) {  // columns kl .. kl+7 lie in one 32-column tile
+                float* pc = sa.pcol + b * 32 + sym_tile(kl, nb);
                 sym_st4_keep(pc, col[0], col[1], col[2], col[3], keep);
                 sym_st4_keep(pc + 4, col[4], col[5], col[6], col[7], keep);
             }
@@ -260,13 +265,14 @@ __global__ void __launch_bounds__(kSymThreads, 1) k_iterate_sym(SymArgs sa) {
                 if (j < o1) {
                     const int64_t cj = j / kSymCC, bj = j / kSymRB;
                     const int64_t nrow = nc - cj, ntot = nrow + bj + 1;
+                    const float* prow_j = sa.prow + sym_tile(j, nc) + cj * 32;  // + q * 32
+                    const float* pcol_j = sa.pcol + sym_tile(j, nb);            // + b * 32
                     for (int64_t q0 = sub; q0 < ntot; q0 += 48 * subs) {
                         float v[48];
 #pragma unroll
                         for (int u = 0; u < 48; ++u) {
                             const int64_t q = q0 + (int64_t)u * subs;
-                            v[u] = q < ntot ? (q < nrow ? __ldcg(sa.prow + (cj + q) * n + j)
-                                                        : __ldcg(sa.pcol + (q - nrow) * n + j))
+                            v[u] = q < ntot ? (q < nrow ? __ldcg(prow_j + q * 32) : __ldcg(pcol_j + (q - nrow) * 32))
                                             : 0.0f;
                         }
 #pragma unroll

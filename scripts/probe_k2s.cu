@@ -34,7 +34,7 @@ int main() {
     SymArgs a{};
     a.it.A = A; a.it.n = n; a.it.lda = n; a.it.b0 = b0; a.it.iters = T; a.it.tol = 0; a.it.w_out = w;
     a.it.norms = nr; a.it.deltas = dl; a.it.y = y; a.it.slots = reinterpret_cast<float*>(sl); a.it.bar = bar;
-    a.it.status = st; a.prow = part; a.pcol = part + sym_nc(n) * n;
+    a.it.status = st; a.prow = part; a.pcol = part + sym_nc(n) * ((n + 31) & ~int64_t(31));
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0); cudaEventCreate(&e1);
     float ms = 0;
