@@ -293,12 +293,13 @@ int resident_warps() {
 mapi_status iterate_launch(const Device& d, int32_t op, const float* A, int64_t n, int64_t lda,
                            const float* b0, int32_t iters, float tol, float* w_out, float* norms,
                            float* deltas, const IterWs& W, cudaStream_t s, Timer* timer,
-                           const double* dP = nullptr, const double* dR = nullptr, int32_t dk = 0) {
+                           const double* dP = nullptr, const double* dR = nullptr, int32_t dk = 0,
+                           float* w_l2 = nullptr, bool* l2_done = nullptr) {
     const int vec = vec_width(A, lda);
     const int pol = load_policy(d, n, lda);
-    MAPI_CUDA(cudaMemsetAsync(W.bar, 0, 256, s));
+    if (l2_done) *l2_done = false;
     if (dk > 0 && !use_resident(d, n)) return fail(MAPI_ERR_BAD_PARAM, "fused deflation needs the resident path");
-    if (use_single(d, n)) {
+    if (use_single(d, n)) {  // (one CTA: no grid barrier counter to reset)
         using KernT = void (*)(IterArgs);
         KernT kern = op == 2 ? k_iterate_single<2> : (op == 1 ? k_iterate_single<1> : k_iterate_single<0>);
         const size_t smem = single_smem_bytes();
@@ -307,14 +308,17 @@ mapi_status iterate_launch(const Device& d, int32_t op, const float* A, int64_t 
         a.A = A; a.n = n; a.lda = lda; a.b0 = b0; a.iters = iters; a.tol = tol;
         a.w_out = w_out; a.norms = norms; a.deltas = deltas; a.y = W.y; a.slots = W.slots;
         a.bar = W.bar; a.status = W.status;
+        a.w_l2 = l2_done ? w_l2 : nullptr;
         if (timer) timer->start();
         kern<<<1, kSingleThreads, smem, s>>>(a);
         if (timer) timer->stop();
         g_launches.fetch_add(1, std::memory_order_relaxed);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return fail(MAPI_ERR_CUDA, "single-CTA launch: %s", cudaGetErrorString(e));
+        if (l2_done && w_l2) *l2_done = true;
         return MAPI_OK;
     }
+    MAPI_CUDA(cudaMemsetAsync(W.bar, 0, 256, s));
     if (use_cluster(d, n)) {
         // K6r (A in registers) for n <= 512 unless MAPI_DENSE_PATH=cluster_smem; K6 (A in shared memory) above
         const bool reg = n <= 512 && strcmp(dense_path_env(), "cluster_smem") != 0;
@@ -799,9 +803,11 @@ mapi_status mapi_iterate(int32_t op, const float* A, int64_t n, int64_t lda, con
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     IterWs W = carve_iterate(ws, n);
     Timer timer(s);
-    st = iterate_launch(d, op, A, n, lda, b0, iters, tol, w_out, norms, deltas, W, s, &timer);
+    bool l2_done = false;
+    st = iterate_launch(d, op, A, n, lda, b0, iters, tol, w_out, norms, deltas, W, s, &timer, nullptr, nullptr, 0,
+                        w_l2_out, &l2_done);
     if (st != MAPI_OK) return st;
-    if (w_l2_out) {
+    if (w_l2_out && !l2_done) {
         k_l2_copy<<<1, 1024, 0, s>>>(n, w_out, w_l2_out);
         MAPI_LAUNCHED();
     }

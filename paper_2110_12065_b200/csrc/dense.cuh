@@ -168,6 +168,7 @@ struct IterArgs {
     const double* dP = nullptr;  // dk x n
     const double* dR = nullptr;  // dk x n
     int32_t dk = 0;
+    float* w_l2 = nullptr;       // K6t only: the final l2 copy written in-kernel (else k_l2_copy runs)
 };
 
 

@@ -143,6 +143,27 @@ __global__ void __launch_bounds__(kSingleThreads, 1) k_iterate_single(IterArgs p
         if (p.tol > 0.0f && delta < (double)p.tol) break;
     }
     if (live) p.w_out[r] = w_s[r];
+    if (p.w_l2) {
+        // the final l2 copy in-kernel, bitwise k_l2_copy's result: fp32 squares, warp butterflies, then
+        // one butterfly over the warp partials padded with zeros to 32 (k_l2_copy's 1024-thread block_sum
+        // sees exactly these values for n <= 256)
+        const float wv = live ? w_s[r] : 0.0f;
+        float part = 0.0f;
+        part += wv * wv;
+        part = warp_sum(part);
+        __shared__ float l2s[kSingleThreads / 32 + 1];
+        __syncthreads();
+        if (lane == 0) l2s[warp] = part;
+        __syncthreads();
+        if (warp == 0) {
+            float x = lane < kSingleThreads / 32 ? l2s[lane] : 0.0f;
+            x = warp_sum(x);
+            if (lane == 0) l2s[kSingleThreads / 32] = x;
+        }
+        __syncthreads();
+        const float l2 = sqrtf(l2s[kSingleThreads / 32]);
+        if (live) p.w_l2[r] = l2 > 0.0f ? wv / l2 : 0.0f;
+    }
     if (tid == 0) {
         p.status[0] = status;
         p.status[1] = done;

@@ -366,6 +366,10 @@ def test_single_cta_path(mapi_lib, orc, monkeypatch, n, pad, op):
         _t2(got, ref.w, res.norms.cpu().numpy(), ref.norms)
     again = m.iterate(Ad, bd, 25, op=opc)
     assert torch.equal(res.w, again.w) and torch.equal(res.deltas, again.deltas)
+    # the in-kernel l2 copy is bitwise the separate k_l2_copy (which mapi_iterate_sym's fallback runs)
+    monkeypatch.setenv("MAPI_SYM_PATH", "full")
+    sep = m.iterate_sym(Ad, bd, 25, op=opc)
+    assert torch.equal(sep.w, res.w) and torch.equal(sep.w_l2, res.w_l2)
     if op != "dot":
         first = m.iterate(Ad, bd, 10, op=opc)
         resumed = m.iterate(Ad, first.w, 15, op=opc)
