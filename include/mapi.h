@@ -72,7 +72,8 @@ typedef enum {
     MAPI_WS_ITERATE_SHARDED = 9,
     MAPI_WS_ITERATE_HOST_MANY = 10, /* n, nnz = lda, k = iters; add 8 bytes per problem beyond 2 */
     MAPI_WS_ITERATE_HOST_MANY_PACKED = 11, /* n, k = iters; add 8 bytes per problem beyond 2 */
-    MAPI_WS_ITERATE_SYM = 12              /* n */
+    MAPI_WS_ITERATE_SYM = 12,             /* n */
+    MAPI_WS_CSR_REORDER = 13              /* n */
 } mapi_ws_op;
 
 /* y = A (op) x — the matrix extension of the MAVP (reading Q6: y_j uses ROW j):
@@ -272,6 +273,21 @@ mapi_status mapi_rank_csr(int64_t n, int64_t nnz, const int32_t *row_ptr, const 
                           const float *cap, const float *bg, const float *b0, int32_t max_iters,
                           float tol, float *w_out, float *w_l2_out, float *deltas,
                           int32_t *iters_done, void *ws, size_t ws_bytes, mapi_stream_t stream);
+
+/* Optional preparation for the ranking path: relabel the nodes by DESCENDING out-degree (ties by ascending
+ * id), so the most gathered sources get the lowest ids, which the gather kernel keeps in shared memory
+ * (K3h).  perm_out[old] = new (n).  row_ptr_out (n+1) / col_idx_out (nnz): the same graph in the
+ * new ids (new row i' = the in-edges of the old node with perm = i', sources renamed, in their original
+ * order).  Rank the relabelled graph (mapi_csr_prepare + mapi_rank_csr with b0 permuted by
+ * mapi_csr_permute) and map the result back with mapi_csr_permute(to_new = 0).  Deterministic (stable
+ * radix sort).  ws: mapi_workspace_size(MAPI_WS_CSR_REORDER, n, 0, 0).  Asynchronous. */
+mapi_status mapi_csr_reorder(int64_t n, int64_t nnz, const int32_t *row_ptr, const int32_t *col_idx,
+                             int32_t *perm_out, int32_t *row_ptr_out, int32_t *col_idx_out, void *ws,
+                             size_t ws_bytes, mapi_stream_t stream);
+/* out[perm[j]] = x[j] (to_new != 0: original ids -> relabelled) or out[j] = x[perm[j]] (to_new == 0:
+ * relabelled -> original).  x and out must not alias.  Asynchronous. */
+mapi_status mapi_csr_permute(int64_t n, const int32_t *perm, const float *x, float *out, int32_t to_new,
+                             mapi_stream_t stream);
 
 /* Bytes of device workspace the call `op` needs for the given sizes (0 if none).
  *   MAPI_WS_MATVEC: 0.  MAPI_WS_ITERATE: n.  MAPI_WS_ITERATE_BATCHED: n, k.

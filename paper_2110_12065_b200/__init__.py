@@ -21,12 +21,12 @@ from ._build import build  # noqa: F401  (re-exported: compile in-tree)
 __all__ = ["load", "build", "MapiError", "mavp_matvec", "mavp_matmat", "min_covariance", "center_rows", "mavp_deflate",
            "mavp_reconstruct", "iterate", "iterate_host", "iterate_batched",
            "pca_topk", "csr_prepare", "rank_csr", "workspace_size", "launch_count", "set_profiling",
-           "last_kernel_ms", "MIN1", "MIN2", "DOT", "iterate_host_many", "iterate_host_many_packed", "pack_upper", "iterate_sym"]
+           "last_kernel_ms", "MIN1", "MIN2", "DOT", "iterate_host_many", "iterate_host_many_packed", "pack_upper", "iterate_sym", "csr_reorder", "csr_permute"]
 
 MIN1, MIN2, DOT = 0, 1, 2  # DOT: regular product of Eq. (1), the RPI comparator
 (WS_MATVEC, WS_ITERATE, WS_ITERATE_BATCHED, WS_PCA_TOPK, WS_CSR_PREPARE, WS_RANK_CSR, WS_ITERATE_HOST,
  WS_MAVP_DEFLATE, WS_RECONSTRUCT, WS_ITERATE_SHARDED, WS_ITERATE_HOST_MANY,
- WS_ITERATE_HOST_MANY_PACKED, WS_ITERATE_SYM) = range(13)
+ WS_ITERATE_HOST_MANY_PACKED, WS_ITERATE_SYM, WS_CSR_REORDER) = range(14)
 STATUS = {0: "MAPI_OK", 1: "MAPI_ERR_NULL", 2: "MAPI_ERR_SHAPE", 3: "MAPI_ERR_BAD_PARAM",
           4: "MAPI_ERR_DEGENERATE", 5: "MAPI_ERR_NEGATIVE", 6: "MAPI_ERR_NONFINITE",
           7: "MAPI_ERR_WORKSPACE", 8: "MAPI_ERR_CUDA"}
@@ -73,6 +73,8 @@ def load():
             "mapi_pca_topk": (st, [i32, P, i64, i64, i32, i32, P, P, P, P, P, sz, P]),
             "mapi_csr_prepare": (st, [i64, i64, P, P, f32, P, P, P, sz, P]),
             "mapi_rank_csr": (st, [i64, i64, P, P, P, P, P, i32, f32, P, P, P, P, P, sz, P]),
+            "mapi_csr_reorder": (st, [i64, i64, P, P, P, P, P, P, sz, P]),
+            "mapi_csr_permute": (st, [i64, P, P, P, i32, P]),
             "mapi_workspace_size": (sz, [i32, i64, i64, i32]),
             "mapi_p2p_exchange_bytes": (sz, [i64, i32]),
             "mapi_p2p_alloc": (st, [sz, ctypes.POINTER(ctypes.c_void_p)]),
@@ -517,3 +519,31 @@ def rank_csr(n: int, row_ptr, col_idx, cap, bg, b0, max_iters: int = 200, tol: f
     _check(st, done.value)
     k = done.value
     return IterResult(w, wl2, None, deltas[:k], k)
+
+def csr_reorder(n: int, row_ptr, col_idx, ws=None, stream=None):
+    """Relabel the graph's nodes by descending out-degree (mapi_csr_reorder): returns (perm, row_ptr',
+    col_idx') with perm[old] = new.  Asynchronous."""
+    torch = _torch()
+    _need(row_ptr, "row_ptr", torch.int32, (n + 1,))
+    _need(col_idx, "col_idx", torch.int32)
+    nnz = col_idx.numel()
+    dev = row_ptr.device
+    perm = torch.empty(n, dtype=torch.int32, device=dev)
+    rp = torch.empty(n + 1, dtype=torch.int32, device=dev)
+    ci = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)[:nnz]
+    ws, need = _workspace(WS_CSR_REORDER, n, device=dev, ws=ws)
+    _check(load().mapi_csr_reorder(n, nnz, _ptr(row_ptr), _ptr(col_idx) if nnz else None, _ptr(perm), _ptr(rp),
+                                   _ptr(ci) if nnz else None, _ptr(ws), need, _stream(stream)))
+    return perm, rp, ci
+
+
+def csr_permute(perm, x, to_new: bool = True, out=None, stream=None):
+    """out[perm[j]] = x[j] (to_new) or out[j] = x[perm[j]] (back to the original ids); asynchronous."""
+    torch = _torch()
+    n = perm.numel()
+    _need(perm, "perm", torch.int32, (n,))
+    _need(x, "x", torch.float32, (n,))
+    out = out if out is not None else torch.empty_like(x)
+    _check(load().mapi_csr_permute(n, _ptr(perm), _ptr(x), _ptr(out), 1 if to_new else 0, _stream(stream)))
+    return out
+

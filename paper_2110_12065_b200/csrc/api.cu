@@ -19,6 +19,7 @@
 #include "packed.cuh"
 #include "single.cuh"
 #include "sym.cuh"
+#include "reorder.cuh"
 #include "csr.cuh"
 #include "deflate.cuh"
 #include "dense.cuh"
@@ -666,6 +667,7 @@ size_t mapi_workspace_size(int32_t op, int64_t n, int64_t nnz, int32_t k) {
     case MAPI_WS_ITERATE_HOST_MANY: return iterate_host_many_ws_bytes(n, nnz, k, 2);
     case MAPI_WS_ITERATE_HOST_MANY_PACKED: return iterate_host_many_ws_bytes(n, packed_lda(n), k, 2, true);
     case MAPI_WS_ITERATE_SYM: return iterate_ws_bytes(n) + align256(sym_partials_bytes(n));
+    case MAPI_WS_CSR_REORDER: return reorder_ws_bytes(n);
     }
     return 0;
 }
@@ -1240,6 +1242,65 @@ mapi_status mapi_rank_csr(int64_t n, int64_t nnz, const int32_t* row_ptr, const 
     if (st == MAPI_ERR_DEGENERATE) return fail(st, "||G (+) w_t||_1 == 0");
     if (st == MAPI_ERR_NONFINITE) return fail(st, "||G (+) w_t||_1 is not finite");
     return st;
+}
+
+mapi_status mapi_csr_reorder(int64_t n, int64_t nnz, const int32_t* row_ptr, const int32_t* col_idx, int32_t* perm_out,
+                             int32_t* row_ptr_out, int32_t* col_idx_out, void* ws, size_t ws_bytes,
+                             mapi_stream_t stream) {
+    if (n < 1) return fail(MAPI_ERR_SHAPE, "n (%lld) must be >= 1", (long long)n);
+    if (nnz < 0 || nnz > INT32_MAX) return fail(MAPI_ERR_SHAPE, "nnz (%lld) out of the int32 index range", (long long)nnz);
+    if (n > INT32_MAX) return fail(MAPI_ERR_SHAPE, "n (%lld) out of the int32 index range", (long long)n);
+    if (!row_ptr || !perm_out || !row_ptr_out || (nnz > 0 && (!col_idx || !col_idx_out)))
+        return fail(MAPI_ERR_NULL, "row_ptr / col_idx / perm_out / row_ptr_out / col_idx_out is NULL");
+    if (!ws) return fail(MAPI_ERR_WORKSPACE, "workspace is NULL");
+    const size_t need = reorder_ws_bytes(n);
+    if (ws_bytes < need) return fail(MAPI_ERR_WORKSPACE, "ws_bytes (%zu) < required (%zu)", ws_bytes, need);
+    Device d;
+    mapi_status st = device_info(d);
+    if (st != MAPI_OK) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    char* p = static_cast<char*>(ws);
+    auto take = [&](size_t bytes) {
+        char* r = p;
+        p += align256(bytes);
+        return r;
+    };
+    uint32_t* deg = reinterpret_cast<uint32_t*>(take(4 * (size_t)n));
+    uint32_t* key = reinterpret_cast<uint32_t*>(take(4 * (size_t)n));
+    uint32_t* key_out = reinterpret_cast<uint32_t*>(take(4 * (size_t)n));
+    int32_t* ids = reinterpret_cast<int32_t*>(take(4 * (size_t)n));
+    int32_t* order = reinterpret_cast<int32_t*>(take(4 * (size_t)n));
+    int32_t* len = reinterpret_cast<int32_t*>(take(4 * (size_t)(n + 1)));
+    size_t tmp_bytes = reorder_cub_bytes(n);
+    void* tmp = take(tmp_bytes);
+    const int grid = d.sms * 8;
+    MAPI_CUDA(cudaMemsetAsync(deg, 0, 4 * (size_t)n, s));
+    if (nnz > 0) k_reorder_outdeg<<<grid, 256, 0, s>>>(nnz, col_idx, deg);
+    k_reorder_keys<<<grid, 256, 0, s>>>(n, deg, key, ids);
+    MAPI_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, key, key_out, ids, order, (int)n, 0, 32, s));
+    k_reorder_perm<<<grid, 256, 0, s>>>(n, order, row_ptr, perm_out, len);
+    tmp_bytes = reorder_cub_bytes(n);
+    MAPI_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, len, row_ptr_out, (int)(n + 1), s));
+    if (nnz > 0) k_reorder_copy<<<grid, 256, 0, s>>>(n, order, row_ptr, col_idx, perm_out, row_ptr_out, col_idx_out);
+    g_launches.fetch_add(6, std::memory_order_relaxed);
+    MAPI_CUDA(cudaGetLastError());
+    return MAPI_OK;
+}
+
+mapi_status mapi_csr_permute(int64_t n, const int32_t* perm, const float* x, float* out, int32_t to_new,
+                             mapi_stream_t stream) {
+    if (n < 1) return fail(MAPI_ERR_SHAPE, "n (%lld) must be >= 1", (long long)n);
+    if (!perm || !x || !out) return fail(MAPI_ERR_NULL, "perm / x / out is NULL");
+    if (x == out) return fail(MAPI_ERR_BAD_PARAM, "x and out must not alias");
+    Device d;
+    mapi_status st = device_info(d);
+    if (st != MAPI_OK) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    k_permute<<<(unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)d.sms * 8), 256, 0, s>>>(n, perm, x, out,
+                                                                                            to_new ? 1 : 0);
+    MAPI_LAUNCHED();
+    MAPI_CUDA(cudaGetLastError());
+    return MAPI_OK;
 }
 
 mapi_status mapi_center_rows(const float* V, int64_t M, int64_t N, int64_t ldv, float* Vc, int64_t ldvc,

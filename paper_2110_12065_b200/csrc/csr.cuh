@@ -283,41 +283,45 @@ __global__ void k_mp_partition(int64_t n, int64_t nnz, const int32_t* __restrict
     part_k[c] = (int32_t)(d - i);
 }
 
-__global__ void __launch_bounds__(kMpThreads) k_rank_rows_mp(int64_t n, int64_t nnz, const int32_t* __restrict__ row_ptr,
-                                                             const int32_t* __restrict__ col_idx,
-                                                             const float* __restrict__ v,
-                                                             const int32_t* __restrict__ part_i,
-                                                             const int32_t* __restrict__ part_k, float* __restrict__ e,
-                                                             int32_t* __restrict__ carry_row,
-                                                             float* __restrict__ carry_val, double* __restrict__ gsum,
-                                                             const int32_t* stop) {
+// Per-tile shared memory of the merge-path gather (one 128-thread group's worth).
+struct MpSmem {
+    int32_t* buf;   // kMpTileBuf words: row ends, then gathered values
+    float* fp;      // kMpThreads
+    int32_t* wl_row;
+    int32_t* wf_row;
+    float* wl_val;  // kMpWarps each
+};
+constexpr int kMpTileBuf = kMpTile + 2 + (kMpTile + 2) / 32 + 1;
+
+// One merge-path tile (kMpThreads threads: tid = thread within the group, sync = its barrier).  HUB > 0:
+// v[0 .. HUB) is read from `hub` (a shared-memory copy, bitwise the same values) instead of L2.
+template <int HUB, typename Sync>
+__device__ __forceinline__ void mp_tile(int64_t tile, int tid, const Sync& sync, const MpSmem& sm, const float* hub,
+                                        int64_t n, int64_t nnz, const int32_t* __restrict__ row_ptr,
+                                        const int32_t* __restrict__ col_idx, const float* __restrict__ v,
+                                        const int32_t* __restrict__ part_i, const int32_t* __restrict__ part_k,
+                                        float* __restrict__ e, int32_t* __restrict__ carry_row,
+                                        float* __restrict__ carry_val, double* __restrict__ gsum, uint64_t pol_s,
+                                        uint64_t pol_k) {
     // shared arrays indexed through pad(): one spare word per 8 so that the lane-strided reads of the
     // consume loop (thread t walks ~8 consecutive items) hit 32 distinct banks instead of 4
     // the stop flag (written by the previous launch) is read together with the partition, not
     // ahead of it: one global round trip before the streams start instead of two
-    const int32_t halt = *stop;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int32_t i0 = part_i[blockIdx.x], i1 = part_i[blockIdx.x + 1];
-    const int32_t k0 = part_k[blockIdx.x], k1 = part_k[blockIdx.x + 1];
-    if (halt) return;
+    const int lane = tid & 31, warp = tid >> 5;
+    const int32_t i0 = part_i[tile], i1 = part_i[tile + 1];
+    const int32_t k0 = part_k[tile], k1 = part_k[tile + 1];
     const int nrows = i1 - i0, nk = k1 - k0;  // nrows + nk == items of this tile
     // one spare word per 32: the staging writes (32 consecutive items per warp) are conflict-free and
     // the consume loop's ~8-apart lane reads land on distinct banks
     auto pad = [](int x) { return x + (x >> 5); };
-#if MAPI_CSR_SHARE
     // one buffer: nrows + 1 row ends, then nk values (nrows + nk <= kMpTile); half the shared memory
     // of two full-size arrays, which leaves more of the unified L1 to cache the gathered v
-    __shared__ int32_t s_buf[kMpTile + 2 + (kMpTile + 2) / 32 + 1];
-    int32_t* s_end = s_buf;
-    float* s_val = reinterpret_cast<float*>(s_buf) + pad(nrows + 1) + 1;
-#else
-    __shared__ int32_t s_end[kMpTile + 1 + (kMpTile + 1) / 32 + 1];  // row_ptr[i0+1 .. i1+1]
-    __shared__ float s_val[kMpTile + kMpTile / 32];                  // v[col_idx[k0 .. k1)]
-#endif
-    __shared__ float s_fp[kMpThreads];      // segmented prefix of the threads' carries
-    __shared__ int32_t wl_row[kMpThreads / 32], wf_row[kMpThreads / 32];
-    __shared__ float wl_val[kMpThreads / 32];
-    const uint64_t pol_s = l2_policy_stream(), pol_k = l2_policy_keep();
+    int32_t* s_end = sm.buf;
+    float* s_val = reinterpret_cast<float*>(sm.buf) + pad(nrows + 1) + 1;
+    float* s_fp = sm.fp;  // segmented prefix of the threads' carries
+    int32_t* wl_row = sm.wl_row;
+    int32_t* wf_row = sm.wf_row;
+    float* wl_val = sm.wl_val;
     // stage row ends (rows i0 .. i1, the last possibly partial) and gathered values
     for (int r = tid; r <= nrows; r += kMpThreads)
         s_end[pad(r)] = (i0 + r < n) ? ld_stream_i32(row_ptr + i0 + r + 1, pol_s) : (int32_t)nnz;
@@ -330,7 +334,18 @@ __global__ void __launch_bounds__(kMpThreads) k_rank_rows_mp(int64_t n, int64_t 
     }
     float xv[kMpIpt];
 #pragma unroll
-    for (int u = 0; u < kMpIpt; ++u) xv[u] = cj[u] >= 0 ? ld_keep_f32(v + cj[u], pol_k) : 0.0f;
+    for (int u = 0; u < kMpIpt; ++u) {
+        if constexpr (HUB > 0) {
+            // branch-free, so the 12 global gathers still issue back to back: hub lanes load v[0] (one
+            // shared sector) and take the shared-memory copy instead
+            const bool inhub = (unsigned)cj[u] < (unsigned)HUB;
+            const float g = ld_keep_f32(v + (inhub || cj[u] < 0 ? 0 : cj[u]), pol_k);
+            const float h = hub[inhub ? cj[u] : 0];
+            xv[u] = cj[u] < 0 ? 0.0f : (inhub ? h : g);
+        } else {
+            xv[u] = cj[u] >= 0 ? ld_keep_f32(v + cj[u], pol_k) : 0.0f;
+        }
+    }
     double gpart = 0.0;
 #pragma unroll
     for (int u = 0; u < kMpIpt; ++u) {
@@ -338,7 +353,7 @@ __global__ void __launch_bounds__(kMpThreads) k_rank_rows_mp(int64_t n, int64_t 
         if (j < nk) s_val[pad(j)] = xv[u];
         gpart += (double)xv[u];
     }
-    __syncthreads();
+    sync();
     // this thread's diagonal within the tile (merge-path search in shared memory)
     const int items = nrows + nk;
     const int dt = min(tid * kMpIpt, items);
@@ -385,7 +400,7 @@ __global__ void __launch_bounds__(kMpThreads) k_rank_rows_mp(int64_t n, int64_t 
         wl_val[warp] = pv;
     }
     if (lane == 0) wf_row[warp] = ri;
-    __syncthreads();
+    sync();
     if (ri == wf_row[warp]) {  // my run reaches the start of my warp: add preceding warps' tails
         float extra = 0.0f;
         for (int q = warp - 1; q >= 0; --q) {
@@ -396,17 +411,86 @@ __global__ void __launch_bounds__(kMpThreads) k_rank_rows_mp(int64_t n, int64_t 
         pv += extra;
     }
     s_fp[tid] = pv;
-    __syncthreads();
+    sync();
     // the first row this thread emits was left open by thread tid-1 (its carry row is this thread's
     // start row), so its preceding partials are exactly s_fp[tid-1]
     if (first_row >= 0) e[i0 + first_row] = (tid > 0 ? s_fp[tid - 1] : 0.0f) + own_first;
     if (tid == kMpThreads - 1) {  // CTA carry-out: the run still open on the tile's last row
-        carry_row[blockIdx.x] = (ri < nrows || (ri == nrows && i1 < n)) ? i0 + ri : -1;
-        carry_val[blockIdx.x] = pv;
+        carry_row[tile] = (ri < nrows || (ri == nrows && i1 < n)) ? i0 + ri : -1;
+        carry_val[tile] = pv;
     }
     // fp64 sum of this tile's gathered values, per warp (k_rank_fixup adds the warps in order)
     gpart = warp_sum(gpart);
-    if (lane == 0) gsum[(int64_t)blockIdx.x * kMpWarps + warp] = gpart;
+    if (lane == 0) gsum[tile * kMpWarps + warp] = gpart;
+}
+
+__global__ void __launch_bounds__(kMpThreads) k_rank_rows_mp(int64_t n, int64_t nnz, const int32_t* __restrict__ row_ptr,
+                                                             const int32_t* __restrict__ col_idx,
+                                                             const float* __restrict__ v,
+                                                             const int32_t* __restrict__ part_i,
+                                                             const int32_t* __restrict__ part_k, float* __restrict__ e,
+                                                             int32_t* __restrict__ carry_row,
+                                                             float* __restrict__ carry_val, double* __restrict__ gsum,
+                                                             const int32_t* stop) {
+    // the stop flag (written by the previous launch) is read together with the partition, not ahead of
+    // it: one global round trip before the streams start instead of two
+    const int32_t halt = *stop;
+    __shared__ int32_t s_buf[kMpTileBuf];
+    __shared__ float s_fp[kMpThreads];
+    __shared__ int32_t wl_row[kMpWarps], wf_row[kMpWarps];
+    __shared__ float wl_val[kMpWarps];
+    if (halt) return;
+    const MpSmem sm{s_buf, s_fp, wl_row, wf_row, wl_val};
+    mp_tile<0>((int64_t)blockIdx.x, threadIdx.x, [] { __syncthreads(); }, sm, nullptr, n, nnz, row_ptr, col_idx, v,
+               part_i, part_k, e, carry_row, carry_val, gsum, l2_policy_stream(), l2_policy_keep());
+}
+
+// K3h (opt-in, MAPI_CSR_HUB=1; measured slower, see csr_rank_run): the same tiles, persistent (kHubCtas
+// CTAs per SM, kHubGroups independent 128-thread groups each with its own named barrier), with the first
+// HUB entries of v copied once per launch into shared memory.  After mapi_csr_reorder (ids by descending
+// out-degree) those are the highest out-degree sources (cfg5: the first 12,288 ids carry ~37% of the
+// edges), whose gathers then cost shared-memory wavefronts instead of one L1 wavefront per lane.  The
+// gather-only probe gained 30% this way (profiles/r01_probe_hub.log), but the persistent tile loop itself
+// runs at half K3's rate.  Bitwise the same e as k_rank_rows_mp.
+constexpr int kHubGroups = 8;
+#ifndef MAPI_CSR_HUBN
+#define MAPI_CSR_HUBN 12288
+#endif
+#ifndef MAPI_CSR_HUB_CTAS
+#define MAPI_CSR_HUB_CTAS 2
+#endif
+constexpr int kHub = MAPI_CSR_HUBN;           // v entries in shared memory per CTA
+constexpr int kHubCtas = MAPI_CSR_HUB_CTAS;   // CTAs per SM (each with its own hub copy)
+inline size_t hub_smem_bytes() {
+    return sizeof(float) * kHub + kHubGroups * (sizeof(int32_t) * kMpTileBuf + sizeof(float) * kMpThreads +
+                                                  sizeof(int32_t) * 2 * kMpWarps + sizeof(float) * kMpWarps);
+}
+template <int HUB>
+__global__ void __launch_bounds__(kMpThreads * kHubGroups, kHubCtas) k_rank_rows_mp_hub(
+    int64_t n, int64_t nnz, const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
+    const float* __restrict__ v, const int32_t* __restrict__ part_i, const int32_t* __restrict__ part_k,
+    float* __restrict__ e, int32_t* __restrict__ carry_row, float* __restrict__ carry_val, double* __restrict__ gsum,
+    const int32_t* stop, int64_t tiles) {
+    if (*(volatile const int32_t*)stop) return;
+    extern __shared__ __align__(16) float hsm_[];
+    float* hub = hsm_;
+    for (int i = threadIdx.x; i < HUB; i += kMpThreads * kHubGroups) hub[i] = i < n ? __ldg(v + i) : 0.0f;
+    const int g = threadIdx.x / kMpThreads, gtid = threadIdx.x % kMpThreads;
+    char* gp = reinterpret_cast<char*>(hsm_ + HUB) +
+               (size_t)g * (sizeof(int32_t) * kMpTileBuf + sizeof(float) * kMpThreads + sizeof(int32_t) * 2 * kMpWarps +
+                            sizeof(float) * kMpWarps);
+    MpSmem sm;
+    sm.buf = reinterpret_cast<int32_t*>(gp);
+    sm.fp = reinterpret_cast<float*>(sm.buf + kMpTileBuf);
+    sm.wl_row = reinterpret_cast<int32_t*>(sm.fp + kMpThreads);
+    sm.wf_row = sm.wl_row + kMpWarps;
+    sm.wl_val = reinterpret_cast<float*>(sm.wf_row + kMpWarps);
+    __syncthreads();
+    const uint64_t pol_s = l2_policy_stream(), pol_k = l2_policy_keep();
+    auto sync = [g] { asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(kMpThreads) : "memory"); };
+    for (int64_t tile = (int64_t)blockIdx.x * kHubGroups + g; tile < tiles; tile += (int64_t)gridDim.x * kHubGroups)
+        mp_tile<HUB>(tile, gtid, sync, sm, hub, n, nnz, row_ptr, col_idx, v, part_i, part_k, e, carry_row, carry_val,
+                     gsum, pol_s, pol_k);
 }
 
 // CTA carry-outs into the rows they belong to (tile order), and the fp64 partials of sum_i e_i.
@@ -594,6 +678,22 @@ inline mapi_status csr_rank_run(int64_t n, int64_t nnz, const int32_t* row_ptr, 
     const bool v4 = (reinterpret_cast<uintptr_t>(bg) % 16 == 0) && (reinterpret_cast<uintptr_t>(cap) % 16 == 0) &&
                     (reinterpret_cast<uintptr_t>(b0) % 16 == 0);
     const int gfix = (int)std::min<int64_t>((T + 255) / 256, kCsrMaxGrid);
+    // K3h (persistent, shared-memory hub copy of v) only when MAPI_CSR_HUB=1 (=2: persistent without the
+    // hub copy); bitwise the same gather as K3.  Measured SLOWER on cfg5 (K3 3.68k it/s; K3h 2.3k on the
+    // relabelled graph; the persistent structure alone 1.67k): the default stays the one-tile-per-CTA K3.
+    const char* he = getenv("MAPI_CSR_HUB");
+    const bool hub = he && (he[0] == '1' || he[0] == '2');
+    const bool persist_only = he && he[0] == '2';
+    const unsigned hub_grid =
+        (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * kHubCtas, (T + kHubGroups - 1) / kHubGroups));
+    if (hub) {
+        err = cudaFuncSetAttribute(k_rank_rows_mp_hub<kHub>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)hub_smem_bytes());
+        if (err == cudaSuccess)
+            err = cudaFuncSetAttribute(k_rank_rows_mp_hub<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)hub_smem_bytes());
+        if (err != cudaSuccess) return csr_cuda_fail(err, "hub kernel smem");
+    }
     k_mp_partition<<<(unsigned)((T + 1 + 255) / 256), 256, 0, s>>>(n, nnz, row_ptr, T, W.part_i, W.part_k);
     launches.fetch_add(1, std::memory_order_relaxed);
     if (ev_a) cudaEventRecord(*ev_a, s);
@@ -604,8 +704,15 @@ inline mapi_status csr_rank_run(int64_t n, int64_t nnz, const int32_t* row_ptr, 
         double* S_next = W.slotS + ((t + 1) & 1) * kCsrMaxGrid;
         float* e_cur = W.e[t & 1];
         const float* e_prev = t == 0 ? nullptr : W.e[(t + 1) & 1];
-        k_rank_rows_mp<<<(unsigned)T, kMpThreads, 0, s>>>(n, nnz, row_ptr, col_idx, W.v, W.part_i, W.part_k, e_cur,
-                                                          W.carry_row, W.carry_val, W.gsum, W.stop);
+        if (hub && persist_only)
+            k_rank_rows_mp_hub<0><<<hub_grid, kMpThreads * kHubGroups, hub_smem_bytes(), s>>>(
+                n, nnz, row_ptr, col_idx, W.v, W.part_i, W.part_k, e_cur, W.carry_row, W.carry_val, W.gsum, W.stop, T);
+        else if (hub)
+            k_rank_rows_mp_hub<kHub><<<hub_grid, kMpThreads * kHubGroups, hub_smem_bytes(), s>>>(
+                n, nnz, row_ptr, col_idx, W.v, W.part_i, W.part_k, e_cur, W.carry_row, W.carry_val, W.gsum, W.stop, T);
+        else
+            k_rank_rows_mp<<<(unsigned)T, kMpThreads, 0, s>>>(n, nnz, row_ptr, col_idx, W.v, W.part_i, W.part_k,
+                                                              e_cur, W.carry_row, W.carry_val, W.gsum, W.stop);
         k_rank_fixup<<<gfix, 256, 0, s>>>(T, W.carry_row, W.carry_val, W.gsum, e_cur, W.slotY, W.stop);
         if (v4)
             k_rank_normalize<true><<<gcol, kCsrThreads, 0, s>>>(n, e_cur, e_prev, b0, W.hist, S_cur, S_next, gcol,

@@ -141,3 +141,82 @@ def test_cfg5_full_size(mapi_lib, orc, cfg5):
     ref10 = orc.rank_csr(n, cfg5["row_ptr"], cfg5["col_idx"], b0=b0, max_iters=10, tol=0.0)
     _t2(res10.w_l2.cpu().numpy(), ref10.w)
     _t3(orc, res10.w.cpu().numpy(), ref10.w)
+
+
+# ------------------------------------------------------------------------------ K3h hub cache + reorder
+
+
+def _graph(name):
+    if name == "gnutella":
+        g = synth.gnutella_like()
+        return g["n"], g["row_ptr"], g["col_idx"]
+    r = np.random.default_rng(11)
+    n = 60000  # more nodes than the hub cache
+    src = np.minimum((r.pareto(1.2, 400000) * 50).astype(np.int64), n - 1)  # skewed sources
+    dst = r.integers(0, n, 400000)
+    rp, ci = synth.csr_by_destination(n, src, dst)
+    return n, rp, ci
+
+
+@pytest.mark.parametrize("name", ["gnutella", "skewed60k"])
+def test_hub_kernel_bitwise(mapi_lib, monkeypatch, name):
+    """K3h (persistent, shared-memory hub copy of v[0, kHub)) and the persistent kernel without it gather
+    the same values in the same tiles and order as K3: the ranking is bitwise identical."""
+    m = mapi_lib
+    n, rp, ci = _graph(name)
+    b0 = np.full(n, 1.0 / n)
+    a, _, _ = _run(m, n, rp, ci, b0, 12, 0.0)  # default: K3
+    monkeypatch.setenv("MAPI_CSR_HUB", "1")
+    b, _, _ = _run(m, n, rp, ci, b0, 12, 0.0)
+    monkeypatch.setenv("MAPI_CSR_HUB", "2")
+    c, _, _ = _run(m, n, rp, ci, b0, 12, 0.0)
+    assert torch.equal(a.w, b.w) and torch.equal(a.deltas, b.deltas)
+    assert torch.equal(a.w, c.w) and torch.equal(a.deltas, c.deltas)
+
+
+@pytest.mark.parametrize("name", ["gnutella", "skewed60k"])
+def test_reorder_is_the_same_graph(mapi_lib, orc, name):
+    """mapi_csr_reorder: perm is a permutation sorted by descending out-degree (ties by id); the relabelled
+    CSR holds exactly the edge set perm(E); ranking the relabelled graph (b0 permuted, result permuted
+    back) matches the oracle on the original graph (T2 + T3)."""
+    m = mapi_lib
+    n, rp, ci = _graph(name)
+    perm, rp2, ci2 = m.csr_reorder(n, _dev(rp, torch.int32), _dev(ci.astype(np.int32)))
+    perm, rp2, ci2 = perm.cpu().numpy(), rp2.cpu().numpy(), ci2.cpu().numpy()
+    assert np.array_equal(np.sort(perm), np.arange(n))
+    outdeg = np.bincount(ci, minlength=n)
+    order = np.argsort(perm)  # order[new] = old
+    assert np.array_equal(order, np.lexsort((np.arange(n), -outdeg)))
+    dst = np.repeat(np.arange(n), np.diff(rp))
+    e_old = set(zip(perm[ci].tolist(), perm[dst].tolist()))
+    dst2 = np.repeat(np.arange(n), np.diff(rp2))
+    assert set(zip(ci2.tolist(), dst2.tolist())) == e_old and ci2.size == ci.size
+    b0 = np.full(n, 1.0 / n, np.float32)
+    b0n = m.csr_permute(_dev(perm, torch.int32), _dev(b0), to_new=True)
+    rp2d, ci2d = _dev(rp2, torch.int32), _dev(ci2.astype(np.int32))
+    cap, bg = m.csr_prepare(n, rp2d, ci2d, 0.85)
+    res = m.rank_csr(n, rp2d, ci2d, cap, bg, b0n, 15, 0.0)
+    w = m.csr_permute(_dev(perm, torch.int32), res.w, to_new=False).cpu().numpy()
+    ref = orc.rank_csr(n, rp, ci, b0=b0, max_iters=15, tol=0.0)
+    _t2(w, ref.w)
+    _t3(orc, w, ref.w)
+
+
+def test_cfg5_reordered_full_size(mapi_lib, orc, cfg5):
+    """cfg5 relabelled by out-degree (bench.py --reorder), 10 fixed iterations mapped back to the original
+    ids: T2 + T3 against the oracle on the original graph; the tol 1e-7 run stops within one iteration of
+    the oracle with the same top-100 (T3)."""
+    m = mapi_lib
+    n = cfg5["n"]
+    perm, rp, ci = m.csr_reorder(n, _dev(cfg5["row_ptr"], torch.int32), _dev(cfg5["col_idx"].astype(np.int32)))
+    b0 = m.csr_permute(perm, _dev(cfg5["b0"]), to_new=True)
+    cap, bg = m.csr_prepare(n, rp, ci, 0.85)
+    res10 = m.rank_csr(n, rp, ci, cap, bg, b0, 10, 0.0)
+    w10 = m.csr_permute(perm, res10.w, to_new=False).cpu().numpy()
+    ref10 = orc.rank_csr(n, cfg5["row_ptr"], cfg5["col_idx"], b0=cfg5["b0"], max_iters=10, tol=0.0)
+    _t2(w10, ref10.w)
+    _t3(orc, w10, ref10.w)
+    res = m.rank_csr(n, rp, ci, cap, bg, b0, 200, 1e-7)
+    ref = orc.rank_csr(n, cfg5["row_ptr"], cfg5["col_idx"], b0=cfg5["b0"], max_iters=200, tol=1e-7)
+    assert abs(res.iters_done - ref.iters_done) <= 1
+    _t3(orc, m.csr_permute(perm, res.w, to_new=False).cpu().numpy(), ref.w)
