@@ -680,7 +680,8 @@ inline mapi_status csr_rank_run(int64_t n, int64_t nnz, const int32_t* row_ptr, 
     const int gfix = (int)std::min<int64_t>((T + 255) / 256, kCsrMaxGrid);
     // K3h (persistent, shared-memory hub copy of v) only when MAPI_CSR_HUB=1 (=2: persistent without the
     // hub copy); bitwise the same gather as K3.  Measured SLOWER on cfg5 (K3 3.68k it/s; K3h 2.3k on the
-    // relabelled graph; the persistent structure alone 1.67k): the default stays the one-tile-per-CTA K3.
+    // relabelled graph; the 104 KB carve-out alone 1.67k: it displaces the L1 cache, whose 13% hit rate on
+    // the hottest v lines K3 relies on): the default stays the one-tile-per-CTA K3.
     const char* he = getenv("MAPI_CSR_HUB");
     const bool hub = he && (he[0] == '1' || he[0] == '2');
     const bool persist_only = he && he[0] == '2';
