@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include "../../include/mapi.h"
 #include "mapi_common.cuh"
 
@@ -694,6 +695,12 @@ inline mapi_status csr_rank_run(int64_t n, int64_t nnz, const int32_t* row_ptr, 
             err = cudaFuncSetAttribute(k_rank_rows_mp_hub<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)hub_smem_bytes());
         if (err != cudaSuccess) return csr_cuda_fail(err, "hub kernel smem");
+    }
+    // (investigation) MAPI_CSR_CARVEOUT=<percent>: shared-memory carve-out preference of K3, i.e. how much
+    // of the unified L1 stays cache for the gathered v
+    if (const char* co = getenv("MAPI_CSR_CARVEOUT")) {
+        err = cudaFuncSetAttribute(k_rank_rows_mp, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(co));
+        if (err != cudaSuccess) return csr_cuda_fail(err, "carveout");
     }
     k_mp_partition<<<(unsigned)((T + 1 + 255) / 256), 256, 0, s>>>(n, nnz, row_ptr, T, W.part_i, W.part_k);
     launches.fetch_add(1, std::memory_order_relaxed);
