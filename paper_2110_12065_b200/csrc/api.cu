@@ -137,6 +137,23 @@ mapi_status check_op(int32_t op, bool dot_ok = false) {
     return MAPI_OK;
 }
 
+// CUDA events for the optional kernel timing come from a per-thread pool (creating / destroying two
+// events per call cost several microseconds of host time inside small problems' steps)
+inline std::vector<cudaEvent_t>& event_pool() {
+    static thread_local std::vector<cudaEvent_t> pool;
+    return pool;
+}
+inline cudaEvent_t event_take() {
+    auto& pool = event_pool();
+    if (!pool.empty()) {
+        cudaEvent_t e = pool.back();
+        pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
 struct Timer {
     cudaEvent_t a = nullptr, b = nullptr;
     cudaStream_t s = nullptr;
@@ -144,8 +161,8 @@ struct Timer {
     explicit Timer(cudaStream_t st) : s(st) {
         on = g_profiling.load() != 0;
         if (on) {
-            cudaEventCreate(&a);
-            cudaEventCreate(&b);
+            a = event_take();
+            b = event_take();
         }
     }
     void start() {
@@ -161,8 +178,8 @@ struct Timer {
         }
     }
     ~Timer() {
-        if (a) cudaEventDestroy(a);
-        if (b) cudaEventDestroy(b);
+        if (a) event_pool().push_back(a);
+        if (b) event_pool().push_back(b);
     }
 };
 
@@ -304,7 +321,11 @@ mapi_status iterate_launch(const Device& d, int32_t op, const float* A, int64_t 
         using KernT = void (*)(IterArgs);
         KernT kern = op == 2 ? k_iterate_single<2> : (op == 1 ? k_iterate_single<1> : k_iterate_single<0>);
         const size_t smem = single_smem_bytes();
-        MAPI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        static thread_local KernT attr_done[3] = {nullptr, nullptr, nullptr};  // attribute set once per kernel
+        if (attr_done[op] != kern) {
+            MAPI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            attr_done[op] = kern;
+        }
         IterArgs a;
         a.A = A; a.n = n; a.lda = lda; a.b0 = b0; a.iters = iters; a.tol = tol;
         a.w_out = w_out; a.norms = norms; a.deltas = deltas; a.y = W.y; a.slots = W.slots;
