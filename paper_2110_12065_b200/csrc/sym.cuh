@@ -316,8 +316,8 @@ __global__ void __launch_bounds__(kSymThreads, 1) k_iterate_sym(SymArgs sa) {
         // ---- w_{t+1} = fp32(y / s_t) (fp64 division, as K2c) for the owned rows only, delta partial
         double dpart = 0.0;
         for (int64_t j = o0 + tid; j < o1; j += blockDim.x) {
-            const float wn = (float)((double)yg[j] / sd);
-            dpart += (double)fabsf(wn - wcur[j]);
+            const float wn = (float)((double)__ldcg(yg + j) / sd);
+            dpart += (double)fabsf(wn - __ldcg(wcur + j));
             wnext[j] = wn;
         }
         const double cta_d = block_sum(dpart, red);
@@ -343,7 +343,7 @@ __global__ void __launch_bounds__(kSymThreads, 1) k_iterate_sym(SymArgs sa) {
         if (p.tol > 0.0f && delta < (double)p.tol) break;
     }
     const float* wfin = wbuf + (done & 1) * n;  // w_done (on a degenerate stop: the last good iterate)
-    for (int64_t j = o0 + tid; j < o1; j += blockDim.x) p.w_out[j] = wfin[j];
+    for (int64_t j = o0 + tid; j < o1; j += blockDim.x) p.w_out[j] = __ldcg(wfin + j);
     if (blockIdx.x == 0 && tid == 0) {
         p.status[0] = status;
         p.status[1] = done;

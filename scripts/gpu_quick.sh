@@ -1,4 +1,2 @@
 mkdir -p gpurun_out
-for i in 1 2; do
-timeout 900 python bench.py --workload cfg5 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/b5.log 2>&1; tail -1 gpurun_out/b5.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('cfg5 L1KEEP', round(d['value']))"
-done
+timeout 900 python -m pytest tests/test_gpu_dense.py tests/test_gpu_random.py -q -x -k "sym or random or host" --timeout 600 > gpurun_out/pytest_quick.log 2>&1; tail -1 gpurun_out/pytest_quick.log
