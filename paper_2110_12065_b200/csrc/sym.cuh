@@ -250,7 +250,8 @@ __global__ void __launch_bounds__(kSymThreads, 1) k_iterate_sym(SymArgs sa) {
         if (blockIdx.x == 0 && tid == 0) p.bar[32 + ((t + 1) & 1)] = 0u;
         // ---- phase 2: y_j of the owned rows.  `subs` threads per row (the most that fit the owned rows in
         // one pass), consecutive threads on consecutive rows (coalesced partial reads); sub k takes partials
-        // q = k, k + subs, ... in ascending order, 48 loads in flight, fp64; the subs meet in shared memory
+        // q = k, k + subs, ... in ascending order, 48 loads in flight, each batch summed
+        // by a fixed fp32 pairwise tree and accumulated in fp64; the subs meet in shared memory
         // and are added in sub order.
         double abs_part = 0.0;
         {
@@ -275,8 +276,13 @@ __global__ void __launch_bounds__(kSymThreads, 1) k_iterate_sym(SymArgs sa) {
                             v[u] = q < ntot ? (q < nrow ? __ldcg(prow_j + q * 32) : __ldcg(pcol_j + (q - nrow) * 32))
                                             : 0.0f;
                         }
+                        // pairwise fp32 tree over the batch (6 levels), one fp64 add per batch: a per-element
+                        // fp64 conversion (F2F, a slow pipe) made this phase F2F-bound
 #pragma unroll
-                        for (int u = 0; u < 48; ++u) acc += (double)v[u];
+                        for (int h = 24; h >= 3; h >>= 1)
+#pragma unroll
+                            for (int u = 0; u < h; ++u) v[u] = v[2 * u] + v[2 * u + 1];
+                        acc += (double)((v[0] + v[1]) + v[2]);
                     }
                 }
                 redp[tid] = acc;
