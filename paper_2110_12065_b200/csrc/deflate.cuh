@@ -45,8 +45,17 @@ __global__ void __launch_bounds__(256) k_colsum_final(int64_t n, int S, const do
                                                       double* __restrict__ r) {
     const int64_t c = (int64_t)blockIdx.x * 256 + threadIdx.x;
     if (c >= n) return;
+    // the same sequential order (s ascending); loads issued 16 at a time instead of one per dependent add
     double acc = 0.0;
-    for (int s = 0; s < S; ++s) acc += part[(int64_t)s * n + c];
+    int s = 0;
+    for (; s + 16 <= S; s += 16) {
+        double v[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) v[u] = part[(int64_t)(s + u) * n + c];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) acc += v[u];
+    }
+    for (; s < S; ++s) acc += part[(int64_t)s * n + c];
     r[c] = acc;
 }
 
