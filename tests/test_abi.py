@@ -128,6 +128,24 @@ def test_validation_before_device(lib):
         m.workspace_size(m.WS_ITERATE_HOST_MANY, 1000, 1000, 50) + 2 * 4 * 1000 * 1001 // 2
 
 
+def test_csr_reorder_permute_validation(lib):
+    """mapi_csr_reorder / mapi_csr_permute validate on the host before touching the device."""
+    fake = ctypes.c_void_p(4096)
+    ws = m.workspace_size(m.WS_CSR_REORDER, 1000)
+    assert ws > 5 * 4 * 1000
+    st = lib.mapi_csr_reorder(0, 10, fake, fake, fake, fake, fake, fake, ws, None)
+    assert st == 2
+    st = lib.mapi_csr_reorder(1000, 10, None, fake, fake, fake, fake, fake, ws, None)
+    assert st == 1
+    st = lib.mapi_csr_reorder(1000, 10, fake, fake, fake, fake, fake, fake, 16, None)
+    assert st == 7
+    st = lib.mapi_csr_reorder(1000, 1 << 40, fake, fake, fake, fake, fake, fake, ws, None)
+    assert st == 2 and "int32" in _err(lib)
+    assert lib.mapi_csr_permute(0, fake, fake, fake, 1, None) == 2
+    assert lib.mapi_csr_permute(10, None, fake, fake, 1, None) == 1
+    assert lib.mapi_csr_permute(10, fake, fake, fake, 1, None) == 3  # x aliases out
+
+
 def test_pack_upper_layout():
     """pack_upper: row j of the packed buffer is A[j, j:], rows back to back (offset j n - j (j-1) / 2),
     checked against numpy's triu index order on odd / even sizes."""
