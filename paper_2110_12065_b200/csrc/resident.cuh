@@ -326,12 +326,15 @@ __global__ void __launch_bounds__(NW * 32, 1) k_iterate_resident(IterArgs p) {
         }
         __syncthreads();  // p_s (in w_s) is overwritten below
     } else {
+    // two rows' loads in flight at a time (the staging is latency-bound: one row per trip took ~2x longer)
 #pragma unroll 1
-    for (int r = 0; r < TR; ++r) {
+    for (int r = 0; r < TR; r += 2) {
         const int i = g * TR + r;
-        float v[32];
+        float v[32], u[32];
         res_load_slice(p.A, p.lda, n, r0 + i, i < R, L, lane, vec4, v);
+        if (r + 1 < TR) res_load_slice(p.A, p.lda, n, r0 + i + 1, i + 1 < R, L, lane, vec4, u);
         tmem_st32(ta + (uint32_t)(kResCPL * r), v);
+        if (r + 1 < TR) tmem_st32(ta + (uint32_t)(kResCPL * (r + 1)), u);
     }
 #pragma unroll
     for (int r = 0; r < RR; ++r) {
@@ -339,13 +342,22 @@ __global__ void __launch_bounds__(NW * 32, 1) k_iterate_resident(IterArgs p) {
         res_load_slice(p.A, p.lda, n, r0 + i, i < R, L, lane, vec4, areg[r]);
     }
 #pragma unroll 1
-    for (int r = 0; r < SR; ++r) {
-        const int i = kResTmemRows + G * RR + g * SR + r;
-        float v[32];
-        res_load_slice(p.A, p.lda, n, r0 + i, i < R, L, lane, vec4, v);
-        float4* dst = reinterpret_cast<float4*>(a_s + (size_t)(g * SR + r) * kResNPad) + 8 * L;
+    for (int r = 0; r < SR; r += 2) {
+        float v[2][32];
 #pragma unroll
-        for (int m = 0; m < 8; ++m) dst[(m + lane) & 7] = make_float4(v[4 * m], v[4 * m + 1], v[4 * m + 2], v[4 * m + 3]);
+        for (int h = 0; h < 2; ++h)
+            if (r + h < SR) {
+                const int i = kResTmemRows + G * RR + g * SR + r + h;
+                res_load_slice(p.A, p.lda, n, r0 + i, i < R, L, lane, vec4, v[h]);
+            }
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+            if (r + h < SR) {
+                float4* dst = reinterpret_cast<float4*>(a_s + (size_t)(g * SR + r + h) * kResNPad) + 8 * L;
+#pragma unroll
+                for (int m = 0; m < 8; ++m)
+                    dst[(m + lane) & 7] = make_float4(v[h][4 * m], v[h][4 * m + 1], v[h][4 * m + 2], v[h][4 * m + 3]);
+            }
     }
     }
     for (int k = tid; k < kResNPad; k += NT) w_s[k] = k < n ? p.b0[k] : 0.0f;
