@@ -192,7 +192,10 @@ __global__ void __launch_bounds__(kSymThreads, 1) k_iterate_sym(SymArgs sa) {
             auto load = [&](float (&buf)[4][8], int rb) {
 #pragma unroll
                 for (int r = 0; r < 4; ++r) {
-                    if (live && rb + r < rows) ld_stream<8, 0>(base + (int64_t)(rb + r) * p.lda, buf[r]);
+                    // (on diagonal tasks a lane whose 8 columns all lie below the row's diagonal loads nothing:
+                    // every one of its terms is masked)
+                    if (live && rb + r < rows && kl + 7 >= j0 + rb + r)
+                        ld_stream<8, 0>(base + (int64_t)(rb + r) * p.lda, buf[r]);
                     else
 #pragma unroll
                         for (int e = 0; e < 8; ++e) buf[r][e] = 0.0f;
