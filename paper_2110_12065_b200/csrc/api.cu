@@ -1001,7 +1001,11 @@ static mapi_status host_many_impl(int32_t op, int32_t count, const float* const*
             if (loaded[j]) cudaEventDestroy(loaded[j]);
             if (freed[j]) cudaEventDestroy(freed[j]);
         }
-        if (cs) cudaStreamDestroy(cs);
+        // an error may leave a queued H2D copy into ws on cs: drain it before the caller can reuse ws
+        if (cs) {
+            cudaStreamSynchronize(cs);
+            cudaStreamDestroy(cs);
+        }
     };
     cudaError_t e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
     for (int j = 0; j < 2 && e == cudaSuccess; ++j) {
@@ -1269,8 +1273,9 @@ mapi_status mapi_csr_reorder(int64_t n, int64_t nnz, const int32_t* row_ptr, con
                              int32_t* row_ptr_out, int32_t* col_idx_out, void* ws, size_t ws_bytes,
                              mapi_stream_t stream) {
     if (n < 1) return fail(MAPI_ERR_SHAPE, "n (%lld) must be >= 1", (long long)n);
-    if (nnz < 0 || nnz > INT32_MAX) return fail(MAPI_ERR_SHAPE, "nnz (%lld) out of the int32 index range", (long long)nnz);
-    if (n > INT32_MAX) return fail(MAPI_ERR_SHAPE, "n (%lld) out of the int32 index range", (long long)n);
+    // same bounds as mapi_csr_prepare / mapi_rank_csr: (int)(n + 1) items feed the CUB scan
+    if (nnz < 0 || nnz >= INT32_MAX) return fail(MAPI_ERR_SHAPE, "nnz (%lld) out of the int32 index range", (long long)nnz);
+    if (n >= INT32_MAX) return fail(MAPI_ERR_SHAPE, "n (%lld) out of the int32 index range", (long long)n);
     if (!row_ptr || !perm_out || !row_ptr_out || (nnz > 0 && (!col_idx || !col_idx_out)))
         return fail(MAPI_ERR_NULL, "row_ptr / col_idx / perm_out / row_ptr_out / col_idx_out is NULL");
     if (!ws) return fail(MAPI_ERR_WORKSPACE, "workspace is NULL");

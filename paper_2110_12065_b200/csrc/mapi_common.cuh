@@ -142,7 +142,9 @@ __device__ __forceinline__ float tree_sum(const float (&a)[N]) {
 // ---------------------------------------------------------------------------------------------
 // Grid barrier for cooperative (co-resident) launches: a monotonically increasing arrival
 // counter; the epoch-th barrier waits until counter >= epoch * gridDim.x.  The counter is
-// zeroed by the host (stream-ordered memset) before each launch.
+// zeroed by the host (stream-ordered memset) before each launch.  Targets are taken modulo
+// 2^32 and compared wrap-safely (a signed difference), so runs longer than 2^32 / gridDim.x
+// barriers stay correct: the counter never leads a waiter's target by 2^31 or more.
 __device__ __forceinline__ void grid_barrier(unsigned int* counter, unsigned int target) {
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -151,7 +153,7 @@ __device__ __forceinline__ void grid_barrier(unsigned int* counter, unsigned int
         unsigned int v;
         do {
             asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
-        } while (v < target);
+        } while ((int)(v - target) < 0);
         __threadfence();
     }
     __syncthreads();

@@ -141,6 +141,10 @@ def test_csr_reorder_permute_validation(lib):
     assert st == 7
     st = lib.mapi_csr_reorder(1000, 1 << 40, fake, fake, fake, fake, fake, fake, ws, None)
     assert st == 2 and "int32" in _err(lib)
+    # the same bounds as mapi_csr_prepare / mapi_rank_csr: n + 1 and nnz must fit the int32 scan
+    big = (1 << 31) - 1
+    assert lib.mapi_csr_reorder(big, 10, fake, fake, fake, fake, fake, fake, 1 << 62, None) == 2
+    assert lib.mapi_csr_reorder(1000, big, fake, fake, fake, fake, fake, fake, ws, None) == 2
     assert lib.mapi_csr_permute(0, fake, fake, fake, 1, None) == 2
     assert lib.mapi_csr_permute(10, None, fake, fake, 1, None) == 1
     assert lib.mapi_csr_permute(10, fake, fake, fake, 1, None) == 3  # x aliases out
