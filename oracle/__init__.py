@@ -76,6 +76,8 @@ def _load():
         lib.orc_rank_csr.argtypes = [i64, i64, P, P, dbl, P, i32, dbl, P, P, P,
                                      ctypes.POINTER(i32)]
         lib.orc_rank_csr.restype = cint
+        lib.orc_rank_csr_op.argtypes = [cint, i64, i64, P, P, dbl, P, i32, dbl, P, P, P, ctypes.POINTER(i32)]
+        lib.orc_rank_csr_op.restype = cint
         lib.orc_num_threads.argtypes = []
         lib.orc_num_threads.restype = cint
         lib.orc_set_num_threads.argtypes = [cint]
@@ -314,8 +316,9 @@ def pca_topk(C, k, iters, b0, op="min1") -> PcaResult:
     return PcaResult(st, P, norms, deltas, done)
 
 
-def rank_csr(n, row_ptr, col_idx, alpha=0.85, b0=None, max_iters=200, tol=1e-7) -> IterResult:
-    """MAPI ranking on G = alpha M + (1-alpha)/n 1 (Eq. 13), CSR by destination."""
+def rank_csr(n, row_ptr, col_idx, alpha=0.85, b0=None, max_iters=200, tol=1e-7, op="min1") -> IterResult:
+    """MAPI ranking on G = alpha M + (1-alpha)/n 1 (Eq. 13), CSR by destination.
+    op="dot": the regular PageRank power iteration G w (RPI arm of Sec. 3.3, reading R13)."""
     row_ptr = np.ascontiguousarray(np.asarray(row_ptr, dtype=np.int64))
     col_idx = np.ascontiguousarray(np.asarray(col_idx, dtype=np.int32))
     if row_ptr.shape != (n + 1,):
@@ -328,9 +331,9 @@ def rank_csr(n, row_ptr, col_idx, alpha=0.85, b0=None, max_iters=200, tol=1e-7) 
     wl2 = np.zeros(n)
     deltas = np.zeros(max_iters)
     done = ctypes.c_int32(0)
-    st = _load().orc_rank_csr(n, nnz, _ptr(row_ptr), _ptr(col_idx), float(alpha), _ptr(b0),
-                              int(max_iters), float(tol), _ptr(w), _ptr(wl2), _ptr(deltas),
-                              ctypes.byref(done))
+    st = _load().orc_rank_csr_op(_op(op), n, nnz, _ptr(row_ptr), _ptr(col_idx), float(alpha), _ptr(b0),
+                                 int(max_iters), float(tol), _ptr(w), _ptr(wl2), _ptr(deltas),
+                                 ctypes.byref(done))
     k = done.value
     return IterResult(st, w, wl2, None, deltas[:k], k)
 

@@ -122,3 +122,18 @@ def google_mavp(n, edges, w, alpha=0.85):
     G = google_matrix(n, edges, alpha)
     w = np.asarray(w, dtype=np.float64)
     return np.sum(np.sign(G * w[None, :]) * np.minimum(np.abs(G), np.abs(w)[None, :]), axis=1)
+
+
+def google_dot(n, edges, w, alpha=0.85):
+    """One dense G w product (Eq. 1 on the materialised Google matrix)."""
+    return google_matrix(n, edges, alpha) @ np.asarray(w, dtype=np.float64)
+
+
+def pagerank_eig(n, edges, alpha=0.85):
+    """The PageRank vector: the eigenvector of the dense G for its eigenvalue 1 (LAPACK geev), l1-unit and
+    non-negative (Perron-Frobenius: G is positive and column-stochastic)."""
+    G = google_matrix(n, edges, alpha)
+    vals, vecs = np.linalg.eig(G)
+    k = int(np.argmin(np.abs(vals - 1.0)))
+    v = np.real(vecs[:, k])
+    return v / v.sum()

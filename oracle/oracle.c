@@ -300,10 +300,17 @@ int orc_pca_topk(int op, const float *C, int64_t n, int64_t ldc, int32_t k, int3
  * i.e. the background term plus the per-edge difference of mins (a literal re-grouping of
  * the sum, not the GPU's clamp form).  Pinned to the dense brute force (oracle/brute.py)
  * on random graphs.  Then Algorithm 1 steps: l1 normalise, delta = ||w'-w||_1,
- * stop when tol > 0 and delta < tol, final l2 copy. */
-int orc_rank_csr(int64_t n, int64_t nnz, const int64_t *row_ptr, const int32_t *col_idx,
-                 double alpha, const double *b0, int32_t max_iters, double tol, double *w_out,
-                 double *w_l2_out, double *deltas, int32_t *iters_done) {
+ * stop when tol > 0 and delta < tol, final l2 copy.
+ * op = ORC_DOT is the regular PageRank power iteration y = G w (Eq. 1 on the G of P:307; the paper's
+ * RPI arm of Sec. 3.3), written the same way:  y_i = S + sum_{j in in(i)} (alpha/outdeg(j)) w_j,
+ * S = sum_j c_j w_j  (distributivity over G_ij = c_j + [j->i] alpha/outdeg(j)); reading R13: the iterate is
+ * l1-normalised every iteration (G is column-stochastic, so ||Gw||_1 = ||w||_1 for w >= 0 and the step is
+ * the textbook PageRank update), with the final l2 copy of P:322.  Pinned to the dense G w brute force and
+ * to the PageRank vector from a dense eigen-solve.  ORC_MIN2 equals ORC_MIN1 here (all terms >= 0). */
+int orc_rank_csr_op(int op, int64_t n, int64_t nnz, const int64_t *row_ptr, const int32_t *col_idx,
+                    double alpha, const double *b0, int32_t max_iters, double tol, double *w_out,
+                    double *w_l2_out, double *deltas, int32_t *iters_done) {
+    if (op != ORC_MIN1 && op != ORC_MIN2 && op != ORC_DOT) return ORC_ERR_BAD_PARAM;
     if (n < 1 || nnz < 0 || !row_ptr || (nnz > 0 && !col_idx) || !b0 || max_iters < 1 ||
         !(alpha > 0.0 && alpha < 1.0) || !(tol >= 0.0))
         return ORC_ERR_BAD_PARAM;
@@ -320,14 +327,21 @@ int orc_rank_csr(int64_t n, int64_t nnz, const int64_t *row_ptr, const int32_t *
     int32_t done = 0;
     for (int32_t t = 0; t < max_iters; ++t) {
         double S = 0.0;
-        for (int64_t j = 0; j < n; ++j) S += fmin(c[j], w[j]);
+        if (op == ORC_DOT)
+            for (int64_t j = 0; j < n; ++j) S += c[j] * w[j];
+        else
+            for (int64_t j = 0; j < n; ++j) S += fmin(c[j], w[j]);
 #pragma omp parallel for schedule(dynamic, 1024)
         for (int64_t i = 0; i < n; ++i) {
             double acc = 0.0;
             for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
                 int32_t j = col_idx[e];
-                double g = c[j] + alpha / (double)outdeg[j];
-                acc += fmin(g, w[j]) - fmin(c[j], w[j]);
+                if (op == ORC_DOT) {
+                    acc += (alpha / (double)outdeg[j]) * w[j];
+                } else {
+                    double g = c[j] + alpha / (double)outdeg[j];
+                    acc += fmin(g, w[j]) - fmin(c[j], w[j]);
+                }
             }
             y[i] = S + acc;
         }
@@ -375,4 +389,12 @@ void orc_set_num_threads(int n) {
 #else
     (void)n;
 #endif
+}
+
+/* The min1 ranking (the original entry point): orc_rank_csr_op with ORC_MIN1. */
+int orc_rank_csr(int64_t n, int64_t nnz, const int64_t *row_ptr, const int32_t *col_idx,
+                 double alpha, const double *b0, int32_t max_iters, double tol, double *w_out,
+                 double *w_l2_out, double *deltas, int32_t *iters_done) {
+    return orc_rank_csr_op(ORC_MIN1, n, nnz, row_ptr, col_idx, alpha, b0, max_iters, tol, w_out, w_l2_out,
+                           deltas, iters_done);
 }

@@ -386,6 +386,42 @@ def test_rank_one_step_vs_dense_arbitrary_w(orc):
     np.testing.assert_allclose(res.w, y / y.sum(), rtol=1e-13)
 
 
+def test_rank_dot_vs_dense_google_product(orc):
+    # RPI arm (reading R13): one step of the oracle's sparse + background dot form equals the dense G w of the
+    # materialised Google matrix, normalised by its l1 norm, from an arbitrary positive w (no sign or min)
+    r = np.random.default_rng(63)
+    for trial in range(20):
+        n = int(r.integers(2, 150))
+        edges, row_ptr, col_idx = synth.random_graph(n, float(r.uniform(0.01, 0.1)), seed=2000 + trial,
+                                                     n_dangling=int(r.integers(0, max(1, n // 5))))
+        w = r.random(n) + 0.01
+        y = brute.google_dot(n, edges, w)
+        res = orc.rank_csr(n, row_ptr, col_idx, b0=w, max_iters=1, tol=0.0, op="dot")
+        assert res.status == orc.OK
+        np.testing.assert_allclose(res.w, y / y.sum(), rtol=1e-13)
+        # column-stochastic G preserves the l1 norm of a non-negative vector
+        assert abs(y.sum() - w.sum()) <= 1e-12 * w.sum()
+
+
+def test_rank_dot_converges_to_pagerank_eigenvector(orc):
+    # the RPI ranking's fixed point is THE PageRank vector: the eigenvalue-1 eigenvector of the dense G
+    # from LAPACK (geev), independent of the iteration
+    for seed, n in ((70, 60), (71, 150)):
+        edges, row_ptr, col_idx = synth.random_graph(n, 0.05, seed=seed, n_dangling=n // 10)
+        pr = brute.pagerank_eig(n, edges)
+        res = orc.rank_csr(n, row_ptr, col_idx, max_iters=400, tol=0.0, op="dot")
+        np.testing.assert_allclose(res.w, pr, rtol=1e-9, atol=1e-14)
+        np.testing.assert_allclose(res.w_l2, pr / np.linalg.norm(pr), rtol=1e-9)
+
+
+def test_rank_min2_equals_min1(orc):
+    # all G_ij > 0 and w >= 0: Eq. (4)'s sign indicator is always 1, so min2 == min1 exactly
+    edges, row_ptr, col_idx = synth.random_graph(90, 0.06, seed=72, n_dangling=9)
+    a = orc.rank_csr(90, row_ptr, col_idx, max_iters=15, tol=0.0)
+    b = orc.rank_csr(90, row_ptr, col_idx, max_iters=15, tol=0.0, op="min2")
+    assert np.array_equal(a.w, b.w)
+
+
 def test_rank_star_graph_hub_first(orc):
     n = 30
     src = np.arange(1, n)
