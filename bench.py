@@ -58,6 +58,9 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--reorder", action="store_true",
                    help="cfg5: relabel nodes by out-degree first (mapi_csr_reorder; measured slower with the default kernel)")
+    p.add_argument("--csr-path", default="plan", choices=["plan", "k3"],
+                   help="cfg5: plan = segmented layout (mapi_csr_plan + mapi_rank_csr_plan, K3s, the default); "
+                        "k3 = the plan-free CSR kernel (mapi_rank_csr)")
     p.add_argument("--no-sym", action="store_true",
                    help="cfg3: time the full-matrix kernel (mapi_iterate) instead of the symmetric one")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -359,12 +362,17 @@ def build_rank(args, m, dev, stream):
         rp, ci, b0 = rp0, ci0, b0_orig
     cap, bg = m.csr_prepare(n, rp, ci, cfg["alpha"])
     T = 200
-    ws, need = m._workspace(m.WS_RANK_CSR, n, nnz, device=dev)
     w, wl2 = torch.empty(n, device=dev), torch.empty(n, device=dev)
     w_out = torch.empty(n, device=dev)
     deltas = torch.empty(T, device=dev)
     done = ctypes.c_int32(0)
     lib = m.load()
+    opc = {"min1": m.MIN1, "min2": m.MIN2, "dot": m.DOT}[args.op]
+    if args.csr_path == "plan" and not reorder:
+        return _build_rank_plan(args, m, dev, stream, cfg, n, nnz, rp, ci, cap, bg, b0, T, opc)
+    if opc == m.DOT:
+        raise SystemExit("--op dot on cfg5 needs --csr-path plan")
+    ws, need = m._workspace(m.WS_RANK_CSR, n, nnz, device=dev)
 
     def step():
         _abi_check(lib, lib.mapi_rank_csr(n, nnz, rp.data_ptr(), ci.data_ptr(), cap.data_ptr(), bg.data_ptr(),
@@ -386,6 +394,72 @@ def build_rank(args, m, dev, stream):
                                    "(mapi_csr_reorder); scores mapped back to the original ids every step"
                                    if reorder else "none (original node ids)"},
                 oracle=("rank", cfg))
+
+
+def _build_rank_plan(args, m, dev, stream, cfg, n, nnz, rp, ci, cap, bg, b0, T, opc):
+    """cfg5 through the segmented layout (K3s): the plan is built once per graph, off the timed
+    steps like the CSR construction (its build time is reported); a step is one mapi_rank_csr_plan call of
+    T fixed iterations (one persistent launch) plus the output kernels."""
+    import ctypes
+
+    import torch
+
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    plan = m.csr_plan(n, rp, ci)
+    torch.cuda.synchronize()
+    plan_s = time.perf_counter() - t0
+    plan = m.csr_plan(n, rp, ci)  # second build: the first one paid one-time CUDA / CUB set-up
+    torch.cuda.synchronize()
+    plan_s2 = time.perf_counter() - t0 - plan_s
+    info = plan.info
+    lib = m.load()
+    ws, need = m._workspace(m.WS_RANK_CSR_PLAN, n, nnz, device=dev)
+    w, wl2 = torch.empty(n, device=dev), torch.empty(n, device=dev)
+    deltas = torch.empty(T, device=dev)
+    done = ctypes.c_int32(0)
+
+    def call(iters, tol):
+        _abi_check(lib, lib.mapi_rank_csr_plan(opc, plan.buf.data_ptr(), ctypes.byref(info), cap.data_ptr(),
+                                               bg.data_ptr(), b0.data_ptr(), iters, tol, w.data_ptr(),
+                                               wl2.data_ptr(), deltas.data_ptr(), ctypes.byref(done),
+                                               ws.data_ptr(), need, stream.cuda_stream))
+        return done.value
+
+    def step():
+        call(T, 0.0)
+        return T
+
+    def extra():
+        """Time to convergence as BASELINE configs[4] specifies it (tol 1e-7 or 200 iterations): median of
+        10 calls, CUDA events around the whole API call (launch, device-side stop, outputs, status sync)."""
+        call(T, 1e-7)
+        torch.cuda.synchronize()
+        times, iters = [], 0
+        for _ in range(10):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            iters = call(T, 1e-7)
+            b.record(stream)
+            torch.cuda.synchronize()
+            times.append(a.elapsed_time(b))
+        return {"time_to_convergence": {"tol": 1e-7, "max_iters": T, "iters": iters,
+                                        "ms_median": float(np.median(times)), "ms_min": float(np.min(times)),
+                                        "calls": len(times), "what": "mapi_rank_csr_plan(tol=1e-7), whole call"},
+                "plan_build": {"first_s": plan_s, "repeat_s": plan_s2, "npieces": int(info.npieces),
+                               "nsrc": int(info.nsrc), "nseg": int(info.nseg), "nwords": int(info.nwords),
+                               "grid": int(info.grid)}}
+
+    # algorithmic HBM bytes per iteration, the same §8(d) count as the K3 path (value-free CSR): row_ptr +
+    # col_idx once, 24 B/node of node state.  The planned layout moves fewer bytes for the edges (2 B words)
+    # and more for the pieces; its measured DRAM traffic is reported from ncu (`traffic`).
+    per_iter = 4.0 * (n + 1) + 4.0 * nnz + 24.0 * n
+    return Work(step=step, unit="iterations/s", per_launch=per_iter * T, bytes_per_unit=per_iter, bound="hbm",
+                kernel="k_rank_plan (K3s: segmented layout, one persistent launch of all iterations)",
+                config={"workload": f"cfg5: {WORKLOADS['cfg5']}", "n": n, "nnz": nnz, "iters_per_step": T,
+                        "tol": 0.0, "l2_flush": "inputs larger than L2 (0.38 GB per iteration)",
+                        "op": args.op, "csr_path": "plan (mapi_csr_plan once per graph + mapi_rank_csr_plan)"},
+                oracle=("rank", cfg), extra=extra, traffic_key="cfg5_plan")
 
 
 def build_mincov(args, m, dev, stream):
@@ -623,6 +697,8 @@ def run_mapi(args, rank, world, local_rank):
                                    "value": fu * world / (fms / 1e3), "unit": work.unit, "steps": fsteps,
                                    "ms_per_step": fms / fsteps,
                                    "hbm_gbs": work.full_bytes * fu * world / (fms / 1e3) / 1e9}
+    if getattr(work, "extra", None) is not None:
+        out.update(work.extra())
     if e0 is not None and e1 is not None and e1 > e0:
         out["energy"] = {"joules": e1 - e0, "joules_per_unit": (e1 - e0) / units, "unit": work.unit.split("/")[0],
                          "avg_power_w": (e1 - e0) / t_wall, "source": "NVML total energy counter, timed region"}

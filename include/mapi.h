@@ -73,7 +73,10 @@ typedef enum {
     MAPI_WS_ITERATE_HOST_MANY = 10, /* n, nnz = lda, k = iters; add 8 bytes per problem beyond 2 */
     MAPI_WS_ITERATE_HOST_MANY_PACKED = 11, /* n, k = iters; add 8 bytes per problem beyond 2 */
     MAPI_WS_ITERATE_SYM = 12,             /* n */
-    MAPI_WS_CSR_REORDER = 13              /* n */
+    MAPI_WS_CSR_REORDER = 13,             /* n */
+    MAPI_WS_CSR_PLAN = 14,                /* n, nnz: bytes of the plan buffer of mapi_csr_plan (an upper bound) */
+    MAPI_WS_CSR_PLAN_BUILD = 15,          /* n, nnz: temporary workspace of mapi_csr_plan */
+    MAPI_WS_RANK_CSR_PLAN = 16            /* n, nnz: workspace of mapi_rank_csr_plan */
 } mapi_ws_op;
 
 /* y = A (op) x — the matrix extension of the MAVP (reading Q6: y_j uses ROW j):
@@ -274,6 +277,42 @@ mapi_status mapi_rank_csr(int64_t n, int64_t nnz, const int32_t *row_ptr, const 
                           float tol, float *w_out, float *w_l2_out, float *deltas,
                           int32_t *iters_done, void *ws, size_t ws_bytes, mapi_stream_t stream);
 
+/* Segmented ranking plan (K3s): a one-time, per-graph layout of the same CSR graph for the
+ * planned ranking kernel.  The sources with at least one out-edge are numbered by DESCENDING out-degree
+ * (ties by ascending id) and cut into segments of 32,767; each segment's edges are stored segment-major,
+ * then by destination row, as 16-bit words (local source offset | end-of-piece flag), where a "piece" is a
+ * run of at most 256 edges of one row inside one segment.  Per iteration every CTA then gathers the v
+ * values of one segment at a time from SHARED memory instead of scattered L2 reads, writes one partial per
+ * piece, and the node pass sums each row's pieces in a fixed (segment, piece) order.  The graph and its
+ * semantics are those of mapi_rank_csr (row_ptr / col_idx by destination, int32, nnz < 2^31).
+ * plan: device buffer of mapi_workspace_size(MAPI_WS_CSR_PLAN, n, nnz, 0) bytes (an upper bound); info
+ * (host) receives the sizes the run needs (keep it with the plan).  ws: MAPI_WS_CSR_PLAN_BUILD bytes of
+ * temporary device workspace.  The plan is tied to the device's SM count (info->grid).  Deterministic.
+ * Synchronises `stream` (two small read-backs size the later steps). */
+typedef struct mapi_csr_plan_info {
+    int64_t n, nnz;      /* the graph */
+    int64_t nsrc;        /* sources with out-degree >= 1 */
+    int64_t npieces;     /* pieces (= partial slots per iteration) */
+    int64_t nwords;      /* 16-bit edge words incl. segment padding */
+    int32_t nseg;        /* segments of 32,767 sources */
+    int32_t grid;        /* CTAs of the planned kernel (one per SM) */
+} mapi_csr_plan_info;
+mapi_status mapi_csr_plan(int64_t n, int64_t nnz, const int32_t *row_ptr, const int32_t *col_idx, void *plan,
+                          size_t plan_bytes, mapi_csr_plan_info *info, void *ws, size_t ws_bytes,
+                          mapi_stream_t stream);
+
+/* MAPI ranking (Eq. 13) through a plan of mapi_csr_plan: the same iteration, stop rule and
+ * outputs as mapi_rank_csr, run as ONE persistent cooperative launch (two grid barriers per iteration; a
+ * tol stop ends it on the device, no per-iteration launches).  op: MAPI_OP_MIN1 / MAPI_OP_MIN2 (identical
+ * here: G >= 0 and w >= 0) or MAPI_OP_DOT — the PageRank power iteration G w (Eq. 1 with G of P:307,
+ * reading R13: y_i = sum_j bg_j w_j + sum_{j -> i} cap_j w_j, normalised by its l1 norm each iteration
+ * (the column-stochastic G preserves it), final l2 copy P:322).  cap, bg, b0 as mapi_rank_csr.
+ * ws: mapi_workspace_size(MAPI_WS_RANK_CSR_PLAN, n, nnz, 0).  Synchronises `stream`. */
+mapi_status mapi_rank_csr_plan(int32_t op, const void *plan, const mapi_csr_plan_info *info, const float *cap,
+                               const float *bg, const float *b0, int32_t max_iters, float tol, float *w_out,
+                               float *w_l2_out, float *deltas, int32_t *iters_done, void *ws, size_t ws_bytes,
+                               mapi_stream_t stream);
+
 /* Optional preparation for the ranking path: relabel the nodes by DESCENDING out-degree (ties by ascending
  * id), so the most gathered sources get the lowest ids, which the gather kernel keeps in shared memory
  * (K3h).  perm_out[old] = new (n).  row_ptr_out (n+1) / col_idx_out (nnz): the same graph in the
@@ -296,7 +335,8 @@ mapi_status mapi_csr_permute(int64_t n, const int32_t *perm, const float *x, flo
  *   MAPI_WS_MAVP_DEFLATE: n = M.  MAPI_WS_RECONSTRUCT: n = M, nnz = N, k = r.
  *   MAPI_WS_ITERATE_SHARDED: 256 (status words).
  *   MAPI_WS_ITERATE_HOST_MANY: n, nnz = lda, k = iters (two slots; + 8 bytes per problem beyond 2).
- *   MAPI_WS_ITERATE_HOST_MANY_PACKED: n, k = iters (same, plus a packed buffer per slot). */
+ *   MAPI_WS_ITERATE_HOST_MANY_PACKED: n, k = iters (same, plus a packed buffer per slot).
+ *   MAPI_WS_CSR_PLAN / MAPI_WS_CSR_PLAN_BUILD / MAPI_WS_RANK_CSR_PLAN: n, nnz. */
 size_t mapi_workspace_size(int32_t op, int64_t n, int64_t nnz, int32_t k);
 
 const char *mapi_status_string(mapi_status status);

@@ -21,12 +21,14 @@ from ._build import build  # noqa: F401  (re-exported: compile in-tree)
 __all__ = ["load", "build", "MapiError", "mavp_matvec", "mavp_matmat", "min_covariance", "center_rows", "mavp_deflate",
            "mavp_reconstruct", "iterate", "iterate_host", "iterate_batched",
            "pca_topk", "csr_prepare", "rank_csr", "workspace_size", "launch_count", "set_profiling",
-           "last_kernel_ms", "MIN1", "MIN2", "DOT", "iterate_host_many", "iterate_host_many_packed", "pack_upper", "iterate_sym", "csr_reorder", "csr_permute"]
+           "last_kernel_ms", "MIN1", "MIN2", "DOT", "iterate_host_many", "iterate_host_many_packed", "pack_upper", "iterate_sym", "csr_reorder", "csr_permute",
+           "csr_plan", "rank_csr_plan", "CsrPlan", "PlanInfo"]
 
 MIN1, MIN2, DOT = 0, 1, 2  # DOT: regular product of Eq. (1), the RPI comparator
 (WS_MATVEC, WS_ITERATE, WS_ITERATE_BATCHED, WS_PCA_TOPK, WS_CSR_PREPARE, WS_RANK_CSR, WS_ITERATE_HOST,
  WS_MAVP_DEFLATE, WS_RECONSTRUCT, WS_ITERATE_SHARDED, WS_ITERATE_HOST_MANY,
- WS_ITERATE_HOST_MANY_PACKED, WS_ITERATE_SYM, WS_CSR_REORDER) = range(14)
+ WS_ITERATE_HOST_MANY_PACKED, WS_ITERATE_SYM, WS_CSR_REORDER, WS_CSR_PLAN, WS_CSR_PLAN_BUILD,
+ WS_RANK_CSR_PLAN) = range(17)
 STATUS = {0: "MAPI_OK", 1: "MAPI_ERR_NULL", 2: "MAPI_ERR_SHAPE", 3: "MAPI_ERR_BAD_PARAM",
           4: "MAPI_ERR_DEGENERATE", 5: "MAPI_ERR_NEGATIVE", 6: "MAPI_ERR_NONFINITE",
           7: "MAPI_ERR_WORKSPACE", 8: "MAPI_ERR_CUDA"}
@@ -74,6 +76,9 @@ def load():
             "mapi_csr_prepare": (st, [i64, i64, P, P, f32, P, P, P, sz, P]),
             "mapi_rank_csr": (st, [i64, i64, P, P, P, P, P, i32, f32, P, P, P, P, P, sz, P]),
             "mapi_csr_reorder": (st, [i64, i64, P, P, P, P, P, P, sz, P]),
+            "mapi_csr_plan": (st, [i64, i64, P, P, P, sz, ctypes.POINTER(PlanInfo), P, sz, P]),
+            "mapi_rank_csr_plan": (st, [i32, P, ctypes.POINTER(PlanInfo), P, P, P, i32, f32, P, P, P, P, P, sz,
+                                        P]),
             "mapi_csr_permute": (st, [i64, P, P, P, i32, P]),
             "mapi_workspace_size": (sz, [i32, i64, i64, i32]),
             "mapi_p2p_exchange_bytes": (sz, [i64, i32]),
@@ -519,6 +524,58 @@ def rank_csr(n: int, row_ptr, col_idx, cap, bg, b0, max_iters: int = 200, tol: f
     _check(st, done.value)
     k = done.value
     return IterResult(w, wl2, None, deltas[:k], k)
+
+class PlanInfo(ctypes.Structure):
+    """mapi_csr_plan_info (include/mapi.h): sizes of a segmented ranking plan."""
+    _fields_ = [("n", ctypes.c_int64), ("nnz", ctypes.c_int64), ("nsrc", ctypes.c_int64),
+                ("npieces", ctypes.c_int64), ("nwords", ctypes.c_int64), ("nseg", ctypes.c_int32),
+                ("grid", ctypes.c_int32)]
+
+
+@dataclass
+class CsrPlan:
+    buf: object          # device uint8 tensor holding the plan
+    info: PlanInfo
+
+
+def csr_plan(n: int, row_ptr, col_idx, ws=None, stream=None) -> CsrPlan:
+    """One-time segmented layout of the graph for rank_csr_plan (mapi_csr_plan, DESIGN.md K3s);
+    synchronises the stream."""
+    torch = _torch()
+    _need(row_ptr, "row_ptr", torch.int32, (n + 1,))
+    _need(col_idx, "col_idx", torch.int32)
+    nnz = col_idx.numel()
+    dev = row_ptr.device
+    bytes_ = workspace_size(WS_CSR_PLAN, n, nnz)
+    buf = torch.empty(max(bytes_, 256), dtype=torch.uint8, device=dev)
+    ws, need = _workspace(WS_CSR_PLAN_BUILD, n, nnz, device=dev, ws=ws)
+    info = PlanInfo()
+    _check(load().mapi_csr_plan(n, nnz, _ptr(row_ptr), _ptr(col_idx) if nnz else None, _ptr(buf), bytes_,
+                                ctypes.byref(info), _ptr(ws), need, _stream(stream)))
+    return CsrPlan(buf, info)
+
+
+def rank_csr_plan(plan: CsrPlan, cap, bg, b0, max_iters: int = 200, tol: float = 1e-7, op: int = MIN1,
+                  want_l2: bool = True, ws=None, stream=None) -> IterResult:
+    """MAPI (op MIN1/MIN2) or PageRank RPI (op DOT) ranking through a plan (mapi_rank_csr_plan, K3s);
+    synchronises the stream."""
+    torch = _torch()
+    n = plan.info.n
+    for name, t in (("cap", cap), ("bg", bg), ("b0", b0)):
+        _need(t, name, torch.float32, (n,))
+    dev = b0.device
+    w = torch.empty(n, dtype=torch.float32, device=dev)
+    wl2 = torch.empty(n, dtype=torch.float32, device=dev) if want_l2 else None
+    deltas = torch.zeros(max_iters, dtype=torch.float32, device=dev)
+    ws, need = _workspace(WS_RANK_CSR_PLAN, n, plan.info.nnz, device=dev, ws=ws)
+    done = ctypes.c_int32(0)
+    st = load().mapi_rank_csr_plan(op, _ptr(plan.buf), ctypes.byref(plan.info), _ptr(cap), _ptr(bg), _ptr(b0),
+                                   int(max_iters), float(tol), _ptr(w), _ptr(wl2), _ptr(deltas),
+                                   ctypes.byref(done), _ptr(ws), need, _stream(stream))
+    _check(st, done.value)
+    k = done.value
+    return IterResult(w, wl2, None, deltas[:k], k)
+
 
 def csr_reorder(n: int, row_ptr, col_idx, ws=None, stream=None):
     """Relabel the graph's nodes by descending out-degree (mapi_csr_reorder): returns (perm, row_ptr',

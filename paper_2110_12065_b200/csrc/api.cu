@@ -13,6 +13,8 @@
 #include <memory>
 
 #include "../../include/mapi.h"
+#include "host_common.h"
+#include "csr_plan.h"
 #include "batched.cuh"
 #include "bulk.cuh"
 #include "resident.cuh"
@@ -29,70 +31,9 @@
 
 using namespace mapi;
 
-// ---------------------------------------------------------------------------------------------
-// errors, instrumentation
-
-static thread_local char g_err[512] = "";
-static std::atomic<uint64_t> g_launches{0};
-static std::atomic<int> g_profiling{0};
-static thread_local float g_last_kernel_ms = 0.0f;
-
-static mapi_status fail(mapi_status st, const char* fmt, ...) {
-    va_list ap;
-    va_start(ap, fmt);
-    vsnprintf(g_err, sizeof(g_err), fmt, ap);
-    va_end(ap);
-    return st;
-}
-
-#define MAPI_CUDA(call)                                                                          \
-    do {                                                                                         \
-        cudaError_t e_ = (call);                                                                 \
-        if (e_ != cudaSuccess)                                                                   \
-            return fail(MAPI_ERR_CUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, \
-                        __LINE__);                                                               \
-    } while (0)
-
-#define MAPI_LAUNCHED()                                                                         \
-    do {                                                                                        \
-        g_launches.fetch_add(1, std::memory_order_relaxed);                                     \
-        cudaError_t e_ = cudaGetLastError();                                                    \
-        if (e_ != cudaSuccess)                                                                  \
-            return fail(MAPI_ERR_CUDA, "launch failed: %s (%s:%d)", cudaGetErrorString(e_),    \
-                        __FILE__, __LINE__);                                                    \
-    } while (0)
+using namespace mapi_host;
 
 namespace {
-
-struct Device {
-    int id = -1;
-    int sms = 0;
-    int smem_optin = 0;
-    int cc_major = 0;
-    size_t l2_bytes = 0;
-};
-
-mapi_status device_info(Device& d) {
-    int id = 0;
-    MAPI_CUDA(cudaGetDevice(&id));
-    static thread_local Device cache;
-    if (cache.id != id) {
-        Device x;
-        x.id = id;
-        MAPI_CUDA(cudaDeviceGetAttribute(&x.sms, cudaDevAttrMultiProcessorCount, id));
-        MAPI_CUDA(cudaDeviceGetAttribute(&x.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, id));
-        MAPI_CUDA(cudaDeviceGetAttribute(&x.cc_major, cudaDevAttrComputeCapabilityMajor, id));
-        int l2 = 0;
-        MAPI_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, id));
-        x.l2_bytes = (size_t)l2;
-        if (x.cc_major != 10)
-            return fail(MAPI_ERR_CUDA, "libmapi is built for sm_100a; device %d has compute capability %d.x",
-                        id, x.cc_major);
-        cache = x;
-    }
-    d = cache;
-    return MAPI_OK;
-}
 
 inline size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
 
@@ -136,52 +77,6 @@ mapi_status check_op(int32_t op, bool dot_ok = false) {
                     op);
     return MAPI_OK;
 }
-
-// CUDA events for the optional kernel timing come from a per-thread pool (creating / destroying two
-// events per call cost several microseconds of host time inside small problems' steps)
-inline std::vector<cudaEvent_t>& event_pool() {
-    static thread_local std::vector<cudaEvent_t> pool;
-    return pool;
-}
-inline cudaEvent_t event_take() {
-    auto& pool = event_pool();
-    if (!pool.empty()) {
-        cudaEvent_t e = pool.back();
-        pool.pop_back();
-        return e;
-    }
-    cudaEvent_t e = nullptr;
-    cudaEventCreate(&e);
-    return e;
-}
-struct Timer {
-    cudaEvent_t a = nullptr, b = nullptr;
-    cudaStream_t s = nullptr;
-    bool on = false;
-    explicit Timer(cudaStream_t st) : s(st) {
-        on = g_profiling.load() != 0;
-        if (on) {
-            a = event_take();
-            b = event_take();
-        }
-    }
-    void start() {
-        if (on) cudaEventRecord(a, s);
-    }
-    void stop() {
-        if (on) cudaEventRecord(b, s);
-    }
-    void harvest() {  // after a stream sync
-        if (on) {
-            float ms = 0.0f;
-            if (cudaEventElapsedTime(&ms, a, b) == cudaSuccess) g_last_kernel_ms = ms;
-        }
-    }
-    ~Timer() {
-        if (a) event_pool().push_back(a);
-        if (b) event_pool().push_back(b);
-    }
-};
 
 // ---------------------------------------------------------------------------------------------
 // dense iterate workspace: [header 256 B: bar @0, status[2] @64, stop @72]
@@ -689,6 +584,9 @@ size_t mapi_workspace_size(int32_t op, int64_t n, int64_t nnz, int32_t k) {
     case MAPI_WS_ITERATE_HOST_MANY_PACKED: return iterate_host_many_ws_bytes(n, packed_lda(n), k, 2, true);
     case MAPI_WS_ITERATE_SYM: return iterate_ws_bytes(n) + align256(sym_partials_bytes(n));
     case MAPI_WS_CSR_REORDER: return reorder_ws_bytes(n);
+    case MAPI_WS_CSR_PLAN: return mapi_plan::plan_bytes_bound(n, nnz);
+    case MAPI_WS_CSR_PLAN_BUILD: return mapi_plan::plan_build_ws_bytes(n, nnz);
+    case MAPI_WS_RANK_CSR_PLAN: return mapi_plan::rank_plan_ws_bytes(n, nnz);
     }
     return 0;
 }
@@ -1209,10 +1107,13 @@ mapi_status mapi_iterate_batched(int32_t op, const float* A, int64_t n, int64_t 
     st = batched_run(op, A, n, lda, B0, k, iters, tol, W_out, norms, deltas, ws, d.sms, s, &timer.a, &timer.b,
                      timer.on, g_launches);
     if (st != MAPI_OK) return fail(st, "%s", batched_last_error());
-    st = batched_finish(ws, n, k, s, iters_done);
+    int32_t bad = -1, bad_iter = 0;
+    st = batched_finish(ws, n, k, s, iters_done, &bad, &bad_iter);
     timer.harvest();
     if (st == MAPI_ERR_CUDA) return fail(st, "%s", batched_last_error());
-    if (st != MAPI_OK) return fail(st, "one or more vectors stopped with %s", mapi_status_string(st));
+    if (st != MAPI_OK)
+        return fail(st, "vector %d (the first of the k that stopped on an error): %s at iteration %d", bad,
+                    st == MAPI_ERR_DEGENERATE ? "||A (+) w_t||_1 == 0" : "||A (+) w_t||_1 is not finite", bad_iter);
     return MAPI_OK;
 }
 

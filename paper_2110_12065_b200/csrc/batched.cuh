@@ -539,8 +539,10 @@ inline mapi_status batched_run(int32_t op, const float* A, int64_t n, int64_t ld
     return MAPI_OK;
 }
 
-// Sync, read per-vector status / iteration counts; returns the worst status.
-inline mapi_status batched_finish(void* ws, int64_t n, int32_t k, cudaStream_t s, int32_t* iters_done) {
+// Sync, read per-vector status / iteration counts; returns the status of the first vector that stopped
+// on an error (its index in *bad, its iteration count in *bad_iter), MAPI_OK if none did.
+inline mapi_status batched_finish(void* ws, int64_t n, int32_t k, cudaStream_t s, int32_t* iters_done,
+                                  int32_t* bad, int32_t* bad_iter) {
     BatchedWs B = carve_batched(ws, n, k);
     int32_t* h = static_cast<int32_t*>(malloc(8 * (size_t)k));
     cudaError_t e = cudaMemcpyAsync(h, B.status, 8 * (size_t)k, cudaMemcpyDeviceToHost, s);
@@ -552,7 +554,11 @@ inline mapi_status batched_finish(void* ws, int64_t n, int32_t k, cudaStream_t s
     mapi_status worst = MAPI_OK;
     for (int32_t v = 0; v < k; ++v) {
         if (iters_done) iters_done[v] = h[2 * v + 1];
-        if (h[2 * v] != 0 && worst == MAPI_OK) worst = (mapi_status)h[2 * v];
+        if (h[2 * v] != 0 && worst == MAPI_OK) {
+            worst = (mapi_status)h[2 * v];
+            *bad = v;
+            *bad_iter = h[2 * v + 1];
+        }
     }
     free(h);
     return worst;

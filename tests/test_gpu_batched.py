@@ -82,7 +82,8 @@ def cfg4():
 
 def test_cfg4_full_size(mapi_lib, orc, cfg4):
     """BASELINE configs[3] at full size (16384^2, k = 64, 100 iterations): every vector vs the GPU
-    single-vector path (itself oracle-checked), vectors {0, 63} vs the fp64 oracle."""
+    single-vector path (itself oracle-checked), vectors {0, 1, 31, 63} (both ends, a neighbour pair and the
+    middle of the 64-vector tile) vs the fp64 oracle."""
     m = mapi_lib
     A = cfg4["A"]
     B0 = torch.from_numpy(cfg4["B0"]).cuda()
@@ -94,7 +95,7 @@ def test_cfg4_full_size(mapi_lib, orc, cfg4):
         _t2(W[v], single.w.cpu().numpy())
     A_host = A.cpu().numpy()
     norms = res.norms.cpu().numpy()
-    for v in (0, 63):
+    for v in (0, 1, 31, 63):
         ref = orc.mapi(A_host, cfg4["B0"][v], T)
         _t2(W[v], ref.w)
         np.testing.assert_allclose(norms[:, v], ref.norms, rtol=1e-5)

@@ -210,6 +210,33 @@ def cfg3_device():
     return cfg
 
 
+@pytest.fixture(scope="module")
+def cfg3_oracle(orc, cfg3_device):
+    """The fp64 oracle's 100 MAPI iterations (Alg. 1) on the fp32 bytes of cfg3's A: ~1 min on
+    the box's host cores.  Shared by the end-to-end tests of both kernels."""
+    A_host = cfg3_device["A"].cpu().numpy()
+    ref = orc.mapi(A_host, cfg3_device["b0"].astype(np.float64), cfg3_device["iters"])
+    assert ref.status == orc.OK and ref.iters_done == 100
+    return ref
+
+
+@pytest.mark.parametrize("kernel", ["sym", "full"])
+def test_cfg3_end_to_end_vs_oracle(mapi_lib, cfg3_oracle, cfg3_device, kernel):
+    """The headline workload exactly as bench.py times it (BASELINE configs[2]: 32768^2, 100 iterations,
+    b0 = 1/sqrt(n)) against the fp64 oracle's own 100-iteration trajectory (no conditioning on the GPU's
+    iterates): T2 on the final l2 vector (|cos| >= 1 - 1e-6, max|diff| <= 1e-4), every per-iteration norm
+    s_t within 1e-5 relative, the l1 iterate within 1e-6 absolute.  kernel = "sym" is mapi_iterate_sym (K2s,
+    the bench path, upper triangle only); "full" is mapi_iterate (K2c, all n^2 entries)."""
+    m = mapi_lib
+    A = cfg3_device["A"]
+    b0 = torch.from_numpy(cfg3_device["b0"]).cuda()
+    res = (m.iterate_sym if kernel == "sym" else m.iterate)(A, b0, 100)
+    assert res.iters_done == 100
+    _t2(res.w_l2.cpu().numpy(), cfg3_oracle.w, res.norms.cpu().numpy(), cfg3_oracle.norms)
+    np.testing.assert_allclose(res.w.cpu().numpy(), cfg3_oracle.w, rtol=0, atol=1e-6)
+    np.testing.assert_allclose(res.deltas.cpu().numpy(), cfg3_oracle.deltas, rtol=1e-3)
+
+
 def test_cfg3_matvec_sampled_rows(mapi_lib, orc, cfg3_device):
     """Full BASELINE size (32768^2, 4 GiB) in the bench launch configuration: T1 on 512 sampled
     rows of one mat-vec from the b0 start and from a rough iterate."""
@@ -644,3 +671,41 @@ def test_cfg3_sym_last_step(mapi_lib, orc, cfg3_device):
         full.norms.cpu().numpy().astype(np.float64))
     again = m.iterate_sym(A, b0, 100)
     assert torch.equal(r100.w, again.w)
+
+
+# ------------------------------------------------------------------------------ error paths
+
+
+@pytest.mark.parametrize("path,n", [("single", 256), ("cluster", 400), ("resident", 2048), ("rows", 1500),
+                                    ("coop", 8192), ("multi", 1000), ("sym", 8192)])
+def test_nonfinite_norm_reported(mapi_lib, monkeypatch, path, n):
+    """MAPI_ERR_NONFINITE (include/mapi.h): min-type terms are bounded by min(|a|, |w|), so a NaN or inf
+    entry is absorbed by FMNMX; the norm becomes non-finite only when the fp32 row sums overflow.  A = b0 =
+    3e38 everywhere overflows y_j at iteration 0 on every dense path; the call reports NONFINITE with
+    iters_done = 0 and the stream stays usable."""
+    m = mapi_lib
+    A = torch.full((n, n), 3e38, device="cuda")
+    b0 = torch.full((n,), 3e38, device="cuda")
+    if path == "sym":
+        monkeypatch.setenv("MAPI_SYM_PATH", "sym")
+        call = m.iterate_sym
+    else:
+        monkeypatch.setenv("MAPI_DENSE_PATH", path)
+        call = m.iterate
+    with pytest.raises(m.MapiError) as ei:
+        call(A, b0, 5)
+    assert ei.value.name == "MAPI_ERR_NONFINITE" and ei.value.iters_done == 0
+    ok = call(torch.eye(n, device="cuda") * 2, torch.full((n,), 1.0 / n, device="cuda"), 2)
+    assert torch.isfinite(ok.w).all()
+
+
+def test_nonfinite_batched_reported(mapi_lib):
+    """The batched path reports NONFINITE per vector: vector 1 overflows, vector 0 stays finite."""
+    m = mapi_lib
+    n = 1024
+    A = torch.full((n, n), 3e38, device="cuda")
+    B0 = torch.full((2, n), 1.0 / n, device="cuda")
+    B0[1] = 3e38
+    with pytest.raises(m.MapiError) as ei:
+        m.iterate_batched(A, B0, 3)
+    assert ei.value.name == "MAPI_ERR_NONFINITE" and "vector 1" in str(ei.value)

@@ -1,8 +1,8 @@
 """GPU parity of mapi_pca_topk (MAPI + L2 deflation; BASELINE configs[1]) vs the oracle.
 
 T2 per principal vector: |cos| >= 1 - 1e-6 and max|diff| <= 1e-4 on the l2-unit vectors; the
-per-iteration norms relative <= 1e-5 (vector 1, undeflated) / 5e-5 (deflated vectors, where the
-fp32 rounding of D_i enters; reading R8 in DESIGN.md).  cfg2 is checked end-to-end and
+per-iteration norms relative <= 1e-5 for every vector, deflated ones included (measured at cfg2 with the
+fp32-rounded D_i: max 5.3e-6 for vector 8, profiles/r02_cfg2_norms.log; reading R8 in DESIGN.md).  cfg2 is checked end-to-end and
 conditioned (the GPU iteration fed the oracle's own D_i, rounded once to fp32) to localise error.
 """
 import numpy as np
@@ -40,7 +40,7 @@ def test_pca_small(mapi_lib, orc, n, k):
     np.testing.assert_allclose(np.linalg.norm(P, axis=1), 1.0, rtol=1e-6)
     for i in range(k):
         _t2(P[i], ref.P[i])
-        np.testing.assert_allclose(res.norms[i].cpu().numpy(), ref.norms[i], rtol=1e-5 if i == 0 else 5e-5)
+        np.testing.assert_allclose(res.norms[i].cpu().numpy(), ref.norms[i], rtol=1e-5)
 
 
 def test_pca_k1_equals_iterate(mapi_lib):
@@ -104,7 +104,7 @@ def test_cfg2_end_to_end(mapi_lib, orc, cfg2):
     P = res.P.cpu().numpy()
     for i in range(k):
         _t2(P[i], ref.P[i])
-        np.testing.assert_allclose(res.norms[i].cpu().numpy(), ref.norms[i], rtol=1e-5 if i == 0 else 5e-5)
+        np.testing.assert_allclose(res.norms[i].cpu().numpy(), ref.norms[i], rtol=1e-5)
     cfg2["oracle_P"] = ref.P
 
 

@@ -143,6 +143,23 @@ def test_cfg5_full_size(mapi_lib, orc, cfg5):
     _t3(orc, res10.w.cpu().numpy(), ref10.w)
 
 
+def test_cfg5_fixed_200_as_benched(mapi_lib, orc, cfg5):
+    """cfg5 exactly as bench.py times it: 200 fixed iterations (tol 0) on the full graph, T2 on the final l2
+    vector and T3 on the top-100 against the oracle's 200-iteration trajectory, plus the per-iteration
+    l1 changes delta_t (1e-3 relative while they are above the fp32 noise floor of an n = 2^22 iterate)."""
+    m = mapi_lib
+    n = cfg5["n"]
+    res, _, _ = _run(m, n, cfg5["row_ptr"], cfg5["col_idx"], cfg5["b0"], 200, 0.0)
+    ref = orc.rank_csr(n, cfg5["row_ptr"], cfg5["col_idx"], b0=cfg5["b0"], max_iters=200, tol=0.0)
+    assert res.iters_done == ref.iters_done == 200
+    _t2(res.w_l2.cpu().numpy(), ref.w)
+    _t3(orc, res.w.cpu().numpy(), ref.w)
+    d_gpu, d_orc = res.deltas.cpu().numpy().astype(np.float64), ref.deltas
+    big = d_orc > 1e-6
+    np.testing.assert_allclose(d_gpu[big], d_orc[big], rtol=1e-3)
+    assert np.all(d_gpu[~big] < 1e-5)
+
+
 # ------------------------------------------------------------------------------ K3h hub cache + reorder
 
 
