@@ -278,24 +278,31 @@ mapi_status mapi_rank_csr(int64_t n, int64_t nnz, const int32_t *row_ptr, const 
                           int32_t *iters_done, void *ws, size_t ws_bytes, mapi_stream_t stream);
 
 /* Segmented ranking plan (K3s): a one-time, per-graph layout of the same CSR graph for the
- * planned ranking kernel.  The sources with at least one out-edge are numbered by DESCENDING out-degree
- * (ties by ascending id) and cut into segments of 32,767; each segment's edges are stored segment-major,
- * then by destination row, as 16-bit words (local source offset | end-of-piece flag), where a "piece" is a
- * run of at most 256 edges of one row inside one segment.  Per iteration every CTA then gathers the v
- * values of one segment at a time from SHARED memory instead of scattered L2 reads, writes one partial per
- * piece, and the node pass sums each row's pieces in a fixed (segment, piece) order.  The graph and its
- * semantics are those of mapi_rank_csr (row_ptr / col_idx by destination, int32, nnz < 2^31).
+ * planned ranking kernel.  Nodes are put in "plan order": sources (out-degree >= 1) by DESCENDING out-degree,
+ * then dangling nodes with in-edges, then isolated nodes (ties by ascending id).  The sources are cut into
+ * segments of 32,767; the edges are stored segment-major, then by the plan position of their destination
+ * row, as 16-bit words (local source offset | end-of-fragment flag), where a "fragment" is a run of one row
+ * inside one segment and one 512-word tile.  Per iteration every CTA gathers the v values of one segment at
+ * a time from SHARED memory instead of scattered L2 reads and writes one partial per fragment; the node pass
+ * collects each batch of rows' fragments through a precomputed (batch, fragment)-ordered list and sums each
+ * row's fragments in a fixed (segment, position) order.  The graph and its semantics are those of
+ * mapi_rank_csr (row_ptr / col_idx by destination, int32, nnz < 2^31).
  * plan: device buffer of mapi_workspace_size(MAPI_WS_CSR_PLAN, n, nnz, 0) bytes (an upper bound); info
  * (host) receives the sizes the run needs (keep it with the plan).  ws: MAPI_WS_CSR_PLAN_BUILD bytes of
  * temporary device workspace.  The plan is tied to the device's SM count (info->grid).  Deterministic.
- * Synchronises `stream` (two small read-backs size the later steps). */
+ * MAPI_ERR_SHAPE if one row has so many fragments that a node batch exceeds the kernel's shared memory
+ * (> 49,152 fragment sums; not reachable below ~2^24 in-edges per row): use mapi_rank_csr then.
+ * Synchronises `stream` (small read-backs size the later steps). */
 typedef struct mapi_csr_plan_info {
     int64_t n, nnz;      /* the graph */
     int64_t nsrc;        /* sources with out-degree >= 1 */
-    int64_t npieces;     /* pieces (= partial slots per iteration) */
-    int64_t nwords;      /* 16-bit edge words incl. segment padding */
+    int64_t npieces;     /* fragments (= partial sums per iteration) */
+    int64_t nwords;      /* 16-bit edge words incl. segment padding (a multiple of 512) */
     int32_t nseg;        /* segments of 32,767 sources */
     int32_t grid;        /* CTAs of the planned kernel (one per SM) */
+    int64_t nlive;       /* non-isolated nodes (plan positions [0, nlive)) */
+    int64_t nbatch;      /* node-pass batches */
+    int64_t nunits;      /* edge-pass work units */
 } mapi_csr_plan_info;
 mapi_status mapi_csr_plan(int64_t n, int64_t nnz, const int32_t *row_ptr, const int32_t *col_idx, void *plan,
                           size_t plan_bytes, mapi_csr_plan_info *info, void *ws, size_t ws_bytes,

@@ -529,7 +529,8 @@ class PlanInfo(ctypes.Structure):
     """mapi_csr_plan_info (include/mapi.h): sizes of a segmented ranking plan."""
     _fields_ = [("n", ctypes.c_int64), ("nnz", ctypes.c_int64), ("nsrc", ctypes.c_int64),
                 ("npieces", ctypes.c_int64), ("nwords", ctypes.c_int64), ("nseg", ctypes.c_int32),
-                ("grid", ctypes.c_int32)]
+                ("grid", ctypes.c_int32), ("nlive", ctypes.c_int64), ("nbatch", ctypes.c_int64),
+                ("nunits", ctypes.c_int64)]
 
 
 @dataclass

@@ -1,29 +1,39 @@
 // csr_plan.cu — K3s: the segmented MAPI ranking step (Eq. 13) for sm_100a.
 //
 // The ranking step is (K3; reading Q10)
-//     y_i = S + sum_{j -> i} v_j,   S = sum_j min(bg_j, w_j),   v_j = min(max(w_j - bg_j, 0), cap_j)
+//     y_i = S + e_i,   e_i = sum_{j -> i} v_j,   S = sum_j min(bg_j, w_j),   v_j = min(max(w_j - bg_j, 0), cap_j)
 // i.e. a gather-sum of v over each row's sources.  On the CSR layout (K3, csr.cuh) every one of the E'
 // gathers is a scattered 4-byte L2 read that costs one L1TEX wavefront: ~245 us per iteration at cfg5
 // against ~60 us of HBM traffic.  K3s changes the LAYOUT, not the arithmetic:
-//   * sources with out-degree >= 1 get compact ids by DESCENDING out-degree (ties by id); compact id p
-//     lives in segment p / 32767 at local offset p % 32767 (offset 32767 is a zero slot);
-//   * the edges are stored segment-major, then by destination row, then in CSR order, as 16-bit words
-//     `local offset | end-of-piece << 15`, where a piece is a run of <= kPieceMax edges of one row inside
-//     one segment (hub rows are split so every piece is short);
-//   * per iteration each CTA copies the v values of one segment (128 KB) into SHARED memory and streams
-//     its contiguous, piece-aligned share of the words: every gather is a shared-memory load, every piece
-//     sum a plain fp32 partial written in piece order (no atomics);
-//   * the node pass sums row i's pieces in (segment, piece) order through a static slot list (pieces
-//     sorted by row), forms y_i = S + e_i and the fp64 node state exactly as K3 does.
-// Everything runs in ONE persistent cooperative launch: init, then per iteration phase A (pieces) ->
-// grid barrier -> phase B (nodes) -> grid barrier -> identical stop decision in every CTA.  A tol stop
-// ends the launch on the device.  Deterministic: every sum has a fixed order for a given plan.
+//   * "plan order": sources (out-degree >= 1) by DESCENDING out-degree, then dangling nodes that have
+//     in-edges, then ISOLATED nodes (no in- and no out-edges); ties by id.  Every per-node array of the run
+//     (bg, cap, e, the v vector) is kept in plan order, so the node pass streams it contiguously;
+//   * source p lives in segment p / 32767 at local offset p % 32767 of the compact v vector (offset 32767 of
+//     every segment is a zero slot);
+//   * the edges are stored segment-major, then by the PLAN position of their destination row, then in CSR
+//     order, as 16-bit words `local offset | end-of-fragment << 15`.  Segment starts are aligned to the
+//     512-word warp tile; a "fragment" is a maximal run of one row inside one segment and one tile;
+//   * phase A: each CTA copies the v values of one segment (128 KB) into SHARED memory and its warps stream
+//     512-word tiles: every gather is a shared-memory load; a warp-level segmented scan (no block
+//     synchronisation) closes the fragments, which are written in fragment order (coalesced) at the tile's
+//     precomputed fragment base;
+//   * phase B: the live nodes are cut into batches (<= 4096 rows, <= 48K slots); a batch's fragment sums are
+//     gathered in (segment, fragment) order — contiguous runs of `part`, coalesced — through the static list
+//     bfrag into shared memory at their slot (row-sorted) positions brel, and every row sums its slots in
+//     (segment, position) order in fp64;
+//   * isolated nodes all have y_i = S and the same bg (checked at run time), so from iteration 1 on they are
+//     one class: count x (their delta and S terms) instead of ~43% of cfg5's node traffic.
+// Everything runs in ONE persistent cooperative launch: init, then per iteration phase A -> grid barrier ->
+// phase B -> grid barrier -> identical stop decision in every CTA.  A tol stop ends the launch on the device.
+// Deterministic: every sum has a fixed order for a given plan.
 //
-// Numerics are K3's (csr.cuh): fp32 gather sums, fp64 per-node state (R9), w_t never stored but
-// recomputed bit-exactly from (S_{t-1}, s_{t-1}, e_{t-1}); the l1 norm s = n S + sum e with sum e taken in
-// fp64 over the gathered values.  Operator DOT (RPI, reading R13): v_j = cap_j w_j, S = sum bg_j w_j.
+// Numerics: fp32 sums inside a fragment (<= 512 terms, ~6.5 on average at cfg5), the fragments of a row
+// summed in fp64; the per-node state is fp64 (R9): e_i is stored in fp64, so w_t = (S_{t-1} + e_{t-1}) /
+// s_{t-1} is recomputed bit-exactly from it; the l1 norm s = n S + sum e with sum e taken in fp64 over the
+// fragment sums.  Operator DOT (RPI, reading R13): v_j = cap_j w_j, S = sum bg_j w_j.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -42,281 +52,291 @@ constexpr int kSegShift = 15;
 constexpr int kSegStride = 1 << kSegShift;  // floats of v per segment in the compact vector (128 KB)
 constexpr int kSegSrc = kSegStride - 1;      // sources per segment; local offset kSegSrc = the zero slot
 constexpr uint16_t kDummy = (uint16_t)kSegSrc;  // padding word: the zero slot, no end flag
-constexpr int kPieceMax = 256;               // edges per piece
-constexpr int kSegAlign = 16;                // segment starts in the word array: one thread's 16 words
+constexpr int kLaneW = 16;                   // words per lane per tile (two 16 B loads)
+constexpr int kTileW = 32 * kLaneW;          // 512 words per warp tile; segment starts are tile-aligned
 constexpr int kThreads = 1024;               // planned kernel: one CTA of 32 warps per SM
-constexpr int kWpt = 16;                     // words per thread per tile (two 16 B loads)
-constexpr int kTile = kThreads * kWpt;       // 16384 words per CTA tile
-constexpr int kMaxGrid = 1024;
-constexpr int kPieceWeight = 2;              // CTA balance: an edge weighs 1, a piece 2 more (its store)
 constexpr int kWarps = kThreads / 32;
-constexpr uint64_t kMagic = 0x4d415049504c414eull;  // "MAPIPLAN"
+constexpr int kMaxGrid = 1024;
+constexpr int kStageF = kWarps * kTileW;     // phase A per-warp fragment stages (floats after the segment)
+constexpr int kSmemF = kSegStride + kStageF; // dynamic shared floats; phase B stages a batch's slots in all of it
+constexpr size_t kPlanSmem = sizeof(float) * (size_t)kSmemF;
+constexpr int kNodeK = 4;                    // rows per thread per batch
+constexpr int kBatchRows = kNodeK * kThreads;
+constexpr int kSlotBlock = 16384;            // a batch never spans two slot blocks (plus its last row)
+constexpr int kUnitBig = 256;                // phase A work units (tiles), taken dynamically: big ones first,
+constexpr int kUnitSmall = kWarps;           // then one tile per warp for the last 1/8 of the tiles
+constexpr uint64_t kMagic = 0x4d41504950334c4eull;
 
 inline size_t al256(size_t b) { return (b + 255) & ~size_t(255); }
-inline int64_t max_segments(int64_t n) { return (n + kSegSrc - 1) / kSegSrc; }
+inline int64_t max_segments(int64_t n) { return std::max<int64_t>(1, (n + kSegSrc - 1) / kSegSrc); }
+inline int64_t nwords_bound(int64_t nnz, int64_t nseg) {
+    return (nnz + kTileW - 1) / kTileW * kTileW + (int64_t)kTileW * nseg;
+}
+inline int64_t nbatch_bound(int64_t n, int64_t nnz) { return n / kBatchRows + nnz / kSlotBlock + 2; }
+inline int64_t nunits_bound(int64_t ntiles, int64_t nseg) { return ntiles / kUnitSmall + nseg + 2; }
 
 // ------------------------------------------------------------------------------- plan layout
-// [hdr 256: magic, n, nnz, nsrc, npieces, nwords, nseg, grid]
-// [q n i32: compact v index seg*32768 + off, -1 if dangling]   [segb nseg+1 i32: padded word start]
-// [ctab grid+1 i32: CTA word ranges]  [ctap grid+1 i32: CTA first piece]
-// [rsp n+1 i32: row i's slots]  [pos npieces i32: slot -> piece]  [words nwords u16]
+// [hdr 256][perm n i32: plan position -> node id][segb nseg+1 i32: padded word start of each segment]
+// [units 3 nunits i32: phase A work units (first tile, end tile, segment) in scheduling order][fbase ntiles+1
+// i32: first fragment of each tile][rsp n+1 i32: plan position -> its first slot][words nwords u16][bfrag nfrag i32: fragments in
+// (batch, fragment) order][brel nfrag u16: their slot within the batch][bstart nbatch+1 i32: batch rows]
 struct PlanView {
-    int32_t *q, *segb, *ctab, *ctap, *rsp, *pos;
+    int32_t *perm, *segb, *units, *fbase, *rsp;
     uint16_t* words;
+    int32_t* bfrag;
+    uint16_t* brel;
+    int32_t* bstart;
 };
-inline PlanView plan_view(void* plan, int64_t n, int64_t nseg, int grid, int64_t npieces) {
+inline PlanView plan_view(void* plan, int64_t n, int64_t nseg, int64_t nunits, int64_t nwords, int64_t nfrag) {
+    const int64_t ntiles = nwords / kTileW;
     char* p = static_cast<char*>(plan) + 256;
     PlanView v;
-    v.q = reinterpret_cast<int32_t*>(p); p += al256(4 * (size_t)n);
+    v.perm = reinterpret_cast<int32_t*>(p); p += al256(4 * (size_t)n);
     v.segb = reinterpret_cast<int32_t*>(p); p += al256(4 * (size_t)(nseg + 1));
-    v.ctab = reinterpret_cast<int32_t*>(p); p += al256(4 * (size_t)(grid + 1));
-    v.ctap = reinterpret_cast<int32_t*>(p); p += al256(4 * (size_t)(grid + 1));
+    v.units = reinterpret_cast<int32_t*>(p); p += al256(12 * (size_t)std::max<int64_t>(nunits, 1));
+    v.fbase = reinterpret_cast<int32_t*>(p); p += al256(4 * (size_t)(ntiles + 1));
     v.rsp = reinterpret_cast<int32_t*>(p); p += al256(4 * (size_t)(n + 1));
-    v.pos = reinterpret_cast<int32_t*>(p); p += al256(4 * (size_t)std::max<int64_t>(npieces, 1));
-    v.words = reinterpret_cast<uint16_t*>(p);
+    v.words = reinterpret_cast<uint16_t*>(p); p += al256(2 * (size_t)std::max<int64_t>(nwords, 1));
+    v.bfrag = reinterpret_cast<int32_t*>(p); p += al256(4 * (size_t)std::max<int64_t>(nfrag, 1));
+    v.brel = reinterpret_cast<uint16_t*>(p); p += al256(2 * (size_t)std::max<int64_t>(nfrag, 1));
+    v.bstart = reinterpret_cast<int32_t*>(p);
     return v;
 }
-inline size_t plan_bytes_exact(int64_t n, int64_t nseg, int grid, int64_t npieces, int64_t nwords) {
-    return 256 + al256(4 * (size_t)n) + al256(4 * (size_t)(nseg + 1)) + 2 * al256(4 * (size_t)(grid + 1)) +
-           al256(4 * (size_t)(n + 1)) + al256(4 * (size_t)std::max<int64_t>(npieces, 1)) + al256(2 * (size_t)nwords);
+inline size_t plan_bytes_exact(int64_t n, int64_t nseg, int64_t nunits, int64_t nwords, int64_t nfrag, int64_t nbatch) {
+    const int64_t ntiles = nwords / kTileW;
+    return 256 + al256(4 * (size_t)n) + al256(4 * (size_t)(nseg + 1)) + al256(12 * (size_t)std::max<int64_t>(nunits, 1)) +
+           al256(4 * (size_t)(ntiles + 1)) + al256(4 * (size_t)(n + 1)) + al256(2 * (size_t)std::max<int64_t>(nwords, 1)) +
+           al256(4 * (size_t)std::max<int64_t>(nfrag, 1)) + al256(2 * (size_t)std::max<int64_t>(nfrag, 1)) +
+           al256(4 * (size_t)(nbatch + 1));
 }
-inline int64_t nwords_bound(int64_t nnz, int64_t nseg) { return nnz + (int64_t)kSegAlign * (nseg + 1); }
 
 size_t plan_bytes_bound(int64_t n, int64_t nnz) {
     if (n < 1 || nnz < 0) return 0;
     const int64_t nseg = max_segments(n);
-    // npieces <= nnz (every piece holds >= 1 edge)
-    return plan_bytes_exact(n, nseg, kMaxGrid, nnz, nwords_bound(nnz, nseg));
+    // nfrag <= nnz (every fragment holds >= 1 edge)
+    const int64_t nw = nwords_bound(nnz, nseg);
+    return plan_bytes_exact(n, nseg, nunits_bound(nw / kTileW, nseg), nw, nnz, nbatch_bound(n, nnz));
 }
 
 // ------------------------------------------------------------------------------- build workspace
 struct BuildWs {
+    uint32_t* counter;  // [0] nsrc, [1] isolated nodes, [2] max slots of a batch
     uint32_t *outdeg, *skey, *skey2;
-    int32_t *sval, *sval2;
-    int32_t* erow;
-    uint32_t *ekey, *ekey2;
-    int32_t *eval, *eval2;
-    int32_t* srow;
-    uint16_t* soff;
-    int32_t *runb, *runb2;
-    uint32_t *pe, *pid;
-    int32_t *prow, *pend, *piota, *prow2;
-    int32_t *segstart, *rcnt;
-    uint32_t* counter;  // [0] nsrc
+    int32_t *sval, *inv, *rcnt, *segb, *bflag, *bincl;
+    int32_t *segcnt, *segstart, *tcnt;
+    uint64_t *ekey, *ekey2;
+    uint32_t *eoff, *eoff2, *fstart, *fid;
+    int32_t *frow, *frow2, *fidx, *pos, *fslot, *fbat, *fbat2;
     void* cub;
     size_t cub_bytes;
 };
 
-struct MaxOp {
-    __device__ __forceinline__ int32_t operator()(int32_t a, int32_t b) const { return a > b ? a : b; }
-};
-
-inline size_t cub_bytes_needed(int64_t n, int64_t nnz) {
-    const int nn = (int)std::max<int64_t>(n, 1), ne = (int)std::max<int64_t>(nnz, 1);
-    size_t a = 0, b = 0, c = 0, d = 0, e = 0;
+inline size_t cub_bytes_needed(int64_t n, int64_t nnz, int64_t ntiles) {
+    const int nn = (int)std::max<int64_t>(n + 1, 1), ne = (int)std::max<int64_t>(nnz, 1);
+    size_t a = 0, b = 0, c = 0, d = 0, f = 0, g = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, a, (const uint32_t*)nullptr, (uint32_t*)nullptr, (const int32_t*)nullptr,
-                                    (int32_t*)nullptr, std::max(nn, ne), 0, 32);
-    cub::DeviceScan::ExclusiveSum(nullptr, b, (const uint32_t*)nullptr, (uint32_t*)nullptr, ne);
-    cub::DeviceScan::InclusiveScan(nullptr, c, (const int32_t*)nullptr, (int32_t*)nullptr, MaxOp{}, ne);
-    cub::DeviceScan::ExclusiveSum(nullptr, d, (const int32_t*)nullptr, (int32_t*)nullptr, nn + 1);
-    e = std::max(std::max(a, b), std::max(c, d));
-    return e + 1024;
+                                    (int32_t*)nullptr, nn, 0, 32);
+    cub::DeviceRadixSort::SortPairs(nullptr, b, (const uint64_t*)nullptr, (uint64_t*)nullptr,
+                                    (const uint32_t*)nullptr, (uint32_t*)nullptr, ne, 0, 64);
+    cub::DeviceRadixSort::SortPairs(nullptr, c, (const int32_t*)nullptr, (int32_t*)nullptr, (const int32_t*)nullptr,
+                                    (int32_t*)nullptr, ne, 0, 32);
+    cub::DeviceScan::ExclusiveSum(nullptr, d, (const uint32_t*)nullptr, (uint32_t*)nullptr, ne);
+    cub::DeviceScan::ExclusiveSum(nullptr, f, (const int32_t*)nullptr, (int32_t*)nullptr,
+                                  (int)std::max<int64_t>(std::max<int64_t>(n, ntiles) + 1, 1));
+    cub::DeviceScan::InclusiveSum(nullptr, g, (const int32_t*)nullptr, (int32_t*)nullptr, nn);
+    return std::max({a, b, c, d, f, g}) + 1024;
 }
 
 size_t plan_build_ws_bytes(int64_t n, int64_t nnz) {
     if (n < 1 || nnz < 0) return 0;
-    const size_t N = 4 * (size_t)(n + 1), E = 4 * (size_t)std::max<int64_t>(nnz, 1);
-    return 256 + 5 * al256(N) + 10 * al256(E) + al256(2 * (size_t)std::max<int64_t>(nnz, 1)) + 5 * al256(E) +
-           al256(4 * (size_t)(max_segments(n) + 1)) + al256(N) + al256(cub_bytes_needed(n, nnz));
+    const int64_t nseg = max_segments(n), ntiles = nwords_bound(nnz, nseg) / kTileW;
+    const size_t N = al256(4 * (size_t)(n + 1)), E = al256(4 * (size_t)std::max<int64_t>(nnz, 1));
+    return 256 + 10 * N + 2 * al256(4 * (size_t)(nseg + 1)) + al256(4 * (size_t)(ntiles + 1)) + 4 * E /*ekey x2*/ +
+           11 * E + al256(cub_bytes_needed(n, nnz, ntiles));
 }
 
 inline BuildWs carve_build(void* ws, int64_t n, int64_t nnz) {
+    const int64_t nseg = max_segments(n), ntiles = nwords_bound(nnz, nseg) / kTileW;
     char* p = static_cast<char*>(ws);
     BuildWs b;
     b.counter = reinterpret_cast<uint32_t*>(p);
     p += 256;
     const size_t N = al256(4 * (size_t)(n + 1)), E = al256(4 * (size_t)std::max<int64_t>(nnz, 1));
-    auto takeN = [&]() { char* r = p; p += N; return r; };
-    auto takeE = [&]() { char* r = p; p += E; return r; };
-    b.outdeg = reinterpret_cast<uint32_t*>(takeN());
-    b.skey = reinterpret_cast<uint32_t*>(takeN());
-    b.skey2 = reinterpret_cast<uint32_t*>(takeN());
-    b.sval = reinterpret_cast<int32_t*>(takeN());
-    b.sval2 = reinterpret_cast<int32_t*>(takeN());
-    b.erow = reinterpret_cast<int32_t*>(takeE());
-    b.ekey = reinterpret_cast<uint32_t*>(takeE());
-    b.ekey2 = reinterpret_cast<uint32_t*>(takeE());
-    b.eval = reinterpret_cast<int32_t*>(takeE());
-    b.eval2 = reinterpret_cast<int32_t*>(takeE());
-    b.srow = reinterpret_cast<int32_t*>(takeE());
-    b.runb = reinterpret_cast<int32_t*>(takeE());
-    b.runb2 = reinterpret_cast<int32_t*>(takeE());
-    b.pe = reinterpret_cast<uint32_t*>(takeE());
-    b.pid = reinterpret_cast<uint32_t*>(takeE());
-    b.soff = reinterpret_cast<uint16_t*>(p);
-    p += al256(2 * (size_t)std::max<int64_t>(nnz, 1));
-    b.prow = reinterpret_cast<int32_t*>(takeE());
-    b.pend = reinterpret_cast<int32_t*>(takeE());
-    b.piota = reinterpret_cast<int32_t*>(takeE());
-    b.prow2 = reinterpret_cast<int32_t*>(takeE());
-    takeE();  // spare
-    b.segstart = reinterpret_cast<int32_t*>(p);
-    p += al256(4 * (size_t)(max_segments(n) + 1));
-    b.rcnt = reinterpret_cast<int32_t*>(takeN());
+    auto take = [&](size_t bytes) { char* r = p; p += bytes; return r; };
+    b.outdeg = reinterpret_cast<uint32_t*>(take(N));
+    b.skey = reinterpret_cast<uint32_t*>(take(N));
+    b.skey2 = reinterpret_cast<uint32_t*>(take(N));
+    b.sval = reinterpret_cast<int32_t*>(take(N));
+    b.inv = reinterpret_cast<int32_t*>(take(N));
+    b.rcnt = reinterpret_cast<int32_t*>(take(N));
+    b.segb = reinterpret_cast<int32_t*>(take(N));  // nseg + 1 <= n + 1
+    b.bflag = reinterpret_cast<int32_t*>(take(N));
+    b.bincl = reinterpret_cast<int32_t*>(take(N));
+    take(N);  // spare
+    b.segcnt = reinterpret_cast<int32_t*>(take(al256(4 * (size_t)(nseg + 1))));
+    b.segstart = reinterpret_cast<int32_t*>(take(al256(4 * (size_t)(nseg + 1))));
+    b.tcnt = reinterpret_cast<int32_t*>(take(al256(4 * (size_t)(ntiles + 1))));
+    b.ekey = reinterpret_cast<uint64_t*>(take(2 * E));
+    b.ekey2 = reinterpret_cast<uint64_t*>(take(2 * E));
+    b.eoff = reinterpret_cast<uint32_t*>(take(E));
+    b.eoff2 = reinterpret_cast<uint32_t*>(take(E));
+    b.fstart = reinterpret_cast<uint32_t*>(take(E));
+    b.fid = reinterpret_cast<uint32_t*>(take(E));
+    b.frow = reinterpret_cast<int32_t*>(take(E));
+    b.frow2 = reinterpret_cast<int32_t*>(take(E));
+    b.fidx = reinterpret_cast<int32_t*>(take(E));
+    b.pos = reinterpret_cast<int32_t*>(take(E));
+    b.fslot = reinterpret_cast<int32_t*>(take(E));
+    b.fbat = reinterpret_cast<int32_t*>(take(E));
+    b.fbat2 = reinterpret_cast<int32_t*>(take(E));
     b.cub = p;
-    b.cub_bytes = cub_bytes_needed(n, nnz);
+    b.cub_bytes = cub_bytes_needed(n, nnz, ntiles);
     return b;
 }
 
 // ------------------------------------------------------------------------------- build kernels
+#define GRID_STRIDE(i, count) \
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (count); i += (int64_t)gridDim.x * blockDim.x)
+
 __global__ void kp_outdeg(int64_t nnz, const int32_t* __restrict__ col_idx, uint32_t* __restrict__ outdeg) {
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x)
-        atomicAdd(outdeg + col_idx[e], 1u);  // integer histogram: order-independent
+    GRID_STRIDE(e, nnz) atomicAdd(outdeg + col_idx[e], 1u);  // integer histogram: order-independent
 }
 
-// sort key: descending out-degree (dangling last), value = id (stable sort keeps ties by ascending id)
-__global__ void kp_src_keys(int64_t n, const uint32_t* __restrict__ outdeg, uint32_t* __restrict__ key,
-                            int32_t* __restrict__ val, uint32_t* nsrc) {
-    uint32_t cnt = 0;
-    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+// plan-order key: sources by descending out-degree, then dangling nodes with in-edges, then isolated nodes;
+// value = id (the stable sort keeps ties by ascending id)
+__global__ void kp_src_keys(int64_t n, const uint32_t* __restrict__ outdeg, const int32_t* __restrict__ row_ptr,
+                            uint32_t* __restrict__ key, int32_t* __restrict__ val, uint32_t* counter) {
+    uint32_t ns = 0, ni = 0;
+    GRID_STRIDE(j, n) {
         const uint32_t d = outdeg[j];
-        key[j] = 0xffffffffu - d;
+        const bool has_in = row_ptr[j + 1] > row_ptr[j];
+        key[j] = d > 0 ? 0xfffffffdu - d : (has_in ? 0xfffffffeu : 0xffffffffu);
         val[j] = (int32_t)j;
-        cnt += d > 0;
+        ns += d > 0;
+        ni += (d == 0 && !has_in);
     }
-    cnt = __reduce_add_sync(0xffffffffu, cnt);
-    if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(nsrc, cnt);
-}
-
-__global__ void kp_q(int64_t nsrc, const int32_t* __restrict__ order, int32_t* __restrict__ q) {
-    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nsrc; p += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t seg = p / kSegSrc, off = p - seg * kSegSrc;
-        q[order[p]] = (int32_t)(seg * kSegStride + off);
+    ns = __reduce_add_sync(0xffffffffu, ns);
+    ni = __reduce_add_sync(0xffffffffu, ni);
+    if ((threadIdx.x & 31) == 0) {
+        if (ns) atomicAdd(counter + 0, ns);
+        if (ni) atomicAdd(counter + 1, ni);
     }
 }
 
-// per edge: its row (binary search in row_ptr), segment key, edge id
+__global__ void kp_inv(int64_t n, const int32_t* __restrict__ perm, int32_t* __restrict__ inv) {
+    GRID_STRIDE(p, n) inv[perm[p]] = (int32_t)p;
+}
+
+// per edge: key = (segment of its source, plan position of its row), value = the source's local offset
 __global__ void kp_edges(int64_t n, int64_t nnz, const int32_t* __restrict__ row_ptr,
-                         const int32_t* __restrict__ col_idx, const int32_t* __restrict__ q,
-                         int32_t* __restrict__ erow, uint32_t* __restrict__ ekey, int32_t* __restrict__ eval) {
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x) {
+                         const int32_t* __restrict__ col_idx, const int32_t* __restrict__ inv,
+                         uint64_t* __restrict__ ekey, uint32_t* __restrict__ eoff) {
+    GRID_STRIDE(e, nnz) {
         int64_t lo = 0, hi = n - 1;  // the row i with row_ptr[i] <= e < row_ptr[i+1]
         while (lo < hi) {
             const int64_t mid = (lo + hi + 1) >> 1;
             if ((int64_t)row_ptr[mid] <= e) lo = mid;
             else hi = mid - 1;
         }
-        erow[e] = (int32_t)lo;
-        ekey[e] = (uint32_t)(q[col_idx[e]] >> kSegShift);
-        eval[e] = (int32_t)e;
+        const int32_t ps = inv[col_idx[e]];
+        const uint32_t seg = (uint32_t)(ps / kSegSrc), off = (uint32_t)(ps - (int32_t)seg * kSegSrc);
+        ekey[e] = ((uint64_t)seg << 32) | (uint32_t)inv[lo];
+        eoff[e] = off;
     }
 }
 
-// sorted position k: row, local offset, run-start marker (max-scanned into the run begin), segment starts
-__global__ void kp_sorted(int64_t nnz, const uint32_t* __restrict__ eks, const int32_t* __restrict__ evs,
-                          const int32_t* __restrict__ erow, const int32_t* __restrict__ col_idx,
-                          const int32_t* __restrict__ q, int32_t* __restrict__ srow, uint16_t* __restrict__ soff,
-                          int32_t* __restrict__ runmark, int32_t* __restrict__ segstart) {
-    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t e = evs[k];
-        const int32_t row = erow[e];
-        const uint32_t seg = eks[k];
-        srow[k] = row;
-        soff[k] = (uint16_t)(q[col_idx[e]] & (kSegStride - 1));
-        bool start = k == 0;
-        if (!start) {
-            const uint32_t sp = eks[k - 1];
-            start = sp != seg || erow[evs[k - 1]] != row;
-            if (sp != seg) segstart[seg] = (int32_t)k;
-        } else {
-            segstart[seg] = 0;
-        }
-        runmark[k] = start ? (int32_t)k : 0;
+// segment of each sorted edge: counts and first positions
+__global__ void kp_segcount(int64_t nnz, const uint64_t* __restrict__ ek, int32_t* __restrict__ segcnt,
+                            int32_t* __restrict__ segstart) {
+    GRID_STRIDE(k, nnz) {
+        const uint32_t seg = (uint32_t)(ek[k] >> 32);
+        if (k == 0 || (uint32_t)(ek[k - 1] >> 32) != seg) segstart[seg] = (int32_t)k;
+        atomicAdd(segcnt + seg, 1);
     }
 }
 
-// end-of-piece flags: the run ends, or the piece reached kPieceMax edges
-__global__ void kp_piece_end(int64_t nnz, const int32_t* __restrict__ runb, const int32_t* __restrict__ runmark,
-                             uint32_t* __restrict__ pe) {
-    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x) {
-        // runmark[k+1] != 0 <=> a run starts at k+1 (k+1 > 0)
-        const bool next_run = (k + 1 == nnz) || runmark[k + 1] != 0;
-        const bool full = ((k - runb[k] + 1) % kPieceMax) == 0;
-        pe[k] = (next_run || full) ? 1u : 0u;
-    }
-}
-
-// per piece (at its last edge k): its row and its (unpadded) end; per-row piece counts
-__global__ void kp_pieces(int64_t nnz, const uint32_t* __restrict__ pe, const uint32_t* __restrict__ pid,
-                          const int32_t* __restrict__ srow, int32_t* __restrict__ prow, int32_t* __restrict__ pend,
-                          int32_t* __restrict__ piota, int32_t* __restrict__ rcnt) {
-    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x) {
-        if (!pe[k]) continue;
-        const uint32_t p = pid[k];
-        prow[p] = srow[k];
-        pend[p] = (int32_t)(k + 1);
-        piota[p] = (int32_t)p;
-        atomicAdd(rcnt + srow[k], 1);
-    }
-}
-
-// padded segment starts (one thread: nseg is small)
-__global__ void kp_segb(int32_t nseg, int64_t nnz, int32_t* __restrict__ segstart, int32_t* __restrict__ segb) {
+// padded segment starts, tile-aligned (one thread: nseg is small)
+__global__ void kp_segb(int32_t nseg, const int32_t* __restrict__ segcnt, int32_t* __restrict__ segb) {
     if (blockIdx.x != 0 || threadIdx.x != 0) return;
-    segstart[nseg] = (int32_t)nnz;
     int64_t acc = 0;
     for (int32_t s = 0; s < nseg; ++s) {
         segb[s] = (int32_t)acc;
-        const int64_t cnt = (int64_t)segstart[s + 1] - segstart[s];
-        acc += (cnt + kSegAlign - 1) / kSegAlign * kSegAlign;
+        acc += ((int64_t)segcnt[s] + kTileW - 1) / kTileW * kTileW;
     }
     segb[nseg] = (int32_t)acc;
 }
 
+__device__ __forceinline__ int64_t padded_pos(int64_t k, uint32_t seg, const int32_t* segstart, const int32_t* segb) {
+    return k - segstart[seg] + segb[seg];
+}
+
+// a fragment starts where the (segment, row) run starts or a tile starts
+__global__ void kp_fstart(int64_t nnz, const uint64_t* __restrict__ ek, const int32_t* __restrict__ segstart,
+                          const int32_t* __restrict__ segb, uint32_t* __restrict__ fstart) {
+    GRID_STRIDE(k, nnz) {
+        const uint64_t key = ek[k];
+        const int64_t pw = padded_pos(k, (uint32_t)(key >> 32), segstart, segb);
+        fstart[k] = (k == 0 || ek[k - 1] != key || pw % kTileW == 0) ? 1u : 0u;
+    }
+}
+
+// fragment rows / ids, per-row and per-tile fragment counts, and the words
+__global__ void kp_frag(int64_t nnz, const uint64_t* __restrict__ ek, const uint32_t* __restrict__ eoff,
+                        const uint32_t* __restrict__ fstart, const uint32_t* __restrict__ fid,
+                        const int32_t* __restrict__ segstart, const int32_t* __restrict__ segb,
+                        int32_t* __restrict__ frow, int32_t* __restrict__ fidx, int32_t* __restrict__ rcnt,
+                        int32_t* __restrict__ tcnt, uint16_t* __restrict__ words) {
+    GRID_STRIDE(k, nnz) {
+        const uint64_t key = ek[k];
+        const int64_t pw = padded_pos(k, (uint32_t)(key >> 32), segstart, segb);
+        const bool end = (k + 1 == nnz) || fstart[k + 1];
+        words[pw] = (uint16_t)(eoff[k] | (end ? 0x8000u : 0u));
+        if (fstart[k]) {
+            const uint32_t f = fid[k];
+            const int32_t row = (int32_t)(uint32_t)key;
+            frow[f] = row;
+            fidx[f] = (int32_t)f;
+            atomicAdd(rcnt + row, 1);
+            atomicAdd(tcnt + pw / kTileW, 1);
+        }
+    }
+}
+
 __global__ void kp_fill_words(int64_t nwords, uint16_t* __restrict__ words) {
-    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nwords; k += (int64_t)gridDim.x * blockDim.x)
-        words[k] = kDummy;
+    GRID_STRIDE(k, nwords) words[k] = kDummy;
 }
 
-__global__ void kp_words(int64_t nnz, const uint32_t* __restrict__ eks, const uint16_t* __restrict__ soff,
-                         const uint32_t* __restrict__ pe, const int32_t* __restrict__ segstart,
-                         const int32_t* __restrict__ segb, uint16_t* __restrict__ words) {
-    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t s = eks[k];
-        words[k + segb[s] - segstart[s]] = (uint16_t)(soff[k] | (pe[k] << 15));
-    }
+__global__ void kp_fslot(int64_t nfrag, const int32_t* __restrict__ pos, int32_t* __restrict__ fslot) {
+    GRID_STRIDE(r, nfrag) fslot[pos[r]] = (int32_t)r;
 }
 
-// CTA c's first piece: the pieces whose cumulative weight (edges + kPieceWeight per piece) is <= c W / G;
-// its word range starts at that piece's first (padded) word.  Piece-aligned boundaries: no carries
-// between CTAs.
-__global__ void kp_cta(int grid, int64_t nnz, int64_t npieces, int64_t nwords, const int32_t* __restrict__ pend,
-                       const uint32_t* __restrict__ eks, const int32_t* __restrict__ segstart,
-                       const int32_t* __restrict__ segb, int32_t* __restrict__ ctab, int32_t* __restrict__ ctap) {
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c > grid) return;
-    if (c == 0 || c == grid) {
-        ctab[c] = c == 0 ? 0 : (int32_t)nwords;
-        ctap[c] = c == 0 ? 0 : (int32_t)npieces;
-        return;
+// batch starts over the live rows: every kBatchRows rows and wherever the slot position enters a new slot
+// block, so a batch holds <= kBatchRows rows and < kSlotBlock + (its last row's slots) slots
+__global__ void kp_bflag(int64_t nlive, const int32_t* __restrict__ rsp, int32_t* __restrict__ flag) {
+    GRID_STRIDE(r, nlive) flag[r] = (r == 0 || r % kBatchRows == 0 || rsp[r] / kSlotBlock != rsp[r - 1] / kSlotBlock);
+}
+__global__ void kp_bstart(int64_t nlive, const int32_t* __restrict__ flag, const int32_t* __restrict__ incl,
+                          int32_t* __restrict__ bstart) {
+    GRID_STRIDE(r, nlive) if (flag[r]) bstart[incl[r] - 1] = (int32_t)r;
+    if (blockIdx.x == 0 && threadIdx.x == 0) bstart[incl[nlive - 1]] = (int32_t)nlive;
+}
+__global__ void kp_fbat(int64_t nfrag, const int32_t* __restrict__ frow, const int32_t* __restrict__ incl,
+                        int32_t* __restrict__ fbat, int32_t* __restrict__ fidx) {
+    GRID_STRIDE(f, nfrag) {
+        fbat[f] = incl[frow[f]] - 1;
+        fidx[f] = (int32_t)f;
     }
-    const double W = (double)nnz + (double)kPieceWeight * (double)npieces;
-    const double target = W * (double)c / (double)grid;
-    int64_t lo = 0, hi = npieces;  // count of pieces p with Wend(p) <= target
-    while (lo < hi) {
-        const int64_t mid = (lo + hi) >> 1;
-        const double wend = (double)pend[mid] + (double)kPieceWeight * (double)(mid + 1);
-        if (wend <= target) lo = mid + 1;
-        else hi = mid;
-    }
-    const int64_t P = lo;
-    ctap[c] = (int32_t)P;
-    if (P >= npieces) {
-        ctab[c] = (int32_t)nwords;
-    } else {
-        const int64_t k = P == 0 ? 0 : pend[P - 1];  // first edge of piece P
-        const uint32_t s = eks[k];
-        ctab[c] = (int32_t)(k + segb[s] - segstart[s]);
+}
+// slot of each listed fragment relative to its batch's first slot; the largest batch (shared capacity)
+__global__ void kp_brel(int64_t nfrag, const int32_t* __restrict__ bfrag, const int32_t* __restrict__ fbat,
+                        const int32_t* __restrict__ fslot, const int32_t* __restrict__ bstart,
+                        const int32_t* __restrict__ rsp, uint16_t* __restrict__ brel, uint32_t* maxslots) {
+    GRID_STRIDE(k, nfrag) {
+        const int32_t f = bfrag[k], b = fbat[f];
+        const int32_t R0 = rsp[bstart[b]], R1 = rsp[bstart[b + 1]];
+        const int32_t rel = fslot[f] - R0;
+        brel[k] = (uint16_t)min(rel, 65535);
+        if (k == (int64_t)R0) atomicMax(maxslots, (uint32_t)(R1 - R0));
     }
 }
 
@@ -325,52 +345,70 @@ __global__ void kp_cta(int grid, int64_t nnz, int64_t npieces, int64_t nwords, c
 // ================================================================================ run
 namespace mapi_plan {
 
-// workspace: [hdr 256: status[2] @0, stop @8, bar u32 @12, hist (S, s) x 2 f64 @32, flags @96]
-//            [e0 n f32][e1 n f32][vc nseg*32768 f32][part npieces f32]
-//            [slotS 2*G f64][slotY G f64][slotD G f64][slotQ G f64]
+// workspace: [hdr 256: status[2] @0, stop @8, bar u32 @12, non-uniform isolated bg @16, unit counters u32 x 4
+//            @20, hist (S, s) x 2 f64 @48]
+//            [e0 n f64][e1 n f64][bgp n f32][capp n f32][vc nseg*32768 f32][part nfrag f32]
+//            [slotY nunits f64: phase A unit sums][slotD nbatch f64][slotS 2 x nbatch f64: batch partials]
+//            [slotDi G f64][slotSi 2 x G f64: isolated-node partials per CTA][slotQ G f64]
 struct RunWs {
     int32_t* status;
     int32_t* stop;
     unsigned* bar;
+    int32_t* iso_mixed;
+    unsigned* ctr;  // [0..1] phase A unit counters, [2..3] phase B batch counters (by iteration parity)
     double* hist;
-    float *e0, *e1, *vc, *part;
-    double *slotS, *slotY, *slotD, *slotQ;
+    double *e0, *e1;
+    float *bgp, *capp, *vc, *part;
+    double *slotY, *slotD, *slotS, *slotDi, *slotSi, *slotQ;
+    int64_t nbatch;
 };
-inline size_t run_ws_exact(int64_t n, int64_t nseg, int64_t npieces) {
-    return 256 + 2 * al256(4 * (size_t)n) + al256(4 * (size_t)kSegStride * (size_t)std::max<int64_t>(nseg, 1)) +
-           al256(4 * (size_t)std::max<int64_t>(npieces, 1)) + 5 * al256(8 * (size_t)kMaxGrid);
+inline size_t run_ws_exact(int64_t n, int64_t nseg, int64_t nfrag, int64_t nunits, int64_t nbatch) {
+    return 256 + 2 * al256(8 * (size_t)n) + 2 * al256(4 * (size_t)n) +
+           al256(4 * (size_t)kSegStride * (size_t)std::max<int64_t>(nseg, 1)) +
+           al256(4 * (size_t)std::max<int64_t>(nfrag, 1)) + al256(8 * (size_t)std::max<int64_t>(nunits, 1)) +
+           3 * al256(8 * (size_t)std::max<int64_t>(nbatch, 1)) + 4 * al256(8 * (size_t)kMaxGrid);
 }
 size_t rank_plan_ws_bytes(int64_t n, int64_t nnz) {
     if (n < 1 || nnz < 0) return 0;
-    return run_ws_exact(n, max_segments(n), std::max<int64_t>(nnz, 1));
+    const int64_t nseg = max_segments(n), nw = nwords_bound(nnz, nseg);
+    return run_ws_exact(n, nseg, std::max<int64_t>(nnz, 1), nunits_bound(nw / kTileW, nseg), nbatch_bound(n, nnz));
 }
-inline RunWs carve_run(void* ws, int64_t n, int64_t nseg, int64_t npieces) {
+inline RunWs carve_run(void* ws, int64_t n, int64_t nseg, int64_t nfrag, int64_t nunits, int64_t nbatch) {
     char* p = static_cast<char*>(ws);
     RunWs r;
     r.status = reinterpret_cast<int32_t*>(p);
     r.stop = reinterpret_cast<int32_t*>(p + 8);
     r.bar = reinterpret_cast<unsigned*>(p + 12);
-    r.hist = reinterpret_cast<double*>(p + 32);
+    r.iso_mixed = reinterpret_cast<int32_t*>(p + 16);
+    r.ctr = reinterpret_cast<unsigned*>(p + 20);
+    r.hist = reinterpret_cast<double*>(p + 48);
     p += 256;
-    r.e0 = reinterpret_cast<float*>(p); p += al256(4 * (size_t)n);
-    r.e1 = reinterpret_cast<float*>(p); p += al256(4 * (size_t)n);
+    r.e0 = reinterpret_cast<double*>(p); p += al256(8 * (size_t)n);
+    r.e1 = reinterpret_cast<double*>(p); p += al256(8 * (size_t)n);
+    r.bgp = reinterpret_cast<float*>(p); p += al256(4 * (size_t)n);
+    r.capp = reinterpret_cast<float*>(p); p += al256(4 * (size_t)n);
     r.vc = reinterpret_cast<float*>(p); p += al256(4 * (size_t)kSegStride * (size_t)std::max<int64_t>(nseg, 1));
-    r.part = reinterpret_cast<float*>(p); p += al256(4 * (size_t)std::max<int64_t>(npieces, 1));
-    r.slotS = reinterpret_cast<double*>(p); p += 2 * al256(8 * (size_t)kMaxGrid);
-    r.slotY = reinterpret_cast<double*>(p); p += al256(8 * (size_t)kMaxGrid);
-    r.slotD = reinterpret_cast<double*>(p); p += al256(8 * (size_t)kMaxGrid);
+    r.part = reinterpret_cast<float*>(p); p += al256(4 * (size_t)std::max<int64_t>(nfrag, 1));
+    r.slotY = reinterpret_cast<double*>(p); p += al256(8 * (size_t)std::max<int64_t>(nunits, 1));
+    const size_t B = al256(8 * (size_t)std::max<int64_t>(nbatch, 1));
+    r.slotD = reinterpret_cast<double*>(p); p += B;
+    r.slotS = reinterpret_cast<double*>(p); p += 2 * B;  // parity q at slotS + q * (B / 8)
+    r.slotDi = reinterpret_cast<double*>(p); p += al256(8 * (size_t)kMaxGrid);
+    r.slotSi = reinterpret_cast<double*>(p); p += 2 * al256(8 * (size_t)kMaxGrid);
     r.slotQ = reinterpret_cast<double*>(p);
+    r.nbatch = (int64_t)(B / 8);  // parity stride of slotS
     return r;
 }
 
 struct RunArgs {
-    int64_t n;
-    int32_t nseg, iters;
+    int64_t n, nlive, nsrc;
+    int32_t nseg, iters, nunits, nbatch;
     float tol;
-    const int32_t *q, *segb, *ctab, *ctap, *rsp, *pos;
-    const uint16_t* words;
+    const int32_t *perm, *segb, *units, *fbase, *rsp, *bstart, *bfrag;
+    const uint16_t *brel, *words;
     const float *cap, *bg, *b0;
     float* deltas;
+    unsigned long long* trace;  // optional: phase stamps (globaltimer), see PLAN_STAMP
     RunWs w;
 };
 
@@ -392,204 +430,246 @@ __device__ __forceinline__ double node_s(double w, float bg) {
     if constexpr (OP == 2) return (double)bg * w;
     else return fmin((double)bg, w);
 }
+// compact v index of plan position p < nsrc
+__device__ __forceinline__ int64_t vc_index(int64_t p) {
+    const int64_t seg = p / kSegSrc;
+    return seg * kSegStride + (p - seg * kSegSrc);
+}
 
-// sum of G fp64 slots in a fixed order (warp 0 lane-strided, butterfly), broadcast; slots written by
-// other CTAs of this launch are read through L2
-__device__ __forceinline__ double slots_sum(const double* slots, int count, double* red) {
+// sum of `count` fp64 slots in a fixed order (thread i: slots i, i + 1024, ... ascending, then the block
+// tree), broadcast; slots written by other CTAs of this launch are read through L2
+__device__ __forceinline__ double slots_sum(const double* slots, int64_t count, double* red) {
+    double part = 0.0;
+    for (int64_t c = threadIdx.x; c < count; c += blockDim.x) part += __ldcg(slots + c);
+    return mapi::block_sum(part, red);
+}
+// two block sums at once (one set of barriers), results broadcast
+__device__ __forceinline__ void block_sum2(double& a, double& b, double* red) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    a = mapi::warp_sum(a);
+    b = mapi::warp_sum(b);
     __syncthreads();
-    if (threadIdx.x < 32) {
-        double part = 0.0;
-        for (int c = threadIdx.x; c < count; c += 32) part += __ldcg(slots + c);
-        part = mapi::warp_sum(part);
-        if (threadIdx.x == 0) red[32] = part;
+    if (lane == 0) {
+        red[warp] = a;
+        red[40 + warp] = b;
     }
     __syncthreads();
-    return red[32];
+    if (warp == 0) {
+        double x = red[lane], y = red[40 + lane];
+        x = mapi::warp_sum(x);
+        y = mapi::warp_sum(y);
+        if (lane == 0) {
+            red[32] = x;
+            red[72] = y;
+        }
+    }
+    __syncthreads();
+    a = red[32];
+    b = red[72];
 }
 
-// segmented-scan element: piece count, carried fp32 sum, "a piece ended here" flag
-struct ScanEl {
-    int c;
-    float v;
-    int f;
-};
-__device__ __forceinline__ ScanEl scan_op(const ScanEl& a, const ScanEl& b) {  // a before b
-    return ScanEl{a.c + b.c, b.f ? b.v : a.v + b.v, a.f | b.f};
+// one 512-word tile: 16 words per lane (lane l: words 16 l .. 16 l + 15), gathers from the shared segment,
+// fragments closed by a warp-level segmented scan, staged in the warp's shared buffer in fragment order and
+// written to part[fb ..) with coalesced stores.  Returns the fp64 sum of the tile's fragment sums.
+__device__ __forceinline__ double plan_tile(const uint4 (&wd)[2], const float* __restrict__ vseg, int32_t fb,
+                                            float* __restrict__ stage, float* __restrict__ part, int lane) {
+    const uint32_t u[8] = {wd[0].x, wd[0].y, wd[0].z, wd[0].w, wd[1].x, wd[1].y, wd[1].z, wd[1].w};
+    float x[kLaneW];
+    uint32_t fl = 0;
+#pragma unroll
+    for (int h = 0; h < 8; ++h) {
+        const uint32_t lo = u[h] & 0xffffu, hi = u[h] >> 16;
+        x[2 * h] = vseg[lo & 0x7fffu];
+        x[2 * h + 1] = vseg[hi & 0x7fffu];
+        fl |= (lo >> 15) << (2 * h);
+        fl |= (hi >> 15) << (2 * h + 1);
+    }
+    const int cnt = __popc(fl);
+    const int last = fl ? 31 - __clz(fl) : -1;
+    float tail = 0.0f;  // words after the lane's last end flag (all of them if none)
+#pragma unroll
+    for (int i = 0; i < kLaneW; ++i)
+        if (i > last) tail += x[i];
+    // inclusive segmented scan over lanes of (has flag, tail): the run carried into the next lane
+    int f = cnt > 0;
+    float v = tail;
+    int cpre = cnt;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const int fo = __shfl_up_sync(0xffffffffu, f, off);
+        const float vo = __shfl_up_sync(0xffffffffu, v, off);
+        const int co = __shfl_up_sync(0xffffffffu, cpre, off);
+        if (lane >= off) {
+            if (!f) v = vo + v;
+            f |= fo;
+            cpre += co;
+        }
+    }
+    float carry = __shfl_up_sync(0xffffffffu, v, 1);
+    const int total = __shfl_sync(0xffffffffu, cpre, 31);
+    const int before = cpre - cnt;
+    if (lane == 0) carry = 0.0f;
+    // close this lane's fragments in word order: the first one continues the carried run
+    float acc = carry;
+    int k = before;
+#pragma unroll
+    for (int i = 0; i < kLaneW; ++i) {
+        acc += x[i];
+        if ((fl >> i) & 1u) {
+            stage[k++] = acc;
+            acc = 0.0f;
+        }
+    }
+    __syncwarp();
+    double gs = 0.0;
+    for (int i = lane; i < total; i += 32) {
+        const float y = stage[i];
+        __stcg(part + fb + i, y);
+        gs += (double)y;
+    }
+    __syncwarp();  // the stage is reused by the warp's next tile
+    return gs;
 }
 
-struct PlanSmem {
-    ScanEl wtot[kWarps];   // warp inclusive totals
-    ScanEl wpre[kWarps];   // exclusive warp prefixes (incl. the tile carry)
-    ScanEl total;          // tile carry-out
-    double red[33];
-};
+// trace layout: [64 iterations][4] CTA 0 stamps, then per CTA [4] sums over iterations 3..63 of the stamps'
+// differences (phase A, barrier 1, phase B, barrier 2 + stop test), ns
+#define PLAN_STAMP(k)                                                                                    \
+    if (a.trace && tid == 0 && t < 64) {                                                                 \
+        unsigned long long gt_;                                                                          \
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt_));                                          \
+        if (c == 0) a.trace[t * 4 + (k)] = gt_;                                                          \
+        if (t >= 3 && (k) > 0) a.trace[256 + c * 4 + (k) - 1] += gt_ - tprev_;                           \
+        if (t >= 3 && (k) == 0) a.trace[256 + c * 4 + 3] += gt_ - tprev_;                               \
+        tprev_ = gt_;                                                                                    \
+    }
 
 template <int OP>
 __global__ void __launch_bounds__(kThreads, 1) k_rank_plan(RunArgs a) {
-    extern __shared__ __align__(16) float vseg[];  // kSegStride floats
-    __shared__ PlanSmem sm;
+    extern __shared__ __align__(16) float vseg[];  // phase A: segment (kSegStride) + warp stages; phase B: slots
+    __shared__ double red[80];
+    __shared__ int32_t s_next[2];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int G = gridDim.x, c = blockIdx.x;
-    const int64_t n = a.n;
+    const int64_t n = a.n, nlive = a.nlive, niso = n - nlive;
+    const int32_t nb = a.nbatch;
     RunWs& W = a.w;
+    const int64_t SB = W.nbatch;  // parity stride of slotS
     unsigned epoch = 0;
-    // node range of this CTA (phase B / init): contiguous, multiple of 4
-    const int64_t chunk = ((n + G - 1) / G + 3) & ~int64_t(3);
-    const int64_t j0 = std::min<int64_t>(n, (int64_t)c * chunk), j1 = std::min<int64_t>(n, j0 + chunk);
+    const int64_t i0 = nlive + niso * c / G, i1 = nlive + niso * (c + 1) / G;  // isolated-node slice
+    const float bg_iso = niso > 0 ? a.bg[a.perm[nlive]] : 0.0f;
 
-    // ---- init: w_0 = b0 (>= 0), v, S_0 partials (parity 0)
+    // ---- init: plan-order copies of bg / cap, w_0 = b0 (>= 0), v, S_0 partials per batch (parity 0)
     {
+        int neg = 0, mixed = 0;
+        for (int32_t b = (int32_t)((int64_t)nb * c / G); b < (int32_t)((int64_t)nb * (c + 1) / G); ++b) {
+            double sp = 0.0;
+            for (int64_t p = a.bstart[b] + tid; p < a.bstart[b + 1]; p += kThreads) {
+                const int32_t id = a.perm[p];
+                const double wj = (double)a.b0[id];
+                neg |= wj < 0.0;
+                const float bgj = a.bg[id], cp = a.cap[id];
+                W.bgp[p] = bgj;
+                W.capp[p] = cp;
+                if (p < a.nsrc) W.vc[vc_index(p)] = node_v<OP>(wj, bgj, cp);
+                sp += node_s<OP>(wj, bgj);
+            }
+            const double S = mapi::block_sum(sp, red);
+            if (tid == 0) W.slotS[b] = S;
+        }
         double sp = 0.0;
-        int neg = 0;
-        for (int64_t j = j0 + tid; j < j1; j += kThreads) {
-            const double wj = (double)a.b0[j];
+        for (int64_t p = i0 + tid; p < i1; p += kThreads) {
+            const int32_t id = a.perm[p];
+            const double wj = (double)a.b0[id];
             neg |= wj < 0.0;
-            const float b = a.bg[j];
-            const int32_t qj = a.q[j];
-            if (qj >= 0) W.vc[qj] = node_v<OP>(wj, b, a.cap[j]);
-            sp += node_s<OP>(wj, b);
+            const float bgj = a.bg[id];
+            W.bgp[p] = bgj;
+            mixed |= __float_as_uint(bgj) != __float_as_uint(bg_iso);
+            sp += node_s<OP>(wj, bgj);
         }
         if (__syncthreads_or(neg) && tid == 0) {
             W.status[0] = MAPI_ERR_NEGATIVE;
             W.stop[0] = 1;
         }
-        const double S = mapi::block_sum(sp, sm.red);
-        if (tid == 0) W.slotS[c] = S;
+        if (__syncthreads_or(mixed) && tid == 0) atomicOr(W.iso_mixed, 1);
+        const double S = mapi::block_sum(sp, red);
+        if (tid == 0) W.slotSi[c] = S;
         mapi::grid_barrier(W.bar, ++epoch * G);
         if (*(volatile int32_t*)W.stop) return;
     }
+    const bool iso_class = *(volatile int32_t*)W.iso_mixed == 0;
 
-    // CTA word range and first piece; the segment holding its first word
-    const int32_t cb = a.ctab[c], ce = a.ctab[c + 1];
-    const int32_t p0 = a.ctap[c];
-    int s0 = 0;
-    {
-        int lo = 0, hi = a.nseg - 1;  // largest s with segb[s] <= cb
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (a.segb[mid] <= cb) lo = mid;
-            else hi = mid - 1;
-        }
-        s0 = lo;
-    }
     const float4* vc4 = reinterpret_cast<const float4*>(W.vc);
     const uint4* words4 = reinterpret_cast<const uint4*>(a.words);
+    float* wstage = vseg + kSegStride + warp * kTileW;
+    unsigned long long tprev_ = 0;
+    int cur_seg = -1;  // the segment held in shared memory (phase B overwrites it)
 
     for (int32_t t = 0; t < a.iters; ++t) {
-        // ================= phase A: piece partials of e_i = sum_{j -> i} v_j (fp32), fp64 sum of the gathers
-        double gp = 0.0;
-        int32_t piece = p0;
-        float carry = 0.0f;
-        int32_t pb = cb;
-        for (int s = s0; pb < ce; ++s) {
-            const int32_t run_end = min(ce, a.segb[s + 1]);
-            if (run_end <= pb) continue;
-            __syncthreads();  // the previous run's gathers are done
-            for (int i = tid; i < kSegStride / 4; i += kThreads) reinterpret_cast<float4*>(vseg)[i] = __ldcg(vc4 + (int64_t)s * (kSegStride / 4) + i);
+        PLAN_STAMP(0);
+        // ================= phase A: fragment sums of e_i (fp32) over units taken from a counter; per unit the
+        // fp64 sum of its fragment sums (slotY[unit]: a fixed order whichever CTA ran it)
+        {
+            unsigned* ctr = W.ctr + (t & 1);
+            if (tid == 0) s_next[0] = (int32_t)atomicAdd(ctr, 1u);
             __syncthreads();
-            for (int32_t base = pb & ~(kWpt - 1); base < run_end; base += kTile) {
-                const int32_t idx = base + tid * kWpt;
-                uint32_t wd[8];
-                if (idx < run_end && idx + kWpt > pb) {
-                    const uint4 A = __ldcs(words4 + idx / 8), B = __ldcs(words4 + idx / 8 + 1);
-                    wd[0] = A.x; wd[1] = A.y; wd[2] = A.z; wd[3] = A.w;
-                    wd[4] = B.x; wd[5] = B.y; wd[6] = B.z; wd[7] = B.w;
-                    if (idx < pb || idx + kWpt > run_end) {  // the CTA's first / last 16 words: mask others'
+            int q = 0;
+            for (int32_t u = s_next[0]; u < a.nunits; u = s_next[q]) {
+                const int32_t ta = __ldg(a.units + 3 * u), tb = __ldg(a.units + 3 * u + 1), seg = __ldg(a.units + 3 * u + 2);
+                if (tid == 0) s_next[q ^ 1] = (int32_t)atomicAdd(ctr, 1u);  // the next unit, fetched early
+                if (seg != cur_seg) {  // uniform across the block
+                    __syncthreads();  // the previous unit's gathers are done
+                    const float4* src = vc4 + (int64_t)seg * (kSegStride / 4);
+                    float4 r[kSegStride / 4 / kThreads];
 #pragma unroll
-                        for (int h = 0; h < 8; ++h) {
-                            const int32_t x0 = idx + 2 * h;
-                            uint32_t lo16 = wd[h] & 0xffffu, hi16 = wd[h] >> 16;
-                            if (x0 < pb || x0 >= run_end) lo16 = kDummy;
-                            if (x0 + 1 < pb || x0 + 1 >= run_end) hi16 = kDummy;
-                            wd[h] = lo16 | (hi16 << 16);
-                        }
+                    for (int i = 0; i < kSegStride / 4 / kThreads; ++i) r[i] = __ldcg(src + tid + i * kThreads);
+#pragma unroll
+                    for (int i = 0; i < kSegStride / 4 / kThreads; ++i)
+                        reinterpret_cast<float4*>(vseg)[tid + i * kThreads] = r[i];
+                    __syncthreads();
+                    cur_seg = seg;
+                }
+                double gp = 0.0;
+                int32_t tile = ta + warp;
+                uint4 cur[2], nxt[2];
+                int32_t fb = 0, fbn = 0;
+                if (tile < tb) {
+                    cur[0] = __ldcs(words4 + (int64_t)tile * (kTileW / 8) + 2 * lane);
+                    cur[1] = __ldcs(words4 + (int64_t)tile * (kTileW / 8) + 2 * lane + 1);
+                    fb = __ldg(a.fbase + tile);
+                }
+                for (; tile < tb; tile += kWarps) {
+                    const int32_t tn = tile + kWarps;
+                    if (lane == 0 && tn + kWarps < tb) {  // two tiles ahead: into L2 (no registers held)
+                        const uint16_t* pf = a.words + (int64_t)(tn + kWarps) * kTileW;
+                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pf), "r"(kTileW * 2) : "memory");
                     }
-                } else {
-#pragma unroll
-                    for (int h = 0; h < 8; ++h) wd[h] = (uint32_t)kDummy | ((uint32_t)kDummy << 16);
-                }
-                float x[kWpt];
-                uint32_t fl = 0;
-#pragma unroll
-                for (int h = 0; h < 8; ++h) {
-                    const uint32_t lo16 = wd[h] & 0xffffu, hi16 = wd[h] >> 16;
-                    x[2 * h] = vseg[lo16 & 0x7fffu];
-                    x[2 * h + 1] = vseg[hi16 & 0x7fffu];
-                    fl |= (lo16 >> 15) << (2 * h);
-                    fl |= (hi16 >> 15) << (2 * h + 1);
-                }
-                const int cnt = __popc(fl);
-                const int last = fl ? 31 - __clz(fl) : -1;
-                float tail = 0.0f;
-#pragma unroll
-                for (int i = 0; i < kWpt; ++i) {
-                    gp += (double)x[i];
-                    if (i > last) tail += x[i];
-                }
-                // block-wide segmented scan of (cnt, tail, cnt > 0): warp level
-                ScanEl el{cnt, tail, cnt > 0};
-#pragma unroll
-                for (int off = 1; off < 32; off <<= 1) {
-                    ScanEl o;
-                    o.c = __shfl_up_sync(0xffffffffu, el.c, off);
-                    o.v = __shfl_up_sync(0xffffffffu, el.v, off);
-                    o.f = __shfl_up_sync(0xffffffffu, el.f, off);
-                    if (lane >= off) el = scan_op(o, el);
-                }
-                ScanEl ex;  // warp-exclusive
-                ex.c = __shfl_up_sync(0xffffffffu, el.c, 1);
-                ex.v = __shfl_up_sync(0xffffffffu, el.v, 1);
-                ex.f = __shfl_up_sync(0xffffffffu, el.f, 1);
-                if (lane == 0) ex = ScanEl{0, 0.0f, 0};
-                if (lane == 31) sm.wtot[warp] = el;
-                __syncthreads();
-                if (warp == 0) {  // warp prefixes, the tile carry first
-                    ScanEl x0 = sm.wtot[lane];
-                    ScanEl inc = x0;
-#pragma unroll
-                    for (int off = 1; off < 32; off <<= 1) {
-                        ScanEl o;
-                        o.c = __shfl_up_sync(0xffffffffu, inc.c, off);
-                        o.v = __shfl_up_sync(0xffffffffu, inc.v, off);
-                        o.f = __shfl_up_sync(0xffffffffu, inc.f, off);
-                        if (lane >= off) inc = scan_op(o, inc);
+                    if (tn < tb) {  // the warp's next tile, in flight while this one is gathered
+                        nxt[0] = __ldcs(words4 + (int64_t)tn * (kTileW / 8) + 2 * lane);
+                        nxt[1] = __ldcs(words4 + (int64_t)tn * (kTileW / 8) + 2 * lane + 1);
+                        fbn = __ldg(a.fbase + tn);
                     }
-                    const ScanEl init{0, carry, 0};
-                    ScanEl exw;
-                    exw.c = __shfl_up_sync(0xffffffffu, inc.c, 1);
-                    exw.v = __shfl_up_sync(0xffffffffu, inc.v, 1);
-                    exw.f = __shfl_up_sync(0xffffffffu, inc.f, 1);
-                    sm.wpre[lane] = lane == 0 ? init : scan_op(init, exw);
-                    if (lane == 31) sm.total = scan_op(init, inc);
+                    gp += plan_tile(cur, vseg, fb, wstage, W.part, lane);
+                    cur[0] = nxt[0];
+                    cur[1] = nxt[1];
+                    fb = fbn;
                 }
-                __syncthreads();
-                const ScanEl pre = scan_op(sm.wpre[warp], ex);  // everything before this thread
-                const ScanEl tot = sm.total;
-                // walk: complete this thread's pieces, first one carrying the preceding threads' sums
-                float acc = pre.v;
-                int k = 0;
-                float* out = W.part + piece + pre.c;
-#pragma unroll
-                for (int i = 0; i < kWpt; ++i) {
-                    acc += x[i];
-                    if ((fl >> i) & 1u) {
-                        __stcg(out + k, acc);
-                        acc = 0.0f;
-                        ++k;
-                    }
-                }
-                carry = tot.v;
-                piece += tot.c;
+                const double ug = mapi::block_sum(gp, red);  // its barriers also publish s_next[q ^ 1]
+                if (tid == 0) W.slotY[u] = ug;
+                q ^= 1;
             }
-            pb = run_end;
         }
-        const double Gs = mapi::block_sum(gp, sm.red);
-        if (tid == 0) W.slotY[c] = Gs;
+        PLAN_STAMP(1);
         mapi::grid_barrier(W.bar, ++epoch * G);
+        PLAN_STAMP(2);
+        // every CTA is past iteration t - 1's counters: re-arm them for iteration t + 1
+        if (c == 0 && tid == 0) {
+            W.ctr[(t + 1) & 1] = 0u;
+            W.ctr[2 + ((t + 1) & 1)] = 0u;
+        }
 
         // ================= phase B: s = n S + sum e, w_{t+1} = (S + e) / s (fp64), delta, next v and S
-        const double S = slots_sum(W.slotS + (t & 1) * kMaxGrid, G, sm.red);
-        const double s = (double)n * S + slots_sum(W.slotY, G, sm.red);
+        const double S = slots_sum(W.slotS + (t & 1) * SB, nb, red) + slots_sum(W.slotSi + (t & 1) * kMaxGrid, G, red);
+        const double s = (double)n * S + slots_sum(W.slotY, a.nunits, red);
         if (!(s > 0.0) || isinf(s)) {  // uniform: every CTA sees the same s
             if (c == 0 && tid == 0) {
                 W.status[0] = (s == 0.0) ? MAPI_ERR_DEGENERATE : MAPI_ERR_NONFINITE;
@@ -602,30 +682,101 @@ __global__ void __launch_bounds__(kThreads, 1) k_rank_plan(RunArgs a) {
         const double Sp = first ? 0.0 : __ldcg(W.hist + (t & 1) * 2);
         const double sp_ = first ? 1.0 : __ldcg(W.hist + (t & 1) * 2 + 1);
         const double rs = 1.0 / s, rsp = 1.0 / sp_;
-        float* e_cur = (t & 1) ? W.e1 : W.e0;
-        const float* e_prev = (t & 1) ? W.e0 : W.e1;
-        double dp = 0.0, sn = 0.0;
-        for (int64_t j = j0 + tid; j < j1; j += kThreads) {
-            const int32_t r0 = __ldg(a.rsp + j), r1 = __ldg(a.rsp + j + 1);
-            float e = 0.0f;
-            for (int32_t r = r0; r < r1; ++r) e += __ldcg(W.part + __ldg(a.pos + r));
-            const double wn = qdiv(S + (double)e, s, rs);
-            const double wo = first ? (double)a.b0[j] : qdiv(Sp + (double)__ldcg(e_prev + j), sp_, rsp);
-            dp += fabs(wn - wo);
-            const float b = a.bg[j];
-            const int32_t qj = a.q[j];
-            if (qj >= 0) W.vc[qj] = node_v<OP>(wn, b, a.cap[j]);
-            sn += node_s<OP>(wn, b);
-            e_cur[j] = e;
+        double* e_cur = (t & 1) ? W.e1 : W.e0;
+        const double* e_prev = (t & 1) ? W.e0 : W.e1;
+        double* slotSn = W.slotS + ((t + 1) & 1) * SB;
+        cur_seg = -1;  // the batches overwrite the shared segment
+        {
+            unsigned* ctr = W.ctr + 2 + (t & 1);
+            if (tid == 0) s_next[0] = (int32_t)atomicAdd(ctr, 1u);
+            __syncthreads();
+            int q = 0;
+            for (int32_t b = s_next[0]; b < nb; b = s_next[q]) {
+                if (tid == 0) s_next[q ^ 1] = (int32_t)atomicAdd(ctr, 1u);
+                const int64_t bs = a.bstart[b], be = a.bstart[b + 1];
+                int32_t r0[kNodeK], r1[kNodeK];
+                double eo[kNodeK], e[kNodeK];
+                float bgv[kNodeK], cpv[kNodeK];
+#pragma unroll
+                for (int k = 0; k < kNodeK; ++k) {
+                    const int64_t p = bs + tid + (int64_t)k * kThreads;
+                    const bool in = p < be;
+                    r0[k] = in ? __ldg(a.rsp + p) : 0;
+                    r1[k] = in ? __ldg(a.rsp + p + 1) : 0;
+                    eo[k] = in ? (first ? (double)a.b0[a.perm[p]] : __ldcg(e_prev + p)) : 0.0;
+                    bgv[k] = in ? W.bgp[p] : 0.0f;
+                    cpv[k] = in ? W.capp[p] : 0.0f;
+                    e[k] = 0.0;
+                }
+                const int32_t R0 = __ldg(a.rsp + bs), R1 = __ldg(a.rsp + be);
+                __syncthreads();  // the previous batch's (or phase A's) shared reads are done
+                {
+                    constexpr int kU = 4;
+                    for (int32_t kb = R0 + tid; kb < R1; kb += kU * kThreads) {
+                        int32_t f[kU], rl[kU];
+#pragma unroll
+                        for (int u = 0; u < kU; ++u) {
+                            const int32_t k = kb + u * kThreads;
+                            f[u] = k < R1 ? __ldg(a.bfrag + k) : -1;
+                            rl[u] = k < R1 ? (int32_t)__ldg(a.brel + k) : 0;
+                        }
+                        float v[kU];
+#pragma unroll
+                        for (int u = 0; u < kU; ++u) v[u] = f[u] >= 0 ? __ldcg(W.part + f[u]) : 0.0f;
+#pragma unroll
+                        for (int u = 0; u < kU; ++u)
+                            if (f[u] >= 0) vseg[rl[u]] = v[u];
+                    }
+                }
+                __syncthreads();
+#pragma unroll
+                for (int k = 0; k < kNodeK; ++k)
+                    for (int32_t r = r0[k]; r < r1[k]; ++r) e[k] += (double)vseg[r - R0];
+                double dp = 0.0, sn = 0.0;
+#pragma unroll
+                for (int k = 0; k < kNodeK; ++k) {
+                    const int64_t p = bs + tid + (int64_t)k * kThreads;
+                    if (p >= be) continue;
+                    const double wn = qdiv(S + e[k], s, rs);
+                    const double wo = first ? eo[k] : qdiv(Sp + eo[k], sp_, rsp);
+                    dp += fabs(wn - wo);
+                    if (p < a.nsrc) W.vc[vc_index(p)] = node_v<OP>(wn, bgv[k], cpv[k]);
+                    sn += node_s<OP>(wn, bgv[k]);
+                    e_cur[p] = e[k];
+                }
+                block_sum2(dp, sn, red);  // its barriers also publish s_next[q ^ 1]
+                if (tid == 0) {
+                    W.slotD[b] = dp;
+                    slotSn[b] = sn;
+                }
+                q ^= 1;
+            }
         }
-        const double D = mapi::block_sum(dp, sm.red);
-        const double Sn = mapi::block_sum(sn, sm.red);
-        if (tid == 0) {
-            W.slotD[c] = D;
-            W.slotS[((t + 1) & 1) * kMaxGrid + c] = Sn;
+        // isolated nodes: y = S for all; per node on the first iteration (w_0 = b0 differs) or when their bg
+        // differ, else one class term
+        {
+            double dp = 0.0, sn = 0.0;
+            const double wn = qdiv(S, s, rs);
+            if (first || !iso_class) {
+                const double wc = first ? 0.0 : qdiv(Sp, sp_, rsp);
+                for (int64_t p = i0 + tid; p < i1; p += kThreads) {
+                    const double wo = first ? (double)a.b0[a.perm[p]] : wc;
+                    dp += fabs(wn - wo);
+                    sn += node_s<OP>(wn, W.bgp[p]);
+                }
+            } else if (c == 0 && tid == 0 && niso > 0) {
+                dp += (double)niso * fabs(wn - qdiv(Sp, sp_, rsp));
+                sn += (double)niso * node_s<OP>(wn, bg_iso);
+            }
+            block_sum2(dp, sn, red);
+            if (tid == 0) {
+                W.slotDi[c] = dp;
+                W.slotSi[((t + 1) & 1) * kMaxGrid + c] = sn;
+            }
         }
+        PLAN_STAMP(3);
         mapi::grid_barrier(W.bar, ++epoch * G);
-        const double d = slots_sum(W.slotD, G, sm.red);
+        const double d = slots_sum(W.slotD, nb, red) + slots_sum(W.slotDi, G, red);
         if (c == 0 && tid == 0) {
             W.hist[((t + 1) & 1) * 2] = S;
             W.hist[((t + 1) & 1) * 2 + 1] = s;
@@ -636,10 +787,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_rank_plan(RunArgs a) {
     }
 }
 
-// Outputs: w = (S + e)/s of the last iteration (b0 if none) in fp64 as the loop formed it; w_out = fp32(w),
-// per-CTA sums of w^2, then the optional l2 copy.
+// Outputs: w = (S + e)/s of the last iteration (b0 if none) in fp64 as the loop formed it (e = 0 for the
+// isolated nodes); w_out = fp32(w) in node-id order, per-CTA sums of w^2, then the optional l2 copy.
 struct Last {
-    const float* e;
+    const double* e;
     double S, s;
     bool none;
 };
@@ -653,21 +804,24 @@ __device__ __forceinline__ Last last_iter(const RunWs& W) {
     r.s = r.none ? 1.0 : W.hist[((last + 1) & 1) * 2 + 1];
     return r;
 }
-__global__ void __launch_bounds__(256) k_plan_output(int64_t n, RunWs W, const float* __restrict__ b0,
-                                                     float* __restrict__ w_out) {
+__global__ void __launch_bounds__(256) k_plan_output(int64_t n, int64_t nlive, RunWs W, const int32_t* __restrict__ perm,
+                                                     const float* __restrict__ b0, float* __restrict__ w_out) {
     __shared__ double red[33];
     const Last L = last_iter(W);
     const double rls = 1.0 / L.s;
     double part = 0.0;
-    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
-        const double x = L.none ? (double)b0[j] : qdiv(L.S + (double)L.e[j], L.s, rls);
-        w_out[j] = (float)x;
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t id = perm[p];
+        const double x = L.none ? (double)b0[id] : qdiv(L.S + (p < nlive ? L.e[p] : 0.0), L.s, rls);
+        w_out[id] = (float)x;
         part = fma(x, x, part);
     }
     const double qs = mapi::block_sum(part, red);
     if (threadIdx.x == 0) W.slotQ[blockIdx.x] = qs;
 }
-__global__ void __launch_bounds__(256) k_plan_output_l2(int64_t n, RunWs W, const float* __restrict__ b0, int nq,
+__global__ void __launch_bounds__(256) k_plan_output_l2(int64_t n, int64_t nlive, RunWs W,
+                                                        const int32_t* __restrict__ perm,
+                                                        const float* __restrict__ b0, int nq,
                                                         float* __restrict__ w_l2) {
     __shared__ double red[33];
     const Last L = last_iter(W);
@@ -680,9 +834,10 @@ __global__ void __launch_bounds__(256) k_plan_output_l2(int64_t n, RunWs W, cons
     }
     __syncthreads();
     const double l2 = sqrt(red[32]);
-    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
-        const double x = L.none ? (double)b0[j] : qdiv(L.S + (double)L.e[j], L.s, rls);
-        w_l2[j] = l2 > 0.0 ? (float)(x / l2) : 0.0f;
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t id = perm[p];
+        const double x = L.none ? (double)b0[id] : qdiv(L.S + (p < nlive ? L.e[p] : 0.0), L.s, rls);
+        w_l2[id] = l2 > 0.0 ? (float)(x / l2) : 0.0f;
     }
 }
 
@@ -699,7 +854,7 @@ mapi_status mapi_csr_plan(int64_t n, int64_t nnz, const int32_t* row_ptr, const 
     if (n < 1) return fail(MAPI_ERR_SHAPE, "n (%lld) must be >= 1", (long long)n);
     if (n >= (int64_t)INT32_MAX - kSegStride)
         return fail(MAPI_ERR_SHAPE, "n (%lld) out of the int32 index range", (long long)n);
-    if (nnz < 0 || nnz >= (int64_t)INT32_MAX - kSegAlign * (max_segments(n) + 2))
+    if (nnz < 0 || nwords_bound(nnz, max_segments(n)) >= (int64_t)INT32_MAX)
         return fail(MAPI_ERR_SHAPE, "nnz (%lld) out of the int32 index range", (long long)nnz);
     if (!row_ptr || !plan || !info || (nnz > 0 && !col_idx))
         return fail(MAPI_ERR_NULL, "row_ptr / col_idx / plan / info is NULL");
@@ -713,100 +868,162 @@ mapi_status mapi_csr_plan(int64_t n, int64_t nnz, const int32_t* row_ptr, const 
     if (st != MAPI_OK) return st;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     int occ = 0;
-    MAPI_CUDA(cudaFuncSetAttribute(k_rank_plan<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * kSegStride));
-    MAPI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_rank_plan<0>, kThreads, 4 * kSegStride));
+    MAPI_CUDA(cudaFuncSetAttribute(k_rank_plan<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPlanSmem));
+    MAPI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_rank_plan<0>, kThreads, kPlanSmem));
     if (occ < 1) return fail(MAPI_ERR_CUDA, "planned ranking kernel does not fit on an SM");
     const int grid = std::min(d.sms, kMaxGrid);
     BuildWs B = carve_build(ws, n, nnz);
-    const unsigned g1 = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 8 * (int64_t)d.sms));
-    const unsigned ge = (unsigned)std::max<int64_t>(1, std::min<int64_t>((nnz + 255) / 256, 16 * (int64_t)d.sms));
+    auto blocks = [&](int64_t items, int per_sm) {
+        return (unsigned)std::max<int64_t>(1, std::min<int64_t>((items + 255) / 256, (int64_t)per_sm * d.sms));
+    };
+    const unsigned gn = blocks(n, 8), ge = blocks(nnz, 16);
+    const int64_t nseg_max = max_segments(n), ntiles_max = nwords_bound(nnz, nseg_max) / kTileW;
     MAPI_CUDA(cudaMemsetAsync(B.counter, 0, 256, s));
     MAPI_CUDA(cudaMemsetAsync(B.outdeg, 0, 4 * (size_t)n, s));
     MAPI_CUDA(cudaMemsetAsync(B.rcnt, 0, 4 * (size_t)(n + 1), s));
+    MAPI_CUDA(cudaMemsetAsync(B.segcnt, 0, 4 * (size_t)(nseg_max + 1), s));
+    MAPI_CUDA(cudaMemsetAsync(B.segstart, 0, 4 * (size_t)(nseg_max + 1), s));
+    MAPI_CUDA(cudaMemsetAsync(B.tcnt, 0, 4 * (size_t)(ntiles_max + 1), s));
     if (nnz > 0) {
         kp_outdeg<<<ge, 256, 0, s>>>(nnz, col_idx, B.outdeg);
         MAPI_LAUNCHED();
     }
-    kp_src_keys<<<g1, 256, 0, s>>>(n, B.outdeg, B.skey, B.sval, B.counter);
+    kp_src_keys<<<gn, 256, 0, s>>>(n, B.outdeg, row_ptr, B.skey, B.sval, B.counter);
     MAPI_LAUNCHED();
+    // plan order into the plan's first array (its offset does not depend on the later sizes)
+    int32_t* perm = plan_view(plan, n, 1, 0, 0, 0).perm;
     size_t tb = B.cub_bytes;
-    MAPI_CUDA(cub::DeviceRadixSort::SortPairs(B.cub, tb, B.skey, B.skey2, B.sval, B.sval2, (int)n, 0, 32, s));
-    uint32_t nsrc_h = 0;
-    MAPI_CUDA(cudaMemcpyAsync(&nsrc_h, B.counter, 4, cudaMemcpyDeviceToHost, s));
+    MAPI_CUDA(cub::DeviceRadixSort::SortPairs(B.cub, tb, B.skey, B.skey2, B.sval, perm, (int)n, 0, 32, s));
+    kp_inv<<<gn, 256, 0, s>>>(n, perm, B.inv);
+    MAPI_LAUNCHED();
+    uint32_t cnt_h[2] = {0, 0};
+    MAPI_CUDA(cudaMemcpyAsync(cnt_h, B.counter, 8, cudaMemcpyDeviceToHost, s));
     MAPI_CUDA(cudaStreamSynchronize(s));
-    const int64_t nsrc = nsrc_h;
+    const int64_t nsrc = cnt_h[0], nlive = n - (int64_t)cnt_h[1];
     const int32_t nseg = (int32_t)std::max<int64_t>(1, (nsrc + kSegSrc - 1) / kSegSrc);
-    PlanView P = plan_view(plan, n, nseg, grid, std::max<int64_t>(nnz, 1));  // pos sized by the bound for now
-    MAPI_CUDA(cudaMemsetAsync(P.q, 0xff, 4 * (size_t)n, s));
-    if (nsrc > 0) {
-        kp_q<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((nsrc + 255) / 256, 8 * (int64_t)d.sms)), 256, 0, s>>>(
-            nsrc, B.sval2, P.q);
-        MAPI_LAUNCHED();
-    }
-    int64_t npieces = 0, nwords = 0;
     if (nnz > 0) {
-        kp_edges<<<ge, 256, 0, s>>>(n, nnz, row_ptr, col_idx, P.q, B.erow, B.ekey, B.eval);
+        kp_edges<<<ge, 256, 0, s>>>(n, nnz, row_ptr, col_idx, B.inv, B.ekey, B.eoff);
         MAPI_LAUNCHED();
-        int bits = 1;
+        int bits = 0;
         while ((1ll << bits) < (int64_t)nseg) ++bits;
         tb = B.cub_bytes;
-        MAPI_CUDA(cub::DeviceRadixSort::SortPairs(B.cub, tb, B.ekey, B.ekey2, B.eval, B.eval2, (int)nnz, 0, bits, s));
-        kp_sorted<<<ge, 256, 0, s>>>(nnz, B.ekey2, B.eval2, B.erow, col_idx, P.q, B.srow, B.soff, B.runb, B.segstart);
+        MAPI_CUDA(cub::DeviceRadixSort::SortPairs(B.cub, tb, B.ekey, B.ekey2, B.eoff, B.eoff2, (int)nnz, 0, 32 + bits,
+                                                  s));
+        kp_segcount<<<ge, 256, 0, s>>>(nnz, B.ekey2, B.segcnt, B.segstart);
         MAPI_LAUNCHED();
-        tb = B.cub_bytes;
-        MAPI_CUDA(cub::DeviceScan::InclusiveScan(B.cub, tb, B.runb, B.runb2, MaxOp{}, (int)nnz, s));
-        kp_piece_end<<<ge, 256, 0, s>>>(nnz, B.runb2, B.runb, B.pe);
-        MAPI_LAUNCHED();
-        tb = B.cub_bytes;
-        MAPI_CUDA(cub::DeviceScan::ExclusiveSum(B.cub, tb, B.pe, B.pid, (int)nnz, s));
-        uint32_t last[2] = {0, 0};
-        MAPI_CUDA(cudaMemcpyAsync(&last[0], B.pid + nnz - 1, 4, cudaMemcpyDeviceToHost, s));
-        MAPI_CUDA(cudaMemcpyAsync(&last[1], B.pe + nnz - 1, 4, cudaMemcpyDeviceToHost, s));
-        MAPI_CUDA(cudaStreamSynchronize(s));
-        npieces = (int64_t)last[0] + last[1];
-        kp_pieces<<<ge, 256, 0, s>>>(nnz, B.pe, B.pid, B.srow, B.prow, B.pend, B.piota, B.rcnt);
-        MAPI_LAUNCHED();
-        kp_segb<<<1, 32, 0, s>>>(nseg, nnz, B.segstart, P.segb);
-        MAPI_LAUNCHED();
-        int32_t nw = 0;
-        MAPI_CUDA(cudaMemcpyAsync(&nw, P.segb + nseg, 4, cudaMemcpyDeviceToHost, s));
-        MAPI_CUDA(cudaStreamSynchronize(s));
-        nwords = nw;
-    } else {
-        MAPI_CUDA(cudaMemsetAsync(P.segb, 0, 4 * (size_t)(nseg + 1), s));
     }
-    // final layout with the exact piece count (pos shrinks; words follow it)
-    P = plan_view(plan, n, nseg, grid, npieces);
-    if (nwords > 0) {
-        kp_fill_words<<<(unsigned)std::min<int64_t>((nwords + 255) / 256, 16 * (int64_t)d.sms), 256, 0, s>>>(nwords, P.words);
+    // tile-aligned segment starts: they size the word array
+    kp_segb<<<1, 32, 0, s>>>(nseg, B.segcnt, B.segb);
+    MAPI_LAUNCHED();
+    int64_t nfrag = 0, nwords = 0;
+    std::vector<int32_t> segb_h(nseg + 1);
+    MAPI_CUDA(cudaMemcpyAsync(segb_h.data(), B.segb, 4 * (size_t)(nseg + 1), cudaMemcpyDeviceToHost, s));
+    MAPI_CUDA(cudaStreamSynchronize(s));
+    nwords = segb_h[nseg];
+    const int64_t ntiles = nwords / kTileW;
+    // phase A work units in scheduling order: segments from the last to the first, kUnitBig tiles per unit
+    // until only 1/8 of all tiles remain, then kUnitSmall (one tile per warp): the dynamically scheduled
+    // tail is fine-grained, and consecutive units mostly share a segment
+    std::vector<int32_t> units_h;
+    {
+        int64_t done = 0;
+        for (int32_t sg = nseg - 1; sg >= 0; --sg) {
+            int64_t ta = segb_h[sg] / kTileW;
+            const int64_t te = segb_h[sg + 1] / kTileW;
+            while (ta < te) {
+                const int64_t size = std::min<int64_t>(te - ta, (ntiles - done) > ntiles / 8 ? kUnitBig : kUnitSmall);
+                units_h.push_back((int32_t)ta);
+                units_h.push_back((int32_t)(ta + size));
+                units_h.push_back(sg);
+                ta += size;
+                done += size;
+            }
+        }
+    }
+    const int64_t nunits = (int64_t)units_h.size() / 3;
+    if (nunits > nunits_bound(ntiles, nseg)) return fail(MAPI_ERR_CUDA, "internal: %lld units", (long long)nunits);
+    if (nnz > 0) {
+        kp_fstart<<<ge, 256, 0, s>>>(nnz, B.ekey2, B.segstart, B.segb, B.fstart);
         MAPI_LAUNCHED();
-        kp_words<<<ge, 256, 0, s>>>(nnz, B.ekey2, B.soff, B.pe, B.segstart, P.segb, P.words);
+        tb = B.cub_bytes;
+        MAPI_CUDA(cub::DeviceScan::ExclusiveSum(B.cub, tb, B.fstart, B.fid, (int)nnz, s));
+        uint32_t last[2] = {0, 0};
+        MAPI_CUDA(cudaMemcpyAsync(&last[0], B.fid + nnz - 1, 4, cudaMemcpyDeviceToHost, s));
+        MAPI_CUDA(cudaMemcpyAsync(&last[1], B.fstart + nnz - 1, 4, cudaMemcpyDeviceToHost, s));
+        MAPI_CUDA(cudaStreamSynchronize(s));
+        nfrag = (int64_t)last[0] + last[1];
+    }
+    PlanView P = plan_view(plan, n, nseg, nunits, nwords, nfrag);
+    MAPI_CUDA(cudaMemcpyAsync(P.segb, B.segb, 4 * (size_t)(nseg + 1), cudaMemcpyDeviceToDevice, s));
+    if (nunits > 0)
+        MAPI_CUDA(cudaMemcpyAsync(P.units, units_h.data(), 4 * units_h.size(), cudaMemcpyHostToDevice, s));
+    if (nnz > 0) {
+        kp_fill_words<<<blocks(nwords, 16), 256, 0, s>>>(nwords, P.words);
         MAPI_LAUNCHED();
-        // slots: pieces stably sorted by row (the (segment, piece) order within a row is kept)
+        kp_frag<<<ge, 256, 0, s>>>(nnz, B.ekey2, B.eoff2, B.fstart, B.fid, B.segstart, P.segb, B.frow, B.fidx, B.rcnt,
+                                   B.tcnt, P.words);
+        MAPI_LAUNCHED();
+        // row-sorted slots (stable: the (segment, position) order within a row is kept) and their inverse
         int rbits = 1;
         while ((1ll << rbits) < n) ++rbits;
         tb = B.cub_bytes;
-        MAPI_CUDA(cub::DeviceRadixSort::SortPairs(B.cub, tb, B.prow, B.prow2, B.piota, P.pos, (int)npieces, 0, rbits, s));
+        MAPI_CUDA(cub::DeviceRadixSort::SortPairs(B.cub, tb, B.frow, B.frow2, B.fidx, B.pos, (int)nfrag, 0, rbits, s));
+        kp_fslot<<<ge, 256, 0, s>>>(nfrag, B.pos, B.fslot);
+        MAPI_LAUNCHED();
     }
     tb = B.cub_bytes;
+    MAPI_CUDA(cub::DeviceScan::ExclusiveSum(B.cub, tb, B.tcnt, P.fbase, (int)(ntiles + 1), s));
+    tb = B.cub_bytes;
     MAPI_CUDA(cub::DeviceScan::ExclusiveSum(B.cub, tb, B.rcnt, P.rsp, (int)(n + 1), s));
-    kp_cta<<<(unsigned)((grid + 1 + 127) / 128), 128, 0, s>>>(grid, nnz, npieces, nwords, B.pend, B.ekey2, B.segstart,
-                                                               P.segb, P.ctab, P.ctap);
-    MAPI_LAUNCHED();
+    // node-pass batches over the live rows, and the fragments in (batch, fragment) order
+    int64_t nbatch = 0;
+    if (nlive > 0) {
+        kp_bflag<<<blocks(nlive, 8), 256, 0, s>>>(nlive, P.rsp, B.bflag);
+        MAPI_LAUNCHED();
+        tb = B.cub_bytes;
+        MAPI_CUDA(cub::DeviceScan::InclusiveSum(B.cub, tb, B.bflag, B.bincl, (int)nlive, s));
+        int32_t nb = 0;
+        MAPI_CUDA(cudaMemcpyAsync(&nb, B.bincl + nlive - 1, 4, cudaMemcpyDeviceToHost, s));
+        MAPI_CUDA(cudaStreamSynchronize(s));
+        nbatch = nb;
+        if (nbatch > nbatch_bound(n, nnz)) return fail(MAPI_ERR_CUDA, "internal: %lld batches", (long long)nbatch);
+        kp_bstart<<<blocks(nlive, 8), 256, 0, s>>>(nlive, B.bflag, B.bincl, P.bstart);
+        MAPI_LAUNCHED();
+    } else {
+        MAPI_CUDA(cudaMemsetAsync(P.bstart, 0, 4, s));
+    }
+    if (nfrag > 0) {
+        kp_fbat<<<ge, 256, 0, s>>>(nfrag, B.frow, B.bincl, B.fbat, B.fidx);
+        MAPI_LAUNCHED();
+        int bbits = 1;
+        while ((1ll << bbits) < nbatch + 1) ++bbits;
+        tb = B.cub_bytes;
+        MAPI_CUDA(cub::DeviceRadixSort::SortPairs(B.cub, tb, B.fbat, B.fbat2, B.fidx, P.bfrag, (int)nfrag, 0, bbits, s));
+        kp_brel<<<ge, 256, 0, s>>>(nfrag, P.bfrag, B.fbat, B.fslot, P.bstart, P.rsp, P.brel, B.counter + 2);
+        MAPI_LAUNCHED();
+    }
+    uint32_t maxslots = 0;
+    MAPI_CUDA(cudaMemcpyAsync(&maxslots, B.counter + 2, 4, cudaMemcpyDeviceToHost, s));
     struct {
         uint64_t magic;
-        int64_t n, nnz, nsrc, npieces, nwords;
+        int64_t n, nnz, nsrc, nfrag, nwords, nlive, nbatch, nunits;
         int32_t nseg, grid;
-    } hdr = {kMagic, n, nnz, nsrc, npieces, nwords, nseg, grid};
+    } hdr = {kMagic, n, nnz, nsrc, nfrag, nwords, nlive, nbatch, nunits, nseg, grid};
     MAPI_CUDA(cudaMemcpyAsync(plan, &hdr, sizeof(hdr), cudaMemcpyHostToDevice, s));
     MAPI_CUDA(cudaStreamSynchronize(s));
+    if (maxslots > (uint32_t)kSmemF)
+        return fail(MAPI_ERR_SHAPE, "a node batch gathers %u fragment sums (> %d): a row with this many fragments "
+                    "needs the plan-free path (mapi_rank_csr)", maxslots, kSmemF);
     info->n = n;
     info->nnz = nnz;
     info->nsrc = nsrc;
-    info->npieces = npieces;
+    info->npieces = nfrag;
     info->nwords = nwords;
     info->nseg = nseg;
     info->grid = grid;
+    info->nlive = nlive;
+    info->nbatch = nbatch;
+    info->nunits = nunits;
     return MAPI_OK;
 }
 
@@ -819,13 +1036,17 @@ mapi_status mapi_rank_csr_plan(int32_t op, const void* plan, const mapi_csr_plan
     if (!plan || !info || !cap || !bg || !b0 || !w_out) return fail(MAPI_ERR_NULL, "a required pointer is NULL");
     const int64_t n = info->n;
     if (n < 1 || info->nnz < 0 || info->grid < 1 || info->grid > kMaxGrid || info->nseg < 1 ||
-        info->npieces < 0 || info->npieces > std::max<int64_t>(info->nnz, 0) || info->nwords < 0)
+        info->npieces < 0 || info->npieces > std::max<int64_t>(info->nnz, 0) || info->nwords < 0 ||
+        info->nwords % kTileW != 0 || info->nsrc < 0 || info->nsrc > n || info->nlive < info->nsrc ||
+        info->nlive > n || info->nbatch < 0 || info->nbatch > nbatch_bound(n, info->nnz) || info->nunits < 0 ||
+        info->nunits > nunits_bound(info->nwords / kTileW, info->nseg) || info->nbatch > INT32_MAX ||
+        (info->nlive > 0) != (info->nbatch > 0))
         return fail(MAPI_ERR_SHAPE, "plan info is inconsistent (n %lld, nnz %lld, grid %d, nseg %d)", (long long)n,
                     (long long)info->nnz, info->grid, info->nseg);
     if (max_iters < 1) return fail(MAPI_ERR_BAD_PARAM, "max_iters (%d) must be >= 1", max_iters);
     if (!(tol >= 0.0f)) return fail(MAPI_ERR_BAD_PARAM, "tol must be >= 0");
     if (!ws) return fail(MAPI_ERR_WORKSPACE, "workspace is NULL");
-    const size_t need = run_ws_exact(n, info->nseg, info->npieces);
+    const size_t need = run_ws_exact(n, info->nseg, info->npieces, info->nunits, info->nbatch);
     if (ws_bytes < need) return fail(MAPI_ERR_WORKSPACE, "ws_bytes (%zu) < required (%zu)", ws_bytes, need);
     Device d;
     mapi_status st = device_info(d);
@@ -833,38 +1054,81 @@ mapi_status mapi_rank_csr_plan(int32_t op, const void* plan, const mapi_csr_plan
     if (info->grid > d.sms)
         return fail(MAPI_ERR_SHAPE, "plan built for %d CTAs; this device has %d SMs", info->grid, d.sms);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    const PlanView P = plan_view(const_cast<void*>(plan), n, info->nseg, info->grid, info->npieces);
+    const PlanView P = plan_view(const_cast<void*>(plan), n, info->nseg, info->nunits, info->nwords, info->npieces);
     RunArgs a;
     a.n = n;
+    a.nlive = info->nlive;
+    a.nsrc = info->nsrc;
     a.nseg = info->nseg;
+    a.nunits = (int32_t)info->nunits;
+    a.nbatch = (int32_t)info->nbatch;
     a.iters = max_iters;
     a.tol = tol;
-    a.q = P.q; a.segb = P.segb; a.ctab = P.ctab; a.ctap = P.ctap; a.rsp = P.rsp; a.pos = P.pos; a.words = P.words;
+    a.perm = P.perm; a.segb = P.segb; a.units = P.units; a.fbase = P.fbase; a.rsp = P.rsp;
+    a.bstart = P.bstart; a.bfrag = P.bfrag; a.brel = P.brel; a.words = P.words;
     a.cap = cap; a.bg = bg; a.b0 = b0; a.deltas = deltas;
-    a.w = carve_run(ws, n, info->nseg, info->npieces);
+    // investigation: MAPI_PLAN_TRACE=1 prints CTA 0's per-phase times (us) of iterations 3..min(iters, 64);
+    // MAPI_PLAN_TRACE_FILE=<path> also writes every CTA's phase times
+    static const bool trace_on = getenv("MAPI_PLAN_TRACE") && atoi(getenv("MAPI_PLAN_TRACE")) > 0;
+    unsigned long long* trace_d = nullptr;
+    if (trace_on) {
+        MAPI_CUDA(cudaMalloc(&trace_d, 8 * (4 * 64 + 4 * kMaxGrid)));
+        MAPI_CUDA(cudaMemsetAsync(trace_d, 0, 8 * (4 * 64 + 4 * kMaxGrid), s));
+    }
+    a.trace = trace_d;
+    a.w = carve_run(ws, n, info->nseg, info->npieces, info->nunits, info->nbatch);
     MAPI_CUDA(cudaMemsetAsync(ws, 0, 256, s));
     // the compact vector's zero slots (offset 32767 of each segment) and unused tail stay 0
     MAPI_CUDA(cudaMemsetAsync(a.w.vc, 0, 4 * (size_t)kSegStride * (size_t)info->nseg, s));
     auto kern = op == MAPI_OP_DOT ? k_rank_plan<2> : k_rank_plan<0>;
-    MAPI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * kSegStride));
+    MAPI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPlanSmem));
     Timer timer(s);
     void* args[] = {&a};
     timer.start();
-    MAPI_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3(info->grid), dim3(kThreads), args,
-                                          (size_t)4 * kSegStride, s));
+    MAPI_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3(info->grid), dim3(kThreads), args, kPlanSmem, s));
     timer.stop();
     g_launches.fetch_add(1, std::memory_order_relaxed);
     const int gout = (int)std::min<int64_t>((n + 255) / 256, std::min(4 * d.sms, kMaxGrid));
-    k_plan_output<<<gout, 256, 0, s>>>(n, a.w, b0, w_out);
+    k_plan_output<<<gout, 256, 0, s>>>(n, info->nlive, a.w, P.perm, b0, w_out);
     MAPI_LAUNCHED();
     if (w_l2_out) {
-        k_plan_output_l2<<<gout, 256, 0, s>>>(n, a.w, b0, gout, w_l2_out);
+        k_plan_output_l2<<<gout, 256, 0, s>>>(n, info->nlive, a.w, P.perm, b0, gout, w_l2_out);
         MAPI_LAUNCHED();
     }
     int32_t h[2] = {0, 0};
     MAPI_CUDA(cudaMemcpyAsync(h, a.w.status, sizeof(h), cudaMemcpyDeviceToHost, s));
     MAPI_CUDA(cudaStreamSynchronize(s));
     timer.harvest();
+    if (trace_d) {
+        std::vector<unsigned long long> tr(4 * 64 + 4 * kMaxGrid);
+        cudaMemcpy(tr.data(), trace_d, 8 * tr.size(), cudaMemcpyDeviceToHost);
+        cudaFree(trace_d);
+        const int it = std::min(h[1], 64) - 3;
+        const char* path = getenv("MAPI_PLAN_TRACE_FILE");
+        if (path && it > 0) {  // per-CTA phase times (dynamic scheduling: the barrier waits show the balance)
+            FILE* f = fopen(path, "w");
+            if (f) {
+                fprintf(f, "cta,phaseA_us,bar1_us,phaseB_us,bar2_us\n");
+                for (int cc = 0; cc < info->grid; ++cc) {
+                    fprintf(f, "%d", cc);
+                    for (int k = 0; k < 4; ++k) fprintf(f, ",%.2f", tr[256 + cc * 4 + k] / 1e3 / it);
+                    fprintf(f, "\n");
+                }
+                fclose(f);
+            }
+        }
+        if (it > 0) {
+            double ph[4] = {0, 0, 0, 0};
+            for (int t = 3; t < 3 + it; ++t) {
+                ph[0] += (tr[t * 4 + 1] - tr[t * 4 + 0]) / 1e3;
+                ph[1] += (tr[t * 4 + 2] - tr[t * 4 + 1]) / 1e3;
+                ph[2] += (tr[t * 4 + 3] - tr[t * 4 + 2]) / 1e3;
+                ph[3] += (t + 1 < 64 ? (tr[(t + 1) * 4 + 0] - tr[t * 4 + 3]) / 1e3 : 0.0);
+            }
+            fprintf(stderr, "[mapi plan trace] us/iteration (CTA 0, %d iterations): phaseA %.1f bar1 %.1f phaseB %.1f bar2 %.1f\n",
+                    it, ph[0] / it, ph[1] / it, ph[2] / it, ph[3] / it);
+        }
+    }
     if (iters_done) *iters_done = h[1];
     if (h[0] == MAPI_ERR_NEGATIVE) return fail(MAPI_ERR_NEGATIVE, "b0 has a negative entry");
     if (h[0] == MAPI_ERR_DEGENERATE) return fail(MAPI_ERR_DEGENERATE, "||G (+) w_t||_1 == 0 at iteration %d", h[1]);
