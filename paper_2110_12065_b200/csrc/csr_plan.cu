@@ -77,12 +77,14 @@ inline int64_t nunits_bound(int64_t ntiles, int64_t nseg) { return ntiles / kUni
 
 // ------------------------------------------------------------------------------- plan layout
 // [hdr 256][perm n i32: plan position -> node id][segb nseg+1 i32: padded word start of each segment]
-// [units 3 nunits i32: phase A work units (first tile, end tile, segment) in scheduling order][fbase ntiles+1
-// i32: first fragment of each tile][rsp n+1 i32: plan position -> its first slot][words nwords u16][bfrag nfrag i32: fragments in
-// (batch, fragment) order][brel nfrag u16: their slot within the batch][bstart nbatch+1 i32: batch rows]
+// [units 3 nunits i32: phase A work units (first tile, end tile, segment) in scheduling order]
+// [fbase ntiles+1 i32: first fragment of each tile][rsp n+1 i32: plan position -> its first slot]
+// [words nwords u16: source offsets][wflags nwords/16 u16: end-of-fragment flags of each lane chunk of 16 words]
+// [bfrag nfrag i32: fragments in (batch, fragment) order][brel nfrag u16: their slot within the batch]
+// [bstart nbatch+1 i32: batch rows]
 struct PlanView {
     int32_t *perm, *segb, *units, *fbase, *rsp;
-    uint16_t* words;
+    uint16_t *words, *wflags;
     int32_t* bfrag;
     uint16_t* brel;
     int32_t* bstart;
@@ -97,6 +99,7 @@ inline PlanView plan_view(void* plan, int64_t n, int64_t nseg, int64_t nunits, i
     v.fbase = reinterpret_cast<int32_t*>(p); p += al256(4 * (size_t)(ntiles + 1));
     v.rsp = reinterpret_cast<int32_t*>(p); p += al256(4 * (size_t)(n + 1));
     v.words = reinterpret_cast<uint16_t*>(p); p += al256(2 * (size_t)std::max<int64_t>(nwords, 1));
+    v.wflags = reinterpret_cast<uint16_t*>(p); p += al256(2 * (size_t)std::max<int64_t>(nwords / kLaneW, 1));
     v.bfrag = reinterpret_cast<int32_t*>(p); p += al256(4 * (size_t)std::max<int64_t>(nfrag, 1));
     v.brel = reinterpret_cast<uint16_t*>(p); p += al256(2 * (size_t)std::max<int64_t>(nfrag, 1));
     v.bstart = reinterpret_cast<int32_t*>(p);
@@ -106,6 +109,7 @@ inline size_t plan_bytes_exact(int64_t n, int64_t nseg, int64_t nunits, int64_t 
     const int64_t ntiles = nwords / kTileW;
     return 256 + al256(4 * (size_t)n) + al256(4 * (size_t)(nseg + 1)) + al256(12 * (size_t)std::max<int64_t>(nunits, 1)) +
            al256(4 * (size_t)(ntiles + 1)) + al256(4 * (size_t)(n + 1)) + al256(2 * (size_t)std::max<int64_t>(nwords, 1)) +
+           al256(2 * (size_t)std::max<int64_t>(nwords / kLaneW, 1)) +
            al256(4 * (size_t)std::max<int64_t>(nfrag, 1)) + al256(2 * (size_t)std::max<int64_t>(nfrag, 1)) +
            al256(4 * (size_t)(nbatch + 1));
 }
@@ -305,6 +309,18 @@ __global__ void kp_frag(int64_t nnz, const uint64_t* __restrict__ ek, const uint
 __global__ void kp_fill_words(int64_t nwords, uint16_t* __restrict__ words) {
     GRID_STRIDE(k, nwords) words[k] = kDummy;
 }
+// per lane chunk of 16 words: the end flags as a 16-bit mask; the words keep only the source offset
+__global__ void kp_wflags(int64_t nchunks, uint16_t* __restrict__ words, uint16_t* __restrict__ wflags) {
+    GRID_STRIDE(ch, nchunks) {
+        uint32_t m = 0;
+        for (int i = 0; i < kLaneW; ++i) {
+            const uint16_t w = words[ch * kLaneW + i];
+            m |= (uint32_t)(w >> 15) << i;
+            words[ch * kLaneW + i] = (uint16_t)(w & 0x7fffu);
+        }
+        wflags[ch] = (uint16_t)m;
+    }
+}
 
 __global__ void kp_fslot(int64_t nfrag, const int32_t* __restrict__ pos, int32_t* __restrict__ fslot) {
     GRID_STRIDE(r, nfrag) fslot[pos[r]] = (int32_t)r;
@@ -405,7 +421,7 @@ struct RunArgs {
     int32_t nseg, iters, nunits, nbatch;
     float tol;
     const int32_t *perm, *segb, *units, *fbase, *rsp, *bstart, *bfrag;
-    const uint16_t *brel, *words;
+    const uint16_t *brel, *words, *wflags;
     const float *cap, *bg, *b0;
     float* deltas;
     unsigned long long* trace;  // optional: phase stamps (globaltimer), see PLAN_STAMP
@@ -468,67 +484,64 @@ __device__ __forceinline__ void block_sum2(double& a, double& b, double* red) {
     b = red[72];
 }
 
-// one 512-word tile: 16 words per lane (lane l: words 16 l .. 16 l + 15), gathers from the shared segment,
-// fragments closed by a warp-level segmented scan, staged in the warp's shared buffer in fragment order and
-// written to part[fb ..) with coalesced stores.  Returns the fp64 sum of the tile's fragment sums.
-__device__ __forceinline__ double plan_tile(const uint4 (&wd)[2], const float* __restrict__ vseg, int32_t fb,
+// one 512-word tile: 16 words per lane (lane l: words 16 l .. 16 l + 15, end flags fl), gathers from the shared
+// segment (shared address sb).  The lane's fragments are closed in word order into the warp's stage at their
+// fragment positions (an exclusive warp scan of the flag counts gives them), the run carried in from the
+// preceding lanes (a segmented warp scan of the lanes' open tails) is added to the lane's first fragment, and
+// the warp writes the stage to part[fb ..) with coalesced stores.  Returns the fp64 sum of the fragment sums
+// (lane partials of the fragment sums it stores, in fp32, one conversion per lane).
+__device__ __forceinline__ double plan_tile(const uint4 (&wd)[2], uint32_t fl, uint32_t sb, int32_t fb,
                                             float* __restrict__ stage, float* __restrict__ part, int lane) {
     const uint32_t u[8] = {wd[0].x, wd[0].y, wd[0].z, wd[0].w, wd[1].x, wd[1].y, wd[1].z, wd[1].w};
     float x[kLaneW];
-    uint32_t fl = 0;
 #pragma unroll
     for (int h = 0; h < 8; ++h) {
-        const uint32_t lo = u[h] & 0xffffu, hi = u[h] >> 16;
-        x[2 * h] = vseg[lo & 0x7fffu];
-        x[2 * h + 1] = vseg[hi & 0x7fffu];
-        fl |= (lo >> 15) << (2 * h);
-        fl |= (hi >> 15) << (2 * h + 1);
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x[2 * h]) : "r"(sb + ((u[h] & 0xffffu) << 2)));
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x[2 * h + 1]) : "r"(sb + ((u[h] >> 16) << 2)));
     }
     const int cnt = __popc(fl);
-    const int last = fl ? 31 - __clz(fl) : -1;
-    float tail = 0.0f;  // words after the lane's last end flag (all of them if none)
-#pragma unroll
-    for (int i = 0; i < kLaneW; ++i)
-        if (i > last) tail += x[i];
-    // inclusive segmented scan over lanes of (has flag, tail): the run carried into the next lane
-    int f = cnt > 0;
-    float v = tail;
-    int cpre = cnt;
+    int c = cnt;  // inclusive warp scan of the flag counts
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
-        const int fo = __shfl_up_sync(0xffffffffu, f, off);
-        const float vo = __shfl_up_sync(0xffffffffu, v, off);
-        const int co = __shfl_up_sync(0xffffffffu, cpre, off);
-        if (lane >= off) {
-            if (!f) v = vo + v;
-            f |= fo;
-            cpre += co;
-        }
+        const int co = __shfl_up_sync(0xffffffffu, c, off);
+        if (lane >= off) c += co;
     }
-    float carry = __shfl_up_sync(0xffffffffu, v, 1);
-    const int total = __shfl_sync(0xffffffffu, cpre, 31);
-    const int before = cpre - cnt;
-    if (lane == 0) carry = 0.0f;
-    // close this lane's fragments in word order: the first one continues the carried run
-    float acc = carry;
-    int k = before;
+    const int total = __shfl_sync(0xffffffffu, c, 31);
+    const int before = c - cnt;
+    // close the lane's fragments (the first one without the carried run); acc ends as the open tail
+    float acc = 0.0f;
+    float* st = stage + before;
 #pragma unroll
     for (int i = 0; i < kLaneW; ++i) {
         acc += x[i];
         if ((fl >> i) & 1u) {
-            stage[k++] = acc;
+            *st++ = acc;
             acc = 0.0f;
         }
     }
+    // inclusive segmented scan over lanes of (has flag, open tail): the run carried into the next lane
+    int f = cnt > 0;
+    float v = acc;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const int fo = __shfl_up_sync(0xffffffffu, f, off);
+        const float vo = __shfl_up_sync(0xffffffffu, v, off);
+        if (lane >= off) {
+            if (!f) v = vo + v;
+            f |= fo;
+        }
+    }
+    const float carry = __shfl_up_sync(0xffffffffu, v, 1);
+    if (lane > 0 && cnt > 0) stage[before] += carry;
     __syncwarp();
-    double gs = 0.0;
+    float ls = 0.0f;
     for (int i = lane; i < total; i += 32) {
         const float y = stage[i];
         __stcg(part + fb + i, y);
-        gs += (double)y;
+        ls += y;
     }
     __syncwarp();  // the stage is reused by the warp's next tile
-    return gs;
+    return (double)ls;
 }
 
 // trace layout: [64 iterations][4] CTA 0 stamps, then per CTA [4] sums over iterations 3..63 of the stamps'
@@ -601,6 +614,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rank_plan(RunArgs a) {
     const float4* vc4 = reinterpret_cast<const float4*>(W.vc);
     const uint4* words4 = reinterpret_cast<const uint4*>(a.words);
     float* wstage = vseg + kSegStride + warp * kTileW;
+    const uint32_t sb_seg = (uint32_t)__cvta_generic_to_shared(vseg);
     unsigned long long tprev_ = 0;
     int cur_seg = -1;  // the segment held in shared memory (phase B overwrites it)
 
@@ -632,9 +646,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_rank_plan(RunArgs a) {
                 int32_t tile = ta + warp;
                 uint4 cur[2], nxt[2];
                 int32_t fb = 0, fbn = 0;
+                uint32_t fl = 0, fln = 0;
                 if (tile < tb) {
                     cur[0] = __ldcs(words4 + (int64_t)tile * (kTileW / 8) + 2 * lane);
                     cur[1] = __ldcs(words4 + (int64_t)tile * (kTileW / 8) + 2 * lane + 1);
+                    fl = __ldcs(a.wflags + (int64_t)tile * 32 + lane);
                     fb = __ldg(a.fbase + tile);
                 }
                 for (; tile < tb; tile += kWarps) {
@@ -646,11 +662,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_rank_plan(RunArgs a) {
                     if (tn < tb) {  // the warp's next tile, in flight while this one is gathered
                         nxt[0] = __ldcs(words4 + (int64_t)tn * (kTileW / 8) + 2 * lane);
                         nxt[1] = __ldcs(words4 + (int64_t)tn * (kTileW / 8) + 2 * lane + 1);
+                        fln = __ldcs(a.wflags + (int64_t)tn * 32 + lane);
                         fbn = __ldg(a.fbase + tn);
                     }
-                    gp += plan_tile(cur, vseg, fb, wstage, W.part, lane);
+                    gp += plan_tile(cur, fl, sb_seg, fb, wstage, W.part, lane);
                     cur[0] = nxt[0];
                     cur[1] = nxt[1];
+                    fl = fln;
                     fb = fbn;
                 }
                 const double ug = mapi::block_sum(gp, red);  // its barriers also publish s_next[q ^ 1]
@@ -963,6 +981,8 @@ mapi_status mapi_csr_plan(int64_t n, int64_t nnz, const int32_t* row_ptr, const 
         kp_frag<<<ge, 256, 0, s>>>(nnz, B.ekey2, B.eoff2, B.fstart, B.fid, B.segstart, P.segb, B.frow, B.fidx, B.rcnt,
                                    B.tcnt, P.words);
         MAPI_LAUNCHED();
+        kp_wflags<<<blocks(nwords / kLaneW, 8), 256, 0, s>>>(nwords / kLaneW, P.words, P.wflags);
+        MAPI_LAUNCHED();
         // row-sorted slots (stable: the (segment, position) order within a row is kept) and their inverse
         int rbits = 1;
         while ((1ll << rbits) < n) ++rbits;
@@ -1065,7 +1085,7 @@ mapi_status mapi_rank_csr_plan(int32_t op, const void* plan, const mapi_csr_plan
     a.iters = max_iters;
     a.tol = tol;
     a.perm = P.perm; a.segb = P.segb; a.units = P.units; a.fbase = P.fbase; a.rsp = P.rsp;
-    a.bstart = P.bstart; a.bfrag = P.bfrag; a.brel = P.brel; a.words = P.words;
+    a.bstart = P.bstart; a.bfrag = P.bfrag; a.brel = P.brel; a.words = P.words; a.wflags = P.wflags;
     a.cap = cap; a.bg = bg; a.b0 = b0; a.deltas = deltas;
     // investigation: MAPI_PLAN_TRACE=1 prints CTA 0's per-phase times (us) of iterations 3..min(iters, 64);
     // MAPI_PLAN_TRACE_FILE=<path> also writes every CTA's phase times
