@@ -766,6 +766,11 @@ mapi_status sym_launch(const Device& d, int32_t op, const float* A, int64_t n, i
     a.it.bar = W.bar; a.it.status = W.status;
     a.prow = partials;
     a.pcol = partials + (size_t)sym_nc(n) * (size_t)((n + 31) & ~int64_t(31));  // row-tiled, whole tiles
+    // the y region (2n doubles) holds the tagged w words of both parities, zeroed so no stale tag matches;
+    // the w region holds y of the owned rows
+    a.wtag = reinterpret_cast<unsigned long long*>(W.y);
+    a.yg = W.w;
+    MAPI_CUDA(cudaMemsetAsync(W.y, 0, sizeof(unsigned long long) * 2 * (size_t)n, s));
     void* args[] = {&a};
     if (timer) timer->start();
     cudaError_t e = cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kSymThreads), args, smem, s);

@@ -16,17 +16,22 @@
 // partials of an 8-row group cross the warp in one reduce-scatter butterfly (9 shuffles) -> P_row[c][j]; the column terms against w_j (a shared-memory broadcast) accumulate per
 // lane in 8 registers over the task's 64 rows (64-term chains) -> P_col[b][k].  On the diagonal tasks
 // the row term keeps k >= j and the column term k > j; everything below the diagonal is skipped (never
-// read into a result: the tests fill it with NaN).  w_t lives in global memory (L2): a task reads its
-// 256 w_k (one 256-bit load per lane) and its 128 w_j (staged per warp in shared memory).
+// read into a result: the tests fill it with NaN).  w_t lives in global memory (L2) as tagged words: a task
+// reads its 256 w_k (8 words per lane) and its 128 w_j (staged per warp in shared memory).
 //
-// Per iteration, three grid barriers: tasks -> | -> each CTA sums the partials of the rows it OWNS (a range
-// balanced by partial count, 4 threads per row, fp64, fixed combine order): y_j = sum_{c >= c(j)} P_row[c][j]
-// + sum_{b <= b(j)} P_col[b][j] (fp32 chains <= 256 terms inside the partials, fp64 across them: within T1,
-// DESIGN.md), fp64 |y| partial per CTA -> | -> s_t (fixed order, every CTA), the owner forms w_{t+1,j} =
-// fp32(y_j / s_t) (fp64 division, as K2c) and its delta partial -> | -> delta_t (fixed order, every CTA),
-// stop test.  Nothing is replicated per CTA (K2c forms all n quotients in every CTA).  Deterministic for a
-// given (n, grid).  Requirements: n % 8 == 0, lda % 8 == 0, 32 B-aligned A (the caller falls back to the
-// full-matrix kernels otherwise); workspace y region >= 4n floats, slots >= 4 x grid doubles.
+// Per iteration, two grid barriers: tasks -> | -> the stop test on delta_{t-1} (lagged, below) -> each CTA sums
+// the partials of the rows it OWNS (a range balanced by partial count, fp64, fixed combine order):
+// y_j = sum_{c >= c(j)} P_row[c][j] + sum_{b <= b(j)} P_col[b][j] (fp32 chains <= 256 terms inside the
+// partials, fp64 across them: within T1), fp64 |y| partial per CTA -> | -> s_t (fixed order, every
+// CTA), the owner forms w_{t+1,j} = fp32(y_j / s_t) (fp64 division, as K2c), its delta partial, and PUBLISHES
+// w_{t+1,j} as one tagged 8-byte word ((t + 2) << 32 | bits) — no third barrier: the next iteration's tasks
+// poll the words of their rows / columns until the tag is current (a reader that sees the tag sees the
+// value: single-copy atomic 64-bit words, no fence).  delta_t is summed after the next iteration's first
+// barrier, so a tol stop at t (delta_t < tol) is decided one task phase late and that phase's partials are
+// discarded: the outputs are exactly those of stopping at t.  Nothing is replicated per CTA (K2c forms all n
+// quotients in every CTA).  Deterministic for a given (n, grid).  Requirements: n % 8 == 0, lda % 8 == 0,
+// 32 B-aligned A (the caller falls back to the full-matrix kernels otherwise); wtag 2n words zeroed per call,
+// yg n floats, slots >= 4 x grid doubles.
 #pragma once
 #include "dense.cuh"
 #include "mapi_common.cuh"
@@ -44,6 +49,8 @@ struct SymArgs {
     IterArgs it;
     float* prow;  // [nc][n] row partials
     float* pcol;  // [nb][n] column partials
+    unsigned long long* wtag;  // [2][n] tagged w words ((t + 1) << 32 | bits(w_t)), zeroed per call
+    float* yg;                 // [n] y of the owned rows
 };
 
 __host__ __device__ inline int64_t sym_nb(int64_t n) { return (n + kSymRB - 1) / kSymRB; }
@@ -97,6 +104,37 @@ __device__ __forceinline__ void sym_st4_keep(float* p, float a, float b, float c
                  : "memory");
 }
 
+__device__ __forceinline__ unsigned long long sym_ld_tag(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void sym_st_tag(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long sym_tagged(uint32_t tag, float w) {
+    return ((unsigned long long)tag << 32) | (unsigned long long)__float_as_uint(w);
+}
+// N tagged words of w_t (tag t + 1) from wt[idx[i]]: all loads in flight, then re-polled until current
+template <int N>
+__device__ __forceinline__ void sym_wait_words(const unsigned long long* wt, const int64_t (&idx)[N], uint32_t tag,
+                                               float (&out)[N]) {
+    unsigned long long v[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) v[i] = idx[i] >= 0 ? sym_ld_tag(wt + idx[i]) : sym_tagged(tag, 0.0f);
+    for (;;) {
+        bool ok = true;
+#pragma unroll
+        for (int i = 0; i < N; ++i) ok &= (uint32_t)(v[i] >> 32) == tag;
+        if (ok) break;
+#pragma unroll
+        for (int i = 0; i < N; ++i)
+            if ((uint32_t)(v[i] >> 32) != tag) v[i] = sym_ld_tag(wt + idx[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) out[i] = __uint_as_float((uint32_t)v[i]);
+}
+
 template <int OP>
 __device__ __forceinline__ float sym_tree8(const float (&a)[8], const float (&w)[8]) {
     float t[8];
@@ -126,22 +164,24 @@ __global__ void __launch_bounds__(kSymThreads, 1) k_iterate_sym(SymArgs sa) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t nb = sym_nb(n), nc = sym_nc(n), ntasks = sym_task_start(nb, nc);
     const int64_t o0 = sym_own_start(blockIdx.x, gridDim.x, n), o1 = sym_own_start(blockIdx.x + 1, gridDim.x, n);
-    // global state (workspace y region, 4n floats): w_t double-buffered by parity, y of the owned rows
-    float* wbuf = p.y;
-    float* yg = p.y + 2 * n;
+    unsigned long long* wtag = sa.wtag;  // [2][n] by iteration parity
+    float* yg = sa.yg;
     double* slotA = reinterpret_cast<double*>(p.slots);  // [2][grid] |y| partials
     double* slotD = slotA + 2 * gridDim.x;              // [2][grid] delta partials
     unsigned int epoch = 0;
     const uint64_t keep = sym_keep_policy();
-    for (int64_t j = o0 + tid; j < o1; j += blockDim.x) wbuf[j] = p.b0[j];
+    for (int64_t j = o0 + tid; j < o1; j += blockDim.x) sym_st_tag(wtag + j, sym_tagged(1u, p.b0[j]));
     grid_barrier(p.bar, ++epoch * gridDim.x);
 
     int32_t done = 0, status = kStOk;
-    for (int32_t t = 0; t < p.iters; ++t) {
-        const float* wcur = wbuf + (t & 1) * n;
-        float* wnext = wbuf + ((t + 1) & 1) * n;
+    bool stopped = false;
+    int32_t t = 0;
+    for (; t < p.iters; ++t) {
+        const unsigned long long* wcur = wtag + (t & 1) * n;  // w_t, tag t + 1
+        unsigned long long* wnext = wtag + ((t + 1) & 1) * n;
+        const uint32_t tag = (uint32_t)t + 1u;
         SYM_STAMP(t, 0);
-        // ---- phase 1: upper-triangle tasks (w read from L2: written by the owners before the last barrier).
+        // ---- phase 1: upper-triangle tasks (w_t from the tagged words; polled until current).
         // Tasks are taken dynamically from a per-iteration counter (SMs stream at different rates: a static
         // deal left the fastest CTAs idle ~40 us per iteration); a task's partials do not depend on which
         // warp computes them, so the results stay bitwise reproducible.  The next task index is fetched
@@ -167,28 +207,9 @@ __global__ void __launch_bounds__(kSymThreads, 1) k_iterate_sym(SymArgs sa) {
             const bool live = kl < n;          // n % 8 == 0: a lane is all in or all out
             const bool diag = c0 < j1;         // some element with k <= j: masked path
             const int rows = (int)(j1 - j0);
-            float wk[8], col[8];
-            if (live) {
-                const float4 u = __ldcg(reinterpret_cast<const float4*>(wcur + kl));
-                const float4 v = __ldcg(reinterpret_cast<const float4*>(wcur + kl) + 1);
-                wk[0] = u.x; wk[1] = u.y; wk[2] = u.z; wk[3] = u.w; wk[4] = v.x; wk[5] = v.y; wk[6] = v.z; wk[7] = v.w;
-            } else {
-#pragma unroll
-                for (int e = 0; e < 8; ++e) wk[e] = 0.0f;
-            }
-#pragma unroll
-            for (int e = 0; e < 8; ++e) col[e] = 0.0f;
-            __syncwarp();  // the previous task's reads of wj_s are done
-#pragma unroll
-            for (int i = 0; i < kSymRB / 32; ++i)
-                wj_s[32 * i + lane] = (32 * i + lane < rows) ? __ldcg(wcur + j0 + 32 * i + lane) : 0.0f;
-            __syncwarp();
-            // partial layouts are row-tiled ([j / 32][chunk or block][j % 32]): phase 2 reads all partials of
-            // 32 consecutive rows as one contiguous run
             float* prow = sa.prow + c * 32;  // + sym_tile(j) for row j
             const float* base = p.A + j0 * p.lda + kl;
             float a[2][4][8];
-            float pr[8];  // per-lane row partials of the current 8-row group
             auto load = [&](float (&buf)[4][8], int rb) {
 #pragma unroll
                 for (int r = 0; r < 4; ++r) {
@@ -201,6 +222,30 @@ __global__ void __launch_bounds__(kSymThreads, 1) k_iterate_sym(SymArgs sa) {
                         for (int e = 0; e < 8; ++e) buf[r][e] = 0.0f;
                 }
             };
+            load(a[0], 0);  // A does not depend on w: in flight while the w words are polled
+            float wk[8], col[8];
+            {
+                int64_t idx[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) idx[e] = live ? kl + e : -1;
+                sym_wait_words<8>(wcur, idx, tag, wk);
+            }
+#pragma unroll
+            for (int e = 0; e < 8; ++e) col[e] = 0.0f;
+            __syncwarp();  // the previous task's reads of wj_s are done
+            {
+                int64_t idx[kSymRB / 32];
+                float v[kSymRB / 32];
+#pragma unroll
+                for (int i = 0; i < kSymRB / 32; ++i) idx[i] = (32 * i + lane < rows) ? j0 + 32 * i + lane : -1;
+                sym_wait_words<kSymRB / 32>(wcur, idx, tag, v);
+#pragma unroll
+                for (int i = 0; i < kSymRB / 32; ++i) wj_s[32 * i + lane] = v[i];
+            }
+            __syncwarp();
+            // partial layouts are row-tiled ([j / 32][chunk or block][j % 32]): phase 2 reads all partials of
+            // 32 consecutive rows as one contiguous run
+            float pr[8];  // per-lane row partials of the current 8-row group
             // rows rb .. rb+3 of the group -> pr[h*4 .. h*4+3] (rows beyond the task add zeros and are
             // never stored)
             auto consume = [&](const float (&buf)[4][8], int rb, int h) {
@@ -231,7 +276,6 @@ __global__ void __launch_bounds__(kSymThreads, 1) k_iterate_sym(SymArgs sa) {
                 const int ri = res_row_of<8>(lane);
                 if ((lane & 3) == 0 && rb + ri < rows) sym_st_keep(prow + sym_tile(j0 + rb + ri, nc), v, keep);
             };
-            load(a[0], 0);
             for (int rb = 0; rb < rows; rb += 8) {
                 load(a[1], rb + 4);
                 consume(a[0], rb, 0);
@@ -251,6 +295,28 @@ __global__ void __launch_bounds__(kSymThreads, 1) k_iterate_sym(SymArgs sa) {
         SYM_STAMP(t, 2);
         // every warp is past its last fetch of iteration t - 1's counter: re-arm it for iteration t + 1
         if (blockIdx.x == 0 && tid == 0) p.bar[32 + ((t + 1) & 1)] = 0u;
+        // ---- the lagged stop test: delta_{t-1} (partials written before this barrier) decides whether w_t
+        // is the result; this iteration's task partials are then discarded
+        if (t > 0) {
+            double delta;
+            {
+                if (warp == 0) {
+                    double pp = 0.0;
+                    for (int cc = lane; cc < (int)gridDim.x; cc += 32) pp += __ldcg(slotD + ((t - 1) & 1) * gridDim.x + cc);
+                    pp = warp_sum(pp);
+                    if (lane == 0) red[33] = pp;
+                }
+                __syncthreads();
+                delta = red[33];
+                __syncthreads();
+            }
+            if (blockIdx.x == 0 && tid == 0 && p.deltas) p.deltas[t - 1] = (float)delta;
+            done = t;
+            if (p.tol > 0.0f && delta < (double)p.tol) {
+                stopped = true;
+                break;
+            }
+        }
         // ---- phase 2: y_j of the owned rows.  `subs` threads per row (the most that fit the owned rows in
         // one pass), consecutive threads on consecutive rows (coalesced partial reads); sub k takes partials
         // q = k, k + subs, ... in ascending order, 48 loads in flight, each batch summed
@@ -320,39 +386,36 @@ __global__ void __launch_bounds__(kSymThreads, 1) k_iterate_sym(SymArgs sa) {
         }
         if (!(sd > 0.0) || isinf(sd)) {  // uniform across the grid
             status = (sd == 0.0) ? kStDegenerate : kStNonfinite;
+            done = t;
+            stopped = true;
             break;
         }
-        // ---- w_{t+1} = fp32(y / s_t) (fp64 division, as K2c) for the owned rows only, delta partial
+        if (blockIdx.x == 0 && tid == 0 && p.norms) p.norms[t] = (float)sd;
+        // ---- w_{t+1} = fp32(y / s_t) (fp64 division, as K2c) for the owned rows: published as tagged words
+        // (tag t + 2) for the next tasks; the delta partial (summed after the next barrier)
         double dpart = 0.0;
         for (int64_t j = o0 + tid; j < o1; j += blockDim.x) {
             const float wn = (float)((double)__ldcg(yg + j) / sd);
-            dpart += (double)fabsf(wn - __ldcg(wcur + j));
-            wnext[j] = wn;
+            const float wo = __uint_as_float((uint32_t)sym_ld_tag(wcur + j));
+            dpart += (double)fabsf(wn - wo);
+            sym_st_tag(wnext + j, sym_tagged(tag + 1u, wn));
         }
         const double cta_d = block_sum(dpart, red);
         if (tid == 0) slotD[(t & 1) * gridDim.x + blockIdx.x] = cta_d;
-        grid_barrier(p.bar, ++epoch * gridDim.x);  // also publishes w_{t+1} for the next tasks
-        double delta;
-        {
-            if (warp == 0) {
-                double pp = 0.0;
-                for (int cc = lane; cc < (int)gridDim.x; cc += 32) pp += __ldcg(slotD + (t & 1) * gridDim.x + cc);
-                pp = warp_sum(pp);
-                if (lane == 0) red[33] = pp;
-            }
-            __syncthreads();
-            delta = red[33];
-            __syncthreads();
-        }
-        if (blockIdx.x == 0 && tid == 0) {
-            if (p.norms) p.norms[t] = (float)sd;
-            if (p.deltas) p.deltas[t] = (float)delta;
-        }
-        done = t + 1;
-        if (p.tol > 0.0f && delta < (double)p.tol) break;
     }
-    const float* wfin = wbuf + (done & 1) * n;  // w_done (on a degenerate stop: the last good iterate)
-    for (int64_t j = o0 + tid; j < o1; j += blockDim.x) p.w_out[j] = __ldcg(wfin + j);
+    if (!stopped) {  // ran all iterations: delta of the last one
+        grid_barrier(p.bar, ++epoch * gridDim.x);
+        if (warp == 0) {
+            double pp = 0.0;
+            for (int cc = lane; cc < (int)gridDim.x; cc += 32) pp += __ldcg(slotD + ((t - 1) & 1) * gridDim.x + cc);
+            pp = warp_sum(pp);
+            if (blockIdx.x == 0 && lane == 0 && p.deltas) p.deltas[t - 1] = (float)pp;
+        }
+        done = t;
+    }
+    // w_done (on a degenerate stop: the last good iterate), from the owned tagged words
+    const unsigned long long* wfin = wtag + (done & 1) * n;
+    for (int64_t j = o0 + tid; j < o1; j += blockDim.x) p.w_out[j] = __uint_as_float((uint32_t)sym_ld_tag(wfin + j));
     if (blockIdx.x == 0 && tid == 0) {
         p.status[0] = status;
         p.status[1] = done;

@@ -1,0 +1,4 @@
+mkdir -p gpurun_out
+timeout 1500 python -m pytest -q -x --timeout 1200 tests/test_gpu_dense.py -k "sym or cfg3" 2>&1 | tail -3
+timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/r2_sym_bench.json 2>&1; python -c "
+import json; d=json.loads(open('gpurun_out/r2_sym_bench.json').read().strip().splitlines()[-1]); print(d['value'], d['roofline']['frac'], d['ms_per_step'], d.get('clocks'))"

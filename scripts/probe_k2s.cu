@@ -24,6 +24,8 @@ int main() {
     cudaMalloc(&A, 4ull * n * n); cudaMalloc(&b0, 4 * n); cudaMalloc(&w, 4 * n); cudaMalloc(&y, 16 * n);
     cudaMalloc(&nr, 4 * T); cudaMalloc(&dl, 4 * T); cudaMalloc(&sl, 8 * 4096); cudaMalloc(&bar, 256); cudaMalloc(&st, 8);
     cudaMalloc(&part, sym_partials_bytes(n));
+    unsigned long long* wtag; float* yg;
+    cudaMalloc(&wtag, 16 * n); cudaMalloc(&yg, 4 * n);
     k_fill_sym<<<4096, 256>>>(A, n);
     std::vector<float> hb(n, 1.0f / 181.0f);
     cudaMemcpy(b0, hb.data(), 4 * n, cudaMemcpyHostToDevice);
@@ -35,11 +37,13 @@ int main() {
     a.it.A = A; a.it.n = n; a.it.lda = n; a.it.b0 = b0; a.it.iters = T; a.it.tol = 0; a.it.w_out = w;
     a.it.norms = nr; a.it.deltas = dl; a.it.y = y; a.it.slots = reinterpret_cast<float*>(sl); a.it.bar = bar;
     a.it.status = st; a.prow = part; a.pcol = part + sym_nc(n) * ((n + 31) & ~int64_t(31));
+    a.wtag = wtag; a.yg = yg;
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0); cudaEventCreate(&e1);
     float ms = 0;
     for (int rep = 0; rep < 2; ++rep) {
         cudaMemset(bar, 0, 256);
+        cudaMemset(wtag, 0, 16 * n);
         void* args[] = {&a};
         cudaEventRecord(e0);
         cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_iterate_sym<0>, dim3(sms), dim3(kSymThreads), args, smem, 0);
@@ -89,7 +93,7 @@ int main() {
         printf("\n");
     }
     printf("K2s n=%lld: %.1f us/iteration (events) | cycles: own tasks %.0f | barrier 1 %.0f | partial reduction %.0f | "
-           "barrier 2 %.0f | s, w, delta %.0f | total %.0f\n", (long long)n, 1e3 * ms / T, ph[0] / cnt, ph[1] / cnt,
+           "barrier 2 %.0f | s, w publish, delta partial %.0f | total %.0f\n", (long long)n, 1e3 * ms / T, ph[0] / cnt, ph[1] / cnt,
            ph[2] / cnt, ph[3] / cnt, ph[4] / cnt, tot / cnt);
     return 0;
 }
