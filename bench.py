@@ -6,8 +6,10 @@
 A step is one whole `mapi_iterate` call (100 MAPI iterations, Algorithm 1 / Eq. 8) on
 BASELINE configs[2] (dense symmetric 32768^2 fp32, 4 GiB).  `value` = MAPI iterations/s over all
 ranks with the matrix resident in HBM; `e2e` = the same through `mapi_iterate_host` with pinned
-HOST buffers (4 GiB H2D + 100 iterations + result D2H per step).  Under torchrun each rank runs
-an independent replica (weak scaling, no data-path collective).
+HOST buffers (H2D + 100 iterations + result D2H per step).  Under torchrun (N > 1) the default is
+K2sp: ONE symmetric problem whose upper-triangle task list is split over the ranks, the partial y
+vectors exchanged inside the kernel over NVLink P2P (strong scaling); --mode p2p /
+sharded / replicas select the row-sharded K2p, the NCCL all-gather comparator or independent replicas.
 
 --impl reference times the fp64 CPU oracle (oracle/, test infrastructure) on the same workload,
 a bounded sample per step, on rank 0 only.
@@ -65,10 +67,12 @@ def parse():
                    help="cfg3: time the full-matrix kernel (mapi_iterate) instead of the symmetric one")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=15.0, help="budget of the oracle sample")
-    p.add_argument("--mode", default="auto", choices=["auto", "single", "p2p", "sharded", "replicas"],
-                   help="multi-GPU layout for cfg3: p2p = row-sharded MAPI with the y exchange fused into one "
-                        "persistent kernel per rank (NVLink P2P; the default for N > 1); sharded = the same "
-                        "with an NCCL all-gather per iteration; replicas = independent copies")
+    p.add_argument("--mode", default="auto", choices=["auto", "single", "sym_p2p", "p2p", "sharded", "replicas"],
+                   help="multi-GPU layout for cfg3: sym_p2p = K2sp, the symmetric kernel's upper-triangle task "
+                        "list split over the ranks with the partial-y exchange fused into one persistent kernel "
+                        "per rank (NVLink P2P; the default for N > 1); p2p = K2p, row blocks with the y exchange "
+                        "fused; sharded = row blocks with an NCCL all-gather per iteration; replicas = "
+                        "independent copies")
     p.add_argument("--op", default="min1", choices=["min1", "min2", "dot"],
                    help="MAVP operator (Eq. 3 / Eq. 4) or 'dot' = the RPI comparator of Eq. (1) (dense workloads)")
     return p.parse_args()
@@ -526,16 +530,44 @@ def build_alg2(args, m, dev, stream):
                 oracle=None)
 
 
-def build_sharded(args, m, dev, stream, fused=False):
-    """cfg3 row-sharded over the ranks (paper_2110_12065_b200.sharded).  fused: K2p, one
-    persistent kernel per rank with the y exchange done in-kernel over NVLink P2P (CUDA IPC mappings);
-    else K1n + an NCCL all-gather of y per iteration."""
+def build_sharded(args, m, dev, stream, fused=False, sym=False):
+    """cfg3 over the ranks (paper_2110_12065_b200.sharded).  sym: K2sp, K2s's upper-triangle
+    task list split over the ranks, one persistent kernel per rank exchanging partial y vectors in-kernel
+    over NVLink P2P (CUDA IPC mappings).  fused: K2p, row blocks, the y rows exchanged in-kernel.  Else K1n
+    + an NCCL all-gather of y per iteration."""
     import torch
 
     import synth
-    from paper_2110_12065_b200.sharded import P2PExchange, iterate_sharded, iterate_sharded_p2p, row_partition
+    from paper_2110_12065_b200.sharded import (P2PExchange, iterate_sharded, iterate_sharded_p2p,
+                                               iterate_sym_sharded_p2p, row_partition, sym_shard)
 
     n, world, rank = 32768, args.world, args.rank
+    if sym:
+        r0, r1, tlo, thi = sym_shard(n, rank, world)
+        cfg = synth.cfg3_rows(r0, r1, device=dev)
+        A_local, b0, iters = cfg["A"], torch.from_numpy(cfg["b0"]).to(dev), cfg["iters"]
+        opc = {"min1": 0, "min2": 1, "dot": 2}[args.op]
+        ex = P2PExchange(n, rank, world, device=dev)
+        ws = torch.empty(int(m.workspace_size(m.WS_ITERATE_SYM, n)), dtype=torch.uint8, device=dev)
+
+        def run(A, b):
+            return iterate_sym_sharded_p2p(A, r0, r1, n, b, iters, ex, 0.0, op=opc, want_trace=False, ws=ws)
+
+        def step():
+            run(A_local, b0)
+            return iters
+
+        job_bytes = sym_bytes_per_iter(n)
+        return Work(step=step, unit="iterations/s", per_launch=job_bytes * iters, bytes_per_unit=job_bytes,
+                    bound="hbm", whole_step=True, shared_units=True,
+                    kernel=(f"K2sp k_iterate_sym_sharded: one cooperative launch per rank, tasks [{tlo}, {thi}) of "
+                            f"K2s's upper-triangle list (rows {r0}..{r1}), partial y exchanged in-kernel (P2P "
+                            "stores + one sys-scope arrival per rank), 100 iterations (step time)"),
+                    config={"workload": f"cfg3: {WORKLOADS['cfg3']}", "n": n, "rows_held": r1 - r0,
+                            "tasks": [tlo, thi], "iters_per_step": iters, "op": args.op,
+                            "exchange": "in-kernel P2P (K2sp), partial y fp32, world x n x 4 B per rank",
+                            "grid": ex.grid, "l2_flush": "inputs larger than L2"},
+                    A=A_local, b0=b0, iters=iters, oracle=None, sharded=True, run=run)
     r0, r1 = row_partition(n, world, rank)
     cfg = synth.cfg3_rows(r0, r1, device=dev)
     A_local = cfg["A"]
@@ -597,11 +629,12 @@ def run_mapi(args, rank, world, local_rank):
     args.rank, args.world = rank, world
     mode = args.mode
     if mode == "auto":
-        mode = "p2p" if (world > 1 and args.workload == "cfg3") else "single"
-    if mode in ("sharded", "p2p") and args.workload != "cfg3":
+        mode = "sym_p2p" if (world > 1 and args.workload == "cfg3" and not args.no_sym) else \
+            ("p2p" if (world > 1 and args.workload == "cfg3") else "single")
+    if mode in ("sharded", "p2p", "sym_p2p") and args.workload != "cfg3":
         raise SystemExit(f"--mode {mode} is implemented for the cfg3 workload")
-    if mode in ("sharded", "p2p"):
-        work = build_sharded(args, m, dev, stream, fused=mode == "p2p")
+    if mode in ("sharded", "p2p", "sym_p2p"):
+        work = build_sharded(args, m, dev, stream, fused=mode == "p2p", sym=mode == "sym_p2p")
     else:
         work = BUILDERS[args.workload](args, m, dev, stream)
     torch.cuda.synchronize()
@@ -614,7 +647,10 @@ def run_mapi(args, rank, world, local_rank):
            "dtype": "f32", "data": "synthetic (seeded recipes, DESIGN.md §5)", "impl": "mapi-b200"}
     cfg_out = dict(work.config)
     if getattr(work, "sharded", False):
-        cfg_out["parallelism"] = f"row-sharded x{world}: NCCL all-gather of y ({4 * 32768} B) per iteration"
+        cfg_out["parallelism"] = {"sym_p2p": f"K2sp x{world}: triangle task list split, partial y exchanged in-kernel",
+                                  "p2p": f"K2p x{world}: row blocks, y rows exchanged in-kernel",
+                                  "sharded": f"row-sharded x{world}: NCCL all-gather of y ({4 * 32768} B) per "
+                                             "iteration"}[mode]
         out["scaling"] = "strong"
     else:
         cfg_out["parallelism"] = f"replicas x{world} (independent problems, no collective)" if dist else "single GPU"

@@ -142,12 +142,19 @@ mapi_status mapi_matvec_normalized(int32_t op, const float *A, int64_t n_rows, i
                                    const float *y_prev, const float *w_prev, float *w_next, float *y_out,
                                    float *s_out, float *delta_out, int32_t *status_out, mapi_stream_t stream);
 
-/* ---- Row-sharded MAPI with the y exchange fused into the kernel.
- * Every rank allocates one EXCHANGE buffer with mapi_p2p_alloc (device memory, zeroed; layout in
- * p2p.cuh: a u64 arrival flag, y for two iteration parities, per-CTA norm partials), publishes its
- * 64-byte CUDA IPC handle (mapi_ipc_get_handle), opens every peer's (mapi_ipc_open_handle; the own
- * buffer is used directly), and passes the device array `peers` (world x u64 base addresses, peers[rank]
- * = own) to mapi_iterate_sharded.  Ownership: the caller frees with mapi_p2p_free / closes with
+/* ---- Multi-GPU MAPI with the exchange fused into the kernel.
+ * Every rank allocates one EXCHANGE buffer with mapi_p2p_alloc (device memory, zeroed; layout in p2p.cuh: a
+ * u64 arrival flag, world x n floats of exchanged y per iteration parity, world rank totals per parity),
+ * publishes its 64-byte CUDA IPC handle (mapi_ipc_get_handle), opens every peer's (mapi_ipc_open_handle; the
+ * own buffer is used directly), and passes the device array `peers` (world x u64 base addresses,
+ * peers[rank] = own) to mapi_iterate_sharded / mapi_iterate_sym_sharded.  Protocol: per iteration each rank
+ * stores its share into every rank's buffer (NVLink P2P, coalesced), fences at system scope, passes a local
+ * grid barrier, and ONE thread release-adds 1 to every rank's flag; every CTA waits for world arrivals.
+ * epoch0 / flag_base: the global iteration index and own flag value at the start of a call (0 / 0 for a
+ * fresh buffer; afterwards advance by *published_out and *published_out x world); identical on every rank.
+ * grid: the CTAs per rank, IDENTICAL on every rank (it fixes the row ownership and the summation orders):
+ * agree on it before the first call (e.g. the minimum SM count over the ranks); 0 = the device's SM count,
+ * allowed only for world == 1.  Ownership: the caller frees with mapi_p2p_free / closes with
  * mapi_ipc_close_handle. */
 size_t mapi_p2p_exchange_bytes(int64_t n, int32_t world);
 mapi_status mapi_p2p_alloc(size_t bytes, void **ptr_out);
@@ -156,23 +163,42 @@ mapi_status mapi_ipc_get_handle(const void *ptr, void *handle_out /* 64 bytes, h
 mapi_status mapi_ipc_open_handle(const void *handle /* 64 bytes, host */, void **ptr_out);
 mapi_status mapi_ipc_close_handle(void *ptr);
 
-/* Algorithm 1 on a row-sharded A in ONE cooperative launch per rank: rank `rank` of `world`
+/* K2p: Algorithm 1 on a row-sharded A in ONE cooperative launch per rank: rank `rank` of `world`
  * holds rows [row0, row0 + m) of the n x n matrix (A_local: m x n, lda; 32 B-aligned rows, lda % 8 == 0,
- * n >= 256); b0 is the full start vector (n).  Per iteration every CTA computes its rows, stores them
- * (and its fp64 norm partial) into every rank's exchange buffer through NVLink P2P, release-adds the
- * peers' flags (system scope) and waits for all world x G arrivals on its own; then s_t, w_{t+1} and
- * delta_t are formed in the same fixed order on every rank (identical bits, identical stop decision).
- * epoch0 / flag_base: the global iteration index and own flag value at the start of this call (0 / 0
- * for a fresh exchange buffer; afterwards advance both by *published_out and *published_out * world *
- * (*grid_out)); identical on every rank.  Outputs: w_out (full n, l1-unit; l2-unit for DOT), norms /
- * deltas (iters, nullable), host *iters_done, *published_out (iterations that reached the exchange),
- * *grid_out (CTAs per rank).  ws: mapi_workspace_size(MAPI_WS_ITERATE_SHARDED, ...) = 256 bytes of
- * status.  Synchronises `stream`. */
+ * n >= 256); b0 is the full start vector (n).  Per iteration every CTA computes its rows into the own buffer,
+ * the rank copies its row block and its |y| total to every peer, then s_t = the rank totals in rank order,
+ * w_{t+1} and delta_t are formed in the same fixed order on every rank (identical bits, identical stop
+ * decision; on one rank bitwise mapi_iterate's cooperative kernel).  Outputs: w_out (full n, l1-unit;
+ * l2-unit for DOT), norms / deltas (iters, nullable), host *iters_done, *published_out (iterations that
+ * reached the exchange), *grid_out.  ws: mapi_workspace_size(MAPI_WS_ITERATE_SHARDED, 0, 0, 0) bytes.
+ * Synchronises `stream`. */
 mapi_status mapi_iterate_sharded(int32_t op, const float *A_local, int64_t m, int64_t n, int64_t lda, int64_t row0,
                                  const float *b0, int32_t iters, float tol, int32_t rank, int32_t world,
-                                 const uint64_t *peers, uint64_t epoch0, uint64_t flag_base, float *w_out,
-                                 float *norms, float *deltas, int32_t *iters_done, int32_t *published_out,
-                                 int32_t *grid_out, void *ws, size_t ws_bytes, mapi_stream_t stream);
+                                 const uint64_t *peers, uint64_t epoch0, uint64_t flag_base, int32_t grid,
+                                 float *w_out, float *norms, float *deltas, int32_t *iters_done,
+                                 int32_t *published_out, int32_t *grid_out, void *ws, size_t ws_bytes,
+                                 mapi_stream_t stream);
+
+/* K2sp: Algorithm 1 on a SYMMETRIC A (Eq. 2 / 5 covariances) over `world` ranks: K2s's upper-
+ * triangle task list (mapi_iterate_sym) is split into equal contiguous ranges; rank r holds only the rows its
+ * tasks read, [row_lo, row_hi) as given by mapi_sym_shard_rows (A_local: (row_hi - row_lo) x n, lda, full
+ * rows; only their upper-triangle part is read).  Per iteration each rank reduces the partials of its own
+ * tasks into a partial y, stores it (fp32) into every rank's buffer, and after the arrivals every rank sums
+ * the world partials in rank order (fp64, one rounding): identical y, s_t, w and stop decision everywhere; on
+ * one rank bitwise mapi_iterate_sym.  Outputs, epoch / flag / grid as mapi_iterate_sharded.  ws:
+ * mapi_workspace_size(MAPI_WS_ITERATE_SYM, n, 0, 0).  Synchronises `stream`. */
+mapi_status mapi_iterate_sym_sharded(int32_t op, const float *A_local, int64_t row_lo, int64_t row_hi, int64_t n,
+                                     int64_t lda, const float *b0, int32_t iters, float tol, int32_t rank,
+                                     int32_t world, const uint64_t *peers, uint64_t epoch0, uint64_t flag_base,
+                                     int32_t grid, float *w_out, float *norms, float *deltas, int32_t *iters_done,
+                                     int32_t *published_out, int32_t *grid_out, void *ws, size_t ws_bytes,
+                                     mapi_stream_t stream);
+/* Host-only helpers of K2sp (no device calls): the rows [*row_lo, *row_hi) and tasks [*task_lo, *task_hi) of
+ * rank `rank`; and, for row j, the rank's valid partial ranges out4 = {first chunk, end chunk, first row
+ * block, end row block} (for tests of the partition). */
+mapi_status mapi_sym_shard_rows(int64_t n, int32_t rank, int32_t world, int64_t *row_lo, int64_t *row_hi,
+                                int64_t *task_lo, int64_t *task_hi);
+mapi_status mapi_sym_shard_valid(int64_t n, int32_t rank, int32_t world, int64_t j, int64_t *out4);
 
 /* mapi_iterate with HOST buffers (end-to-end path): A_host (n x lda), b0_host, w_out_host,
  * w_l2_out_host / norms_host / deltas_host (nullable), iters_done (host).  The call copies A and

@@ -88,7 +88,11 @@ def load():
             "mapi_ipc_open_handle": (st, [P, ctypes.POINTER(ctypes.c_void_p)]),
             "mapi_ipc_close_handle": (st, [P]),
             "mapi_iterate_sharded": (st, [i32, P, i64, i64, i64, i64, P, i32, f32, i32, i32, P, ctypes.c_uint64,
-                                          ctypes.c_uint64, P, P, P, P, P, P, P, sz, P]),
+                                          ctypes.c_uint64, i32, P, P, P, P, P, P, P, sz, P]),
+            "mapi_iterate_sym_sharded": (st, [i32, P, i64, i64, i64, i64, P, i32, f32, i32, i32, P,
+                                              ctypes.c_uint64, ctypes.c_uint64, i32, P, P, P, P, P, P, P, sz, P]),
+            "mapi_sym_shard_rows": (st, [i64, i32, i32, P, P, P, P]),
+            "mapi_sym_shard_valid": (st, [i64, i32, i32, i64, P]),
             "mapi_status_string": (ctypes.c_char_p, [st]),
             "mapi_last_error_message": (ctypes.c_char_p, []),
             "mapi_launch_count": (ctypes.c_uint64, []),

@@ -84,6 +84,9 @@ mapi_status check_op(int32_t op, bool dot_ok = false) {
 constexpr int kMaxGrid = 1024;
 constexpr int kIterThreads = 512;
 
+// K2p workspace: [status[2] @0, grid-barrier counter @64 | 256][CTA |y| partials 2 x kP2pMaxGrid f64]
+size_t sharded_ws_bytes() { return 256 + sizeof(double) * 2 * kP2pMaxGrid; }
+
 size_t iterate_ws_bytes(int64_t n) {
     return 256 + align256(sizeof(double) * 2 * kMaxGrid) + align256(sizeof(double) * 2 * (size_t)n) +
            align256(sizeof(float) * (size_t)n);
@@ -579,7 +582,7 @@ size_t mapi_workspace_size(int32_t op, int64_t n, int64_t nnz, int32_t k) {
     case MAPI_WS_RECONSTRUCT: return outer_ws_bytes(n, nnz, k, nnz);
     case MAPI_WS_CSR_PREPARE: return csr_prepare_ws_bytes(n, nnz);
     case MAPI_WS_RANK_CSR: return csr_rank_ws_bytes(n, nnz);
-    case MAPI_WS_ITERATE_SHARDED: return 256;
+    case MAPI_WS_ITERATE_SHARDED: return sharded_ws_bytes();
     case MAPI_WS_ITERATE_HOST_MANY: return iterate_host_many_ws_bytes(n, nnz, k, 2);
     case MAPI_WS_ITERATE_HOST_MANY_PACKED: return iterate_host_many_ws_bytes(n, packed_lda(n), k, 2, true);
     case MAPI_WS_ITERATE_SYM: return iterate_ws_bytes(n) + align256(sym_partials_bytes(n));
@@ -1357,16 +1360,48 @@ mapi_status mapi_ipc_close_handle(void* ptr) {
     return MAPI_OK;
 }
 
+static mapi_status p2p_common_checks(int32_t rank, int32_t world, int32_t grid) {
+    if (world < 1 || world > kP2pMaxWorld || rank < 0 || rank >= world)
+        return fail(MAPI_ERR_BAD_PARAM, "rank %d / world %d (world in [1, %d])", rank, world, kP2pMaxWorld);
+    if (grid < 0 || grid > kP2pMaxGrid)
+        return fail(MAPI_ERR_BAD_PARAM, "grid (%d) must be in [0, %d]", grid, kP2pMaxGrid);
+    if (world > 1 && grid == 0)
+        return fail(MAPI_ERR_BAD_PARAM, "world > 1 needs an explicit grid agreed by every rank (e.g. the min SM count)");
+    return MAPI_OK;
+}
+static mapi_status p2p_device_checks(int32_t grid, Device& d) {
+    mapi_status st = device_info(d);
+    if (st != MAPI_OK) return st;
+    if (grid > d.sms) return fail(MAPI_ERR_BAD_PARAM, "grid (%d) exceeds the device's %d SMs", grid, d.sms);
+    return MAPI_OK;
+}
+
+static mapi_status p2p_finish(const int32_t* status, cudaStream_t s, Timer& timer, int32_t* iters_done,
+                              int32_t* published_out) {
+    int32_t h[2] = {0, 0};
+    MAPI_CUDA(cudaMemcpyAsync(h, status, sizeof(h), cudaMemcpyDeviceToHost, s));
+    MAPI_CUDA(cudaStreamSynchronize(s));
+    timer.harvest();
+    if (iters_done) *iters_done = h[1];
+    // iterations that reached the exchange: the completed ones, plus the one a degenerate s stopped
+    // (a timed-out exchange leaves the buffers inconsistent: the caller must discard the exchange)
+    if (published_out) *published_out = h[1] + ((h[0] == kStDegenerate || h[0] == kStNonfinite) ? 1 : 0);
+    if (h[0] == kStP2pTimeout)
+        return fail(MAPI_ERR_CUDA, "peer exchange timed out at iteration %d (a rank did not arrive)", h[1]);
+    if (h[0] != 0) return fail((mapi_status)h[0], "degenerate / non-finite norm at iteration %d", h[1]);
+    return MAPI_OK;
+}
+
 mapi_status mapi_iterate_sharded(int32_t op, const float* A_local, int64_t m, int64_t n, int64_t lda, int64_t row0,
                                  const float* b0, int32_t iters, float tol, int32_t rank, int32_t world,
-                                 const uint64_t* peers, uint64_t epoch0, uint64_t flag_base, float* w_out,
-                                 float* norms, float* deltas, int32_t* iters_done, int32_t* published_out,
-                                 int32_t* grid_out, void* ws, size_t ws_bytes, mapi_stream_t stream) {
+                                 const uint64_t* peers, uint64_t epoch0, uint64_t flag_base, int32_t grid_in,
+                                 float* w_out, float* norms, float* deltas, int32_t* iters_done,
+                                 int32_t* published_out, int32_t* grid_out, void* ws, size_t ws_bytes,
+                                 mapi_stream_t stream) {
     mapi_status st = check_op(op, true);
     if (st != MAPI_OK) return st;
     if (!A_local || !b0 || !peers || !w_out || !ws) return fail(MAPI_ERR_NULL, "a required pointer is NULL");
-    if (world < 1 || world > kP2pMaxWorld || rank < 0 || rank >= world)
-        return fail(MAPI_ERR_BAD_PARAM, "rank %d / world %d (world in [1, %d])", rank, world, kP2pMaxWorld);
+    if ((st = p2p_common_checks(rank, world, grid_in)) != MAPI_OK) return st;
     if (n < 256 || m < 1 || m > n || row0 < 0 || row0 + m > n)
         return fail(MAPI_ERR_SHAPE, "rows [%lld, %lld) of n = %lld (n >= 256 required)", (long long)row0,
                     (long long)(row0 + m), (long long)n);
@@ -1374,21 +1409,23 @@ mapi_status mapi_iterate_sharded(int32_t op, const float* A_local, int64_t m, in
     if (vec_width(A_local, lda) != 8) return fail(MAPI_ERR_SHAPE, "A_local rows must be 32 B-aligned (lda %% 8 == 0)");
     if (iters < 1) return fail(MAPI_ERR_BAD_PARAM, "iters (%d) must be >= 1", iters);
     if (!(tol >= 0.0f)) return fail(MAPI_ERR_BAD_PARAM, "tol must be >= 0");
-    if (ws_bytes < 256) return fail(MAPI_ERR_WORKSPACE, "ws_bytes (%zu) < 256", ws_bytes);
+    if (ws_bytes < sharded_ws_bytes()) return fail(MAPI_ERR_WORKSPACE, "ws_bytes (%zu) < %zu", ws_bytes, sharded_ws_bytes());
     Device d;
-    if ((st = device_info(d)) != MAPI_OK) return st;
+    if ((st = p2p_device_checks(grid_in, d)) != MAPI_OK) return st;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const int nw = coop_warps(n);
-    const int grid = (int)std::min<int64_t>({(int64_t)d.sms, m, (int64_t)kP2pMaxGrid});
+    const int grid = grid_in > 0 ? grid_in : (int)std::min<int64_t>({(int64_t)d.sms, (int64_t)kP2pMaxGrid});
     const size_t smem = p2p_smem_bytes(m, n, grid, nw);
     if (smem > (size_t)d.smem_optin) return fail(MAPI_ERR_SHAPE, "n (%lld) too large for the staged w", (long long)n);
     int32_t* status = static_cast<int32_t*>(ws);
-    MAPI_CUDA(cudaMemsetAsync(status, 0, 8, s));
+    MAPI_CUDA(cudaMemsetAsync(ws, 0, 256, s));
     P2PArgs a;
     a.A = A_local; a.m = m; a.n = n; a.lda = lda; a.row0 = row0; a.b0 = b0; a.iters = iters; a.tol = tol;
     a.rank = rank; a.world = world; a.peers = reinterpret_cast<const unsigned long long*>(peers);
     a.epoch0 = epoch0; a.flag_base = flag_base; a.w_out = w_out; a.norms = norms; a.deltas = deltas;
     a.status = status;
+    a.bar = reinterpret_cast<unsigned int*>(static_cast<char*>(ws) + 64);
+    a.cslots = reinterpret_cast<double*>(static_cast<char*>(ws) + 256);
     const int pol = load_policy(d, m, lda);
     Timer timer(s);
     with_op(op, [&](auto OPc) {
@@ -1408,19 +1445,101 @@ mapi_status mapi_iterate_sharded(int32_t op, const float* A_local, int64_t m, in
         });
     });
     if (st != MAPI_OK) return st;
-    int32_t h[2] = {0, 0};
-    MAPI_CUDA(cudaMemcpyAsync(h, status, sizeof(h), cudaMemcpyDeviceToHost, s));
-    MAPI_CUDA(cudaStreamSynchronize(s));
-    timer.harvest();
-    if (iters_done) *iters_done = h[1];
-    // iterations that reached the exchange: the completed ones, plus the one a degenerate s stopped
-    // (a timed-out exchange leaves the buffers inconsistent: the caller must discard the exchange)
-    if (published_out) *published_out = h[1] + ((h[0] == kStDegenerate || h[0] == kStNonfinite) ? 1 : 0);
     if (grid_out) *grid_out = grid;
-    if (h[0] == kStP2pTimeout)
-        return fail(MAPI_ERR_CUDA, "peer exchange timed out at iteration %d (a rank did not arrive)", h[1]);
-    if (h[0] != 0) return fail((mapi_status)h[0], "degenerate / non-finite norm at iteration %d", h[1]);
+    return p2p_finish(status, s, timer, iters_done, published_out);
+}
+
+// ---- K2sp: K2s with the task list split over the ranks (p2p.cuh)
+static inline void sym_shard_tasks(int64_t n, int32_t rank, int32_t world, int64_t& tlo, int64_t& thi) {
+    const int64_t T = sym_task_start(sym_nb(n), sym_nc(n));
+    tlo = T * rank / world;
+    thi = T * (rank + 1) / world;
+}
+
+mapi_status mapi_sym_shard_rows(int64_t n, int32_t rank, int32_t world, int64_t* row_lo, int64_t* row_hi,
+                                int64_t* task_lo, int64_t* task_hi) {
+    if (n < 1) return fail(MAPI_ERR_SHAPE, "n (%lld) must be >= 1", (long long)n);
+    if (world < 1 || world > kP2pMaxWorld || rank < 0 || rank >= world)
+        return fail(MAPI_ERR_BAD_PARAM, "rank %d / world %d (world in [1, %d])", rank, world, kP2pMaxWorld);
+    int64_t tlo, thi, r0, r1;
+    sym_shard_tasks(n, rank, world, tlo, thi);
+    sym_shard_rows(n, tlo, thi, r0, r1);
+    if (row_lo) *row_lo = r0;
+    if (row_hi) *row_hi = r1;
+    if (task_lo) *task_lo = tlo;
+    if (task_hi) *task_hi = thi;
     return MAPI_OK;
+}
+
+mapi_status mapi_sym_shard_valid(int64_t n, int32_t rank, int32_t world, int64_t j, int64_t* out4) {
+    if (n < 1 || j < 0 || j >= n || !out4) return fail(MAPI_ERR_SHAPE, "bad n / j / out");
+    if (world < 1 || world > kP2pMaxWorld || rank < 0 || rank >= world)
+        return fail(MAPI_ERR_BAD_PARAM, "rank %d / world %d", rank, world);
+    int64_t tlo, thi;
+    sym_shard_tasks(n, rank, world, tlo, thi);
+    const SymValid v = sym_valid(j, n, tlo, thi);
+    out4[0] = v.c_lo; out4[1] = v.c_hi; out4[2] = v.b_lo; out4[3] = v.b_hi;
+    return MAPI_OK;
+}
+
+mapi_status mapi_iterate_sym_sharded(int32_t op, const float* A_local, int64_t row_lo, int64_t row_hi, int64_t n,
+                                     int64_t lda, const float* b0, int32_t iters, float tol, int32_t rank,
+                                     int32_t world, const uint64_t* peers, uint64_t epoch0, uint64_t flag_base,
+                                     int32_t grid_in, float* w_out, float* norms, float* deltas,
+                                     int32_t* iters_done, int32_t* published_out, int32_t* grid_out, void* ws,
+                                     size_t ws_bytes, mapi_stream_t stream) {
+    mapi_status st = check_op(op, true);
+    if (st != MAPI_OK) return st;
+    if (!A_local || !b0 || !peers || !w_out || !ws) return fail(MAPI_ERR_NULL, "a required pointer is NULL");
+    if ((st = p2p_common_checks(rank, world, grid_in)) != MAPI_OK) return st;
+    if (n < 8 || n % 8 != 0) return fail(MAPI_ERR_SHAPE, "n (%lld) must be a positive multiple of 8", (long long)n);
+    int64_t tlo, thi, r0, r1;
+    sym_shard_tasks(n, rank, world, tlo, thi);
+    sym_shard_rows(n, tlo, thi, r0, r1);
+    if (row_lo != r0 || row_hi != r1)
+        return fail(MAPI_ERR_SHAPE, "rank %d holds rows [%lld, %lld); mapi_sym_shard_rows gives [%lld, %lld)", rank,
+                    (long long)row_lo, (long long)row_hi, (long long)r0, (long long)r1);
+    if (lda < n || lda % 8 != 0 || (reinterpret_cast<uintptr_t>(A_local) & 31) != 0)
+        return fail(MAPI_ERR_SHAPE, "A_local needs lda >= n, lda %% 8 == 0 and 32 B-aligned rows");
+    if (iters < 1) return fail(MAPI_ERR_BAD_PARAM, "iters (%d) must be >= 1", iters);
+    if (!(tol >= 0.0f)) return fail(MAPI_ERR_BAD_PARAM, "tol must be >= 0");
+    const size_t need = mapi_workspace_size(MAPI_WS_ITERATE_SYM, n, 0, 0);
+    if (ws_bytes < need) return fail(MAPI_ERR_WORKSPACE, "ws_bytes (%zu) < required (%zu)", ws_bytes, need);
+    Device d;
+    if ((st = p2p_device_checks(grid_in, d)) != MAPI_OK) return st;
+    if (sym_smem_bytes(n) > (size_t)d.smem_optin) return fail(MAPI_ERR_SHAPE, "symmetric kernel smem too large");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int grid = grid_in > 0 ? grid_in : (int)std::min<int64_t>({(int64_t)d.sms, n, (int64_t)kP2pMaxGrid});
+    IterWs W = carve_iterate(ws, n);
+    float* partials = reinterpret_cast<float*>(static_cast<char*>(ws) + iterate_ws_bytes(n));
+    MAPI_CUDA(cudaMemsetAsync(W.bar, 0, 256, s));
+    MAPI_CUDA(cudaMemsetAsync(W.y, 0, sizeof(unsigned long long) * 2 * (size_t)n, s));
+    SymShardArgs x;
+    SymArgs& a = x.sa;
+    a.it.A = A_local; a.it.n = n; a.it.lda = lda; a.it.b0 = b0; a.it.iters = iters; a.it.tol = tol;
+    a.it.w_out = w_out; a.it.norms = norms; a.it.deltas = deltas; a.it.y = W.y; a.it.slots = W.slots;
+    a.it.bar = W.bar; a.it.status = W.status;
+    a.prow = partials;
+    a.pcol = partials + (size_t)sym_nc(n) * (size_t)((n + 31) & ~int64_t(31));
+    a.wtag = reinterpret_cast<unsigned long long*>(W.y);
+    a.yg = W.w;
+    x.row0 = r0; x.tlo = tlo; x.thi = thi; x.rank = rank; x.world = world;
+    x.peers = reinterpret_cast<const unsigned long long*>(peers);
+    x.epoch0 = epoch0; x.flag_base = flag_base;
+    using KernT = void (*)(SymShardArgs);
+    KernT kern = op == 2 ? k_iterate_sym_sharded<2> : (op == 1 ? k_iterate_sym_sharded<1> : k_iterate_sym_sharded<0>);
+    const size_t smem = sym_smem_bytes(n);
+    MAPI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    Timer timer(s);
+    void* args[] = {&x};
+    timer.start();
+    cudaError_t e = cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kSymThreads), args, smem, s);
+    timer.stop();
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    if (e != cudaSuccess)
+        return fail(MAPI_ERR_CUDA, "sharded symmetric launch (grid %d): %s", grid, cudaGetErrorString(e));
+    if (grid_out) *grid_out = grid;
+    return p2p_finish(W.status, s, timer, iters_done, published_out);
 }
 
 mapi_status mapi_matvec_normalized(int32_t op, const float* A, int64_t n_rows, int64_t n_cols, int64_t lda,

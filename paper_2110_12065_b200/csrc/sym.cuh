@@ -154,6 +154,255 @@ __device__ long long g_sym_cta[2 * 256 * 32];  // per-CTA task-phase start / end
 #define SYM_STAMP(t, k)
 #endif
 
+// task index of (row block b, chunk c) (c >= b / kSymCR)
+__host__ __device__ inline int64_t sym_task_index(int64_t b, int64_t c, int64_t nc) {
+    return sym_task_start(b, nc) + c - b / kSymCR;
+}
+// Sharded K2s: rank r of P takes the contiguous task range [tlo, thi) = [r T / P, (r + 1) T / P).  For row j
+// its valid partials on rank r: row partials of chunks [c_lo, c_hi) (tasks of strip b(j) in the range, from
+// c(j) on) and column partials of row blocks [b_lo, b_hi) (tasks (b, c(j)), b <= b(j), in the range; their
+// index grows with b).  On one rank both are the full lists.
+struct SymValid {
+    int64_t c_lo, c_hi, b_lo, b_hi;
+};
+__host__ __device__ inline SymValid sym_valid(int64_t j, int64_t n, int64_t tlo, int64_t thi) {
+    const int64_t nc = sym_nc(n), B = j / kSymRB, C = j / kSymCC;
+    SymValid v;
+    const int64_t s0 = sym_task_start(B, nc), half = B / kSymCR;  // strip B: chunks half .. nc-1
+    v.c_lo = tlo - s0 + half;
+    v.c_hi = thi - s0 + half;
+    v.c_lo = v.c_lo < C ? C : v.c_lo;
+    v.c_hi = v.c_hi > nc ? nc : v.c_hi;
+    if (v.c_hi < v.c_lo) v.c_hi = v.c_lo;
+    // column partials: the b in [0, B] with tlo <= index(b, C) < thi
+    int64_t lo = 0, hi = B + 1;  // first b with index >= tlo
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (sym_task_index(mid, C, nc) >= tlo) hi = mid;
+        else lo = mid + 1;
+    }
+    v.b_lo = lo;
+    hi = B + 1;  // first b with index >= thi
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (sym_task_index(mid, C, nc) >= thi) hi = mid;
+        else lo = mid + 1;
+    }
+    v.b_hi = lo;
+    return v;
+}
+// the rows rank r's tasks read: strips b(tlo) .. b(thi - 1)
+__host__ __device__ inline void sym_shard_rows(int64_t n, int64_t tlo, int64_t thi, int64_t& r0, int64_t& r1) {
+    const int64_t nb = sym_nb(n), nc = sym_nc(n);
+    auto strip = [&](int64_t task) {
+        int64_t lo = 0, hi = nb - 1;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi + 1) >> 1;
+            if (sym_task_start(mid, nc) <= task) lo = mid;
+            else hi = mid - 1;
+        }
+        return lo;
+    };
+    if (thi <= tlo) {
+        r0 = r1 = 0;
+        return;
+    }
+    r0 = strip(tlo) * kSymRB;
+    r1 = (strip(thi - 1) + 1) * kSymRB;
+    if (r1 > n) r1 = n;
+}
+
+// ---- phase 1 of K2s: the upper-triangle tasks [tlo, thi) of w_t (tagged words wcur, tag), taken from a
+// counter (`ctr`, zeroed, counts from 0).  A rows are addressed relative to row r0 (the sharded ranks hold
+// only the rows of their strips).
+template <int OP>
+__device__ __forceinline__ void sym_tasks(const SymArgs& sa, const float* A, int64_t r0, int64_t tlo, int64_t thi,
+                                          unsigned int* ctr, const unsigned long long* wcur, uint32_t tag,
+                                          float* wj_s, uint64_t keep) {
+    const IterArgs& p = sa.it;
+    const int64_t n = p.n;
+    const int lane = threadIdx.x & 31;
+    const int64_t nb = sym_nb(n), nc = sym_nc(n);
+    auto fetch = [&]() -> unsigned int {
+        unsigned int v = 0;
+        if (lane == 0) v = atomicAdd(ctr, 1u);
+        return v;
+    };
+    unsigned int nxt = fetch();
+    for (int64_t task = tlo + __shfl_sync(0xffffffffu, nxt, 0); task < thi;) {
+        nxt = fetch();
+        int64_t lo = 0, hi = nb - 1;  // row block: last b with start(b) <= task
+        while (lo < hi) {
+            const int64_t mid = (lo + hi + 1) >> 1;
+            if (sym_task_start(mid, nc) <= task) lo = mid;
+            else hi = mid - 1;
+        }
+        const int64_t b = lo, c = b / kSymCR + (task - sym_task_start(b, nc));
+        const int64_t j0 = b * kSymRB, j1 = min(n, j0 + kSymRB), c0 = c * kSymCC;
+        const int64_t kl = c0 + 8 * lane;  // this lane's first column
+        const bool live = kl < n;          // n % 8 == 0: a lane is all in or all out
+        const bool diag = c0 < j1;         // some element with k <= j: masked path
+        const int rows = (int)(j1 - j0);
+        float* prow = sa.prow + c * 32;  // + sym_tile(j) for row j
+        const float* base = A + (j0 - r0) * p.lda + kl;
+        float a[2][4][8];
+        auto load = [&](float (&buf)[4][8], int rb) {
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                // (on diagonal tasks a lane whose 8 columns all lie below the row's diagonal loads nothing:
+                // every one of its terms is masked)
+                if (live && rb + r < rows && kl + 7 >= j0 + rb + r)
+                    ld_stream<8, 0>(base + (int64_t)(rb + r) * p.lda, buf[r]);
+                else
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) buf[r][e] = 0.0f;
+            }
+        };
+        load(a[0], 0);  // A does not depend on w: in flight while the w words are polled
+        float wk[8], col[8];
+        {
+            int64_t idx[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) idx[e] = live ? kl + e : -1;
+            sym_wait_words<8>(wcur, idx, tag, wk);
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) col[e] = 0.0f;
+        __syncwarp();  // the previous task's reads of wj_s are done
+        {
+            int64_t idx[kSymRB / 32];
+            float v[kSymRB / 32];
+#pragma unroll
+            for (int i = 0; i < kSymRB / 32; ++i) idx[i] = (32 * i + lane < rows) ? j0 + 32 * i + lane : -1;
+            sym_wait_words<kSymRB / 32>(wcur, idx, tag, v);
+#pragma unroll
+            for (int i = 0; i < kSymRB / 32; ++i) wj_s[32 * i + lane] = v[i];
+        }
+        __syncwarp();
+        // partial layouts are row-tiled ([j / 32][chunk or block][j % 32]): phase 2 reads all partials of
+        // 32 consecutive rows as one contiguous run
+        float pr[8];  // per-lane row partials of the current 8-row group
+        // rows rb .. rb+3 of the group -> pr[h*4 .. h*4+3] (rows beyond the task add zeros and are
+        // never stored)
+        auto consume = [&](const float (&buf)[4][8], int rb, int h) {
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const int64_t j = j0 + rb + r;
+                const float wj = wj_s[rb + r];
+                if (!diag) {
+                    pr[4 * h + r] = sym_tree8<OP>(buf[r], wk);
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) col[e] += mavp_term<OP>(buf[r][e], wj);
+                } else {
+                    float tr[8];
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        const int64_t k = kl + e;
+                        tr[e] = k >= j ? mavp_term<OP>(buf[r][e], wk[e]) : 0.0f;
+                        if (k > j) col[e] += mavp_term<OP>(buf[r][e], wj);
+                    }
+                    pr[4 * h + r] = tree_sum(tr);
+                }
+            }
+        };
+        // the 8 row partials of a group across the warp: reduce-scatter butterfly (9 shuffles for 8
+        // rows); lanes with (lane & 3) == 0 hold row res_row_of<8>(lane) and store it
+        auto finish_group = [&](int rb) {
+            const float v = res_lane_reduce<8>(pr, lane);
+            const int ri = res_row_of<8>(lane);
+            if ((lane & 3) == 0 && rb + ri < rows) sym_st_keep(prow + sym_tile(j0 + rb + ri, nc), v, keep);
+        };
+        for (int rb = 0; rb < rows; rb += 8) {
+            load(a[1], rb + 4);
+            consume(a[0], rb, 0);
+            if (rb + 8 < rows) load(a[0], rb + 8);
+            consume(a[1], rb + 4, 1);
+            finish_group(rb);
+        }
+        if (live) {  // columns kl .. kl+7 lie in one 32-column tile
+            float* pc = sa.pcol + b * 32 + sym_tile(kl, nb);
+            sym_st4_keep(pc, col[0], col[1], col[2], col[3], keep);
+            sym_st4_keep(pc + 4, col[4], col[5], col[6], col[7], keep);
+        }
+        task = tlo + __shfl_sync(0xffffffffu, nxt, 0);
+    }
+}
+
+// ---- phase 2 of K2s: y_j of the owned rows [o0, o1) from the partials (SHARDED: only the partials of the
+// task range [tlo, thi); the others are skipped as zeros, which leaves the sums unchanged).  `subs`
+// threads per row (the most that fit the owned rows in one pass), consecutive threads on consecutive rows
+// (coalesced partial reads); sub k takes partials q = k, k + subs, ... in ascending order, 48 loads in
+// flight, each batch summed by a fixed fp32 pairwise tree and accumulated in fp64; the subs meet in shared
+// memory and are added in sub order.  out(j, v) receives fp32(y_j) (for the owner) .
+template <bool SHARDED, typename Out>
+__device__ __forceinline__ void sym_reduce(const SymArgs& sa, int64_t o0, int64_t o1, int64_t tlo, int64_t thi,
+                                           double* redp, Out out) {
+    const int64_t n = sa.it.n, nb = sym_nb(n), nc = sym_nc(n);
+    const int tid = threadIdx.x;
+    const int64_t rown = o1 - o0;
+    const int subs = rown * 8 <= kSymThreads ? 8 : (rown * 4 <= kSymThreads ? 4 : (rown * 2 <= kSymThreads ? 2 : 1));
+    const int rpp = kSymThreads / subs;  // rows per pass
+    const int rl = tid % rpp, sub = tid / rpp;
+    for (int64_t pbase = o0; pbase < o1; pbase += rpp) {
+        const int64_t j = pbase + rl;
+        double acc = 0.0;
+        if (j < o1) {
+            const int64_t cj = j / kSymCC, bj = j / kSymRB;
+            const int64_t nrow = nc - cj, ntot = nrow + bj + 1;
+            const float* prow_j = sa.prow + sym_tile(j, nc) + cj * 32;  // + q * 32
+            const float* pcol_j = sa.pcol + sym_tile(j, nb);            // + b * 32
+            SymValid vr{cj, nc, 0, bj + 1};
+            if constexpr (SHARDED) vr = sym_valid(j, n, tlo, thi);
+            for (int64_t q0 = sub; q0 < ntot; q0 += 48 * subs) {
+                float v[48];
+#pragma unroll
+                for (int u = 0; u < 48; ++u) {
+                    const int64_t q = q0 + (int64_t)u * subs;
+                    if constexpr (SHARDED) {
+                        const bool isrow = q < nrow;
+                        const int64_t x = isrow ? cj + q : q - nrow;
+                        const bool ok = q < ntot && (isrow ? (x >= vr.c_lo && x < vr.c_hi) : (x >= vr.b_lo && x < vr.b_hi));
+                        v[u] = ok ? (isrow ? __ldcg(prow_j + q * 32) : __ldcg(pcol_j + (q - nrow) * 32)) : 0.0f;
+                    } else {
+                        v[u] = q < ntot ? (q < nrow ? __ldcg(prow_j + q * 32) : __ldcg(pcol_j + (q - nrow) * 32))
+                                        : 0.0f;
+                    }
+                }
+                // pairwise fp32 tree over the batch (6 levels), one fp64 add per batch: a per-element
+                // fp64 conversion (F2F, a slow pipe) made this phase F2F-bound
+#pragma unroll
+                for (int h = 24; h >= 3; h >>= 1)
+#pragma unroll
+                    for (int u = 0; u < h; ++u) v[u] = v[2 * u] + v[2 * u + 1];
+                acc += (double)((v[0] + v[1]) + v[2]);
+            }
+        }
+        redp[tid] = acc;
+        __syncthreads();
+        if (tid < rpp && pbase + tid < o1) {
+            double tot = 0.0;
+            for (int k = 0; k < subs; ++k) tot += redp[k * rpp + tid];
+            out(pbase + tid, (float)tot);
+        }
+        __syncthreads();
+    }
+}
+
+// sum of the G fp64 slots of a parity in a fixed order (warp 0 lane-strided, butterfly), broadcast
+__device__ __forceinline__ double sym_slots_sum(const double* slots, double* red, int k) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (warp == 0) {
+        double pp = 0.0;
+        for (int cc = lane; cc < (int)gridDim.x; cc += 32) pp += __ldcg(slots + cc);
+        pp = warp_sum(pp);
+        if (lane == 0) red[k] = pp;
+    }
+    __syncthreads();
+    const double v = red[k];
+    __syncthreads();
+    return v;
+}
+
 template <int OP>
 __global__ void __launch_bounds__(kSymThreads, 1) k_iterate_sym(SymArgs sa) {
     extern __shared__ __align__(16) float sm_[];
@@ -161,8 +410,8 @@ __global__ void __launch_bounds__(kSymThreads, 1) k_iterate_sym(SymArgs sa) {
     double* red = reinterpret_cast<double*>(reinterpret_cast<char*>(sm_) + kSymSmemRegion);
     const IterArgs& p = sa.it;
     const int64_t n = p.n;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t nb = sym_nb(n), nc = sym_nc(n), ntasks = sym_task_start(nb, nc);
+    const int tid = threadIdx.x;
+    const int64_t ntasks = sym_task_start(sym_nb(n), sym_nc(n));
     const int64_t o0 = sym_own_start(blockIdx.x, gridDim.x, n), o1 = sym_own_start(blockIdx.x + 1, gridDim.x, n);
     unsigned long long* wtag = sa.wtag;  // [2][n] by iteration parity
     float* yg = sa.yg;
@@ -181,115 +430,10 @@ __global__ void __launch_bounds__(kSymThreads, 1) k_iterate_sym(SymArgs sa) {
         unsigned long long* wnext = wtag + ((t + 1) & 1) * n;
         const uint32_t tag = (uint32_t)t + 1u;
         SYM_STAMP(t, 0);
-        // ---- phase 1: upper-triangle tasks (w_t from the tagged words; polled until current).
-        // Tasks are taken dynamically from a per-iteration counter (SMs stream at different rates: a static
-        // deal left the fastest CTAs idle ~40 us per iteration); a task's partials do not depend on which
-        // warp computes them, so the results stay bitwise reproducible.  The next task index is fetched
-        // while the current task streams.
-        unsigned int* ctr = p.bar + 32 + (t & 1);  // two counters at byte 128 of the zeroed header
-        auto fetch = [&]() -> unsigned int {
-            unsigned int v = 0;
-            if (lane == 0) v = atomicAdd(ctr, 1u);
-            return v;
-        };
-        unsigned int nxt = fetch();
-        for (int64_t task = __shfl_sync(0xffffffffu, nxt, 0); task < ntasks;) {
-            nxt = fetch();
-            int64_t lo = 0, hi = nb - 1;  // row block: last b with start(b) <= task
-            while (lo < hi) {
-                const int64_t mid = (lo + hi + 1) >> 1;
-                if (sym_task_start(mid, nc) <= task) lo = mid;
-                else hi = mid - 1;
-            }
-            const int64_t b = lo, c = b / kSymCR + (task - sym_task_start(b, nc));
-            const int64_t j0 = b * kSymRB, j1 = min(n, j0 + kSymRB), c0 = c * kSymCC;
-            const int64_t kl = c0 + 8 * lane;  // this lane's first column
-            const bool live = kl < n;          // n % 8 == 0: a lane is all in or all out
-            const bool diag = c0 < j1;         // some element with k <= j: masked path
-            const int rows = (int)(j1 - j0);
-            float* prow = sa.prow + c * 32;  // + sym_tile(j) for row j
-            const float* base = p.A + j0 * p.lda + kl;
-            float a[2][4][8];
-            auto load = [&](float (&buf)[4][8], int rb) {
-#pragma unroll
-                for (int r = 0; r < 4; ++r) {
-                    // (on diagonal tasks a lane whose 8 columns all lie below the row's diagonal loads nothing:
-                    // every one of its terms is masked)
-                    if (live && rb + r < rows && kl + 7 >= j0 + rb + r)
-                        ld_stream<8, 0>(base + (int64_t)(rb + r) * p.lda, buf[r]);
-                    else
-#pragma unroll
-                        for (int e = 0; e < 8; ++e) buf[r][e] = 0.0f;
-                }
-            };
-            load(a[0], 0);  // A does not depend on w: in flight while the w words are polled
-            float wk[8], col[8];
-            {
-                int64_t idx[8];
-#pragma unroll
-                for (int e = 0; e < 8; ++e) idx[e] = live ? kl + e : -1;
-                sym_wait_words<8>(wcur, idx, tag, wk);
-            }
-#pragma unroll
-            for (int e = 0; e < 8; ++e) col[e] = 0.0f;
-            __syncwarp();  // the previous task's reads of wj_s are done
-            {
-                int64_t idx[kSymRB / 32];
-                float v[kSymRB / 32];
-#pragma unroll
-                for (int i = 0; i < kSymRB / 32; ++i) idx[i] = (32 * i + lane < rows) ? j0 + 32 * i + lane : -1;
-                sym_wait_words<kSymRB / 32>(wcur, idx, tag, v);
-#pragma unroll
-                for (int i = 0; i < kSymRB / 32; ++i) wj_s[32 * i + lane] = v[i];
-            }
-            __syncwarp();
-            // partial layouts are row-tiled ([j / 32][chunk or block][j % 32]): phase 2 reads all partials of
-            // 32 consecutive rows as one contiguous run
-            float pr[8];  // per-lane row partials of the current 8-row group
-            // rows rb .. rb+3 of the group -> pr[h*4 .. h*4+3] (rows beyond the task add zeros and are
-            // never stored)
-            auto consume = [&](const float (&buf)[4][8], int rb, int h) {
-#pragma unroll
-                for (int r = 0; r < 4; ++r) {
-                    const int64_t j = j0 + rb + r;
-                    const float wj = wj_s[rb + r];
-                    if (!diag) {
-                        pr[4 * h + r] = sym_tree8<OP>(buf[r], wk);
-#pragma unroll
-                        for (int e = 0; e < 8; ++e) col[e] += mavp_term<OP>(buf[r][e], wj);
-                    } else {
-                        float tr[8];
-#pragma unroll
-                        for (int e = 0; e < 8; ++e) {
-                            const int64_t k = kl + e;
-                            tr[e] = k >= j ? mavp_term<OP>(buf[r][e], wk[e]) : 0.0f;
-                            if (k > j) col[e] += mavp_term<OP>(buf[r][e], wj);
-                        }
-                        pr[4 * h + r] = tree_sum(tr);
-                    }
-                }
-            };
-            // the 8 row partials of a group across the warp: reduce-scatter butterfly (9 shuffles for 8
-            // rows); lanes with (lane & 3) == 0 hold row res_row_of<8>(lane) and store it
-            auto finish_group = [&](int rb) {
-                const float v = res_lane_reduce<8>(pr, lane);
-                const int ri = res_row_of<8>(lane);
-                if ((lane & 3) == 0 && rb + ri < rows) sym_st_keep(prow + sym_tile(j0 + rb + ri, nc), v, keep);
-            };
-            for (int rb = 0; rb < rows; rb += 8) {
-                load(a[1], rb + 4);
-                consume(a[0], rb, 0);
-                if (rb + 8 < rows) load(a[0], rb + 8);
-                consume(a[1], rb + 4, 1);
-                finish_group(rb);
-            }
-            if (live) {  // columns kl .. kl+7 lie in one 32-column tile
-                float* pc = sa.pcol + b * 32 + sym_tile(kl, nb);
-                sym_st4_keep(pc, col[0], col[1], col[2], col[3], keep);
-                sym_st4_keep(pc + 4, col[4], col[5], col[6], col[7], keep);
-            }
-            task = __shfl_sync(0xffffffffu, nxt, 0);
-        }
+        // ---- phase 1: upper-triangle tasks from a per-iteration counter (SMs stream at different rates: a
+        // static deal left the fastest CTAs idle ~40 us per iteration); a task's partials do not depend on
+        // which warp computes them, so the results stay bitwise reproducible
+        sym_tasks<OP>(sa, p.A, 0, 0, ntasks, p.bar + 32 + (t & 1), wcur, tag, wj_s, keep);
         SYM_STAMP(t, 1);
         grid_barrier(p.bar, ++epoch * gridDim.x);
         SYM_STAMP(t, 2);
@@ -298,18 +442,7 @@ __global__ void __launch_bounds__(kSymThreads, 1) k_iterate_sym(SymArgs sa) {
         // ---- the lagged stop test: delta_{t-1} (partials written before this barrier) decides whether w_t
         // is the result; this iteration's task partials are then discarded
         if (t > 0) {
-            double delta;
-            {
-                if (warp == 0) {
-                    double pp = 0.0;
-                    for (int cc = lane; cc < (int)gridDim.x; cc += 32) pp += __ldcg(slotD + ((t - 1) & 1) * gridDim.x + cc);
-                    pp = warp_sum(pp);
-                    if (lane == 0) red[33] = pp;
-                }
-                __syncthreads();
-                delta = red[33];
-                __syncthreads();
-            }
+            const double delta = sym_slots_sum(slotD + ((t - 1) & 1) * gridDim.x, red, 33);
             if (blockIdx.x == 0 && tid == 0 && p.deltas) p.deltas[t - 1] = (float)delta;
             done = t;
             if (p.tol > 0.0f && delta < (double)p.tol) {
@@ -317,73 +450,19 @@ __global__ void __launch_bounds__(kSymThreads, 1) k_iterate_sym(SymArgs sa) {
                 break;
             }
         }
-        // ---- phase 2: y_j of the owned rows.  `subs` threads per row (the most that fit the owned rows in
-        // one pass), consecutive threads on consecutive rows (coalesced partial reads); sub k takes partials
-        // q = k, k + subs, ... in ascending order, 48 loads in flight, each batch summed
-        // by a fixed fp32 pairwise tree and accumulated in fp64; the subs meet in shared memory
-        // and are added in sub order.
+        // ---- phase 2: y_j of the owned rows, |y| partial
         double abs_part = 0.0;
-        {
-            double* redp = reinterpret_cast<double*>(sm_);  // [kSymThreads] (aliases wj_s: phase 1 is over)
-            const int64_t rown = o1 - o0;
-            const int subs = rown * 8 <= kSymThreads ? 8 : (rown * 4 <= kSymThreads ? 4 : (rown * 2 <= kSymThreads ? 2 : 1));
-            const int rpp = kSymThreads / subs;  // rows per pass
-            const int rl = tid % rpp, sub = tid / rpp;
-            for (int64_t pbase = o0; pbase < o1; pbase += rpp) {
-                const int64_t j = pbase + rl;
-                double acc = 0.0;
-                if (j < o1) {
-                    const int64_t cj = j / kSymCC, bj = j / kSymRB;
-                    const int64_t nrow = nc - cj, ntot = nrow + bj + 1;
-                    const float* prow_j = sa.prow + sym_tile(j, nc) + cj * 32;  // + q * 32
-                    const float* pcol_j = sa.pcol + sym_tile(j, nb);            // + b * 32
-                    for (int64_t q0 = sub; q0 < ntot; q0 += 48 * subs) {
-                        float v[48];
-#pragma unroll
-                        for (int u = 0; u < 48; ++u) {
-                            const int64_t q = q0 + (int64_t)u * subs;
-                            v[u] = q < ntot ? (q < nrow ? __ldcg(prow_j + q * 32) : __ldcg(pcol_j + (q - nrow) * 32))
-                                            : 0.0f;
-                        }
-                        // pairwise fp32 tree over the batch (6 levels), one fp64 add per batch: a per-element
-                        // fp64 conversion (F2F, a slow pipe) made this phase F2F-bound
-#pragma unroll
-                        for (int h = 24; h >= 3; h >>= 1)
-#pragma unroll
-                            for (int u = 0; u < h; ++u) v[u] = v[2 * u] + v[2 * u + 1];
-                        acc += (double)((v[0] + v[1]) + v[2]);
-                    }
-                }
-                redp[tid] = acc;
-                __syncthreads();
-                if (tid < rpp && pbase + tid < o1) {
-                    double tot = 0.0;
-                    for (int k = 0; k < subs; ++k) tot += redp[k * rpp + tid];
-                    const float v = (float)tot;
-                    yg[pbase + tid] = v;
-                    abs_part += norm_part<OP>(v);
-                }
-                __syncthreads();
-            }
-        }
+        sym_reduce<false>(sa, o0, o1, 0, ntasks, reinterpret_cast<double*>(sm_), [&](int64_t j, float v) {
+            yg[j] = v;
+            abs_part += norm_part<OP>(v);
+        });
         const double cta_abs = block_sum(abs_part, red);  // its barriers also publish yg to this CTA
         if (tid == 0) slotA[(t & 1) * gridDim.x + blockIdx.x] = cta_abs;
         SYM_STAMP(t, 3);
         grid_barrier(p.bar, ++epoch * gridDim.x);
         SYM_STAMP(t, 4);
         // ---- s_t: the same fixed-order fp64 sum in every CTA
-        double sd;
-        {
-            if (warp == 0) {
-                double pp = 0.0;
-                for (int cc = lane; cc < (int)gridDim.x; cc += 32) pp += __ldcg(slotA + (t & 1) * gridDim.x + cc);
-                pp = warp_sum(pp);
-                if (lane == 0) red[32] = pp;
-            }
-            __syncthreads();
-            sd = norm_final<OP>(red[32]);
-            __syncthreads();
-        }
+        const double sd = norm_final<OP>(sym_slots_sum(slotA + (t & 1) * gridDim.x, red, 32));
         if (!(sd > 0.0) || isinf(sd)) {  // uniform across the grid
             status = (sd == 0.0) ? kStDegenerate : kStNonfinite;
             done = t;
@@ -405,12 +484,8 @@ __global__ void __launch_bounds__(kSymThreads, 1) k_iterate_sym(SymArgs sa) {
     }
     if (!stopped) {  // ran all iterations: delta of the last one
         grid_barrier(p.bar, ++epoch * gridDim.x);
-        if (warp == 0) {
-            double pp = 0.0;
-            for (int cc = lane; cc < (int)gridDim.x; cc += 32) pp += __ldcg(slotD + ((t - 1) & 1) * gridDim.x + cc);
-            pp = warp_sum(pp);
-            if (blockIdx.x == 0 && lane == 0 && p.deltas) p.deltas[t - 1] = (float)pp;
-        }
+        const double delta = sym_slots_sum(slotD + ((t - 1) & 1) * gridDim.x, red, 33);
+        if (blockIdx.x == 0 && tid == 0 && p.deltas) p.deltas[t - 1] = (float)delta;
         done = t;
     }
     // w_done (on a degenerate stop: the last good iterate), from the owned tagged words

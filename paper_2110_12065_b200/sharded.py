@@ -13,12 +13,14 @@ The local mat-vec, the all-gather and the normalisation are injectable so that t
 partition, the gather order, the per-rank agreement) is tested with gloo on CPU (tests/test_dist_host.py).
 The product path passes the CUDA entry points and torch.distributed over NCCL.
 
-`P2PExchange` + `iterate_sharded_p2p` are the fused alternative (K2p, csrc/p2p.cuh): ONE cooperative
-launch per rank runs every iteration and the y exchange happens inside it — each CTA stores its rows of
-y straight into every rank's exchange buffer over NVLink (CUDA IPC mappings), release-adds the peers'
-arrival flags at system scope and waits for all of them; no NCCL call on the data path.  The host side
-here only sets up the mappings once (IPC handles all-gathered over torch.distributed) and carries the
-global iteration epoch / flag base from call to call.
+`P2PExchange` + `iterate_sharded_p2p` / `iterate_sym_sharded_p2p` are the fused paths (K2p / K2sp,
+csrc/p2p.cuh): ONE cooperative launch per rank runs every iteration and the exchange happens inside it —
+each rank stores its share straight into every rank's exchange buffer over NVLink (CUDA IPC mappings),
+then one thread release-adds every rank's arrival flag at system scope and all CTAs wait for all of them;
+no NCCL call on the data path.  K2sp (the N > 1 default for symmetric A) splits K2s's upper-triangle task
+list over the ranks and exchanges partial y vectors.  The host side here only sets up the mappings once
+(IPC handles and SM counts all-gathered over torch.distributed) and carries the global iteration epoch /
+flag base from call to call.
 """
 from __future__ import annotations
 
@@ -149,15 +151,19 @@ def iterate_sharded(A_local, n: int, b0, iters: int, tol: float = 0.0, op: int =
 
 
 class P2PExchange:
-    """The per-rank exchange buffer of K2p and its peers' IPC mappings.
+    """The per-rank exchange buffer of K2p / K2sp and its peers' IPC mappings.
 
     lib: the loaded libmapi (or a stand-in with the same six entry points, for host-logic tests);
     allgather(bytes) -> list of every rank's bytes, in rank order (torch.distributed by default).
+    `grid` is the CTA count every rank launches with: the minimum of the ranks' SM counts (`sms`, default:
+    the device's), agreed here once, because the kernels' row ownership and summation orders depend on it.
     `epoch` / `flag_base` carry the global iteration index and the own flag value across calls; they
-    advance by `published` and `published * world * grid` after each call, identically on every rank.
+    advance by `published` and `published * world` after each call (one arrival per rank per iteration),
+    identically on every rank.
     """
 
-    def __init__(self, n: int, rank: int, world: int, lib=None, allgather=None, group=None, device=None):
+    def __init__(self, n: int, rank: int, world: int, lib=None, allgather=None, group=None, device=None,
+                 sms: int = None):
         import ctypes
 
         if lib is None:
@@ -166,13 +172,21 @@ class P2PExchange:
             lib = load()
         self.lib, self.n, self.rank, self.world = lib, n, rank, world
         self.bytes = int(lib.mapi_p2p_exchange_bytes(n, world))
+        if allgather is None:
+            allgather = _dist_allgather_bytes(group, device)
+        if sms is None:
+            import torch
+
+            sms = torch.cuda.get_device_properties(device if device is not None else 0).multi_processor_count
+        counts = [int.from_bytes(b, "little") for b in allgather(int(sms).to_bytes(8, "little"))]
+        if len(counts) != world:
+            raise ValueError(f"expected {world} SM counts, got {len(counts)}")
+        self.grid = min(min(counts), 1024)
         ptr = ctypes.c_void_p()
         self._check(lib.mapi_p2p_alloc(self.bytes, ctypes.byref(ptr)))
         self.own = int(ptr.value)
         handle = ctypes.create_string_buffer(64)
         self._check(lib.mapi_ipc_get_handle(self.own, handle))
-        if allgather is None:
-            allgather = _dist_allgather_bytes(group, device)
         handles = allgather(bytes(handle.raw))
         if len(handles) != world:
             raise ValueError(f"expected {world} handles, got {len(handles)}")
@@ -201,9 +215,9 @@ class P2PExchange:
 
             raise MapiError(st, self.lib.mapi_last_error_message().decode(errors="replace"))
 
-    def advance(self, published: int, grid: int):
+    def advance(self, published: int):
         self.epoch += published
-        self.flag_base += published * self.world * grid
+        self.flag_base += published * self.world
 
     def close(self):
         for a in self.opened:
@@ -236,7 +250,7 @@ def iterate_sharded_p2p(A_local, n: int, row0: int, b0, iters: int, exchange: P2
 
     import torch
 
-    from . import MapiError, STATUS, WS_ITERATE_SHARDED
+    from . import MapiError, WS_ITERATE_SHARDED
 
     lib = exchange.lib
     dev = A_local.device
@@ -253,11 +267,72 @@ def iterate_sharded_p2p(A_local, n: int, row0: int, b0, iters: int, exchange: P2
     sp = torch.cuda.current_stream(dev).cuda_stream
     st = lib.mapi_iterate_sharded(op, A_local.data_ptr(), m, n, A_local.stride(0), row0, b0.data_ptr(), iters,
                                   float(tol), exchange.rank, exchange.world, exchange.peers_dev.data_ptr(),
-                                  exchange.epoch, exchange.flag_base, w.data_ptr(),
+                                  exchange.epoch, exchange.flag_base, exchange.grid, w.data_ptr(),
                                   None if norms is None else norms.data_ptr(),
                                   None if deltas is None else deltas.data_ptr(), ctypes.byref(done),
                                   ctypes.byref(published), ctypes.byref(grid), ws.data_ptr(), ws.numel(), sp)
-    exchange.advance(published.value, grid.value)
+    exchange.advance(published.value)
+    if st:
+        raise MapiError(st, lib.mapi_last_error_message().decode(errors="replace"), done.value)
+    k = done.value
+    return ShardedResult(w, norms[:k] if norms is not None else None, deltas[:k] if deltas is not None else None, k)
+
+
+# ------------------------------------------------------------------------------ sharded symmetric (K2sp)
+
+
+def sym_shard(n: int, rank: int, world: int, lib=None):
+    """(row_lo, row_hi, task_lo, task_hi) of `rank` for K2sp: the contiguous slice of K2s's upper-triangle
+    task list it runs and the rows those tasks read (mapi_sym_shard_rows; host-only arithmetic)."""
+    import ctypes
+
+    if lib is None:
+        from . import load
+
+        lib = load()
+    out = [ctypes.c_int64() for _ in range(4)]
+    st = lib.mapi_sym_shard_rows(n, rank, world, *[ctypes.byref(o) for o in out])
+    if st:
+        from . import MapiError
+
+        raise MapiError(st, lib.mapi_last_error_message().decode(errors="replace"))
+    return tuple(int(o.value) for o in out)
+
+
+def iterate_sym_sharded_p2p(A_local, row_lo: int, row_hi: int, n: int, b0, iters: int, exchange: P2PExchange,
+                            tol: float = 0.0, op: int = 0, want_trace: bool = True, ws=None) -> ShardedResult:
+    """MAPI on a symmetric A whose upper-triangle task list is split over the ranks (K2sp,
+    mapi_iterate_sym_sharded): A_local holds rows [row_lo, row_hi) = sym_shard(n, rank, world)[:2] (full
+    rows; only their upper-triangle part is read).  Every rank returns the same full w."""
+    import ctypes
+
+    import torch
+
+    from . import MapiError, WS_ITERATE_SYM
+
+    lib = exchange.lib
+    dev = A_local.device
+    if A_local.dim() != 2 or A_local.stride(1) != 1 or A_local.dtype != torch.float32:
+        raise ValueError("A_local must be a row-major fp32 CUDA tensor")
+    if A_local.shape[0] != row_hi - row_lo:
+        raise ValueError(f"A_local has {A_local.shape[0]} rows; the shard holds {row_hi - row_lo}")
+    if exchange.peers_dev is None:
+        exchange.peers_dev = torch.tensor(exchange.peer_addrs, dtype=torch.int64, device=dev)
+    w = torch.empty(n, dtype=torch.float32, device=dev)
+    norms = torch.zeros(iters, dtype=torch.float32, device=dev) if want_trace else None
+    deltas = torch.zeros(iters, dtype=torch.float32, device=dev) if want_trace else None
+    need = int(lib.mapi_workspace_size(WS_ITERATE_SYM, n, 0, 0))
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(need, dtype=torch.uint8, device=dev)
+    done, published, grid = ctypes.c_int32(0), ctypes.c_int32(0), ctypes.c_int32(0)
+    sp = torch.cuda.current_stream(dev).cuda_stream
+    st = lib.mapi_iterate_sym_sharded(op, A_local.data_ptr(), row_lo, row_hi, n, A_local.stride(0), b0.data_ptr(),
+                                      iters, float(tol), exchange.rank, exchange.world,
+                                      exchange.peers_dev.data_ptr(), exchange.epoch, exchange.flag_base,
+                                      exchange.grid, w.data_ptr(), None if norms is None else norms.data_ptr(),
+                                      None if deltas is None else deltas.data_ptr(), ctypes.byref(done),
+                                      ctypes.byref(published), ctypes.byref(grid), ws.data_ptr(), ws.numel(), sp)
+    exchange.advance(published.value)
     if st:
         raise MapiError(st, lib.mapi_last_error_message().decode(errors="replace"), done.value)
     k = done.value

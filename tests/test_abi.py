@@ -99,7 +99,8 @@ def test_validation_before_device(lib):
     sh = lambda **kw: lib.mapi_iterate_sharded(  # noqa: E731
         kw.get("op", 0), kw.get("A", fake), kw.get("m", 256), kw.get("n", 512), kw.get("lda", 512),
         kw.get("row0", 0), fake, kw.get("iters", 5), kw.get("tol", 0.0), kw.get("rank", 0), kw.get("world", 2),
-        kw.get("peers", fake), 0, 0, fake, None, None, None, None, None, fake, kw.get("ws_bytes", 256), None)
+        kw.get("peers", fake), 0, 0, kw.get("grid", 8), fake, None, None, None, None, None, fake,
+        kw.get("ws_bytes", 1 << 20), None)
     assert sh(peers=None) == 1 and "NULL" in _err(lib)
     assert sh(world=0) == 3 and "world" in _err(lib)
     assert sh(rank=2) == 3 and "rank 2" in _err(lib)
@@ -109,6 +110,15 @@ def test_validation_before_device(lib):
     assert sh(iters=0) == 3 and "iters" in _err(lib)
     assert sh(ws_bytes=16) == 7
     assert sh(op=5) == 3
+    assert sh(grid=0) == 3 and "explicit grid" in _err(lib)  # world > 1 must pass the agreed grid
+    assert sh(grid=5000) == 3
+    # sharded symmetric (K2sp): the held rows must be the shard's, before any CUDA call
+    ssh = lambda **kw: lib.mapi_iterate_sym_sharded(  # noqa: E731
+        0, fake, kw.get("lo", 0), kw.get("hi", 1), kw.get("n", 8192), 8192, fake, 5, 0.0, kw.get("rank", 0),
+        kw.get("world", 2), fake, 0, 0, 8, fake, None, None, None, None, None, fake, 1 << 30, None)
+    assert ssh() == 2 and "mapi_sym_shard_rows" in _err(lib)
+    assert ssh(n=1001) == 2
+    assert ssh(world=0) == 3
     # pipelined host problems
     arr = (ctypes.c_void_p * 1)(fake.value)
     st = lib.mapi_iterate_host_many(0, 0, arr, 4, 4, arr, 5, 0.0, arr, None, None, None, fake, 1 << 20, None)
@@ -164,12 +174,13 @@ def test_pack_upper_layout():
 
 
 def test_p2p_exchange_layout_and_new_workspaces(lib):
-    """Exchange buffer = 256 B flag header + y for two parities + fp64 partial slots (2 x world x 1024)."""
+    """Exchange buffer = 256 B flag header + y (fp32) for two parities x world source ranks + fp64 rank
+    totals (2 x world); the K2p workspace holds its status header and the per-CTA partials (2 x 1024)."""
     al = lambda b: (b + 255) // 256 * 256  # noqa: E731
     for n, world in ((4096, 2), (32768, 8), (1000, 1)):
-        assert lib.mapi_p2p_exchange_bytes(n, world) == 256 + al(8 * n) + al(16 * world * 1024)
+        assert lib.mapi_p2p_exchange_bytes(n, world) == 256 + al(8 * world * n) + al(16 * world)
     assert lib.mapi_p2p_exchange_bytes(100, 0) == 0
-    assert lib.mapi_workspace_size(m.WS_ITERATE_SHARDED, 0, 0, 0) == 256
+    assert lib.mapi_workspace_size(m.WS_ITERATE_SHARDED, 0, 0, 0) == 256 + 16 * 1024
     one = lib.mapi_workspace_size(m.WS_ITERATE_HOST, 1024, 1024, 50)
     many = lib.mapi_workspace_size(m.WS_ITERATE_HOST_MANY, 1024, 1024, 50)
     assert many > one and many >= 2 * 4 * 1024 * 1024  # two A slots

@@ -193,11 +193,11 @@ def _p2p_setup_worker(rank, world, port, q):
         return out
 
     lib = _FakeP2PLib(rank)
-    ex = P2PExchange(96, rank, world, lib=lib, allgather=allgather)
+    ex = P2PExchange(96, rank, world, lib=lib, allgather=allgather, sms=148 - 4 * rank)
     peers = list(ex.peer_addrs)
-    ex.advance(7, 148)
-    ex.advance(3, 148)
-    adv = (ex.epoch, ex.flag_base)
+    ex.advance(7)
+    ex.advance(3)
+    adv = (ex.epoch, ex.flag_base, ex.grid)
     ex.close()
     q.put((rank, peers, adv, sorted(lib.closed), lib.freed))
     tdist.barrier()
@@ -205,9 +205,10 @@ def _p2p_setup_worker(rank, world, port, q):
 
 
 def test_p2p_exchange_setup_gloo_world3():
-    """K2p host set-up with three ranks: IPC handles all-gathered in rank order, peers[rank] is the
-    own buffer and peers[q] the mapping of rank q's handle, the epoch / flag base advance by the
-    published iterations (x world x grid), and close() unmaps every peer and frees the own buffer."""
+    """K2p / K2sp host set-up with three ranks: IPC handles all-gathered in rank order, peers[rank] is the
+    own buffer and peers[q] the mapping of rank q's handle, every rank agrees on the same grid (the minimum
+    SM count), the epoch / flag base advance by the published iterations (x world: one arrival per rank per
+    iteration), and close() unmaps every peer and frees the own buffer."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
@@ -223,6 +224,137 @@ def test_p2p_exchange_setup_gloo_world3():
         peers, adv, closed, freed = out[r]
         own = 0x100000 * (r + 1)
         assert peers == [own if p == r else 0xA0000000 + p + 1 for p in range(world)]
-        assert adv == (10, 10 * world * 148)
+        assert adv == (10, 10 * world, 148 - 4 * (world - 1))
         assert closed == sorted(0xA0000000 + p + 1 for p in range(world) if p != r)
         assert freed == [own]
+
+
+# ------------------------------------------------- sharded symmetric K2sp: the task / row partition on CPU
+
+
+def _sym_lib():
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import paper_2110_12065_b200 as m
+
+    m.build()
+    return m.load()
+
+
+def _task_start(b, nc):  # sum_{b' < b} (nc - b' // 2): an independent restatement of the task numbering
+    return sum(nc - bb // 2 for bb in range(b))
+
+
+def _valid(lib, n, rank, world, j):
+    import ctypes
+
+    out = (ctypes.c_int64 * 4)()
+    assert lib.mapi_sym_shard_valid(n, rank, world, j, out) == 0
+    return tuple(out)
+
+
+def test_sym_shard_partition():
+    """K2sp's split of K2s's upper-triangle task list (mapi_sym_shard_rows / mapi_sym_shard_valid, host-only
+    C): the ranks' task ranges tile [0, T); each rank's held rows contain every strip its tasks read; and for
+    every row j the ranks' valid row-partial chunks and column-partial blocks are disjoint, cover
+    [c(j), nc) and [0, b(j)], and are exactly the partials of the tasks the rank owns (checked against an
+    independent enumeration of the task indices)."""
+    from paper_2110_12065_b200.sharded import sym_shard
+
+    lib = _sym_lib()
+    RB, CC = 128, 256
+    for n in (8, 1000, 8192, 33000):
+        nb, nc = -(-n // RB), -(-n // CC)
+        T = _task_start(nb, nc)
+        for world in (1, 2, 3, 8):
+            shards = [sym_shard(n, r, world, lib) for r in range(world)]
+            assert shards[0][2] == 0 and shards[-1][3] == T
+            for r in range(world - 1):
+                assert shards[r][3] == shards[r + 1][2]
+            starts = [_task_start(b, nc) for b in range(nb + 1)]
+            owner = {}
+            for r, (lo, hi, tlo, thi) in enumerate(shards):
+                for b in range(nb):
+                    for c in range(b // 2, nc):
+                        t = starts[b] + c - b // 2
+                        if tlo <= t < thi:
+                            owner[(b, c)] = r
+                            assert lo <= b * RB and min(n, (b + 1) * RB) <= hi, (n, world, r, b)
+            rows = range(n) if n <= 1000 else list(range(0, n, 97)) + [n - 1]
+            for j in rows:
+                B, C = j // RB, j // CC
+                got = [_valid(lib, n, r, world, j) for r in range(world)]
+                for r, (clo, chi, blo, bhi) in enumerate(got):
+                    mine_c = {c for c in range(C, nc) if owner[(B, c)] == r}
+                    mine_b = {b for b in range(B + 1) if owner[(b, C)] == r}
+                    assert set(range(clo, chi)) == mine_c, (n, world, r, j)
+                    assert set(range(blo, bhi)) == mine_b, (n, world, r, j)
+
+
+def _sym_sharded_worker(rank, world, port, q):
+    import sys
+
+    import numpy as np
+    import torch
+    import torch.distributed as tdist
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    lib = _sym_lib()
+    n, RB, CC = 1000, 128, 256
+    r = np.random.default_rng(21)
+    G = r.standard_normal((n, n))
+    A = np.triu(G) + np.triu(G, 1).T
+    w = r.standard_normal(n)
+
+    def term(a, x):  # MAVP term, Eq. (3): sign(a x) min(|a|, |x|)
+        return np.sign(a * x) * np.minimum(np.abs(a), np.abs(x))
+
+    # this rank's partial y from the partials its tasks produce (row terms k >= j of its chunks, column terms
+    # k < j of its row blocks), reading only the upper triangle
+    y = np.zeros(n)
+    for j in range(n):
+        clo, chi, blo, bhi = _valid(lib, n, rank, world, j)
+        for c in range(clo, chi):
+            k = np.arange(max(j, c * CC), min(n, (c + 1) * CC))
+            y[j] += term(A[j, k], w[k]).sum()
+        for b in range(blo, bhi):
+            k = np.arange(b * RB, min(j, (b + 1) * RB))
+            y[j] += term(A[k, j], w[k]).sum()
+    t = torch.from_numpy(y)
+    tdist.all_reduce(t)  # the exchange step: the sum of the ranks' partial y vectors
+    q.put((rank, t.numpy().copy()))
+    tdist.barrier()
+    tdist.destroy_process_group()
+
+
+def test_sym_sharded_partials_gloo_world3():
+    """Three ranks each compute the partial y of their slice of the upper-triangle task list (the valid
+    ranges of mapi_sym_shard_valid); after the exchange (a sum over the ranks) every rank holds y = A (+) w of
+    the full symmetric matrix (oracle mat-vec), i.e. every MAVP term is produced by exactly one rank."""
+    import numpy as np
+
+    import oracle
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    world = 3
+    procs = [ctx.Process(target=_sym_sharded_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    n = 1000
+    r = np.random.default_rng(21)
+    G = r.standard_normal((n, n))
+    A = np.triu(G) + np.triu(G, 1).T
+    w = r.standard_normal(n)
+    ref = oracle.matvec(A, w)
+    for k in range(world):
+        np.testing.assert_array_equal(out[k], out[0])
+    np.testing.assert_allclose(out[0], ref, rtol=1e-12, atol=1e-9)

@@ -153,3 +153,77 @@ def test_p2p_world1_tol_stop_and_degenerate(mapi_lib):
         assert torch.equal(again.w, full.w)
     finally:
         ex.close()
+
+
+# ------------------------------------------------------------ sharded symmetric K2s (K2sp)
+
+
+def _sym(n, seed):
+    r = np.random.default_rng(seed)
+    G = r.standard_normal((n, n)).astype(np.float32) / 16
+    S = np.triu(G) + np.triu(G, 1).T
+    S[np.diag_indices(n)] += np.linspace(4.0, 1.0, n).astype(np.float32)
+    return S.astype(np.float32)
+
+
+@pytest.mark.parametrize("n,op", [(8192, 0), (2056, 0), (2056, 1), (2056, 2)])
+def test_sym_sharded_world1_bitwise_vs_k2s(mapi_lib, monkeypatch, n, op):
+    """With one rank K2sp runs K2s's whole task list, exchanges its partial y through its own buffer and sums
+    one partial: the iterates, norms and deltas are bitwise mapi_iterate_sym's (K2s).  The lower triangle is
+    NaN (never read); consecutive calls continue the exchange epoch."""
+    from paper_2110_12065_b200.sharded import iterate_sym_sharded_p2p, sym_shard
+
+    m = mapi_lib
+    monkeypatch.setenv("MAPI_SYM_PATH", "sym")
+    S = _sym(n, n)
+    dev = np.triu(S) + np.tril(np.full((n, n), np.nan, np.float32), -1)
+    A = torch.from_numpy(dev).cuda()
+    b0 = torch.full((n,), 1 / np.sqrt(n), device="cuda")
+    lo, hi, tlo, thi = sym_shard(n, 0, 1)
+    assert (lo, hi, tlo) == (0, n, 0)
+    ex = _p2p_exchange(n)
+    try:
+        res = iterate_sym_sharded_p2p(A[lo:hi], lo, hi, n, b0, 25, ex, op=op)
+        ref = m.iterate_sym(A, b0, 25, op=op)
+        assert res.iters_done == 25 and ex.epoch == 25
+        assert torch.equal(res.w, ref.w) and torch.equal(res.norms, ref.norms) and torch.equal(res.deltas, ref.deltas)
+        again = iterate_sym_sharded_p2p(A[lo:hi], lo, hi, n, b0, 25, ex, op=op)  # odd epoch parity now
+        assert torch.equal(again.w, ref.w) and ex.epoch == 50
+    finally:
+        ex.close()
+
+
+def test_sym_sharded_world1_tol_and_degenerate(mapi_lib, monkeypatch, orc):
+    """Tol stop (lagged one task phase, same outputs as K2s), the epoch advances by the published iterations,
+    a degenerate matrix stops with MAPI_ERR_DEGENERATE at iteration 0 (one published), T2 vs the oracle."""
+    from paper_2110_12065_b200.sharded import iterate_sym_sharded_p2p
+
+    m = mapi_lib
+    monkeypatch.setenv("MAPI_SYM_PATH", "sym")
+    n = 2048
+    S = _sym(n, 9)
+    A = torch.from_numpy(S).cuda()
+    b0_h = np.full(n, 1 / np.sqrt(n), np.float32)
+    b0 = torch.from_numpy(b0_h).cuda()
+    ex = _p2p_exchange(n)
+    try:
+        full = iterate_sym_sharded_p2p(A, 0, n, n, b0, 120, ex)
+        d = full.deltas.cpu().numpy()
+        tol = float(d[40]) * 1.0001
+        first = int(np.nonzero(d < tol)[0][0])
+        e0 = ex.epoch
+        res = iterate_sym_sharded_p2p(A, 0, n, n, b0, 120, ex, tol=tol)
+        ref = m.iterate_sym(A, b0, 120, tol=tol)
+        assert res.iters_done == ref.iters_done == first + 1 and ex.epoch == e0 + first + 1
+        assert torch.equal(res.w, ref.w) and torch.equal(res.deltas, full.deltas[: first + 1])
+        o = orc.mapi(S, b0_h, first + 1)
+        w = res.w.cpu().numpy().astype(np.float64)
+        _t2(w, o.w)
+        e1 = ex.epoch
+        with pytest.raises(m.MapiError) as ei:
+            iterate_sym_sharded_p2p(torch.zeros(n, n, device="cuda"), 0, n, n, b0, 10, ex)
+        assert ei.value.name == "MAPI_ERR_DEGENERATE" and ex.epoch == e1 + 1
+        again = iterate_sym_sharded_p2p(A, 0, n, n, b0, 120, ex)
+        assert torch.equal(again.w, full.w)
+    finally:
+        ex.close()
