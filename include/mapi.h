@@ -53,9 +53,10 @@ typedef enum {
 } mapi_status;
 
 /* MAPI_OP_MIN1: Eq.(3); MAPI_OP_MIN2: Eq.(4); MAPI_OP_DOT: the regular product of
- * Eq.(1), the RPI comparator: accepted by mapi_mavp_matvec, mapi_iterate(_host)
- * and mapi_pca_topk, where it also switches the normalisation to l2 (b <- Ab/||Ab||_2, norms[t] =
- * ||A w_t||_2); the batched, matmat and ranking entry points take MIN1/MIN2 only. */
+ * Eq.(1), the RPI comparator: accepted by mapi_mavp_matvec, mapi_iterate(_host,
+ * _sym, _sharded), mapi_iterate_batched and mapi_pca_topk, where it also switches the normalisation to l2
+ * (b <- Ab/||Ab||_2, norms[t] = ||A w_t||_2), and by mapi_rank_csr_plan (PageRank G w with the l1
+ * normalisation, reading R13); mapi_mavp_matmat and mapi_rank_csr take MIN1/MIN2 only. */
 typedef enum { MAPI_OP_MIN1 = 0, MAPI_OP_MIN2 = 1, MAPI_OP_DOT = 2 } mapi_op;
 
 /* Workspace query ids (first argument of mapi_workspace_size). */
@@ -240,8 +241,8 @@ mapi_status mapi_iterate_host_many_packed(int32_t op, int32_t count, const float
  * runs"; matrix extension P:69-70 with p = k columns), Y = A (op) W each iteration.
  * B0, W_out: k x n, vector-major (vector v at B0 + v*n).  norms, deltas: iters x k
  * (entry [t*k + v]), nullable.  iters_done (host, k entries, nullable): per-vector count; a
- * vector stops individually when its own delta < tol (tol > 0).  The call returns the worst
- * status over vectors.  Synchronises `stream`. */
+ * vector stops individually when its own delta < tol (tol > 0).  op MAPI_OP_DOT: k independent RPI runs
+ * (Eq. 1, l2 normalisation).  The call returns the worst status over vectors.  Synchronises `stream`. */
 mapi_status mapi_iterate_batched(int32_t op, const float *A, int64_t n, int64_t lda,
                                  const float *B0, int32_t k, int32_t iters, float tol, float *W_out,
                                  float *norms, float *deltas, int32_t *iters_done, void *ws,

@@ -1103,7 +1103,7 @@ mapi_status mapi_pca_topk(int32_t op, const float* C, int64_t n, int64_t ldc, in
 mapi_status mapi_iterate_batched(int32_t op, const float* A, int64_t n, int64_t lda, const float* B0, int32_t k,
                                  int32_t iters, float tol, float* W_out, float* norms, float* deltas,
                                  int32_t* iters_done, void* ws, size_t ws_bytes, mapi_stream_t stream) {
-    mapi_status st = validate_dense(op, A, n, lda, B0, iters, tol, W_out, ws, false);
+    mapi_status st = validate_dense(op, A, n, lda, B0, iters, tol, W_out, ws);
     if (st != MAPI_OK) return st;
     if (k < 1) return fail(MAPI_ERR_BAD_PARAM, "k (%d) must be >= 1", k);
     const size_t need = batched_ws_bytes(n, k);

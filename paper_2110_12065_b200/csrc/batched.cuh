@@ -143,10 +143,11 @@ __global__ void __launch_bounds__(kBThreads) k_batched_partial(const float* __re
     }
 }
 
-// Y[v][j] = sum_s part[s][v][j] (s ascending); colpart[v][blk] = sum_{j in blk} |Y[v][j]|.
+// Y[v][j] = sum_s part[s][v][j] (s ascending); colpart[v][blk] = sum_{j in blk} |Y[v][j]| (l1, MAPI) or
+// Y[v][j]^2 (sq: l2, the RPI comparator of Eq. 1).
 __global__ void __launch_bounds__(256) k_batched_reduce(int64_t n, int32_t kv, int ks,
                                                         const float* __restrict__ part, float* __restrict__ Y,
-                                                        float* __restrict__ colpart, int64_t rb) {
+                                                        float* __restrict__ colpart, int64_t rb, bool sq) {
     __shared__ float red[33];
     const int v = blockIdx.y;
     const int64_t j = (int64_t)blockIdx.x * 256 + threadIdx.x;
@@ -155,16 +156,17 @@ __global__ void __launch_bounds__(256) k_batched_reduce(int64_t n, int32_t kv, i
         for (int s = 0; s < ks; ++s) y += part[((int64_t)s * kv + v) * n + j];
         Y[(int64_t)v * n + j] = y;
     }
-    const float a = block_sum(fabsf(y), red);
+    const float a = block_sum(sq ? y * y : fabsf(y), red);
     if (threadIdx.x == 0) colpart[(int64_t)v * rb + blockIdx.x] = a;
 }
 
-// Per vector v (one CTA each): s = sum colpart (fixed order), W = Y / s, delta, trace, stop.
+// Per vector v (one CTA each): s = sum colpart (fixed order; sq: its square root, the l2 norm of RPI),
+// W = Y / s, delta, trace, stop.
 __global__ void __launch_bounds__(1024) k_batched_normalize(int64_t n, int32_t kv, int32_t t, float tol,
                                                             const float* __restrict__ Y,
                                                             const float* __restrict__ colpart, int64_t rb,
                                                             float* __restrict__ W, float* norms, float* deltas,
-                                                            int32_t* status, int32_t* stop) {
+                                                            int32_t* status, int32_t* stop, bool sq) {
     __shared__ float red[33];
     const int v = blockIdx.x;
     if (stop[v]) return;
@@ -175,7 +177,7 @@ __global__ void __launch_bounds__(1024) k_batched_normalize(int64_t n, int32_t k
         if (threadIdx.x == 0) red[32] = part;
     }
     __syncthreads();
-    const float s = red[32];
+    const float s = sq ? sqrtf(red[32]) : red[32];
     __syncthreads();
     if (!(s > 0.0f) || isinf(s)) {
         if (threadIdx.x == 0) {
@@ -437,10 +439,10 @@ __global__ void __launch_bounds__(SkCfg<TV>::threads, 1) k_batched_streamk(const
     cp_async_wait<0>();
 }
 
-// Y[v][j] = sum of the tile's partials in CTA order; colpart[v][blk] = sum |Y[v][j]| over 256 rows.
+// Y[v][j] = sum of the tile's partials in CTA order; colpart[v][blk] = sum |Y[v][j]| (sq: Y^2) over 256 rows.
 __global__ void __launch_bounds__(256) k_batched_reduce2(int64_t n, int32_t kv, StreamK plan, int G,
                                                          const float* __restrict__ part, float* __restrict__ Y,
-                                                         float* __restrict__ colpart, int64_t rb) {
+                                                         float* __restrict__ colpart, int64_t rb, bool sq) {
     __shared__ float red[33];
     const int v = blockIdx.y;
     const int64_t j = (int64_t)blockIdx.x * 256 + threadIdx.x;
@@ -454,7 +456,7 @@ __global__ void __launch_bounds__(256) k_batched_reduce2(int64_t n, int32_t kv, 
             y += part[((tile * kMaxParts + p) * kB2V + (v - vt * kB2V)) * kB2M + (j - rt * kB2M)];
         Y[(int64_t)v * n + j] = y;
     }
-    const float a = block_sum(fabsf(y), red);
+    const float a = block_sum(sq ? y * y : fabsf(y), red);
     if (threadIdx.x == 0) colpart[(int64_t)v * rb + blockIdx.x] = a;
 }
 
@@ -505,8 +507,9 @@ inline mapi_status batched_run(int32_t op, const float* A, int64_t n, int64_t ld
     // v2 (256 threads, 8x8 register tiles) is the default; MAPI_BATCHED_PATH=v3 selects the 512-thread
     // 8x4 variant with the fold in shared memory (measured 63.5% vs 64.5% of the FMNMX peak at cfg4)
     const bool v3 = env && strcmp(env, "v3") == 0;
-    auto k2 = op == 1 ? k_batched_streamk<1, 8> : k_batched_streamk<0, 8>;
-    auto k3 = op == 1 ? k_batched_streamk<1, 4> : k_batched_streamk<0, 4>;
+    auto k2 = op == 2 ? k_batched_streamk<2, 8> : (op == 1 ? k_batched_streamk<1, 8> : k_batched_streamk<0, 8>);
+    auto k3 = op == 2 ? k_batched_streamk<2, 4> : (op == 1 ? k_batched_streamk<1, 4> : k_batched_streamk<0, 4>);
+    const bool sq = op == 2;  // RPI: l2 normalisation (Eq. 1)
     const size_t sm2 = streamk_smem_bytes<8>(), sm3 = streamk_smem_bytes<4>();
     if (v2) {
         if ((e = cudaFuncSetAttribute(v3 ? k3 : k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(v3 ? sm3 : sm2))) !=
@@ -520,16 +523,18 @@ inline mapi_status batched_run(int32_t op, const float* A, int64_t n, int64_t ld
                 k3<<<plan.grid, SkCfg<4>::threads, sm3, s>>>(A, n, lda, B.W, k, plan, B.part);
             else
                 k2<<<plan.grid, SkCfg<8>::threads, sm2, s>>>(A, n, lda, B.W, k, plan, B.part);
-            k_batched_reduce2<<<gr, 256, 0, s>>>(n, k, plan, plan.grid, B.part, B.Y, B.colpart, B.rb);
+            k_batched_reduce2<<<gr, 256, 0, s>>>(n, k, plan, plan.grid, B.part, B.Y, B.colpart, B.rb, sq);
         } else {
-            if (op == 1)
+            if (op == 2)
+                k_batched_partial<2><<<gp, kBThreads, 0, s>>>(A, n, lda, B.W, k, kslice, B.part);
+            else if (op == 1)
                 k_batched_partial<1><<<gp, kBThreads, 0, s>>>(A, n, lda, B.W, k, kslice, B.part);
             else
                 k_batched_partial<0><<<gp, kBThreads, 0, s>>>(A, n, lda, B.W, k, kslice, B.part);
-            k_batched_reduce<<<gr, 256, 0, s>>>(n, k, ks, B.part, B.Y, B.colpart, B.rb);
+            k_batched_reduce<<<gr, 256, 0, s>>>(n, k, ks, B.part, B.Y, B.colpart, B.rb, sq);
         }
         k_batched_normalize<<<k, 1024, 0, s>>>(n, k, t, tol, B.Y, B.colpart, B.rb, B.W, norms, deltas, B.status,
-                                               B.stop);
+                                               B.stop, sq);
         launches.fetch_add(3, std::memory_order_relaxed);
         if ((e = cudaGetLastError()) != cudaSuccess) return batched_cuda_fail(e, "batched launch");
     }

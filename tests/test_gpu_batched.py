@@ -41,6 +41,30 @@ def test_batched_small(mapi_lib, orc, n, k, op):
         np.testing.assert_allclose(norms[:, v], ref.norms, rtol=1e-5)
 
 
+@pytest.mark.parametrize("n,k", [(300, 5), (1000, 64), (4100, 9)])
+def test_batched_rpi_matches_oracle(mapi_lib, orc, monkeypatch, n, k):
+    """op = DOT on the batched kernels (stream-K v2 and the split-K v1): k independent RPI runs (Eq. 1, l2
+    normalisation) against the oracle's RPI per vector (T2, norms = ||A w_t||_2 at 1e-5)."""
+    m = mapi_lib
+    r = np.random.default_rng(n + k)
+    G = r.standard_normal((n, n)).astype(np.float32) / np.sqrt(n)
+    A = ((G + G.T) / 2 + np.diag(np.linspace(3.0, 1.0, n))).astype(np.float32)
+    B0 = r.standard_normal((k, n))
+    B0 = (B0 / np.linalg.norm(B0, axis=1, keepdims=True)).astype(np.float32)
+    T = 15
+    for path in ("v2", "v1"):
+        if path == "v1":
+            monkeypatch.setenv("MAPI_BATCHED_PATH", "v1")
+        res = m.iterate_batched(torch.from_numpy(A).cuda(), torch.from_numpy(B0).cuda(), T, op=m.DOT)
+        W, norms = res.W.cpu().numpy(), res.norms.cpu().numpy()
+        for v in sorted({0, k // 2, k - 1}):
+            ref = orc.rpi(A, B0[v], T)
+            assert res.iters_done[v] == T
+            _t2(W[v], ref.w)
+            np.testing.assert_allclose(np.linalg.norm(W[v]), 1.0, rtol=1e-5)
+            np.testing.assert_allclose(norms[:, v], ref.norms, rtol=1e-5)
+
+
 def test_batched_tol_per_vector_and_identity(mapi_lib):
     m = mapi_lib
     n, k = 96, 4
