@@ -756,8 +756,11 @@ def e2e_dense(args, m, A, b0, iters, dev, stream, world, dist):
     """End to end through the public host API, pipelined the way a server runs a stream of problems: each
     step's matrix and b0 go from pinned host memory to the device on a copy stream while the previous step
     iterates, and each w + trace comes back.  A symmetric matrix (cfg3's covariance-like A, exactly
-    symmetric by construction) travels as its packed upper triangle (mapi_iterate_host_many_packed: half
-    the PCIe bytes, unpacked bitwise on the device); any other matrix as a whole (mapi_iterate_host_many)."""
+    symmetric by construction) is handed over as the FULL host matrix, of which only the upper-triangle
+    block rows cross PCIe (mapi_iterate_host_many_sym: 2-D copies, half the bytes, no host-side packing),
+    then K2s; `packed` reports the same stream given as packed upper triangles (mapi_iterate_host_many_packed,
+    the triangle packed once on the host by the native mapi_pack_upper_host, its time reported).  Any other
+    matrix travels whole (mapi_iterate_host_many)."""
     import torch
 
     n, lda = A.shape[0], A.stride(0)
@@ -767,45 +770,61 @@ def e2e_dense(args, m, A, b0, iters, dev, stream, world, dist):
     # earlier problem's iterations, so it is amortised over the stream, as a server would see it
     steps = max(2, min(max(args.steps, 20), 40))
     outs = [torch.empty(n, dtype=torch.float32, pin_memory=True) for _ in range(steps)]
-    if sym:
-        A_h = m.pack_upper(A.cpu(), out=torch.empty(n * (n + 1) // 2, dtype=torch.float32, pin_memory=True))
-        need = int(m.load().mapi_workspace_size(m.WS_ITERATE_HOST_MANY_PACKED, n, 0, iters)) + 8 * steps
-        h2d = 4 * (n * (n + 1) // 2) + 4 * n
-        path = ("mapi_iterate_host_many_packed: per step, the pinned host matrix as its packed upper triangle "
-                "(n(n+1)/2 floats) + b0 -> device on a copy stream overlapping the previous step's iterations, "
-                "bitwise unpack on the device (k_unpack_sym), 100 iterations, w + trace -> host")
-    else:
-        A_h = torch.empty((n, lda), dtype=torch.float32, pin_memory=True)
-        A_h.copy_(A.as_strided((n, lda), (lda, 1)) if lda == n else A)
+    A_full = torch.empty((n, lda), dtype=torch.float32, pin_memory=True)
+    A_full.copy_(A.as_strided((n, lda), (lda, 1)) if lda == n else A)
+
+    def timed(run):
+        run(2)  # warm-up
+        torch.cuda.synchronize()
+        if dist:
+            import torch.distributed as tdist
+
+            tdist.barrier()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        run(steps)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        return max_over_ranks(ev0.elapsed_time(ev1), dev)
+
+    d2h = 4 * n + 8 * iters + 8
+    if not sym:
         need = int(m.load().mapi_workspace_size(m.WS_ITERATE_HOST_MANY, n, lda, iters)) + 8 * steps
-        h2d = 4 * n * lda + 4 * n
-        path = ("mapi_iterate_host_many: per step, pinned host A,b0 -> device (copy stream, overlapping the "
-                "previous step's iterations), 100 iterations, w + trace -> host")
+        ws = torch.empty(need, dtype=torch.uint8, device=dev)
+        ms = timed(lambda c: m.iterate_host_many([A_full] * c, [b0_h] * c, iters, outs=outs[:c], ws=ws, stream=stream))
+        del ws
+        return {"value": world * iters * steps / (ms / 1e3), "unit": "iterations/s",
+                "h2d_bytes_per_step": 4 * n * lda + 4 * n, "d2h_bytes_per_step": d2h, "steps": steps,
+                "ms_per_step": ms / steps,
+                "path": "mapi_iterate_host_many: per step, pinned host A,b0 -> device (copy stream, overlapping the "
+                        "previous step's iterations), 100 iterations, w + trace -> host"}
+    need = int(m.load().mapi_workspace_size(m.WS_ITERATE_HOST_MANY_SYM, n, 0, iters)) + 8 * steps
     ws = torch.empty(need, dtype=torch.uint8, device=dev)
-
-    def run(count):
-        if sym:
-            m.iterate_host_many_packed([A_h] * count, n, [b0_h] * count, iters, outs=outs[:count], ws=ws,
-                                       stream=stream)
-        else:
-            m.iterate_host_many([A_h] * count, [b0_h] * count, iters, outs=outs[:count], ws=ws, stream=stream)
-
-    run(2)  # warm-up
-    torch.cuda.synchronize()
-    if dist:
-        import torch.distributed as tdist
-
-        tdist.barrier()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record(stream)
-    run(steps)
-    ev1.record(stream)
-    torch.cuda.synchronize()
-    ms = max_over_ranks(ev0.elapsed_time(ev1), dev)
-    del ws, A_h
-    return {"value": world * iters * steps / (ms / 1e3), "unit": "iterations/s",
-            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 4 * n + 8 * iters + 8,
-            "steps": steps, "ms_per_step": ms / steps, "path": path}
+    ms = timed(lambda c: m.iterate_host_many_sym([A_full] * c, [b0_h] * c, iters, outs=outs[:c], ws=ws, stream=stream))
+    h2d = sum(4 * (n - j0) * min(128, n - j0) for j0 in range(0, n, 128)) + 4 * n
+    out = {"value": world * iters * steps / (ms / 1e3), "unit": "iterations/s", "h2d_bytes_per_step": h2d,
+           "d2h_bytes_per_step": d2h, "steps": steps, "ms_per_step": ms / steps,
+           "path": "mapi_iterate_host_many_sym: per step, the FULL pinned host matrix of which only the upper-"
+                   "triangle block rows (one 2-D copy per 128-row block) + b0 go to the device on a copy stream "
+                   "overlapping the previous step's iterations, K2s, 100 iterations, w + trace -> host"}
+    del ws
+    A_p = torch.empty(n * (n + 1) // 2, dtype=torch.float32, pin_memory=True)
+    t0 = time.perf_counter()
+    m.pack_upper(A_full[:, :n] if lda != n else A_full, out=A_p)
+    pack_s = time.perf_counter() - t0
+    del A_full
+    need = int(m.load().mapi_workspace_size(m.WS_ITERATE_HOST_MANY_PACKED, n, 0, iters)) + 8 * steps
+    ws = torch.empty(need, dtype=torch.uint8, device=dev)
+    msp = timed(lambda c: m.iterate_host_many_packed([A_p] * c, n, [b0_h] * c, iters, outs=outs[:c], ws=ws,
+                                                     stream=stream))
+    out["packed"] = {"value": world * iters * steps / (msp / 1e3), "unit": "iterations/s",
+                     "h2d_bytes_per_step": 4 * (n * (n + 1) // 2) + 4 * n, "d2h_bytes_per_step": d2h,
+                     "ms_per_step": msp / steps, "host_pack_s_once": pack_s,
+                     "path": "mapi_iterate_host_many_packed: the packed upper triangle (packed once on the host by "
+                             "mapi_pack_upper_host, not in the timed region) + b0 -> device, bitwise device unpack, "
+                             "K2s, 100 iterations, w + trace -> host"}
+    del ws, A_p
+    return out
 
 
 def e2e_sharded(args, m, A_local, b0, iters, dev, stream, world, run=None):

@@ -77,7 +77,8 @@ typedef enum {
     MAPI_WS_CSR_REORDER = 13,             /* n */
     MAPI_WS_CSR_PLAN = 14,                /* n, nnz: bytes of the plan buffer of mapi_csr_plan (an upper bound) */
     MAPI_WS_CSR_PLAN_BUILD = 15,          /* n, nnz: temporary workspace of mapi_csr_plan */
-    MAPI_WS_RANK_CSR_PLAN = 16            /* n, nnz: workspace of mapi_rank_csr_plan */
+    MAPI_WS_RANK_CSR_PLAN = 16,           /* n, nnz: workspace of mapi_rank_csr_plan */
+    MAPI_WS_ITERATE_HOST_MANY_SYM = 17    /* n, k = iters; add 8 bytes per problem beyond 2 */
 } mapi_ws_op;
 
 /* y = A (op) x — the matrix extension of the MAVP (reading Q6: y_j uses ROW j):
@@ -236,6 +237,23 @@ mapi_status mapi_iterate_host_many_packed(int32_t op, int32_t count, const float
                                           float *const *w_out_hosts, float *const *norms_hosts,
                                           float *const *deltas_hosts, int32_t *iters_done, void *ws,
                                           size_t ws_bytes, mapi_stream_t stream);
+
+/* mapi_iterate_host_many for SYMMETRIC matrices given as FULL host matrices (n x lda, pinned for overlap):
+ * only the upper-triangle block rows are copied host->device (one 2-D copy per 128-row block: columns
+ * [128 b, n) of rows [128 b, 128 b + 128)), half the PCIe bytes and no host-side packing, and K2s
+ * (mapi_iterate_sym) iterates on them; the strictly-lower part of the device copy is never read.  Results
+ * bitwise those of mapi_iterate_sym on the device matrix.  ws: mapi_workspace_size(
+ * MAPI_WS_ITERATE_HOST_MANY_SYM, n, 0, iters) + 8 * max(0, count - 2) bytes.  Synchronises `stream`. */
+mapi_status mapi_iterate_host_many_sym(int32_t op, int32_t count, const float *const *A_hosts, int64_t n, int64_t lda,
+                                       const float *const *b0_hosts, int32_t iters, float tol,
+                                       float *const *w_out_hosts, float *const *norms_hosts,
+                                       float *const *deltas_hosts, int32_t *iters_done, void *ws, size_t ws_bytes,
+                                       mapi_stream_t stream);
+
+/* Host-side input preparation for mapi_iterate_host_many_packed: the upper triangle of the n x lda host
+ * matrix A in LAPACK packed row-major order (row j = A[j, j:], n(n+1)/2 floats into `out`), copied by
+ * `threads` host threads (0 = all hardware threads).  Pure data movement; synchronous. */
+mapi_status mapi_pack_upper_host(const float *A, int64_t n, int64_t lda, float *out, int32_t threads);
 
 /* Batched MAPI: k independent runs of mapi_iterate on the same A ("multiple independent
  * runs"; matrix extension P:69-70 with p = k columns), Y = A (op) W each iteration.

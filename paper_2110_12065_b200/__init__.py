@@ -21,14 +21,14 @@ from ._build import build  # noqa: F401  (re-exported: compile in-tree)
 __all__ = ["load", "build", "MapiError", "mavp_matvec", "mavp_matmat", "min_covariance", "center_rows", "mavp_deflate",
            "mavp_reconstruct", "iterate", "iterate_host", "iterate_batched",
            "pca_topk", "csr_prepare", "rank_csr", "workspace_size", "launch_count", "set_profiling",
-           "last_kernel_ms", "MIN1", "MIN2", "DOT", "iterate_host_many", "iterate_host_many_packed", "pack_upper", "iterate_sym", "csr_reorder", "csr_permute",
+           "last_kernel_ms", "MIN1", "MIN2", "DOT", "iterate_host_many", "iterate_host_many_packed", "iterate_host_many_sym", "pack_upper", "iterate_sym", "csr_reorder", "csr_permute",
            "csr_plan", "rank_csr_plan", "CsrPlan", "PlanInfo"]
 
 MIN1, MIN2, DOT = 0, 1, 2  # DOT: regular product of Eq. (1), the RPI comparator
 (WS_MATVEC, WS_ITERATE, WS_ITERATE_BATCHED, WS_PCA_TOPK, WS_CSR_PREPARE, WS_RANK_CSR, WS_ITERATE_HOST,
  WS_MAVP_DEFLATE, WS_RECONSTRUCT, WS_ITERATE_SHARDED, WS_ITERATE_HOST_MANY,
  WS_ITERATE_HOST_MANY_PACKED, WS_ITERATE_SYM, WS_CSR_REORDER, WS_CSR_PLAN, WS_CSR_PLAN_BUILD,
- WS_RANK_CSR_PLAN) = range(17)
+ WS_RANK_CSR_PLAN, WS_ITERATE_HOST_MANY_SYM) = range(18)
 STATUS = {0: "MAPI_OK", 1: "MAPI_ERR_NULL", 2: "MAPI_ERR_SHAPE", 3: "MAPI_ERR_BAD_PARAM",
           4: "MAPI_ERR_DEGENERATE", 5: "MAPI_ERR_NEGATIVE", 6: "MAPI_ERR_NONFINITE",
           7: "MAPI_ERR_WORKSPACE", 8: "MAPI_ERR_CUDA"}
@@ -71,6 +71,8 @@ def load():
             "mapi_iterate_host_many": (st, [i32, i32, P, i64, i64, P, i32, f32, P, P, P, P, P, sz, P]),
             "mapi_iterate_sym": (st, [i32, P, i64, i64, P, i32, f32, P, P, P, P, P, P, sz, P]),
             "mapi_iterate_host_many_packed": (st, [i32, i32, P, i64, P, i32, f32, P, P, P, P, P, sz, P]),
+            "mapi_iterate_host_many_sym": (st, [i32, i32, P, i64, i64, P, i32, f32, P, P, P, P, P, sz, P]),
+            "mapi_pack_upper_host": (st, [P, i64, i64, P, i32]),
             "mapi_iterate_batched": (st, [i32, P, i64, i64, P, i32, i32, f32, P, P, P, P, P, sz, P]),
             "mapi_pca_topk": (st, [i32, P, i64, i64, i32, i32, P, P, P, P, P, sz, P]),
             "mapi_csr_prepare": (st, [i64, i64, P, P, f32, P, P, P, sz, P]),
@@ -382,23 +384,57 @@ def iterate_host_many(As, b0s, iters: int, tol: float = 0.0, op: int = MIN1, ws=
     return res
 
 
-def pack_upper(A, out=None):
+def pack_upper(A, out=None, threads: int = 0):
     """Host-side input preparation for iterate_host_many_packed: the upper triangle of a symmetric n x n
-    fp32 CPU matrix in packed row-major order (row j = A[j, j:], LAPACK "packed" layout), n(n+1)/2 floats.
-    Pure data movement (no arithmetic); `out` may be a pinned 1-D fp32 tensor to fill."""
+    fp32 CPU matrix in packed row-major order (row j = A[j, j:], LAPACK "packed" layout), n(n+1)/2 floats,
+    copied by `threads` native host threads (mapi_pack_upper_host; 0 = all).  Pure data movement (no
+    arithmetic); `out` may be a pinned 1-D fp32 tensor to fill."""
     torch = _torch()
     A = torch.as_tensor(A)
-    if A.dim() != 2 or A.shape[0] != A.shape[1] or A.dtype != torch.float32 or A.is_cuda:
-        raise ValueError("A must be a square fp32 CPU matrix")
+    if A.dim() != 2 or A.shape[0] != A.shape[1] or A.dtype != torch.float32 or A.is_cuda or A.stride(1) != 1:
+        raise ValueError("A must be a square row-major fp32 CPU matrix")
     n = A.shape[0]
     out = out if out is not None else torch.empty(n * (n + 1) // 2, dtype=torch.float32)
-    if out.numel() != n * (n + 1) // 2:
-        raise ValueError("out must hold n(n+1)/2 floats")
-    off = 0
-    for j in range(n):
-        out[off:off + n - j].copy_(A[j, j:])
-        off += n - j
+    if out.numel() != n * (n + 1) // 2 or not out.is_contiguous():
+        raise ValueError("out must be a contiguous tensor of n(n+1)/2 floats")
+    _check(load().mapi_pack_upper_host(A.data_ptr(), n, A.stride(0), out.data_ptr(), int(threads)))
     return out
+
+
+def iterate_host_many_sym(As, b0s, iters: int, tol: float = 0.0, op: int = MIN1, ws=None, outs=None,
+                          want_trace: bool = True, stream=None) -> list:
+    """iterate_host_many for SYMMETRIC matrices given as full pinned host matrices: only the upper-triangle
+    block rows cross PCIe (mapi_iterate_host_many_sym: one 2-D copy per 128-row block), K2s iterates on them.
+    Returns one IterResult per problem; synchronises the stream."""
+    torch = _torch()
+    count = len(As)
+    if count < 1 or len(b0s) != count:
+        raise ValueError("need >= 1 problem and one b0 per problem")
+    n = As[0].shape[0]
+    for A, b in zip(As, b0s):
+        if A.is_cuda or b.is_cuda or A.dtype != torch.float32 or A.dim() != 2 or A.shape[0] != n or \
+                A.stride(1) != 1 or A.stride(0) != As[0].stride(0):
+            raise ValueError("As must be n x lda row-major fp32 CPU tensors with one lda (pinned for overlap)")
+    lda = As[0].stride(0)
+    outs = outs if outs is not None else [torch.empty(n, dtype=torch.float32) for _ in range(count)]
+    pin = torch.cuda.is_available()
+    norms = [torch.zeros(iters, dtype=torch.float32, pin_memory=pin) for _ in range(count)] if want_trace else None
+    deltas = [torch.zeros(iters, dtype=torch.float32, pin_memory=pin) for _ in range(count)] if want_trace else None
+    lib = load()
+    need = int(lib.mapi_workspace_size(WS_ITERATE_HOST_MANY_SYM, n, 0, iters)) + 8 * max(0, count - 2)
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(need, dtype=torch.uint8, device="cuda")
+    arr = lambda ts: (ctypes.c_void_p * count)(*[t.data_ptr() for t in ts])  # noqa: E731
+    done = (ctypes.c_int32 * count)()
+    st = lib.mapi_iterate_host_many_sym(op, count, arr(As), n, lda, arr(b0s), int(iters), float(tol), arr(outs),
+                                        arr(norms) if norms else None, arr(deltas) if deltas else None, done,
+                                        _ptr(ws), ws.numel(), _stream(stream))
+    _check(st)
+    res = []
+    for i in range(count):
+        k = done[i]
+        res.append(IterResult(outs[i], None, norms[i][:k] if norms else None, deltas[i][:k] if deltas else None, k))
+    return res
 
 
 def iterate_host_many_packed(Aps, n: int, b0s, iters: int, tol: float = 0.0, op: int = MIN1, ws=None, outs=None,

@@ -11,6 +11,7 @@
 #include <type_traits>
 #include <vector>
 #include <memory>
+#include <thread>
 
 #include "../../include/mapi.h"
 #include "host_common.h"
@@ -551,13 +552,14 @@ float mapi_last_kernel_ms(void) { return g_last_kernel_ms; }
 // count independent host problems, pipelined: problem i+1's A / b0 host->device copies (a second, copy
 // stream) overlap problem i's iterations (the compute stream); two device slots alternate.
 // packed: each slot also holds the packed upper triangle (n(n+1)/2 floats) the host sends
-size_t iterate_host_many_ws_bytes(int64_t n, int64_t lda, int32_t iters, int32_t count, bool packed = false) {
+// sym: symmetric problems (packed or upper-triangle copies) may run K2s, which needs its partial buffers
+size_t iterate_host_many_ws_bytes(int64_t n, int64_t lda, int32_t iters, int32_t count, bool packed = false,
+                                  bool sym = false) {
     const size_t slot = align256(sizeof(float) * (size_t)n * (size_t)lda) + 2 * align256(sizeof(float) * (size_t)n) +
                         2 * align256(sizeof(float) * (size_t)std::max(iters, 1)) +
                         (packed ? align256(sizeof(float) * (size_t)packed_floats(n)) : 0);
-    // packed (= symmetric) problems may run K2s, which needs its partial buffers
     return iterate_ws_bytes(n) + 2 * slot + sizeof(int32_t) * 2 * (size_t)std::max(count, 2) +
-           (packed ? 256 + align256(sym_partials_bytes(n)) : 0);  // (+256: alignment of the partials)
+           ((packed || sym) ? 256 + align256(sym_partials_bytes(n)) : 0);  // (+256: alignment of the partials)
 }
 // device leading dimension of the unpacked matrix: 32 B-aligned rows (the 256-bit load path)
 inline int64_t packed_lda(int64_t n) { return (n + 7) & ~int64_t(7); }
@@ -585,6 +587,7 @@ size_t mapi_workspace_size(int32_t op, int64_t n, int64_t nnz, int32_t k) {
     case MAPI_WS_ITERATE_SHARDED: return sharded_ws_bytes();
     case MAPI_WS_ITERATE_HOST_MANY: return iterate_host_many_ws_bytes(n, nnz, k, 2);
     case MAPI_WS_ITERATE_HOST_MANY_PACKED: return iterate_host_many_ws_bytes(n, packed_lda(n), k, 2, true);
+    case MAPI_WS_ITERATE_HOST_MANY_SYM: return iterate_host_many_ws_bytes(n, packed_lda(n), k, 2, false, true);
     case MAPI_WS_ITERATE_SYM: return iterate_ws_bytes(n) + align256(sym_partials_bytes(n));
     case MAPI_WS_CSR_REORDER: return reorder_ws_bytes(n);
     case MAPI_WS_CSR_PLAN: return mapi_plan::plan_bytes_bound(n, nnz);
@@ -854,20 +857,28 @@ mapi_status mapi_iterate_host(int32_t op, const float* A_host, int64_t n, int64_
     return st;
 }
 
-// packed = true: A_hosts[i] are packed upper triangles (n(n+1)/2 floats), unpacked on the device into an
-// n x packed_lda(n) matrix before the iterations (lda is ignored)
+// mode kFull: A_hosts[i] are full n x lda matrices, copied whole.  kPacked: packed upper triangles
+// (n(n+1)/2 floats), unpacked on the device into an n x packed_lda(n) matrix.  kSymUpper: full symmetric
+// n x lda host matrices of which only the upper-triangle block rows are copied (one 2-D copy per 128-row
+// block: columns [128 b, n) of rows [128 b, 128 b + 128)) into an n x packed_lda(n) device matrix — what
+// K2s reads, half the PCIe bytes, no host-side packing.
+enum HostMode { kFull = 0, kPacked = 1, kSymUpper = 2 };
 static mapi_status host_many_impl(int32_t op, int32_t count, const float* const* A_hosts, int64_t n, int64_t lda,
                                   const float* const* b0_hosts, int32_t iters, float tol, float* const* w_out_hosts,
                                   float* const* norms_hosts, float* const* deltas_hosts, int32_t* iters_done,
-                                  void* ws, size_t ws_bytes, mapi_stream_t stream, bool packed) {
+                                  void* ws, size_t ws_bytes, mapi_stream_t stream, HostMode mode) {
     if (count < 1) return fail(MAPI_ERR_BAD_PARAM, "count (%d) must be >= 1", count);
     if (!A_hosts || !b0_hosts || !w_out_hosts) return fail(MAPI_ERR_NULL, "A_hosts / b0_hosts / w_out_hosts is NULL");
-    if (packed) lda = packed_lda(n);
+    const bool packed = mode == kPacked;
+    const int64_t lda_host = lda;
+    if (mode != kFull) lda = packed_lda(n);
     for (int32_t i = 0; i < count; ++i) {
         mapi_status st = validate_dense(op, A_hosts[i], n, lda, b0_hosts[i], iters, tol, w_out_hosts[i], ws);
         if (st != MAPI_OK) return fail(st, "problem %d: %s", i, g_err);
     }
-    const size_t need = iterate_host_many_ws_bytes(n, lda, iters, count, packed);
+    if (mode == kSymUpper && lda_host < n)
+        return fail(MAPI_ERR_SHAPE, "lda (%lld) < n (%lld)", (long long)lda_host, (long long)n);
+    const size_t need = iterate_host_many_ws_bytes(n, lda, iters, count, mode == kPacked, mode == kSymUpper);
     if (ws_bytes < need) return fail(MAPI_ERR_WORKSPACE, "ws_bytes (%zu) < required (%zu)", ws_bytes, need);
     Device d;
     mapi_status st = device_info(d);
@@ -898,8 +909,10 @@ static mapi_status host_many_impl(int32_t op, int32_t count, const float* const*
     }
     int32_t* st_all = reinterpret_cast<int32_t*>(p);
     p += sizeof(int32_t) * 2 * (size_t)std::max(count, 2);
+    // symmetric problems run K2s where it applies (both slots are 256 B-aligned: the same answer for each)
+    const bool sym_k = mode != kFull && use_sym(d, sl[0].A, n, lda);
     // K2s partials (the packed input is symmetric), 256 B-aligned (float4 stores)
-    float* sym_part = packed ? reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(p) + 255) & ~uintptr_t(255)) : nullptr;
+    float* sym_part = mode != kFull ? reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(p) + 255) & ~uintptr_t(255)) : nullptr;
     cudaStream_t cs = nullptr;
     cudaEvent_t loaded[2] = {nullptr, nullptr}, freed[2] = {nullptr, nullptr};
     auto cleanup = [&]() {
@@ -932,11 +945,23 @@ static mapi_status host_many_impl(int32_t op, int32_t count, const float* const*
         Slot& x = sl[i & 1];
         cudaError_t r = cudaSuccess;
         if (i >= 2) r = cudaStreamWaitEvent(cs, freed[i & 1], 0);
-        if (r == cudaSuccess)
-            r = packed ? cudaMemcpyAsync(x.pk, A_hosts[i], sizeof(float) * (size_t)packed_floats(n),
-                                         cudaMemcpyHostToDevice, cs)
-                       : cudaMemcpyAsync(x.A, A_hosts[i], sizeof(float) * (size_t)n * (size_t)lda,
-                                         cudaMemcpyHostToDevice, cs);
+        if (r == cudaSuccess) {
+            if (mode == kPacked)
+                r = cudaMemcpyAsync(x.pk, A_hosts[i], sizeof(float) * (size_t)packed_floats(n), cudaMemcpyHostToDevice,
+                                    cs);
+            else if (mode == kFull)
+                r = cudaMemcpyAsync(x.A, A_hosts[i], sizeof(float) * (size_t)n * (size_t)lda, cudaMemcpyHostToDevice, cs);
+            else if (!sym_k)  // the full-matrix kernels will run: the whole matrix
+                r = cudaMemcpy2DAsync(x.A, sizeof(float) * (size_t)lda, A_hosts[i], sizeof(float) * (size_t)lda_host,
+                                      sizeof(float) * (size_t)n, (size_t)n, cudaMemcpyHostToDevice, cs);
+            else
+                for (int64_t j0 = 0; j0 < n && r == cudaSuccess; j0 += kSymRB) {
+                    const int64_t rows = std::min<int64_t>(kSymRB, n - j0);
+                    r = cudaMemcpy2DAsync(x.A + j0 * lda + j0, sizeof(float) * (size_t)lda, A_hosts[i] + j0 * lda_host + j0,
+                                          sizeof(float) * (size_t)lda_host, sizeof(float) * (size_t)(n - j0),
+                                          (size_t)rows, cudaMemcpyHostToDevice, cs);
+                }
+        }
         if (r == cudaSuccess) r = cudaMemcpyAsync(x.b0, b0_hosts[i], sizeof(float) * (size_t)n, cudaMemcpyHostToDevice, cs);
         if (r == cudaSuccess) r = cudaEventRecord(loaded[i & 1], cs);
         return r;
@@ -953,7 +978,7 @@ static mapi_status host_many_impl(int32_t op, int32_t count, const float* const*
             g_launches.fetch_add(1, std::memory_order_relaxed);
             if ((e = cudaGetLastError()) != cudaSuccess) break;
         }
-        st = (packed && use_sym(d, x.A, n, lda))
+        st = sym_k
                  ? sym_launch(d, op, x.A, n, lda, x.b0, iters, tol, x.w, x.nrm, x.dlt, W, sym_part, s, nullptr)
                  : iterate_launch(d, op, x.A, n, lda, x.b0, iters, tol, x.w, x.nrm, x.dlt, W, s, nullptr);
         if (st != MAPI_OK) break;
@@ -991,7 +1016,46 @@ mapi_status mapi_iterate_host_many(int32_t op, int32_t count, const float* const
                                    float* const* norms_hosts, float* const* deltas_hosts, int32_t* iters_done,
                                    void* ws, size_t ws_bytes, mapi_stream_t stream) {
     return host_many_impl(op, count, A_hosts, n, lda, b0_hosts, iters, tol, w_out_hosts, norms_hosts, deltas_hosts,
-                          iters_done, ws, ws_bytes, stream, false);
+                          iters_done, ws, ws_bytes, stream, kFull);
+}
+
+mapi_status mapi_iterate_host_many_sym(int32_t op, int32_t count, const float* const* A_hosts, int64_t n, int64_t lda,
+                                       const float* const* b0_hosts, int32_t iters, float tol,
+                                       float* const* w_out_hosts, float* const* norms_hosts,
+                                       float* const* deltas_hosts, int32_t* iters_done, void* ws, size_t ws_bytes,
+                                       mapi_stream_t stream) {
+    return host_many_impl(op, count, A_hosts, n, lda, b0_hosts, iters, tol, w_out_hosts, norms_hosts, deltas_hosts,
+                          iters_done, ws, ws_bytes, stream, kSymUpper);
+}
+
+// LAPACK-style packed upper triangle of a host matrix (row j = A[j, j:]), `threads` host threads (0 = all
+// hardware threads): pure data movement for mapi_iterate_host_many_packed callers
+mapi_status mapi_pack_upper_host(const float* A, int64_t n, int64_t lda, float* out, int32_t threads) {
+    if (!A || !out) return fail(MAPI_ERR_NULL, "A / out is NULL");
+    if (n < 1 || lda < n) return fail(MAPI_ERR_SHAPE, "n (%lld) / lda (%lld)", (long long)n, (long long)lda);
+    int T = threads > 0 ? threads : (int)std::max(1u, std::thread::hardware_concurrency());
+    T = (int)std::min<int64_t>(T, n);
+    std::vector<std::thread> pool;
+    // thread k takes rows with balanced element counts: cumulative count of rows < j is j n - j (j - 1) / 2
+    auto start = [&](int k) {
+        const double total = (double)n * (double)(n + 1) / 2.0, target = total * k / T;
+        int64_t lo = 0, hi = n;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if ((double)mid * (double)n - (double)mid * (double)(mid - 1) / 2.0 >= target) hi = mid;
+            else lo = mid + 1;
+        }
+        return lo;
+    };
+    for (int k = 0; k < T; ++k) {
+        const int64_t j0 = start(k), j1 = start(k + 1);
+        pool.emplace_back([=]() {
+            for (int64_t j = j0; j < j1; ++j)
+                memcpy(out + (j * n - j * (j - 1) / 2), A + j * lda + j, sizeof(float) * (size_t)(n - j));
+        });
+    }
+    for (auto& th : pool) th.join();
+    return MAPI_OK;
 }
 
 mapi_status mapi_iterate_host_many_packed(int32_t op, int32_t count, const float* const* Ap_hosts, int64_t n,
@@ -1000,7 +1064,7 @@ mapi_status mapi_iterate_host_many_packed(int32_t op, int32_t count, const float
                                           float* const* deltas_hosts, int32_t* iters_done, void* ws, size_t ws_bytes,
                                           mapi_stream_t stream) {
     return host_many_impl(op, count, Ap_hosts, n, 0, b0_hosts, iters, tol, w_out_hosts, norms_hosts, deltas_hosts,
-                          iters_done, ws, ws_bytes, stream, true);
+                          iters_done, ws, ws_bytes, stream, kPacked);
 }
 
 mapi_status mapi_pca_topk(int32_t op, const float* C, int64_t n, int64_t ldc, int32_t k, int32_t iters,

@@ -577,6 +577,34 @@ def test_iterate_host_many_packed_bitwise(mapi_lib, n):
                 a.norms.numpy().astype(np.float64))
 
 
+@pytest.mark.parametrize("n", [1, 33, 1000, 2600, 8192, 8200])
+def test_iterate_host_many_sym_bitwise(mapi_lib, n):
+    """Symmetric matrices handed over as FULL host matrices (mapi_iterate_host_many_sym): only the upper-
+    triangle block rows are copied where K2s runs (n >= 8192; the host's strictly-lower triangle is NaN there
+    and never crosses PCIe / is never read), the whole matrix otherwise; results bitwise mapi_iterate_sym on
+    the device matrix, padded host rows (lda > n) included."""
+    m = mapi_lib
+    r = np.random.default_rng(n + 29)
+    As, b0s, Sd = [], [], []
+    lda = n + 5
+    for i in range(2):
+        G = r.standard_normal((n, n)).astype(np.float32)
+        S = np.triu(G) + np.triu(G, 1).T + np.eye(n, dtype=np.float32) * (3 + i)
+        host = np.full((n, lda), np.nan, np.float32)
+        host[:, :n] = S
+        if n >= 8192:
+            host[:, :n][np.tril_indices(n, -1)] = np.nan
+        As.append(torch.from_numpy(host).pin_memory()[:, :n])
+        Sd.append(torch.from_numpy(S).cuda())
+        b0s.append(torch.full((n,), 1 / np.sqrt(n)).pin_memory())
+    res = m.iterate_host_many_sym(As, b0s, 12)
+    for A, b0, got in zip(Sd, b0s, res):
+        ref = m.iterate_sym(A, b0.cuda(), 12)
+        assert got.iters_done == 12
+        assert torch.equal(ref.w.cpu(), got.w) and torch.equal(ref.norms.cpu(), got.norms)
+        assert np.all(np.isfinite(got.w.numpy()))
+
+
 # ------------------------------------------------------------------------------ symmetric path (K2s)
 
 
