@@ -137,3 +137,30 @@ def pagerank_eig(n, edges, alpha=0.85):
     k = int(np.argmin(np.abs(vals - 1.0)))
     v = np.real(vecs[:, k])
     return v / v.sum()
+
+
+def minibatch_mapi(X, batch, beta, w0, gram="min1"):
+    """Algorithm 3 written out literally for tiny inputs: per iteration the batch mean of the
+    samples' matrices A~_i[j][k] = x_ij (gram) x_ik, w_{t+1} = M (.) w_t - beta w_{t-1} with (.) the min1
+    product of Eq. (3), then both w_t and w_{t+1} divided by ||w_{t+1}||_1 (step 5 verbatim).
+    Returns (w_T, [||w_{t+1}||_1 for each t])."""
+    term = OPS[gram]
+    D = len(w0)
+    w = [float(v) for v in w0]
+    wp = [0.0] * D
+    norms = []
+    for row_ids in batch:
+        s = len(row_ids)
+        M = [[0.0] * D for _ in range(D)]
+        for i in row_ids:
+            x = [float(v) for v in X[i]]
+            for j in range(D):
+                for k in range(D):
+                    M[j][k] += term([x[j]], [x[k]])
+        M = [[M[j][k] / s for k in range(D)] for j in range(D)]
+        y = [min1(M[j], w) - beta * wp[j] for j in range(D)]
+        st = sum(abs(v) for v in y)
+        norms.append(st)
+        wp = [v / st for v in w]
+        w = [v / st for v in y]
+    return np.array(w), np.array(norms)

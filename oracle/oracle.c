@@ -375,6 +375,67 @@ int orc_rank_csr_op(int op, int64_t n, int64_t nnz, const int64_t *row_ptr, cons
 }
 
 /* Number of OpenMP threads the oracle will use (reported beside every oracle timing). */
+/* Algorithm 3 (§3.2): mini-batch MAPI with momentum, in the paper's step order.
+ *   X: N x D fp64 samples (rows, ldx); batch: T x s row indices (the i.i.d. draws of step 3 are INPUTS,
+ *   drawn by the caller); beta: momentum; w0: D (step 1; used as given);
+ *   gram_op: the product forming each sample's matrix A~_i (reading R14): ORC_MIN1 (the paper, P:266:
+ *   "we apply MAPI on A = X^T (.) X", A~_i[j][k] = x_ij (.) x_ik) or ORC_DOT (x_ij x_ik).
+ *   t = 0 .. T-1:
+ *     step 3/4: M = (1/s) sum_{i in batch t} A~_i   (entries summed over the batch in batch order, then / s)
+ *               y_j = sum_k term_min1(M[j][k], w_t[k]) - beta w_{t-1}[j]    (w_{-1} = 0; row j of M, Q6)
+ *     step 5:   s_t = ||y||_1;  w_{t-1} <- w_t / s_t;  w_t <- y / s_t       (both by ||w_{t+1}||_1, verbatim)
+ *   optional final l2 copy (Alg. 3 line 7).  norms[t] = s_t.  DEGENERATE if s_t == 0, NONFINITE if not finite
+ *   (w_out then holds the last good iterate). */
+int orc_minibatch_mapi(const double *X, int64_t N, int64_t D, int64_t ldx, const int64_t *batch, int32_t s,
+                       int32_t T, double beta, const double *w0, int gram_op, double *w_out, double *w_l2_out,
+                       double *norms, int32_t *iters_done) {
+    if (N < 1 || D < 1 || ldx < D || s < 1 || T < 1 || !X || !batch || !w0) return ORC_ERR_BAD_PARAM;
+    for (int64_t q = 0; q < (int64_t)T * s; ++q)
+        if (batch[q] < 0 || batch[q] >= N) return ORC_ERR_BAD_PARAM;
+    double *M = (double *)malloc(sizeof(double) * (size_t)(D * D));
+    double *w = (double *)malloc(sizeof(double) * (size_t)D);
+    double *wp = (double *)calloc((size_t)D, sizeof(double));
+    double *y = (double *)malloc(sizeof(double) * (size_t)D);
+    memcpy(w, w0, sizeof(double) * (size_t)D);
+    int status = ORC_OK;
+    int32_t done = 0;
+    for (int32_t t = 0; t < T; ++t) {
+        for (int64_t e = 0; e < D * D; ++e) M[e] = 0.0;
+        for (int32_t i = 0; i < s; ++i) {
+            const double *x = X + batch[(int64_t)t * s + i] * ldx;
+            for (int64_t j = 0; j < D; ++j)
+                for (int64_t k = 0; k < D; ++k) M[j * D + k] += orc_term(gram_op, x[j], x[k]);
+        }
+        for (int64_t e = 0; e < D * D; ++e) M[e] /= (double)s;
+        for (int64_t j = 0; j < D; ++j) {
+            double acc = 0.0;
+            for (int64_t k = 0; k < D; ++k) acc += orc_term(ORC_MIN1, M[j * D + k], w[k]);
+            y[j] = acc - beta * wp[j];
+        }
+        double st = 0.0;
+        for (int64_t j = 0; j < D; ++j) st += fabs(y[j]);
+        if (!isfinite(st)) { status = ORC_ERR_NONFINITE; break; }
+        if (st == 0.0) { status = ORC_ERR_DEGENERATE; break; }
+        for (int64_t j = 0; j < D; ++j) {
+            wp[j] = w[j] / st;
+            w[j] = y[j] / st;
+        }
+        if (norms) norms[t] = st;
+        done = t + 1;
+    }
+    if (w_out) memcpy(w_out, w, sizeof(double) * (size_t)D);
+    if (w_l2_out) {
+        double l2 = orc_norm(ORC_NORM_L2, w, D);
+        for (int64_t j = 0; j < D; ++j) w_l2_out[j] = l2 > 0.0 ? w[j] / l2 : 0.0;
+    }
+    if (iters_done) *iters_done = done;
+    free(M);
+    free(w);
+    free(wp);
+    free(y);
+    return status;
+}
+
 int orc_num_threads(void) {
 #ifdef _OPENMP
     return omp_get_max_threads();

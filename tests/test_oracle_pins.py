@@ -571,3 +571,54 @@ def test_outer_apply_rows_matches_full(orc):
     full = orc.outer_apply(W, X, "min1", subtract=True)
     rows = np.array([0, 7, 39, 7])
     np.testing.assert_array_equal(orc.outer_apply_rows(W, X, rows, "min1", subtract=True), full[rows])
+
+
+# ------------------------------------------------------------------ Algorithm 3 (mini-batch MAPI with momentum)
+
+
+@pytest.mark.parametrize("gram", ["min1", "dot"])
+@pytest.mark.parametrize("beta", [0.0, 0.225, 0.9])
+def test_minibatch_mapi_matches_brute(orc, gram, beta):
+    """Alg. 3 against the literal pure-Python statement (brute.minibatch_mapi): random tiny
+    datasets, i.i.d. batches with replacement (step 3), momentum (step 4), both iterates rescaled by
+    ||w_{t+1}||_1 (step 5 verbatim), the traced norms and the final l2 copy (line 7)."""
+    for seed in range(6):
+        r = np.random.default_rng(300 + seed)
+        N, D, T, s = int(r.integers(1, 9)), int(r.integers(1, 5)), int(r.integers(1, 6)), int(r.integers(1, 5))
+        X = r.standard_normal((N, D))
+        idx = r.integers(0, N, (T, s))
+        w0 = r.standard_normal(D)
+        w0 /= np.linalg.norm(w0)
+        got = orc.minibatch_mapi(X, idx, beta, w0, gram=gram)
+        if got.status != 0:  # a degenerate draw (tiny D): the brute force divides by zero there
+            continue
+        w, norms = brute.minibatch_mapi(X, idx, beta, w0, gram=gram)
+        np.testing.assert_allclose(got.w, w, rtol=1e-12, atol=1e-15)
+        np.testing.assert_allclose(got.norms, norms, rtol=1e-12)
+        np.testing.assert_allclose(got.w_l2, w / np.linalg.norm(w), rtol=1e-12, atol=1e-15)
+
+
+def test_minibatch_mapi_full_batch_no_momentum_is_algorithm_1(orc):
+    """beta = 0 and every batch = all N samples: Alg. 3 reduces to Alg. 1 on A = (1/N) X^T (.) X,
+    iterate for iterate (the fp64 oracle power iteration on that matrix, the matrix formed by the brute
+    force's Eq. (3) on the columns of X)."""
+    r = np.random.default_rng(77)
+    N, D, T = 40, 6, 12
+    X = r.standard_normal((N, D))
+    idx = np.tile(np.arange(N), (T, 1))
+    w0 = r.standard_normal(D)
+    w0 /= np.linalg.norm(w0)
+    got = orc.minibatch_mapi(X, idx, 0.0, w0)
+    M = np.array([[brute.min1(X[:, j], X[:, k]) / N for k in range(D)] for j in range(D)])
+    ref = orc.power_iterate(M, w0, T, op="min1")
+    assert got.iters_done == ref.iters_done == T
+    np.testing.assert_allclose(got.w, ref.w, rtol=1e-12, atol=1e-15)
+    np.testing.assert_allclose(got.norms, ref.norms, rtol=1e-12)
+
+
+def test_minibatch_mapi_degenerate_and_bad_input(orc):
+    X = np.zeros((5, 3))
+    res = orc.minibatch_mapi(X, np.zeros((2, 2), np.int64), 0.1, np.ones(3) / np.sqrt(3))
+    assert res.status == orc.ERR_DEGENERATE and res.iters_done == 0
+    with pytest.raises(ValueError):
+        orc.minibatch_mapi(np.ones((5, 3)), np.full((2, 2), 5), 0.1, np.ones(3))  # index out of range
