@@ -439,7 +439,10 @@ __device__ __forceinline__ double qdiv(double x, double d, double rd) {
 template <int OP>
 __device__ __forceinline__ float node_v(double w, float bg, float cap) {
     if constexpr (OP == 2) return (float)((double)cap * w);
-    else return (float)fmin(fmax(w - (double)bg, 0.0), (double)cap);
+    // rounding to fp32 is monotone and 0 / cap are fp32 values, so clamping after the rounding gives exactly
+    // fp32(min(max(w - bg, 0), cap)) with one conversion less (F2F.F64.F32 + DADD issue at 16 lanes/clk/SM,
+    // profiles/r02_probe_fp64.log)
+    else return fminf(fmaxf((float)(w - (double)bg), 0.0f), cap);
 }
 template <int OP>
 __device__ __forceinline__ double node_s(double w, float bg) {
@@ -452,13 +455,6 @@ __device__ __forceinline__ int64_t vc_index(int64_t p) {
     return seg * kSegStride + (p - seg * kSegSrc);
 }
 
-// sum of `count` fp64 slots in a fixed order (thread i: slots i, i + 1024, ... ascending, then the block
-// tree), broadcast; slots written by other CTAs of this launch are read through L2
-__device__ __forceinline__ double slots_sum(const double* slots, int64_t count, double* red) {
-    double part = 0.0;
-    for (int64_t c = threadIdx.x; c < count; c += blockDim.x) part += __ldcg(slots + c);
-    return mapi::block_sum(part, red);
-}
 // two block sums at once (one set of barriers), results broadcast
 __device__ __forceinline__ void block_sum2(double& a, double& b, double* red) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -544,6 +540,24 @@ __device__ __forceinline__ double plan_tile(const uint4 (&wd)[2], uint32_t fl, u
     return (double)ls;
 }
 
+// A tile's loads in a FIXED order (asm volatile: not reordered against each other): the two 16-byte word
+// loads first, then the tile's fragment base and the lane's flags.  Phase A's time moved between 78 and 88 us
+// with edits elsewhere in the kernel; ncu's source view of a slow build showed the first word load 15% of the
+// phase on the long scoreboard after the compiler had hoisted the flags / base loads above it
+// (profiles/r02_exp_k3s_tma_phaseb.log).
+__device__ __forceinline__ void tile_loads(const uint4* words4, const uint16_t* wflags, const int32_t* fbase,
+                                           int32_t tile, int lane, uint4 (&w)[2], uint32_t& fl, int32_t& fb) {
+    const uint4* p = words4 + (int64_t)tile * (kTileW / 8) + 2 * lane;
+    asm volatile("ld.global.cs.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(w[0].x), "=r"(w[0].y), "=r"(w[0].z), "=r"(w[0].w) : "l"(p));
+    asm volatile("ld.global.cs.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(w[1].x), "=r"(w[1].y), "=r"(w[1].z), "=r"(w[1].w) : "l"(p + 1));
+    asm volatile("ld.global.nc.s32 %0, [%1];" : "=r"(fb) : "l"(fbase + tile));
+    uint16_t f16;
+    asm volatile("ld.global.cs.u16 %0, [%1];" : "=h"(f16) : "l"(wflags + (int64_t)tile * 32 + lane));
+    fl = f16;
+}
+
 // trace layout: [64 iterations][4] CTA 0 stamps, then per CTA [4] sums over iterations 3..63 of the stamps'
 // differences (phase A, barrier 1, phase B, barrier 2 + stop test), ns
 #define PLAN_STAMP(k)                                                                                    \
@@ -616,6 +630,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rank_plan(RunArgs a) {
     float* wstage = vseg + kSegStride + warp * kTileW;
     const uint32_t sb_seg = (uint32_t)__cvta_generic_to_shared(vseg);
     unsigned long long tprev_ = 0;
+    double Sprev = 0.0, sprev = 1.0;  // (S, s) of the previous iteration
     int cur_seg = -1;  // the segment held in shared memory (phase B overwrites it)
 
     for (int32_t t = 0; t < a.iters; ++t) {
@@ -647,23 +662,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_rank_plan(RunArgs a) {
                 uint4 cur[2], nxt[2];
                 int32_t fb = 0, fbn = 0;
                 uint32_t fl = 0, fln = 0;
-                if (tile < tb) {
-                    cur[0] = __ldcs(words4 + (int64_t)tile * (kTileW / 8) + 2 * lane);
-                    cur[1] = __ldcs(words4 + (int64_t)tile * (kTileW / 8) + 2 * lane + 1);
-                    fl = __ldcs(a.wflags + (int64_t)tile * 32 + lane);
-                    fb = __ldg(a.fbase + tile);
-                }
+                if (tile < tb) tile_loads(words4, a.wflags, a.fbase, tile, lane, cur, fl, fb);
                 for (; tile < tb; tile += kWarps) {
                     const int32_t tn = tile + kWarps;
+                    // the warp's next tile, in flight while this one is gathered
+                    if (tn < tb) tile_loads(words4, a.wflags, a.fbase, tn, lane, nxt, fln, fbn);
                     if (lane == 0 && tn + kWarps < tb) {  // two tiles ahead: into L2 (no registers held)
                         const uint16_t* pf = a.words + (int64_t)(tn + kWarps) * kTileW;
                         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pf), "r"(kTileW * 2) : "memory");
-                    }
-                    if (tn < tb) {  // the warp's next tile, in flight while this one is gathered
-                        nxt[0] = __ldcs(words4 + (int64_t)tn * (kTileW / 8) + 2 * lane);
-                        nxt[1] = __ldcs(words4 + (int64_t)tn * (kTileW / 8) + 2 * lane + 1);
-                        fln = __ldcs(a.wflags + (int64_t)tn * 32 + lane);
-                        fbn = __ldg(a.fbase + tn);
                     }
                     gp += plan_tile(cur, fl, sb_seg, fb, wstage, W.part, lane);
                     cur[0] = nxt[0];
@@ -686,8 +692,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_rank_plan(RunArgs a) {
         }
 
         // ================= phase B: s = n S + sum e, w_{t+1} = (S + e) / s (fp64), delta, next v and S
-        const double S = slots_sum(W.slotS + (t & 1) * SB, nb, red) + slots_sum(W.slotSi + (t & 1) * kMaxGrid, G, red);
-        const double s = (double)n * S + slots_sum(W.slotY, a.nunits, red);
+        // S = the batches' and the isolated slices' partials, sum e = the units' partials: all loads in flight
+        // at once, one pair of block sums (fixed order: thread-strided partials, then the block tree)
+        double S = 0.0, ye = 0.0;
+        {
+            const double* ps = W.slotS + (t & 1) * SB;
+            const double* pi = W.slotSi + (t & 1) * kMaxGrid;
+            for (int64_t k = tid; k < nb; k += kThreads) S += __ldcg(ps + k);
+            for (int64_t k = tid; k < G; k += kThreads) S += __ldcg(pi + k);
+            for (int64_t k = tid; k < a.nunits; k += kThreads) ye += __ldcg(W.slotY + k);
+            block_sum2(S, ye, red);
+        }
+        const double s = (double)n * S + ye;
         if (!(s > 0.0) || isinf(s)) {  // uniform: every CTA sees the same s
             if (c == 0 && tid == 0) {
                 W.status[0] = (s == 0.0) ? MAPI_ERR_DEGENERATE : MAPI_ERR_NONFINITE;
@@ -696,9 +712,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_rank_plan(RunArgs a) {
             return;
         }
         const bool first = t == 0;
-        // (S_{t-1}, s_{t-1}) written by CTA 0 last iteration: read through L2 (L1 is not coherent)
-        const double Sp = first ? 0.0 : __ldcg(W.hist + (t & 1) * 2);
-        const double sp_ = first ? 1.0 : __ldcg(W.hist + (t & 1) * 2 + 1);
+        // (S_{t-1}, s_{t-1}): every CTA formed the same values last iteration
+        const double Sp = Sprev, sp_ = sprev;
         const double rs = 1.0 / s, rsp = 1.0 / sp_;
         double* e_cur = (t & 1) ? W.e1 : W.e0;
         const double* e_prev = (t & 1) ? W.e0 : W.e1;
@@ -794,7 +809,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_rank_plan(RunArgs a) {
         }
         PLAN_STAMP(3);
         mapi::grid_barrier(W.bar, ++epoch * G);
-        const double d = slots_sum(W.slotD, nb, red) + slots_sum(W.slotDi, G, red);
+        double dpart = 0.0;
+        for (int64_t k = tid; k < nb; k += kThreads) dpart += __ldcg(W.slotD + k);
+        for (int64_t k = tid; k < G; k += kThreads) dpart += __ldcg(W.slotDi + k);
+        const double d = mapi::block_sum(dpart, red);
+        Sprev = S;
+        sprev = s;
         if (c == 0 && tid == 0) {
             W.hist[((t + 1) & 1) * 2] = S;
             W.hist[((t + 1) & 1) * 2 + 1] = s;
@@ -1145,8 +1165,10 @@ mapi_status mapi_rank_csr_plan(int32_t op, const void* plan, const mapi_csr_plan
                 ph[2] += (tr[t * 4 + 3] - tr[t * 4 + 2]) / 1e3;
                 ph[3] += (t + 1 < 64 ? (tr[(t + 1) * 4 + 0] - tr[t * 4 + 3]) / 1e3 : 0.0);
             }
-            fprintf(stderr, "[mapi plan trace] us/iteration (CTA 0, %d iterations): phaseA %.1f bar1 %.1f phaseB %.1f bar2 %.1f\n",
-                    it, ph[0] / it, ph[1] / it, ph[2] / it, ph[3] / it);
+            fprintf(stderr, "[mapi plan trace] us/iteration (CTA 0, %d iterations): phaseA %.1f bar1 %.1f phaseB %.1f bar2 %.1f"
+                    " (nbatch %lld, nunits %lld, nfrag %lld, nlive %lld)\n",
+                    it, ph[0] / it, ph[1] / it, ph[2] / it, ph[3] / it, (long long)info->nbatch,
+                    (long long)info->nunits, (long long)info->npieces, (long long)info->nlive);
         }
     }
     if (iters_done) *iters_done = h[1];
