@@ -78,7 +78,8 @@ typedef enum {
     MAPI_WS_CSR_PLAN = 14,                /* n, nnz: bytes of the plan buffer of mapi_csr_plan (an upper bound) */
     MAPI_WS_CSR_PLAN_BUILD = 15,          /* n, nnz: temporary workspace of mapi_csr_plan */
     MAPI_WS_RANK_CSR_PLAN = 16,           /* n, nnz: workspace of mapi_rank_csr_plan */
-    MAPI_WS_ITERATE_HOST_MANY_SYM = 17    /* n, k = iters; add 8 bytes per problem beyond 2 */
+    MAPI_WS_ITERATE_HOST_MANY_SYM = 17,   /* n, k = iters; add 8 bytes per problem beyond 2 */
+    MAPI_WS_MINIBATCH = 18                /* n = D, nnz = s (batch size), k = T (iterations) */
 } mapi_ws_op;
 
 /* y = A (op) x — the matrix extension of the MAVP (reading Q6: y_j uses ROW j):
@@ -380,6 +381,27 @@ mapi_status mapi_csr_reorder(int64_t n, int64_t nnz, const int32_t *row_ptr, con
 mapi_status mapi_csr_permute(int64_t n, const int32_t *perm, const float *x, float *out, int32_t to_new,
                              mapi_stream_t stream);
 
+/* Algorithm 3, mini-batch MAPI with momentum (Section 3.2; K10, readings R14 / R15):
+ *   for t = 0 .. T-1:  M_t = (1/s) sum_{i in batch t} A~_i,  A~_i[j][k] = x_ij (gram_op) x_ik   (steps 3-4)
+ *                      y_j = sum_k min1-term(M_t[j][k], w_t[k]) - beta w_{t-1}[j]   (w_{-1} = 0)   (step 4)
+ *                      s_t = ||y||_1;  w_{t-1} <- w_t / s_t;  w_t <- y / s_t                     (step 5)
+ * X: N x D samples (device, fp32, row-major, leading dimension ldx >= D), 1 <= D <= 64 (MAPI_ERR_SHAPE
+ * beyond).  batch: T x s int32 row indices in [0, N) (device) — the i.i.d. draws of step 3 are the caller's;
+ * an index outside [0, N) is detected on the device (it is read as a zero sample) and the call returns
+ * MAPI_ERR_BAD_PARAM after the run.  gram_op: MAPI_OP_MIN1 (the paper's A = X^T (.) X) or
+ * MAPI_OP_DOT (x_i x_i^T).  w0: D (used as given, step 1).  w_prev0 (D or NULL): the momentum vector to
+ * continue a run from (NULL: the paper's w_{-1} = 0).  Outputs: w_out D (l1-unit w_T), w_l2_out (D or NULL,
+ * Alg. 3 line 7), w_prev_out (D or NULL: w_{T-1} / s_{T-1}, the state a continued run needs), norms (T or
+ * NULL: s_t), *iters_done (host, may be NULL).  MAPI_ERR_DEGENERATE /
+ * MAPI_ERR_NONFINITE as for mapi_iterate (w_out = the last good iterate).  Because the draws are inputs,
+ * all M_t are formed in parallel before the T dependent steps.  T <= 65535.
+ * ws: mapi_workspace_size(MAPI_WS_MINIBATCH, D, s, T).  Synchronises `stream`. */
+mapi_status mapi_minibatch(int32_t gram_op, const float *X, int64_t N, int64_t D, int64_t ldx,
+                           const int32_t *batch, int32_t s, int32_t T, float beta, const float *w0,
+                           const float *w_prev0, float *w_out, float *w_l2_out, float *w_prev_out,
+                           float *norms, int32_t *iters_done, void *ws, size_t ws_bytes,
+                           mapi_stream_t stream);
+
 /* Bytes of device workspace the call `op` needs for the given sizes (0 if none).
  *   MAPI_WS_MATVEC: 0.  MAPI_WS_ITERATE: n.  MAPI_WS_ITERATE_BATCHED: n, k.
  *   MAPI_WS_PCA_TOPK: n, k.  MAPI_WS_CSR_PREPARE / MAPI_WS_RANK_CSR: n, nnz.
@@ -388,7 +410,8 @@ mapi_status mapi_csr_permute(int64_t n, const int32_t *perm, const float *x, flo
  *   MAPI_WS_ITERATE_SHARDED: 256 (status words).
  *   MAPI_WS_ITERATE_HOST_MANY: n, nnz = lda, k = iters (two slots; + 8 bytes per problem beyond 2).
  *   MAPI_WS_ITERATE_HOST_MANY_PACKED: n, k = iters (same, plus a packed buffer per slot).
- *   MAPI_WS_CSR_PLAN / MAPI_WS_CSR_PLAN_BUILD / MAPI_WS_RANK_CSR_PLAN: n, nnz. */
+ *   MAPI_WS_CSR_PLAN / MAPI_WS_CSR_PLAN_BUILD / MAPI_WS_RANK_CSR_PLAN: n, nnz.
+ *   MAPI_WS_MINIBATCH: n = D, nnz = s, k = T. */
 size_t mapi_workspace_size(int32_t op, int64_t n, int64_t nnz, int32_t k);
 
 const char *mapi_status_string(mapi_status status);

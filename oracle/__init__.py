@@ -78,7 +78,8 @@ def _load():
         lib.orc_rank_csr.restype = cint
         lib.orc_rank_csr_op.argtypes = [cint, i64, i64, P, P, dbl, P, i32, dbl, P, P, P, ctypes.POINTER(i32)]
         lib.orc_rank_csr_op.restype = cint
-        lib.orc_minibatch_mapi.argtypes = [P, i64, i64, i64, P, i32, i32, dbl, P, cint, P, P, P, ctypes.POINTER(i32)]
+        lib.orc_minibatch_mapi.argtypes = [P, i64, i64, i64, P, i32, i32, dbl, P, cint, P, P, P, ctypes.POINTER(i32),
+                                           P, P]
         lib.orc_minibatch_mapi.restype = cint
         lib.orc_num_threads.argtypes = []
         lib.orc_num_threads.restype = cint
@@ -340,12 +341,13 @@ def rank_csr(n, row_ptr, col_idx, alpha=0.85, b0=None, max_iters=200, tol=1e-7, 
     return IterResult(st, w, wl2, None, deltas[:k], k)
 
 
-def minibatch_mapi(X, batch, beta, w0, gram="min1") -> IterResult:
+def minibatch_mapi(X, batch, beta, w0, gram="min1", w_prev0=None) -> IterResult:
     """Algorithm 3: mini-batch MAPI with momentum on the samples X (N x D, fp64).  batch: T x s
     row indices (the i.i.d. draws of step 3, an input); beta: momentum; w0: the start (step 1, used as
     given); gram: 'min1' (A~_i = x_i (.) x_i^T, the paper's A = X^T (.) X, reading R14) or 'dot'
     (x_i x_i^T).  Returns w (l1-unit w_T), w_l2 (Alg. 3 line 7), norms[t] = ||w_{t+1}||_1 before
-    normalisation; deltas are not defined for Alg. 3 (empty)."""
+    normalisation; deltas are not defined for Alg. 3 (empty).  w_prev0: the momentum vector to continue a run
+    from (default: the paper's w_{-1} = 0); the result's w_prev is the momentum vector after the last step."""
     X = np.ascontiguousarray(np.asarray(X, np.float64))
     N, D = X.shape
     batch = np.ascontiguousarray(np.asarray(batch, np.int64))
@@ -355,14 +357,21 @@ def minibatch_mapi(X, batch, beta, w0, gram="min1") -> IterResult:
     w0 = _f64(w0)
     if w0.shape != (D,):
         raise ValueError(f"w0 must have D = {D} entries")
-    w, wl2, norms = np.zeros(D), np.zeros(D), np.zeros(T)
+    w, wl2, norms, wprev = np.zeros(D), np.zeros(D), np.zeros(T), np.zeros(D)
+    if w_prev0 is not None:
+        w_prev0 = _f64(w_prev0)
+        if w_prev0.shape != (D,):
+            raise ValueError(f"w_prev0 must have D = {D} entries")
     done = ctypes.c_int32(0)
     st = _load().orc_minibatch_mapi(_ptr(X), N, D, D, _ptr(batch), int(s), int(T), float(beta), _ptr(w0),
-                                    _op(gram), _ptr(w), _ptr(wl2), _ptr(norms), ctypes.byref(done))
+                                    _op(gram), _ptr(w), _ptr(wl2), _ptr(norms), ctypes.byref(done),
+                                    None if w_prev0 is None else _ptr(w_prev0), _ptr(wprev))
     if st == ERR_BAD_PARAM:
         raise ValueError("minibatch_mapi: bad parameters (empty input or a batch index out of range)")
     k = done.value
-    return IterResult(st, w, wl2, norms[:k], np.zeros(0), k)
+    res = IterResult(st, w, wl2, norms[:k], np.zeros(0), k)
+    res.w_prev = wprev
+    return res
 
 
 def rank_order(scores) -> np.ndarray:

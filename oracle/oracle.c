@@ -385,10 +385,13 @@ int orc_rank_csr_op(int op, int64_t n, int64_t nnz, const int64_t *row_ptr, cons
  *               y_j = sum_k term_min1(M[j][k], w_t[k]) - beta w_{t-1}[j]    (w_{-1} = 0; row j of M, Q6)
  *     step 5:   s_t = ||y||_1;  w_{t-1} <- w_t / s_t;  w_t <- y / s_t       (both by ||w_{t+1}||_1, verbatim)
  *   optional final l2 copy (Alg. 3 line 7).  norms[t] = s_t.  DEGENERATE if s_t == 0, NONFINITE if not finite
- *   (w_out then holds the last good iterate). */
+ *   (w_out then holds the last good iterate).
+ *   wprev0 (nullable): the momentum vector to start from instead of w_{-1} = 0, and wprev_out (nullable): the
+ *   momentum vector after the last step (w_{T-1} / s_{T-1}) — the state a run needs to be continued; they
+ *   change nothing in the steps above. */
 int orc_minibatch_mapi(const double *X, int64_t N, int64_t D, int64_t ldx, const int64_t *batch, int32_t s,
                        int32_t T, double beta, const double *w0, int gram_op, double *w_out, double *w_l2_out,
-                       double *norms, int32_t *iters_done) {
+                       double *norms, int32_t *iters_done, const double *wprev0, double *wprev_out) {
     if (N < 1 || D < 1 || ldx < D || s < 1 || T < 1 || !X || !batch || !w0) return ORC_ERR_BAD_PARAM;
     for (int64_t q = 0; q < (int64_t)T * s; ++q)
         if (batch[q] < 0 || batch[q] >= N) return ORC_ERR_BAD_PARAM;
@@ -397,6 +400,7 @@ int orc_minibatch_mapi(const double *X, int64_t N, int64_t D, int64_t ldx, const
     double *wp = (double *)calloc((size_t)D, sizeof(double));
     double *y = (double *)malloc(sizeof(double) * (size_t)D);
     memcpy(w, w0, sizeof(double) * (size_t)D);
+    if (wprev0) memcpy(wp, wprev0, sizeof(double) * (size_t)D);
     int status = ORC_OK;
     int32_t done = 0;
     for (int32_t t = 0; t < T; ++t) {
@@ -424,6 +428,7 @@ int orc_minibatch_mapi(const double *X, int64_t N, int64_t D, int64_t ldx, const
         done = t + 1;
     }
     if (w_out) memcpy(w_out, w, sizeof(double) * (size_t)D);
+    if (wprev_out) memcpy(wprev_out, wp, sizeof(double) * (size_t)D);
     if (w_l2_out) {
         double l2 = orc_norm(ORC_NORM_L2, w, D);
         for (int64_t j = 0; j < D; ++j) w_l2_out[j] = l2 > 0.0 ? w[j] / l2 : 0.0;

@@ -22,13 +22,13 @@ __all__ = ["load", "build", "MapiError", "mavp_matvec", "mavp_matmat", "min_cova
            "mavp_reconstruct", "iterate", "iterate_host", "iterate_batched",
            "pca_topk", "csr_prepare", "rank_csr", "workspace_size", "launch_count", "set_profiling",
            "last_kernel_ms", "MIN1", "MIN2", "DOT", "iterate_host_many", "iterate_host_many_packed", "iterate_host_many_sym", "pack_upper", "iterate_sym", "csr_reorder", "csr_permute",
-           "csr_plan", "rank_csr_plan", "CsrPlan", "PlanInfo"]
+           "csr_plan", "rank_csr_plan", "CsrPlan", "PlanInfo", "minibatch"]
 
 MIN1, MIN2, DOT = 0, 1, 2  # DOT: regular product of Eq. (1), the RPI comparator
 (WS_MATVEC, WS_ITERATE, WS_ITERATE_BATCHED, WS_PCA_TOPK, WS_CSR_PREPARE, WS_RANK_CSR, WS_ITERATE_HOST,
  WS_MAVP_DEFLATE, WS_RECONSTRUCT, WS_ITERATE_SHARDED, WS_ITERATE_HOST_MANY,
  WS_ITERATE_HOST_MANY_PACKED, WS_ITERATE_SYM, WS_CSR_REORDER, WS_CSR_PLAN, WS_CSR_PLAN_BUILD,
- WS_RANK_CSR_PLAN, WS_ITERATE_HOST_MANY_SYM) = range(18)
+ WS_RANK_CSR_PLAN, WS_ITERATE_HOST_MANY_SYM, WS_MINIBATCH) = range(19)
 STATUS = {0: "MAPI_OK", 1: "MAPI_ERR_NULL", 2: "MAPI_ERR_SHAPE", 3: "MAPI_ERR_BAD_PARAM",
           4: "MAPI_ERR_DEGENERATE", 5: "MAPI_ERR_NEGATIVE", 6: "MAPI_ERR_NONFINITE",
           7: "MAPI_ERR_WORKSPACE", 8: "MAPI_ERR_CUDA"}
@@ -83,6 +83,8 @@ def load():
                                         P]),
             "mapi_csr_permute": (st, [i64, P, P, P, i32, P]),
             "mapi_workspace_size": (sz, [i32, i64, i64, i32]),
+            "mapi_minibatch": (st, [i32, P, i64, i64, i64, P, i32, i32, f32, P, P, P, P, P, P, ctypes.POINTER(i32), P,
+                                    sz, P]),
             "mapi_p2p_exchange_bytes": (sz, [i64, i32]),
             "mapi_p2p_alloc": (st, [sz, ctypes.POINTER(ctypes.c_void_p)]),
             "mapi_p2p_free": (st, [P]),
@@ -564,6 +566,36 @@ def rank_csr(n: int, row_ptr, col_idx, cap, bg, b0, max_iters: int = 200, tol: f
     _check(st, done.value)
     k = done.value
     return IterResult(w, wl2, None, deltas[:k], k)
+
+def minibatch(X, batch, beta: float, w0, gram: int = MIN1, want_l2: bool = True, w_prev0=None, ws=None,
+              stream=None) -> IterResult:
+    """Algorithm 3, mini-batch MAPI with momentum (mapi_minibatch): X N x D fp32 samples, batch
+    T x s int32 row indices (the caller's draws), w0 D, w_prev0 the momentum vector of a continued run (None:
+    w_{-1} = 0).  norms[t] = ||w_{t+1}||_1 before normalisation; the `deltas` field carries the momentum
+    vector after the last step (w_prev, for continuing).  Synchronises the stream."""
+    torch = _torch()
+    N, D, ldx = _matrix(X, "X")
+    _need(batch, "batch", torch.int32)
+    if batch.dim() != 2 or not batch.is_contiguous():
+        raise ValueError("batch must be a contiguous (T, s) int32 tensor")
+    T, s = batch.shape
+    _need(w0, "w0", torch.float32, (D,))
+    if w_prev0 is not None:
+        _need(w_prev0, "w_prev0", torch.float32, (D,))
+    dev = X.device
+    w = torch.empty(D, dtype=torch.float32, device=dev)
+    wl2 = torch.empty(D, dtype=torch.float32, device=dev) if want_l2 else None
+    wprev = torch.empty(D, dtype=torch.float32, device=dev)
+    norms = torch.zeros(max(T, 1), dtype=torch.float32, device=dev)
+    ws, need = _workspace(WS_MINIBATCH, D, s, T, device=dev, ws=ws)
+    done = ctypes.c_int32(0)
+    st = load().mapi_minibatch(gram, _ptr(X), N, D, ldx, _ptr(batch), int(s), int(T), float(beta), _ptr(w0),
+                               _ptr(w_prev0), _ptr(w), _ptr(wl2), _ptr(wprev), _ptr(norms), ctypes.byref(done),
+                               _ptr(ws), need, _stream(stream))
+    _check(st, done.value)
+    k = done.value
+    return IterResult(w, wl2, norms[:k], wprev, k)
+
 
 class PlanInfo(ctypes.Structure):
     """mapi_csr_plan_info (include/mapi.h): sizes of a segmented ranking plan."""

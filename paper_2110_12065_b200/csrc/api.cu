@@ -16,6 +16,7 @@
 #include "../../include/mapi.h"
 #include "host_common.h"
 #include "csr_plan.h"
+#include "minibatch.h"
 #include "batched.cuh"
 #include "bulk.cuh"
 #include "resident.cuh"
@@ -593,6 +594,7 @@ size_t mapi_workspace_size(int32_t op, int64_t n, int64_t nnz, int32_t k) {
     case MAPI_WS_CSR_PLAN: return mapi_plan::plan_bytes_bound(n, nnz);
     case MAPI_WS_CSR_PLAN_BUILD: return mapi_plan::plan_build_ws_bytes(n, nnz);
     case MAPI_WS_RANK_CSR_PLAN: return mapi_plan::rank_plan_ws_bytes(n, nnz);
+    case MAPI_WS_MINIBATCH: return mapi_mb::minibatch_ws_bytes(n, nnz, k);  // n = D, nnz = s, k = T
     }
     return 0;
 }

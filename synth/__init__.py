@@ -358,3 +358,19 @@ def random_vector(n, seed, kind="normal"):
         v[u < 0.05] = 0.0
         v[(u >= 0.05) & (u < 0.08)] = -0.0
     return v.astype(np.float32)
+
+
+def stochastic_pca(N=10**6, D=10, gap=0.1, seed=7):
+    """The synthetic eigen-gap dataset of the paper's stochastic-PCA comparison: X = U Sigma V^T with
+    random orthonormal U (N x D), V (D x D) and Sigma = diag(1, sqrt(1 - gap), ..., sqrt(1 - gap)), so
+    C = X^T X has eigen-gap `gap`.  Returns X (fp32, one cast) and u1 = V[:, 0] (fp64).  Input recipe only."""
+    g = np.random.default_rng(seed)
+    U, _ = np.linalg.qr(g.standard_normal((N, D)))
+    V, _ = np.linalg.qr(g.standard_normal((D, D)))
+    sig = np.array([1.0] + [np.sqrt(1.0 - gap)] * (D - 1))
+    return ((U * sig) @ V.T).astype(np.float32), V[:, 0].copy()
+
+
+def batch_draws(N, T, s, seed=8):
+    """Algorithm 3 step 3: T mini-batches of s i.i.d. uniform row indices (with replacement), int32."""
+    return np.random.default_rng(seed).integers(0, N, (T, s)).astype(np.int32)

@@ -616,6 +616,23 @@ def test_minibatch_mapi_full_batch_no_momentum_is_algorithm_1(orc):
     np.testing.assert_allclose(got.norms, ref.norms, rtol=1e-12)
 
 
+def test_minibatch_mapi_continuation(orc):
+    """The optional (w_prev0, w_prev) state changes no step: T1 steps, then T2 more from the returned
+    (w, w_prev), reproduce T1 + T2 steps exactly; and w_prev after one step from w_{-1} = 0 is w_0 / s_0
+    (Alg. 3 step 5, verbatim: both vectors divided by ||w_{t+1}||_1, R15)."""
+    r = np.random.default_rng(11)
+    X = r.standard_normal((40, 5))
+    idx = r.integers(0, 40, (9, 6))
+    w0 = r.standard_normal(5)
+    full = orc.minibatch_mapi(X, idx, 0.3, w0)
+    a = orc.minibatch_mapi(X, idx[:4], 0.3, w0)
+    b = orc.minibatch_mapi(X, idx[4:], 0.3, a.w, w_prev0=a.w_prev)
+    assert np.array_equal(b.w, full.w) and np.array_equal(b.w_prev, full.w_prev)
+    assert np.array_equal(np.concatenate([a.norms, b.norms]), full.norms)
+    one = orc.minibatch_mapi(X, idx[:1], 0.3, w0)
+    np.testing.assert_allclose(one.w_prev, w0 / one.norms[0], rtol=1e-15)
+
+
 def test_minibatch_mapi_degenerate_and_bad_input(orc):
     X = np.zeros((5, 3))
     res = orc.minibatch_mapi(X, np.zeros((2, 2), np.int64), 0.1, np.ones(3) / np.sqrt(3))
