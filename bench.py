@@ -44,6 +44,9 @@ WORKLOADS = {
               "(seed 6), C = V (+) V^T / (N-1), 16384^2 fp32 output",
     "mincov_k4096": "NEXT-1 MAVP matrix product, ALU-bound regime: 4096 x 8192 N(0,1) rows (seed 7), "
                     "C = V (+) V^T / 8192, 4096^2 output",
+    "alg3": "NEXT-4 Alg. 3 mini-batch MAPI with momentum at the paper's shape (P:264): X = U Sigma V^T, "
+            "N = 10^6, D = 10, eigen-gap 0.1 (seed 7), s = 128 i.i.d. draws per step (seed 8), beta = 0.225, "
+            "T = 100 iterations per call",
     "alg2": "NEXT-2 Alg. 2 image reconstruction end to end (steps 3-8): 10 occluded 128x128 synthetic copies "
             "(seed 6), min-covariance, 2 x 100 MAPI iterations, MAVP deflation, reconstruction",
 }
@@ -530,6 +533,35 @@ def build_alg2(args, m, dev, stream):
                 oracle=None)
 
 
+def build_alg3(args, m, dev, stream):
+    import torch
+
+    import synth
+
+    N, D, s_, T, beta = 10**6, 10, 128, 100, 0.225
+    X, _ = synth.stochastic_pca(N=N, D=D, seed=7)
+    Xd = torch.from_numpy(X).to(dev)
+    idx = torch.from_numpy(synth.batch_draws(N, T, s_, seed=8)).to(dev)
+    w0 = np.random.default_rng(1).standard_normal(D)
+    w0d = torch.from_numpy((w0 / np.linalg.norm(w0)).astype(np.float32)).to(dev)
+    gram = 2 if args.op == "dot" else 0
+    ws = torch.empty(int(m.workspace_size(m.WS_MINIBATCH, D, s_, T)), dtype=torch.uint8, device=dev)
+
+    def step():
+        m.minibatch(Xd, idx, beta, w0d, gram=gram, want_l2=False, ws=ws)
+        return T
+
+    terms = float(T) * (s_ + 1) * D * D  # MAVP terms per call: the batch gram (s D^2) + step 4 (D^2) per iteration
+    return Work(step=step, unit="iterations/s", per_launch=terms, bytes_per_unit=terms / T, bound="alu",
+                kernel="mapi_minibatch: k_minibatch_gram (all M_t in parallel) + k_minibatch_reduce + "
+                       "k_minibatch_iterate (one CTA, the dependent chain; latency-bound: ~1.8 us per iteration)",
+                whole_step=True,
+                config={"workload": f"alg3: {WORKLOADS['alg3']}", "N": N, "D": D, "s": s_, "T": T, "beta": beta,
+                        "gram": "dot" if gram else "min1",
+                        "l2_flush": "none: 12,900 terms per iteration, a latency-bound dependent chain"},
+                oracle=("alg3", X, idx.cpu().numpy(), beta, w0d.cpu().numpy(), "dot" if gram else "min1"))
+
+
 def build_sharded(args, m, dev, stream, fused=False, sym=False):
     """cfg3 over the ranks (paper_2110_12065_b200.sharded).  sym: K2sp, K2s's upper-triangle
     task list split over the ranks, one persistent kernel per rank exchanging partial y vectors in-kernel
@@ -603,7 +635,7 @@ def build_sharded(args, m, dev, stream, fused=False, sym=False):
                 A=A_local, b0=b0, iters=iters, oracle=None, sharded=True, run=run)
 
 
-BUILDERS = {"cfg1": build_dense, "alg2": build_alg2, "cfg3": build_dense, "cfg2": build_pca, "cfg4": build_batched,
+BUILDERS = {"cfg1": build_dense, "alg2": build_alg2, "alg3": build_alg3, "cfg3": build_dense, "cfg2": build_pca, "cfg4": build_batched,
             "cfg5": build_rank, "mincov": build_mincov, "mincov_k4096": build_mincov}
 
 
@@ -732,7 +764,20 @@ def run_mapi(args, rank, world, local_rank):
         out["full_matrix_path"] = {"kernel": "k_iterate_coop (K2c, mapi_iterate: all n^2 entries read)",
                                    "value": fu * world / (fms / 1e3), "unit": work.unit, "steps": fsteps,
                                    "ms_per_step": fms / fsteps,
-                                   "hbm_gbs": work.full_bytes * fu * world / (fms / 1e3) / 1e9}
+                                   "hbm_gbs": work.full_bytes * fu * world / (fms / 1e3) / 1e9,
+                                   "bytes_per_iteration": work.full_bytes,
+                                   "note": "SURVEY 8(d) / BASELINE.md count these full-matrix bytes "
+                                           "(4,294,967,296 B + w, y per cfg3 iteration; their 1,525 it/s ceiling is "
+                                           "this read at the measured copy peak); a read-only stream can exceed "
+                                           "the copy (read + write) peak"}
+        out["full_matrix_path"]["frac_of_measured_copy_peak"] = out["full_matrix_path"]["hbm_gbs"] / (peak * world)
+        out["full_matrix_path"]["frac_of_read_ceiling_7200"] = out["full_matrix_path"]["hbm_gbs"] / (7200.0 * world)
+        if "roofline" in out and out["roofline"].get("bound") == "hbm":
+            # the builder's measured read-only streaming ceiling on this B200 (DESIGN.md 6 K2c: 7.2 TB/s)
+            out["roofline"]["frac_of_read_ceiling_7200"] = out["roofline"]["achieved"] / (7200.0 * world)
+            out["roofline"]["bytes_note"] = ("K2s reads the upper triangle of the symmetric A once per iteration "
+                                             "(2,147,614,720 B + w, y) and forms all n^2 terms: achieved uses the "
+                                             "triangle's bytes, not SURVEY 8(d)'s full-matrix count")
     if getattr(work, "extra", None) is not None:
         out.update(work.extra())
     if e0 is not None and e1 is not None and e1 > e0:
@@ -745,7 +790,9 @@ def run_mapi(args, rank, world, local_rank):
         else:
             out["e2e"] = e2e_dense(args, m, work.A, work.b0, work.iters, dev, stream, world, dist)
     if not args.no_cpu_baseline and world == 1 and rank == 0 and work.oracle is not None:
-        if work.oracle[0] == "dense":
+        if work.oracle[0] == "alg3":
+            out["cpu_baseline"] = cpu_baseline_alg3(args, *work.oracle[1:])
+        elif work.oracle[0] == "dense":
             out["cpu_baseline"] = cpu_baseline_dense(args, *work.oracle[1:])
         else:
             out["cpu_baseline"] = cpu_baseline_rank(args, work.oracle[1])
@@ -899,6 +946,21 @@ def cpu_baseline_rank(args, cfg):
     dt = time.perf_counter() - t0
     return {"value": r.iters_done / dt, "unit": "iterations/s", "cores": oracle.num_threads(), "kind": "oracle",
             "sample": f"{r.iters_done} of 200 fixed ranking iterations on the full cfg5 graph ({dt:.1f} s)"}
+
+
+def cpu_baseline_alg3(args, X, idx, beta, w0, gram):
+    import oracle
+
+    oracle.build()
+    X64, idx64, w64 = X.astype(np.float64), idx.astype(np.int64), w0.astype(np.float64)
+    oracle.minibatch_mapi(X64, idx64, beta, w64, gram=gram)  # warm-up
+    reps, t0 = 0, time.perf_counter()
+    while time.perf_counter() - t0 < min(args.cpu_seconds, 5.0):
+        r = oracle.minibatch_mapi(X64, idx64, beta, w64, gram=gram)
+        reps += 1
+    dt = time.perf_counter() - t0
+    return {"value": reps * r.iters_done / dt, "unit": "iterations/s", "cores": 1, "kind": "oracle",
+            "sample": f"{reps} whole {r.iters_done}-iteration runs of the fp64 oracle (serial C, {dt:.1f} s)"}
 
 
 def traffic_from_profiles(workload):
