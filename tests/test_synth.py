@@ -61,3 +61,15 @@ def test_covariance_like_rows_is_a_slice_of_the_full_matrix():
     full = synth.covariance_like(F, 0.25, d, block=32)
     for row0, row1 in ((0, 32), (32, 64), (64, 96), (32, 96)):
         np.testing.assert_array_equal(synth.covariance_like_rows(F, 0.25, d, row0, row1, block=32), full[row0:row1])
+
+
+def test_stochastic_pca_recipe():
+    """C = X^T X has eigenvalues {1, 0.9 x 9} (eigen-gap 0.1) and u1 is its dominant eigenvector."""
+    X, u1 = synth.stochastic_pca(N=4000, D=10, gap=0.1, seed=7)
+    assert X.dtype == np.float32 and X.shape == (4000, 10)
+    ev, V = np.linalg.eigh(X.astype(np.float64).T @ X.astype(np.float64))
+    np.testing.assert_allclose(ev, [0.9] * 9 + [1.0], rtol=1e-5)
+    assert abs(V[:, -1] @ u1) > 1 - 1e-5
+    idx = synth.batch_draws(4000, 7, 33, seed=8)
+    assert idx.dtype == np.int32 and idx.shape == (7, 33) and idx.min() >= 0 and idx.max() < 4000
+    assert np.array_equal(idx, synth.batch_draws(4000, 7, 33, seed=8))
