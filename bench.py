@@ -9,7 +9,8 @@ ranks with the matrix resident in HBM; `e2e` = the same through `mapi_iterate_ho
 HOST buffers (H2D + 100 iterations + result D2H per step).  Under torchrun (N > 1) the default is
 K2sp: ONE symmetric problem whose upper-triangle task list is split over the ranks, the partial y
 vectors exchanged inside the kernel over NVLink P2P (strong scaling); --mode p2p /
-sharded / replicas select the row-sharded K2p, the NCCL all-gather comparator or independent replicas.
+sharded / replicas select the row-sharded K2p, the NCCL all-gather comparator or independent replicas;
+--workload cfg4 at N > 1 splits the batch's k independent runs over the ranks (no collective).
 
 --impl reference times the fp64 CPU oracle (oracle/, test infrastructure) on the same workload,
 a bounded sample per step, on rank 0 only.
@@ -320,9 +321,18 @@ def build_batched(args, m, dev, stream):
 
     import synth
 
+    from paper_2110_12065_b200.sharded import vector_partition
+
     cfg = synth.cfg4(device=dev)
     A = cfg["A"]
     B0 = torch.from_numpy(cfg["B0"]).to(dev)
+    k_all = B0.shape[0]
+    # N > 1: the k independent runs are split over the ranks (no data-path collective); every
+    # rank holds A.  The job is the whole batch: total work fixed -> "strong" scaling of the batch.
+    k0, k1 = vector_partition(k_all, args.world, args.rank)
+    if k1 <= k0:
+        raise SystemExit(f"cfg4: {k_all} start vectors cannot be split over {args.world} ranks")
+    B0 = B0[k0:k1].contiguous()
     n, k, T = A.shape[0], B0.shape[0], cfg["iters"]
     ws, need = m._workspace(m.WS_ITERATE_BATCHED, n, 0, k, device=dev)
     W = torch.empty_like(B0)
@@ -339,9 +349,9 @@ def build_batched(args, m, dev, stream):
     return Work(step=step, unit="vector-iterations/s", per_launch=float(n) * n * k * T,
                 bytes_per_unit=4.0 * n * n / k, bound="alu",
                 kernel="k_batched_partial + reduce + normalize loop (events around the iteration loop)",
-                config={"workload": f"cfg4: {WORKLOADS['cfg4']}", "n": n, "k": k, "iters": T, "op": "min1",
-                        "l2_flush": "inputs larger than L2 (1 GiB matrix)"},
-                oracle=("dense", A, B0[0].contiguous(), T))
+                config={"workload": f"cfg4: {WORKLOADS['cfg4']}", "n": n, "k": k_all, "k_per_rank": k, "iters": T,
+                        "op": "min1", "l2_flush": "inputs larger than L2 (1 GiB matrix)"},
+                oracle=("dense", A, B0[0].contiguous(), T), ksplit=args.world > 1)
 
 
 def build_rank(args, m, dev, stream):
@@ -683,6 +693,10 @@ def run_mapi(args, rank, world, local_rank):
                                   "p2p": f"K2p x{world}: row blocks, y rows exchanged in-kernel",
                                   "sharded": f"row-sharded x{world}: NCCL all-gather of y ({4 * 32768} B) per "
                                              "iteration"}[mode]
+        out["scaling"] = "strong"
+    elif getattr(work, "ksplit", False):
+        cfg_out["parallelism"] = (f"k-split x{world}: the batch's independent runs partitioned over the ranks "
+                                  "(iterate_batched_sharded), no data-path collective")
         out["scaling"] = "strong"
     else:
         cfg_out["parallelism"] = f"replicas x{world} (independent problems, no collective)" if dist else "single GPU"

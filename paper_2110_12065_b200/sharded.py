@@ -9,6 +9,9 @@ of Algorithm 1:
                                            every rank -> bitwise identical w and stop decision everywhere
                                            (no separate all-reduce of s is needed)
 
+`iterate_batched_sharded` partitions the k independent runs of the batched path (cfg4) over the ranks — no
+data-path collective at all.
+
 The local mat-vec, the all-gather and the normalisation are injectable so that the orchestration (the
 partition, the gather order, the per-rank agreement) is tested with gloo on CPU (tests/test_dist_host.py).
 The product path passes the CUDA entry points and torch.distributed over NCCL.
@@ -33,6 +36,49 @@ def row_partition(n: int, world: int, rank: int):
         raise ValueError(f"row-sharded MAPI needs n ({n}) divisible by the world size ({world})")
     per = n // world
     return rank * per, (rank + 1) * per
+
+
+def vector_partition(k: int, world: int, rank: int):
+    """Contiguous balanced slice [k0, k1) of k independent start vectors for `rank` (k need not divide)."""
+    if not (0 <= rank < world):
+        raise ValueError(f"rank {rank} outside a world of {world}")
+    return rank * k // world, (rank + 1) * k // world
+
+
+def iterate_batched_sharded(A, B0, iters: int, tol: float = 0.0, op: int = 0, group=None, run_local=None,
+                            gather: bool = False):
+    """Batched MAPI (P:69-70 with p = k columns, BASELINE configs[3]) over the ranks: the k runs are
+    independent problems on the same A, so they partition with NO data-path collective: every
+    rank holds A (1 GiB at cfg4) and runs its contiguous slice of the start vectors through
+    mapi_iterate_batched.  B0: the FULL k x n starts (every rank slices its own rows).  Returns (k0, k1,
+    result) with the local slice's BatchedResult, or, with gather=True, every rank's W / norms / iteration
+    counts all-gathered afterwards (one collective after the run, off the hot path; needs k % world == 0).
+    run_local(A, B0_local, iters, tol, op) is injectable for the CPU (gloo) test."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    k = B0.shape[0]
+    k0, k1 = vector_partition(k, world, rank)
+    if run_local is None:
+        from . import iterate_batched as run_local
+    res = run_local(A, B0[k0:k1].contiguous(), iters, tol, op) if k1 > k0 else None
+    if not gather or world == 1:
+        return k0, k1, res
+    if k % world != 0:
+        raise ValueError(f"gather=True needs k ({k}) divisible by the world size ({world})")
+    W = torch.empty_like(B0)
+    dist.all_gather_into_tensor(W, res.W.contiguous(), group=group)
+    T_, kl = res.norms.shape
+    norms = torch.empty((world * T_, kl), dtype=res.norms.dtype, device=res.norms.device)
+    dist.all_gather_into_tensor(norms, res.norms.contiguous(), group=group)
+    norms = norms.view(world, T_, kl)
+    done = torch.tensor(list(res.iters_done), dtype=torch.int32, device=B0.device)
+    done_all = torch.empty(k, dtype=torch.int32, device=B0.device)
+    dist.all_gather_into_tensor(done_all, done, group=group)
+    # norms are iters x k_local per rank: back to iters x k, vector-major as on one GPU
+    return k0, k1, (W, torch.cat(list(norms), dim=1), done_all)
 
 
 @dataclass

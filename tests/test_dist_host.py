@@ -130,6 +130,74 @@ def test_row_sharded_mapi_gloo_world2():
     assert out[0][2] == 12
 
 
+def _batched_worker(rank, world, port, q):
+    import sys
+
+    import numpy as np
+    import torch
+    import torch.distributed as tdist
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle
+    from paper_2110_12065_b200 import BatchedResult
+    from paper_2110_12065_b200.sharded import iterate_batched_sharded
+
+    n, k, T = 40, 6, 9
+    r = np.random.default_rng(5)
+    A = (r.standard_normal((n, n)) + 2 * np.eye(n)).astype(np.float32)
+    B0 = r.standard_normal((k, n)).astype(np.float32)
+    B0 /= np.linalg.norm(B0, axis=1, keepdims=True)
+
+    def run_local(A_, B_, iters, tol, op):  # CPU stand-in for mapi_iterate_batched (test only): the oracle per vector
+        rs = [oracle.mapi(A_.numpy(), b.numpy(), iters) for b in B_]
+        return BatchedResult(torch.from_numpy(np.stack([x.w for x in rs]).astype(np.float32)),
+                             torch.from_numpy(np.stack([x.norms for x in rs], 1).astype(np.float32)), None,
+                             [x.iters_done for x in rs])
+
+    k0, k1, (W, norms, done) = iterate_batched_sharded(torch.from_numpy(A), torch.from_numpy(B0), T, run_local=run_local,
+                                                       gather=True)
+    q.put((rank, k0, k1, W.numpy().copy(), norms.numpy().copy(), done.numpy().copy()))
+    tdist.barrier()
+    tdist.destroy_process_group()
+
+
+def test_batched_k_sharded_gloo_world2():
+    """cfg4's k independent runs split over two ranks (no data-path collective): the slices tile [0, k), and the
+    gathered W / norms equal the oracle's per-vector MAPI in the single-GPU (vector-major) layout."""
+    import numpy as np
+
+    import oracle
+    from paper_2110_12065_b200.sharded import vector_partition
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_batched_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = {r: rest for r, *rest in [q.get(timeout=180) for _ in range(2)]}
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert (out[0][0], out[0][1], out[1][0], out[1][1]) == (0, 3, 3, 6)
+    np.testing.assert_array_equal(out[0][2], out[1][2])
+    n, k, T = 40, 6, 9
+    r = np.random.default_rng(5)
+    A = (r.standard_normal((n, n)) + 2 * np.eye(n)).astype(np.float32)
+    B0 = r.standard_normal((k, n)).astype(np.float32)
+    B0 /= np.linalg.norm(B0, axis=1, keepdims=True)
+    for j in range(k):
+        ref = oracle.mapi(A, B0[j], T)
+        np.testing.assert_allclose(out[0][2][j], ref.w, rtol=2e-6, atol=1e-7)
+        np.testing.assert_allclose(out[0][3][:, j], ref.norms, rtol=1e-6)
+    assert list(out[0][4]) == [T] * k
+    for world in (1, 2, 3, 5, 8):  # the slices tile [0, k) for any world, k not divisible included
+        cuts = [vector_partition(7, world, rr) for rr in range(world)]
+        assert cuts[0][0] == 0 and cuts[-1][1] == 7 and all(a[1] == b[0] for a, b in zip(cuts, cuts[1:]))
+
+
 def test_row_partition():
     from paper_2110_12065_b200.sharded import row_partition
 
