@@ -778,6 +778,10 @@ mapi_status sym_launch(const Device& d, int32_t op, const float* A, int64_t n, i
     // the w region holds y of the owned rows
     a.wtag = reinterpret_cast<unsigned long long*>(W.y);
     a.yg = W.w;
+    {  // investigation switch; the default was chosen from the sweep in profiles/r02_probe_k2s_prefetch.log
+        static const int pf = getenv("MAPI_SYM_PREFETCH") ? atoi(getenv("MAPI_SYM_PREFETCH")) : kSymPrefetchRows;
+        a.prefetch_rows = std::max(0, std::min(pf, kSymRB));
+    }
     MAPI_CUDA(cudaMemsetAsync(W.y, 0, sizeof(unsigned long long) * 2 * (size_t)n, s));
     void* args[] = {&a};
     if (timer) timer->start();
@@ -1589,6 +1593,7 @@ mapi_status mapi_iterate_sym_sharded(int32_t op, const float* A_local, int64_t r
     a.pcol = partials + (size_t)sym_nc(n) * (size_t)((n + 31) & ~int64_t(31));
     a.wtag = reinterpret_cast<unsigned long long*>(W.y);
     a.yg = W.w;
+    a.prefetch_rows = 0;
     x.row0 = r0; x.tlo = tlo; x.thi = thi; x.rank = rank; x.world = world;
     x.peers = reinterpret_cast<const unsigned long long*>(peers);
     x.epoch0 = epoch0; x.flag_base = flag_base;

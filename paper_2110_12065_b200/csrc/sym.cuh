@@ -41,6 +41,7 @@ namespace mapi {
 
 constexpr int kSymRB = 128;        // rows per task (column-partial chain length: T1's 128-term limit)
 constexpr int kSymCC = 256;        // columns per task (one 1 KB row chunk per warp row)
+constexpr int kSymPrefetchRows = 16;  // default of SymArgs::prefetch_rows (sweep: profiles/r02_probe_k2s_prefetch.log)
 constexpr int kSymNW = 16;         // warps per CTA
 constexpr int kSymThreads = kSymNW * 32;
 constexpr int kSymCR = kSymCC / kSymRB;  // chunks per row block (2): tasks of block b start at chunk b / 2
@@ -51,6 +52,7 @@ struct SymArgs {
     float* pcol;  // [nb][n] column partials
     unsigned long long* wtag;  // [2][n] tagged w words ((t + 1) << 32 | bits(w_t)), zeroed per call
     float* yg;                 // [n] y of the owned rows
+    int32_t prefetch_rows;     // K2s: rows per first-wave task prefetched into L2 across the epilogue (0: off)
 };
 
 __host__ __device__ inline int64_t sym_nb(int64_t n) { return (n + kSymRB - 1) / kSymRB; }
@@ -458,6 +460,27 @@ __global__ void __launch_bounds__(kSymThreads, 1) k_iterate_sym(SymArgs sa) {
         });
         const double cta_abs = block_sum(abs_part, red);  // its barriers also publish yg to this CTA
         if (tid == 0) slotA[(t & 1) * gridDim.x + blockIdx.x] = cta_abs;
+        // HBM is idle from here until the next tasks start (barrier, s_t, the w publish: ~16 us): pull the
+        // first rows of the next iteration's first wave of tasks (counter values 0 .. G kSymNW - 1) into L2
+        // (bulk prefetches: no registers, nothing to wait for; A does not depend on w)
+        if (sa.prefetch_rows > 0 && t + 1 < p.iters) {
+            const int64_t task = (int64_t)blockIdx.x * kSymNW + (tid >> 5);
+            if (task < ntasks) {
+                const int64_t nbk = sym_nb(n), nck = sym_nc(n);
+                int64_t lo = 0, hi = nbk - 1;  // row block: last b with start(b) <= task
+                while (lo < hi) {
+                    const int64_t mid = (lo + hi + 1) >> 1;
+                    if (sym_task_start(mid, nck) <= task) lo = mid;
+                    else hi = mid - 1;
+                }
+                const int64_t c0 = (lo / kSymCR + (task - sym_task_start(lo, nck))) * kSymCC, j0 = lo * kSymRB;
+                const uint32_t bytes = (uint32_t)min((int64_t)kSymCC, n - c0) * 4u;
+                for (int r = tid & 31; r < sa.prefetch_rows && r < kSymRB && j0 + r < n; r += 32) {
+                    const float* src = p.A + (j0 + r) * p.lda + c0;
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+                }
+            }
+        }
         SYM_STAMP(t, 3);
         grid_barrier(p.bar, ++epoch * gridDim.x);
         SYM_STAMP(t, 4);
