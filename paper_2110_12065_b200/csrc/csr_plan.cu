@@ -79,12 +79,14 @@ inline int64_t nunits_bound(int64_t ntiles, int64_t nseg) { return ntiles / kUni
 // [hdr 256][perm n i32: plan position -> node id][segb nseg+1 i32: padded word start of each segment]
 // [units 3 nunits i32: phase A work units (first tile, end tile, segment) in scheduling order]
 // [fbase ntiles+1 i32: first fragment of each tile][rsp n+1 i32: plan position -> its first slot]
-// [words nwords u16: source offsets][wflags nwords/16 u16: end-of-fragment flags of each lane chunk of 16 words]
+// [words nwords u16: source offsets][wflags nwords/16 u32: per lane chunk of 16 words, the end-of-fragment flags
+//  (low 16 bits) and the number of fragments that end in the tile's preceding chunks (high 16 bits)]
 // [bfrag nfrag i32: fragments in (batch, fragment) order][brel nfrag u16: their slot within the batch]
 // [bstart nbatch+1 i32: batch rows]
 struct PlanView {
     int32_t *perm, *segb, *units, *fbase, *rsp;
-    uint16_t *words, *wflags;
+    uint16_t* words;
+    uint32_t* wflags;
     int32_t* bfrag;
     uint16_t* brel;
     int32_t* bstart;
@@ -99,7 +101,7 @@ inline PlanView plan_view(void* plan, int64_t n, int64_t nseg, int64_t nunits, i
     v.fbase = reinterpret_cast<int32_t*>(p); p += al256(4 * (size_t)(ntiles + 1));
     v.rsp = reinterpret_cast<int32_t*>(p); p += al256(4 * (size_t)(n + 1));
     v.words = reinterpret_cast<uint16_t*>(p); p += al256(2 * (size_t)std::max<int64_t>(nwords, 1));
-    v.wflags = reinterpret_cast<uint16_t*>(p); p += al256(2 * (size_t)std::max<int64_t>(nwords / kLaneW, 1));
+    v.wflags = reinterpret_cast<uint32_t*>(p); p += al256(4 * (size_t)std::max<int64_t>(nwords / kLaneW, 1));
     v.bfrag = reinterpret_cast<int32_t*>(p); p += al256(4 * (size_t)std::max<int64_t>(nfrag, 1));
     v.brel = reinterpret_cast<uint16_t*>(p); p += al256(2 * (size_t)std::max<int64_t>(nfrag, 1));
     v.bstart = reinterpret_cast<int32_t*>(p);
@@ -109,7 +111,7 @@ inline size_t plan_bytes_exact(int64_t n, int64_t nseg, int64_t nunits, int64_t 
     const int64_t ntiles = nwords / kTileW;
     return 256 + al256(4 * (size_t)n) + al256(4 * (size_t)(nseg + 1)) + al256(12 * (size_t)std::max<int64_t>(nunits, 1)) +
            al256(4 * (size_t)(ntiles + 1)) + al256(4 * (size_t)(n + 1)) + al256(2 * (size_t)std::max<int64_t>(nwords, 1)) +
-           al256(2 * (size_t)std::max<int64_t>(nwords / kLaneW, 1)) +
+           al256(4 * (size_t)std::max<int64_t>(nwords / kLaneW, 1)) +
            al256(4 * (size_t)std::max<int64_t>(nfrag, 1)) + al256(2 * (size_t)std::max<int64_t>(nfrag, 1)) +
            al256(4 * (size_t)(nbatch + 1));
 }
@@ -309,8 +311,11 @@ __global__ void kp_frag(int64_t nnz, const uint64_t* __restrict__ ek, const uint
 __global__ void kp_fill_words(int64_t nwords, uint16_t* __restrict__ words) {
     GRID_STRIDE(k, nwords) words[k] = kDummy;
 }
-// per lane chunk of 16 words: the end flags as a 16-bit mask; the words keep only the source offset
-__global__ void kp_wflags(int64_t nchunks, uint16_t* __restrict__ words, uint16_t* __restrict__ wflags) {
+// per lane chunk of 16 words: the end flags as a 16-bit mask and, in the high half, the number of fragments
+// ending in the tile's preceding chunks (the lane's first position in the warp's fragment stage: static, so
+// the run kernel needs no warp scan of the counts); the words keep only the source offset.  A warp of this
+// kernel covers exactly one tile (32 consecutive chunks: the block size and nchunks are multiples of 32).
+__global__ void kp_wflags(int64_t nchunks, uint16_t* __restrict__ words, uint32_t* __restrict__ wflags) {
     GRID_STRIDE(ch, nchunks) {
         uint32_t m = 0;
         for (int i = 0; i < kLaneW; ++i) {
@@ -318,7 +323,14 @@ __global__ void kp_wflags(int64_t nchunks, uint16_t* __restrict__ words, uint16_
             m |= (uint32_t)(w >> 15) << i;
             words[ch * kLaneW + i] = (uint16_t)(w & 0x7fffu);
         }
-        wflags[ch] = (uint16_t)m;
+        const int lane = threadIdx.x & 31;
+        int c = __popc(m);
+        const int cnt = c;
+        for (int off = 1; off < 32; off <<= 1) {
+            const int co = __shfl_up_sync(0xffffffffu, c, off);
+            if (lane >= off) c += co;
+        }
+        wflags[ch] = m | ((uint32_t)(c - cnt) << 16);
     }
 }
 
@@ -421,7 +433,8 @@ struct RunArgs {
     int32_t nseg, iters, nunits, nbatch;
     float tol;
     const int32_t *perm, *segb, *units, *fbase, *rsp, *bstart, *bfrag;
-    const uint16_t *brel, *words, *wflags;
+    const uint16_t *brel, *words;
+    const uint32_t* wflags;
     const float *cap, *bg, *b0;
     float* deltas;
     unsigned long long* trace;  // optional: phase stamps (globaltimer), see PLAN_STAMP
@@ -482,8 +495,8 @@ __device__ __forceinline__ void block_sum2(double& a, double& b, double* red) {
 
 // one 512-word tile: 16 words per lane (lane l: words 16 l .. 16 l + 15, end flags fl), gathers from the shared
 // segment (shared address sb).  The lane's fragments are closed in word order into the warp's stage at their
-// fragment positions (an exclusive warp scan of the flag counts gives them), the run carried in from the
-// preceding lanes (a segmented warp scan of the lanes' open tails) is added to the lane's first fragment, and
+// fragment positions (static: the plan stores each lane's first position beside its flags), the run carried in
+// from the preceding lanes (a segmented warp scan of the lanes' open tails) is added to the lane's first fragment, and
 // the warp writes the stage to part[fb ..) with coalesced stores.  Returns the fp64 sum of the fragment sums
 // (lane partials of the fragment sums it stores, in fp32, one conversion per lane).
 __device__ __forceinline__ double plan_tile(const uint4 (&wd)[2], uint32_t fl, uint32_t sb, int32_t fb,
@@ -495,15 +508,10 @@ __device__ __forceinline__ double plan_tile(const uint4 (&wd)[2], uint32_t fl, u
         asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x[2 * h]) : "r"(sb + ((u[h] & 0xffffu) << 2)));
         asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x[2 * h + 1]) : "r"(sb + ((u[h] >> 16) << 2)));
     }
-    const int cnt = __popc(fl);
-    int c = cnt;  // inclusive warp scan of the flag counts
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-        const int co = __shfl_up_sync(0xffffffffu, c, off);
-        if (lane >= off) c += co;
-    }
-    const int total = __shfl_sync(0xffffffffu, c, 31);
-    const int before = c - cnt;
+    // fl: the lane's end-of-fragment flags (low half) and its first stage position (high half, from the plan)
+    const int cnt = __popc(fl & 0xffffu);
+    const int before = (int)(fl >> 16);
+    const int total = __shfl_sync(0xffffffffu, before + cnt, 31);
     // close the lane's fragments (the first one without the carried run); acc ends as the open tail
     float acc = 0.0f;
     float* st = stage + before;
@@ -515,7 +523,10 @@ __device__ __forceinline__ double plan_tile(const uint4 (&wd)[2], uint32_t fl, u
             acc = 0.0f;
         }
     }
-    // inclusive segmented scan over lanes of (has flag, open tail): the run carried into the next lane
+    // inclusive segmented scan over lanes of (has flag, open tail): the run carried into the next lane.  A
+    // lane is final once a flag has been seen within its reach (f) or its reach covers lane 0; with ~2.5
+    // fragment ends per lane that is the case for every lane after one or two of the five steps, and the
+    // remaining steps would change nothing: leave early (same values, bit for bit)
     int f = cnt > 0;
     float v = acc;
 #pragma unroll
@@ -526,6 +537,7 @@ __device__ __forceinline__ double plan_tile(const uint4 (&wd)[2], uint32_t fl, u
             if (!f) v = vo + v;
             f |= fo;
         }
+        if (__all_sync(0xffffffffu, f || lane < 2 * off)) break;
     }
     const float carry = __shfl_up_sync(0xffffffffu, v, 1);
     if (lane > 0 && cnt > 0) stage[before] += carry;
@@ -545,7 +557,7 @@ __device__ __forceinline__ double plan_tile(const uint4 (&wd)[2], uint32_t fl, u
 // with edits elsewhere in the kernel; ncu's source view of a slow build showed the first word load 15% of the
 // phase on the long scoreboard after the compiler had hoisted the flags / base loads above it
 // (profiles/r02_exp_k3s_tma_phaseb.log).
-__device__ __forceinline__ void tile_loads(const uint4* words4, const uint16_t* wflags, const int32_t* fbase,
+__device__ __forceinline__ void tile_loads(const uint4* words4, const uint32_t* wflags, const int32_t* fbase,
                                            int32_t tile, int lane, uint4 (&w)[2], uint32_t& fl, int32_t& fb) {
     const uint4* p = words4 + (int64_t)tile * (kTileW / 8) + 2 * lane;
     asm volatile("ld.global.cs.v4.u32 {%0, %1, %2, %3}, [%4];"
@@ -553,9 +565,7 @@ __device__ __forceinline__ void tile_loads(const uint4* words4, const uint16_t* 
     asm volatile("ld.global.cs.v4.u32 {%0, %1, %2, %3}, [%4];"
                  : "=r"(w[1].x), "=r"(w[1].y), "=r"(w[1].z), "=r"(w[1].w) : "l"(p + 1));
     asm volatile("ld.global.nc.s32 %0, [%1];" : "=r"(fb) : "l"(fbase + tile));
-    uint16_t f16;
-    asm volatile("ld.global.cs.u16 %0, [%1];" : "=h"(f16) : "l"(wflags + (int64_t)tile * 32 + lane));
-    fl = f16;
+    asm volatile("ld.global.cs.u32 %0, [%1];" : "=r"(fl) : "l"(wflags + (int64_t)tile * 32 + lane));
 }
 
 // trace layout: [64 iterations][4] CTA 0 stamps, then per CTA [4] sums over iterations 3..63 of the stamps'
