@@ -79,7 +79,8 @@ typedef enum {
     MAPI_WS_CSR_PLAN_BUILD = 15,          /* n, nnz: temporary workspace of mapi_csr_plan */
     MAPI_WS_RANK_CSR_PLAN = 16,           /* n, nnz: workspace of mapi_rank_csr_plan */
     MAPI_WS_ITERATE_HOST_MANY_SYM = 17,   /* n, k = iters; add 8 bytes per problem beyond 2 */
-    MAPI_WS_MINIBATCH = 18                /* n = D, nnz = s (batch size), k = T (iterations) */
+    MAPI_WS_MINIBATCH = 18,               /* n = D, nnz = s (batch size), k = T (iterations) */
+    MAPI_WS_RANK_CSR_SHARD = 19           /* n nodes, nnz = the rank's edges, k = m (the rank's rows) */
 } mapi_ws_op;
 
 /* y = A (op) x — the matrix extension of the MAVP (reading Q6: y_j uses ROW j):
@@ -366,6 +367,38 @@ mapi_status mapi_rank_csr_plan(int32_t op, const void *plan, const mapi_csr_plan
                                float *w_l2_out, float *deltas, int32_t *iters_done, void *ws, size_t ws_bytes,
                                mapi_stream_t stream);
 
+/* MAPI ranking with the destination rows PARTITIONED OVER RANKS (K3n; the ranking
+ * update of Eq. 13, exactly as mapi_rank_csr computes it).  Rank r owns the rows [row0, row0 + m):
+ * row_ptr_local (m + 1 int32, rebased so that row_ptr_local[0] == 0) and col_idx_local (nnz_local int32 GLOBAL
+ * source ids in [0, n)) are its part of the CSR-by-destination graph.  cap, bg (mapi_csr_prepare on the WHOLE
+ * graph) and b0 are full n-vectors on every rank; every rank keeps the full node state in its workspace and runs
+ * the same fixed-order node kernels on it, so s_t, w_t, delta_t and the stop decision are bitwise identical on
+ * all ranks.  One iteration t (t = 0, 1, ... in order) is three steps on ONE stream:
+ *   mapi_rank_csr_shard_rows(t):      e_t[row0, row0 + m) = the gather-sum over the rank's edges; *e_out
+ *                                     (host pointer, may be NULL) receives the DEVICE address of e_t (n floats);
+ *   the caller's collective:          all-gather the ranks' blocks of e_t in place (n * 4 bytes in total);
+ *   mapi_rank_csr_shard_normalize(t): sum_i e_i over all n (fixed order), s_t = n S_t + sum e, w_{t+1},
+ *                                     v_{t+1}, S_{t+1}, delta_t -> deltas[t] (device, nullable), iteration
+ *                                     count, stop flag (tol > 0 && delta_t < tol), DEGENERATE / NONFINITE.
+ * All three are ASYNCHRONOUS; once the stop flag or an error status is set every later step returns at once on
+ * the device.  mapi_rank_csr_shard_begin starts a run (state in ws; w_0 = b0 >= 0 else MAPI_ERR_NEGATIVE at
+ * finish).  mapi_rank_csr_shard_finish writes w_out (n, l1-unit; NULL: only read the status — the host's
+ * periodic stop check) and w_l2_out (nullable), *iters_done and *stopped (host, nullable), SYNCHRONISES
+ * `stream` and returns the run's status.  ws: mapi_workspace_size(MAPI_WS_RANK_CSR_SHARD, n, nnz_local, m),
+ * the same buffer for every call of a run.  m == 0 (a rank without rows) is valid. */
+mapi_status mapi_rank_csr_shard_begin(int64_t n, int64_t m, int64_t nnz_local, const int32_t *row_ptr_local,
+                                      const float *cap, const float *bg, const float *b0, void *ws, size_t ws_bytes,
+                                      mapi_stream_t stream);
+mapi_status mapi_rank_csr_shard_rows(int64_t n, int64_t m, int64_t row0, int64_t nnz_local,
+                                     const int32_t *row_ptr_local, const int32_t *col_idx_local, int32_t t,
+                                     float **e_out, void *ws, size_t ws_bytes, mapi_stream_t stream);
+mapi_status mapi_rank_csr_shard_normalize(int64_t n, int64_t m, int64_t nnz_local, const float *cap, const float *bg,
+                                          const float *b0, int32_t t, float tol, float *deltas, void *ws,
+                                          size_t ws_bytes, mapi_stream_t stream);
+mapi_status mapi_rank_csr_shard_finish(int64_t n, int64_t m, int64_t nnz_local, const float *b0, float *w_out,
+                                       float *w_l2_out, int32_t *iters_done, int32_t *stopped, void *ws,
+                                       size_t ws_bytes, mapi_stream_t stream);
+
 /* Optional preparation for the ranking path: relabel the nodes by DESCENDING out-degree (ties by ascending
  * id), so the most gathered sources get the lowest ids, which the gather kernel keeps in shared memory
  * (K3h).  perm_out[old] = new (n).  row_ptr_out (n+1) / col_idx_out (nnz): the same graph in the
@@ -411,7 +444,8 @@ mapi_status mapi_minibatch(int32_t gram_op, const float *X, int64_t N, int64_t D
  *   MAPI_WS_ITERATE_HOST_MANY: n, nnz = lda, k = iters (two slots; + 8 bytes per problem beyond 2).
  *   MAPI_WS_ITERATE_HOST_MANY_PACKED: n, k = iters (same, plus a packed buffer per slot).
  *   MAPI_WS_CSR_PLAN / MAPI_WS_CSR_PLAN_BUILD / MAPI_WS_RANK_CSR_PLAN: n, nnz.
- *   MAPI_WS_MINIBATCH: n = D, nnz = s, k = T. */
+ *   MAPI_WS_MINIBATCH: n = D, nnz = s, k = T.
+ *   MAPI_WS_RANK_CSR_SHARD: n nodes, nnz = the rank's edges, k = m (the rank's rows). */
 size_t mapi_workspace_size(int32_t op, int64_t n, int64_t nnz, int32_t k);
 
 const char *mapi_status_string(mapi_status status);

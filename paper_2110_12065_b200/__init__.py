@@ -28,7 +28,7 @@ MIN1, MIN2, DOT = 0, 1, 2  # DOT: regular product of Eq. (1), the RPI comparator
 (WS_MATVEC, WS_ITERATE, WS_ITERATE_BATCHED, WS_PCA_TOPK, WS_CSR_PREPARE, WS_RANK_CSR, WS_ITERATE_HOST,
  WS_MAVP_DEFLATE, WS_RECONSTRUCT, WS_ITERATE_SHARDED, WS_ITERATE_HOST_MANY,
  WS_ITERATE_HOST_MANY_PACKED, WS_ITERATE_SYM, WS_CSR_REORDER, WS_CSR_PLAN, WS_CSR_PLAN_BUILD,
- WS_RANK_CSR_PLAN, WS_ITERATE_HOST_MANY_SYM, WS_MINIBATCH) = range(19)
+ WS_RANK_CSR_PLAN, WS_ITERATE_HOST_MANY_SYM, WS_MINIBATCH, WS_RANK_CSR_SHARD) = range(20)
 STATUS = {0: "MAPI_OK", 1: "MAPI_ERR_NULL", 2: "MAPI_ERR_SHAPE", 3: "MAPI_ERR_BAD_PARAM",
           4: "MAPI_ERR_DEGENERATE", 5: "MAPI_ERR_NEGATIVE", 6: "MAPI_ERR_NONFINITE",
           7: "MAPI_ERR_WORKSPACE", 8: "MAPI_ERR_CUDA"}
@@ -77,6 +77,11 @@ def load():
             "mapi_pca_topk": (st, [i32, P, i64, i64, i32, i32, P, P, P, P, P, sz, P]),
             "mapi_csr_prepare": (st, [i64, i64, P, P, f32, P, P, P, sz, P]),
             "mapi_rank_csr": (st, [i64, i64, P, P, P, P, P, i32, f32, P, P, P, P, P, sz, P]),
+            "mapi_rank_csr_shard_begin": (st, [i64, i64, i64, P, P, P, P, P, sz, P]),
+            "mapi_rank_csr_shard_rows": (st, [i64, i64, i64, i64, P, P, i32, ctypes.POINTER(ctypes.c_void_p), P, sz,
+                                              P]),
+            "mapi_rank_csr_shard_normalize": (st, [i64, i64, i64, P, P, P, i32, f32, P, P, sz, P]),
+            "mapi_rank_csr_shard_finish": (st, [i64, i64, i64, P, P, P, P, P, P, sz, P]),
             "mapi_csr_reorder": (st, [i64, i64, P, P, P, P, P, P, sz, P]),
             "mapi_csr_plan": (st, [i64, i64, P, P, P, sz, ctypes.POINTER(PlanInfo), P, sz, P]),
             "mapi_rank_csr_plan": (st, [i32, P, ctypes.POINTER(PlanInfo), P, P, P, i32, f32, P, P, P, P, P, sz,

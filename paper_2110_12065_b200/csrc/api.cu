@@ -595,6 +595,7 @@ size_t mapi_workspace_size(int32_t op, int64_t n, int64_t nnz, int32_t k) {
     case MAPI_WS_CSR_PLAN_BUILD: return mapi_plan::plan_build_ws_bytes(n, nnz);
     case MAPI_WS_RANK_CSR_PLAN: return mapi_plan::rank_plan_ws_bytes(n, nnz);
     case MAPI_WS_MINIBATCH: return mapi_mb::minibatch_ws_bytes(n, nnz, k);  // n = D, nnz = s, k = T
+    case MAPI_WS_RANK_CSR_SHARD: return csr_rank_ws_bytes(n, nnz, k);  // n nodes, nnz = local edges, k = m
     }
     return 0;
 }
@@ -1242,6 +1243,91 @@ mapi_status mapi_rank_csr(int64_t n, int64_t nnz, const int32_t* row_ptr, const 
     st = csr_rank_finish(ws, n, nnz, s, iters_done);
     timer.harvest();
     if (st == MAPI_ERR_CUDA) return fail(st, "%s", csr_last_error());
+    if (st == MAPI_ERR_NEGATIVE) return fail(st, "b0 has a negative entry");
+    if (st == MAPI_ERR_DEGENERATE) return fail(st, "||G (+) w_t||_1 == 0");
+    if (st == MAPI_ERR_NONFINITE) return fail(st, "||G (+) w_t||_1 is not finite");
+    return st;
+}
+
+// ---- K3n: MAPI ranking with the destination rows partitioned over ranks (csr.cuh)
+static mapi_status shard_check(int64_t n, int64_t m, int64_t row0, int64_t nnz, const void* ws, size_t ws_bytes) {
+    if (n < 1 || n >= (int64_t)INT32_MAX) return fail(MAPI_ERR_SHAPE, "n (%lld) must be in [1, 2^31)", (long long)n);
+    if (nnz < 0 || nnz >= (int64_t)INT32_MAX)
+        return fail(MAPI_ERR_SHAPE, "nnz_local (%lld) must be in [0, 2^31)", (long long)nnz);
+    if (m < 0 || row0 < 0 || row0 + m > n)
+        return fail(MAPI_ERR_SHAPE, "rows [%lld, %lld) are not inside [0, %lld)", (long long)row0,
+                    (long long)(row0 + m), (long long)n);
+    if (!ws) return fail(MAPI_ERR_WORKSPACE, "workspace is NULL");
+    if (ws_bytes < csr_rank_ws_bytes(n, nnz, m))
+        return fail(MAPI_ERR_WORKSPACE, "ws_bytes (%zu) < required (%zu)", ws_bytes, csr_rank_ws_bytes(n, nnz, m));
+    return MAPI_OK;
+}
+
+mapi_status mapi_rank_csr_shard_begin(int64_t n, int64_t m, int64_t nnz_local, const int32_t* row_ptr_local,
+                                      const float* cap, const float* bg, const float* b0, void* ws, size_t ws_bytes,
+                                      mapi_stream_t stream) {
+    mapi_status st = shard_check(n, m, 0, nnz_local, ws, ws_bytes);
+    if (st != MAPI_OK) return st;
+    if ((m > 0 && !row_ptr_local) || !cap || !bg || !b0)
+        return fail(MAPI_ERR_NULL, "a required pointer (row_ptr_local/cap/bg/b0) is NULL");
+    Device d;
+    if ((st = device_info(d)) != MAPI_OK) return st;
+    st = csr_shard_begin(n, m, nnz_local, row_ptr_local, cap, bg, b0, ws, d.sms, static_cast<cudaStream_t>(stream),
+                         g_launches);
+    if (st != MAPI_OK) return fail(st, "%s", csr_last_error());
+    return MAPI_OK;
+}
+
+mapi_status mapi_rank_csr_shard_rows(int64_t n, int64_t m, int64_t row0, int64_t nnz_local,
+                                     const int32_t* row_ptr_local, const int32_t* col_idx_local, int32_t t,
+                                     float** e_out, void* ws, size_t ws_bytes, mapi_stream_t stream) {
+    mapi_status st = shard_check(n, m, row0, nnz_local, ws, ws_bytes);
+    if (st != MAPI_OK) return st;
+    if (m > 0 && (!row_ptr_local || (nnz_local > 0 && !col_idx_local)))
+        return fail(MAPI_ERR_NULL, "row_ptr_local/col_idx_local is NULL");
+    if (t < 0) return fail(MAPI_ERR_BAD_PARAM, "t (%d) must be >= 0", t);
+    st = csr_shard_rows(n, m, row0, nnz_local, row_ptr_local, col_idx_local, t, e_out, ws,
+                        static_cast<cudaStream_t>(stream), g_launches);
+    if (st != MAPI_OK) return fail(st, "%s", csr_last_error());
+    return MAPI_OK;
+}
+
+mapi_status mapi_rank_csr_shard_normalize(int64_t n, int64_t m, int64_t nnz_local, const float* cap, const float* bg,
+                                          const float* b0, int32_t t, float tol, float* deltas, void* ws,
+                                          size_t ws_bytes, mapi_stream_t stream) {
+    mapi_status st = shard_check(n, m, 0, nnz_local, ws, ws_bytes);
+    if (st != MAPI_OK) return st;
+    if (!cap || !bg || !b0) return fail(MAPI_ERR_NULL, "a required pointer (cap/bg/b0) is NULL");
+    if (t < 0) return fail(MAPI_ERR_BAD_PARAM, "t (%d) must be >= 0", t);
+    if (!(tol >= 0.0f)) return fail(MAPI_ERR_BAD_PARAM, "tol (%g) must be >= 0", (double)tol);
+    Device d;
+    if ((st = device_info(d)) != MAPI_OK) return st;
+    st = csr_shard_normalize(n, m, nnz_local, cap, bg, b0, t, tol, deltas, ws, d.sms,
+                             static_cast<cudaStream_t>(stream), g_launches);
+    if (st != MAPI_OK) return fail(st, "%s", csr_last_error());
+    return MAPI_OK;
+}
+
+mapi_status mapi_rank_csr_shard_finish(int64_t n, int64_t m, int64_t nnz_local, const float* b0, float* w_out,
+                                       float* w_l2_out, int32_t* iters_done, int32_t* stopped, void* ws,
+                                       size_t ws_bytes, mapi_stream_t stream) {
+    mapi_status st = shard_check(n, m, 0, nnz_local, ws, ws_bytes);
+    if (st != MAPI_OK) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (w_out) {
+        if (!b0) return fail(MAPI_ERR_NULL, "b0 is NULL");
+        Device d;
+        if ((st = device_info(d)) != MAPI_OK) return st;
+        st = csr_shard_output(n, m, nnz_local, b0, w_out, w_l2_out, ws, d.sms, s, g_launches);
+        if (st != MAPI_OK) return fail(st, "%s", csr_last_error());
+    }
+    int32_t h[3] = {0, 0, 0};  // status, iterations done, stop flag
+    cudaError_t e = cudaMemcpyAsync(h, ws, sizeof(h), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return fail(MAPI_ERR_CUDA, "status read-back: %s", cudaGetErrorString(e));
+    if (iters_done) *iters_done = h[1];
+    if (stopped) *stopped = h[2];
+    st = (mapi_status)h[0];
     if (st == MAPI_ERR_NEGATIVE) return fail(st, "b0 has a negative entry");
     if (st == MAPI_ERR_DEGENERATE) return fail(st, "||G (+) w_t||_1 == 0");
     if (st == MAPI_ERR_NONFINITE) return fail(st, "||G (+) w_t||_1 is not finite");

@@ -110,16 +110,17 @@ struct CsrWs {
 
 inline int64_t mp_tiles(int64_t n, int64_t nnz) { return (n + nnz + kMpTile - 1) / kMpTile; }
 
-inline size_t csr_rank_ws_bytes(int64_t n, int64_t nnz) {
-    const int64_t T = mp_tiles(n, nnz);
+// n: nodes (the e / v arrays); m: rows this workspace gathers (m = n on one GPU, the owned block when sharded)
+inline size_t csr_rank_ws_bytes(int64_t n, int64_t nnz, int64_t m = -1) {
+    const int64_t T = mp_tiles(m < 0 ? n : m, nnz);
     return 256 + 3 * cal256(4 * (size_t)n) + 4 * cal256(8 * (size_t)kCsrMaxGrid) +
            2 * cal256(4 * (size_t)(T + 1)) + 2 * cal256(4 * (size_t)T) + cal256(8 * (size_t)T * kMpWarps);
 }
 
-inline CsrWs carve_csr(void* ws, int64_t n, int64_t nnz) {
+inline CsrWs carve_csr(void* ws, int64_t n, int64_t nnz, int64_t m = -1) {
     char* p = static_cast<char*>(ws);
     CsrWs c;
-    c.tiles = mp_tiles(n, nnz);
+    c.tiles = mp_tiles(m < 0 ? n : m, nnz);
     c.status = reinterpret_cast<int32_t*>(p);
     c.stop = reinterpret_cast<int32_t*>(p + 8);
     c.counter = reinterpret_cast<uint32_t*>(p + 12);
@@ -752,6 +753,113 @@ inline mapi_status csr_rank_finish(void* ws, int64_t /*n*/, int64_t /*nnz*/, cud
     if (e != cudaSuccess) return csr_cuda_fail(e, "status read-back");
     if (iters_done) *iters_done = h[1];
     return (mapi_status)h[0];
+}
+
+// ------------------------------------------------------------------ K3n: the ranking over ranks
+// SURVEY 8(e) / DESIGN.md 8: rank r owns the destination rows [row0, row0 + m) of the graph (its sub-CSR:
+// row_ptr rebased to 0, GLOBAL source ids in col_idx); every rank keeps the full n-node state (e, v and
+// the fp64 scalars) and runs the SAME node kernels on it, so w, s_t, delta_t and the stop decision are
+// bitwise identical on every rank.  Per iteration t:
+//   rows:       e_t[row0 .. row0 + m) = gather-sum of v_t over the rank's edges  (K3b on the sub-CSR)
+//   exchange:   all-gather of the e_t blocks (the caller's collective: NCCL; n * 4 bytes in total)
+//   normalize:  sum_i e_i over all n in a fixed order -> s_t, then K3c+d unchanged (w, v_{t+1}, S, delta)
+// The per-iteration launches are enqueued by the caller (one call per step), so the collective sits
+// between them on the same stream; after a tol stop the remaining launches exit at once.
+inline int csr_node_grid(int64_t n, int sms) {
+    return (int)std::min<int64_t>({(n + kCsrThreads - 1) / kCsrThreads, (int64_t)4 * sms, (int64_t)kCsrMaxGrid});
+}
+
+// sum_i e_i over all n nodes: per-CTA fp64 partials in a fixed (grid-stride, then block tree) order
+__global__ void __launch_bounds__(kCsrThreads) k_rank_esum(int64_t n, const float* __restrict__ e,
+                                                           double* __restrict__ slotY, const int32_t* stop) {
+    __shared__ double red[33];
+    if (*(volatile const int32_t*)stop) return;
+    double g = 0.0;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+        g += (double)e[j];
+    const double G = block_sum(g, red);
+    if (threadIdx.x == 0) slotY[blockIdx.x] = G;
+}
+
+inline mapi_status csr_shard_begin(int64_t n, int64_t m, int64_t nnz, const int32_t* row_ptr, const float* cap,
+                                   const float* bg, const float* b0, void* ws, int sms, cudaStream_t s,
+                                   std::atomic<uint64_t>& launches) {
+    CsrWs W = carve_csr(ws, n, nnz, m);
+    cudaError_t err = cudaMemsetAsync(ws, 0, 256, s);
+    if (err != cudaSuccess) return csr_cuda_fail(err, "memset");
+    if (m > 0) {
+        k_mp_partition<<<(unsigned)((W.tiles + 1 + 255) / 256), 256, 0, s>>>(m, nnz, row_ptr, W.tiles, W.part_i,
+                                                                              W.part_k);
+        launches.fetch_add(1, std::memory_order_relaxed);
+    }
+    k_rank_init<<<csr_node_grid(n, sms), kCsrThreads, 0, s>>>(n, b0, bg, cap, W.v, W.slotS, W.status, W.stop);
+    launches.fetch_add(1, std::memory_order_relaxed);
+    if ((err = cudaGetLastError()) != cudaSuccess) return csr_cuda_fail(err, "shard begin launch");
+    return MAPI_OK;
+}
+
+// iteration t's gather over the owned rows; *e_out = the n-float device array e_t whose block
+// [row0, row0 + m) is now valid and whose other blocks the exchange fills
+inline mapi_status csr_shard_rows(int64_t n, int64_t m, int64_t row0, int64_t nnz, const int32_t* row_ptr,
+                                  const int32_t* col_idx, int32_t t, float** e_out, void* ws, cudaStream_t s,
+                                  std::atomic<uint64_t>& launches) {
+    CsrWs W = carve_csr(ws, n, nnz, m);
+    float* e_cur = W.e[t & 1];
+    if (e_out) *e_out = e_cur;
+    if (m == 0) return MAPI_OK;
+    const int64_t T = W.tiles;
+    const int gfix = (int)std::min<int64_t>((T + 255) / 256, kCsrMaxGrid);
+    k_rank_rows_mp<<<(unsigned)T, kMpThreads, 0, s>>>(m, nnz, row_ptr, col_idx, W.v, W.part_i, W.part_k,
+                                                      e_cur + row0, W.carry_row, W.carry_val, W.gsum, W.stop);
+    // the carries of rows spanning tiles; its slotY output (the LOCAL sum of e) is overwritten by
+    // csr_shard_normalize's sum over all n
+    k_rank_fixup<<<gfix, 256, 0, s>>>(T, W.carry_row, W.carry_val, W.gsum, e_cur + row0, W.slotY, W.stop);
+    launches.fetch_add(2, std::memory_order_relaxed);
+    const cudaError_t err = cudaGetLastError();
+    if (err != cudaSuccess) return csr_cuda_fail(err, "shard rows launch");
+    return MAPI_OK;
+}
+
+// after the exchange: s_t, w_{t+1}, v_{t+1}, S_{t+1}, delta_t, trace and stop flag, on the full state
+inline mapi_status csr_shard_normalize(int64_t n, int64_t m, int64_t nnz, const float* cap, const float* bg,
+                                       const float* b0, int32_t t, float tol, float* deltas, void* ws, int sms,
+                                       cudaStream_t s, std::atomic<uint64_t>& launches) {
+    CsrWs W = carve_csr(ws, n, nnz, m);
+    const int gcol = csr_node_grid(n, sms);
+    const bool v4 = (reinterpret_cast<uintptr_t>(bg) % 16 == 0) && (reinterpret_cast<uintptr_t>(cap) % 16 == 0) &&
+                    (reinterpret_cast<uintptr_t>(b0) % 16 == 0);
+    double* S_cur = W.slotS + (t & 1) * kCsrMaxGrid;
+    double* S_next = W.slotS + ((t + 1) & 1) * kCsrMaxGrid;
+    float* e_cur = W.e[t & 1];
+    const float* e_prev = t == 0 ? nullptr : W.e[(t + 1) & 1];
+    k_rank_esum<<<gcol, kCsrThreads, 0, s>>>(n, e_cur, W.slotY, W.stop);
+    if (v4)
+        k_rank_normalize<true><<<gcol, kCsrThreads, 0, s>>>(n, e_cur, e_prev, b0, W.hist, S_cur, S_next, gcol, W.slotY,
+                                                            gcol, bg, cap, W.v, W.slotD, W.s, W.counter, t, tol, deltas,
+                                                            W.status, W.stop);
+    else
+        k_rank_normalize<false><<<gcol, kCsrThreads, 0, s>>>(n, e_cur, e_prev, b0, W.hist, S_cur, S_next, gcol,
+                                                             W.slotY, gcol, bg, cap, W.v, W.slotD, W.s, W.counter, t,
+                                                             tol, deltas, W.status, W.stop);
+    launches.fetch_add(2, std::memory_order_relaxed);
+    const cudaError_t err = cudaGetLastError();
+    if (err != cudaSuccess) return csr_cuda_fail(err, "shard normalize launch");
+    return MAPI_OK;
+}
+
+inline mapi_status csr_shard_output(int64_t n, int64_t m, int64_t nnz, const float* b0, float* w_out, float* w_l2_out,
+                                    void* ws, int sms, cudaStream_t s, std::atomic<uint64_t>& launches) {
+    CsrWs W = carve_csr(ws, n, nnz, m);
+    const int gcol = csr_node_grid(n, sms);
+    k_rank_output<<<gcol, kCsrThreads, 0, s>>>(n, W.e[0], W.e[1], W.hist, W.status, b0, w_out, W.slotD);
+    launches.fetch_add(1, std::memory_order_relaxed);
+    if (w_l2_out) {
+        k_rank_output_l2<<<gcol, kCsrThreads, 0, s>>>(n, W.e[0], W.e[1], W.hist, W.status, b0, W.slotD, gcol, w_l2_out);
+        launches.fetch_add(1, std::memory_order_relaxed);
+    }
+    const cudaError_t err = cudaGetLastError();
+    if (err != cudaSuccess) return csr_cuda_fail(err, "shard output launch");
+    return MAPI_OK;
 }
 
 }  // namespace mapi

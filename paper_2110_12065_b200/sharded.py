@@ -383,3 +383,166 @@ def iterate_sym_sharded_p2p(A_local, row_lo: int, row_hi: int, n: int, b0, iters
         raise MapiError(st, lib.mapi_last_error_message().decode(errors="replace"), done.value)
     k = done.value
     return ShardedResult(w, norms[:k] if norms is not None else None, deltas[:k] if deltas is not None else None, k)
+
+
+# --------------------------------------------------------------- CSR ranking over ranks (K3n)
+
+
+def csr_row_partition(row_ptr, world: int):
+    """Contiguous destination-row blocks [starts[r], starts[r+1]) of near-equal merge-path cost
+    (rows + in-edges: what the gather kernel's tiles count), from the host copy of row_ptr (n + 1).  Index
+    bookkeeping only — no method arithmetic.  Returns world + 1 ints; blocks may be empty when world > n."""
+    import numpy as np
+
+    rp = np.asarray(row_ptr.cpu() if hasattr(row_ptr, "cpu") else row_ptr, dtype=np.int64)
+    n = rp.shape[0] - 1
+    if world < 1:
+        raise ValueError("world must be >= 1")
+    cost = rp - rp[0] + np.arange(n + 1, dtype=np.int64)  # items before row i
+    total = int(cost[-1])
+    starts = [0]
+    for r in range(1, world):
+        starts.append(max(starts[-1], int(np.searchsorted(cost, (total * r + world - 1) // world, side="left"))))
+    starts.append(n)
+    return [min(s, n) for s in starts]
+
+
+def csr_shard(row_ptr, col_idx, r0: int, r1: int):
+    """The sub-CSR of the destination rows [r0, r1): row_ptr rebased to 0 (r1 - r0 + 1 entries) and the
+    matching slice of col_idx (global source ids kept)."""
+    lo, hi = int(row_ptr[r0]), int(row_ptr[r1])
+    return (row_ptr[r0:r1 + 1] - lo).contiguous(), col_idx[lo:hi].contiguous()
+
+
+class CsrShardSession:
+    """One rank's run of the sharded ranking (mapi_rank_csr_shard_*): begin() once, then per iteration
+    rows(t) -> the caller's all-gather of the e_t blocks -> normalize(t); finish() returns the result.
+    Everything is enqueued on the current stream.  `lib` is injectable for the CPU orchestration test."""
+
+    def __init__(self, n: int, row0: int, row_ptr_local, col_idx_local, cap, bg, b0, max_iters: int,
+                 tol: float = 1e-7, lib=None, stream=None):
+        import ctypes
+
+        import torch
+
+        from . import WS_RANK_CSR_SHARD, load
+
+        self.lib = lib or load()
+        self.n, self.row0, self.m = int(n), int(row0), int(row_ptr_local.numel()) - 1
+        self.nnz = int(col_idx_local.numel())
+        self.rp, self.ci, self.cap, self.bg, self.b0 = row_ptr_local, col_idx_local, cap, bg, b0
+        self.max_iters, self.tol = int(max_iters), float(tol)
+        dev = b0.device
+        self.need = int(self.lib.mapi_workspace_size(WS_RANK_CSR_SHARD, self.n, self.nnz, self.m))
+        self.ws = torch.empty(self.need, dtype=torch.uint8, device=dev)
+        self.deltas = torch.zeros(self.max_iters, dtype=torch.float32, device=dev)
+        self.sp = stream if stream is not None else (torch.cuda.current_stream(dev).cuda_stream
+                                                     if dev.type == "cuda" else None)
+        self._c, self._torch = ctypes, torch
+
+    def _check(self, st):
+        if st:
+            from . import MapiError
+
+            raise MapiError(st, self.lib.mapi_last_error_message().decode())
+
+    def begin(self):
+        self._check(self.lib.mapi_rank_csr_shard_begin(self.n, self.m, self.nnz, self.rp.data_ptr(),
+                                                       self.cap.data_ptr(), self.bg.data_ptr(), self.b0.data_ptr(),
+                                                       self.ws.data_ptr(), self.need, self.sp))
+
+    def rows(self, t: int) -> int:
+        """Enqueue iteration t's gather over the owned rows; returns the device address of e_t (n floats)."""
+        e = self._c.c_void_p(0)
+        self._check(self.lib.mapi_rank_csr_shard_rows(self.n, self.m, self.row0, self.nnz, self.rp.data_ptr(),
+                                                      self.ci.data_ptr() if self.nnz else None, int(t),
+                                                      self._c.byref(e), self.ws.data_ptr(), self.need, self.sp))
+        return e.value
+
+    def e_view(self, t: int):
+        """e_t as a tensor view into the workspace (the collective's in-place buffer)."""
+        base = 256 + (t & 1) * ((4 * self.n + 255) & ~255)
+        return self.ws[base:base + 4 * self.n].view(self._torch.float32)
+
+    def normalize(self, t: int):
+        self._check(self.lib.mapi_rank_csr_shard_normalize(self.n, self.m, self.nnz, self.cap.data_ptr(),
+                                                           self.bg.data_ptr(), self.b0.data_ptr(), int(t), self.tol,
+                                                           self.deltas.data_ptr(), self.ws.data_ptr(), self.need,
+                                                           self.sp))
+
+    def poll(self):
+        """(iterations done, stopped) — synchronises the stream (the host's periodic stop check)."""
+        done, stopped = self._c.c_int32(0), self._c.c_int32(0)
+        self._check(self.lib.mapi_rank_csr_shard_finish(self.n, self.m, self.nnz, None, None, None,
+                                                        self._c.byref(done), self._c.byref(stopped),
+                                                        self.ws.data_ptr(), self.need, self.sp))
+        return done.value, bool(stopped.value)
+
+    def finish(self, want_l2: bool = True):
+        from . import IterResult
+
+        dev = self.b0.device
+        w = self._torch.empty(self.n, dtype=self._torch.float32, device=dev)
+        wl2 = self._torch.empty(self.n, dtype=self._torch.float32, device=dev) if want_l2 else None
+        done = self._c.c_int32(0)
+        st = self.lib.mapi_rank_csr_shard_finish(self.n, self.m, self.nnz, self.b0.data_ptr(), w.data_ptr(),
+                                                 wl2.data_ptr() if want_l2 else None, self._c.byref(done), None,
+                                                 self.ws.data_ptr(), self.need, self.sp)
+        if st:
+            from . import MapiError
+
+            raise MapiError(st, self.lib.mapi_last_error_message().decode(), done.value)
+        k = done.value
+        return IterResult(w, wl2, None, self.deltas[:k], k)
+
+
+def rank_csr_sharded(n: int, starts, row_ptr_local, col_idx_local, cap, bg, b0, max_iters: int = 200,
+                     tol: float = 1e-7, want_l2: bool = True, group=None, check_every: int = 8, lib=None,
+                     all_gather=None):
+    """MAPI ranking (Eq. 13) with the destination rows partitioned over the ranks:
+    rank r holds the sub-CSR of rows [starts[r], starts[r+1]) (csr_row_partition / csr_shard) and the full
+    cap / bg / b0.  Per iteration: the local gather, ONE collective (the all-gather of the e_t blocks, in
+    place in the workspace, n * 4 bytes in total) and the node kernels on the full state, which every rank
+    runs identically — no all-reduce of s_t or delta_t is needed and all ranks take the same stop decision.
+    With tol > 0 the host reads the device stop flag every `check_every` iterations (the launches enqueued
+    after a stop return at once on the device).  all_gather(e_full, starts, rank) is injectable."""
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    if len(starts) != world + 1 or starts[0] != 0 or starts[-1] != n:
+        raise ValueError(f"starts must have world + 1 = {world + 1} entries from 0 to n")
+    r0, r1 = int(starts[rank]), int(starts[rank + 1])
+    if int(row_ptr_local.numel()) - 1 != r1 - r0:
+        raise ValueError(f"row_ptr_local has {int(row_ptr_local.numel()) - 1} rows; the partition gives {r1 - r0}")
+    ses = CsrShardSession(n, r0, row_ptr_local, col_idx_local, cap, bg, b0, max_iters, tol, lib=lib)
+    if all_gather is None:
+        all_gather = _e_all_gather(group, world)
+    ses.begin()
+    for t in range(max_iters):
+        ses.rows(t)
+        if world > 1:
+            all_gather(ses.e_view(t), starts, rank)
+        ses.normalize(t)
+        if tol > 0.0 and (t + 1) % max(1, check_every) == 0 and t + 1 < max_iters:
+            if ses.poll()[1]:
+                break
+    return ses.finish(want_l2)
+
+
+def _e_all_gather(group, world):
+    """In-place all-gather of the ranks' row blocks of e_t: one NCCL all-gather when the blocks are equal,
+    else one broadcast per non-empty block (NCCL groups uneven all-gathers the same way)."""
+    import torch.distributed as dist
+
+    def gather(e_full, starts, rank):
+        sizes = [starts[q + 1] - starts[q] for q in range(world)]
+        if len(set(sizes)) == 1:
+            dist.all_gather_into_tensor(e_full, e_full[starts[rank]:starts[rank + 1]].clone(), group=group)
+            return
+        for q in range(world):
+            if sizes[q]:
+                dist.broadcast(e_full[starts[q]:starts[q + 1]], src=dist.get_global_rank(group, q) if group else q,
+                               group=group)
+
+    return gather

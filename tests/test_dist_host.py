@@ -3,6 +3,7 @@ reference arm's rank-0-only rule (replicas, no data-path collecti
 import os
 import socket
 
+import pytest
 import torch.multiprocessing as mp
 
 
@@ -426,3 +427,164 @@ def test_sym_sharded_partials_gloo_world3():
     for k in range(world):
         np.testing.assert_array_equal(out[k], out[0])
     np.testing.assert_allclose(out[0], ref, rtol=1e-12, atol=1e-9)
+
+
+# -------------------------------------------------------- CSR ranking over ranks (K3n): orchestration on CPU
+
+
+class _FakeCsrShardLib:
+    """Stand-in for mapi_rank_csr_shard_* (host orchestration test only; test code, so it may restate the
+    exact sparse + background form of Eq. 13 in numpy fp64): the pointers are those of CPU tensors, e_t lives
+    in the caller's workspace at the library's offsets so that the in-place collective works on it."""
+
+    def __init__(self):
+        self.state = {}
+
+    @staticmethod
+    def _arr(ptr, count, dtype):
+        import ctypes
+
+        import numpy as np
+
+        if count == 0:
+            return np.zeros(0, dtype)
+        size = count * np.dtype(dtype).itemsize
+        return np.frombuffer((ctypes.c_char * size).from_address(ptr), dtype=dtype)
+
+    def mapi_workspace_size(self, op, n, nnz, k):
+        return 256 + 2 * ((4 * n + 255) & ~255)
+
+    def _e(self, ws, n, t):
+        import numpy as np
+
+        return self._arr(ws + 256 + (t & 1) * ((4 * n + 255) & ~255), n, np.float32)
+
+    def mapi_rank_csr_shard_begin(self, n, m, nnz, rp, cap, bg, b0, ws, need, sp):
+        import numpy as np
+
+        f = np.float32
+        self.state[ws] = dict(w=self._arr(b0, n, f).astype(np.float64), cap=self._arr(cap, n, f).astype(np.float64),
+                              bg=self._arr(bg, n, f).astype(np.float64), done=0, stop=0)
+        return 0
+
+    def mapi_rank_csr_shard_rows(self, n, m, row0, nnz, rp, ci, t, e_out, ws, need, sp):
+        import numpy as np
+
+        s = self.state[ws]
+        if s["stop"]:
+            return 0
+        v = np.minimum(np.maximum(s["w"] - s["bg"], 0.0), s["cap"])
+        rp_ = self._arr(rp, m + 1, np.int32)
+        ci_ = self._arr(ci, nnz, np.int32) if nnz else np.zeros(0, np.int32)
+        e = self._e(ws, n, t)
+        for i in range(m):
+            e[row0 + i] = v[ci_[rp_[i]:rp_[i + 1]]].sum()
+        return 0
+
+    def mapi_rank_csr_shard_normalize(self, n, m, nnz, cap, bg, b0, t, tol, deltas, ws, need, sp):
+        import numpy as np
+
+        s = self.state[ws]
+        if s["stop"]:
+            return 0
+        S = np.minimum(s["bg"], s["w"]).sum()
+        y = S + self._e(ws, n, t).astype(np.float64)
+        wn = y / y.sum()
+        d = np.abs(wn - s["w"]).sum()
+        self._arr(deltas, t + 1, np.float32)[t] = d
+        s["w"], s["done"] = wn, t + 1
+        if tol > 0 and d < tol:
+            s["stop"] = 1
+        return 0
+
+    def mapi_rank_csr_shard_finish(self, n, m, nnz, b0, w_out, w_l2, done, stopped, ws, need, sp):
+        import numpy as np
+
+        s = self.state[ws]
+        if w_out:
+            self._arr(w_out, n, np.float32)[:] = s["w"]
+            if w_l2:
+                self._arr(w_l2, n, np.float32)[:] = s["w"] / np.linalg.norm(s["w"])
+        if done is not None:
+            done._obj.value = s["done"]
+        if stopped is not None:
+            stopped._obj.value = s["stop"]
+        return 0
+
+    def mapi_last_error_message(self):
+        return b""
+
+
+def _csr_sharded_worker(rank, world, port, q):
+    import sys
+
+    import numpy as np
+    import torch
+    import torch.distributed as tdist
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    import synth
+    from paper_2110_12065_b200.sharded import csr_row_partition, csr_shard, rank_csr_sharded
+
+    n = 257
+    edges, row_ptr, col_idx = synth.random_graph(n, 0.04, seed=11, n_dangling=25)
+    outdeg = np.bincount(edges[:, 0], minlength=n)
+    alpha = 0.85
+    with np.errstate(divide="ignore"):
+        cap = np.where(outdeg > 0, alpha / outdeg, 0.0).astype(np.float32)
+    bg = np.where(outdeg > 0, (1 - alpha) / n, 1.0 / n).astype(np.float32)
+    starts = csr_row_partition(row_ptr, world)
+    rp = torch.from_numpy(row_ptr.astype(np.int32))
+    ci = torch.from_numpy(col_idx.astype(np.int32))
+    rpl, cil = csr_shard(rp, ci, starts[rank], starts[rank + 1])
+    b0 = torch.full((n,), 1.0 / n, dtype=torch.float32)
+    out = {}
+    for name, tol, iters in (("fixed", 0.0, 12), ("tol", 1e-7, 200)):
+        res = rank_csr_sharded(n, starts, rpl, cil, torch.from_numpy(cap), torch.from_numpy(bg), b0, iters, tol,
+                               lib=_FakeCsrShardLib(), check_every=3)
+        out[name] = (res.w.numpy().copy(), res.deltas.numpy().copy(), res.iters_done)
+    q.put((rank, starts, out))
+    tdist.barrier()
+    tdist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_csr_rank_sharded_gloo(world):
+    """sharded.rank_csr_sharded over gloo: the row partition tiles [0, n) with balanced rows + in-edges, the
+    in-place exchange of the e_t blocks (uneven blocks: one broadcast per owner) delivers every owner's rows
+    to every rank, all ranks finish with the same w / deltas / iteration count (fixed count and tol stop with
+    a periodic host check), and the result is the oracle's rank_csr."""
+    import numpy as np
+
+    import oracle
+    import synth
+
+    oracle.build()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_csr_sharded_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = {r: rest for r, *rest in [q.get(timeout=180) for _ in range(world)]}
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    n = 257
+    edges, row_ptr, col_idx = synth.random_graph(n, 0.04, seed=11, n_dangling=25)
+    b0 = np.full(n, 1.0 / n, dtype=np.float32)
+    starts = got[0][0]
+    assert starts[0] == 0 and starts[-1] == n and all(a <= b for a, b in zip(starts, starts[1:]))
+    items = [(starts[r + 1] - starts[r]) + int(row_ptr[starts[r + 1]] - row_ptr[starts[r]]) for r in range(world)]
+    assert max(items) - min(items) <= 2 * (1 + int(np.max(np.diff(row_ptr))))
+    for name, tol, iters in (("fixed", 0.0, 12), ("tol", 1e-7, 200)):
+        ref = oracle.rank_csr(n, row_ptr, col_idx, b0=b0, max_iters=iters, tol=tol)
+        w0, d0, k0 = got[0][1][name]
+        for r in range(1, world):
+            w, d, k = got[r][1][name]
+            assert k == k0 and np.array_equal(w, w0) and np.array_equal(d, d0)
+        assert k0 == ref.iters_done
+        np.testing.assert_allclose(w0, ref.w, rtol=1e-6, atol=1e-12)
+        np.testing.assert_allclose(d0, ref.deltas, rtol=1e-3, atol=1e-9)
