@@ -64,7 +64,7 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--reorder", action="store_true",
                    help="cfg5: relabel nodes by out-degree first (mapi_csr_reorder; measured slower with the default kernel)")
-    p.add_argument("--csr-path", default="plan", choices=["plan", "k3"],
+    p.add_argument("--csr-path", default="plan", choices=["plan", "k3", "shard"],
                    help="cfg5: plan = segmented layout (mapi_csr_plan + mapi_rank_csr_plan, K3s, the default); "
                         "k3 = the plan-free CSR kernel (mapi_rank_csr)")
     p.add_argument("--no-sym", action="store_true",
@@ -385,6 +385,36 @@ def build_rank(args, m, dev, stream):
     done = ctypes.c_int32(0)
     lib = m.load()
     opc = {"min1": m.MIN1, "min2": m.MIN2, "dot": m.DOT}[args.op]
+    if args.world > 1 or args.csr_path == "shard":
+        # N > 1: the destination rows partitioned over the ranks (K3n, sharded.rank_csr_sharded): every
+        # rank builds the same graph, keeps its row block, and the ranks exchange the e_t blocks (NCCL)
+        if opc != m.MIN1 or reorder:
+            raise SystemExit("the sharded cfg5 path runs --op min1 without --reorder")
+        from paper_2110_12065_b200 import sharded
+
+        starts = sharded.csr_row_partition(cfg["row_ptr"], args.world)
+        r0, r1 = starts[args.rank], starts[args.rank + 1]
+        rpl, cil = sharded.csr_shard(rp, ci, r0, r1)
+        nnz_l = cil.numel()
+        del rp, ci, rp0, ci0
+
+        def step():
+            torch.cuda.set_stream(stream)
+            res = sharded.rank_csr_sharded(n, starts, rpl, cil, cap, bg, b0, T, 0.0)
+            assert res.iters_done == T
+            return T
+
+        # whole-job algorithmic bytes per iteration: row_ptr + col_idx once over the ranks, e written by the
+        # gathers, and the node kernels' 24 B/node on EVERY rank (they are replicated, not sharded)
+        per_iter = 4.0 * (n + args.world) + 4.0 * nnz + 4.0 * n + 24.0 * n * args.world
+        return Work(step=step, unit="iterations/s", per_launch=per_iter * T, bytes_per_unit=per_iter, bound="hbm",
+                    kernel="K3n: k_rank_rows_mp + k_rank_fixup on the rank's rows, all-gather of e_t, k_rank_esum + "
+                           "k_rank_normalize on the full node state (events around the loop)",
+                    config={"workload": f"cfg5: {WORKLOADS['cfg5']}", "n": n, "nnz": nnz, "iters_per_step": T,
+                            "tol": 0.0, "rows_local": r1 - r0, "nnz_local": nnz_l,
+                            "exchange": f"all-gather of the e_t row blocks, {4 * n} B in total per iteration (NCCL)",
+                            "l2_flush": "inputs larger than L2", "op": args.op, "csr_path": "shard (K3n)"},
+                    oracle=None, whole_step=True, shared_units=True, csr_shard=True, traffic_key="cfg5_shard")
     if args.csr_path == "plan" and not reorder:
         return _build_rank_plan(args, m, dev, stream, cfg, n, nnz, rp, ci, cap, bg, b0, T, opc)
     if opc == m.DOT:
@@ -694,6 +724,10 @@ def run_mapi(args, rank, world, local_rank):
                                   "sharded": f"row-sharded x{world}: NCCL all-gather of y ({4 * 32768} B) per "
                                              "iteration"}[mode]
         out["scaling"] = "strong"
+    elif getattr(work, "csr_shard", False):
+        cfg_out["parallelism"] = (f"K3n x{world}: destination rows partitioned (rows + in-edges balanced), one "
+                                  "all-gather of e_t per iteration, node kernels replicated")
+        out["scaling"] = "strong"
     elif getattr(work, "ksplit", False):
         cfg_out["parallelism"] = (f"k-split x{world}: the batch's independent runs partitioned over the ranks "
                                   "(iterate_batched_sharded), no data-path collective")
@@ -742,7 +776,7 @@ def run_mapi(args, rank, world, local_rank):
                 "gpu_launches": int(launches), "wall_s_timed": t_wall})
     traffic = traffic_from_profiles(getattr(work, "traffic_key", args.workload))
     if work.bound == "hbm":
-        gpus_in_roof = world if getattr(work, "sharded", False) else 1
+        gpus_in_roof = world if (getattr(work, "sharded", False) or getattr(work, "csr_shard", False)) else 1
         out["hbm_gbs"] = work.bytes_per_unit * job_units / (elapsed_ms / 1e3) / 1e9
         out["hbm_frac_of_measured"] = out["hbm_gbs"] / (peak * world)
         out["hbm_frac_of_nominal_8000"] = out["hbm_gbs"] / (8000.0 * world)

@@ -252,22 +252,36 @@ __global__ void kp_edges(int64_t n, int64_t nnz, const int32_t* __restrict__ row
 }
 
 // segment of each sorted edge: counts and first positions
+// The edges are sorted by segment: only the run boundaries write (segstart = first edge of the segment's run,
+// segcnt = one past its last edge until kp_segb turns it into the count; both zeroed before, so a segment
+// without edges keeps 0 / 0).  (A per-edge atomicAdd on the ~60 counters took 41 of the plan build's 50 ms.)
 __global__ void kp_segcount(int64_t nnz, const uint64_t* __restrict__ ek, int32_t* __restrict__ segcnt,
                             int32_t* __restrict__ segstart) {
     GRID_STRIDE(k, nnz) {
         const uint32_t seg = (uint32_t)(ek[k] >> 32);
-        if (k == 0 || (uint32_t)(ek[k - 1] >> 32) != seg) segstart[seg] = (int32_t)k;
-        atomicAdd(segcnt + seg, 1);
+        if (k == 0) {
+            segstart[seg] = 0;
+        } else {
+            const uint32_t prev = (uint32_t)(ek[k - 1] >> 32);
+            if (prev != seg) {
+                segstart[seg] = (int32_t)k;
+                segcnt[prev] = (int32_t)k;
+            }
+        }
+        if (k == nnz - 1) segcnt[seg] = (int32_t)nnz;
     }
 }
 
-// padded segment starts, tile-aligned (one thread: nseg is small)
-__global__ void kp_segb(int32_t nseg, const int32_t* __restrict__ segcnt, int32_t* __restrict__ segb) {
+// run ends -> counts, and the padded segment starts, tile-aligned (one thread: nseg is small)
+__global__ void kp_segb(int32_t nseg, int32_t* __restrict__ segcnt, const int32_t* __restrict__ segstart,
+                        int32_t* __restrict__ segb) {
     if (blockIdx.x != 0 || threadIdx.x != 0) return;
     int64_t acc = 0;
     for (int32_t s = 0; s < nseg; ++s) {
+        const int32_t cnt = segcnt[s] > 0 ? segcnt[s] - segstart[s] : 0;
+        segcnt[s] = cnt;
         segb[s] = (int32_t)acc;
-        acc += ((int64_t)segcnt[s] + kTileW - 1) / kTileW * kTileW;
+        acc += ((int64_t)cnt + kTileW - 1) / kTileW * kTileW;
     }
     segb[nseg] = (int32_t)acc;
 }
@@ -331,6 +345,68 @@ __global__ void kp_wflags(int64_t nchunks, uint16_t* __restrict__ words, uint32_
             if (lane >= off) c += co;
         }
         wflags[ch] = m | ((uint32_t)(c - cnt) << 16);
+    }
+}
+
+// Bank-conflict-aware word order (plan time; after kp_wflags: the words are 15-bit source offsets, the end flags
+// sit in wflags).  Phase A's gather step i reads, warp-wide, word 16 l + i of every lane l from the shared
+// segment: a random 32-address gather costs ~3.9 extra shared-memory wavefronts (ncu: 44% of K3s's shared
+// wavefronts were conflict replays, profiles/r02_cfg5_k3s_raw.csv).  The words of one lane that belong to the
+// same fragment may be summed in any fixed order, so within each (lane chunk, fragment) group the offsets are
+// re-assigned to the group's steps greedily, lanes in order, each word to the free step where its bank holds
+// the fewest distinct addresses so far (an equal address is a broadcast and costs nothing).  One warp per
+// tile; only the order of the fp32 additions inside a fragment changes (fixed by the plan: deterministic).
+__global__ void __launch_bounds__(256) kp_deconflict(int64_t ntiles, uint16_t* __restrict__ words,
+                                                     const uint32_t* __restrict__ wflags) {
+    __shared__ uint8_t hist[8][kLaneW][32];    // per warp: distinct addresses per (step, bank)
+    __shared__ uint16_t first[8][kLaneW][32];  // the first address seen there
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int64_t tile = (int64_t)blockIdx.x * 8 + warp; tile < ntiles; tile += (int64_t)gridDim.x * 8) {
+        for (int i = lane; i < kLaneW * 32; i += 32) (&hist[warp][0][0])[i] = 0;
+        __syncwarp();
+        uint16_t* w = words + tile * kTileW + kLaneW * lane;
+        const uint32_t fl = wflags[tile * 32 + lane] & 0xffffu;
+        uint16_t x[kLaneW], out[kLaneW];
+#pragma unroll
+        for (int i = 0; i < kLaneW; ++i) x[i] = w[i];
+        for (int l = 0; l < 32; ++l) {
+            if (lane == l) {
+                int g0 = 0;
+                while (g0 < kLaneW) {
+                    int g1 = g0;  // the group ends at the first end flag at or after g0 (or with the chunk)
+                    while (g1 < kLaneW - 1 && !((fl >> g1) & 1u)) ++g1;
+                    uint32_t free_steps = ((2u << g1) - 1u) & ~((1u << g0) - 1u);
+                    for (int k = g0; k <= g1; ++k) {
+                        const uint16_t a = x[k];
+                        const int bank = a & 31;
+                        int best = g0, bestc = 1 << 30;
+                        bool best_same = false;
+                        for (int st = g0; st <= g1; ++st) {
+                            if (!((free_steps >> st) & 1u)) continue;
+                            int c = hist[warp][st][bank];
+                            const bool same = c > 0 && first[warp][st][bank] == a;
+                            if (same) c = 0;
+                            if (c < bestc) {
+                                bestc = c;
+                                best = st;
+                                best_same = same;
+                            }
+                        }
+                        out[best] = a;
+                        free_steps &= ~(1u << best);
+                        if (!best_same) {
+                            if (hist[warp][best][bank] == 0) first[warp][best][bank] = a;
+                            ++hist[warp][best][bank];
+                        }
+                    }
+                    g0 = g1 + 1;
+                }
+            }
+            __syncwarp();
+        }
+#pragma unroll
+        for (int i = 0; i < kLaneW; ++i) w[i] = out[i];
+        __syncwarp();
     }
 }
 
@@ -961,7 +1037,7 @@ mapi_status mapi_csr_plan(int64_t n, int64_t nnz, const int32_t* row_ptr, const 
         MAPI_LAUNCHED();
     }
     // tile-aligned segment starts: they size the word array
-    kp_segb<<<1, 32, 0, s>>>(nseg, B.segcnt, B.segb);
+    kp_segb<<<1, 32, 0, s>>>(nseg, B.segcnt, B.segstart, B.segb);
     MAPI_LAUNCHED();
     int64_t nfrag = 0, nwords = 0;
     std::vector<int32_t> segb_h(nseg + 1);
@@ -1013,6 +1089,13 @@ mapi_status mapi_csr_plan(int64_t n, int64_t nnz, const int32_t* row_ptr, const 
         MAPI_LAUNCHED();
         kp_wflags<<<blocks(nwords / kLaneW, 8), 256, 0, s>>>(nwords / kLaneW, P.words, P.wflags);
         MAPI_LAUNCHED();
+        {  // investigation switch (MAPI_PLAN_DECONFLICT=0: keep the words in destination order)
+            const char* dc = getenv("MAPI_PLAN_DECONFLICT");
+            if (!dc || dc[0] != '0') {
+                kp_deconflict<<<blocks(ntiles * 32, 8), 256, 0, s>>>(ntiles, P.words, P.wflags);
+                MAPI_LAUNCHED();
+            }
+        }
         // row-sorted slots (stable: the (segment, position) order within a row is kept) and their inverse
         int rbits = 1;
         while ((1ll << rbits) < n) ++rbits;
