@@ -353,56 +353,56 @@ __global__ void kp_wflags(int64_t nchunks, uint16_t* __restrict__ words, uint32_
 // segment: a random 32-address gather costs ~3.9 extra shared-memory wavefronts (ncu: 44% of K3s's shared
 // wavefronts were conflict replays, profiles/r02_cfg5_k3s_raw.csv).  The words of one lane that belong to the
 // same fragment may be summed in any fixed order, so within each (lane chunk, fragment) group the offsets are
-// re-assigned to the group's steps greedily, lanes in order, each word to the free step where its bank holds
-// the fewest distinct addresses so far (an equal address is a broadcast and costs nothing).  One warp per
-// tile; only the order of the fp32 additions inside a fragment changes (fixed by the plan: deterministic).
+// re-assigned to the group's steps greedily, lanes in order, each word to the free step where its bank is
+// used by the fewest other lanes; kDeconflictRounds passes, a lane's own words taken out of the counts before
+// it is re-assigned.  One warp per tile; only the order of the fp32 additions inside a fragment changes (fixed
+// by the plan: deterministic).
+constexpr int kDeconflictRounds = 2;  // sweep: profiles/r02_probe_k3s_deconflict.log (1: 6,279, 2: 6,300, 3: 6,309, 8: 6,315 it/s)
 __global__ void __launch_bounds__(256) kp_deconflict(int64_t ntiles, uint16_t* __restrict__ words,
-                                                     const uint32_t* __restrict__ wflags) {
-    __shared__ uint8_t hist[8][kLaneW][32];    // per warp: distinct addresses per (step, bank)
-    __shared__ uint16_t first[8][kLaneW][32];  // the first address seen there
+                                                     const uint32_t* __restrict__ wflags, int rounds) {
+    __shared__ uint8_t cnt[8][kLaneW][32];  // per warp: lanes using (step, bank)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int64_t tile = (int64_t)blockIdx.x * 8 + warp; tile < ntiles; tile += (int64_t)gridDim.x * 8) {
-        for (int i = lane; i < kLaneW * 32; i += 32) (&hist[warp][0][0])[i] = 0;
+        for (int i = lane; i < kLaneW * 32; i += 32) (&cnt[warp][0][0])[i] = 0;
         __syncwarp();
         uint16_t* w = words + tile * kTileW + kLaneW * lane;
         const uint32_t fl = wflags[tile * 32 + lane] & 0xffffu;
         uint16_t x[kLaneW], out[kLaneW];
 #pragma unroll
-        for (int i = 0; i < kLaneW; ++i) x[i] = w[i];
-        for (int l = 0; l < 32; ++l) {
-            if (lane == l) {
-                int g0 = 0;
-                while (g0 < kLaneW) {
-                    int g1 = g0;  // the group ends at the first end flag at or after g0 (or with the chunk)
-                    while (g1 < kLaneW - 1 && !((fl >> g1) & 1u)) ++g1;
-                    uint32_t free_steps = ((2u << g1) - 1u) & ~((1u << g0) - 1u);
-                    for (int k = g0; k <= g1; ++k) {
-                        const uint16_t a = x[k];
-                        const int bank = a & 31;
-                        int best = g0, bestc = 1 << 30;
-                        bool best_same = false;
-                        for (int st = g0; st <= g1; ++st) {
-                            if (!((free_steps >> st) & 1u)) continue;
-                            int c = hist[warp][st][bank];
-                            const bool same = c > 0 && first[warp][st][bank] == a;
-                            if (same) c = 0;
-                            if (c < bestc) {
-                                bestc = c;
-                                best = st;
-                                best_same = same;
-                            }
-                        }
-                        out[best] = a;
-                        free_steps &= ~(1u << best);
-                        if (!best_same) {
-                            if (hist[warp][best][bank] == 0) first[warp][best][bank] = a;
-                            ++hist[warp][best][bank];
-                        }
+        for (int i = 0; i < kLaneW; ++i) out[i] = w[i];
+        for (int round = 0; round < rounds; ++round) {
+            for (int l = 0; l < 32; ++l) {
+                if (lane == l) {
+                    for (int i = 0; i < kLaneW; ++i) {
+                        x[i] = out[i];
+                        if (round > 0) --cnt[warp][i][x[i] & 31];
                     }
-                    g0 = g1 + 1;
+                    int g0 = 0;
+                    while (g0 < kLaneW) {
+                        int g1 = g0;  // the group ends at the first end flag at or after g0 (or with the chunk)
+                        while (g1 < kLaneW - 1 && !((fl >> g1) & 1u)) ++g1;
+                        uint32_t free_steps = ((2u << g1) - 1u) & ~((1u << g0) - 1u);
+                        for (int k = g0; k <= g1; ++k) {
+                            const uint16_t a = x[k];
+                            const int bank = a & 31;
+                            int best = g0, bestc = 1 << 30;
+                            for (int st = g0; st <= g1; ++st) {
+                                if (!((free_steps >> st) & 1u)) continue;
+                                const int c = cnt[warp][st][bank];
+                                if (c < bestc) {
+                                    bestc = c;
+                                    best = st;
+                                }
+                            }
+                            out[best] = a;
+                            free_steps &= ~(1u << best);
+                            ++cnt[warp][best][bank];
+                        }
+                        g0 = g1 + 1;
+                    }
                 }
+                __syncwarp();
             }
-            __syncwarp();
         }
 #pragma unroll
         for (int i = 0; i < kLaneW; ++i) w[i] = out[i];
@@ -1089,10 +1089,11 @@ mapi_status mapi_csr_plan(int64_t n, int64_t nnz, const int32_t* row_ptr, const 
         MAPI_LAUNCHED();
         kp_wflags<<<blocks(nwords / kLaneW, 8), 256, 0, s>>>(nwords / kLaneW, P.words, P.wflags);
         MAPI_LAUNCHED();
-        {  // investigation switch (MAPI_PLAN_DECONFLICT=0: keep the words in destination order)
+        {  // investigation switch: MAPI_PLAN_DECONFLICT=<passes> (0: keep the words in destination order)
             const char* dc = getenv("MAPI_PLAN_DECONFLICT");
-            if (!dc || dc[0] != '0') {
-                kp_deconflict<<<blocks(ntiles * 32, 8), 256, 0, s>>>(ntiles, P.words, P.wflags);
+            const int rounds = dc ? std::max(0, std::min(atoi(dc), 16)) : kDeconflictRounds;
+            if (rounds > 0) {
+                kp_deconflict<<<blocks(ntiles * 32, 8), 256, 0, s>>>(ntiles, P.words, P.wflags, rounds);
                 MAPI_LAUNCHED();
             }
         }

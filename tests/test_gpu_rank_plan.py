@@ -150,6 +150,31 @@ def test_plan_vs_csr_path(mapi_lib):
     np.testing.assert_allclose(a.w.cpu().numpy(), k3.w.cpu().numpy(), rtol=2e-5, atol=1e-12)
 
 
+@pytest.mark.parametrize("name", ["hubs70k", "skewed60k", "uniform230k"])
+def test_plan_word_order_only_reorders_sums(mapi_lib, monkeypatch, name):
+    """The plan-time bank-conflict-aware word order (kp_deconflict, K3s 3c) only permutes the source
+    offsets inside a (lane chunk, fragment) group: with it (default passes, and 5 passes) and without it
+    (MAPI_PLAN_DECONFLICT=0) the plan has the same sizes and the run gives the same iteration count and the same
+    scores up to the fp32 addition order inside a fragment."""
+    m = mapi_lib
+    n, row_ptr, col_idx = _graphs()[name]
+    b0 = np.full(n, 1.0 / n, np.float32)
+    runs = {}
+    for passes in ("0", None, "5"):
+        if passes is None:
+            monkeypatch.delenv("MAPI_PLAN_DECONFLICT", raising=False)
+        else:
+            monkeypatch.setenv("MAPI_PLAN_DECONFLICT", passes)
+        res, plan, _ = _plan_run(m, n, row_ptr, col_idx, b0, 12, 0.0)
+        runs[passes] = (res.w.cpu().numpy().astype(np.float64), res.deltas.cpu().numpy(), res.iters_done,
+                        (plan.info.npieces, plan.info.nwords, plan.info.nseg, plan.info.nunits))
+    w0, d0, k0, sz0 = runs["0"]
+    for key in (None, "5"):
+        w, d, k, sz = runs[key]
+        assert k == k0 == 12 and sz == sz0
+        np.testing.assert_allclose(w, w0, rtol=2e-6, atol=1e-12)
+        np.testing.assert_allclose(d, d0, rtol=1e-3, atol=1e-8)
+
 def test_plan_edge_cases(mapi_lib, orc):
     m = mapi_lib
     # no edges at all: every column dangling, w stays uniform
