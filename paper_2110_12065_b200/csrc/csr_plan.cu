@@ -357,7 +357,6 @@ __global__ void kp_wflags(int64_t nchunks, uint16_t* __restrict__ words, uint32_
 // used by the fewest other lanes; kDeconflictRounds passes, a lane's own words taken out of the counts before
 // it is re-assigned.  One warp per tile; only the order of the fp32 additions inside a fragment changes (fixed
 // by the plan: deterministic).
-constexpr int kDeconflictMode = 1;    // 1: (lane chunk, fragment) groups; 2: whole fragments (kp_deconflict_frag)
 constexpr int kDeconflictRounds = 2;  // sweep: profiles/r02_probe_k3s_deconflict.log (1: 6,279, 2: 6,300, 3: 6,309, 8: 6,315 it/s)
 __global__ void __launch_bounds__(256) kp_deconflict(int64_t ntiles, uint16_t* __restrict__ words,
                                                      const uint32_t* __restrict__ wflags, int rounds) {
@@ -407,78 +406,6 @@ __global__ void __launch_bounds__(256) kp_deconflict(int64_t ntiles, uint16_t* _
         }
 #pragma unroll
         for (int i = 0; i < kLaneW; ++i) w[i] = out[i];
-        __syncwarp();
-    }
-}
-
-// Variant 2 (MAPI_PLAN_DECONFLICT_MODE=2): the same idea with the whole FRAGMENT as the group — a fragment that
-// spans several lanes of the tile may place any of its words at any of its (lane, step) positions.  One warp per
-// tile, positions in order; for each position the warp picks, among the fragment's unused words, the one whose
-// bank is used by the fewest lanes at that step (lanes scan the candidates 32 at a time, warp argmin; ties to
-// the lowest index, so the result is deterministic).
-__global__ void __launch_bounds__(256) kp_deconflict_frag(int64_t ntiles, uint16_t* __restrict__ words,
-                                                          const uint32_t* __restrict__ wflags) {
-    __shared__ uint16_t pool[8][kTileW], outw[8][kTileW], gbeg[8][kTileW], gend[8][kTileW];
-    __shared__ uint8_t used[8][kTileW];
-    __shared__ uint8_t cnt[8][kLaneW][32];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int64_t tile = (int64_t)blockIdx.x * 8 + warp; tile < ntiles; tile += (int64_t)gridDim.x * 8) {
-        for (int i = lane; i < kLaneW * 32; i += 32) (&cnt[warp][0][0])[i] = 0;
-        uint16_t* w = words + tile * kTileW;
-        for (int i = lane; i < kTileW; i += 32) {
-            pool[warp][i] = w[i];
-            used[warp][i] = 0;
-        }
-        const uint32_t fl = wflags[tile * 32 + lane] & 0xffffu;
-        // group = maximal run of positions up to and including an end flag (the unflagged tail of the tile, if
-        // any, is padding: one last group)
-        int lastf = fl ? kLaneW * lane + (31 - __clz(fl)) : -1;   // this lane's last flagged position
-        int firstf = fl ? kLaneW * lane + (__ffs(fl) - 1) : kTileW;  // and its first
-        int pe = lastf, nf = firstf;
-        for (int off = 1; off < 32; off <<= 1) {  // inclusive max-scan (up) / min-scan (down)
-            const int a = __shfl_up_sync(0xffffffffu, pe, off), b = __shfl_down_sync(0xffffffffu, nf, off);
-            if (lane >= off) pe = max(pe, a);
-            if (lane + off < 32) nf = min(nf, b);
-        }
-        int prev_end = __shfl_up_sync(0xffffffffu, pe, 1);      // last flag before this lane's chunk
-        if (lane == 0) prev_end = -1;
-        int next_flag = __shfl_down_sync(0xffffffffu, nf, 1);   // first flag after this lane's chunk
-        if (lane == 31) next_flag = kTileW;
-        for (int i = 0; i < kLaneW; ++i) {
-            const int pos = kLaneW * lane + i;
-            gbeg[warp][pos] = (uint16_t)(prev_end + 1);
-            if ((fl >> i) & 1u) prev_end = pos;
-        }
-        for (int i = kLaneW - 1; i >= 0; --i) {
-            const int pos = kLaneW * lane + i;
-            if ((fl >> i) & 1u) next_flag = pos;
-            gend[warp][pos] = (uint16_t)min(next_flag, kTileW - 1);
-        }
-        __syncwarp();
-        for (int pos = 0; pos < kTileW; ++pos) {
-            const int step = pos & (kLaneW - 1), ga = gbeg[warp][pos], gb = gend[warp][pos];
-            uint32_t key = 0xffffffffu;  // (count << 16) | candidate index
-            for (int c = ga + lane; c <= gb; c += 32)
-                if (!used[warp][c]) {
-                    const uint32_t k = ((uint32_t)cnt[warp][step][pool[warp][c] & 31] << 16) | (uint32_t)c;
-                    key = min(key, k);
-                }
-            if (gb - ga >= 1) {
-#pragma unroll
-                for (int off = 16; off > 0; off >>= 1) key = min(key, __shfl_xor_sync(0xffffffffu, key, off));
-            } else {
-                key = __shfl_sync(0xffffffffu, key, 0);
-            }
-            if (lane == 0) {
-                const int c = (int)(key & 0xffffu);
-                const uint16_t a = pool[warp][c];
-                outw[warp][pos] = a;
-                used[warp][c] = 1;
-                ++cnt[warp][step][a & 31];
-            }
-            __syncwarp();
-        }
-        for (int i = lane; i < kTileW; i += 32) w[i] = outw[warp][i];
         __syncwarp();
     }
 }
@@ -1165,12 +1092,7 @@ mapi_status mapi_csr_plan(int64_t n, int64_t nnz, const int32_t* row_ptr, const 
         {  // investigation switch: MAPI_PLAN_DECONFLICT=<passes> (0: keep the words in destination order)
             const char* dc = getenv("MAPI_PLAN_DECONFLICT");
             const int rounds = dc ? std::max(0, std::min(atoi(dc), 16)) : kDeconflictRounds;
-            const char* md = getenv("MAPI_PLAN_DECONFLICT_MODE");
-            const int mode = md ? atoi(md) : kDeconflictMode;
-            if (rounds > 0 && mode == 2) {
-                kp_deconflict_frag<<<blocks(ntiles * 32, 8), 256, 0, s>>>(ntiles, P.words, P.wflags);
-                MAPI_LAUNCHED();
-            } else if (rounds > 0) {
+            if (rounds > 0) {
                 kp_deconflict<<<blocks(ntiles * 32, 8), 256, 0, s>>>(ntiles, P.words, P.wflags, rounds);
                 MAPI_LAUNCHED();
             }
