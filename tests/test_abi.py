@@ -160,6 +160,34 @@ def test_csr_reorder_permute_validation(lib):
     assert lib.mapi_csr_permute(10, fake, fake, fake, 1, None) == 3  # x aliases out
 
 
+def test_rank_csr_shard_validation(lib):
+    """mapi_rank_csr_shard_* (K3n) validate on the host before touching the device; the workspace grows with the
+    node count (full node state on every rank) and with the rank's rows + edges (merge-path tiles)."""
+    fake = ctypes.c_void_p(4096)
+    n, m_rows, nnz = 1000, 300, 5000
+    ws = m.workspace_size(m.WS_RANK_CSR_SHARD, n, nnz, m_rows)
+    assert ws >= 256 + 3 * 4 * n
+    assert m.workspace_size(m.WS_RANK_CSR_SHARD, 2 * n, nnz, m_rows) > ws
+    assert m.workspace_size(m.WS_RANK_CSR_SHARD, n, 100 * nnz, m_rows) > ws
+    assert m.workspace_size(m.WS_RANK_CSR_SHARD, n, nnz, n) <= m.workspace_size(m.WS_RANK_CSR, n, nnz)
+    begin, rows, norm, fin = (lib.mapi_rank_csr_shard_begin, lib.mapi_rank_csr_shard_rows,
+                              lib.mapi_rank_csr_shard_normalize, lib.mapi_rank_csr_shard_finish)
+    assert begin(0, 0, 0, fake, fake, fake, fake, fake, ws, None) == 2
+    assert begin(n, n + 1, nnz, fake, fake, fake, fake, fake, 1 << 40, None) == 2 and "rows" in _err(lib)
+    assert begin(n, m_rows, 1 << 40, fake, fake, fake, fake, fake, 1 << 60, None) == 2
+    assert begin(n, m_rows, nnz, fake, fake, fake, fake, None, ws, None) == 7
+    assert begin(n, m_rows, nnz, fake, fake, fake, fake, fake, 16, None) == 7
+    assert begin(n, m_rows, nnz, None, fake, fake, fake, fake, ws, None) == 1
+    assert begin(n, m_rows, nnz, fake, None, fake, fake, fake, ws, None) == 1
+    assert rows(n, m_rows, 800, nnz, fake, fake, 0, None, fake, ws, None) == 2  # rows [800, 1100) leave [0, n)
+    assert rows(n, m_rows, 0, nnz, fake, None, 0, None, fake, ws, None) == 1
+    assert rows(n, m_rows, 0, nnz, fake, fake, -1, None, fake, ws, None) == 3
+    assert norm(n, m_rows, nnz, fake, fake, None, 0, 0.0, None, fake, ws, None) == 1
+    assert norm(n, m_rows, nnz, fake, fake, fake, 0, -1.0, None, fake, ws, None) == 3
+    assert norm(n, m_rows, nnz, fake, fake, fake, -2, 0.0, None, fake, ws, None) == 3
+    assert fin(n, m_rows, nnz, fake, fake, None, None, None, None, ws, None) == 7
+    assert fin(n, m_rows, nnz, None, fake, None, None, None, fake, ws, None) == 1
+
 def test_pack_upper_layout():
     """pack_upper: row j of the packed buffer is A[j, j:], rows back to back (offset j n - j (j-1) / 2),
     checked against numpy's triu index order on odd / even sizes."""
