@@ -439,6 +439,7 @@ class CsrShardSession:
         self.sp = stream if stream is not None else (torch.cuda.current_stream(dev).cuda_stream
                                                      if dev.type == "cuda" else None)
         self._c, self._torch = ctypes, torch
+        self._e_addr = [0, 0]
 
     def _check(self, st):
         if st:
@@ -457,11 +458,18 @@ class CsrShardSession:
         self._check(self.lib.mapi_rank_csr_shard_rows(self.n, self.m, self.row0, self.nnz, self.rp.data_ptr(),
                                                       self.ci.data_ptr() if self.nnz else None, int(t),
                                                       self._c.byref(e), self.ws.data_ptr(), self.need, self.sp))
+        self._e_addr[t & 1] = e.value
         return e.value
 
     def e_view(self, t: int):
-        """e_t as a tensor view into the workspace (the collective's in-place buffer)."""
-        base = 256 + (t & 1) * ((4 * self.n + 255) & ~255)
+        """e_t as a tensor view into the workspace (the collective's in-place buffer), at the address
+        rows(t) reported."""
+        addr = self._e_addr[t & 1]
+        if not addr:
+            raise RuntimeError("e_view(t) needs rows(t) first")
+        base = addr - self.ws.data_ptr()
+        if base < 0 or base + 4 * self.n > self.need:
+            raise RuntimeError("e_t lies outside the workspace")
         return self.ws[base:base + 4 * self.n].view(self._torch.float32)
 
     def normalize(self, t: int):
