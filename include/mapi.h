@@ -338,7 +338,7 @@ mapi_status mapi_rank_csr(int64_t n, int64_t nnz, const int32_t *row_ptr, const 
  * (host) receives the sizes the run needs (keep it with the plan).  ws: MAPI_WS_CSR_PLAN_BUILD bytes of
  * temporary device workspace.  The plan is tied to the device's SM count (info->grid).  Deterministic.
  * MAPI_ERR_SHAPE if one row has so many fragments that a node batch exceeds the kernel's shared memory
- * (> 49,152 fragment sums; not reachable below ~2^24 in-edges per row): use mapi_rank_csr then.
+ * (> 49,152 fragment sums in a batch of up to 32,768 + one row's; not reachable below ~2^23 in-edges per row): use mapi_rank_csr then.
  * Synchronises `stream` (small read-backs size the later steps). */
 typedef struct mapi_csr_plan_info {
     int64_t n, nnz;      /* the graph */

@@ -62,7 +62,9 @@ constexpr int kSmemF = kSegStride + kStageF; // dynamic shared floats; phase B s
 constexpr size_t kPlanSmem = sizeof(float) * (size_t)kSmemF;
 constexpr int kNodeK = 4;                    // rows per thread per batch
 constexpr int kBatchRows = kNodeK * kThreads;
-constexpr int kSlotBlock = 16384;            // a batch never spans two slot blocks (plus its last row)
+constexpr int kSlotBlock = 16384;            // a batch never spans two slot blocks (plus its last row): the bound's block
+constexpr int kSlotBlockRun = 32768;         // the block the plan is cut with (>= kSlotBlock): 893 instead of 1,201
+                                             // batches at cfg5, phase B 75 -> 67 us (profiles/r02_probe_k3s_slotblock.log)
 constexpr int kUnitBig = 256;                // phase A work units (tiles), taken dynamically: big ones first,
 constexpr int kUnitSmall = kWarps;           // then one tile per warp for the last 1/8 of the tiles
 constexpr uint64_t kMagic = 0x4d41504950334c4eull;
@@ -416,8 +418,8 @@ __global__ void kp_fslot(int64_t nfrag, const int32_t* __restrict__ pos, int32_t
 
 // batch starts over the live rows: every kBatchRows rows and wherever the slot position enters a new slot
 // block, so a batch holds <= kBatchRows rows and < kSlotBlock + (its last row's slots) slots
-__global__ void kp_bflag(int64_t nlive, const int32_t* __restrict__ rsp, int32_t* __restrict__ flag) {
-    GRID_STRIDE(r, nlive) flag[r] = (r == 0 || r % kBatchRows == 0 || rsp[r] / kSlotBlock != rsp[r - 1] / kSlotBlock);
+__global__ void kp_bflag(int64_t nlive, const int32_t* __restrict__ rsp, int32_t* __restrict__ flag, int32_t slot_block) {
+    GRID_STRIDE(r, nlive) flag[r] = (r == 0 || r % kBatchRows == 0 || rsp[r] / slot_block != rsp[r - 1] / slot_block);
 }
 __global__ void kp_bstart(int64_t nlive, const int32_t* __restrict__ flag, const int32_t* __restrict__ incl,
                           int32_t* __restrict__ bstart) {
@@ -1112,7 +1114,11 @@ mapi_status mapi_csr_plan(int64_t n, int64_t nnz, const int32_t* row_ptr, const 
     // node-pass batches over the live rows, and the fragments in (batch, fragment) order
     int64_t nbatch = 0;
     if (nlive > 0) {
-        kp_bflag<<<blocks(nlive, 8), 256, 0, s>>>(nlive, P.rsp, B.bflag);
+        // investigation switch: MAPI_PLAN_SLOT_BLOCK=<slots> in [kSlotBlock, 2 kSlotBlock] (fewer, larger batches;
+        // nbatch_bound stays valid: it assumes the smallest block)
+        const char* sbe = getenv("MAPI_PLAN_SLOT_BLOCK");
+        const int32_t slot_block = sbe ? std::max(kSlotBlock, std::min(atoi(sbe), 2 * kSlotBlock)) : kSlotBlockRun;
+        kp_bflag<<<blocks(nlive, 8), 256, 0, s>>>(nlive, P.rsp, B.bflag, slot_block);
         MAPI_LAUNCHED();
         tb = B.cub_bytes;
         MAPI_CUDA(cub::DeviceScan::InclusiveSum(B.cub, tb, B.bflag, B.bincl, (int)nlive, s));
